@@ -1,0 +1,461 @@
+"""CPU oracle for the ANCKA clustering hot path -- TEST INFRASTRUCTURE ONLY.
+
+This module restates, in numpy/scipy, the algorithm of the reference
+package (`/root/reference/pkg/src/ancka`, v0.1.0).  Every function cites
+the reference file:line it follows.  It exists for three callers only:
+
+* `tests/` (parity checker for the CUDA path),
+* `__graft_entry__.smoke()` (one tiny CUDA-vs-oracle check),
+* `bench.py` (`cpu_baseline` leg and `--impl reference`).
+
+The product package `paper_2408_05459_b200` never imports it: the product
+path has no CPU fallback.
+
+Parity pinning: `tests/golden/make_golden.py` runs the *reference itself*
+(importable in the build container from /root/reference) on seeded inputs
+and freezes its outputs as `tests/golden/*.npz`; `tests/test_oracle_golden.py`
+checks this restatement against every one of them (bit-exact for integer
+outputs, <=1e-12 for floating point).
+
+Data model: plain arrays.  A network is a dict
+    {"kind": "graph"|"hypergraph", "S": csr (A n x n, or H m x n),
+     "directed": bool, "X": ndarray or csr}
+"""
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+import scipy.sparse as sp
+
+ALPHA, BETA, GAMMA = 0.2, 0.5, 3
+DISC_ROUNDS, DISC_TOL = 100, 1e-10          # engine.py:37-38
+
+
+class OracleError(ValueError):
+    """Mirrors ancka.NetworkError (network.py:39-40)."""
+
+
+# ----------------------------------------------------------------------------
+# network.py
+# ----------------------------------------------------------------------------
+def canon_csr(m, what="matrix"):
+    """check_sparse_nonneg (network.py:43-63): sorted, deduplicated, no zeros."""
+    m = sp.csr_matrix(m, copy=True)
+    if m.nnz and (m.indices.min() < 0 or m.indices.max() >= m.shape[1]):
+        raise OracleError(f"{what}: column index out of range")
+    m.sum_duplicates()
+    m.sort_indices()
+    m.eliminate_zeros()
+    if m.nnz:
+        if not np.isfinite(m.data).all():
+            raise OracleError(f"{what}: non-finite values are not allowed")
+        if (m.data < 0).any():
+            raise OracleError(f"{what}: negative values are not allowed")
+    return m
+
+
+def sym_union(a):
+    """symmetrize_union (network.py:261-263): pattern union max(A, A^T)."""
+    return canon_csr(a.maximum(a.T), "adjacency")
+
+
+def clean_network(net):
+    """validate_network (network.py:266-313), structural cleanup only."""
+    net = dict(net)
+    s = canon_csr(net["S"], "structure")
+    if net["kind"] == "hypergraph":
+        keep = np.diff(s.indptr) >= 2
+        if not keep.all():
+            s = canon_csr(s[keep], "incidence")
+    else:
+        dups = int((s.data > 1).sum())
+        loops = int(s.diagonal().astype(bool).sum())
+        if dups or loops:
+            s = s.copy()
+            s.data = np.minimum(s.data, 1.0)
+            s.setdiag(0)
+            s = canon_csr(s, "adjacency")
+    net["S"] = s
+    return net
+
+
+def structural_degree(net):
+    """node_degrees (network.py:316-328): pattern counts."""
+    s = net["S"]
+    if net["kind"] == "hypergraph":
+        return np.asarray((s != 0).sum(axis=0)).ravel().astype(np.float64)
+    a = sym_union(s) if net.get("directed") else s
+    return np.asarray((a != 0).sum(axis=1)).ravel().astype(np.float64)
+
+
+def default_K(kind, n):
+    """default_knn_k (network.py:232-235)."""
+    return 10 if (kind == "hypergraph" or n > 100_000) else 50
+
+
+# ----------------------------------------------------------------------------
+# knn.py (exact mode)
+# ----------------------------------------------------------------------------
+def unit_rows(x):
+    """_normalize_rows (knn.py:54-65): L2-normalise, zero rows stay zero."""
+    if sp.issparse(x):
+        x = x.tocsr().astype(np.float64)
+        nrm = np.sqrt(np.asarray(x.multiply(x).sum(axis=1)).ravel())
+        scale = np.where(nrm > 0, 1.0 / np.where(nrm > 0, nrm, 1.0), 0.0)
+        return (sp.diags(scale) @ x).tocsr(), nrm
+    x = np.asarray(x, dtype=np.float64)
+    nrm = np.linalg.norm(x, axis=1)
+    scale = np.where(nrm > 0, 1.0 / np.where(nrm > 0, nrm, 1.0), 0.0)
+    return x * scale[:, None], nrm
+
+
+def _select_row(sims_row, K):
+    """_ordered_top_k (knn.py:83-98) as one lexicographic sort.
+
+    Order is (value desc, index asc) over strictly positive entries; the
+    first K of that order are exactly the reference's selection (its
+    boundary ties resolve to the smaller index, then a stable sort on -value).
+    """
+    pos = np.flatnonzero(sims_row > 0)
+    if pos.size == 0:
+        return pos
+    order = np.lexsort((pos, -sims_row[pos]))
+    return pos[order[:K]]
+
+
+def knn_exact(X, K, block_rows=None):
+    """knn_search_exact (knn.py:112-140).  Returns (ids int64 (n,K) padded -1,
+    scores f64 (n,K) padded 0)."""
+    xn, nrm = unit_rows(X)
+    n = xn.shape[0]
+    if K >= n:
+        raise OracleError(f"K={K} must be smaller than n={n}")
+    if block_rows is None:
+        block_rows = max(16, min(4096, int(2.5e7 // max(n, 1))))
+    right = xn.T.tocsc() if sp.issparse(xn) else xn.T
+    ids = np.full((n, K), -1, dtype=np.int64)
+    scores = np.zeros((n, K), dtype=np.float64)
+    for lo in range(0, n, block_rows):
+        hi = min(lo + block_rows, n)
+        blk = xn[lo:hi] @ right
+        blk = blk.toarray() if sp.issparse(blk) else np.asarray(blk)
+        blk[np.arange(hi - lo), np.arange(lo, hi)] = -1.0
+        for r in range(hi - lo):
+            if nrm[lo + r] == 0.0:
+                continue
+            sel = _select_row(blk[r], K)
+            ids[lo + r, : sel.size] = sel
+            scores[lo + r, : sel.size] = np.minimum(blk[r, sel], 1.0)
+    return ids, scores
+
+
+def knn_adjacency(ids, scores):
+    """build_knn_adjacency (knn.py:294-309): A_K = M + M^T, sorted CSR."""
+    n = ids.shape[0]
+    ok = ids != -1
+    rows = np.repeat(np.arange(n), ok.sum(axis=1))
+    m = sp.csr_matrix((scores[ok], (rows, ids[ok])), shape=(n, n))
+    a = (m + m.T).tocsr()
+    a.sort_indices()
+    return a
+
+
+def row_stochastic(a):
+    """_row_normalize (walk.py:38-44) == knn_transition (knn.py:312-324)."""
+    rs = np.asarray(a.sum(axis=1)).ravel()
+    inv = np.divide(1.0, rs, out=np.zeros_like(rs), where=rs > 0)
+    p = (sp.diags(inv) @ a).tocsr()
+    p.sort_indices()
+    return p, rs == 0
+
+
+# ----------------------------------------------------------------------------
+# walk.py
+# ----------------------------------------------------------------------------
+def make_operator(net, p_k, knn_zero, alpha=ALPHA, beta=BETA, gamma=GAMMA):
+    """build_walk_operator (walk.py:107-132) with beta_vector (walk.py:47-57),
+    hypergraph_factors (walk.py:60-71), graph_transition (walk.py:74-79)."""
+    deg = structural_degree(net)
+    n = deg.size
+    b = np.full(n, float(beta))
+    b[deg == 0] = 1.0
+    b[np.asarray(knn_zero, dtype=bool)] = 0.0
+    op = {"kind": net["kind"], "n": n, "alpha": float(alpha), "gamma": int(gamma),
+          "beta": b, "p_k": p_k, "degrees": deg,
+          "selfloop": np.flatnonzero((deg == 0) & (b == 0.0))}
+    s = net["S"]
+    if net["kind"] == "hypergraph":
+        op["p_v"], _ = row_stochastic(s.T.tocsr())
+        op["p_e"], _ = row_stochastic(s)
+    else:
+        op["p_n"], _ = row_stochastic(sym_union(s) if net.get("directed") else s)
+    return op
+
+
+def structure_apply(op, m):
+    """apply_structure (walk.py:135-150)."""
+    if m.shape[0] != op["n"]:
+        raise OracleError("block/operator size mismatch")
+    out = op["p_v"] @ (op["p_e"] @ m) if op["kind"] == "hypergraph" else op["p_n"] @ m
+    sl = op["selfloop"]
+    if sl.size:
+        out[sl] += m[sl]
+    return out
+
+
+def structure_apply_t(op, m):
+    """apply_structure_rowvec (walk.py:153-174): (c x n) block times P_struct."""
+    mt = np.ascontiguousarray(m.T)
+    if op["kind"] == "hypergraph":
+        out = (op["p_e"].T @ (op["p_v"].T @ mt)).T
+    else:
+        out = (op["p_n"].T @ mt).T
+    out = np.ascontiguousarray(out)
+    sl = op["selfloop"]
+    if sl.size:
+        out[:, sl] += m[:, sl]
+    return out
+
+
+def joint_apply(op, m):
+    """apply_joint_transition (walk.py:177-190): (I-B) P_N M + B P_K M."""
+    m = np.asarray(m, dtype=np.float64)
+    vec = m.ndim == 1
+    if vec:
+        m = m[:, None]
+    b = op["beta"][:, None]
+    out = (1.0 - b) * structure_apply(op, m) + b * (op["p_k"] @ m)
+    return out.ravel() if vec else out
+
+
+def dense_P(op):
+    """dense_transition (walk.py:193-208), small n only."""
+    if op["kind"] == "hypergraph":
+        pn = (op["p_v"] @ op["p_e"]).toarray()
+    else:
+        pn = op["p_n"].toarray()
+    sl = op["selfloop"]
+    if sl.size:
+        pn[sl, sl] += 1.0
+    b = op["beta"][:, None]
+    return (1.0 - b) * pn + b * op["p_k"].toarray()
+
+
+# ----------------------------------------------------------------------------
+# engine.py
+# ----------------------------------------------------------------------------
+def sizes_of(labels, k):
+    return np.bincount(labels, minlength=k)
+
+
+def unit_membership(labels, k):
+    """normalize_bcm (engine.py:75-84)."""
+    sz = sizes_of(labels, k)
+    if (sz == 0).any():
+        raise OracleError("empty cluster: normalization undefined")
+    y = np.zeros((labels.size, k))
+    y[np.arange(labels.size), labels] = 1.0 / np.sqrt(sz[labels])
+    return y
+
+
+def greedy_init(op, k, t_i, alpha):
+    """init_bcm (engine.py:87-127).  Returns (labels, centers)."""
+    n, deg = op["n"], op["degrees"]
+    if k > n:
+        raise OracleError(f"k={k} exceeds node count n={n}")
+    rank = np.lexsort((np.arange(n), -deg))
+    live = int((deg > 0).sum())
+    if k > live:
+        warnings.warn("too few nonzero-degree nodes; filling centers in index order")
+        chosen = set(rank[:live].tolist())
+        fill = [i for i in range(n) if i not in chosen][: k - live]
+        centers = np.sort(np.array(sorted(chosen) + fill, dtype=np.int64))
+    else:
+        centers = np.sort(rank[:k])
+    pi0 = np.zeros((k, n))
+    pi0[np.arange(k), centers] = alpha
+    pi = pi0.copy()
+    for _ in range(t_i):
+        pi = (1.0 - alpha) * structure_apply_t(op, pi) + pi0
+    labels = np.argmax(pi, axis=0).astype(np.int64)
+    if (sizes_of(labels, k) == 0).any():
+        warnings.warn("greedy init left empty cluster(s); pinning centers")
+        labels = labels.copy()
+        labels[centers] = np.arange(k)
+    return labels, centers
+
+
+def qr_step(op, q_prev, rng):
+    """orthogonal_step (engine.py:130-149): apply, Householder QR, noise on
+    rank-deficient columns, sign fix so diag(R) >= 0."""
+    z = joint_apply(op, q_prev)
+    q, r = np.linalg.qr(z)
+    dg = np.abs(np.diag(r))
+    bad = dg < 1e-12 * max(1.0, dg.max() if dg.size else 1.0)
+    if bad.any():
+        warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
+        z = z.copy()
+        z[:, bad] += 1e-8 * rng.standard_normal((z.shape[0], int(bad.sum())))
+        q, r = np.linalg.qr(z)
+    sgn = np.where(np.diag(r) < 0, -1.0, 1.0)
+    return q * sgn, r * sgn[:, None]
+
+
+def _second_best(scores):
+    return np.partition(scores, -2, axis=1)[:, -2]
+
+
+def _refill_empty(labels, scores, k):
+    """_reseed_empty_columns (engine.py:162-180)."""
+    empties = np.flatnonzero(sizes_of(labels, k) == 0)
+    if empties.size == 0 or k < 2 or scores.shape[1] < 2:
+        return labels
+    labels = labels.copy()
+    margin = _second_best(scores)
+    for c in empties:
+        movable = sizes_of(labels, k)[labels] >= 2
+        if not movable.any():
+            break
+        labels[int(np.argmax(np.where(movable, margin, -np.inf)))] = c
+    return labels
+
+
+def _rounding_run(qt, rot, rounds, tol):
+    """_alternate_rounding (engine.py:183-206)."""
+    n, k = qt.shape
+    objs = []
+    labels = np.zeros(n, dtype=np.int64)
+    scores = qt @ rot
+    done = False
+    for _ in range(rounds):
+        scores = qt @ rot
+        labels = _refill_empty(np.argmax(scores, axis=1), scores, k)
+        sz = sizes_of(labels, k).astype(np.float64)
+        w = np.divide(1.0, sz[labels], out=np.zeros(n), where=sz[labels] > 0)
+        ytil = np.zeros((n, k))
+        ytil[np.arange(n), labels] = w
+        u, om, vh = np.linalg.svd(ytil.T @ qt)
+        objs.append(n - 2.0 * float(om.sum()))
+        if len(objs) >= 2 and abs(objs[-1] - objs[-2]) < tol:
+            done = True
+            break
+        rot = vh.T @ u.T
+    return labels, scores, objs, done
+
+
+def _prototype_start(qt, k):
+    """_prototype_rotation (engine.py:209-218)."""
+    rot = np.zeros((k, k))
+    rot[:, 0] = qt[0]
+    acc = np.zeros(qt.shape[0])
+    for j in range(1, k):
+        acc += np.abs(qt @ rot[:, j - 1])
+        rot[:, j] = qt[int(np.argmin(acc))]
+    return rot
+
+
+def discretize(q, rounds=DISC_ROUNDS, tol=DISC_TOL):
+    """discretize (engine.py:221-263).  Returns dict(labels, scores, objs,
+    converged, runs)."""
+    q = np.asarray(q, dtype=np.float64)
+    if q.ndim != 2 or q.shape[1] < 1:
+        raise OracleError("discretize expects an n x k block with k >= 1")
+    n, k = q.shape
+    nrm = np.linalg.norm(q, axis=1)
+    if (nrm == 0).any():
+        warnings.warn(f"{int((nrm == 0).sum())} all-zero row(s); assigning to cluster 0")
+    qt = np.divide(q, nrm[:, None], out=np.zeros_like(q), where=nrm[:, None] > 0)
+    best, runs = None, []
+    for name, rot in (("identity", np.eye(k)), ("prototype", _prototype_start(qt, k))):
+        res = _rounding_run(qt, rot, rounds, tol)
+        runs.append((name, res[2]))
+        if best is None or res[2][-1] < best[2][-1] - 1e-15:
+            best = res
+    labels, scores, objs, done = best
+    return {"labels": labels, "scores": scores, "objs": objs, "converged": done,
+            "runs": runs}
+
+
+def repair(labels, scores, k):
+    """repair_empty_clusters (engine.py:266-288)."""
+    empties = np.flatnonzero(sizes_of(labels, k) == 0)
+    if empties.size == 0:
+        return labels
+    warnings.warn(f"re-seeding {empties.size} empty cluster(s) after discretization")
+    labels = labels.copy()
+    margin = _second_best(scores) if scores.shape[1] >= 2 else scores[:, 0]
+    for c in empties:
+        movable = sizes_of(labels, k)[labels] >= 2
+        if not movable.any():
+            raise OracleError("cannot repair empty clusters: no movable nodes")
+        labels[int(np.argmax(np.where(movable, margin, -np.inf)))] = c
+    return labels
+
+
+def mhc(op, labels, k):
+    """calc_mhc (engine.py:291-299)."""
+    yh = unit_membership(labels, k)
+    f0 = op["alpha"] * yh
+    f = f0.copy()
+    for _ in range(op["gamma"]):
+        f = (1.0 - op["alpha"]) * joint_apply(op, f) + f0
+    return 1.0 - float(np.einsum("ij,ij->", yh, f)) / k
+
+
+def build(net, k, knn_k=None, alpha=ALPHA, beta=BETA, gamma=GAMMA, knn=None):
+    """build_pipeline (engine.py:302-340), exact KNN only.  `knn`=(ids, scores)
+    injects neighbour lists the way the reference's .aknn cache does."""
+    net = clean_network(net)
+    deg_n = structural_degree(net).size
+    if k > deg_n:
+        raise OracleError(f"k={k} exceeds node count n={deg_n}")
+    K = knn_k if knn_k is not None else default_K(net["kind"], deg_n)
+    K = min(K, deg_n - 1)
+    if knn is None:
+        ids, scores = knn_exact(net["X"], K)
+    else:
+        ids, scores = knn
+    adj = knn_adjacency(ids, scores)
+    p_k, zero = row_stochastic(adj)
+    return make_operator(net, p_k, zero, alpha, beta, gamma), (ids, scores, adj)
+
+
+def run(net, k, knn_k=None, alpha=ALPHA, beta=BETA, gamma=GAMMA, eps_q=0.005,
+        t_a=1000, t_i=25, tau=5, seed=0, early_stop=True, knn=None):
+    """run_ancka (engine.py:343-437).  Returns a dict with labels, mhc,
+    iterations, stop_reason, history and the operator."""
+    op, knn_out = build(net, k, knn_k, alpha, beta, gamma, knn)
+    labels0, _ = greedy_init(op, k, t_i, alpha)
+    rng = np.random.default_rng(seed)
+    n = op["n"]
+    q = np.concatenate([np.full((n, 1), 1.0 / np.sqrt(n)), unit_membership(labels0, k)], axis=1)
+    q = q[:, :n]
+    best_phi = mhc(op, labels0, k)
+    best = labels0
+    hist = [(0, best_phi)]
+    stop, it, err = "max_iterations", 0, None
+    try:
+        for t in range(1, t_a + 1):
+            it = t
+            q_prev = q
+            q, _ = qr_step(op, q_prev, rng)
+            if t % tau:
+                continue
+            d = discretize(q[:, 1:])
+            lab = repair(d["labels"], d["scores"], k)
+            phi = mhc(op, lab, k)
+            hist.append((t, phi))
+            if phi < best_phi:
+                best_phi, best = phi, lab
+            if float(np.linalg.norm(q - q_prev)) < eps_q:
+                stop = "subspace_converged"
+                break
+            if early_stop and len(hist) >= 3 and hist[-3][1] < hist[-2][1] < hist[-1][1]:
+                stop = "mhc_rising"
+                break
+    except OracleError as exc:
+        err, stop = str(exc), "error"
+    return {"labels": best, "mhc": best_phi, "iterations": it, "stop_reason": stop,
+            "history": hist, "q": q, "op": op, "knn": knn_out, "labels0": labels0,
+            "error": err}

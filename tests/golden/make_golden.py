@@ -1,0 +1,168 @@
+"""Freeze outputs of the REFERENCE package as golden fixtures.
+
+Run in the build container (the only place /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference (`/root/reference/pkg/src/ancka`) and its
+own test-fixture builders (`/root/reference/pkg/tests/conftest.py`), runs the
+hot-path functions on seeded inputs and writes small .npz files next to this
+script.  The oracle (`oracle/ancka_cpu.py`) is pinned against these files by
+`tests/test_oracle_golden.py`; the CUDA path is then checked against the
+oracle and against these files.  Nothing on the GPU box reads /root/reference.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import warnings
+from pathlib import Path
+
+import numpy as np
+import scipy.sparse as sp
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, "/root/reference/pkg/tests")
+sys.path.insert(0, str(HERE.parents[1]))
+
+import ancka  # noqa: E402  (the reference)
+from ancka import engine, knn, walk  # noqa: E402
+from conftest import make_random_instance, random_membership  # noqa: E402
+
+from paper_2408_05459_b200 import synth  # noqa: E402
+
+warnings.simplefilter("ignore")
+
+
+def _csr(prefix, m, out):
+    m = sp.csr_matrix(m)
+    out[prefix + "_indptr"] = m.indptr.astype(np.int64)
+    out[prefix + "_indices"] = m.indices.astype(np.int64)
+    out[prefix + "_data"] = m.data.astype(np.float64)
+    out[prefix + "_shape"] = np.asarray(m.shape, dtype=np.int64)
+
+
+def _x(prefix, x, out):
+    if sp.issparse(x):
+        _csr(prefix + "_csr", x, out)
+    else:
+        out[prefix + "_dense"] = np.asarray(x, dtype=np.float64)
+
+
+def spec_examples():
+    out = {}
+    x = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    nl = ancka.knn_search_exact(x, 1)
+    out["ex1_X"] = x
+    out["ex1_ids"], out["ex1_scores"] = nl.ids, nl.scores
+    g = ancka.build_knn_adjacency(nl, x)
+    out["ex1_AK"] = g.adjacency.toarray()
+    p, z = ancka.knn_transition(g)
+    out["ex1_PK"] = p.toarray()
+    x2 = np.array([[1.0, 0.0], [-1.0, 0.0], [0.0, 1.0], [1.0, 0.1]])
+    nl2 = ancka.knn_search_exact(x2, 2)
+    out["ex2_X"], out["ex2_ids"], out["ex2_scores"] = x2, nl2.ids, nl2.scores
+    np.savez_compressed(HERE / "spec_examples.npz", **out)
+
+
+def random_instances(n_seeds=60):
+    """Per-op outputs on conftest.make_random_instance(seed) (conftest.py:69-82)."""
+    out = {}
+    for seed in range(n_seeds):
+        op, g, net = make_random_instance(seed)
+        p = f"s{seed}_"
+        rng = np.random.default_rng(1000 + seed)
+        out[p + "kind"] = np.array(net.kind.value)
+        out[p + "directed"] = np.array(bool(net.directed))
+        out[p + "beta"] = np.array((0.0, 0.5, 1.0)[(seed // 3) % 3])   # conftest.py:80
+        out[p + "beta_vec"] = op.beta
+        out[p + "gamma"] = np.array(op.gamma)
+        struct = net.incidence if net.kind is ancka.NetworkKind.HYPERGRAPH else (
+            net.adjacency if net.kind is ancka.NetworkKind.GRAPH else None)
+        if struct is None:                      # multiplex: out of scope
+            out[p + "skip"] = np.array(True)
+            continue
+        out[p + "skip"] = np.array(False)
+        _csr(p + "S", struct, out)
+        _x(p + "X", net.attributes, out)
+        out[p + "knn_ids"] = g.neighbors.ids
+        out[p + "knn_scores"] = g.neighbors.scores
+        _csr(p + "AK", g.adjacency, out)
+        _csr(p + "PK", op.p_k, out)
+        out[p + "selfloop"] = op.selfloop
+        n = op.n
+        m = rng.standard_normal((n, 3))
+        out[p + "M"] = m
+        out[p + "apply"] = walk.apply_joint_transition(op, m)
+        out[p + "apply_t"] = walk.apply_structure_rowvec(op, m.T.copy())
+        out[p + "dense"] = walk.dense_transition(op)
+        k = int(min(3, n))
+        out[p + "init"] = engine.init_bcm(op, k, 5, 0.2).assignment
+        lab = random_membership(rng, n, k)
+        out[p + "lab"] = lab
+        out[p + "mhc"] = np.array(engine.calc_mhc(op, ancka.BcmMatrix(lab, k)))
+        out[p + "mhc_brute"] = np.array(walk.brute_mhc_oracle(op, ancka.BcmMatrix(lab, k)))
+        q0 = np.linalg.qr(rng.standard_normal((n, k + 1)))[0] if n > k else None
+        if q0 is not None:
+            out[p + "q0"] = q0
+            q1, r1 = engine.orthogonal_step(op, q0, np.random.default_rng(seed))
+            out[p + "q1"], out[p + "r1"] = q1, r1
+        qd = rng.standard_normal((n, k))
+        d = engine.discretize(qd)
+        out[p + "qd"] = qd
+        out[p + "disc_labels"] = d.y.assignment
+        out[p + "disc_objs"] = np.asarray(d.objectives)
+        out[p + "disc_scores"] = d.scores
+    np.savez_compressed(HERE / "random_instances.npz", **out)
+
+
+def _net(inst):
+    if inst.kind == "graph":
+        return ancka.AttributedNetwork.graph(inst.structure, inst.X)
+    return ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
+
+
+RUNS = [  # (shape, seed, n, p_in, words, early_stop)
+    ("cora", 0, 300, 0.8, 18, True),
+    ("cora", 1, 400, 0.5, 8, True),
+    ("citeseer", 0, 300, 0.8, 32, True),
+    ("dblp", 2, 500, 0.8, 20, True),
+    ("amazon2m", 0, 300, 0.8, None, True),
+    ("cora", 3, 250, 0.8, 18, False),
+]
+
+
+def end_to_end():
+    out, meta = {}, []
+    for i, (shape, seed, n, p_in, words, early) in enumerate(RUNS):
+        inst = synth.make(shape, seed=seed, n=n, p_in=p_in, words=words)
+        p = f"r{i}_"
+        _csr(p + "S", inst.structure, out)
+        _x(p + "X", inst.X, out)
+        params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=seed,
+                                     knn_mode=ancka.KnnMode.EXACT,
+                                     t_a=60 if not early else 1000)
+        res = ancka.run_ancka(_net(inst), params, early_stop=early)
+        out[p + "labels"] = res.y.assignment
+        out[p + "mhc"] = np.array(res.mhc)
+        out[p + "iterations"] = np.array(res.iterations)
+        out[p + "history"] = np.asarray(res.state.mhc_history, dtype=np.float64)
+        out[p + "knn_ids"] = res.knn.neighbors.ids
+        out[p + "knn_scores"] = res.knn.neighbors.scores
+        out[p + "q"] = res.state.q
+        out[p + "planted"] = inst.labels
+        meta.append({"shape": shape, "seed": seed, "n": n, "p_in": p_in, "words": words,
+                     "kind": inst.kind, "k": inst.k, "stop_reason": res.stop_reason,
+                     "early_stop": early, "t_a": params.t_a,
+                     "ari_vs_planted": float(ancka.ari(inst.labels, res.y.assignment))})
+    np.savez_compressed(HERE / "end_to_end.npz", **out)
+    (HERE / "end_to_end.json").write_text(json.dumps(meta, indent=1))
+
+
+if __name__ == "__main__":
+    spec_examples()
+    random_instances()
+    end_to_end()
+    for f in sorted(HERE.glob("*.npz")):
+        print(f.name, f.stat().st_size)
