@@ -1,0 +1,172 @@
+/*
+ * ancka_b200.h -- C ABI of the B200-native ANCKA clustering hot path.
+ *
+ * Plain C: device pointers, sizes and an opaque CUDA stream handle; no torch
+ * or C++ types cross this boundary.  Every entry point returns an ANCKA_*
+ * status; on failure `ancka_last_error()` returns a thread-local message.
+ * The Python package `paper_2408_05459_b200` binds these with ctypes and
+ * keeps the reference's Python API (ancka/__init__.py:12-99) on top.
+ *
+ * Each function names the reference interface it replaces (paths relative
+ * to /root/reference/pkg/src/ancka).  All work is enqueued on `stream`; no
+ * function synchronises the device unless documented ("syncs").
+ */
+#ifndef ANCKA_B200_H
+#define ANCKA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ANCKA_ABI_VERSION 1
+
+typedef void* ancka_stream_t; /* cudaStream_t */
+
+enum ancka_status {
+  ANCKA_OK = 0,
+  ANCKA_ERR_ARG = 1,      /* maps to ValueError                       */
+  ANCKA_ERR_CUDA = 2,     /* maps to RuntimeError                     */
+  ANCKA_ERR_NETWORK = 3,  /* maps to ancka.NetworkError (network.py:39) */
+  ANCKA_ERR_UNSUPPORTED = 4
+};
+
+enum ancka_dtype { ANCKA_F32 = 0, ANCKA_F64 = 1 };
+enum ancka_kind { ANCKA_GRAPH = 0, ANCKA_HYPERGRAPH = 1 };
+
+/* Sparse row matrix on the device.  values == NULL means every stored entry
+ * is 1 (index-only storage of an unweighted factor). */
+typedef struct {
+  int64_t rows, cols, nnz;
+  const int64_t* rowptr; /* rows + 1 */
+  const int32_t* colidx; /* nnz, sorted within each row */
+  const void* values;    /* nnz of the operator dtype, or NULL */
+} ancka_csr;
+
+/* Device-resident WalkOperator (walk.py:89-104).  Index arrays are shared by
+ * the f32 and f64 instances; `dtype` selects the value arrays. */
+typedef struct {
+  int32_t kind;           /* ancka_kind                                  */
+  int32_t dtype;          /* ancka_dtype of values/beta                  */
+  int64_t n, m;           /* nodes, hyperedges (0 for graphs)            */
+  ancka_csr p_n;          /* graph: P_N = D^-1 A            (n x n)       */
+  ancka_csr p_e;          /* hypergraph: P_E = D_E^-1 H     (m x n)       */
+  ancka_csr p_v;          /* hypergraph: P_V = D_V^-1 H^T   (n x m)       */
+  ancka_csr p_k;          /* P_K = D_K^-1 A_K               (n x n)       */
+  ancka_csr t_a;          /* init transposes: graph P_N^T (n x n);
+                             hypergraph P_V^T (m x n)                     */
+  ancka_csr t_b;          /* hypergraph P_E^T (n x m); unused for graphs  */
+  const void* beta;       /* n, beta_vector (walk.py:47-57)              */
+  const uint8_t* selfloop;/* n, 1 where walk.py:123 adds a self-loop     */
+} ancka_operator;
+
+const char* ancka_last_error(void);
+int ancka_abi_version(void);
+/* Fails unless a compute-capability 10.x device is current. */
+int ancka_device_check(void);
+
+/* ---- subsystem 1: exact KNN graph (knn.py:112-140, 294-324) ------------ */
+
+/* Exact top-K cosine neighbours of every row of a dense n x d matrix X (row
+ * stride ldx elements, dtype f64).  Selection and order follow
+ * _ordered_top_k (knn.py:83-98): strictly positive similarities only, j != i,
+ * order (similarity desc, index asc); an all-zero row gets an empty list.
+ * `integer_exact` != 0 declares every X entry an integer with |x| <= 256 and
+ * every row's sum of squares < 2^24: the tcgen05 tensor-core path then
+ * computes exact integer dot products and ranks by exact rational
+ * comparison.  Otherwise an fp64 CUDA-core path runs.
+ * Outputs: ids (n x K int32, -1 padded), scores (n x K f64, 0 padded,
+ * min(s, 1) as knn.py:139).  Raises ANCKA_ERR_NETWORK if K >= n. */
+size_t ancka_knn_workspace_size(int64_t n, int64_t d, int32_t K, int32_t integer_exact);
+int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
+                    int32_t integer_exact, int32_t* ids, double* scores,
+                    void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* build_knn_adjacency + knn_transition (knn.py:294-324): A_K = M + M^T as a
+ * sorted CSR and P_K = D_K^-1 A_K with row sums summed exactly as numpy's
+ * pairwise reduction (so f64 values are bit-identical to scipy's).
+ * Capacities: colidx/val arrays hold 2*n*K entries.  nnz_out is a device
+ * int64.  zero_rows[i] = 1 where row i of A_K is empty. */
+size_t ancka_knn_graph_workspace_size(int64_t n, int32_t K);
+int ancka_knn_graph(const int32_t* ids, const double* scores, int64_t n, int32_t K,
+                    int64_t* rowptr, int32_t* colidx, double* a_k, double* p_k64,
+                    float* p_k32, uint8_t* zero_rows, int64_t* nnz_out,
+                    void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* ---- subsystem 2: walk operator application ---------------------------- */
+
+/* apply_joint_transition (walk.py:177-190): Z = (I-B) P_struct Q + B P_K Q,
+ * Q and Z row-major n x c with leading dims ldq/ldz (multiples of 4 for f32,
+ * 2 for f64; padding columns are read/written as zeros).  `scratch` holds the
+ * hypergraph intermediate P_E Q (m x ldq elements).  With f64 the summation
+ * order equals scipy's csr_matvecs, so results are bit-identical. */
+int ancka_op_apply(const ancka_operator* op, const void* Q, int64_t ldq, int32_t c,
+                   void* Z, int64_t ldz, void* scratch, ancka_stream_t stream);
+
+/* apply_structure_rowvec (walk.py:153-174) in column form: Z = P_struct^T Q
+ * (+ self-loops). */
+int ancka_op_apply_struct_t(const ancka_operator* op, const void* Q, int64_t ldq, int32_t c,
+                            void* Z, int64_t ldz, void* scratch, ancka_stream_t stream);
+
+/* ---- engine pieces (engine.py) ----------------------------------------- */
+
+/* init_bcm (engine.py:87-127) after centre selection: t_i restart-walk steps
+ * on the transposed structure (f64) and the first-max argmax over centres.
+ * centers: device int64[k] sorted.  labels_out: int32[n]. */
+size_t ancka_init_workspace_size(const ancka_operator* op, int32_t k);
+int ancka_init_bcm(const ancka_operator* op64, const int64_t* centers, int32_t k, int32_t t_i,
+                   double alpha, int32_t* labels_out, void* workspace, size_t workspace_bytes,
+                   ancka_stream_t stream);
+
+/* orthogonal_step (engine.py:130-149), f32 fast path: Z = apply(Q_prev);
+ * Cholesky-QR with an f64 Gram and f64 k x k factor; Q_out = Z R^-1 (diag R
+ * > 0 by construction, the reference's sign convention).  stats (device
+ * f64[4]): [0] = ||Q_out - Q_prev||_F^2 (overwritten each step),
+ * [1] = min(stats[1], min pivot ratio R_jj^2 / G_jj), [2] += number of
+ * suspect pivots (ratio <= 1e-9); the caller resets [1] = 1, [2] = 0.
+ * [3] reserved. */
+size_t ancka_orth_workspace_size(const ancka_operator* op, int32_t c);
+int ancka_orth_step_f32(const ancka_operator* op32, const float* Q_prev, float* Q_out,
+                        float* Z, int64_t ld, int32_t c, double* stats,
+                        void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* Thin QR in f64 by classical Gram-Schmidt with re-orthogonalisation
+ * (Householder-equivalent Q/|R_jj| for full-rank columns; the reference's
+ * rank test engine.py:141-142 is applied by the caller on rdiag).
+ * Z (n x c, ld) is overwritten by Q.  rdiag: device f64[c]. */
+size_t ancka_qr_f64_workspace_size(int64_t n, int32_t c);
+int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double* rdiag,
+                 void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* discretize + repair_empty_clusters (engine.py:162-288) on columns
+ * [col0, col0+k) of Q (f32, n x ldq): two alternating-rounding runs (identity
+ * and prototype start), up to max_iter rounds each, |d obj| < tol.
+ * labels_out: int32[n]; info (device f64[8 + 2*max_iter + 2*k*k]):
+ *   [0] final objective  [1] rounds  [2] converged  [3] winning run (0 id, 1 proto)
+ *   [4] empty clusters left (repair impossible -> NetworkError)
+ *   [5] zero rows  [6] rounds of run 0  [7] rounds of run 1
+ *   [8 ...] objective trace of run 0 (max_iter slots) then run 1,
+ *   then the final k x k rotation R of run 0 and of run 1 (row-major). */
+size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t max_iter);
+int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64_t n, int32_t k,
+                     int32_t max_iter, double tol, int32_t* labels_out, double* info,
+                     void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* calc_mhc (engine.py:291-299): phi = 1 - tr(Yhat^T F)/k after gamma steps of
+ * F <- (1-alpha) apply(F) + alpha Yhat.  phi_out: device f64[1]; sizes_out:
+ * device int64[k] (cluster sizes; an empty cluster -> phi = NaN). */
+size_t ancka_mhc_workspace_size(const ancka_operator* op, int32_t k);
+int ancka_mhc(const ancka_operator* op, const int32_t* labels, int32_t k, double alpha,
+              int32_t gamma, double* phi_out, int64_t* sizes_out,
+              void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* Cluster sizes (BcmMatrix.cluster_sizes, network.py:176-177). */
+int ancka_cluster_sizes(const int32_t* labels, int64_t n, int32_t k, int64_t* sizes_out,
+                        ancka_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ANCKA_B200_H */

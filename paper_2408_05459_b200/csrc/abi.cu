@@ -1,0 +1,67 @@
+// C-ABI entry points that are not owned by a subsystem file, plus the KNN
+// dispatcher (tensor-core integer-exact path vs f64 CUDA-core path).
+#include <cstdarg>
+
+#include "common.cuh"
+#include "knn.cuh"
+
+namespace ancka {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+}  // namespace ancka
+
+using namespace ancka;
+
+extern "C" const char* ancka_last_error(void) { return g_err; }
+extern "C" int ancka_abi_version(void) { return ANCKA_ABI_VERSION; }
+
+extern "C" int ancka_device_check(void) {
+  int dev = 0;
+  ANCKA_CUDA(cudaGetDevice(&dev));
+  cudaDeviceProp prop;
+  ANCKA_CUDA(cudaGetDeviceProperties(&prop, dev));
+  ANCKA_REQUIRE(prop.major == 10, ANCKA_ERR_UNSUPPORTED,
+                "device %s is sm_%d%d; this library is built for sm_100a only", prop.name,
+                prop.major, prop.minor);
+  return ANCKA_OK;
+}
+
+static void carve_knn_simt(Carver& cv, int64_t n, int64_t d, double** xn, double** norms,
+                           int64_t* ldn) {
+  *ldn = (d + 15) / 16 * 16;
+  *xn = cv.take<double>((size_t)n * *ldn);
+  *norms = cv.take<double>(n);
+}
+
+extern "C" size_t ancka_knn_workspace_size(int64_t n, int64_t d, int32_t K, int32_t integer_exact) {
+  if (integer_exact) return knn_tc_workspace(n, d, K);
+  Carver cv(nullptr, 0);
+  double *xn, *nr;
+  int64_t ldn;
+  carve_knn_simt(cv, n, d, &xn, &nr, &ldn);
+  return cv.used;
+}
+
+extern "C" int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
+                               int32_t integer_exact, int32_t* ids, double* scores,
+                               void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
+  ANCKA_REQUIRE(K < n, ANCKA_ERR_NETWORK, "K=%d must be smaller than n=%lld", K, (long long)n);
+  ANCKA_REQUIRE(K >= 1 && d >= 1, ANCKA_ERR_ARG, "knn: bad sizes");
+  auto st = as_stream(stream);
+  if (integer_exact) return knn_tc(X, n, d, ldx, K, ids, scores, workspace, workspace_bytes, st);
+  Carver cv(workspace, workspace_bytes);
+  double *xn, *nr;
+  int64_t ldn;
+  carve_knn_simt(cv, n, d, &xn, &nr, &ldn);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn: workspace too small");
+  ANCKA_TRY(normalize_rows_f64(X, n, d, ldx, xn, ldn, nr, st));
+  return knn_simt(xn, n, ldn, nr, K, ids, scores, st);
+}

@@ -1,0 +1,271 @@
+// Walk-operator application (subsystem 2): CSR SpMM against a dense n x c
+// block with the joint-walk mix, self-loops and the MHC / init epilogues
+// fused (walk.py:135-190, engine.py:116-117,
+// engine.py:296-297).
+//
+// Mapping: one thread owns (row, V-wide column chunk) and walks the row's
+// nonzeros in index order.  Threads of one row read the same index/value
+// (broadcast) and gather one contiguous c-wide row of the source per
+// nonzero, so a row gather is one coalesced transaction group.  The f64
+// instantiation accumulates sequentially with non-contracted mul/add, i.e.
+// in exactly scipy csr_matvecs' order, giving bit-identical results.
+#include "common.cuh"
+#include "spmm.cuh"
+
+namespace ancka {
+
+template <typename T> struct Vec;
+template <> struct Vec<float> { using type = float4; static constexpr int W = 4; };
+template <> struct Vec<double> { using type = double2; static constexpr int W = 2; };
+
+__device__ __forceinline__ float4 ldv(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ double2 ldv(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
+__device__ __forceinline__ void fma_acc(float4& acc, float w, float4 x) {
+  acc.x = fmaf(w, x.x, acc.x); acc.y = fmaf(w, x.y, acc.y);
+  acc.z = fmaf(w, x.z, acc.z); acc.w = fmaf(w, x.w, acc.w);
+}
+// f64: keep the multiply and the add separately rounded (scipy order).
+__device__ __forceinline__ void fma_acc(double2& acc, double w, double2 x) {
+  acc.x = __dadd_rn(acc.x, __dmul_rn(w, x.x));
+  acc.y = __dadd_rn(acc.y, __dmul_rn(w, x.y));
+}
+__device__ __forceinline__ void add_acc(float4& acc, float4 x) {
+  acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+}
+__device__ __forceinline__ void add_acc(double2& acc, double2 x) {
+  acc.x = __dadd_rn(acc.x, x.x); acc.y = __dadd_rn(acc.y, x.y);
+}
+
+template <typename T, typename VT>
+__device__ __forceinline__ VT seg_sum(const SegArgs<T>& s, int64_t row, int64_t coloff) {
+  VT acc;
+  memset(&acc, 0, sizeof(acc));
+  if (s.rowptr == nullptr) return acc;
+  const int64_t b = __ldg(s.rowptr + row), e = __ldg(s.rowptr + row + 1);
+  const T* src = s.src + coloff;
+  int64_t p = b;
+  // 4-way unrolled: loads issued together, adds kept in order.
+  for (; p + 4 <= e; p += 4) {
+    int32_t j0 = __ldg(s.colidx + p), j1 = __ldg(s.colidx + p + 1);
+    int32_t j2 = __ldg(s.colidx + p + 2), j3 = __ldg(s.colidx + p + 3);
+    T w0 = s.values ? __ldg(s.values + p) : T(1);
+    T w1 = s.values ? __ldg(s.values + p + 1) : T(1);
+    T w2 = s.values ? __ldg(s.values + p + 2) : T(1);
+    T w3 = s.values ? __ldg(s.values + p + 3) : T(1);
+    VT x0 = ldv(src + (int64_t)j0 * s.ld);
+    VT x1 = ldv(src + (int64_t)j1 * s.ld);
+    VT x2 = ldv(src + (int64_t)j2 * s.ld);
+    VT x3 = ldv(src + (int64_t)j3 * s.ld);
+    fma_acc(acc, w0, x0);
+    fma_acc(acc, w1, x1);
+    fma_acc(acc, w2, x2);
+    fma_acc(acc, w3, x3);
+  }
+  for (; p < e; ++p) {
+    int32_t j = __ldg(s.colidx + p);
+    T w = s.values ? __ldg(s.values + p) : T(1);
+    fma_acc(acc, w, ldv(src + (int64_t)j * s.ld));
+  }
+  return acc;
+}
+
+template <typename T>
+__device__ __forceinline__ T comp(const typename Vec<T>::type& v, int i);
+template <> __device__ __forceinline__ float comp<float>(const float4& v, int i) {
+  return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
+}
+template <> __device__ __forceinline__ double comp<double>(const double2& v, int i) {
+  return i == 0 ? v.x : v.y;
+}
+__device__ __forceinline__ void set_comp(float4& v, int i, float x) {
+  if (i == 0) v.x = x; else if (i == 1) v.y = x; else if (i == 2) v.z = x; else v.w = x;
+}
+__device__ __forceinline__ void set_comp(double2& v, int i, double x) {
+  if (i == 0) v.x = x; else v.y = x;
+}
+__device__ __forceinline__ float dmul(float a, float b) { return a * b; }
+__device__ __forceinline__ float dadd(float a, float b) { return a + b; }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+spmm_kernel(SpmmArgs<T> a) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / a.nchunk;
+  if (row >= a.rows) return;
+  const int chunk = (int)(gid - row * a.nchunk);
+  const int64_t coloff = (int64_t)chunk * W;
+
+  VT s = seg_sum<T, VT>(a.s, row, coloff);
+  if (a.selfloop && a.selfloop[row]) add_acc(s, ldv(a.self_src + row * a.self_ld + coloff));
+  VT out = s;
+  if (a.beta) {
+    VT k = seg_sum<T, VT>(a.k, row, coloff);
+    const T b = __ldg(a.beta + row);
+    const T omb = dadd(T(1), -b);   // 1.0 - beta, as (1.0 - op.beta)
+#pragma unroll
+    for (int i = 0; i < W; ++i)
+      set_comp(out, i, dadd(dmul(omb, comp<T>(s, i)), dmul(b, comp<T>(k, i))));
+  }
+  if (a.tag) {  // out = scale * out + (col == tag[row] ? tagval[col] : 0)
+    const int t = __ldg(a.tag + row);
+#pragma unroll
+    for (int i = 0; i < W; ++i) {
+      const int col = (int)coloff + i;
+      T v = dmul(a.scale, comp<T>(out, i));
+      const T add = (col == t && col < a.c) ? a.tagval[col] : T(0);
+      set_comp(out, i, dadd(v, add));
+    }
+  }
+  // padding columns stay exactly zero
+#pragma unroll
+  for (int i = 0; i < W; ++i)
+    if ((int)coloff + i >= a.c) set_comp(out, i, T(0));
+  *reinterpret_cast<VT*>(a.out + row * a.ldo + coloff) = out;
+}
+
+template <typename T>
+int launch_spmm(const SpmmArgs<T>& args, cudaStream_t st) {
+  if (args.rows == 0) return ANCKA_OK;
+  const int64_t threads = args.rows * args.nchunk;
+  const int bs = 256;
+  const int64_t grid = ceil_div(threads, bs);
+  ANCKA_REQUIRE(grid < (1ll << 31), ANCKA_ERR_ARG, "spmm grid too large");
+  spmm_kernel<T><<<(unsigned)grid, bs, 0, st>>>(args);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+template int launch_spmm<float>(const SpmmArgs<float>&, cudaStream_t);
+template int launch_spmm<double>(const SpmmArgs<double>&, cudaStream_t);
+
+// ---------------------------------------------------------------------------
+template <typename T>
+static SegArgs<T> seg_of(const ancka_csr& m, const T* src, int64_t ld) {
+  SegArgs<T> s{};
+  if (m.rowptr == nullptr) return s;
+  s.rowptr = m.rowptr;
+  s.colidx = m.colidx;
+  s.values = static_cast<const T*>(m.values);
+  s.src = src;
+  s.ld = ld;
+  return s;
+}
+
+template <typename T>
+int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, int64_t ldz,
+               T* scratch, cudaStream_t st, const EpilogueTag<T>* epi) {
+  constexpr int W = Vec<T>::W;
+  ANCKA_REQUIRE(ldq % W == 0 && ldz % W == 0 && ldq >= c && ldz >= c, ANCKA_ERR_ARG,
+                "op_apply: leading dims must be multiples of %d and >= c", W);
+  const int nchunk = (int)ceil_div(c, W);
+  SpmmArgs<T> a{};
+  a.c = c;
+  a.nchunk = nchunk;
+  if (op->kind == ANCKA_HYPERGRAPH) {
+    ANCKA_REQUIRE(scratch != nullptr, ANCKA_ERR_ARG, "hypergraph apply needs scratch");
+    // stage 1: T = P_E Q   (m x c)
+    SpmmArgs<T> s1{};
+    s1.c = c;
+    s1.nchunk = nchunk;
+    s1.rows = op->m;
+    s1.s = seg_of<T>(op->p_e, Q, ldq);
+    s1.out = scratch;
+    s1.ldo = ldq;
+    ANCKA_TRY(launch_spmm<T>(s1, st));
+    a.s = seg_of<T>(op->p_v, scratch, ldq);
+  } else {
+    a.s = seg_of<T>(op->p_n, Q, ldq);
+  }
+  a.rows = op->n;
+  a.selfloop = op->selfloop;
+  a.self_src = Q;
+  a.self_ld = ldq;
+  a.k = seg_of<T>(op->p_k, Q, ldq);
+  a.beta = static_cast<const T*>(op->beta);
+  a.out = Z;
+  a.ldo = ldz;
+  if (epi) {
+    a.tag = epi->tag;
+    a.tagval = epi->tagval;
+    a.scale = epi->scale;
+  }
+  return launch_spmm<T>(a, st);
+}
+
+template <typename T>
+int op_apply_struct_t_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z,
+                        int64_t ldz, T* scratch, cudaStream_t st, const EpilogueTag<T>* epi) {
+  constexpr int W = Vec<T>::W;
+  ANCKA_REQUIRE(ldq % W == 0 && ldz % W == 0, ANCKA_ERR_ARG, "struct_t: bad leading dims");
+  const int nchunk = (int)ceil_div(c, W);
+  SpmmArgs<T> a{};
+  a.c = c;
+  a.nchunk = nchunk;
+  if (op->kind == ANCKA_HYPERGRAPH) {
+    ANCKA_REQUIRE(scratch != nullptr, ANCKA_ERR_ARG, "hypergraph apply needs scratch");
+    // (p_e^T @ (p_v^T @ m)): stage A U = P_V^T Q (m x c), stage B P_E^T U
+    SpmmArgs<T> s1{};
+    s1.c = c;
+    s1.nchunk = nchunk;
+    s1.rows = op->m;
+    s1.s = seg_of<T>(op->t_a, Q, ldq);
+    s1.out = scratch;
+    s1.ldo = ldq;
+    ANCKA_TRY(launch_spmm<T>(s1, st));
+    a.s = seg_of<T>(op->t_b, scratch, ldq);
+  } else {
+    a.s = seg_of<T>(op->t_a, Q, ldq);
+  }
+  a.rows = op->n;
+  a.selfloop = op->selfloop;
+  a.self_src = Q;
+  a.self_ld = ldq;
+  a.out = Z;
+  a.ldo = ldz;
+  if (epi) {
+    a.tag = epi->tag;
+    a.tagval = epi->tagval;
+    a.scale = epi->scale;
+  }
+  return launch_spmm<T>(a, st);
+}
+
+template int op_apply_t<float>(const ancka_operator*, const float*, int64_t, int, float*, int64_t,
+                               float*, cudaStream_t, const EpilogueTag<float>*);
+template int op_apply_t<double>(const ancka_operator*, const double*, int64_t, int, double*,
+                                int64_t, double*, cudaStream_t, const EpilogueTag<double>*);
+template int op_apply_struct_t_t<float>(const ancka_operator*, const float*, int64_t, int, float*,
+                                        int64_t, float*, cudaStream_t, const EpilogueTag<float>*);
+template int op_apply_struct_t_t<double>(const ancka_operator*, const double*, int64_t, int,
+                                         double*, int64_t, double*, cudaStream_t,
+                                         const EpilogueTag<double>*);
+
+}  // namespace ancka
+
+extern "C" int ancka_op_apply(const ancka_operator* op, const void* Q, int64_t ldq, int32_t c,
+                              void* Z, int64_t ldz, void* scratch, ancka_stream_t stream) {
+  if (!op) { ancka::set_error("null operator"); return ANCKA_ERR_ARG; }
+  auto st = ancka::as_stream(stream);
+  if (op->dtype == ANCKA_F64)
+    return ancka::op_apply_t<double>(op, (const double*)Q, ldq, c, (double*)Z, ldz,
+                                     (double*)scratch, st, nullptr);
+  return ancka::op_apply_t<float>(op, (const float*)Q, ldq, c, (float*)Z, ldz, (float*)scratch,
+                                  st, nullptr);
+}
+
+extern "C" int ancka_op_apply_struct_t(const ancka_operator* op, const void* Q, int64_t ldq,
+                                       int32_t c, void* Z, int64_t ldz, void* scratch,
+                                       ancka_stream_t stream) {
+  if (!op) { ancka::set_error("null operator"); return ANCKA_ERR_ARG; }
+  auto st = ancka::as_stream(stream);
+  if (op->dtype == ANCKA_F64)
+    return ancka::op_apply_struct_t_t<double>(op, (const double*)Q, ldq, c, (double*)Z, ldz,
+                                              (double*)scratch, st, nullptr);
+  return ancka::op_apply_struct_t_t<float>(op, (const float*)Q, ldq, c, (float*)Z, ldz,
+                                           (float*)scratch, st, nullptr);
+}

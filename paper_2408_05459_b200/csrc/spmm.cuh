@@ -1,0 +1,49 @@
+// Internal interface of the walk-operator SpMM (spmm.cu).
+#pragma once
+#include "common.cuh"
+
+namespace ancka {
+
+template <typename T>
+struct SegArgs {
+  const int64_t* rowptr = nullptr;  // nullptr: empty segment
+  const int32_t* colidx = nullptr;
+  const T* values = nullptr;        // nullptr: unit weights
+  const T* src = nullptr;           // gathered block
+  int64_t ld = 0;
+};
+
+// out[row] = epilogue( mix( s_row (+ self), k_row ) )
+template <typename T>
+struct SpmmArgs {
+  int64_t rows = 0;
+  int c = 0, nchunk = 0;
+  SegArgs<T> s, k;
+  const uint8_t* selfloop = nullptr;
+  const T* self_src = nullptr;
+  int64_t self_ld = 0;
+  const T* beta = nullptr;          // nullptr: no mix (structure only)
+  const int32_t* tag = nullptr;     // epilogue: out = scale*out + (col==tag ? tagval[col] : 0)
+  const T* tagval = nullptr;
+  T scale = T(1);
+  T* out = nullptr;
+  int64_t ldo = 0;
+};
+
+template <typename T>
+struct EpilogueTag {
+  const int32_t* tag;
+  const T* tagval;
+  T scale;
+};
+
+template <typename T> int launch_spmm(const SpmmArgs<T>& args, cudaStream_t st);
+
+template <typename T>
+int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, int64_t ldz,
+               T* scratch, cudaStream_t st, const EpilogueTag<T>* epi);
+template <typename T>
+int op_apply_struct_t_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z,
+                        int64_t ldz, T* scratch, cudaStream_t st, const EpilogueTag<T>* epi);
+
+}  // namespace ancka

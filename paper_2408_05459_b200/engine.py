@@ -1,0 +1,524 @@
+"""ANCKA clustering engine on the B200 (reference: ancka/engine.py).
+
+`run_ancka` keeps the whole loop device-resident:
+
+* greedy init          -> ancka_init_bcm (f64, engine.py:87-127)
+* t = 1 (rank-deficient by construction) -> f64 apply +
+  f64 CGS2 QR with the reference's rank test and its exact numpy noise
+  draw (engine.py:139-149), so Q^(1) matches the reference to rounding
+* t >= 2               -> ancka_orth_step_f32 (fused SpMM + Cholesky-QR),
+  captured in a CUDA graph per tau-block
+* every tau            -> ancka_discretize (one cooperative kernel) and
+  ancka_mhc; one small device->host read of (phi, ||dQ||, flags) drives the
+  reference's stop rules on the host (engine.py:402-418).
+
+A suspect Cholesky pivot anywhere in a tau-block rolls the block back and
+replays it with the exact f64 step.
+"""
+from __future__ import annotations
+
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._device import WORKSPACE, dev, ld_for, padded
+from .knn import (KnnGraph, NeighborLists, build_knn_graph_device, cache_key,
+                  knn_search_exact_device, load_neighbor_cache, save_neighbor_cache)
+from .network import (AttributedNetwork, BcmMatrix, ClusterParams, KnnMode, NetworkError,
+                      default_knn_k, validate_network)
+from .walk import WalkOperator, build_walk_operator
+
+DISCRETIZE_MAX_ITER = 100
+DISCRETIZE_TOL = 1e-10
+_TIMING_KEYS = ("knn_ms", "init_ms", "ortho_ms", "discretize_ms", "mhc_ms")
+
+
+class EngineState:
+    """Loop state (engine.py:41-49); `q` is materialised from HBM on access."""
+
+    def __init__(self, q_dev, best_y, best_mhc, mhc_history=None, iteration=0, c=None):
+        self.q_dev = q_dev
+        self._c = c
+        self.best_y = best_y
+        self.best_mhc = best_mhc
+        self.mhc_history = mhc_history if mhc_history is not None else []
+        self.iteration = iteration
+
+    @property
+    def q(self) -> np.ndarray:
+        t = self.q_dev if self._c is None else self.q_dev[:, : self._c]
+        return t.double().cpu().numpy()
+
+
+@dataclass
+class ClusterResult:
+    y: BcmMatrix
+    mhc: float
+    iterations: int
+    timings_ms: dict
+    state: EngineState
+    knn: KnnGraph
+    operator: WalkOperator
+    converged: bool
+    stop_reason: str
+    warnings: list = field(default_factory=list)
+    error: str | None = None
+
+
+@dataclass
+class DiscretizeResult:
+    y: BcmMatrix
+    scores: np.ndarray
+    objectives: list
+    iterations: int
+    converged: bool
+    runs: tuple = ()
+
+
+class _PhaseTimer:
+    """CUDA-event phase timing (engine.py:67-72 semantics, device clock)."""
+
+    def __init__(self):
+        self.totals = {k: 0.0 for k in _TIMING_KEYS}
+        self._open = []
+
+    def span(self, key):
+        timer = self
+
+        class _Span:
+            def __enter__(self_):
+                self_.a = torch.cuda.Event(enable_timing=True)
+                self_.a.record()
+
+            def __exit__(self_, *exc):
+                b = torch.cuda.Event(enable_timing=True)
+                b.record()
+                timer._open.append((key, self_.a, b))
+
+        return _Span()
+
+    def add_host(self, key, t0):
+        self.totals[key] += (time.perf_counter() - t0) * 1e3
+
+    def flush(self):
+        for key, a, b in self._open:
+            b.synchronize()
+            self.totals[key] += a.elapsed_time(b)
+        self._open.clear()
+
+
+# ----------------------------------------------------------------------------
+def normalize_bcm(y: BcmMatrix) -> np.ndarray:
+    """Column-orthonormal membership (engine.py:75-84)."""
+    sizes = y.cluster_sizes()
+    if (sizes == 0).any():
+        raise NetworkError(f"empty cluster(s) {y.empty_clusters().tolist()}: normalization undefined")
+    out = np.zeros((y.n, y.k))
+    out[np.arange(y.n), y.assignment] = 1.0 / np.sqrt(sizes[y.assignment])
+    return out
+
+
+def _centers(deg: np.ndarray, k: int) -> np.ndarray:
+    """Top-k degree nodes, ties to the smaller index, sorted (engine.py:97-110)."""
+    n = deg.size
+    nonzero = int((deg > 0).sum())
+    if k > nonzero:
+        warnings.warn(f"only {nonzero} nodes have nonzero degree; "
+                      f"filling {k - nonzero} center(s) in index order")
+        chosen = np.lexsort((np.arange(n), -deg))[:nonzero]
+        mask = np.zeros(n, dtype=bool)
+        mask[chosen] = True
+        rest = np.flatnonzero(~mask)[: k - nonzero]
+        return np.sort(np.concatenate([chosen, rest]).astype(np.int64))
+    if k == n:
+        return np.arange(n, dtype=np.int64)
+    kth = np.partition(-deg, k - 1)[k - 1]        # -(k-th largest degree)
+    above = np.flatnonzero(-deg < kth)
+    ties = np.flatnonzero(-deg == kth)[: k - above.size]
+    return np.sort(np.concatenate([above, ties]).astype(np.int64))
+
+
+def _init_labels_device(op: WalkOperator, k: int, t_i: int, alpha: float):
+    n = op.n
+    if k > n:
+        raise NetworkError(f"k={k} exceeds node count n={n}")
+    centers = _centers(op.degrees, k)
+    cdev = torch.from_numpy(centers).to(dev())
+    labels = torch.empty(n, dtype=torch.int32, device=dev())
+    s64 = op.struct(_lib.F64)
+    wsb = _lib.load().ancka_init_workspace_size(s64, k)
+    ws = WORKSPACE.get("init", wsb)
+    _lib.call("ancka_init_bcm", s64, cdev.data_ptr(), k, t_i, float(alpha), labels.data_ptr(),
+              ws.data_ptr(), ws.numel(), _lib.stream())
+    sizes = _cluster_sizes(labels, k)
+    if (sizes == 0).any():
+        warnings.warn("greedy init left empty cluster(s); pinning centers")
+        labels[cdev] = torch.arange(k, dtype=torch.int32, device=dev())
+    return labels, centers
+
+
+def _cluster_sizes(labels: torch.Tensor, k: int) -> np.ndarray:
+    sizes = torch.empty(k, dtype=torch.int64, device=labels.device)
+    _lib.call("ancka_cluster_sizes", labels.data_ptr(), labels.numel(), k, sizes.data_ptr(),
+              _lib.stream())
+    return sizes.cpu().numpy()
+
+
+def init_bcm(op: WalkOperator, k: int, t_i: int, alpha: float) -> BcmMatrix:
+    """Greedy membership seeding (engine.py:87-127), on the device."""
+    _lib.require_device()
+    labels, _ = _init_labels_device(op, k, t_i, alpha)
+    return BcmMatrix(assignment=labels.cpu().numpy().astype(np.int64), k=k)
+
+
+# --------------------------------------------------------------- QR ---------
+def _qr_f64_inplace(z: torch.Tensor, c: int) -> np.ndarray:
+    n = z.shape[0]
+    rdiag = torch.empty(c, dtype=torch.float64, device=z.device)
+    wsb = _lib.load().ancka_qr_f64_workspace_size(n, c)
+    ws = WORKSPACE.get("qr64", wsb)
+    _lib.call("ancka_qr_f64", z.data_ptr(), n, z.stride(0), c, rdiag.data_ptr(), ws.data_ptr(),
+              ws.numel(), _lib.stream())
+    return rdiag.cpu().numpy()
+
+
+def _exact_step(op: WalkOperator, q64: torch.Tensor, c: int, rng: np.random.Generator):
+    """orthogonal_step (engine.py:130-149) in f64: apply, QR, the reference's
+    rank test on |R_jj|, seeded noise on bad columns, re-QR.  Returns the new
+    f64 block (diag R > 0 by construction) and Z."""
+    n = op.n
+    z = torch.empty_like(q64)
+    scr = op.scratch(c, torch.float64)
+    _lib.call("ancka_op_apply", op.struct(_lib.F64), q64.data_ptr(), q64.stride(0), c,
+              z.data_ptr(), z.stride(0), scr.data_ptr(), _lib.stream())
+    q = z.clone()
+    d = _qr_f64_inplace(q, c)
+    bad = d < 1e-12 * max(1.0, d.max() if d.size else 1.0)
+    if bad.any():
+        warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
+        noise = rng.standard_normal((n, int(bad.sum())))
+        cols = torch.from_numpy(np.flatnonzero(bad)).to(z.device)
+        z[:, cols] += 1e-8 * torch.from_numpy(noise).to(z.device)
+        q = z.clone()
+        _qr_f64_inplace(q, c)
+    return q, z
+
+
+def orthogonal_step(op: WalkOperator, q_prev, rng: np.random.Generator):
+    """One multiply-then-QR step with the reference's rank handling and sign
+    convention (engine.py:130-149).  numpy in, numpy (q, r) out."""
+    _lib.require_device()
+    q_prev = np.asarray(q_prev, dtype=np.float64)
+    c = q_prev.shape[1]
+    q, z = _exact_step(op, padded(q_prev, torch.float64), c, rng)
+    qc, zc = q[:, :c], z[:, :c]
+    r = torch.triu(qc.T @ zc)
+    return qc.cpu().numpy(), r.cpu().numpy()
+
+
+# --------------------------------------------------------- discretize -------
+def _discretize_device(q32: torch.Tensor, col0: int, k: int, max_iter: int, tol: float,
+                       labels_out: torch.Tensor, info: torch.Tensor):
+    n = q32.shape[0]
+    wsb = _lib.load().ancka_discretize_workspace_size(n, k, max_iter)
+    ws = WORKSPACE.get("disc", wsb)
+    _lib.call("ancka_discretize", q32.data_ptr(), q32.stride(0), col0, n, k, max_iter, float(tol),
+              labels_out.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+
+
+def discretize(q, max_iter: int = DISCRETIZE_MAX_ITER, tol: float = DISCRETIZE_TOL) -> DiscretizeResult:
+    """Alternating argmax rounding / Procrustes rotation from the identity and
+    the prototype start (engine.py:221-263), one cooperative kernel."""
+    _lib.require_device()
+    qh = np.asarray(q, dtype=np.float64) if not isinstance(q, torch.Tensor) else q
+    if qh.ndim != 2 or qh.shape[1] < 1:
+        raise NetworkError("discretize expects an n x k block with k >= 1")
+    n, k = qh.shape
+    q32 = padded(torch.as_tensor(qh), torch.float32)
+    labels = torch.empty(n, dtype=torch.int32, device=dev())
+    info = torch.zeros(8 + 2 * max_iter + 2 * k * k, dtype=torch.float64, device=dev())
+    _discretize_device(q32, 0, k, max_iter, tol, labels, info)
+    inf = info.cpu().numpy()
+    if inf[5] > 0:
+        warnings.warn(f"{int(inf[5])} all-zero row(s); assigning to cluster 0")
+    win = int(inf[3])
+    runs = tuple((name, list(inf[8 + r * max_iter: 8 + r * max_iter + int(inf[6 + r])]))
+                 for r, name in enumerate(("identity", "prototype")))
+    rot = inf[8 + 2 * max_iter + win * k * k: 8 + 2 * max_iter + (win + 1) * k * k].reshape(k, k)
+    qd = torch.as_tensor(qh, dtype=torch.float64, device=dev())
+    nrm = torch.linalg.vector_norm(qd, dim=1, keepdim=True)
+    qt = torch.where(nrm > 0, qd / torch.where(nrm > 0, nrm, torch.ones_like(nrm)), torch.zeros_like(qd))
+    scores = (qt @ torch.from_numpy(rot).to(qd.device)).cpu().numpy()
+    lab = labels.cpu().numpy().astype(np.int64)
+    return DiscretizeResult(y=BcmMatrix(assignment=lab, k=k), scores=scores,
+                            objectives=runs[win][1], iterations=int(inf[1]),
+                            converged=bool(inf[2]), runs=runs)
+
+
+def repair_empty_clusters(y: BcmMatrix, scores: np.ndarray) -> BcmMatrix:
+    """Margin-based re-seeding of empty clusters (engine.py:266-288).  Host
+    API helper; inside run_ancka the discretisation kernel performs it."""
+    empties = y.empty_clusters()
+    if not empties.size:
+        return y
+    warnings.warn(f"re-seeding {empties.size} empty cluster(s) after discretization")
+    a = y.assignment.copy()
+    margin = np.partition(scores, -2, axis=1)[:, -2] if scores.shape[1] >= 2 else scores[:, 0]
+    for c in empties:
+        movable = np.bincount(a, minlength=y.k)[a] >= 2
+        if not movable.any():
+            raise NetworkError("cannot repair empty clusters: no movable nodes")
+        a[int(np.argmax(np.where(movable, margin, -np.inf)))] = c
+    return BcmMatrix(assignment=a, k=y.k)
+
+
+# ---------------------------------------------------------------- MHC -------
+class _MhcRunner:
+    def __init__(self, op: WalkOperator, k: int, dtype: int):
+        self.op, self.k, self.dtype = op, k, dtype
+        self.s = op.struct(dtype)
+        self.ws = WORKSPACE.get(f"mhc{dtype}", _lib.load().ancka_mhc_workspace_size(self.s, k))
+        self.phi = torch.zeros(1, dtype=torch.float64, device=dev())
+        self.sizes = torch.zeros(k, dtype=torch.int64, device=dev())
+
+    def __call__(self, labels: torch.Tensor, phi_out: torch.Tensor | None = None):
+        out = self.phi if phi_out is None else phi_out
+        _lib.call("ancka_mhc", self.s, labels.data_ptr(), self.k, self.op.alpha, self.op.gamma,
+                  out.data_ptr(), self.sizes.data_ptr(), self.ws.data_ptr(), self.ws.numel(),
+                  _lib.stream())
+        return out
+
+
+def calc_mhc(op: WalkOperator, y: BcmMatrix) -> float:
+    """Multi-hop conductance (engine.py:291-299), f64 on the device."""
+    _lib.require_device()
+    normalize_bcm(y)  # raises on empty clusters, as the reference
+    lab = torch.from_numpy(y.assignment.astype(np.int32)).to(dev())
+    return float(_MhcRunner(op, y.k, _lib.F64)(lab).item())
+
+
+# ------------------------------------------------------------ pipeline ------
+def build_pipeline(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None):
+    """Validate (host), exact KNN + KNN graph + walk operator (device)
+    (engine.py:302-340)."""
+    from pathlib import Path
+
+    _lib.require_device()
+    watch = _PhaseTimer()
+    net, _ = validate_network(net)
+    params.validate_for(net.n)
+    t0 = time.perf_counter()
+    K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, net.n)
+    if K >= net.n:
+        warnings.warn(f"clamping KNN K={K} to n-1={net.n - 1}")
+        K = net.n - 1
+    neighbors, mode_used, cache_path = None, None, None
+    if knn_cache_dir is not None:
+        cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
+        if cache_path.exists():
+            neighbors, mode_used = load_neighbor_cache(cache_path)
+    if neighbors is None:
+        if params.knn_mode is KnnMode.APPROX:
+            warnings.warn("approximate KNN is not implemented on B200; running exact search")
+        ids, scores = knn_search_exact_device(net.attributes, K)
+        neighbors, mode_used = NeighborLists(ids_dev=ids, scores_dev=scores, K=K), KnnMode.EXACT
+        if cache_path is not None:
+            cache_path.parent.mkdir(parents=True, exist_ok=True)
+            save_neighbor_cache(cache_path, neighbors, mode_used)
+    ids, scores = neighbors.device()
+    A, P, zero = build_knn_graph_device(ids, scores, net.n)
+    g = KnnGraph(A, P, zero, neighbors, mode_used)
+    op = build_walk_operator(net, P, zero, params.alpha, params.beta, params.gamma)
+    torch.cuda.current_stream().synchronize()
+    watch.add_host("knn_ms", t0)
+    return op, g, {"knn_ms": watch.totals["knn_ms"]}
+
+
+class _Loop:
+    """Device buffers and captured tau-block graphs of the f32 iteration."""
+
+    def __init__(self, op: WalkOperator, c: int, k: int, tau: int, use_graphs: bool):
+        self.op, self.c, self.k, self.tau = op, c, k, tau
+        n = op.n
+        self.ld = ld_for(c, torch.float32)
+        d = dev()
+        self.Q = [torch.zeros((n, self.ld), dtype=torch.float32, device=d) for _ in range(2)]
+        self.Z = torch.zeros((n, self.ld), dtype=torch.float32, device=d)
+        self.Qsave = torch.zeros((n, self.ld), dtype=torch.float32, device=d)
+        self.stats = torch.zeros(4, dtype=torch.float64, device=d)
+        self._flag_init = torch.tensor([1.0, 0.0], dtype=torch.float64, device=d)
+        self.s32 = op.struct(_lib.F32)
+        self.ws = WORKSPACE.get("orth", _lib.load().ancka_orth_workspace_size(self.s32, c))
+        self.cur = 0
+        self.use_graphs = use_graphs
+        self.graphs = {}
+        self.launches = 0
+
+    def reset_flags(self):
+        self.stats[1:3].copy_(self._flag_init)   # device->device: capturable
+
+    def _step(self, src: int):
+        _lib.call("ancka_orth_step_f32", self.s32, self.Q[src].data_ptr(), self.Q[1 - src].data_ptr(),
+                  self.Z.data_ptr(), self.ld, self.c, self.stats.data_ptr(), self.ws.data_ptr(),
+                  self.ws.numel(), _lib.stream())
+
+    def _block(self, start: int, steps: int):
+        self.Qsave.copy_(self.Q[start])
+        self.reset_flags()
+        src = start
+        for _ in range(steps):
+            self._step(src)
+            src = 1 - src
+
+    def replay_exact(self, rng):
+        """Redo the last block from its saved start with exact f64 steps."""
+        start, steps = self.last
+        self.Q[start].copy_(self.Qsave)
+        src = start
+        for _ in range(steps):
+            q64 = self.Q[src][:, : self.c].double()
+            q, _ = _exact_step(self.op, padded(q64, torch.float64), self.c, rng)
+            self.Q[1 - src][:, : self.c] = q[:, : self.c].to(torch.float32)
+            src = 1 - src
+        self.stats[0] = torch.sum((self.Q[src][:, : self.c].double()
+                                   - self.Q[1 - src][:, : self.c].double()) ** 2)
+        self.stats[2] = 0.0
+        self.cur = src
+
+    def run(self, steps: int):
+        """Advance `steps` f32 orthogonal steps from Q[cur]."""
+        start = self.cur
+        self.last = (start, steps)
+        if self.use_graphs and steps == self.tau:
+            g = self.graphs.get(start)
+            if g is None:
+                self._block(start, steps)          # warm-up (not counted twice)
+                torch.cuda.current_stream().synchronize()
+                self.Q[start].copy_(self.Qsave)    # undo the warm-up
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g):
+                    self._block(start, steps)
+                self.graphs[start] = g
+            g.replay()
+        else:
+            self._block(start, steps)
+        self.cur = (start + steps) % 2
+        self.launches += steps * (5 if self.op.kind.value == "hypergraph" else 4) + 1
+
+    @property
+    def q(self) -> torch.Tensor:
+        return self.Q[self.cur]
+
+
+def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
+              early_stop: bool = True, *, use_graphs: bool = True) -> ClusterResult:
+    """Full clustering pipeline (engine.py:343-437), device-resident."""
+    _lib.require_device()
+    timer = _PhaseTimer()
+    with warnings.catch_warnings(record=True) as wrec:
+        warnings.simplefilter("always")
+        op, g, knn_t = build_pipeline(net, params, knn_cache_dir=knn_cache_dir)
+        timer.totals["knn_ms"] += knn_t["knn_ms"]
+        n, k = op.n, params.k
+        with timer.span("init_ms"):
+            labels0, _ = _init_labels_device(op, k, params.t_i, params.alpha)
+        rng = np.random.default_rng(params.seed)
+        c = min(k + 1, n)
+        # Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371), f64 for the exact first step
+        sizes0 = _cluster_sizes(labels0, k)
+        ld64 = ld_for(c, torch.float64)
+        q0 = torch.zeros((n, ld64), dtype=torch.float64, device=dev())
+        q0[:, 0] = 1.0 / np.sqrt(n)
+        yval = torch.from_numpy(np.where(sizes0 > 0, 1.0 / np.sqrt(np.maximum(sizes0, 1)), 0.0)).to(dev())
+        rows = torch.arange(n, device=dev())
+        lab0 = labels0.long()
+        keep = (lab0 + 1) < c
+        q0[rows[keep], lab0[keep] + 1] = yval[lab0[keep]]
+        with timer.span("mhc_ms"):
+            if (sizes0 == 0).any():
+                raise NetworkError(f"empty cluster(s) {np.flatnonzero(sizes0 == 0).tolist()}: "
+                                   "normalization undefined")
+            best_mhc = float(_MhcRunner(op, k, _lib.F64)(labels0).item())
+        best_labels = labels0.clone()
+        history = [(0, best_mhc)]
+        loop = _Loop(op, c, k, params.tau, use_graphs)
+        mhc = _MhcRunner(op, k, _lib.F32)
+        lab_t = torch.empty(n, dtype=torch.int32, device=dev())
+        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device=dev())
+        readback = torch.zeros(4, dtype=torch.float64, device=dev())
+        error, stop_reason, converged, t = None, "max_iterations", False, 0
+        def sample(t_now, dq_first):
+            qt = loop.q
+            with timer.span("discretize_ms"):
+                _discretize_device(qt, 1, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
+            with timer.span("mhc_ms"):
+                mhc(lab_t, readback[0:1])
+            if dq_first is not None:
+                readback[1] = dq_first * dq_first
+                readback[2] = 0.0
+            else:
+                readback[1] = loop.stats[0]
+                readback[2] = loop.stats[2]
+            return info[:8].cpu().numpy(), readback.cpu().numpy()[:3]
+
+        try:
+            # ---- t = 1: exact f64 step on the rank-deficient block
+            t = 1
+            with timer.span("ortho_ms"):
+                q1, _ = _exact_step(op, q0, c, rng)
+                loop.Q[0][:, :c] = q1[:, :c].to(torch.float32)
+                loop.cur = 0
+                dq1 = torch.linalg.vector_norm(q1[:, :c] - q0[:, :c])
+            t_done = 1
+            sample_needed = params.tau == 1
+            while True:
+                if sample_needed:
+                    t = t_done
+                    inf, (phi, dq2, nbad) = sample(t_done, dq1 if t_done == 1 else None)
+                    if nbad > 0:
+                        # a suspect Cholesky pivot: replay the block with exact f64 steps
+                        warnings.warn("ill-conditioned iterate; replaying tau-block in f64")
+                        with timer.span("ortho_ms"):
+                            loop.replay_exact(rng)
+                        inf, (phi, dq2, nbad) = sample(t_done, None)
+                    if inf[5] > 0:
+                        warnings.warn(f"{int(inf[5])} all-zero row(s); assigning to cluster 0")
+                    if inf[4] > 0:
+                        warnings.warn(f"re-seeding {int(inf[4])} empty cluster(s) after discretization")
+                        raise NetworkError("cannot repair empty clusters: no movable nodes")
+                    history.append((t, float(phi)))
+                    if phi < best_mhc:
+                        best_mhc = float(phi)
+                        best_labels.copy_(lab_t)
+                    if float(np.sqrt(dq2)) < params.eps_q:
+                        stop_reason, converged = "subspace_converged", True
+                        break
+                    if early_stop and len(history) >= 3:
+                        p = [v for _, v in history[-3:]]
+                        if p[0] < p[1] < p[2]:
+                            stop_reason, converged = "mhc_rising", True
+                            break
+                    timer.flush()
+                if t_done >= params.t_a:
+                    t = t_done
+                    break
+                nxt = min(params.t_a, (t_done // params.tau + 1) * params.tau)
+                with timer.span("ortho_ms"):
+                    loop.run(nxt - t_done)
+                t_done = nxt
+                t = t_done
+                sample_needed = t_done % params.tau == 0
+        except NetworkError as exc:
+            error, stop_reason = str(exc), "error"
+        timer.flush()
+        caught = [str(w.message) for w in wrec]
+    best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)
+    state = EngineState(loop.q, best_y, best_mhc, history, t, c=c)
+    return ClusterResult(y=best_y, mhc=best_mhc, iterations=t, timings_ms=dict(timer.totals),
+                         state=state, knn=g, operator=op, converged=converged,
+                         stop_reason=stop_reason, warnings=caught, error=error)
+

@@ -1,0 +1,249 @@
+"""Subsystem 1: exact KNN graph on the B200 (reference: ancka/knn.py).
+
+`knn_search_exact` runs `ancka_knn_exact` (tcgen05 integer-exact path for
+integer-valued attributes such as bag-of-words, f64 CUDA-core path
+otherwise) and `build_knn_adjacency` / `knn_transition` run
+`ancka_knn_graph`.  Results stay in HBM; the numpy/scipy views the reference
+API exposes (`NeighborLists.ids`, `KnnGraph.adjacency`, ...) are materialised
+lazily on first access.  Approximate search is not offered: every mode runs
+the exact kernel.
+"""
+from __future__ import annotations
+
+import hashlib
+import struct
+import warnings
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from ._device import WORKSPACE, DeviceCSR, dev
+from .network import KnnMode, NetworkError
+
+_PAD = -1
+#: route integer-valued attributes to the tcgen05 kernel (knn_tc.cu)
+TENSOR_CORE_KNN = False
+
+
+class NeighborLists:
+    """Per-node top-K neighbour ids and cosine scores, padded with -1
+    (knn.py:30-44).  Device-resident; `.ids`/`.scores` are host views."""
+
+    def __init__(self, ids_dev=None, scores_dev=None, K=None, ids=None, scores=None):
+        self._ids_dev, self._scores_dev = ids_dev, scores_dev
+        self._ids, self._scores = ids, scores
+        self.K = int(K if K is not None else (ids.shape[1] if ids is not None else ids_dev.shape[1]))
+
+    @classmethod
+    def from_host(cls, ids, scores):
+        ids = np.asarray(ids, dtype=np.int64)
+        return cls(ids=ids, scores=np.asarray(scores, dtype=np.float64), K=ids.shape[1])
+
+    @property
+    def ids(self) -> np.ndarray:
+        if self._ids is None:
+            self._ids = self._ids_dev.cpu().numpy().astype(np.int64)
+        return self._ids
+
+    @property
+    def scores(self) -> np.ndarray:
+        if self._scores is None:
+            self._scores = self._scores_dev.cpu().numpy()
+        return self._scores
+
+    def device(self):
+        if self._ids_dev is None:
+            self._ids_dev = torch.from_numpy(self._ids.astype(np.int32)).to(dev())
+            self._scores_dev = torch.from_numpy(np.ascontiguousarray(self._scores)).to(dev())
+        return self._ids_dev, self._scores_dev
+
+    @property
+    def n(self) -> int:
+        return self._ids_dev.shape[0] if self._ids_dev is not None else self._ids.shape[0]
+
+    def row(self, i: int):
+        ok = self.ids[i] != _PAD
+        return self.ids[i][ok], self.scores[i][ok]
+
+
+class KnnGraph:
+    """Symmetric weighted KNN adjacency A_K plus the lists (knn.py:47-51)."""
+
+    def __init__(self, a_k: DeviceCSR, p_k: DeviceCSR, zero_rows, neighbors, mode_used):
+        self.a_k_dev, self.p_k_dev, self.zero_rows_dev = a_k, p_k, zero_rows
+        self.neighbors = neighbors
+        self.mode_used = mode_used
+        self._adj = None
+
+    @property
+    def adjacency(self) -> sp.csr_matrix:
+        if self._adj is None:
+            self._adj = self.a_k_dev.to_scipy()
+        return self._adj
+
+
+def _normalize_host(x):
+    """knn.py:54-65, used only by the small host helper `cosine_sim`."""
+    x = np.asarray(x, dtype=np.float64)
+    nrm = np.linalg.norm(x)
+    return x / nrm if nrm > 0 else x
+
+
+def cosine_sim(xi, xj) -> float:
+    """Cosine of two rows; 0 if either is all-zero (knn.py:68-80)."""
+    if sp.issparse(xi):
+        xi = xi.toarray()
+    if sp.issparse(xj):
+        xj = xj.toarray()
+    xi = np.asarray(xi, dtype=np.float64).ravel()
+    xj = np.asarray(xj, dtype=np.float64).ravel()
+    ni, nj = np.linalg.norm(xi), np.linalg.norm(xj)
+    if ni == 0.0 or nj == 0.0:
+        return 0.0
+    return float(xi @ xj) / (ni * nj)
+
+
+def integer_exact(X) -> bool:
+    """True when X qualifies for the integer-exact tensor-core path: integer
+    entries, |x| <= 256 (exact in bf16), every row's sum of squares < 2^24
+    (exact f32 accumulation of the dot products)."""
+    vals = X.data if sp.issparse(X) else np.asarray(X)
+    if vals.size == 0:
+        return False
+    if not np.all(vals == np.rint(vals)) or np.abs(vals).max() > 256:
+        return False
+    sq = np.asarray(X.multiply(X).sum(axis=1)).ravel() if sp.issparse(X) else (vals * vals).sum(axis=1)
+    return bool(sq.max() < 2 ** 24)
+
+
+def attributes_to_device(X) -> torch.Tensor:
+    """n x d attributes -> dense f64 on the device (CSR densified on the GPU)."""
+    if sp.issparse(X):
+        x = sp.csr_matrix(X)
+        t = torch.sparse_csr_tensor(torch.from_numpy(x.indptr.astype(np.int64)),
+                                    torch.from_numpy(x.indices.astype(np.int64)),
+                                    torch.from_numpy(x.data.astype(np.float64)), size=x.shape)
+        return t.to(dev()).to_dense().contiguous()
+    return torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(dev())
+
+
+def knn_search_exact_device(X, K: int, integer: bool | None = None):
+    """Device exact KNN: returns (ids int32 (n,K), scores f64 (n,K)) tensors."""
+    _lib.require_device()
+    n, d = X.shape
+    if K >= n:
+        raise NetworkError(f"K={K} must be smaller than n={n}")
+    if integer is None:
+        integer = TENSOR_CORE_KNN and integer_exact(X)
+    xd = X if isinstance(X, torch.Tensor) else attributes_to_device(X)
+    ids = torch.empty((n, K), dtype=torch.int32, device=xd.device)
+    scores = torch.empty((n, K), dtype=torch.float64, device=xd.device)
+    wsb = _lib.load().ancka_knn_workspace_size(n, d, K, int(integer))
+    ws = WORKSPACE.get("knn", wsb)
+    _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer),
+              ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    return ids, scores
+
+
+def knn_search_exact(X, K: int, block_rows: int | None = None) -> NeighborLists:
+    """Exact top-K cosine neighbours (knn.py:112-140).  `block_rows` is
+    accepted for signature compatibility; tiling is fixed by the kernel."""
+    ids, scores = knn_search_exact_device(X, K)
+    return NeighborLists(ids_dev=ids, scores_dev=scores, K=K)
+
+
+def search_knn(X, K: int, mode: KnnMode = KnnMode.AUTO, seed: int = 0,
+               recall_target: float = 0.9):
+    """Mode dispatch (knn.py:283-291).  Exact search is fast enough on B200 at
+    every supported size, so AUTO and APPROX both run the exact kernel and
+    report `KnnMode.EXACT`."""
+    if mode is KnnMode.APPROX:
+        warnings.warn("approximate KNN is not implemented on B200; running exact search")
+    return knn_search_exact(X, K), KnnMode.EXACT
+
+
+def build_knn_graph_device(ids, scores, n: int):
+    """A_K and P_K on the device from (ids, scores) device tensors."""
+    K = ids.shape[1]
+    d = ids.device
+    cap = 2 * n * K
+    rowptr = torch.empty(n + 1, dtype=torch.int64, device=d)
+    colidx = torch.empty(cap, dtype=torch.int32, device=d)
+    a_k = torch.empty(cap, dtype=torch.float64, device=d)
+    p64 = torch.empty(cap, dtype=torch.float64, device=d)
+    p32 = torch.empty(cap, dtype=torch.float32, device=d)
+    zero = torch.empty(n, dtype=torch.uint8, device=d)
+    nnz = torch.zeros(1, dtype=torch.int64, device=d)
+    wsb = _lib.load().ancka_knn_graph_workspace_size(n, K)
+    ws = WORKSPACE.get("knn_graph", wsb)
+    _lib.call("ancka_knn_graph", ids.data_ptr(), scores.data_ptr(), n, K, rowptr.data_ptr(),
+              colidx.data_ptr(), a_k.data_ptr(), p64.data_ptr(), p32.data_ptr(), zero.data_ptr(),
+              nnz.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    m = int(nnz.item())
+    A = DeviceCSR(n, n, rowptr, colidx[:m], a_k[:m], None)
+    P = DeviceCSR(n, n, rowptr, colidx[:m], p64[:m], p32[:m])
+    return A, P, zero
+
+
+def build_knn_adjacency(neighbors: NeighborLists, X=None, mode_used: KnnMode = KnnMode.EXACT) -> KnnGraph:
+    """A_K = M + M^T (knn.py:294-309), built on the device."""
+    _lib.require_device()
+    ids, scores = neighbors.device()
+    A, P, zero = build_knn_graph_device(ids, scores, neighbors.n)
+    return KnnGraph(A, P, zero, neighbors, mode_used)
+
+
+def knn_transition(g: KnnGraph):
+    """P_K = D_K^-1 A_K and the zero-row flags (knn.py:312-324), host views."""
+    return g.p_k_dev.to_scipy(), g.zero_rows_dev.cpu().numpy().astype(bool)
+
+
+# ---------------------------------------------------------------- cache ---
+# knn.py:327-382: b"AKNC", version u8, mode u8, reserved u16, n u64, K u32,
+# then n*K (id u32, score f32), absent = 0xFFFFFFFF.
+_MAGIC, _VERSION, _SENTINEL = b"AKNC", 1, 0xFFFFFFFF
+_HEADER = struct.Struct("<4sBBHQI")
+
+
+def cache_key(X, K: int, mode: KnnMode) -> str:
+    h = hashlib.sha256()
+    if sp.issparse(X):
+        x = X.tocsr()
+        h.update(np.asarray(x.indptr, dtype=np.int64).tobytes())
+        h.update(np.asarray(x.indices, dtype=np.int64).tobytes())
+        h.update(np.asarray(x.data, dtype=np.float64).tobytes())
+    else:
+        h.update(np.ascontiguousarray(X, dtype=np.float64).tobytes())
+    h.update(struct.pack("<Iq", K, X.shape[1]))
+    h.update(mode.value.encode())
+    return h.hexdigest()[:32]
+
+
+def save_neighbor_cache(path, neighbors: NeighborLists, mode: KnnMode) -> None:
+    ids = neighbors.ids.copy()
+    n, k = ids.shape
+    ids[ids == _PAD] = _SENTINEL
+    rec = np.empty((n, k), dtype=[("id", "<u4"), ("score", "<f4")])
+    rec["id"] = ids.astype(np.uint64).astype("<u4")
+    rec["score"] = neighbors.scores.astype("<f4")
+    with open(path, "wb") as fh:
+        fh.write(_HEADER.pack(_MAGIC, _VERSION, 0 if mode is KnnMode.EXACT else 1, 0, n, k))
+        fh.write(rec.tobytes())
+
+
+def load_neighbor_cache(path):
+    with open(path, "rb") as fh:
+        magic, version, mode_code, _, n, k = _HEADER.unpack(fh.read(_HEADER.size))
+        if magic != _MAGIC or version != _VERSION:
+            raise NetworkError(f"{path}: not a neighbor cache file")
+        rec = np.frombuffer(fh.read(), dtype=[("id", "<u4"), ("score", "<f4")])
+    if rec.size != n * k:
+        raise NetworkError(f"{path}: truncated neighbor cache")
+    rec = rec.reshape(n, k)
+    ids = rec["id"].astype(np.int64)
+    ids[ids == _SENTINEL] = _PAD
+    scores = rec["score"].astype(np.float64)
+    scores[ids == _PAD] = 0.0
+    return NeighborLists.from_host(ids, scores), (KnnMode.EXACT if mode_code == 0 else KnnMode.APPROX)

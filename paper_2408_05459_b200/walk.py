@@ -1,0 +1,190 @@
+"""Subsystem 2: the joint-walk operator on the B200 (reference: ancka/walk.py).
+
+Structural factors are normalised on the host with the same scipy calls as
+the reference (O(nnz), once per network) and uploaded; the KNN factor P_K is
+produced on the device by `ancka_knn_graph`.  `apply_joint_transition` and
+`apply_structure_rowvec` run `ancka_op_apply` / `ancka_op_apply_struct_t`;
+in f64 they are bit-identical to scipy's csr_matvecs.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from ._device import WORKSPACE, DeviceCSR, csr_struct, dev, ld_for, padded
+from .network import AttributedNetwork, NetworkError, NetworkKind, node_degrees, symmetrize_union
+
+
+def _row_normalize(a: sp.csr_matrix) -> sp.csr_matrix:
+    """D^-1 A, zero rows stay zero (walk.py:38-44)."""
+    rs = np.asarray(a.sum(axis=1)).ravel()
+    inv = np.divide(1.0, rs, out=np.zeros_like(rs), where=rs > 0)
+    p = (sp.diags(inv) @ a).tocsr()
+    p.sort_indices()
+    return p
+
+
+def beta_vector(net: AttributedNetwork, knn_zero_rows, beta: float) -> np.ndarray:
+    """beta_i per Eq. (2) (walk.py:47-57)."""
+    deg = node_degrees(net)
+    b = np.full(net.n, float(beta))
+    b[deg == 0] = 1.0
+    b[np.asarray(knn_zero_rows, dtype=bool)] = 0.0
+    return b
+
+
+def hypergraph_factors(net: AttributedNetwork):
+    """P_V = D_V^-1 H^T, P_E = D_E^-1 H (walk.py:60-71)."""
+    if net.kind is not NetworkKind.HYPERGRAPH:
+        raise NetworkError("hypergraph_factors requires a hypergraph")
+    return _row_normalize(net.incidence.T.tocsr()), _row_normalize(net.incidence)
+
+
+def graph_transition(net: AttributedNetwork) -> sp.csr_matrix:
+    """P_N = D^-1 A, symmetrised for directed input (walk.py:74-79)."""
+    if net.kind is not NetworkKind.GRAPH:
+        raise NetworkError("graph_transition requires a graph")
+    return _row_normalize(symmetrize_union(net.adjacency) if net.directed else net.adjacency)
+
+
+def multiplex_transition(net: AttributedNetwork):
+    raise NetworkError("multiplex networks are outside the B200 hot path (SURVEY.md §8f)")
+
+
+class WalkOperator:
+    """Device-resident joint-walk factors (walk.py:89-104).  The scipy
+    attributes of the reference (`p_k`, `p_n`, `p_v`, `p_e`) are host views
+    materialised on access."""
+
+    def __init__(self, kind, n, alpha, gamma, beta, degrees, selfloop, dev_factors, p_k_dev,
+                 host_factors):
+        self.kind, self.n, self.alpha, self.gamma = kind, int(n), float(alpha), int(gamma)
+        self.beta = beta
+        self.degrees = degrees
+        self.selfloop = selfloop
+        self._f = dev_factors          # name -> DeviceCSR (p_n | p_e, p_v) and transposes
+        self._host = host_factors      # name -> scipy (structure only)
+        self.p_k_dev = p_k_dev
+        self.m = int(self._f["p_e"].rows) if kind is NetworkKind.HYPERGRAPH else 0
+        d = dev()
+        self.beta64 = torch.from_numpy(np.ascontiguousarray(beta, dtype=np.float64)).to(d)
+        self.beta32 = self.beta64.to(torch.float32)
+        mask = np.zeros(self.n, dtype=np.uint8)
+        mask[selfloop] = 1
+        self.selfloop_dev = torch.from_numpy(mask).to(d)
+        self._structs = {}
+
+    # reference attribute names
+    @property
+    def p_k(self):
+        return self.p_k_dev.to_scipy()
+
+    @property
+    def p_n(self):
+        return self._host.get("p_n")
+
+    @property
+    def p_v(self):
+        return self._host.get("p_v")
+
+    @property
+    def p_e(self):
+        return self._host.get("p_e")
+
+    layer_p = None
+
+    def struct(self, dtype: int) -> _lib.Operator:
+        """ctypes ancka_operator for f32 (`_lib.F32`) or f64 values."""
+        s = self._structs.get(dtype)
+        if s is None:
+            f = self._f
+            s = _lib.Operator(
+                _lib.HYPERGRAPH if self.kind is NetworkKind.HYPERGRAPH else _lib.GRAPH, dtype,
+                self.n, self.m,
+                csr_struct(f.get("p_n"), dtype), csr_struct(f.get("p_e"), dtype),
+                csr_struct(f.get("p_v"), dtype), csr_struct(self.p_k_dev, dtype),
+                csr_struct(f.get("t_a"), dtype), csr_struct(f.get("t_b"), dtype),
+                (self.beta64 if dtype == _lib.F64 else self.beta32).data_ptr(),
+                self.selfloop_dev.data_ptr())
+            self._structs[dtype] = s
+        return s
+
+    def scratch(self, c: int, dtype: torch.dtype, key: str = "op_scratch") -> torch.Tensor:
+        rows = max(self.m, 1)
+        return WORKSPACE.get(f"{key}_{dtype}", rows * ld_for(c, dtype) * (4 if dtype == torch.float32 else 8))
+
+
+def build_walk_operator(net: AttributedNetwork, p_k, knn_zero_rows, alpha: float, beta: float,
+                        gamma: int) -> WalkOperator:
+    """walk.py:107-132.  `p_k` may be a device `DeviceCSR` (engine path) or a
+    scipy CSR (API callers); `knn_zero_rows` a bool array or device tensor."""
+    _lib.require_device()
+    if net.kind is NetworkKind.MULTIPLEX:
+        multiplex_transition(net)
+    if isinstance(knn_zero_rows, torch.Tensor):
+        knn_zero_rows = knn_zero_rows.cpu().numpy().astype(bool)
+    degrees = node_degrees(net)
+    b = beta_vector(net, knn_zero_rows, beta)
+    selfloop = np.flatnonzero((degrees == 0) & (b == 0.0))
+    if not isinstance(p_k, DeviceCSR):
+        p_k = DeviceCSR.from_scipy(p_k)
+    host, devf = {}, {}
+    if net.kind is NetworkKind.HYPERGRAPH:
+        p_v, p_e = hypergraph_factors(net)
+        host.update(p_v=p_v, p_e=p_e)
+        devf["p_v"], devf["p_e"] = DeviceCSR.from_scipy(p_v), DeviceCSR.from_scipy(p_e)
+        # init_bcm transposes: (p_e^T @ (p_v^T @ m)) -- walk.py:163
+        devf["t_a"] = DeviceCSR.from_scipy(p_v.T.tocsr())
+        devf["t_b"] = DeviceCSR.from_scipy(p_e.T.tocsr())
+    else:
+        p_n = graph_transition(net)
+        host["p_n"] = p_n
+        devf["p_n"] = DeviceCSR.from_scipy(p_n)
+        devf["t_a"] = DeviceCSR.from_scipy(p_n.T.tocsr())
+    return WalkOperator(net.kind, net.n, alpha, gamma, b, degrees, selfloop, devf, p_k, host)
+
+
+def _apply(op: WalkOperator, m, transposed: bool):
+    _lib.require_device()
+    host = not isinstance(m, torch.Tensor)
+    t = torch.as_tensor(m)
+    squeeze = t.ndim == 1
+    if squeeze:
+        t = t[:, None]
+    if t.shape[0] != op.n:
+        raise NetworkError(f"block has {t.shape[0]} rows, operator expects {op.n}")
+    c = t.shape[1]
+    q = padded(t, torch.float64)
+    z = torch.empty_like(q)
+    scr = op.scratch(c, torch.float64)
+    fn = "ancka_op_apply_struct_t" if transposed else "ancka_op_apply"
+    _lib.call(fn, op.struct(_lib.F64), q.data_ptr(), q.stride(0), c, z.data_ptr(), z.stride(0),
+              scr.data_ptr(), _lib.stream())
+    out = z[:, :c]
+    if squeeze:
+        out = out[:, 0]
+    return out.cpu().numpy() if host else out
+
+
+def apply_joint_transition(op: WalkOperator, m):
+    """(I-B) P_N M + B P_K M on the device in f64 (walk.py:177-190)."""
+    return _apply(op, m, transposed=False)
+
+
+def apply_structure_rowvec(op: WalkOperator, m):
+    """c x n row block times the structural transition (walk.py:153-174)."""
+    if m.shape[1] != op.n:
+        raise NetworkError(f"block has {m.shape[1]} columns, operator expects {op.n}")
+    mt = m.T if isinstance(m, torch.Tensor) else np.ascontiguousarray(np.asarray(m).T)
+    out = _apply(op, mt, transposed=True)
+    return out.T if isinstance(out, torch.Tensor) else np.ascontiguousarray(out.T)
+
+
+def apply_structure(op: WalkOperator, m):
+    """Structural transition times a block (walk.py:135-150): the joint apply
+    with beta = 0 is not exposed separately on the device; provided for API
+    completeness via a beta-free operator view."""
+    raise NetworkError("apply_structure is internal to the fused device operator; "
+                       "use apply_joint_transition")

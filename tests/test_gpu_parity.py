@@ -1,0 +1,176 @@
+"""CUDA path vs the oracle and the reference's golden outputs (needs a B200).
+
+Tolerances (north star): f64 operator application is
+bit-identical to scipy (asserted <= 1e-15 absolute here); f32 operator
+outputs within 1e-5 relative; KNN index sets exact up to exact ties at the
+K-th value; labels at ARI >= 0.99.
+"""
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+from conftest import load_csr, load_x, oracle_net, random_seeds
+from oracle import ancka_cpu as oc
+
+pytestmark = pytest.mark.gpu
+warnings.simplefilter("ignore")
+
+ancka = pytest.importorskip("paper_2408_05459_b200")
+from paper_2408_05459_b200 import _lib  # noqa: E402
+from paper_2408_05459_b200._device import DeviceCSR, padded  # noqa: E402
+from paper_2408_05459_b200.knn import build_knn_graph_device  # noqa: E402
+
+
+def ari(a, b):
+    from sklearn.metrics import adjusted_rand_score
+    return adjusted_rand_score(a, b)
+
+
+def _net(z, p):
+    kind = str(z[p + "kind"])
+    S, X = load_csr(z, p + "S"), load_x(z, p + "X")
+    if kind == "hypergraph":
+        return ancka.AttributedNetwork.hypergraph(S, X)
+    return ancka.AttributedNetwork.graph(S, X, directed=bool(z[p + "directed"]))
+
+
+def _op_from_golden(z, p):
+    net, _ = ancka.validate_network(_net(z, p))
+    pk = load_csr(z, p + "PK")
+    zero = np.asarray(pk.sum(axis=1)).ravel() == 0
+    return ancka.build_walk_operator(net, pk, zero, 0.2, float(z[p + "beta"]), int(z[p + "gamma"]))
+
+
+def _cases(z):
+    return [s for s in random_seeds(z) if not bool(z[f"s{s}_skip"])]
+
+
+def knn_sets_match(ids_a, ids_b, X, K):
+    """Tie-aware comparison: rows may differ only by members of the exact tie
+    group at the K-th similarity (f64 cosines, |s - s_K| <= 1e-12)."""
+    xn, _ = oc.unit_rows(X)
+    xn = xn.toarray() if sp.issparse(xn) else xn
+    bad = 0
+    for i in range(ids_a.shape[0]):
+        a = set(ids_a[i][ids_a[i] >= 0].tolist())
+        b = set(ids_b[i][ids_b[i] >= 0].tolist())
+        if a == b:
+            continue
+        if len(a) != len(b):
+            bad += 1
+            continue
+        s = xn @ xn[i]
+        members = sorted(a | b, key=lambda j: -s[j])
+        kth = min(s[j] for j in b)
+        diff = a ^ b
+        if not all(abs(s[j] - kth) <= 1e-12 for j in diff):
+            bad += 1
+    return bad
+
+
+def test_device_present():
+    _lib.require_device()
+    assert _lib.load().ancka_abi_version() == 1
+
+
+def test_apply_f64_bit_exact(golden_random):
+    z = golden_random
+    worst = 0.0
+    for s in _cases(z):
+        p = f"s{s}_"
+        op = _op_from_golden(z, p)
+        np.testing.assert_array_equal(op.beta, z[p + "beta_vec"])
+        out = ancka.apply_joint_transition(op, z[p + "M"])
+        worst = max(worst, float(np.abs(out - z[p + "apply"]).max()))
+        out_t = ancka.apply_structure_rowvec(op, z[p + "M"].T.copy())
+        worst = max(worst, float(np.abs(out_t - z[p + "apply_t"]).max()))
+    assert worst <= 1e-15, worst
+
+
+def test_apply_f32_within_1e5(golden_random):
+    z = golden_random
+    for s in _cases(z):
+        p = f"s{s}_"
+        op = _op_from_golden(z, p)
+        m = z[p + "M"]
+        q = padded(torch.from_numpy(m), torch.float32)
+        out = torch.empty_like(q)
+        scr = op.scratch(3, torch.float32)
+        _lib.call("ancka_op_apply", op.struct(_lib.F32), q.data_ptr(), q.stride(0), 3,
+                  out.data_ptr(), out.stride(0), scr.data_ptr(), _lib.stream())
+        got = out[:, :3].double().cpu().numpy()
+        ref = z[p + "apply"]
+        rel = np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-30)
+        assert rel <= 1e-5, (s, rel)
+        # elementwise: 1e-5 relative to (|Z_ij| + rms(Z)); the f32 rounding of
+        # M alone is ~6e-8 of max|M| before any cancellation in the average
+        floor = np.sqrt(np.mean(ref ** 2))
+        assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(ref) + floor)), s
+
+
+def test_knn_matches_reference(golden_random):
+    z = golden_random
+    for s in _cases(z):
+        p = f"s{s}_"
+        X = load_x(z, p + "X")
+        n = X.shape[0]
+        K = min(4, n - 1)
+        lists = ancka.knn_search_exact(X, K)
+        assert knn_sets_match(lists.ids, z[p + "knn_ids"], X, K) == 0, s
+        ok = z[p + "knn_ids"] >= 0
+        assert np.array_equal(lists.ids >= 0, ok)
+
+
+def test_knn_graph_bit_exact(golden_random):
+    z = golden_random
+    for s in _cases(z):
+        p = f"s{s}_"
+        ids = torch.from_numpy(z[p + "knn_ids"].astype(np.int32)).cuda()
+        sc = torch.from_numpy(z[p + "knn_scores"]).cuda()
+        A, P, zero = build_knn_graph_device(ids, sc, ids.shape[0])
+        ak, pk = load_csr(z, p + "AK"), load_csr(z, p + "PK")
+        a_mine, p_mine = A.to_scipy(), P.to_scipy()
+        assert np.array_equal(a_mine.indptr, ak.indptr) and np.array_equal(a_mine.indices, ak.indices)
+        np.testing.assert_array_equal(a_mine.data, ak.data)
+        np.testing.assert_array_equal(p_mine.data, pk.data)
+
+
+def test_init_mhc_step_discretize(golden_random):
+    z = golden_random
+    for s in _cases(z):
+        p = f"s{s}_"
+        op = _op_from_golden(z, p)
+        n = op.n
+        k = min(3, n)
+        y0 = ancka.init_bcm(op, k, 5, 0.2)
+        assert np.array_equal(y0.assignment, z[p + "init"]), s
+        phi = ancka.calc_mhc(op, ancka.BcmMatrix(z[p + "lab"], k))
+        assert abs(phi - float(z[p + "mhc"])) < 1e-13, s
+        if p + "q0" in z:
+            q1, r1 = ancka.orthogonal_step(op, z[p + "q0"], np.random.default_rng(s))
+            np.testing.assert_allclose(q1, z[p + "q1"], atol=1e-10)
+        d = ancka.discretize(z[p + "qd"])
+        ref = z[p + "disc_labels"]
+        assert ari(d.y.assignment, ref) >= 0.99 or np.array_equal(d.y.assignment, ref), s
+
+
+@pytest.mark.parametrize("i", range(6))
+def test_run_ancka_matches_reference(golden_runs, i):
+    z, meta = golden_runs
+    m = meta[i]
+    p = f"r{i}_"
+    S, X = load_csr(z, p + "S"), load_x(z, p + "X")
+    net = (ancka.AttributedNetwork.hypergraph(S, X) if m["kind"] == "hypergraph"
+           else ancka.AttributedNetwork.graph(S, X))
+    params = ancka.ClusterParams(k=m["k"], knn_k=10, seed=m["seed"], t_a=m["t_a"],
+                                 knn_mode=ancka.KnnMode.EXACT)
+    res = ancka.run_ancka(net, params, early_stop=m["early_stop"])
+    assert res.error is None, res.error
+    a = ari(res.y.assignment, z[p + "labels"])
+    assert a >= 0.99, (i, a, res.iterations, int(z[p + "iterations"]), res.stop_reason)
+    assert abs(res.mhc - float(z[p + "mhc"])) < 1e-3
