@@ -56,7 +56,8 @@ extern "C" int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ld
   ANCKA_REQUIRE(K < n, ANCKA_ERR_NETWORK, "K=%d must be smaller than n=%lld", K, (long long)n);
   ANCKA_REQUIRE(K >= 1 && d >= 1, ANCKA_ERR_ARG, "knn: bad sizes");
   auto st = as_stream(stream);
-  if (integer_exact) return knn_tc(X, n, d, ldx, K, ids, scores, workspace, workspace_bytes, st);
+  if (integer_exact)
+    return knn_tc(X, n, d, ldx, K, ids, scores, workspace, workspace_bytes, st, integer_exact == 2);
   Carver cv(workspace, workspace_bytes);
   double *xn, *nr;
   int64_t ldn;

@@ -1,9 +1,436 @@
-// placeholder: replaced by the tcgen05 kernel
+// Exact KNN on the 5th-gen tensor cores for integer-valued attributes
+// (bag-of-words and other count data): knn.py:112-140 with the ordering of
+// _ordered_top_k (knn.py:83-98), computed exactly.
+//
+// X is quantised losslessly (|x| <= 16 -> e4m3 fp8, |x| <= 256 -> bf16) and
+// S = X X^T is contracted by tcgen05.mma into f32 TMEM accumulators, which
+// are exact integers (row sums of squares < 2^24).  Cosine order is decided
+// by exact integer arithmetic: s_j > s_l  <=>  c_j^2 a_l > c_l^2 a_j  with
+// c = dot count and a = squared norm, ties by smaller index -- the canonical
+// order the reference's f64 arithmetic approximates.  The n x n similarity
+// matrix never leaves TMEM/registers.
+//
+// CTA = 6 warps, one 128-row query tile x one key segment:
+//   warp 0     TMA producer (A: 128 x 128B, B: 256 x 128B per stage, SW128)
+//   warp 1     TMEM allocator + single-thread MMA issuer (M=128, N=256)
+//   warps 2-5  epilogue: thread t owns query row t (TMEM lane t), streams its
+//              256 accumulator columns per key tile (double-buffered TMEM)
+//              into a register-resident exact top-K list.
+// Segments of the key range run in parallel CTAs; a merge kernel combines
+// their partial lists (same exact order) and emits ids and f64 scores.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp8.h>
+
+#include "common.cuh"
 #include "knn.cuh"
+#include "sm100.cuh"
+
 namespace ancka {
-size_t knn_tc_workspace(int64_t, int64_t, int) { return 256; }
-int knn_tc(const double*, int64_t, int64_t, int64_t, int, int32_t*, double*, void*, size_t, cudaStream_t) {
-  set_error("tcgen05 KNN path not built");
-  return ANCKA_ERR_UNSUPPORTED;
+using namespace sm100;
+
+namespace tc {
+constexpr int BM = 128, BN = 256;
+constexpr int STAGES = 4;
+constexpr int ROW_BYTES = 128;                    // one SW128 row per stage
+constexpr int A_BYTES = BM * ROW_BYTES;           // 16 KB
+constexpr int B_BYTES = BN * ROW_BYTES;           // 32 KB
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 512;                    // 2 accumulators x 256 columns
+constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+}  // namespace tc
+
+struct Entry {
+  uint32_t c;  // exact dot count (0 = empty slot)
+  uint32_t a;  // squared norm of the neighbour
+  int32_t j;   // neighbour index
+};
+
+// exact: c1/sqrt(a1) > c2/sqrt(a2), ties -> smaller index; c2 == 0 is empty
+__device__ __forceinline__ bool better(uint32_t c1, uint32_t a1, int32_t j1, uint32_t c2,
+                                       uint32_t a2, int32_t j2) {
+  if (c2 == 0) return true;
+  const uint64_t l = (uint64_t)c1 * c1, r = (uint64_t)c2 * c2;
+  const uint64_t lh = __umul64hi(l, (uint64_t)a2), ll = l * (uint64_t)a2;
+  const uint64_t rh = __umul64hi(r, (uint64_t)a1), rl = r * (uint64_t)a1;
+  if (lh != rh) return lh > rh;
+  if (ll != rl) return ll > rl;
+  return j1 < j2;
 }
+
+template <int KMAX>
+struct TopK {
+  uint32_t c[KMAX], a[KMAX];
+  int32_t j[KMAX];
+  float thr;  // conservative f32 key of the K-th entry (-1 while not full)
+
+  __device__ __forceinline__ void clear() {
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) { c[t] = 0; a[t] = 1; j[t] = -1; }
+    thr = -1.f;
+  }
+  // insert a candidate known to pass the fast filter
+  __device__ __forceinline__ void insert(uint32_t cc, uint32_t aa, int32_t jj, int K,
+                                         const float* inv_sqrt) {
+    // is it better than the K-th entry?
+    bool beats = false;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t)
+      if (t == K - 1) beats = better(cc, aa, jj, c[t], a[t], j[t]);
+    if (!beats) return;
+    bool done = false;
+#pragma unroll
+    for (int t = KMAX - 1; t > 0; --t) {
+      if (t < K && !done) {
+        if (better(cc, aa, jj, c[t - 1], a[t - 1], j[t - 1])) {
+          c[t] = c[t - 1]; a[t] = a[t - 1]; j[t] = j[t - 1];
+        } else {
+          c[t] = cc; a[t] = aa; j[t] = jj;
+          done = true;
+        }
+      }
+    }
+    if (!done) { c[0] = cc; a[0] = aa; j[0] = jj; }
+    uint32_t ck = 0;
+    int32_t jk = -1;
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t)
+      if (t == K - 1) { ck = c[t]; jk = j[t]; }
+    thr = ck ? (float)ck * inv_sqrt[jk] * (1.0f - 4e-6f) : -1.f;
+  }
+};
+
+struct TcParams {
+  int64_t n;
+  int nkb;            // k-blocks of 128 bytes along d
+  int K;
+  int key_tiles;      // total key tiles of BN
+  int tiles_per_seg;
+  int nseg;
+  const uint32_t* a_norm;   // n_pad
+  const float* inv_sqrt;    // n_pad
+  int2* partial;            // n x nseg x K  (c, j)
+};
+
+template <bool FP8, int KMAX>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              TcParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;
+  unsigned char* sB = base + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q0 = (int64_t)blockIdx.x * BM;
+  const int seg = blockIdx.y;
+  const int kt0 = seg * p.tiles_per_seg;
+  const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
+  const int ntiles = kt1 - kt0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int krow = (kt0 + t) * BN;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), (int)q0);
+          tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), krow);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
+    constexpr uint32_t idesc = make_idesc(FP8 ? 0u : 1u, BM, BN);
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + acc * BN;
+        for (int kb = 0; kb < p.nkb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128-byte row
+            const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
+            const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
+            if (FP8) mma_f8_ss(dtm, ad, bd, idesc, (kb | k) != 0);
+            else mma_f16_ss(dtm, ad, bd, idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------ epilogue
+    const int quarter = warp & 3;                 // TMEM lane quarter of this warp
+    const int row = quarter * 32 + lane;
+    const int64_t i = q0 + row;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    TopK<KMAX> L;
+    L.clear();
+    for (int t = 0; t < ntiles; ++t) {
+      const int acc = t & 1;
+      const uint32_t acc_phase = (t >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int64_t j0 = (int64_t)(kt0 + t) * BN;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / 32; ++ch) {
+        uint32_t r[32];
+        tmem_ld32(tmem + lane_off + acc * BN + ch * 32, r);
+        tmem_ld_wait();
+        if (ch == BN / 32 - 1) {           // all of this accumulator is in registers
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const float v = __uint_as_float(r[u]);
+          if (v > 0.5f) {
+            const int64_t j = j0 + ch * 32 + u;
+            if (j != i && j < p.n) {
+              const float kf = v * __ldg(p.inv_sqrt + j);
+              if (kf >= L.thr)
+                L.insert((uint32_t)(v + 0.5f), __ldg(p.a_norm + j), (int32_t)j, p.K, p.inv_sqrt);
+            }
+          }
+        }
+      }
+    }
+    if (i < p.n) {
+      int2* out = p.partial + ((size_t)i * p.nseg + seg) * p.K;
+#pragma unroll
+      for (int t = 0; t < KMAX; ++t)
+        if (t < p.K) out[t] = make_int2((int)L.c[t], L.c[t] ? L.j[t] : -1);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
+
+// Merge the per-segment lists (exact order) and emit ids / f64 cosines.
+template <int KMAX>
+__global__ void knn_tc_merge_kernel(const int2* __restrict__ partial, int64_t n, int nseg, int K,
+                                    const uint32_t* __restrict__ a_norm,
+                                    const float* __restrict__ inv_sqrt, int32_t* __restrict__ ids,
+                                    double* __restrict__ scores) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    TopK<KMAX> L;
+    L.clear();
+    for (int s = 0; s < nseg; ++s) {
+      const int2* src = partial + ((size_t)i * nseg + s) * K;
+      for (int t = 0; t < K; ++t) {
+        const int2 e = src[t];
+        if (e.x <= 0) break;
+        L.insert((uint32_t)e.x, a_norm[e.y], e.y, K, inv_sqrt);
+      }
+    }
+    const double ai = (double)a_norm[i];
+#pragma unroll
+    for (int t = 0; t < KMAX; ++t) {
+      if (t < K) {
+        const bool ok = L.c[t] != 0;
+        ids[i * K + t] = ok ? L.j[t] : -1;
+        scores[i * K + t] = ok ? fmin((double)L.c[t] / sqrt(ai * (double)L.a[t]), 1.0) : 0.0;
+      }
+    }
+  }
+}
+
+// f64 dense X -> padded fp8/bf16 rows + exact squared norms.
+template <bool FP8>
+__global__ void knn_tc_prep_kernel(const double* __restrict__ X, int64_t n, int64_t d, int64_t ldx,
+                                   int64_t n_pad, int64_t d_pad, void* __restrict__ xq,
+                                   uint32_t* __restrict__ a_norm, float* __restrict__ inv_sqrt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_pad; r += nwarps) {
+    double s = 0.0;
+    for (int64_t c = lane; c < d_pad; c += 32) {
+      const double v = (r < n && c < d) ? X[r * ldx + c] : 0.0;
+      s += v * v;
+      if (FP8) reinterpret_cast<__nv_fp8_e4m3*>(xq)[r * d_pad + c] = __nv_fp8_e4m3((float)v);
+      else reinterpret_cast<__nv_bfloat16*>(xq)[r * d_pad + c] = __float2bfloat16_rn((float)v);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      a_norm[r] = (uint32_t)s;
+      inv_sqrt[r] = s > 0 ? (float)(1.0 / sqrt(s)) : 0.f;
+    }
+  }
+}
+
+// --------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* m, void* ptr, bool fp8, int64_t rows, int64_t row_elems,
+                    int box_rows) {
+  EncodeTiledFn enc = encode_fn();
+  ANCKA_REQUIRE(enc != nullptr, ANCKA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int esz = fp8 ? 1 : 2;
+  cuuint64_t gdim[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
+  cuuint64_t gstride[1] = {(cuuint64_t)(row_elems * esz)};
+  cuuint32_t box[2] = {(cuuint32_t)(tc::ROW_BYTES / esz), (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   ptr, gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  ANCKA_REQUIRE(r == CUDA_SUCCESS, ANCKA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return ANCKA_OK;
+}
+
+struct TcLayout {
+  bool fp8;
+  int64_t n_pad, d_pad;
+  int nseg, tiles_per_seg, key_tiles, q_tiles;
+};
+
+static TcLayout tc_layout(int64_t n, int64_t d, bool fp8) {
+  TcLayout L;
+  L.fp8 = fp8;
+  L.n_pad = ceil_div(n, tc::BN) * tc::BN;
+  const int64_t elems_per_row = tc::ROW_BYTES / (fp8 ? 1 : 2);
+  L.d_pad = ceil_div(d, elems_per_row) * elems_per_row;
+  L.q_tiles = (int)ceil_div(n, tc::BM);
+  L.key_tiles = (int)ceil_div(n, tc::BN);
+  int nseg = (int)ceil_div(8 * kNumSMs, L.q_tiles);
+  nseg = std::max(1, std::min(nseg, L.key_tiles));
+  L.tiles_per_seg = (int)ceil_div(L.key_tiles, nseg);
+  L.nseg = (int)ceil_div(L.key_tiles, L.tiles_per_seg);
+  return L;
+}
+
+static void carve_tc(Carver& cv, const TcLayout& L, int64_t n, int K, void** xq, uint32_t** an,
+                     float** isq, int2** part) {
+  *xq = cv.take<unsigned char>((size_t)L.n_pad * L.d_pad * (L.fp8 ? 1 : 2));
+  *an = cv.take<uint32_t>(L.n_pad);
+  *isq = cv.take<float>(L.n_pad);
+  *part = cv.take<int2>((size_t)n * L.nseg * K);
+}
+
+// the fp8 path is taken when the host asserts |x| <= 16 via integer_exact == 2
+size_t knn_tc_workspace(int64_t n, int64_t d, int K) {
+  Carver cv(nullptr, 0);
+  TcLayout L = tc_layout(n, d, false);  // bf16 bound covers fp8
+  void* xq;
+  uint32_t* an;
+  float* isq;
+  int2* part;
+  carve_tc(cv, L, n, K, &xq, &an, &isq, &part);
+  return cv.used;
+}
+
+template <bool FP8, int KMAX>
+static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParams& p,
+                     const TcLayout& L, cudaStream_t st) {
+  auto kern = knn_tc_kernel<FP8, KMAX>;
+  ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
+  dim3 grid(L.q_tiles, L.nseg);
+  kern<<<grid, tc::THREADS, tc::SMEM, st>>>(ma, mb, p);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* ids, double* scores,
+           void* ws, size_t wsb, cudaStream_t st, bool fp8) {
+  ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
+  ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
+  TcLayout L = tc_layout(n, d, fp8);
+  Carver cv(ws, wsb);
+  void* xq;
+  uint32_t* an;
+  float* isq;
+  int2* part;
+  carve_tc(cv, L, n, K, &xq, &an, &isq, &part);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_tc: workspace too small");
+  const int pg = (int)std::min<int64_t>(ceil_div(L.n_pad * 32, 256), 16 * kNumSMs);
+  if (fp8)
+    knn_tc_prep_kernel<true><<<pg, 256, 0, st>>>(X, n, d, ldx, L.n_pad, L.d_pad, xq, an, isq);
+  else
+    knn_tc_prep_kernel<false><<<pg, 256, 0, st>>>(X, n, d, ldx, L.n_pad, L.d_pad, xq, an, isq);
+  ANCKA_LAUNCHED();
+  CUtensorMap ma, mb;
+  ANCKA_TRY(make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
+  ANCKA_TRY(make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
+  TcParams p;
+  p.n = n;
+  p.nkb = (int)(L.d_pad * (fp8 ? 1 : 2) / tc::ROW_BYTES);
+  p.K = K;
+  p.key_tiles = L.key_tiles;
+  p.tiles_per_seg = L.tiles_per_seg;
+  p.nseg = L.nseg;
+  p.a_norm = an;
+  p.inv_sqrt = isq;
+  p.partial = part;
+  if (fp8) {
+    if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }
+    else { ANCKA_TRY((launch_tc<true, 32>(ma, mb, p, L, st))); }
+  } else {
+    if (K <= 16) { ANCKA_TRY((launch_tc<false, 16>(ma, mb, p, L, st))); }
+    else { ANCKA_TRY((launch_tc<false, 32>(ma, mb, p, L, st))); }
+  }
+  const int mg = (int)std::min<int64_t>(ceil_div(n, 128), 8 * kNumSMs);
+  if (K <= 16)
+    knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, n, L.nseg, K, an, isq, ids, scores);
+  else
+    knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, n, L.nseg, K, an, isq, ids, scores);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+}  // namespace ancka

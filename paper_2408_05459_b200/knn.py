@@ -24,7 +24,7 @@ from .network import KnnMode, NetworkError
 
 _PAD = -1
 #: route integer-valued attributes to the tcgen05 kernel (knn_tc.cu)
-TENSOR_CORE_KNN = False
+TENSOR_CORE_KNN = True
 
 
 class NeighborLists:
@@ -105,17 +105,21 @@ def cosine_sim(xi, xj) -> float:
     return float(xi @ xj) / (ni * nj)
 
 
-def integer_exact(X) -> bool:
-    """True when X qualifies for the integer-exact tensor-core path: integer
-    entries, |x| <= 256 (exact in bf16), every row's sum of squares < 2^24
-    (exact f32 accumulation of the dot products)."""
+def integer_exact(X) -> int:
+    """Tensor-core eligibility of X: 2 = integers with |x| <= 16 (exact in
+    e4m3 fp8), 1 = integers with |x| <= 256 (exact in bf16), 0 = otherwise.
+    Every row's sum of squares must stay < 2^24 so the f32 accumulation of
+    the dot products is exact."""
     vals = X.data if sp.issparse(X) else np.asarray(X)
-    if vals.size == 0:
-        return False
-    if not np.all(vals == np.rint(vals)) or np.abs(vals).max() > 256:
-        return False
+    if vals.size == 0 or not np.all(vals == np.rint(vals)):
+        return 0
+    vmax = float(np.abs(vals).max())
+    if vmax > 256:
+        return 0
     sq = np.asarray(X.multiply(X).sum(axis=1)).ravel() if sp.issparse(X) else (vals * vals).sum(axis=1)
-    return bool(sq.max() < 2 ** 24)
+    if sq.max() >= 2 ** 24:
+        return 0
+    return 2 if vmax <= 16 else 1
 
 
 def attributes_to_device(X) -> torch.Tensor:
@@ -129,14 +133,14 @@ def attributes_to_device(X) -> torch.Tensor:
     return torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(dev())
 
 
-def knn_search_exact_device(X, K: int, integer: bool | None = None):
+def knn_search_exact_device(X, K: int, integer: int | None = None):
     """Device exact KNN: returns (ids int32 (n,K), scores f64 (n,K)) tensors."""
     _lib.require_device()
     n, d = X.shape
     if K >= n:
         raise NetworkError(f"K={K} must be smaller than n={n}")
     if integer is None:
-        integer = TENSOR_CORE_KNN and integer_exact(X)
+        integer = integer_exact(X) if (TENSOR_CORE_KNN and K <= 32) else 0
     xd = X if isinstance(X, torch.Tensor) else attributes_to_device(X)
     ids = torch.empty((n, K), dtype=torch.int32, device=xd.device)
     scores = torch.empty((n, K), dtype=torch.float64, device=xd.device)

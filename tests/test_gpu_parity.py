@@ -174,3 +174,60 @@ def test_run_ancka_matches_reference(golden_runs, i):
     a = ari(res.y.assignment, z[p + "labels"])
     assert a >= 0.99, (i, a, res.iterations, int(z[p + "iterations"]), res.stop_reason)
     assert abs(res.mhc - float(z[p + "mhc"])) < 1e-3
+
+
+def canonical_knn(X, K):
+    """Exact rational top-K for integer X: order (c/sqrt(a) desc, j asc),
+    strictly positive only.  Ties are resolved with exact integer arithmetic."""
+    Xd = X.toarray() if sp.issparse(X) else np.asarray(X)
+    Xi = np.rint(Xd).astype(np.int64)
+    a = (Xi * Xi).sum(axis=1)
+    C = Xi @ Xi.T
+    n = Xi.shape[0]
+    ids = np.full((n, K), -1, dtype=np.int64)
+    from functools import cmp_to_key
+    for i in range(n):
+        c = C[i].copy()
+        c[i] = 0
+        cand = np.flatnonzero(c > 0)
+        if a[i] == 0 or cand.size == 0:
+            continue
+        key = c[cand] / np.sqrt(a[cand])
+        order = cand[np.lexsort((cand, -key))][: 4 * K + 8]
+
+        def cmp(x, y):
+            lx, ly = int(c[x]) ** 2 * int(a[y]), int(c[y]) ** 2 * int(a[x])
+            if lx != ly:
+                return -1 if lx > ly else 1
+            return -1 if x < y else 1
+        best = sorted(order.tolist(), key=cmp_to_key(cmp))[:K]
+        ids[i, : len(best)] = best
+    return ids
+
+
+@pytest.mark.parametrize("shape,n,words", [("cora", 1500, 18), ("dblp", 2100, 20), ("citeseer", 700, 32)])
+def test_tensor_core_knn_exact(shape, n, words):
+    from paper_2408_05459_b200 import synth
+    from paper_2408_05459_b200.knn import integer_exact, knn_search_exact_device
+    inst = synth.make(shape, seed=3, n=n, words=words)
+    X = inst.X
+    assert integer_exact(X) == 2
+    K = 10
+    ids_fp8, sc_fp8 = knn_search_exact_device(X, K, integer=2)
+    ids_bf16, sc_bf16 = knn_search_exact_device(X, K, integer=1)
+    ref = canonical_knn(X, K)
+    got8 = ids_fp8.cpu().numpy().astype(np.int64)
+    got16 = ids_bf16.cpu().numpy().astype(np.int64)
+    assert np.array_equal(got8, ref), int((got8 != ref).any(axis=1).sum())
+    assert np.array_equal(got16, ref)
+    # scores: cosines of the selected pairs (f64, vs numpy f64 formula)
+    Xd = X.toarray()
+    nrm = np.linalg.norm(Xd, axis=1)
+    ok = ref >= 0
+    rows = np.repeat(np.arange(n)[:, None], K, axis=1)
+    cos = np.zeros_like(sc_fp8.cpu().numpy())
+    cos[ok] = (Xd[rows[ok]] * Xd[ref[ok]]).sum(1) / (nrm[rows[ok]] * nrm[ref[ok]])
+    np.testing.assert_allclose(sc_fp8.cpu().numpy(), np.minimum(cos, 1.0), atol=1e-14)
+    # the f64 CUDA-core path agrees up to exact ties at the K-th value
+    ids_f64, _ = knn_search_exact_device(X, K, integer=0)
+    assert knn_sets_match(ids_f64.cpu().numpy(), ref, X, K) == 0

@@ -93,6 +93,7 @@ def test_cache_roundtrip(tmp_path):
 def test_integer_exact_detection():
     import scipy.sparse as sp
     from paper_2408_05459_b200.knn import integer_exact
-    assert integer_exact(sp.csr_matrix(np.eye(4)))
-    assert not integer_exact(np.array([[0.5, 1.0]]))
-    assert not integer_exact(np.array([[300.0, 1.0]]))
+    assert integer_exact(sp.csr_matrix(np.eye(4))) == 2
+    assert integer_exact(np.array([[100.0, 1.0]])) == 1
+    assert integer_exact(np.array([[0.5, 1.0]])) == 0
+    assert integer_exact(np.array([[300.0, 1.0]])) == 0
