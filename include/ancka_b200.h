@@ -64,6 +64,9 @@ typedef struct {
 
 const char* ancka_last_error(void);
 int ancka_abi_version(void);
+/* Number of kernels this library has enqueued (stream capture counts once;
+ * CUDA-graph replays are not seen here). */
+int64_t ancka_launch_count(void);
 /* Fails unless a compute-capability 10.x device is current. */
 int ancka_device_check(void);
 

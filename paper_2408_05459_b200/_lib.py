@@ -36,6 +36,7 @@ _SIGS = {
     "ancka_last_error": (ctypes.c_char_p, []),
     "ancka_abi_version": (c_int32, []),
     "ancka_device_check": (c_int32, []),
+    "ancka_launch_count": (c_int64, []),
     "ancka_knn_workspace_size": (c_size_t, [c_int64, c_int64, c_int32, c_int32]),
     "ancka_knn_exact": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32,
                                   c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),

@@ -1,5 +1,6 @@
 // C-ABI entry points that are not owned by a subsystem file, plus the KNN
 // dispatcher (tensor-core integer-exact path vs f64 CUDA-core path).
+#include <atomic>
 #include <cstdarg>
 
 #include "common.cuh"
@@ -8,6 +9,9 @@
 namespace ancka {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -22,6 +26,7 @@ using namespace ancka;
 
 extern "C" const char* ancka_last_error(void) { return g_err; }
 extern "C" int ancka_abi_version(void) { return ANCKA_ABI_VERSION; }
+extern "C" int64_t ancka_launch_count(void) { return g_launches.load(); }
 
 extern "C" int ancka_device_check(void) {
   int dev = 0;

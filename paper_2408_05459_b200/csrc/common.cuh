@@ -13,8 +13,9 @@
 namespace ancka {
 
 void set_error(const char* fmt, ...);
+void note_launch();  // counts kernel launches issued by this library
 
-#define ANCKA_CUDA(expr)                                                              \
+#define ANCKA_CUDA(expr)                                                         \
   do {                                                                                \
     cudaError_t _e = (expr);                                                          \
     if (_e != cudaSuccess) {                                                          \
@@ -25,6 +26,7 @@ void set_error(const char* fmt, ...);
 
 #define ANCKA_LAUNCHED()                                                              \
   do {                                                                                \
+    ::ancka::note_launch();                                                           \
     cudaError_t _e = cudaGetLastError();                                              \
     if (_e != cudaSuccess) {                                                          \
       ::ancka::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \

@@ -517,6 +517,7 @@ static int launch_disc(DiscParams& p, cudaStream_t st) {
   int64_t grid = std::min(want, std::min((int64_t)per_sm * sms, (int64_t)disc_grid_cap()));
   if (grid < 1) grid = 1;
   void* args[] = {&p};
+  note_launch();
   ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(kDiscThreads),
                                          args, smem, st));
   return ANCKA_OK;

@@ -153,6 +153,7 @@ extern "C" int ancka_knn_graph(const int32_t* ids, const double* scores, int64_t
                                             w.agg, w.nruns, SumOp(), E, st));
   const int gr = (int)std::min<int64_t>(ceil_div(n + 1, 256), 16 * kNumSMs);
   knn_rowptr_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.nruns, n, rowptr, nnz_out);
+  ANCKA_LAUNCHED();
   knn_finish_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.agg, rowptr, n, colidx, a_k,
                                                      p_k64, p_k32, zero_rows);
   ANCKA_LAUNCHED();

@@ -21,6 +21,7 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "knn.cuh"
@@ -35,9 +36,11 @@ constexpr int STAGES = 4;
 constexpr int ROW_BYTES = 128;                    // one SW128 row per stage
 constexpr int A_BYTES = BM * ROW_BYTES;           // 16 KB
 constexpr int B_BYTES = BN * ROW_BYTES;           // 32 KB
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;                      // two per TMEM lane quarter
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
+constexpr int EPI_COLS = BN / (EPI_WARPS / 4);    // accumulator columns per epilogue warp
 constexpr int TMEM_COLS = 512;                    // 2 accumulators x 256 columns
-constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256 + 32 * EPI_WARPS * 33 * 4;
 }  // namespace tc
 
 struct Entry {
@@ -58,45 +61,79 @@ __device__ __forceinline__ bool better(uint32_t c1, uint32_t a1, int32_t j1, uin
   return j1 < j2;
 }
 
+// f32 keys c * rsqrt(a) carry < 3e-7 relative error, so two keys whose f32
+// values differ by more than kBand relative are ordered by the f32 compare;
+// only keys inside the band need the exact integer comparison.
+constexpr float kBand = 4e-6f;
+
+// Register-resident exact top-K.  The list always has KMAX slots; the first
+// KMAX-K are padding with key +inf (never displaced) and the K live entries
+// occupy slots KMAX-K..KMAX-1, best first.  The K-th entry is therefore
+// always slot KMAX-1 and no slot is ever addressed by a runtime index, which
+// keeps the arrays in registers.
 template <int KMAX>
 struct TopK {
   uint32_t c[KMAX], a[KMAX];
   int32_t j[KMAX];
-  float thr;  // conservative f32 key of the K-th entry (-1 while not full)
+  float f[KMAX];           // f32 keys: +inf padding, 0 empty
+  float thr_lo, thr_hi;    // band around the K-th key (-1 while not full)
 
-  __device__ __forceinline__ void clear() {
+  __device__ __forceinline__ void clear(int K) {
 #pragma unroll
-    for (int t = 0; t < KMAX; ++t) { c[t] = 0; a[t] = 1; j[t] = -1; }
-    thr = -1.f;
+    for (int t = 0; t < KMAX; ++t) {
+      const bool pad = t < KMAX - K;
+      c[t] = 0; a[t] = 1; j[t] = -1;
+      f[t] = pad ? __int_as_float(0x7f800000) : 0.f;
+    }
+    thr_lo = thr_hi = -1.f;
   }
-  // insert a candidate known to pass the fast filter
-  __device__ __forceinline__ void insert(uint32_t cc, uint32_t aa, int32_t jj, int K,
-                                         const float* inv_sqrt) {
-    // is it better than the K-th entry?
-    bool beats = false;
+
+  // does the candidate rank before entry t?
+  __device__ __forceinline__ static bool above(float ff, uint32_t cc, uint32_t aa, int32_t jj,
+                                               float f2, uint32_t c2, uint32_t a2, int32_t j2) {
+    if (f2 == 0.f) return true;                       // empty slot
+    if (ff > f2 * (1.f + kBand)) return true;
+    if (ff < f2 * (1.f - kBand)) return false;        // includes +inf padding
+    return better(cc, aa, jj, c2, a2, j2);
+  }
+
+  // Does the candidate enter the list?  a_norm is read only inside the band.
+  __device__ __forceinline__ bool admits(float ff, uint32_t cc, int32_t jj,
+                                         const uint32_t* __restrict__ a_norm) const {
+    if (ff < thr_lo) return false;
+    const float fk = f[KMAX - 1];
+    if (fk == 0.f || ff > thr_hi) return true;
+    const uint32_t aa = __ldg(a_norm + jj);
+    if (cc == c[KMAX - 1] && aa == a[KMAX - 1]) return jj < j[KMAX - 1];  // exact (c, a) tie
+    return better(cc, aa, jj, c[KMAX - 1], a[KMAX - 1], j[KMAX - 1]);
+  }
+
+  // rank against every slot with independent compares, then shift with
+  // fixed-index selects
+  __device__ __forceinline__ void insert(float ff, uint32_t cc, uint32_t aa, int32_t jj) {
+    int pos = 0;
 #pragma unroll
-    for (int t = 0; t < KMAX; ++t)
-      if (t == K - 1) beats = better(cc, aa, jj, c[t], a[t], j[t]);
-    if (!beats) return;
-    bool done = false;
+    for (int t = 0; t < KMAX; ++t) pos += above(ff, cc, aa, jj, f[t], c[t], a[t], j[t]) ? 0 : 1;
 #pragma unroll
     for (int t = KMAX - 1; t > 0; --t) {
-      if (t < K && !done) {
-        if (better(cc, aa, jj, c[t - 1], a[t - 1], j[t - 1])) {
-          c[t] = c[t - 1]; a[t] = a[t - 1]; j[t] = j[t - 1];
-        } else {
-          c[t] = cc; a[t] = aa; j[t] = jj;
-          done = true;
-        }
-      }
+      const bool sh = t > pos, put = t == pos;
+      c[t] = sh ? c[t - 1] : (put ? cc : c[t]);
+      a[t] = sh ? a[t - 1] : (put ? aa : a[t]);
+      j[t] = sh ? j[t - 1] : (put ? jj : j[t]);
+      f[t] = sh ? f[t - 1] : (put ? ff : f[t]);
     }
-    if (!done) { c[0] = cc; a[0] = aa; j[0] = jj; }
-    uint32_t ck = 0;
-    int32_t jk = -1;
+    if (pos == 0) { c[0] = cc; a[0] = aa; j[0] = jj; f[0] = ff; }
+    const float fk = f[KMAX - 1];
+    thr_lo = fk == 0.f ? -1.f : fk * (1.f - kBand);
+    thr_hi = fk == 0.f ? -1.f : fk * (1.f + kBand);
+  }
+
+  // entry r (0 = best) of the K live entries, written without runtime indexing
+  template <typename F>
+  __device__ __forceinline__ void emit(int K, F&& out) const {
 #pragma unroll
     for (int t = 0; t < KMAX; ++t)
-      if (t == K - 1) { ck = c[t]; jk = j[t]; }
-    thr = ck ? (float)ck * inv_sqrt[jk] * (1.0f - 4e-6f) : -1.f;
+      if (t >= KMAX - K) out(t - (KMAX - K), c[t], a[t], j[t]);
   }
 };
 
@@ -110,6 +147,7 @@ struct TcParams {
   const uint32_t* a_norm;   // n_pad
   const float* inv_sqrt;    // n_pad
   int2* partial;            // n x nseg x K  (c, j)
+  int debug;                // 0 normal; 1 skip epilogue math; 2 skip MMA issue
 };
 
 template <bool FP8, int KMAX>
@@ -139,7 +177,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], 4); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
     fence_barrier_init();
   }
   if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
@@ -185,6 +223,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128-byte row
             const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
             const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
+            if (p.debug == 2) continue;
             if (FP8) mma_f8_ss(dtm, ad, bd, idesc, (kb | k) != 0);
             else mma_f16_ss(dtm, ad, bd, idesc, (kb | k) != 0);
           }
@@ -196,47 +235,64 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     }
   } else {
     // ------------------------------------------------------ epilogue
+    const int ew = warp - 2;                      // epilogue warp 0..EPI_WARPS-1
     const int quarter = warp & 3;                 // TMEM lane quarter of this warp
+    const int half = ew / 4;                      // which column range of the tile
     const int row = quarter * 32 + lane;
     const int64_t i = q0 + row;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     TopK<KMAX> L;
-    L.clear();
+    L.clear(p.K);
+    float* stash = reinterpret_cast<float*>(tmem_slot + 4) + (threadIdx.x - 64) * 33;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int64_t j0 = (int64_t)(kt0 + t) * BN;
+      const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
 #pragma unroll 1
-      for (int ch = 0; ch < BN / 32; ++ch) {
+      for (int ch = 0; ch < EPI_COLS / 32; ++ch) {
         uint32_t r[32];
-        tmem_ld32(tmem + lane_off + acc * BN + ch * 32, r);
+        tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + ch * 32, r);
         tmem_ld_wait();
-        if (ch == BN / 32 - 1) {           // all of this accumulator is in registers
+        if (ch == EPI_COLS / 32 - 1) {     // this warp's share is in registers
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        if (p.debug == 1) continue;
+        // fast filter (branch-free, unrolled): candidate bitmask against the
+        // current K-th key; the rare survivors take one out-of-line slow path
+        const int64_t jb = j0 + ch * 32;
+        uint32_t mask = 0;
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
           const float v = __uint_as_float(r[u]);
-          if (v > 0.5f) {
-            const int64_t j = j0 + ch * 32 + u;
-            if (j != i && j < p.n) {
-              const float kf = v * __ldg(p.inv_sqrt + j);
-              if (kf >= L.thr)
-                L.insert((uint32_t)(v + 0.5f), __ldg(p.a_norm + j), (int32_t)j, p.K, p.inv_sqrt);
-            }
-          }
+          const float kf = v * __ldg(p.inv_sqrt + jb + u);
+          const bool keep = (v > 0.5f) & (kf >= L.thr_lo);
+          mask |= (uint32_t)keep << u;
+          stash[u] = v;
+        }
+        if (i >= jb && i < jb + 32) mask &= ~(1u << (int)(i - jb));   // j != i
+        if (jb + 32 > p.n) mask &= p.n > jb ? (1u << (int)(p.n - jb)) - 1u : 0u;
+#pragma unroll 1
+        while (mask) {
+          const int u = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const float v = stash[u];
+          const int32_t j = (int32_t)(jb + u);
+          const float kf = v * __ldg(p.inv_sqrt + j);
+          const uint32_t cc = (uint32_t)(v + 0.5f);
+          if (L.admits(kf, cc, j, p.a_norm)) L.insert(kf, cc, __ldg(p.a_norm + j), j);
         }
       }
     }
     if (i < p.n) {
-      int2* out = p.partial + ((size_t)i * p.nseg + seg) * p.K;
-#pragma unroll
-      for (int t = 0; t < KMAX; ++t)
-        if (t < p.K) out[t] = make_int2((int)L.c[t], L.c[t] ? L.j[t] : -1);
+      const int lists = p.nseg * (EPI_WARPS / 4);
+      int2* out = p.partial + ((size_t)i * lists + seg * (EPI_WARPS / 4) + half) * p.K;
+      L.emit(p.K, [&](int r, uint32_t c, uint32_t, int32_t j) {
+        out[r] = make_int2((int)c, c ? j : -1);
+      });
     }
   }
   tc_fence_before();
@@ -253,24 +309,23 @@ __global__ void knn_tc_merge_kernel(const int2* __restrict__ partial, int64_t n,
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     TopK<KMAX> L;
-    L.clear();
+    L.clear(K);
     for (int s = 0; s < nseg; ++s) {
       const int2* src = partial + ((size_t)i * nseg + s) * K;
       for (int t = 0; t < K; ++t) {
         const int2 e = src[t];
         if (e.x <= 0) break;
-        L.insert((uint32_t)e.x, a_norm[e.y], e.y, K, inv_sqrt);
+        const float kf = (float)e.x * inv_sqrt[e.y];
+        if (L.admits(kf, (uint32_t)e.x, e.y, a_norm))
+          L.insert(kf, (uint32_t)e.x, a_norm[e.y], e.y);
       }
     }
     const double ai = (double)a_norm[i];
-#pragma unroll
-    for (int t = 0; t < KMAX; ++t) {
-      if (t < K) {
-        const bool ok = L.c[t] != 0;
-        ids[i * K + t] = ok ? L.j[t] : -1;
-        scores[i * K + t] = ok ? fmin((double)L.c[t] / sqrt(ai * (double)L.a[t]), 1.0) : 0.0;
-      }
-    }
+    L.emit(K, [&](int r, uint32_t c, uint32_t a, int32_t j) {
+      const bool ok = c != 0;
+      ids[i * K + r] = ok ? j : -1;
+      scores[i * K + r] = ok ? fmin((double)c / sqrt(ai * (double)a), 1.0) : 0.0;
+    });
   }
 }
 
@@ -360,7 +415,7 @@ static void carve_tc(Carver& cv, const TcLayout& L, int64_t n, int K, void** xq,
   *xq = cv.take<unsigned char>((size_t)L.n_pad * L.d_pad * (L.fp8 ? 1 : 2));
   *an = cv.take<uint32_t>(L.n_pad);
   *isq = cv.take<float>(L.n_pad);
-  *part = cv.take<int2>((size_t)n * L.nseg * K);
+  *part = cv.take<int2>((size_t)n * L.nseg * (tc::EPI_WARPS / 4) * K);
 }
 
 // the fp8 path is taken when the host asserts |x| <= 16 via integer_exact == 2
@@ -417,6 +472,7 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   p.a_norm = an;
   p.inv_sqrt = isq;
   p.partial = part;
+  p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
   if (fp8) {
     if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }
     else { ANCKA_TRY((launch_tc<true, 32>(ma, mb, p, L, st))); }
@@ -426,9 +482,9 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   }
   const int mg = (int)std::min<int64_t>(ceil_div(n, 128), 8 * kNumSMs);
   if (K <= 16)
-    knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, n, L.nseg, K, an, isq, ids, scores);
+    knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, n, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
   else
-    knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, n, L.nseg, K, an, isq, ids, scores);
+    knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, n, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

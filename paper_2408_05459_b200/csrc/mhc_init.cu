@@ -120,6 +120,7 @@ static int mhc_t(const ancka_operator* op, const int32_t* labels, int k, double 
   const int64_t n = op->n;
   ANCKA_TRY(cluster_sizes(labels, n, k, sizes, st));
   mhc_tagval_kernel<T><<<1, 256, 0, st>>>(sizes, k, alpha, w.tagval, w.yhat);
+  ANCKA_LAUNCHED();
   const int fg = (int)std::min<int64_t>(ceil_div(n * ld, 256), 16 * kNumSMs);
   fill_tag_kernel<T><<<std::max(fg, 1), 256, 0, st>>>(labels, n, ld, k, w.tagval, w.F0);
   ANCKA_LAUNCHED();
@@ -131,6 +132,7 @@ static int mhc_t(const ancka_operator* op, const int32_t* labels, int k, double 
     std::swap(cur, nxt);
   }
   mhc_trace_kernel<T><<<kTraceBlocks, 256, 0, st>>>(cur, n, ld, labels, w.yhat, w.partial);
+  ANCKA_LAUNCHED();
   mhc_finish_kernel<<<1, 256, 0, st>>>(w.partial, kTraceBlocks, sizes, k, phi);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
@@ -232,7 +234,9 @@ extern "C" int ancka_init_bcm(const ancka_operator* op64, const int64_t* centers
   const int64_t ld = (k + 1) / 2 * 2;
   const int g = (int)std::min<int64_t>(ceil_div(n, 256), 8 * kNumSMs);
   center_of_kernel<<<std::max(g, 1), 256, 0, st>>>(centers, k, n, w.center_of, w.tagval, alpha);
+  ANCKA_LAUNCHED();
   center_set_kernel<<<1, 256, 0, st>>>(centers, k, w.center_of);
+  ANCKA_LAUNCHED();
   const int fg = (int)std::min<int64_t>(ceil_div(n * ld, 256), 16 * kNumSMs);
   fill_tag_kernel<double><<<std::max(fg, 1), 256, 0, st>>>(w.center_of, n, ld, k, w.tagval, w.P0);
   ANCKA_LAUNCHED();

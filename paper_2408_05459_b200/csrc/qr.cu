@@ -367,12 +367,16 @@ extern "C" int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double*
       cgs_dots_kernel<<<dim3(kQrBlocks, j), 256, 0, st>>>(Z, n, ld, j, partial, 0);
       cgs_reduce_kernel<<<1, 256, 0, st>>>(partial, kQrBlocks, j, proj);
       cgs_update_kernel<<<ug, ub, 0, st>>>(Z, n, ld, j, proj, 0, rdiag);
+      note_launch();
+      note_launch();
+      ANCKA_LAUNCHED();
     }
     // norm: dots of column j with itself, stored at proj[j]
     cgs_dots_kernel<<<dim3(kQrBlocks, 1), 256, 0, st>>>(Z, n, ld, j, partial, 1);
     ANCKA_LAUNCHED();
     cgs_reduce_kernel<<<1, 256, 0, st>>>(partial, kQrBlocks, 1, proj + j);
     cgs_update_kernel<<<ug, ub, 0, st>>>(Z, n, ld, j, proj, 1, rdiag);
+    note_launch();
     ANCKA_LAUNCHED();
   }
   return ANCKA_OK;

@@ -26,11 +26,12 @@ import torch
 
 from . import _lib
 from ._device import WORKSPACE, dev, ld_for, padded
-from .knn import (KnnGraph, NeighborLists, build_knn_graph_device, cache_key,
-                  knn_search_exact_device, load_neighbor_cache, save_neighbor_cache)
+from .knn import (KnnGraph, NeighborLists, attributes_to_device, build_knn_graph_device,
+                  cache_key, integer_exact, knn_search_exact_device, load_neighbor_cache,
+                  save_neighbor_cache)
 from .network import (AttributedNetwork, BcmMatrix, ClusterParams, KnnMode, NetworkError,
                       default_knn_k, validate_network)
-from .walk import WalkOperator, build_walk_operator
+from .walk import StructureFactors, WalkOperator, build_walk_operator
 
 DISCRETIZE_MAX_ITER = 100
 DISCRETIZE_TOL = 1e-10
@@ -302,40 +303,73 @@ def calc_mhc(op: WalkOperator, y: BcmMatrix) -> float:
 
 
 # ------------------------------------------------------------ pipeline ------
-def build_pipeline(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None):
-    """Validate (host), exact KNN + KNN graph + walk operator (device)
-    (engine.py:302-340)."""
+@dataclass
+class PreparedNetwork:
+    """A validated network whose attributes and structural factors are
+    resident in HBM: the input of the device pipeline (build_pipeline_device)."""
+
+    net: AttributedNetwork
+    K: int
+    x_dev: torch.Tensor
+    x_level: int            # 2 fp8-exact, 1 bf16-exact, 0 general (knn.integer_exact)
+    factors: StructureFactors
+    cache_path: object = None
+
+    def h2d_bytes(self, x) -> int:
+        import scipy.sparse as sp
+        xb = (x.indptr.nbytes + x.indices.nbytes + x.data.nbytes) if sp.issparse(x) else x.nbytes
+        return int(xb + self.factors.h2d_bytes())
+
+
+def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None) -> PreparedNetwork:
+    """Host validation (network.py:266-313) and the one-time uploads."""
     from pathlib import Path
 
     _lib.require_device()
-    watch = _PhaseTimer()
     net, _ = validate_network(net)
     params.validate_for(net.n)
-    t0 = time.perf_counter()
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, net.n)
     if K >= net.n:
         warnings.warn(f"clamping KNN K={K} to n-1={net.n - 1}")
         K = net.n - 1
-    neighbors, mode_used, cache_path = None, None, None
+    cache_path = None
     if knn_cache_dir is not None:
         cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
-        if cache_path.exists():
-            neighbors, mode_used = load_neighbor_cache(cache_path)
+    level = integer_exact(net.attributes) if K <= 32 else 0
+    return PreparedNetwork(net, K, attributes_to_device(net.attributes), level,
+                           StructureFactors(net), cache_path)
+
+
+def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):
+    """Exact KNN, KNN graph and walk operator on the device (engine.py:314-339)."""
+    K, n = prep.K, prep.net.n
+    neighbors, mode_used = None, None
+    if prep.cache_path is not None and prep.cache_path.exists():
+        neighbors, mode_used = load_neighbor_cache(prep.cache_path)
     if neighbors is None:
         if params.knn_mode is KnnMode.APPROX:
             warnings.warn("approximate KNN is not implemented on B200; running exact search")
-        ids, scores = knn_search_exact_device(net.attributes, K)
+        ids, scores = knn_search_exact_device(prep.x_dev, K, integer=prep.x_level)
         neighbors, mode_used = NeighborLists(ids_dev=ids, scores_dev=scores, K=K), KnnMode.EXACT
-        if cache_path is not None:
-            cache_path.parent.mkdir(parents=True, exist_ok=True)
-            save_neighbor_cache(cache_path, neighbors, mode_used)
+        if prep.cache_path is not None:
+            prep.cache_path.parent.mkdir(parents=True, exist_ok=True)
+            save_neighbor_cache(prep.cache_path, neighbors, mode_used)
     ids, scores = neighbors.device()
-    A, P, zero = build_knn_graph_device(ids, scores, net.n)
+    A, P, zero = build_knn_graph_device(ids, scores, n)
     g = KnnGraph(A, P, zero, neighbors, mode_used)
-    op = build_walk_operator(net, P, zero, params.alpha, params.beta, params.gamma)
+    op = build_walk_operator(prep.net, P, zero, params.alpha, params.beta, params.gamma,
+                             factors=prep.factors)
+    return op, g
+
+
+def build_pipeline(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None):
+    """Validate (host), exact KNN + KNN graph + walk operator (device)
+    (engine.py:302-340).  Returns (operator, KnnGraph, timings)."""
+    t0 = time.perf_counter()
+    prep = prepare_network(net, params, knn_cache_dir)
+    op, g = build_pipeline_device(prep, params)
     torch.cuda.current_stream().synchronize()
-    watch.add_host("knn_ms", t0)
-    return op, g, {"knn_ms": watch.totals["knn_ms"]}
+    return op, g, {"knn_ms": (time.perf_counter() - t0) * 1e3}
 
 
 class _Loop:
@@ -356,7 +390,8 @@ class _Loop:
         self.cur = 0
         self.use_graphs = use_graphs
         self.graphs = {}
-        self.launches = 0
+        self.captured = 0   # kernel launches recorded into graphs (not executed)
+        self.replayed = 0   # kernel launches executed by graph replays
 
     def reset_flags(self):
         self.stats[1:3].copy_(self._flag_init)   # device->device: capturable
@@ -396,18 +431,22 @@ class _Loop:
         if self.use_graphs and steps == self.tau:
             g = self.graphs.get(start)
             if g is None:
-                self._block(start, steps)          # warm-up (not counted twice)
+                self._block(start, steps)          # warm-up
                 torch.cuda.current_stream().synchronize()
                 self.Q[start].copy_(self.Qsave)    # undo the warm-up
                 g = torch.cuda.CUDAGraph()
+                c0 = _lib.load().ancka_launch_count()
                 with torch.cuda.graph(g):
                     self._block(start, steps)
-                self.graphs[start] = g
+                nodes = _lib.load().ancka_launch_count() - c0
+                self.graphs[start] = (g, nodes)
+                self.captured += nodes             # captured, not executed
+            g, nodes = self.graphs[start]
             g.replay()
+            self.replayed += nodes
         else:
             self._block(start, steps)
         self.cur = (start + steps) % 2
-        self.launches += steps * (5 if self.op.kind.value == "hypergraph" else 4) + 1
 
     @property
     def q(self) -> torch.Tensor:
@@ -416,13 +455,31 @@ class _Loop:
 
 def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
               early_stop: bool = True, *, use_graphs: bool = True) -> ClusterResult:
-    """Full clustering pipeline (engine.py:343-437), device-resident."""
+    """Full clustering pipeline (engine.py:343-437): host validation and
+    uploads, then the device-resident pipeline (`run_prepared`)."""
     _lib.require_device()
-    timer = _PhaseTimer()
     with warnings.catch_warnings(record=True) as wrec:
         warnings.simplefilter("always")
-        op, g, knn_t = build_pipeline(net, params, knn_cache_dir=knn_cache_dir)
-        timer.totals["knn_ms"] += knn_t["knn_ms"]
+        t0 = time.perf_counter()
+        prep = prepare_network(net, params, knn_cache_dir)
+        prep_ms = (time.perf_counter() - t0) * 1e3
+    res = run_prepared(prep, params, early_stop, use_graphs=use_graphs)
+    res.timings_ms["knn_ms"] += prep_ms
+    res.warnings = [str(w.message) for w in wrec] + res.warnings
+    return res
+
+
+def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool = True, *,
+                 use_graphs: bool = True) -> ClusterResult:
+    """The device pipeline on HBM-resident inputs: KNN -> KNN graph ->
+    operator -> init -> orthogonal iterations / discretisation / MHC."""
+    _lib.require_device()
+    timer = _PhaseTimer()
+    launches0 = _lib.load().ancka_launch_count()
+    with warnings.catch_warnings(record=True) as wrec:
+        warnings.simplefilter("always")
+        with timer.span("knn_ms"):
+            op, g = build_pipeline_device(prep, params)
         n, k = op.n, params.k
         with timer.span("init_ms"):
             labels0, _ = _init_labels_device(op, k, params.t_i, params.alpha)
@@ -518,7 +575,12 @@ def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
         caught = [str(w.message) for w in wrec]
     best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)
     state = EngineState(loop.q, best_y, best_mhc, history, t, c=c)
-    return ClusterResult(y=best_y, mhc=best_mhc, iterations=t, timings_ms=dict(timer.totals),
-                         state=state, knn=g, operator=op, converged=converged,
-                         stop_reason=stop_reason, warnings=caught, error=error)
+    res = ClusterResult(y=best_y, mhc=best_mhc, iterations=t, timings_ms=dict(timer.totals),
+                        state=state, knn=g, operator=op, converged=converged,
+                        stop_reason=stop_reason, warnings=caught, error=error)
+    # kernels of this library executed by the run (graph captures excluded,
+    # graph replays included)
+    res.gpu_launches = int(_lib.load().ancka_launch_count() - launches0 - loop.captured
+                           + loop.replayed)
+    return res
 

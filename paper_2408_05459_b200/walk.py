@@ -53,45 +53,80 @@ def multiplex_transition(net: AttributedNetwork):
     raise NetworkError("multiplex networks are outside the B200 hot path (SURVEY.md §8f)")
 
 
+class StructureFactors:
+    """Host-normalised structural factors uploaded once (walk.py:60-79), plus
+    the init transposes (walk.py:163-165) and the pattern degrees."""
+
+    def __init__(self, net: AttributedNetwork):
+        if net.kind is NetworkKind.MULTIPLEX:
+            multiplex_transition(net)
+        self.kind, self.n = net.kind, net.n
+        self.degrees = node_degrees(net)
+        self.host, self.dev = {}, {}
+        if net.kind is NetworkKind.HYPERGRAPH:
+            p_v, p_e = hypergraph_factors(net)
+            self.host.update(p_v=p_v, p_e=p_e)
+            self.dev["p_v"], self.dev["p_e"] = DeviceCSR.from_scipy(p_v), DeviceCSR.from_scipy(p_e)
+            # init_bcm transposes: (p_e^T @ (p_v^T @ m)), walk.py:163
+            self.dev["t_a"] = DeviceCSR.from_scipy(p_v.T.tocsr())
+            self.dev["t_b"] = DeviceCSR.from_scipy(p_e.T.tocsr())
+            self.m = p_e.shape[0]
+        else:
+            p_n = graph_transition(net)
+            self.host["p_n"] = p_n
+            self.dev["p_n"] = DeviceCSR.from_scipy(p_n)
+            self.dev["t_a"] = DeviceCSR.from_scipy(p_n.T.tocsr())
+            self.m = 0
+        self.degrees_dev = torch.from_numpy(self.degrees).to(dev())
+
+    def h2d_bytes(self) -> int:
+        return int(sum(m.rowptr.numel() * 8 + m.colidx.numel() * 4 + m.val64.numel() * 8
+                       for m in self.dev.values()) + self.degrees.nbytes)
+
+
 class WalkOperator:
     """Device-resident joint-walk factors (walk.py:89-104).  The scipy
-    attributes of the reference (`p_k`, `p_n`, `p_v`, `p_e`) are host views
-    materialised on access."""
+    attributes of the reference (`p_k`, `p_n`, `p_v`, `p_e`, `beta`,
+    `selfloop`) are host views materialised on access."""
 
-    def __init__(self, kind, n, alpha, gamma, beta, degrees, selfloop, dev_factors, p_k_dev,
-                 host_factors):
-        self.kind, self.n, self.alpha, self.gamma = kind, int(n), float(alpha), int(gamma)
-        self.beta = beta
-        self.degrees = degrees
-        self.selfloop = selfloop
-        self._f = dev_factors          # name -> DeviceCSR (p_n | p_e, p_v) and transposes
-        self._host = host_factors      # name -> scipy (structure only)
+    def __init__(self, factors: StructureFactors, p_k_dev: DeviceCSR, beta_dev, alpha, gamma):
+        self.kind, self.n, self.m = factors.kind, factors.n, factors.m
+        self.alpha, self.gamma = float(alpha), int(gamma)
+        self.degrees = factors.degrees
+        self._fac = factors
+        self._f = factors.dev
         self.p_k_dev = p_k_dev
-        self.m = int(self._f["p_e"].rows) if kind is NetworkKind.HYPERGRAPH else 0
-        d = dev()
-        self.beta64 = torch.from_numpy(np.ascontiguousarray(beta, dtype=np.float64)).to(d)
-        self.beta32 = self.beta64.to(torch.float32)
-        mask = np.zeros(self.n, dtype=np.uint8)
-        mask[selfloop] = 1
-        self.selfloop_dev = torch.from_numpy(mask).to(d)
+        self.beta64 = beta_dev
+        self.beta32 = beta_dev.to(torch.float32)
+        self.selfloop_dev = ((factors.degrees_dev == 0) & (beta_dev == 0)).to(torch.uint8)
         self._structs = {}
+        self._beta_host = None
 
-    # reference attribute names
+    @property
+    def beta(self) -> np.ndarray:
+        if self._beta_host is None:
+            self._beta_host = self.beta64.cpu().numpy()
+        return self._beta_host
+
+    @property
+    def selfloop(self) -> np.ndarray:
+        return np.flatnonzero(self.selfloop_dev.cpu().numpy())
+
     @property
     def p_k(self):
         return self.p_k_dev.to_scipy()
 
     @property
     def p_n(self):
-        return self._host.get("p_n")
+        return self._fac.host.get("p_n")
 
     @property
     def p_v(self):
-        return self._host.get("p_v")
+        return self._fac.host.get("p_v")
 
     @property
     def p_e(self):
-        return self._host.get("p_e")
+        return self._fac.host.get("p_e")
 
     layer_p = None
 
@@ -116,34 +151,26 @@ class WalkOperator:
         return WORKSPACE.get(f"{key}_{dtype}", rows * ld_for(c, dtype) * (4 if dtype == torch.float32 else 8))
 
 
+def beta_device(factors: StructureFactors, knn_zero_rows, beta: float) -> torch.Tensor:
+    """beta_vector (walk.py:47-57) on the device."""
+    z = knn_zero_rows if isinstance(knn_zero_rows, torch.Tensor) else \
+        torch.from_numpy(np.asarray(knn_zero_rows, dtype=bool)).to(dev())
+    b = torch.full((factors.n,), float(beta), dtype=torch.float64, device=dev())
+    b = torch.where(factors.degrees_dev == 0, torch.ones_like(b), b)
+    return torch.where(z.bool(), torch.zeros_like(b), b)
+
+
 def build_walk_operator(net: AttributedNetwork, p_k, knn_zero_rows, alpha: float, beta: float,
-                        gamma: int) -> WalkOperator:
+                        gamma: int, factors: StructureFactors | None = None) -> WalkOperator:
     """walk.py:107-132.  `p_k` may be a device `DeviceCSR` (engine path) or a
-    scipy CSR (API callers); `knn_zero_rows` a bool array or device tensor."""
+    scipy CSR (API callers); `knn_zero_rows` a bool array or device tensor;
+    `factors` reuses already-uploaded structural factors."""
     _lib.require_device()
-    if net.kind is NetworkKind.MULTIPLEX:
-        multiplex_transition(net)
-    if isinstance(knn_zero_rows, torch.Tensor):
-        knn_zero_rows = knn_zero_rows.cpu().numpy().astype(bool)
-    degrees = node_degrees(net)
-    b = beta_vector(net, knn_zero_rows, beta)
-    selfloop = np.flatnonzero((degrees == 0) & (b == 0.0))
+    if factors is None:
+        factors = StructureFactors(net)
     if not isinstance(p_k, DeviceCSR):
         p_k = DeviceCSR.from_scipy(p_k)
-    host, devf = {}, {}
-    if net.kind is NetworkKind.HYPERGRAPH:
-        p_v, p_e = hypergraph_factors(net)
-        host.update(p_v=p_v, p_e=p_e)
-        devf["p_v"], devf["p_e"] = DeviceCSR.from_scipy(p_v), DeviceCSR.from_scipy(p_e)
-        # init_bcm transposes: (p_e^T @ (p_v^T @ m)) -- walk.py:163
-        devf["t_a"] = DeviceCSR.from_scipy(p_v.T.tocsr())
-        devf["t_b"] = DeviceCSR.from_scipy(p_e.T.tocsr())
-    else:
-        p_n = graph_transition(net)
-        host["p_n"] = p_n
-        devf["p_n"] = DeviceCSR.from_scipy(p_n)
-        devf["t_a"] = DeviceCSR.from_scipy(p_n.T.tocsr())
-    return WalkOperator(net.kind, net.n, alpha, gamma, b, degrees, selfloop, devf, p_k, host)
+    return WalkOperator(factors, p_k, beta_device(factors, knn_zero_rows, beta), alpha, gamma)
 
 
 def _apply(op: WalkOperator, m, transposed: bool):
