@@ -77,6 +77,7 @@ struct TopK {
   int32_t j[KMAX];
   float f[KMAX];           // f32 keys: +inf padding, 0 empty
   float thr_lo, thr_hi;    // band around the K-th key (-1 while not full)
+  float floor_lo;          // shared lower bound of the row's true K-th key (banded)
 
   __device__ __forceinline__ void clear(int K) {
 #pragma unroll
@@ -86,6 +87,15 @@ struct TopK {
       f[t] = pad ? __int_as_float(0x7f800000) : 0.f;
     }
     thr_lo = thr_hi = -1.f;
+    floor_lo = -1.f;
+  }
+
+  // raise the pruning floor to a bound learned elsewhere (another list of
+  // the same row): any key below it cannot be among the row's top K
+  __device__ __forceinline__ void raise_floor(float bound) {
+    const float lo = bound * (1.f - kBand);
+    floor_lo = fmaxf(floor_lo, lo);
+    thr_lo = fmaxf(thr_lo, floor_lo);
   }
 
   // does the candidate rank before entry t?
@@ -124,7 +134,7 @@ struct TopK {
     }
     if (pos == 0) { c[0] = cc; a[0] = aa; j[0] = jj; f[0] = ff; }
     const float fk = f[KMAX - 1];
-    thr_lo = fk == 0.f ? -1.f : fk * (1.f - kBand);
+    thr_lo = fmaxf(fk == 0.f ? -1.f : fk * (1.f - kBand), floor_lo);
     thr_hi = fk == 0.f ? -1.f : fk * (1.f + kBand);
   }
 
@@ -148,6 +158,7 @@ struct TcParams {
   const float* inv_sqrt;    // n_pad
   int2* partial;            // n x nseg x K  (c, j)
   int debug;                // 0 normal; 1 skip epilogue math; 2 skip MMA issue
+  int* row_bound;           // n: best known K-th key per row (f32 bits, atomicMax)
 };
 
 template <bool FP8, int KMAX>
@@ -194,7 +205,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int t = 0; t < ntiles; ++t) {
         const int krow = (kt0 + t) * BN;
         for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_sleep(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
           tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), (int)q0);
           tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), krow);
@@ -211,11 +222,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       for (int t = 0; t < ntiles; ++t) {
         const int acc = t & 1;
         const uint32_t acc_phase = (t >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t dtm = tmem + acc * BN;
         for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_sleep(&full[stage], phase);
           tc_fence_after();
           const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
           const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
@@ -243,11 +254,13 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     TopK<KMAX> L;
     L.clear(p.K);
+    float published = 0.f;
     float* stash = reinterpret_cast<float*>(tmem_slot + 4) + (threadIdx.x - 64) * 33;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&tfull[acc], acc_phase);
+      if (i < p.n) L.raise_floor(__int_as_float(__ldcg(p.row_bound + i)));
       tc_fence_after();
       const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
 #pragma unroll 1
@@ -283,7 +296,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
           const int32_t j = (int32_t)(jb + u);
           const float kf = v * __ldg(p.inv_sqrt + j);
           const uint32_t cc = (uint32_t)(v + 0.5f);
-          if (L.admits(kf, cc, j, p.a_norm)) L.insert(kf, cc, __ldg(p.a_norm + j), j);
+          if (L.admits(kf, cc, j, p.a_norm)) {
+            L.insert(kf, cc, __ldg(p.a_norm + j), j);
+            const float fk = L.f[KMAX - 1];
+            if (fk > published) {        // share the row's improved bound
+              atomicMax(p.row_bound + i, __float_as_int(fk));
+              published = fk;
+            }
+          }
         }
       }
     }
@@ -411,10 +431,11 @@ static TcLayout tc_layout(int64_t n, int64_t d, bool fp8) {
 }
 
 static void carve_tc(Carver& cv, const TcLayout& L, int64_t n, int K, void** xq, uint32_t** an,
-                     float** isq, int2** part) {
+                     float** isq, int** rb, int2** part) {
   *xq = cv.take<unsigned char>((size_t)L.n_pad * L.d_pad * (L.fp8 ? 1 : 2));
   *an = cv.take<uint32_t>(L.n_pad);
   *isq = cv.take<float>(L.n_pad);
+  *rb = cv.take<int>(L.n_pad);
   *part = cv.take<int2>((size_t)n * L.nseg * (tc::EPI_WARPS / 4) * K);
 }
 
@@ -425,8 +446,9 @@ size_t knn_tc_workspace(int64_t n, int64_t d, int K) {
   void* xq;
   uint32_t* an;
   float* isq;
+  int* rb;
   int2* part;
-  carve_tc(cv, L, n, K, &xq, &an, &isq, &part);
+  carve_tc(cv, L, n, K, &xq, &an, &isq, &rb, &part);
   return cv.used;
 }
 
@@ -450,8 +472,9 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   void* xq;
   uint32_t* an;
   float* isq;
+  int* rb;
   int2* part;
-  carve_tc(cv, L, n, K, &xq, &an, &isq, &part);
+  carve_tc(cv, L, n, K, &xq, &an, &isq, &rb, &part);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_tc: workspace too small");
   const int pg = (int)std::min<int64_t>(ceil_div(L.n_pad * 32, 256), 16 * kNumSMs);
   if (fp8)
@@ -472,6 +495,8 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   p.a_norm = an;
   p.inv_sqrt = isq;
   p.partial = part;
+  p.row_bound = rb;
+  ANCKA_CUDA(cudaMemsetAsync(rb, 0, sizeof(int) * L.n_pad, st));
   p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
   if (fp8) {
     if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }

@@ -47,6 +47,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// same, but the waiting thread may be suspended (up to `ns`) until the phase
+// completes instead of re-issuing the probe: keeps idle warps off the issue
+// ports of busy ones
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 100000) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(ns)
+      : "memory");
+}
 
 // -------------------------------------------------------------------- TMA
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
