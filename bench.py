@@ -80,7 +80,26 @@ class ClockSampler:
         self.index, self.samples, self._stop = index, [], threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
+    def _nvml(self):
+        """In-process NVML sampler (no subprocess spawning during timing)."""
+        import pynvml as nv
+        nv.nvmlInit()
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop.is_set():
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
+            self._stop.wait(0.05)
+
     def _run(self):
+        try:
+            self._nvml()
+            return
+        except Exception:
+            pass
         while not self._stop.is_set():
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
@@ -319,7 +338,8 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 5), "unit": "s", "n_gpus": ws,
                 "steps": args.steps, "warmup": max(args.warmup, 3),
-                "ms_per_step": round(t_step, 3), "higher_is_better": False, "scaling": "weak",
+                "ms_per_step": round(t_step, 3), "step_ms": [round(x, 3) for x in step_ms],
+                "higher_is_better": False, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
                 "config": workload_config(inst, K) | {"parallelism": f"replicas x{ws}"},
                 "knn_build_s": round(res.timings_ms["knn_ms"] / 1e3, 5),

@@ -45,6 +45,23 @@ typedef struct {
   const void* values;    /* nnz of the operator dtype, or NULL */
 } ancka_csr;
 
+/* Load-balancing plan for the f32 operator application: rows whose
+ * structural + KNN nonzeros exceed a threshold ("long" rows, e.g. KNN hubs)
+ * are cut into pieces of bounded length that are summed by separate threads
+ * and combined in a fixed order (deterministic).  All pointers NULL / counts 0
+ * disable it.  The f64 path ignores it (it keeps scipy's sequential order). */
+typedef struct {
+  int64_t n_long, n_pieces;
+  const uint8_t* is_long;     /* n                                        */
+  const int32_t* long_rows;   /* n_long                                   */
+  const int64_t* piece_ptr;   /* n_long + 1: pieces of each long row      */
+  const int32_t* piece_seg;   /* n_pieces: 0 structural, 1 KNN segment    */
+  const int64_t* piece_begin; /* n_pieces: nonzero range [begin, end)     */
+  const int64_t* piece_end;
+  void* partial;              /* n_pieces x max_ld f32 scratch            */
+  int64_t max_ld;
+} ancka_row_split;
+
 /* Device-resident WalkOperator (walk.py:89-104).  Index arrays are shared by
  * the f32 and f64 instances; `dtype` selects the value arrays. */
 typedef struct {
@@ -60,6 +77,7 @@ typedef struct {
   ancka_csr t_b;          /* hypergraph P_E^T (n x m); unused for graphs  */
   const void* beta;       /* n, beta_vector (walk.py:47-57)              */
   const uint8_t* selfloop;/* n, 1 where walk.py:123 adds a self-loop     */
+  ancka_row_split split;  /* f32 load balancing of the n-row pass         */
 } ancka_operator;
 
 const char* ancka_last_error(void);

@@ -24,10 +24,17 @@ class CSR(ctypes.Structure):
                 ("rowptr", c_void_p), ("colidx", c_void_p), ("values", c_void_p)]
 
 
+class RowSplit(ctypes.Structure):
+    _fields_ = [("n_long", c_int64), ("n_pieces", c_int64), ("is_long", c_void_p),
+                ("long_rows", c_void_p), ("piece_ptr", c_void_p), ("piece_seg", c_void_p),
+                ("piece_begin", c_void_p), ("piece_end", c_void_p), ("partial", c_void_p),
+                ("max_ld", c_int64)]
+
+
 class Operator(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("dtype", c_int32), ("n", c_int64), ("m", c_int64),
                 ("p_n", CSR), ("p_e", CSR), ("p_v", CSR), ("p_k", CSR), ("t_a", CSR),
-                ("t_b", CSR), ("beta", c_void_p), ("selfloop", c_void_p)]
+                ("t_b", CSR), ("beta", c_void_p), ("selfloop", c_void_p), ("split", RowSplit)]
 
 
 _OP = POINTER(Operator)

@@ -15,6 +15,7 @@
 //      obj = n - 2 sum(sigma), |d obj| < tol test, R = V U^T.
 // No float atomics anywhere: results are bit-reproducible run to run.
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -141,24 +142,92 @@ __device__ void phase_accumulate(const DiscParams& p, float* sR, float* tile, in
     __syncthreads();
     atomicAdd(&zsum, zeros);
     __syncthreads();
-    if (threadIdx.x == 0) p.part_arg[blockIdx.x * 2] = zsum;
+    // integer-valued double adds are exact, hence order independent
+    if (threadIdx.x == 0 && zsum) atomicAdd(&p.ctrl[C_ZERO], (double)zsum);
   }
   __syncthreads();
 }
 
 // CTA 0: reduce M partials -> M (smem f64) and counts (global)
+// All threads of CTA 0 take part: entry e is summed by G groups over
+// interleaved block subsets, then the G group sums are added in fixed order.
 __device__ void reduce_m(const DiscParams& p, double* M) {
-  const int k = p.k;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += p.part_m[(int64_t)b * k * k + e];
-    M[e] = s;
+  __shared__ double rsum[kDiscThreads];
+  __shared__ long long rcnt[kDiscThreads];
+  const int k = p.k, kk = k * k, nb = gridDim.x, t = threadIdx.x;
+  if (kk >= kDiscThreads) {
+    for (int e = t; e < kk; e += blockDim.x) {
+      double s0 = 0.0, s1 = 0.0;
+      int b = 0;
+      for (; b + 1 < nb; b += 2) {
+        s0 += p.part_m[(int64_t)b * kk + e];
+        s1 += p.part_m[(int64_t)(b + 1) * kk + e];
+      }
+      if (b < nb) s0 += p.part_m[(int64_t)b * kk + e];
+      M[e] = s0 + s1;
+    }
+  } else {
+    const int G = kDiscThreads / kk, g = t / kk, e = t % kk;
+    if (g < G) {
+      double s = 0.0;
+      for (int b = g; b < nb; b += G) s += p.part_m[(int64_t)b * kk + e];
+      rsum[g * kk + e] = s;
+    }
+    __syncthreads();
+    if (t < kk) {
+      double s = 0.0;
+      for (int gg = 0; gg < G; ++gg) s += rsum[gg * kk + t];
+      M[t] = s;
+    }
   }
-  for (int e = threadIdx.x; e < k; e += blockDim.x) {
-    int64_t s = 0;
-    for (int b = 0; b < (int)gridDim.x; ++b) s += p.part_cnt[(int64_t)b * k + e];
-    p.counts[e] = s;
+  {
+    const int G = kDiscThreads / k, g = t / k, e = t % k;
+    if (g < G) {
+      long long s = 0;
+      for (int b = g; b < nb; b += G) s += p.part_cnt[(int64_t)b * k + e];
+      rcnt[g * k + e] = s;
+    }
+    __syncthreads();
+    if (t < k) {
+      long long s = 0;
+      for (int gg = 0; gg < G; ++gg) s += rcnt[gg * k + t];
+      p.counts[t] = s;
+    }
   }
+  __syncthreads();
+}
+
+// CTA 0: reduce the per-CTA (value, index) partials in part_arg in parallel.
+// want_max: first max (larger value, then smaller index) else first min
+// (smaller value, then smaller index); entries with index < 0 are empty.
+__device__ void cta_reduce_arg(const double* part, int nb, bool want_max, double& v_out,
+                               long long& i_out) {
+  __shared__ double sv[kDiscThreads];
+  __shared__ long long si[kDiscThreads];
+  double v = 0.0;
+  long long id = -1;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+    const long long i2 = (long long)part[b * 2 + 1];
+    const double v2 = part[b * 2];
+    const bool take = i2 >= 0 && (id < 0 || (want_max ? v2 > v : v2 < v) || (v2 == v && i2 < id));
+    if (take) { v = v2; id = i2; }
+  }
+  sv[threadIdx.x] = v;
+  si[threadIdx.x] = id;
+  __syncthreads();
+  for (int s = kDiscThreads / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const double v2 = sv[threadIdx.x + s];
+      const long long i2 = si[threadIdx.x + s];
+      const double v1 = sv[threadIdx.x];
+      const long long i1 = si[threadIdx.x];
+      const bool take = i2 >= 0 && (i1 < 0 || (want_max ? v2 > v1 : v2 < v1) || (v2 == v1 && i2 < i1));
+      if (take) { sv[threadIdx.x] = v2; si[threadIdx.x] = i2; }
+    }
+    __syncthreads();
+  }
+  v_out = sv[0];
+  i_out = si[0];
   __syncthreads();
 }
 
@@ -323,17 +392,15 @@ discretize_kernel(DiscParams p) {
           p.part_arg[blockIdx.x * 2 + 1] = (double)bx[0];
         }
         grid.sync();
-        if (cta0 && threadIdx.x == 0) {
-          double v = INFINITY;
-          long long idx = -1;
-          for (int b = 0; b < (int)gridDim.x; ++b) {
-            long long i2 = (long long)p.part_arg[b * 2 + 1];
-            double v2 = p.part_arg[b * 2];
-            if (i2 >= 0 && (idx < 0 || v2 < v || (v2 == v && i2 < idx))) { v = v2; idx = i2; }
+        if (cta0) {
+          double v;
+          long long idx;
+          cta_reduce_arg(p.part_arg, gridDim.x, false, v, idx);
+          if (threadIdx.x == 0) {
+            double q[KMAX], nrm;
+            load_row<KMAX>(p, idx < 0 ? 0 : idx, q, nrm);
+            for (int l = 0; l < k; ++l) p.Rg[l * k + j] = q[l];
           }
-          double q[KMAX], nrm;
-          load_row<KMAX>(p, idx < 0 ? 0 : idx, q, nrm);
-          for (int l = 0; l < k; ++l) p.Rg[l * k + j] = q[l];
         }
         grid.sync();
       }
@@ -341,6 +408,7 @@ discretize_kernel(DiscParams p) {
     if (cta0 && threadIdx.x == 0) {
       p.ctrl[C_CONV] = 0;
       p.ctrl[C_STOP] = 0;
+      if (run == 0) p.ctrl[C_ZERO] = 0;
     }
     grid.sync();
 
@@ -357,11 +425,6 @@ discretize_kernel(DiscParams p) {
           int ne = 0;
           for (int c = 0; c < k; ++c) ne += p.counts[c] == 0;
           p.ctrl[C_NEMPTY] = ne;
-          if (run == 0 && it == 0) {
-            double z = 0;
-            for (int b = 0; b < (int)gridDim.x; ++b) z += p.part_arg[b * 2];
-            p.ctrl[C_ZERO] = z;
-          }
         }
       }
       grid.sync();
@@ -372,14 +435,10 @@ discretize_kernel(DiscParams p) {
           if (p.counts[c] != 0) continue;   // counts is uniform across CTAs here
           partial_argmax_movable(p, s_red);
           grid.sync();
+          double vmax = 0.0;
+          long long idx = -1;
+          if (cta0) cta_reduce_arg(p.part_arg, gridDim.x, true, vmax, idx);
           if (cta0 && threadIdx.x == 0) {
-            float v = -INFINITY;
-            long long idx = -1;
-            for (int b = 0; b < (int)gridDim.x; ++b) {
-              long long i2 = (long long)p.part_arg[b * 2 + 1];
-              float v2 = (float)p.part_arg[b * 2];
-              if (i2 >= 0 && (idx < 0 || v2 > v || (v2 == v && i2 < idx))) { v = v2; idx = i2; }
-            }
             p.ctrl[C_ARGIDX] = (double)idx;
             if (idx >= 0) {
               const int old = p.labels[idx];
@@ -513,7 +572,9 @@ static int launch_disc(DiscParams& p, cudaStream_t st) {
   int dev = 0, sms = 0;
   ANCKA_CUDA(cudaGetDevice(&dev));
   ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  int64_t want = ceil_div(p.n, kDiscThreads);
+  // rows per CTA: enough work per phase to amortise the grid barrier
+  static const int64_t min_rows = getenv("ANCKA_DISC_ROWS") ? atoll(getenv("ANCKA_DISC_ROWS")) : 2048;
+  int64_t want = ceil_div(p.n, std::max<int64_t>(kDiscThreads, min_rows));
   int64_t grid = std::min(want, std::min((int64_t)per_sm * sms, (int64_t)disc_grid_cap()));
   if (grid < 1) grid = 1;
   void* args[] = {&p};

@@ -89,22 +89,14 @@ __device__ __forceinline__ float dadd(float a, float b) { return a + b; }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
 
-template <typename T>
-__global__ void __launch_bounds__(256)
-spmm_kernel(SpmmArgs<T> a) {
-  using VT = typename Vec<T>::type;
+// self-loop, beta mix, tag epilogue and store of one (row, chunk)
+template <typename T, typename VT>
+__device__ __forceinline__ void finish_row(const SpmmArgs<T>& a, int64_t row, int64_t coloff,
+                                           VT s, VT k) {
   constexpr int W = Vec<T>::W;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t row = gid / a.nchunk;
-  if (row >= a.rows) return;
-  const int chunk = (int)(gid - row * a.nchunk);
-  const int64_t coloff = (int64_t)chunk * W;
-
-  VT s = seg_sum<T, VT>(a.s, row, coloff);
   if (a.selfloop && a.selfloop[row]) add_acc(s, ldv(a.self_src + row * a.self_ld + coloff));
   VT out = s;
   if (a.beta) {
-    VT k = seg_sum<T, VT>(a.k, row, coloff);
     const T b = __ldg(a.beta + row);
     const T omb = dadd(T(1), -b);   // 1.0 - beta, as (1.0 - op.beta)
 #pragma unroll
@@ -129,6 +121,67 @@ spmm_kernel(SpmmArgs<T> a) {
 }
 
 template <typename T>
+__global__ void __launch_bounds__(256)
+spmm_kernel(SpmmArgs<T> a) {
+  using VT = typename Vec<T>::type;
+  constexpr int W = Vec<T>::W;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t row = gid / a.nchunk;
+  if (row >= a.rows) return;
+  if (a.skip && a.skip[row]) return;            // long row: pieces + combine
+  const int chunk = (int)(gid - row * a.nchunk);
+  const int64_t coloff = (int64_t)chunk * W;
+  VT s = seg_sum<T, VT>(a.s, row, coloff);
+  VT k;
+  if (a.beta) k = seg_sum<T, VT>(a.k, row, coloff);
+  else memset(&k, 0, sizeof(k));
+  finish_row<T, VT>(a, row, coloff, s, k);
+}
+
+// one bounded nonzero range of a long row -> partial[piece]
+__global__ void __launch_bounds__(256)
+spmm_piece_kernel(SpmmArgs<float> a, ancka_row_split sp) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t pc = gid / a.nchunk;
+  if (pc >= sp.n_pieces) return;
+  const int64_t coloff = (int64_t)(gid - pc * a.nchunk) * 4;
+  const SegArgs<float>& g = sp.piece_seg[pc] ? a.k : a.s;
+  const int64_t e = sp.piece_end[pc];
+  const float* src = g.src + coloff;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  int64_t p = sp.piece_begin[pc];
+  for (; p + 4 <= e; p += 4) {
+    const int32_t j0 = __ldg(g.colidx + p), j1 = __ldg(g.colidx + p + 1);
+    const int32_t j2 = __ldg(g.colidx + p + 2), j3 = __ldg(g.colidx + p + 3);
+    const float w0 = g.values ? __ldg(g.values + p) : 1.f, w1 = g.values ? __ldg(g.values + p + 1) : 1.f;
+    const float w2 = g.values ? __ldg(g.values + p + 2) : 1.f, w3 = g.values ? __ldg(g.values + p + 3) : 1.f;
+    const float4 x0 = ldv(src + (int64_t)j0 * g.ld), x1 = ldv(src + (int64_t)j1 * g.ld);
+    const float4 x2 = ldv(src + (int64_t)j2 * g.ld), x3 = ldv(src + (int64_t)j3 * g.ld);
+    fma_acc(acc, w0, x0); fma_acc(acc, w1, x1); fma_acc(acc, w2, x2); fma_acc(acc, w3, x3);
+  }
+  for (; p < e; ++p)
+    fma_acc(acc, g.values ? __ldg(g.values + p) : 1.f, ldv(src + (int64_t)__ldg(g.colidx + p) * g.ld));
+  *reinterpret_cast<float4*>(static_cast<float*>(sp.partial) + pc * sp.max_ld + coloff) = acc;
+}
+
+// fixed-order combination of the pieces of each long row + the row epilogue
+__global__ void __launch_bounds__(256)
+spmm_combine_kernel(SpmmArgs<float> a, ancka_row_split sp) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t li = gid / a.nchunk;
+  if (li >= sp.n_long) return;
+  const int64_t coloff = (int64_t)(gid - li * a.nchunk) * 4;
+  const int64_t row = sp.long_rows[li];
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f), k = s;
+  const float* part = static_cast<const float*>(sp.partial);
+  for (int64_t pc = sp.piece_ptr[li]; pc < sp.piece_ptr[li + 1]; ++pc) {
+    const float4 v = *reinterpret_cast<const float4*>(part + pc * sp.max_ld + coloff);
+    if (sp.piece_seg[pc]) add_acc(k, v); else add_acc(s, v);
+  }
+  finish_row<float, float4>(a, row, coloff, s, k);
+}
+
+template <typename T>
 int launch_spmm(const SpmmArgs<T>& args, cudaStream_t st) {
   if (args.rows == 0) return ANCKA_OK;
   const int64_t threads = args.rows * args.nchunk;
@@ -136,6 +189,16 @@ int launch_spmm(const SpmmArgs<T>& args, cudaStream_t st) {
   const int64_t grid = ceil_div(threads, bs);
   ANCKA_REQUIRE(grid < (1ll << 31), ANCKA_ERR_ARG, "spmm grid too large");
   spmm_kernel<T><<<(unsigned)grid, bs, 0, st>>>(args);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+static int launch_split(const SpmmArgs<float>& a, const ancka_row_split& sp, cudaStream_t st) {
+  ANCKA_REQUIRE(a.nchunk * 4 <= sp.max_ld, ANCKA_ERR_ARG, "row split scratch narrower than block");
+  const int64_t t1 = sp.n_pieces * a.nchunk, t2 = sp.n_long * a.nchunk;
+  spmm_piece_kernel<<<(unsigned)ceil_div(t1, 256), 256, 0, st>>>(a, sp);
+  ANCKA_LAUNCHED();
+  spmm_combine_kernel<<<(unsigned)ceil_div(t2, 256), 256, 0, st>>>(a, sp);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
@@ -193,6 +256,13 @@ int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, i
     a.tag = epi->tag;
     a.tagval = epi->tagval;
     a.scale = epi->scale;
+  }
+  if constexpr (std::is_same<T, float>::value) {
+    if (op->split.n_long > 0) {
+      a.skip = op->split.is_long;
+      ANCKA_TRY(launch_spmm<T>(a, st));
+      return launch_split(a, op->split, st);
+    }
   }
   return launch_spmm<T>(a, st);
 }

@@ -1,5 +1,7 @@
 // Internal interface of the walk-operator SpMM (spmm.cu).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace ancka {
@@ -23,6 +25,7 @@ struct SpmmArgs {
   const T* self_src = nullptr;
   int64_t self_ld = 0;
   const T* beta = nullptr;          // nullptr: no mix (structure only)
+  const uint8_t* skip = nullptr;    // rows handled by the row-split path
   const int32_t* tag = nullptr;     // epilogue: out = scale*out + (col==tag ? tagval[col] : 0)
   const T* tagval = nullptr;
   T scale = T(1);

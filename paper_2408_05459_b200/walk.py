@@ -142,9 +142,54 @@ class WalkOperator:
                 csr_struct(f.get("p_v"), dtype), csr_struct(self.p_k_dev, dtype),
                 csr_struct(f.get("t_a"), dtype), csr_struct(f.get("t_b"), dtype),
                 (self.beta64 if dtype == _lib.F64 else self.beta32).data_ptr(),
-                self.selfloop_dev.data_ptr())
+                self.selfloop_dev.data_ptr(),
+                self._split_plan() if dtype == _lib.F32 else _lib.RowSplit())
             self._structs[dtype] = s
         return s
+
+    # rows costing more than LONG_ROW nonzeros are cut into PIECE-long pieces
+    LONG_ROW, PIECE, MAX_LD = 64, 32, 256
+
+    def _split_plan(self) -> _lib.RowSplit:
+        """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs)."""
+        srp = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"].rowptr.cpu().numpy()
+        krp = self.p_k_dev.rowptr.cpu().numpy()
+        ls, lk = np.diff(srp), np.diff(krp)
+        long_rows = np.flatnonzero(ls + lk > self.LONG_ROW).astype(np.int32)
+        if long_rows.size == 0:
+            return _lib.RowSplit()
+        P = self.PIECE
+        ns = -(-ls[long_rows] // P)                   # structural pieces per long row
+        nk = -(-lk[long_rows] // P)                   # KNN pieces per long row
+        per = ns + nk
+        ptr = np.concatenate([[0], np.cumsum(per)])
+        # within-row piece ordinal q and its segment (structural pieces first)
+        q = np.arange(ptr[-1]) - np.repeat(ptr[:-1], per)
+        rrep = np.repeat(long_rows, per)
+        is_k = q >= np.repeat(ns, per)
+        qq = np.where(is_k, q - np.repeat(ns, per), q)
+        rb = np.where(is_k, krp[rrep], srp[rrep])
+        re = np.where(is_k, krp[rrep + 1], srp[rrep + 1])
+        begins = rb + qq * P
+        ends = np.minimum(re, begins + P)
+        segs = is_k.astype(np.int32)
+        d = dev()
+        mask = np.zeros(self.n, dtype=np.uint8)
+        mask[long_rows] = 1
+        self._plan = {
+            "is_long": torch.from_numpy(mask).to(d),
+            "long_rows": torch.from_numpy(long_rows).to(d),
+            "piece_ptr": torch.from_numpy(ptr.astype(np.int64)).to(d),
+            "piece_seg": torch.from_numpy(segs).to(d),
+            "piece_begin": torch.from_numpy(begins.astype(np.int64)).to(d),
+            "piece_end": torch.from_numpy(ends.astype(np.int64)).to(d),
+            "partial": torch.empty(len(segs) * self.MAX_LD, dtype=torch.float32, device=d),
+        }
+        p = self._plan
+        return _lib.RowSplit(long_rows.size, len(segs), p["is_long"].data_ptr(),
+                             p["long_rows"].data_ptr(), p["piece_ptr"].data_ptr(),
+                             p["piece_seg"].data_ptr(), p["piece_begin"].data_ptr(),
+                             p["piece_end"].data_ptr(), p["partial"].data_ptr(), self.MAX_LD)
 
     def scratch(self, c: int, dtype: torch.dtype, key: str = "op_scratch") -> torch.Tensor:
         rows = max(self.m, 1)
