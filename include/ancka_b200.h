@@ -105,6 +105,15 @@ int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t 
                     int32_t integer_exact, int32_t* ids, double* scores,
                     void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
+/* Same, with X given as a CSR matrix (indptr n+1, sorted indices, f64 data):
+ * the quantised tensor-core operand is built directly from the nonzeros (no
+ * dense f64 copy).  Integer-exact path only (integer_exact = 1 bf16, 2 fp8);
+ * the workspace is ancka_knn_workspace_size(n, d, K, integer_exact). */
+int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices, const double* data,
+                        int64_t n, int64_t d, int32_t K, int32_t integer_exact, int32_t* ids,
+                        double* scores, void* workspace, size_t workspace_bytes,
+                        ancka_stream_t stream);
+
 /* build_knn_adjacency + knn_transition (knn.py:294-324): A_K = M + M^T as a
  * sorted CSR and P_K = D_K^-1 A_K with row sums summed exactly as numpy's
  * pairwise reduction (so f64 values are bit-identical to scipy's).

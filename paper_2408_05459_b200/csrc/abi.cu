@@ -71,3 +71,14 @@ extern "C" int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ld
   ANCKA_TRY(normalize_rows_f64(X, n, d, ldx, xn, ldn, nr, st));
   return knn_simt(xn, n, ldn, nr, K, ids, scores, st);
 }
+
+extern "C" int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices, const double* data,
+                                   int64_t n, int64_t d, int32_t K, int32_t integer_exact,
+                                   int32_t* ids, double* scores, void* workspace,
+                                   size_t workspace_bytes, ancka_stream_t stream) {
+  ANCKA_REQUIRE(K < n, ANCKA_ERR_NETWORK, "K=%d must be smaller than n=%lld", K, (long long)n);
+  ANCKA_REQUIRE(integer_exact == 1 || integer_exact == 2, ANCKA_ERR_UNSUPPORTED,
+                "CSR attributes are supported on the integer-exact tensor-core path only");
+  return knn_tc_csr(indptr, indices, data, n, d, K, ids, scores, workspace, workspace_bytes,
+                    as_stream(stream), integer_exact == 2);
+}

@@ -2,18 +2,21 @@
 // (engine.py:162-263) plus the post-pass repair check (engine.py:266-288).
 //
 // One cooperative persistent kernel runs both alternating-rounding starts
-// (identity, prototype) for up to max_iter rounds without returning to the
-// host.  Per round:
-//   A  every CTA: row-normalise its rows of Q[:, col0:col0+k], score against R
-//      (k x k, smem broadcast), first-max argmax + second-best margin, and
-//      accumulate per-cluster column sums of Q~ deterministically (each
-//      thread owns one column of one accumulator group; fixed row order).
-//   B  CTA 0: fixed-order reduction of the CTA partials -> M, sizes; empty
-//      clusters are re-seeded with the reference's margin rule (grid-wide
-//      first-max argmax per empty cluster), then M is recomputed.
-//   C  CTA 0: Y~ = Y/size, one-sided Jacobi SVD of Y~^T Q~ in f64,
-//      obj = n - 2 sum(sigma), |d obj| < tol test, R = V U^T.
-// No float atomics anywhere: results are bit-reproducible run to run.
+// (identity, prototype; engine.py:247-253) for up to max_iter rounds without
+// returning to the host.  Per round:
+//   A  every CTA: row-normalise its rows of Q[:, col0:col0+k], score them
+//      against R (k x k, shared-memory broadcast), first-max argmax and
+//      second-best margin, and accumulate per-cluster column sums of Q~
+//      deterministically (each thread owns one column of one accumulator
+//      group, fixed row order) into a double-buffered per-CTA partial.
+//   -- one grid barrier --
+//   B  every CTA, redundantly and identically: fixed-order reduction of the
+//      partials -> M (k x k, f64) and the cluster sizes; Y~ = Y/size (the
+//      reference's 1/size, engine.py:194-198); polar factor R = V U^T of
+//      (Y~^T Q~)^T by Newton-Schulz (the SVD's V U^T, engine.py:199-205) and
+//      sum(sigma) = tr(R Y~^T Q~); obj = n - 2 sum(sigma); |d obj| < tol.
+// Empty clusters (rare) take a slower path with the reference's margin rule
+// (engine.py:162-180).  No float atomics: results are bit-reproducible.
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -34,28 +37,13 @@ struct DiscParams {
   int32_t* labels_run0; // saved labels of run 0
   float* margin;        // n, second-best score
   double* proto_acc;    // n, prototype accumulator
-  double* part_m;       // grid x k x k
-  int64_t* part_cnt;    // grid x k
-  double* part_arg;     // grid x 2  (value, index) for grid argmax/argmin
-  double* Rg;           // k x k f64 rotation (row l, col j)
-  double* ctrl;         // control block (see below)
-  int64_t* counts;      // k
+  double* part_m;       // 2 x grid x k x k
+  int64_t* part_cnt;    // 2 x grid x k
+  double* part_arg;     // 2 x grid x 3  (value, index, label)
+  double* Rg;           // k x k f64 rotation (row l, col j), written by CTA 0
   double* info;         // output info
+  unsigned long long* tdbg;  // optional phase timing (ANCKA_DISC_TIMING)
   int groups;           // accumulator groups per CTA
-};
-
-// ctrl layout
-enum { C_CONV = 0, C_OBJ_PREV, C_NEMPTY, C_ARGIDX, C_STOP, C_ZERO, C_NCTRL = 8 };
-
-template <int KMAX>
-struct Smem {
-  // phase A view
-  float* R;      // k*k f32 scores rotation
-  float* tile;   // kDiscThreads*k
-  int* tlab;     // kDiscThreads
-  double* acc;   // groups*k*k
-  int* cnt;      // k
-  double* red;   // 64 scratch
 };
 
 template <int KMAX>
@@ -71,30 +59,39 @@ __device__ __forceinline__ void load_row(const DiscParams& p, int64_t i, double*
   nrm = sqrt(s);
   const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
 #pragma unroll
-  for (int l = 0; l < KMAX; ++l) q[l] = nrm > 0 ? q[l] / nrm : 0.0;
-  (void)inv;
+  for (int l = 0; l < KMAX; ++l) q[l] *= inv;
 }
 
-// Phase A.  score=true: compute labels + margins from R; false: use labels.
+struct Rows {
+  int64_t r0, r1;
+};
+__device__ __forceinline__ Rows my_rows(int64_t n) {
+  const int64_t rpb = ceil_div(n, gridDim.x);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb;
+  return {r0, lmin(n, r0 + rpb)};
+}
+
+// Phase A.  score=true: labels + margins from R; false: keep labels.
 template <int KMAX>
-__device__ void phase_accumulate(const DiscParams& p, float* sR, float* tile, int* tlab,
-                                 double* acc, int* cnt, bool score, int* zero_rows) {
+__device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, float* tile,
+                                 int* tlab, double* acc, int* cnt, bool score, int* zeros_out) {
   const int k = p.k;
   const int G = p.groups;
   for (int e = threadIdx.x; e < G * k * k; e += blockDim.x) acc[e] = 0.0;
-  for (int e = threadIdx.x; e < k; e += blockDim.x) cnt[e] = 0;
+  for (int e = threadIdx.x; e < G * k; e += blockDim.x) cnt[e] = 0;
   __syncthreads();
-  const int64_t rows_per_block = ceil_div(p.n, gridDim.x);
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = lmin(p.n, r0 + rows_per_block);
+  const Rows R = my_rows(p.n);
   int zeros = 0;
-  for (int64_t t0 = r0; t0 < r1; t0 += kDiscThreads) {
+  for (int64_t t0 = R.r0; t0 < R.r1; t0 += kDiscThreads) {
     const int64_t i = t0 + threadIdx.x;
-    if (i < r1) {
+    if (i < R.r1) {
       double q[KMAX];
       double nrm;
       load_row<KMAX>(p, i, q, nrm);
       if (nrm == 0.0) ++zeros;
+      float qf[KMAX];
+#pragma unroll
+      for (int l = 0; l < KMAX; ++l) qf[l] = (float)q[l];
       int lab;
       if (score) {
         float best = -INFINITY, second = -INFINITY;
@@ -103,7 +100,7 @@ __device__ void phase_accumulate(const DiscParams& p, float* sR, float* tile, in
           float s = 0.f;
 #pragma unroll
           for (int l = 0; l < KMAX; ++l)
-            if (l < k) s = fmaf((float)q[l], sR[l * k + j], s);
+            if (l < k) s = fmaf(qf[l], sR[l * k + j], s);
           if (s > best) { second = best; best = s; lab = j; }
           else if (s > second) second = s;
         }
@@ -114,64 +111,74 @@ __device__ void phase_accumulate(const DiscParams& p, float* sR, float* tile, in
       }
 #pragma unroll
       for (int l = 0; l < KMAX; ++l)
-        if (l < k) tile[threadIdx.x * k + l] = (float)q[l];
+        if (l < k) tile[threadIdx.x * k + l] = qf[l];
       tlab[threadIdx.x] = lab;
-      atomicAdd(&cnt[lab], 1);  // integer: order independent
     }
     __syncthreads();
-    const int tr = (int)lmin(kDiscThreads, r1 - t0);
+    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
     const int t = threadIdx.x;
     if (t < G * k) {
       const int j = t % k, g = t / k;
       double* a = acc + (size_t)g * k * k;
-      for (int r = g; r < tr; r += G) a[tlab[r] * k + j] += (double)tile[r * k + j];
+      int* cg_ = cnt + g * k;                 // column-0 owners also count members
+      for (int r = g; r < tr; r += G) {
+        const int l = tlab[r];
+        a[l * k + j] += (double)tile[r * k + j];
+        if (j == 0) cg_[l] += 1;
+      }
     }
     __syncthreads();
   }
-  // combine groups (fixed order) and publish the CTA partial
+  double* pm = p.part_m + ((size_t)buf * gridDim.x + blockIdx.x) * k * k;
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     double s = 0.0;
     for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
-    p.part_m[(int64_t)blockIdx.x * k * k + e] = s;
+    pm[e] = s;
   }
-  for (int e = threadIdx.x; e < k; e += blockDim.x)
-    p.part_cnt[(int64_t)blockIdx.x * k + e] = cnt[e];
-  if (zero_rows) {
+  int64_t* pc = p.part_cnt + ((size_t)buf * gridDim.x + blockIdx.x) * k;
+  for (int e = threadIdx.x; e < k; e += blockDim.x) {
+    int s = 0;
+    for (int g = 0; g < G; ++g) s += cnt[g * k + e];
+    pc[e] = s;
+  }
+  if (zeros_out) {
     __shared__ int zsum;
     if (threadIdx.x == 0) zsum = 0;
     __syncthreads();
     atomicAdd(&zsum, zeros);
     __syncthreads();
-    // integer-valued double adds are exact, hence order independent
-    if (threadIdx.x == 0 && zsum) atomicAdd(&p.ctrl[C_ZERO], (double)zsum);
+    if (threadIdx.x == 0) *zeros_out = zsum;   // reduced over CTAs via part_cnt below
   }
   __syncthreads();
 }
 
-// CTA 0: reduce M partials -> M (smem f64) and counts (global)
-// All threads of CTA 0 take part: entry e is summed by G groups over
-// interleaved block subsets, then the G group sums are added in fixed order.
-__device__ void reduce_m(const DiscParams& p, double* M) {
-  __shared__ double rsum[kDiscThreads];
-  __shared__ long long rcnt[kDiscThreads];
+// Every CTA: fixed-order reduction of buffer `buf` -> M (smem f64), sizes.
+__device__ void reduce_partials(const DiscParams& p, int buf, double* M, long long* sizes,
+                                double* rsum, long long* rcnt) {
   const int k = p.k, kk = k * k, nb = gridDim.x, t = threadIdx.x;
+  const double* pm = p.part_m + (size_t)buf * nb * kk;
+  const int64_t* pc = p.part_cnt + (size_t)buf * nb * k;
   if (kk >= kDiscThreads) {
     for (int e = t; e < kk; e += blockDim.x) {
       double s0 = 0.0, s1 = 0.0;
       int b = 0;
-      for (; b + 1 < nb; b += 2) {
-        s0 += p.part_m[(int64_t)b * kk + e];
-        s1 += p.part_m[(int64_t)(b + 1) * kk + e];
-      }
-      if (b < nb) s0 += p.part_m[(int64_t)b * kk + e];
+      for (; b + 1 < nb; b += 2) { s0 += pm[(size_t)b * kk + e]; s1 += pm[(size_t)(b + 1) * kk + e]; }
+      if (b < nb) s0 += pm[(size_t)b * kk + e];
       M[e] = s0 + s1;
     }
   } else {
     const int G = kDiscThreads / kk, g = t / kk, e = t % kk;
-    if (g < G) {
-      double s = 0.0;
-      for (int b = g; b < nb; b += G) s += p.part_m[(int64_t)b * kk + e];
-      rsum[g * kk + e] = s;
+    if (g < G) {  // 4 independent accumulators (memory-level parallelism), fixed order
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+      int b = g;
+      for (; b + 3 * G < nb; b += 4 * G) {
+        s0 += pm[(size_t)b * kk + e];
+        s1 += pm[(size_t)(b + G) * kk + e];
+        s2 += pm[(size_t)(b + 2 * G) * kk + e];
+        s3 += pm[(size_t)(b + 3 * G) * kk + e];
+      }
+      for (; b < nb; b += G) s0 += pm[(size_t)b * kk + e];
+      rsum[g * kk + e] = (s0 + s1) + (s2 + s3);
     }
     __syncthreads();
     if (t < kk) {
@@ -184,36 +191,35 @@ __device__ void reduce_m(const DiscParams& p, double* M) {
     const int G = kDiscThreads / k, g = t / k, e = t % k;
     if (g < G) {
       long long s = 0;
-      for (int b = g; b < nb; b += G) s += p.part_cnt[(int64_t)b * k + e];
+      for (int b = g; b < nb; b += G) s += pc[(size_t)b * k + e];
       rcnt[g * k + e] = s;
     }
     __syncthreads();
     if (t < k) {
       long long s = 0;
       for (int gg = 0; gg < G; ++gg) s += rcnt[gg * k + t];
-      p.counts[t] = s;
+      sizes[t] = s;
     }
   }
   __syncthreads();
 }
 
-// CTA 0: reduce the per-CTA (value, index) partials in part_arg in parallel.
-// want_max: first max (larger value, then smaller index) else first min
-// (smaller value, then smaller index); entries with index < 0 are empty.
-__device__ void cta_reduce_arg(const double* part, int nb, bool want_max, double& v_out,
-                               long long& i_out) {
-  __shared__ double sv[kDiscThreads];
-  __shared__ long long si[kDiscThreads];
+// Every CTA: reduce (value, index, label) partials of buffer `buf`.
+// want_max: first max (larger value, then smaller index), else first min.
+__device__ void reduce_arg(const double* part, int nb, bool want_max, double& v_out,
+                           long long& i_out, int& lab_out, double* sv, long long* si, int* sl) {
   double v = 0.0;
   long long id = -1;
+  int lb = 0;
   for (int b = threadIdx.x; b < nb; b += blockDim.x) {
-    const long long i2 = (long long)part[b * 2 + 1];
-    const double v2 = part[b * 2];
+    const long long i2 = (long long)part[b * 3 + 1];
+    const double v2 = part[b * 3];
     const bool take = i2 >= 0 && (id < 0 || (want_max ? v2 > v : v2 < v) || (v2 == v && i2 < id));
-    if (take) { v = v2; id = i2; }
+    if (take) { v = v2; id = i2; lb = (int)part[b * 3 + 2]; }
   }
   sv[threadIdx.x] = v;
   si[threadIdx.x] = id;
+  sl[threadIdx.x] = lb;
   __syncthreads();
   for (int s = kDiscThreads / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
@@ -222,307 +228,376 @@ __device__ void cta_reduce_arg(const double* part, int nb, bool want_max, double
       const double v1 = sv[threadIdx.x];
       const long long i1 = si[threadIdx.x];
       const bool take = i2 >= 0 && (i1 < 0 || (want_max ? v2 > v1 : v2 < v1) || (v2 == v1 && i2 < i1));
-      if (take) { sv[threadIdx.x] = v2; si[threadIdx.x] = i2; }
+      if (take) { sv[threadIdx.x] = v2; si[threadIdx.x] = i2; sl[threadIdx.x] = sl[threadIdx.x + s]; }
     }
     __syncthreads();
   }
   v_out = sv[0];
   i_out = si[0];
+  lab_out = sl[0];
   __syncthreads();
 }
 
-// Grid-wide first-max of margin over movable rows (sizes[label] >= 2).
-__device__ void partial_argmax_movable(const DiscParams& p, double* red) {
-  const int64_t rows_per_block = ceil_div(p.n, gridDim.x);
-  const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
-  const int64_t r1 = lmin(p.n, r0 + rows_per_block);
-  float best = -INFINITY;
-  int64_t bi = -1;
-  for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-    if (p.counts[p.labels[i]] >= 2) {
-      const float m = p.margin[i];
-      if (bi < 0 || m > best || (m == best && i < bi)) { best = m; bi = i; }
-    }
-  }
-  // block reduce (value desc, index asc), deterministic
-  __shared__ float sv[kDiscThreads];
-  __shared__ long long si[kDiscThreads];
-  sv[threadIdx.x] = best;
-  si[threadIdx.x] = bi;
+// CTA-local first-max/first-min (value, index, label) -> part[blockIdx]
+__device__ void block_arg(double v, long long id, int lab, bool want_max, double* part,
+                          double* sv, long long* si, int* sl) {
+  sv[threadIdx.x] = v;
+  si[threadIdx.x] = id;
+  sl[threadIdx.x] = lab;
   __syncthreads();
   for (int s = kDiscThreads / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
-      float v2 = sv[threadIdx.x + s];
-      long long i2 = si[threadIdx.x + s];
-      float v1 = sv[threadIdx.x];
-      long long i1 = si[threadIdx.x];
-      bool take = (i2 >= 0) && (i1 < 0 || v2 > v1 || (v2 == v1 && i2 < i1));
-      if (take) { sv[threadIdx.x] = v2; si[threadIdx.x] = i2; }
+      const double v2 = sv[threadIdx.x + s];
+      const long long i2 = si[threadIdx.x + s];
+      const double v1 = sv[threadIdx.x];
+      const long long i1 = si[threadIdx.x];
+      const bool take = i2 >= 0 && (i1 < 0 || (want_max ? v2 > v1 : v2 < v1) || (v2 == v1 && i2 < i1));
+      if (take) { sv[threadIdx.x] = v2; si[threadIdx.x] = i2; sl[threadIdx.x] = sl[threadIdx.x + s]; }
     }
     __syncthreads();
   }
   if (threadIdx.x == 0) {
-    p.part_arg[blockIdx.x * 2] = sv[0];
-    p.part_arg[blockIdx.x * 2 + 1] = (double)si[0];
+    part[blockIdx.x * 3] = sv[0];
+    part[blockIdx.x * 3 + 1] = (double)si[0];
+    part[blockIdx.x * 3 + 2] = (double)sl[0];
   }
-  (void)red;
+  __syncthreads();
 }
 
-// one-sided Jacobi SVD of A (k x k, row-major f64, smem) by CTA 0.
-// On return A holds U*Sigma (columns), V the right vectors; sigma in sig.
-__device__ void jacobi_svd(double* A, double* V, double* sig, int k, int* flag) {
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) V[e] = (e / k == e % k) ? 1.0 : 0.0;
-  __syncthreads();
-  const int K2 = k + (k & 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nwarps = blockDim.x >> 5;
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    if (threadIdx.x == 0) *flag = 0;
-    __syncthreads();
-    for (int step = 0; step < K2 - 1; ++step) {
-      for (int pi = warp; pi < K2 / 2; pi += nwarps) {
-        int a, b;
-        if (pi == 0) { a = step; b = K2 - 1; }
-        else { a = (step + pi) % (K2 - 1); b = (step - pi + K2 - 1) % (K2 - 1); }
-        if (a > b) { int t = a; a = b; b = t; }
-        if (b >= k) continue;
-        double al = 0, be = 0, ga = 0;
-        for (int r = lane; r < k; r += 32) {
-          double x = A[r * k + a], y = A[r * k + b];
-          al += x * x; be += y * y; ga += x * y;
-        }
-        al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > 1e-15 * sqrt(al * be)) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
-          for (int r = lane; r < k; r += 32) {
-            double x = A[r * k + a], y = A[r * k + b];
-            A[r * k + a] = cs * x - sn * y;
-            A[r * k + b] = sn * x + cs * y;
-            double vx = V[r * k + a], vy = V[r * k + b];
-            V[r * k + a] = cs * vx - sn * vy;
-            V[r * k + b] = sn * vx + cs * vy;
-          }
-          if (lane == 0) *flag = 1;
-        }
-      }
-      __syncthreads();
-    }
-    if (*flag == 0) break;
-    __syncthreads();
-  }
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
-    double s = 0;
-    for (int r = 0; r < k; ++r) s += A[r * k + j] * A[r * k + j];
-    sig[j] = sqrt(s);
-  }
-  __syncthreads();
+// Polar factor of A^T (A = M~ = U S V^T):  X -> V U^T by Newton-Schulz
+// X <- 1.5 X - 0.5 X X^T X from X0 = A^T / ||A||_F (all singular values in
+// (0, 1]).  Returns sum(sigma) = tr(X A).  Identical arithmetic in every CTA.
+//
+// k <= 8: warp 0 keeps X and Y in registers (entries lane and lane+32) and
+// forms the products with shuffles -- no barriers inside the iteration.
+__device__ __forceinline__ double wget(double v0, double v1, int e) {
+  const double a = __shfl_sync(0xffffffffu, v0, e & 31);
+  const double b = __shfl_sync(0xffffffffu, v1, e & 31);
+  return e < 32 ? a : b;
 }
+
+__device__ double polar_ns_small(const double* A, double* X, int k, int* iters) {
+  const int kk = k * k, lane = threadIdx.x & 31;
+  const int e0 = lane, e1 = lane + 32;
+  const bool v0ok = e0 < kk, v1ok = e1 < kk;
+  double a0 = v0ok ? A[e0] : 0.0, a1 = v1ok ? A[e1] : 0.0;
+  double s = warp_sum(a0 * a0 + a1 * a1);
+  const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
+  // X = A^T * inv: X[e] = A[(e % k) * k + e / k]
+  double x0 = v0ok ? A[(e0 % k) * k + e0 / k] * inv : 0.0;
+  double x1 = v1ok ? A[(e1 % k) * k + e1 / k] * inv : 0.0;
+  const int r0 = e0 / k, c0 = e0 % k, r1 = e1 / k, c1 = e1 % k;
+  int it = 0;
+  for (; it < 100; ++it) {
+    double y0 = 0.0, y1 = 0.0;                          // Y = X^T X
+    for (int l = 0; l < k; ++l) {
+      const double p0 = wget(x0, x1, l * k + (v0ok ? r0 : 0));
+      const double q0 = wget(x0, x1, l * k + (v0ok ? c0 : 0));
+      const double p1 = wget(x0, x1, l * k + (v1ok ? r1 : 0));
+      const double q1 = wget(x0, x1, l * k + (v1ok ? c1 : 0));
+      y0 += p0 * q0;
+      y1 += p1 * q1;
+    }
+    double t0 = 0.0, t1 = 0.0;                          // T = X Y
+    for (int l = 0; l < k; ++l) {
+      const double p0 = wget(x0, x1, (v0ok ? r0 : 0) * k + l);
+      const double q0 = wget(y0, y1, l * k + (v0ok ? c0 : 0));
+      const double p1 = wget(x0, x1, (v1ok ? r1 : 0) * k + l);
+      const double q1 = wget(y0, y1, l * k + (v1ok ? c1 : 0));
+      t0 += p0 * q0;
+      t1 += p1 * q1;
+    }
+    const double n0 = 1.5 * x0 - 0.5 * t0, n1 = 1.5 * x1 - 0.5 * t1;
+    const bool moved = (v0ok && fabs(n0 - x0) > 1e-14 * k) || (v1ok && fabs(n1 - x1) > 1e-14 * k);
+    x0 = v0ok ? n0 : 0.0;
+    x1 = v1ok ? n1 : 0.0;
+    if (!__any_sync(0xffffffffu, moved)) { ++it; break; }
+  }
+  if (v0ok) X[e0] = x0;
+  if (v1ok) X[e1] = x1;
+  // tr(X A) = sum_{a,b} X[a][b] A[b][a]
+  double tr = (v0ok ? x0 * A[c0 * k + r0] : 0.0) + (v1ok ? x1 * A[c1 * k + r1] : 0.0);
+  tr = warp_sum(tr);
+  if (lane == 0) *iters = it;
+  return tr;
+}
+
+__device__ double polar_ns(const double* A, double* X, double* Y, double* T, int k, int* flag,
+                           double* red, int* iters) {
+  __shared__ double s_tr;
+  if (k <= 8) {
+    if (threadIdx.x < 32) {
+      const double tr = polar_ns_small(A, X, k, iters);
+      if (threadIdx.x == 0) s_tr = tr;
+    }
+    __syncthreads();
+    return s_tr;
+  }
+  const int kk = k * k, t = threadIdx.x;
+  double s = 0.0;
+  for (int e = t; e < kk; e += blockDim.x) s += A[e] * A[e];
+  s = block_sum(s, red);
+  const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
+  for (int e = t; e < kk; e += blockDim.x) X[(e % k) * k + e / k] = A[e] * inv;  // A^T
+  __syncthreads();
+  int it = 0;
+  for (; it < 100; ++it) {
+    for (int e = t; e < kk; e += blockDim.x) {            // Y = X^T X
+      const int a = e / k, b = e % k;
+      double v = 0.0;
+      for (int l = 0; l < k; ++l) v += X[l * k + a] * X[l * k + b];
+      Y[e] = v;
+    }
+    __syncthreads();
+    if (t == 0) *flag = 0;
+    for (int e = t; e < kk; e += blockDim.x) {            // T = X Y
+      const int a = e / k, b = e % k;
+      double v = 0.0;
+      for (int l = 0; l < k; ++l) v += X[a * k + l] * Y[l * k + b];
+      T[e] = v;
+    }
+    __syncthreads();
+    for (int e = t; e < kk; e += blockDim.x) {
+      const double xn = 1.5 * X[e] - 0.5 * T[e];
+      if (fabs(xn - X[e]) > 1e-14 * k) *flag = 1;
+      X[e] = xn;
+    }
+    __syncthreads();
+    const bool more = *flag != 0;
+    __syncthreads();
+    if (!more) { ++it; break; }
+  }
+  double tr = 0.0;                                        // tr(X A)
+  for (int e = t; e < kk; e += blockDim.x) {
+    const int a = e / k, b = e % k;
+    tr += X[a * k + b] * A[b * k + a];
+  }
+  tr = block_sum(tr, red);
+  if (t == 0) *iters = it;
+  __syncthreads();
+  return tr;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// CTA 0 accumulates ns between stamps: slot s gets (now - previous stamp)
+#define TSTAMP(s)                                                      \
+  do {                                                                 \
+    if (p.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {               \
+      const unsigned long long _n = gtimer();                          \
+      if ((s) != 0) p.tdbg[(s)] += _n - t_prev;                        \
+      t_prev = _n;                                                     \
+    }                                                                  \
+  } while (0)
 
 template <int KMAX>
 __global__ void __launch_bounds__(kDiscThreads)
 discretize_kernel(DiscParams p) {
+  unsigned long long t_prev = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int k = p.k;
+  const int k = p.k, kk = k * k;
   const int G = p.groups;
-  // phase-A carve
+  const int nb = gridDim.x;
+  // persistent: scoring rotation (f32) and prototype rotation (f64)
   float* sR = reinterpret_cast<float*>(smraw);
-  double* acc = reinterpret_cast<double*>(smraw + align_dev(k * k * 4));
-  float* tile = reinterpret_cast<float*>(reinterpret_cast<unsigned char*>(acc) + align_dev((size_t)G * k * k * 8));
-  int* tlab = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(tile) + align_dev((size_t)kDiscThreads * k * 4));
+  double* sRp = reinterpret_cast<double*>(smraw + align_dev((size_t)kk * 4));
+  unsigned char* dyn = smraw + align_dev((size_t)kk * 4) + align_dev((size_t)kk * 8);
+  // phase-A view
+  double* acc = reinterpret_cast<double*>(dyn);
+  float* tile = reinterpret_cast<float*>(dyn + align_dev((size_t)G * kk * 8));
+  int* tlab = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(tile) +
+                                     align_dev((size_t)kDiscThreads * k * 4));
   int* cnt = tlab + kDiscThreads;
-  // phase-B/C carve (CTA 0 only; aliases acc/tile)
-  double* M = acc;
-  double* Vm = M + k * k;
-  double* sig = Vm + k * k;
-  __shared__ int s_flag;
-  __shared__ double s_red[64];
+  // phase-B view (aliases phase A)
+  double* M = reinterpret_cast<double*>(dyn);
+  double* X = M + kk;
+  double* Y = X + kk;
+  double* T = Y + kk;
+  long long* sizes = reinterpret_cast<long long*>(T + kk);
+  __shared__ double rsum[kDiscThreads];
+  __shared__ long long rcnt[kDiscThreads];
+  __shared__ double sv[kDiscThreads];
+  __shared__ long long si[kDiscThreads];
+  __shared__ int sl[kDiscThreads];
+  __shared__ double red[32];
+  __shared__ int s_flag, s_zero;
 
   const bool cta0 = blockIdx.x == 0;
+  const Rows rows = my_rows(p.n);
+  int buf = 0;                 // partial-buffer parity (advances per barrier)
+  double final_obj[2] = {0.0, 0.0};
+  int final_rounds[2] = {0, 0};
+  double final_conv[2] = {0.0, 0.0};
+  int empties_left[2] = {0, 0};
+
   for (int run = 0; run < 2; ++run) {
-    // ---- initial rotation
+    // ---------------------------------------------------- initial rotation
     if (run == 0) {
-      if (cta0)
-        for (int e = threadIdx.x; e < k * k; e += blockDim.x) p.Rg[e] = (e / k == e % k) ? 1.0 : 0.0;
+      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (e / k == e % k) ? 1.f : 0.f;
+      if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = (e / k == e % k) ? 1.0 : 0.0;
     } else {
-      // prototype rotation (engine.py:209-218): R[:,0] = q~[0]; greedy min-acc rows
-      if (cta0 && threadIdx.x == 0) {
+      // prototype rotation (engine.py:209-218): R[:,0] = q~[0]; greedy rows
+      if (threadIdx.x == 0) {
         double q[KMAX], nrm;
         load_row<KMAX>(p, 0, q, nrm);
-        for (int l = 0; l < k; ++l) p.Rg[l * k + 0] = q[l];
+        for (int l = 0; l < k; ++l) sRp[l * k] = q[l];
       }
-      const int64_t rpb = ceil_div(p.n, gridDim.x);
-      const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = lmin(p.n, r0 + rpb);
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) p.proto_acc[i] = 0.0;
-      grid.sync();
+      for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) p.proto_acc[i] = 0.0;
+      __syncthreads();
+      TSTAMP(0);
       for (int j = 1; j < k; ++j) {
-        double best = INFINITY;
-        int64_t bi = -1;
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        double best = 0.0;
+        long long bi = -1;
+        for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) {
           double q[KMAX], nrm;
           load_row<KMAX>(p, i, q, nrm);
           double d = 0.0;
 #pragma unroll
           for (int l = 0; l < KMAX; ++l)
-            if (l < k) d += q[l] * p.Rg[l * k + (j - 1)];
+            if (l < k) d += q[l] * sRp[l * k + (j - 1)];
           const double a = p.proto_acc[i] + fabs(d);
           p.proto_acc[i] = a;
           if (bi < 0 || a < best) { best = a; bi = i; }
         }
-        // block first-min (value asc, index asc)
-        __shared__ double bv[kDiscThreads];
-        __shared__ long long bx[kDiscThreads];
-        bv[threadIdx.x] = best;
-        bx[threadIdx.x] = bi;
+        double* part = p.part_arg + (size_t)buf * nb * 3;
+        block_arg(best, bi, 0, false, part, sv, si, sl);
+        grid.sync();
+        TSTAMP(5);
+        double v;
+        long long idx;
+        int lab;
+        reduce_arg(part, nb, false, v, idx, lab, sv, si, sl);
+        if (threadIdx.x == 0) {
+          double q[KMAX], nrm;
+          load_row<KMAX>(p, idx < 0 ? 0 : idx, q, nrm);
+          for (int l = 0; l < k; ++l) sRp[l * k + j] = q[l];
+        }
+        buf ^= 1;
         __syncthreads();
-        for (int s = kDiscThreads / 2; s > 0; s >>= 1) {
-          if (threadIdx.x < s) {
-            double v2 = bv[threadIdx.x + s];
-            long long i2 = bx[threadIdx.x + s];
-            bool take = i2 >= 0 && (bx[threadIdx.x] < 0 || v2 < bv[threadIdx.x] ||
-                                    (v2 == bv[threadIdx.x] && i2 < bx[threadIdx.x]));
-            if (take) { bv[threadIdx.x] = v2; bx[threadIdx.x] = i2; }
+      }
+      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (float)sRp[e];
+      if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = sRp[e];
+    }
+    __syncthreads();
+
+    // ---------------------------------------------------------- rounds
+    double obj_prev = 0.0;
+    bool conv = false;
+    int rounds = 0;
+    for (int it = 0; it < p.max_iter; ++it) {
+      TSTAMP(0);
+      phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, true,
+                             (run == 0 && it == 0) ? &s_zero : nullptr);
+      if (run == 0 && it == 0 && threadIdx.x == 0)   // fold the zero-row count into the
+        p.part_cnt[((size_t)(buf ^ 1) * nb + blockIdx.x) * k] = s_zero;  // idle buffer
+      TSTAMP(6);
+      grid.sync();
+      TSTAMP(1);
+      if (run == 0 && it == 0 && cta0 && threadIdx.x == 0) {   // zero rows (engine.py:239-242)
+        long long z = 0;
+        for (int b = 0; b < nb; ++b) z += p.part_cnt[((size_t)(buf ^ 1) * nb + b) * k];
+        p.info[5] = (double)z;
+      }
+      reduce_partials(p, buf, M, sizes, rsum, rcnt);
+      TSTAMP(2);
+      buf ^= 1;
+      int nempty = 0;
+      for (int c = 0; c < k; ++c) nempty += sizes[c] == 0;
+      if (nempty > 0 && k >= 2) {
+        // _reseed_empty_columns (engine.py:162-180): every CTA tracks sizes
+        for (int c = 0; c < k; ++c) {
+          if (sizes[c] != 0) continue;
+          double bestm = 0.0;
+          long long bi = -1;
+          int blab = 0;
+          for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) {
+            const int l = p.labels[i];
+            if (sizes[l] >= 2) {
+              const double m = p.margin[i];
+              if (bi < 0 || m > bestm) { bestm = m; bi = i; blab = l; }
+            }
+          }
+          double* part = p.part_arg + (size_t)buf * nb * 3;
+          block_arg(bestm, bi, blab, true, part, sv, si, sl);
+          grid.sync();
+          double v;
+          long long idx;
+          int old;
+          reduce_arg(part, nb, true, v, idx, old, sv, si, sl);
+          buf ^= 1;
+          if (idx < 0) break;                          // no movable node left
+          if (threadIdx.x == 0) {
+            sizes[old] -= 1;
+            sizes[c] += 1;
+            if (idx >= rows.r0 && idx < rows.r1) p.labels[idx] = c;   // owner CTA
           }
           __syncthreads();
         }
-        if (threadIdx.x == 0) {
-          p.part_arg[blockIdx.x * 2] = bv[0];
-          p.part_arg[blockIdx.x * 2 + 1] = (double)bx[0];
-        }
+        phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, false, nullptr);
         grid.sync();
-        if (cta0) {
-          double v;
-          long long idx;
-          cta_reduce_arg(p.part_arg, gridDim.x, false, v, idx);
-          if (threadIdx.x == 0) {
-            double q[KMAX], nrm;
-            load_row<KMAX>(p, idx < 0 ? 0 : idx, q, nrm);
-            for (int l = 0; l < k; ++l) p.Rg[l * k + j] = q[l];
-          }
-        }
-        grid.sync();
+        reduce_partials(p, buf, M, sizes, rsum, rcnt);
+        buf ^= 1;
       }
-    }
-    if (cta0 && threadIdx.x == 0) {
-      p.ctrl[C_CONV] = 0;
-      p.ctrl[C_STOP] = 0;
-      if (run == 0) p.ctrl[C_ZERO] = 0;
-    }
-    grid.sync();
-
-    int rounds = 0;
-    for (int it = 0; it < p.max_iter; ++it) {
-      for (int e = threadIdx.x; e < k * k; e += blockDim.x) sR[e] = (float)p.Rg[e];
+      // Y~ = Y / size, polar factor and objective
+      for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+        const long long sz = sizes[e / k];
+        M[e] = sz > 0 ? M[e] / (double)sz : 0.0;
+      }
       __syncthreads();
-      phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, true,
-                             (run == 0 && it == 0) ? &s_flag : nullptr);
-      grid.sync();
-      if (cta0) {
-        reduce_m(p, M);
-        if (threadIdx.x == 0) {
-          int ne = 0;
-          for (int c = 0; c < k; ++c) ne += p.counts[c] == 0;
-          p.ctrl[C_NEMPTY] = ne;
-        }
-      }
-      grid.sync();
-      const int nempty = (int)p.ctrl[C_NEMPTY];
-      if (nempty > 0 && k >= 2) {
-        // _reseed_empty_columns (engine.py:162-180)
-        for (int c = 0; c < k; ++c) {
-          if (p.counts[c] != 0) continue;   // counts is uniform across CTAs here
-          partial_argmax_movable(p, s_red);
-          grid.sync();
-          double vmax = 0.0;
-          long long idx = -1;
-          if (cta0) cta_reduce_arg(p.part_arg, gridDim.x, true, vmax, idx);
-          if (cta0 && threadIdx.x == 0) {
-            p.ctrl[C_ARGIDX] = (double)idx;
-            if (idx >= 0) {
-              const int old = p.labels[idx];
-              p.labels[idx] = c;
-              p.counts[old] -= 1;
-              p.counts[c] += 1;
-            }
-          }
-          grid.sync();
-          if (p.ctrl[C_ARGIDX] < 0) break;  // no movable node left
-        }
-        phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, false, nullptr);
-        grid.sync();
-        if (cta0) reduce_m(p, M);
-      }
-      if (cta0) {
-        // Y~ = Y / size ; SVD(Y~^T Q~)
-        for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-          const int64_t sz = p.counts[e / k];
-          M[e] = sz > 0 ? M[e] / (double)sz : 0.0;
-        }
-        __syncthreads();
-        jacobi_svd(M, Vm, sig, k, &s_flag);
-        if (threadIdx.x == 0) {
-          double ssum = 0;
-          for (int j = 0; j < k; ++j) ssum += sig[j];
-          const double obj = (double)p.n - 2.0 * ssum;
-          p.info[8 + run * p.max_iter + it] = obj;
-          const bool conv = it >= 1 && fabs(obj - p.ctrl[C_OBJ_PREV]) < p.tol;
-          p.ctrl[C_OBJ_PREV] = obj;
-          p.ctrl[C_CONV] = conv ? 1.0 : 0.0;
-        }
-        __syncthreads();
-        // keep R = the rotation that produced the final scores when the run
-        // ends without converging (last round)
-        if (p.ctrl[C_CONV] == 0.0 && it + 1 < p.max_iter) {
-          // R = V U^T with U = A/sigma (columns)
-          for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-            const int a = e / k, b = e % k;
-            double s = 0;
-            for (int j = 0; j < k; ++j)
-              if (sig[j] > 0) s += Vm[a * k + j] * (M[b * k + j] / sig[j]);
-            p.Rg[e] = s;
-          }
-        }
-      }
-      grid.sync();
+      TSTAMP(3);
+      int ns_it = 0;
+      const double ssum = polar_ns(M, X, Y, T, k, &s_flag, red, &s_flag);
+      ns_it = s_flag;
+      if (p.tdbg && cta0 && threadIdx.x == 0) p.tdbg[7] += ns_it;
+      TSTAMP(4);
+      const double obj = (double)p.n - 2.0 * ssum;
+      if (cta0 && threadIdx.x == 0) p.info[8 + run * p.max_iter + it] = obj;
+      conv = it >= 1 && fabs(obj - obj_prev) < p.tol;
+      obj_prev = obj;
       rounds = it + 1;
-      if (p.ctrl[C_CONV] != 0.0) break;
-    }
-    // finish the run: publish its final rotation, then its summary
-    if (cta0)
-      for (int e = threadIdx.x; e < k * k; e += blockDim.x)
-        p.info[8 + 2 * p.max_iter + run * k * k + e] = p.Rg[e];
-    if (cta0 && threadIdx.x == 0) {
-      p.info[6 + run] = rounds;
-      const double obj = p.info[8 + run * p.max_iter + rounds - 1];
-      if (run == 0) {
-        p.info[0] = obj; p.info[1] = rounds; p.info[2] = p.ctrl[C_CONV]; p.info[3] = 0;
+      if (conv || it + 1 == p.max_iter) {
         int ne = 0;
-        for (int c = 0; c < k; ++c) ne += p.counts[c] == 0;
-        p.info[4] = ne;
-      } else if (obj < p.info[0] - 1e-15) {
-        p.info[0] = obj; p.info[1] = rounds; p.info[2] = p.ctrl[C_CONV]; p.info[3] = 1;
-        int ne = 0;
-        for (int c = 0; c < k; ++c) ne += p.counts[c] == 0;
-        p.info[4] = ne;
+        for (int c = 0; c < k; ++c) ne += sizes[c] == 0;
+        empties_left[run] = ne;
+        break;
       }
-      if (run == 0) p.info[5] = p.ctrl[C_ZERO];
+      // next rotation R = V U^T (engine.py:205)
+      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (float)X[e];
+      if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = X[e];
+      __syncthreads();
     }
-    {
-      const int64_t rpb = ceil_div(p.n, gridDim.x);
-      const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = lmin(p.n, r0 + rpb);
-      if (run == 0)
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) p.labels_run0[i] = p.labels[i];
+    final_obj[run] = obj_prev;
+    final_rounds[run] = rounds;
+    final_conv[run] = conv ? 1.0 : 0.0;
+    // publish the rotation that produced this run's final scores
+    if (cta0) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < kk; e += blockDim.x)
+        p.info[8 + 2 * p.max_iter + run * kk + e] = p.Rg[e];
     }
-    grid.sync();
+    if (run == 0)
+      for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x)
+        p.labels_run0[i] = p.labels[i];
+    __syncthreads();
   }
-  // winner: identity unless the prototype run won
-  if (p.info[3] == 0.0) {
-    const int64_t rpb = ceil_div(p.n, gridDim.x);
-    const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = lmin(p.n, r0 + rpb);
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) p.labels[i] = p.labels_run0[i];
+  // identity wins unless the prototype run is lower by more than 1e-15
+  const int win = final_obj[1] < final_obj[0] - 1e-15 ? 1 : 0;
+  if (cta0 && threadIdx.x == 0) {
+    p.info[0] = final_obj[win];
+    p.info[1] = final_rounds[win];
+    p.info[2] = final_conv[win];
+    p.info[3] = win;
+    p.info[4] = empties_left[win];
+    p.info[6] = final_rounds[0];
+    p.info[7] = final_rounds[1];
   }
+  if (win == 0)
+    for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x)
+      p.labels[i] = p.labels_run0[i];
 }
 
 }  // namespace ancka
@@ -537,10 +612,12 @@ static int disc_groups(int k) {
 }
 
 static size_t disc_smem(int k, int G) {
-  size_t a = align_dev((size_t)k * k * 4) + align_dev((size_t)G * k * k * 8) +
-             align_dev((size_t)kDiscThreads * k * 4) + (kDiscThreads + k) * 4;
-  size_t b = align_dev((size_t)k * k * 4) + (2 * (size_t)k * k + k) * 8;
-  return std::max(a, b) + 64;
+  const size_t kk = (size_t)k * k;
+  const size_t fixed = align_dev(kk * 4) + align_dev(kk * 8);
+  const size_t a = align_dev((size_t)G * kk * 8) + align_dev((size_t)kDiscThreads * k * 4) +
+                   (kDiscThreads + (size_t)G * k) * 4;
+  const size_t b = 4 * kk * 8 + (size_t)k * 8;
+  return fixed + std::max(a, b) + 64;
 }
 
 static int disc_grid_cap() { return 4 * kNumSMs; }
@@ -552,12 +629,10 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   cv.take<int32_t>(n);              // labels_run0
   cv.take<float>(n);                // margin
   cv.take<double>(n);               // proto_acc
-  cv.take<double>((size_t)grid * k * k);
-  cv.take<int64_t>((size_t)grid * k);
-  cv.take<double>((size_t)grid * 2);
+  cv.take<double>((size_t)2 * grid * k * k);
+  cv.take<int64_t>((size_t)2 * grid * k);
+  cv.take<double>((size_t)2 * grid * 3);
   cv.take<double>((size_t)k * k);
-  cv.take<double>(C_NCTRL);
-  cv.take<int64_t>(k);
   return cv.used;
 }
 
@@ -572,8 +647,9 @@ static int launch_disc(DiscParams& p, cudaStream_t st) {
   int dev = 0, sms = 0;
   ANCKA_CUDA(cudaGetDevice(&dev));
   ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // rows per CTA: enough work per phase to amortise the grid barrier
-  static const int64_t min_rows = getenv("ANCKA_DISC_ROWS") ? atoll(getenv("ANCKA_DISC_ROWS")) : 2048;
+  // rows per CTA (tunable): enough work per phase to amortise the grid barrier
+  static const int64_t min_rows =
+      getenv("ANCKA_DISC_ROWS") ? atoll(getenv("ANCKA_DISC_ROWS")) : kDiscThreads;
   int64_t want = ceil_div(p.n, std::max<int64_t>(kDiscThreads, min_rows));
   int64_t grid = std::min(want, std::min((int64_t)per_sm * sms, (int64_t)disc_grid_cap()));
   if (grid < 1) grid = 1;
@@ -597,17 +673,16 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.labels_run0 = cv.take<int32_t>(n);
   p.margin = cv.take<float>(n);
   p.proto_acc = cv.take<double>(n);
-  p.part_m = cv.take<double>((size_t)grid * k * k);
-  p.part_cnt = cv.take<int64_t>((size_t)grid * k);
-  p.part_arg = cv.take<double>((size_t)grid * 2);
+  p.part_m = cv.take<double>((size_t)2 * grid * k * k);
+  p.part_cnt = cv.take<int64_t>((size_t)2 * grid * k);
+  p.part_arg = cv.take<double>((size_t)2 * grid * 3);
   p.Rg = cv.take<double>((size_t)k * k);
-  p.ctrl = cv.take<double>(C_NCTRL);
-  p.counts = cv.take<int64_t>(k);
   p.info = info;
+  p.tdbg = getenv("ANCKA_DISC_TIMING") ? (unsigned long long*)(info + 8 + 2 * (size_t)max_iter + 2 * (size_t)k * k) : nullptr;
   p.groups = disc_groups(k);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize: workspace too small");
   auto st = as_stream(stream);
-  ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k), st));
+  ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 8 : 0)), st));
   if (k <= 8) return launch_disc<8>(p, st);
   if (k <= 16) return launch_disc<16>(p, st);
   if (k <= 32) return launch_disc<32>(p, st);

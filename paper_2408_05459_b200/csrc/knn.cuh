@@ -13,4 +13,7 @@ int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int 
 size_t knn_tc_workspace(int64_t n, int64_t d, int K);
 int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* ids, double* scores,
            void* ws, size_t wsb, cudaStream_t st, bool fp8);
+int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t n,
+               int64_t d, int K, int32_t* ids, double* scores, void* ws, size_t wsb,
+               cudaStream_t st, bool fp8);
 }  // namespace ancka

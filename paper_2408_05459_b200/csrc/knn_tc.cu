@@ -463,6 +463,62 @@ static int launch_tc(const CUtensorMap& ma, const CUtensorMap& mb, const TcParam
   return ANCKA_OK;
 }
 
+// CSR X -> zero-filled padded fp8/bf16 rows + exact squared norms (warp per row)
+template <bool FP8>
+__global__ void knn_tc_prep_csr_kernel(const int64_t* __restrict__ indptr,
+                                       const int32_t* __restrict__ indices,
+                                       const double* __restrict__ data, int64_t n, int64_t n_pad,
+                                       int64_t d_pad, void* __restrict__ xq,
+                                       uint32_t* __restrict__ a_norm, float* __restrict__ inv_sqrt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n_pad; r += nwarps) {
+    double s = 0.0;
+    if (r < n) {
+      for (int64_t q = indptr[r] + lane; q < indptr[r + 1]; q += 32) {
+        const double v = data[q];
+        const int64_t c = indices[q];
+        s += v * v;
+        if (FP8) reinterpret_cast<__nv_fp8_e4m3*>(xq)[r * d_pad + c] = __nv_fp8_e4m3((float)v);
+        else reinterpret_cast<__nv_bfloat16*>(xq)[r * d_pad + c] = __float2bfloat16_rn((float)v);
+      }
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      a_norm[r] = (uint32_t)s;
+      inv_sqrt[r] = s > 0 ? (float)(1.0 / sqrt(s)) : 0.f;
+    }
+  }
+}
+
+static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, const TcLayout& L,
+                       int64_t n, int K, int32_t* ids, double* scores, cudaStream_t st, bool fp8);
+
+int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t n,
+               int64_t d, int K, int32_t* ids, double* scores, void* ws, size_t wsb,
+               cudaStream_t st, bool fp8) {
+  ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
+  ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
+  TcLayout L = tc_layout(n, d, fp8);
+  Carver cv(ws, wsb);
+  void* xq;
+  uint32_t* an;
+  float* isq;
+  int* rb;
+  int2* part;
+  carve_tc(cv, L, n, K, &xq, &an, &isq, &rb, &part);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_tc: workspace too small");
+  ANCKA_CUDA(cudaMemsetAsync(xq, 0, (size_t)L.n_pad * L.d_pad * (fp8 ? 1 : 2), st));
+  const int pg = (int)std::min<int64_t>(ceil_div(L.n_pad * 32, 256), 16 * kNumSMs);
+  if (fp8)
+    knn_tc_prep_csr_kernel<true><<<pg, 256, 0, st>>>(indptr, indices, data, n, L.n_pad, L.d_pad, xq, an, isq);
+  else
+    knn_tc_prep_csr_kernel<false><<<pg, 256, 0, st>>>(indptr, indices, data, n, L.n_pad, L.d_pad, xq, an, isq);
+  ANCKA_LAUNCHED();
+  return knn_tc_main(xq, an, isq, rb, part, L, n, K, ids, scores, st, fp8);
+}
+
 int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* ids, double* scores,
            void* ws, size_t wsb, cudaStream_t st, bool fp8) {
   ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
@@ -482,6 +538,11 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   else
     knn_tc_prep_kernel<false><<<pg, 256, 0, st>>>(X, n, d, ldx, L.n_pad, L.d_pad, xq, an, isq);
   ANCKA_LAUNCHED();
+  return knn_tc_main(xq, an, isq, rb, part, L, n, K, ids, scores, st, fp8);
+}
+
+static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, const TcLayout& L,
+                       int64_t n, int K, int32_t* ids, double* scores, cudaStream_t st, bool fp8) {
   CUtensorMap ma, mb;
   ANCKA_TRY(make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
   ANCKA_TRY(make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));

@@ -105,10 +105,31 @@ chol_kernel(const double* __restrict__ partial, int nblocks, int c, float* __res
   double* X = sm + npairs;      // packed upper inverse, npairs
   __shared__ double s_minratio;
   __shared__ int s_bad;
-  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-    double s = 0.0;
-    for (int b = 0; b < nblocks; ++b) s += partial[(int64_t)b * npairs + p];
-    R[p] = s;
+  __shared__ double gsum[256];
+  if (npairs >= (int)blockDim.x / 2) {
+    for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+      double s0 = 0.0, s1 = 0.0;
+      int b = 0;
+      for (; b + 1 < nblocks; b += 2) {
+        s0 += partial[(int64_t)b * npairs + p];
+        s1 += partial[(int64_t)(b + 1) * npairs + p];
+      }
+      if (b < nblocks) s0 += partial[(int64_t)b * npairs + p];
+      R[p] = s0 + s1;
+    }
+  } else {  // G groups of threads sum interleaved block subsets; fixed-order combine
+    const int G = blockDim.x / npairs, g = threadIdx.x / npairs, p = threadIdx.x % npairs;
+    if (g < G) {
+      double s = 0.0;
+      for (int b = g; b < nblocks; b += G) s += partial[(int64_t)b * npairs + p];
+      gsum[g * npairs + p] = s;
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < npairs) {
+      double s = 0.0;
+      for (int gg = 0; gg < G; ++gg) s += gsum[gg * npairs + threadIdx.x];
+      R[threadIdx.x] = s;
+    }
   }
   if (threadIdx.x == 0) { s_minratio = 1.0; s_bad = 0; }
   __syncthreads();

@@ -145,7 +145,14 @@ spmm_piece_kernel(SpmmArgs<float> a, ancka_row_split sp) {
   const int64_t pc = gid / a.nchunk;
   if (pc >= sp.n_pieces) return;
   const int64_t coloff = (int64_t)(gid - pc * a.nchunk) * 4;
-  const SegArgs<float>& g = sp.piece_seg[pc] ? a.k : a.s;
+  // select scalar fields (not a reference into the parameter struct, which
+  // would force a local-memory copy of the kernel parameters)
+  const bool kseg = sp.piece_seg[pc] != 0;
+  SegArgs<float> g;
+  g.colidx = kseg ? a.k.colidx : a.s.colidx;
+  g.values = kseg ? a.k.values : a.s.values;
+  g.src = kseg ? a.k.src : a.s.src;
+  g.ld = kseg ? a.k.ld : a.s.ld;
   const int64_t e = sp.piece_end[pc];
   const float* src = g.src + coloff;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);

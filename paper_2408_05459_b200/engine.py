@@ -310,7 +310,7 @@ class PreparedNetwork:
 
     net: AttributedNetwork
     K: int
-    x_dev: torch.Tensor
+    x_dev: object           # knn.DeviceAttributes
     x_level: int            # 2 fp8-exact, 1 bf16-exact, 0 general (knn.integer_exact)
     factors: StructureFactors
     cache_path: object = None
@@ -336,7 +336,7 @@ def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir
     if knn_cache_dir is not None:
         cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
     level = integer_exact(net.attributes) if K <= 32 else 0
-    return PreparedNetwork(net, K, attributes_to_device(net.attributes), level,
+    return PreparedNetwork(net, K, attributes_to_device(net.attributes, level), level,
                            StructureFactors(net), cache_path)
 
 
@@ -434,10 +434,18 @@ class _Loop:
                 self._block(start, steps)          # warm-up
                 torch.cuda.current_stream().synchronize()
                 self.Q[start].copy_(self.Qsave)    # undo the warm-up
+                # manual capture on a side stream: torch.cuda.graph() would run
+                # gc.collect() + empty_cache() on every capture
                 g = torch.cuda.CUDAGraph()
                 c0 = _lib.load().ancka_launch_count()
-                with torch.cuda.graph(g):
+                cur = torch.cuda.current_stream()
+                side = torch.cuda.Stream()
+                side.wait_stream(cur)
+                with torch.cuda.stream(side):
+                    g.capture_begin()
                     self._block(start, steps)
+                    g.capture_end()
+                cur.wait_stream(side)
                 nodes = _lib.load().ancka_launch_count() - c0
                 self.graphs[start] = (g, nodes)
                 self.captured += nodes             # captured, not executed

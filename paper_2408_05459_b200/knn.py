@@ -122,32 +122,67 @@ def integer_exact(X) -> int:
     return 2 if vmax <= 16 else 1
 
 
-def attributes_to_device(X) -> torch.Tensor:
-    """n x d attributes -> dense f64 on the device (CSR densified on the GPU)."""
-    if sp.issparse(X):
-        x = sp.csr_matrix(X)
-        t = torch.sparse_csr_tensor(torch.from_numpy(x.indptr.astype(np.int64)),
-                                    torch.from_numpy(x.indices.astype(np.int64)),
-                                    torch.from_numpy(x.data.astype(np.float64)), size=x.shape)
-        return t.to(dev()).to_dense().contiguous()
-    return torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(dev())
+class DeviceAttributes:
+    """Attributes resident in HBM: CSR (integer-exact sparse input, fed to the
+    tensor-core kernel as is) or dense f64."""
+
+    def __init__(self, X, level: int):
+        self.shape = X.shape
+        self.level = level
+        d = dev()
+        if sp.issparse(X) and level > 0:
+            x = sp.csr_matrix(X)
+            self.indptr = torch.from_numpy(x.indptr.astype(np.int64)).to(d)
+            self.indices = torch.from_numpy(x.indices.astype(np.int32)).to(d)
+            self.data = torch.from_numpy(x.data.astype(np.float64)).to(d)
+            self.dense = None
+        elif sp.issparse(X):
+            x = sp.csr_matrix(X)
+            t = torch.sparse_csr_tensor(torch.from_numpy(x.indptr.astype(np.int64)),
+                                        torch.from_numpy(x.indices.astype(np.int64)),
+                                        torch.from_numpy(x.data.astype(np.float64)), size=x.shape)
+            self.dense = t.to(d).to_dense().contiguous()
+        else:
+            self.dense = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(d)
+
+
+def attributes_to_device(X, level: int = 0) -> DeviceAttributes:
+    return DeviceAttributes(X, level)
 
 
 def knn_search_exact_device(X, K: int, integer: int | None = None):
-    """Device exact KNN: returns (ids int32 (n,K), scores f64 (n,K)) tensors."""
+    """Device exact KNN: returns (ids int32 (n,K), scores f64 (n,K)) tensors.
+    X: numpy/scipy host matrix, DeviceAttributes, or a dense f64 CUDA tensor."""
     _lib.require_device()
     n, d = X.shape
     if K >= n:
         raise NetworkError(f"K={K} must be smaller than n={n}")
     if integer is None:
-        integer = integer_exact(X) if (TENSOR_CORE_KNN and K <= 32) else 0
-    xd = X if isinstance(X, torch.Tensor) else attributes_to_device(X)
-    ids = torch.empty((n, K), dtype=torch.int32, device=xd.device)
-    scores = torch.empty((n, K), dtype=torch.float64, device=xd.device)
+        integer = (X.level if isinstance(X, DeviceAttributes) else
+                   0 if isinstance(X, torch.Tensor) else integer_exact(X))
+    if not (TENSOR_CORE_KNN and K <= 32):
+        integer = 0
+    if isinstance(X, torch.Tensor):
+        xa = None
+        xd = X
+    else:
+        xa = X if isinstance(X, DeviceAttributes) else DeviceAttributes(X, integer)
+        xd = xa.dense
+        if xd is None and integer == 0:  # CSR held for the TC path, f64 path requested
+            xd = torch.sparse_csr_tensor(xa.indptr, xa.indices.long(), xa.data,
+                                         size=xa.shape).to_dense()
+    dv = dev()
+    ids = torch.empty((n, K), dtype=torch.int32, device=dv)
+    scores = torch.empty((n, K), dtype=torch.float64, device=dv)
     wsb = _lib.load().ancka_knn_workspace_size(n, d, K, int(integer))
     ws = WORKSPACE.get("knn", wsb)
-    _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer),
-              ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    if xd is None:
+        _lib.call("ancka_knn_exact_csr", xa.indptr.data_ptr(), xa.indices.data_ptr(),
+                  xa.data.data_ptr(), n, d, K, int(integer), ids.data_ptr(), scores.data_ptr(),
+                  ws.data_ptr(), ws.numel(), _lib.stream())
+    else:
+        _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer),
+                  ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     return ids, scores
 
 

@@ -1,0 +1,36 @@
+"""Per-phase ns inside the discretize kernel (ANCKA_DISC_TIMING=1)."""
+import os
+import sys
+import warnings
+from pathlib import Path
+
+os.environ["ANCKA_DISC_TIMING"] = "1"
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+warnings.simplefilter("ignore")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2408_05459_b200 as ancka  # noqa: E402
+from paper_2408_05459_b200 import engine, synth  # noqa: E402
+
+inst = synth.make("dblp", seed=0)
+net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
+params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
+res = ancka.run_ancka(net, params)
+q = res.state.q_dev
+k = inst.k
+lab = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
+info = torch.zeros(8 + 200 + 2 * k * k + 8, dtype=torch.float64, device=q.device)
+for rep in range(3):
+    info.zero_()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    engine._discretize_device(q, 1, k, 100, 1e-10, lab, info)
+    b.record()
+    b.synchronize()
+    t = info[8 + 200 + 2 * k * k:].cpu().numpy().view(np.uint64)
+    names = ["-", "sync_after_A", "reduce", "-", "polar", "proto_iter", "phaseA", "ns_iters"]
+    inf = info[:8].cpu().numpy()
+    print(f"total {a.elapsed_time(b)*1e3:.0f} us rounds={inf[6]:.0f}+{inf[7]:.0f}",
+          {names[i]: int(t[i]) // 1000 for i in (1, 2, 4, 5, 6)}, "us; NS iterations", int(t[7]))
