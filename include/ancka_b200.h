@@ -162,6 +162,16 @@ int ancka_orth_step_f32(const ancka_operator* op32, const float* Q_prev, float* 
                         float* Z, int64_t ld, int32_t c, double* stats,
                         void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
+/* `steps` consecutive f32 orthogonal steps in ONE cooperative kernel for
+ * narrow blocks (c <= 8, ld == 8): Q0 is the input, the result lands in Q0
+ * if `steps` is even and Q1 if odd.  stats as ancka_orth_step_f32 ([0] is
+ * the last step's ||dQ||_F^2).  Returns ANCKA_ERR_UNSUPPORTED for other
+ * shapes (callers then use ancka_orth_step_f32). */
+size_t ancka_orth_block_workspace_size(const ancka_operator* op);
+int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float* Q1, float* Z, int64_t ld,
+                         int32_t c, int32_t steps, double* stats, void* workspace,
+                         size_t workspace_bytes, ancka_stream_t stream);
+
 /* Thin QR in f64 by classical Gram-Schmidt with re-orthogonalisation
  * (Householder-equivalent Q/|R_jj| for full-rank columns; the reference's
  * rank test engine.py:141-142 is applied by the caller on rdiag).

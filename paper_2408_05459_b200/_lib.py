@@ -63,6 +63,9 @@ _SIGS = {
     "ancka_orth_workspace_size": (c_size_t, [_OP, c_int32]),
     "ancka_orth_step_f32": (c_int32, [_OP, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                       c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_orth_block_workspace_size": (c_size_t, [_OP]),
+    "ancka_orth_block_f32": (c_int32, [_OP, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                       c_int32, c_void_p, c_void_p, c_size_t, c_void_p]),
     "ancka_qr_f64_workspace_size": (c_size_t, [c_int64, c_int32]),
     "ancka_qr_f64": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p, c_size_t,
                                c_void_p]),

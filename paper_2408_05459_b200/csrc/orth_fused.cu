@@ -1,0 +1,442 @@
+// Fused orthogonal iterations for narrow blocks (c <= 8): one cooperative
+// persistent kernel runs `steps` iterations of orthogonal_step
+// (engine.py:130-149) -- the joint-walk SpMM (walk.py:177-190), the Gram
+// matrix, the Cholesky factor R, Q = Z R^-1 and ||Q - Q_prev||_F^2 -- with
+// four grid barriers per step instead of eight kernel launches.  This is the
+// latency-bound regime of the small configurations (Cora, Citeseer, DBLP
+// shapes), where every phase touches only a few MB that sit in L2.
+//
+// One thread owns one row and its 8 (padded) columns: the row's Gram
+// contribution is thread-local, so Z never has to be re-read.  Long rows
+// (KNN hubs) are processed as fixed-size pieces and combined in a fixed
+// order, exactly as the multi-kernel path.  Every CTA reduces the Gram
+// partials and factors the 8 x 8 matrix itself (identical arithmetic), so
+// no extra barrier is needed to broadcast R^-1.  Deterministic throughout.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ancka {
+
+constexpr int kOfThreads = 256;
+constexpr int kC = 8;                       // padded block width
+constexpr int kNP = kC * (kC + 1) / 2;      // Gram upper-triangle entries
+constexpr double kFx = 1125899906842624.0;  // 2^50 fixed-point scale of Gram sums
+constexpr double kFxInv = 1.0 / 1125899906842624.0;
+
+struct OfParams {
+  ancka_operator op;         // f32 operator (by value)
+  float* Q[2];               // ping-pong blocks, n x 8
+  float* Z;                  // n x 8
+  float* T;                  // m x 8 (hypergraph)
+  int c, steps;
+  long long* gram_fx;        // 2 x kNP fixed-point Gram accumulators
+  double* dq_part;           // grid
+  double* stats;             // [0] dq^2 of the last step, [1] min pivot ratio, [2] += bad pivots
+  unsigned long long* tdbg;  // optional phase timers (ANCKA_ORTH_TIMING): stats[4..11]
+};
+
+__device__ __forceinline__ unsigned long long of_timer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define OF_STAMP(s)                                                   \
+  do {                                                                \
+    if (P.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {              \
+      const unsigned long long _n = of_timer();                       \
+      if ((s) >= 0) P.tdbg[(s)] += _n - t_prev;                       \
+      t_prev = _n;                                                    \
+    }                                                                 \
+  } while (0)
+
+__device__ __forceinline__ void f8_load(const float* p, float (&v)[kC]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void f8_store(float* p, const float (&v)[kC]) {
+  reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+  reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+}
+
+// acc += sum_{p in [b, e)} w_p * src[col_p]   (sequential, 2-way unrolled)
+__device__ __forceinline__ void seg8(const int32_t* __restrict__ ci, const float* __restrict__ val,
+                                     const float* __restrict__ src, int64_t b, int64_t e,
+                                     float (&acc)[kC]) {
+  int64_t p = b;
+  for (; p + 2 <= e; p += 2) {
+    const int32_t j0 = __ldg(ci + p), j1 = __ldg(ci + p + 1);
+    const float w0 = val ? __ldg(val + p) : 1.f, w1 = val ? __ldg(val + p + 1) : 1.f;
+    float x0[kC], x1[kC];
+    f8_load(src + (int64_t)j0 * kC, x0);
+    f8_load(src + (int64_t)j1 * kC, x1);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w0, x0[u], acc[u]);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w1, x1[u], acc[u]);
+  }
+  if (p < e) {
+    const int32_t j = __ldg(ci + p);
+    const float w = val ? __ldg(val + p) : 1.f;
+    float x[kC];
+    f8_load(src + (int64_t)j * kC, x);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w, x[u], acc[u]);
+  }
+}
+
+// strided partial sum: lanes of a group of `gw` lanes take nonzeros
+// b + lane, b + lane + gw, ... (the group's partial sums are reduced after)
+__device__ __forceinline__ void seg8_strided(const int32_t* __restrict__ ci,
+                                             const float* __restrict__ val,
+                                             const float* __restrict__ src, int64_t b, int64_t e,
+                                             int lane, int gw, float (&acc)[kC]) {
+  int64_t p = b + lane;
+  for (; p + gw < e; p += 2 * gw) {
+    const int32_t j0 = __ldg(ci + p), j1 = __ldg(ci + p + gw);
+    const float w0 = val ? __ldg(val + p) : 1.f, w1 = val ? __ldg(val + p + gw) : 1.f;
+    float x0[kC], x1[kC];
+    f8_load(src + (int64_t)j0 * kC, x0);
+    f8_load(src + (int64_t)j1 * kC, x1);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w0, x0[u], acc[u]);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w1, x1[u], acc[u]);
+  }
+  if (p < e) {
+    const int32_t j = __ldg(ci + p);
+    const float w = val ? __ldg(val + p) : 1.f;
+    float x[kC];
+    f8_load(src + (int64_t)j * kC, x);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) acc[u] = fmaf(w, x[u], acc[u]);
+  }
+}
+
+// butterfly sum over groups of `gw` lanes (gw a power of two <= 32)
+__device__ __forceinline__ void group_sum(float (&v)[kC], int gw) {
+  for (int o = gw >> 1; o > 0; o >>= 1)
+#pragma unroll
+    for (int u = 0; u < kC; ++u) v[u] += __shfl_xor_sync(0xffffffffu, v[u], o);
+}
+
+__device__ __forceinline__ void gram_add(const float (&z)[kC], double (&g)[kNP]) {
+  int q = 0;
+#pragma unroll
+  for (int a = 0; a < kC; ++a)
+#pragma unroll
+    for (int b = a; b < kC; ++b) g[q++] += (double)(z[a] * z[b]);
+}
+
+// z = mix(s, k) for row i, store, add to the Gram partial
+__device__ __forceinline__ void finish8(const OfParams& P, int64_t i, const float* Qp,
+                                        float (&s)[kC], float (&kk)[kC]) {
+  const ancka_operator& op = P.op;
+  if (op.selfloop[i]) {
+    float x[kC];
+    f8_load(Qp + i * kC, x);
+#pragma unroll
+    for (int u = 0; u < kC; ++u) s[u] += x[u];
+  }
+  const float b = __ldg(static_cast<const float*>(op.beta) + i);
+  const float omb = 1.f - b;
+  float z[kC];
+#pragma unroll
+  for (int u = 0; u < kC; ++u) z[u] = u < P.c ? omb * s[u] + b * kk[u] : 0.f;
+  f8_store(P.Z + i * kC, z);
+}
+
+// deterministic CTA reduction of the per-thread Gram partial -> global slot
+__device__ void block_gram(double (&g)[kNP], double* out, double* red /* 32*kNP */) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < kNP; ++q) {
+    double v = g[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp * kNP + q] = v;
+  }
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  for (int q = threadIdx.x; q < kNP; q += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < nw; ++w) v += red[w * kNP + q];
+    out[q] = v;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pidx(int a, int b) {  // a <= b, packed upper of 8 x 8
+  return a * kC - (a * (a - 1)) / 2 + (b - a);
+}
+
+__global__ void __launch_bounds__(kOfThreads, 4)
+orth_fused_kernel(OfParams P) {
+  cg::grid_group grid = cg::this_grid();
+  const ancka_operator& op = P.op;
+  const bool hyper = op.kind == ANCKA_HYPERGRAPH;
+  // scalar selects (a runtime-selected reference into parameter space would
+  // force a local copy of the whole parameter block)
+  const int64_t* S_rp = hyper ? op.p_v.rowptr : op.p_n.rowptr;
+  const int32_t* S_ci = hyper ? op.p_v.colidx : op.p_n.colidx;
+  const float* Sval = static_cast<const float*>(hyper ? op.p_v.values : op.p_n.values);
+  const int64_t* K_rp = op.p_k.rowptr;
+  const int32_t* K_ci = op.p_k.colidx;
+  const float* Kval = static_cast<const float*>(op.p_k.values);
+  const ancka_row_split& sp = op.split;
+  const int64_t n = op.n;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  const int nb = gridDim.x;
+
+  __shared__ double red[(kOfThreads / 32) * kNP];
+  __shared__ double G[kNP];
+  __shared__ float Rinv[kC * kC];
+  __shared__ double s_stat[2];
+
+  unsigned long long t_prev = 0;
+  for (int step = 0; step < P.steps; ++step) {
+    OF_STAMP(-1);
+    const float* Qp = P.Q[step & 1];
+    float* Qn = P.Q[(step + 1) & 1];
+    const int buf = step & 1;
+    // row groups: 8 lanes per regular row, a whole warp per long row
+    const int lane = threadIdx.x & 31;
+    const int sub = lane & 7;
+    const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
+    const int64_t goct = gtid >> 3, noct = gsz >> 3;
+    // ---- P1: T = P_E Q (hypergraph)
+    if (hyper) {
+      const float* Eval = static_cast<const float*>(op.p_e.values);
+      const int64_t m = op.m;
+      for (int64_t e0 = goct; e0 < ((m + noct - 1) / noct) * noct; e0 += noct) {
+        const int64_t e = e0;
+        float acc[kC] = {};
+        if (e < m) seg8_strided(op.p_e.colidx, Eval, Qp, op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
+                                sub, 8, acc);
+        group_sum(acc, 8);
+        if (e < m && sub == 0) f8_store(P.T + e * kC, acc);
+      }
+      OF_STAMP(0);
+      grid.sync();
+      OF_STAMP(1);
+    }
+    const float* Ssrc = hyper ? P.T : Qp;
+    // ---- P2: rows (Z + Gram): regular rows by 8-lane groups ...
+    const int64_t nround = ((n + noct - 1) / noct) * noct;
+    for (int64_t i = goct; i < nround; i += noct) {
+      const bool live = i < n && !(sp.is_long && sp.is_long[i]);
+      float s[kC] = {}, kk[kC] = {};
+      if (live) {
+        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, 8, s);
+        seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], sub, 8, kk);
+      }
+      group_sum(s, 8);
+      group_sum(kk, 8);
+      if (live && sub == 0) finish8(P, i, Qp, s, kk);
+    }
+    // ... and long rows (KNN hubs) by whole warps
+    const int64_t lround = ((sp.n_long + nwarps - 1) / nwarps) * nwarps;
+    for (int64_t li = gwarp; li < lround; li += nwarps) {
+      const bool live = li < sp.n_long;
+      const int64_t i = live ? sp.long_rows[li] : 0;
+      float s[kC] = {}, kk[kC] = {};
+      if (live) {
+        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], lane, 32, s);
+        seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], lane, 32, kk);
+      }
+      group_sum(s, 32);
+      group_sum(kk, 32);
+      if (live && lane == 0) finish8(P, i, Qp, s, kk);
+    }
+    OF_STAMP(2);
+    grid.sync();
+    // ---- P3: Gram partial of this CTA's rows of Z (lane = row, shuffle sums)
+    {
+      const int warp_in = threadIdx.x >> 5;
+      double gq0 = 0.0, gq1 = 0.0;   // lane owns Gram entries lane and lane + 32
+      const int64_t rows_per_cta = (n + nb - 1) / nb;
+      const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+      const int64_t r1 = lmin(n, r0 + rows_per_cta);
+      for (int64_t base = r0 + warp_in * 32; base < r1; base += (int64_t)blockDim.x) {
+        const int64_t i = base + lane;
+        float z[kC] = {};
+        if (i < r1) f8_load(P.Z + i * kC, z);
+        int q = 0;
+#pragma unroll
+        for (int a = 0; a < kC; ++a)
+#pragma unroll
+          for (int b2 = a; b2 < kC; ++b2, ++q) {
+            float v = z[a] * z[b2];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == q) gq0 += (double)v;
+            if (lane + 32 == q) gq1 += (double)v;
+          }
+      }
+      red[warp_in * kNP + lane] = gq0;
+      if (lane + 32 < kNP) red[warp_in * kNP + lane + 32] = gq1;
+      __syncthreads();
+      for (int q = threadIdx.x; q < kNP; q += blockDim.x) {
+        double v = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w * kNP + q];
+        // 64-bit fixed point: integer sums are order independent, so the
+        // grid-wide Gram is bit-reproducible without a partials pass
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + q),
+                  (unsigned long long)(long long)llrint(v * kFx));
+      }
+      __syncthreads();
+    }
+    OF_STAMP(3);
+    grid.sync();
+    OF_STAMP(4);
+    // ---- P4: every CTA: Gram (fixed-point sums), Cholesky, R^-1 (identical)
+    if (threadIdx.x < kNP) G[threadIdx.x] = (double)P.gram_fx[buf * kNP + threadIdx.x] * kFxInv;
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x < kNP) P.gram_fx[(buf ^ 1) * kNP + threadIdx.x] = 0;
+    if (threadIdx.x == 0) {
+      // Cholesky of the padded 8 x 8 Gram (identity on padding), fully
+      // unrolled so the factor lives in registers
+      double R[kC][kC], X[kC][kC];
+#pragma unroll
+      for (int a2 = 0; a2 < kC; ++a2)
+#pragma unroll
+        for (int b3 = 0; b3 < kC; ++b3)
+          R[a2][b3] = (a2 < P.c && b3 < P.c) ? (a2 <= b3 ? G[pidx(a2, b3)] : 0.0)
+                                             : (a2 == b3 ? 1.0 : 0.0);
+      double minratio = 1.0;
+      int bad = 0;
+#pragma unroll
+      for (int j = 0; j < kC; ++j) {
+        const double gjj = R[j][j];
+        double piv = gjj;
+#pragma unroll
+        for (int l = 0; l < j; ++l) piv -= R[l][j] * R[l][j];
+        const double ratio = gjj > 0 ? piv / gjj : 0.0;
+        if (j < P.c) {
+          minratio = fmin(minratio, ratio);
+          if (!(ratio > 1e-9)) { ++bad; piv = fmax(piv, 1e-30 + 1e-9 * fmax(gjj, 0.0)); }
+        }
+        const double rjj = sqrt(piv);
+        R[j][j] = rjj;
+#pragma unroll
+        for (int q = j + 1; q < kC; ++q) {
+          double v = R[j][q];
+#pragma unroll
+          for (int l = 0; l < j; ++l) v -= R[l][j] * R[l][q];
+          R[j][q] = v / rjj;
+        }
+      }
+#pragma unroll
+      for (int bcol = 0; bcol < kC; ++bcol) {
+#pragma unroll
+        for (int a2 = 0; a2 < kC; ++a2) X[a2][bcol] = 0.0;
+        X[bcol][bcol] = 1.0 / R[bcol][bcol];
+#pragma unroll
+        for (int a2 = bcol - 1; a2 >= 0; --a2) {
+          double v = 0.0;
+#pragma unroll
+          for (int l = a2 + 1; l <= bcol; ++l) v += R[a2][l] * X[l][bcol];
+          X[a2][bcol] = -v / R[a2][a2];
+        }
+      }
+#pragma unroll
+      for (int a2 = 0; a2 < kC; ++a2)
+#pragma unroll
+        for (int b3 = 0; b3 < kC; ++b3)
+          Rinv[a2 * kC + b3] = (a2 <= b3 && b3 < P.c) ? (float)X[a2][b3] : 0.f;
+      s_stat[0] = minratio;
+      s_stat[1] = bad;
+    }
+    __syncthreads();
+    OF_STAMP(5);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      P.stats[1] = fmin(P.stats[1], s_stat[0]);
+      P.stats[2] += s_stat[1];
+    }
+    // ---- P5: Q = Z R^-1 and ||Q - Q_prev||^2
+    double dq = 0.0;
+    for (int64_t i = gtid; i < n; i += gsz) {
+      float z[kC], qo[kC], qv[kC];
+      f8_load(P.Z + i * kC, z);
+      f8_load(Qp + i * kC, qo);
+#pragma unroll
+      for (int b2 = 0; b2 < kC; ++b2) {
+        float v = 0.f;
+#pragma unroll
+        for (int a = 0; a <= b2; ++a) v = fmaf(z[a], Rinv[a * kC + b2], v);
+        qv[b2] = v;
+        const double d = (double)v - (double)qo[b2];
+        dq += d * d;
+      }
+      f8_store(Qn + i * kC, qv);
+    }
+    dq = block_sum(dq, red);
+    if (threadIdx.x == 0) P.dq_part[blockIdx.x] = dq;
+    OF_STAMP(6);
+    grid.sync();
+    OF_STAMP(7);
+  }
+  if (blockIdx.x == 0) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < nb; b += blockDim.x) s += P.dq_part[b];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) P.stats[0] = s;
+  }
+}
+
+}  // namespace ancka
+
+using namespace ancka;
+
+static int of_grid_cap() { return 8 * kNumSMs; }
+
+extern "C" size_t ancka_orth_block_workspace_size(const ancka_operator* op) {
+  Carver cv(nullptr, 0);
+  cv.take<float>(op && op->kind == ANCKA_HYPERGRAPH ? (size_t)op->m * kC : 1);
+  cv.take<long long>(2 * kNP);
+  cv.take<double>(of_grid_cap());
+  return cv.used;
+}
+
+extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float* Q1, float* Z,
+                                    int64_t ld, int32_t c, int32_t steps, double* stats,
+                                    void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
+  ANCKA_REQUIRE(op32 && op32->dtype == ANCKA_F32, ANCKA_ERR_ARG, "orth_block needs the f32 operator");
+  ANCKA_REQUIRE(ld == kC && c >= 1 && c <= kC, ANCKA_ERR_UNSUPPORTED,
+                "fused orthogonal block supports c <= 8 with ld == 8");
+  ANCKA_REQUIRE(op32->split.n_pieces == 0 || op32->split.max_ld >= kC, ANCKA_ERR_ARG,
+                "row-split scratch too narrow");
+  Carver cv(workspace, workspace_bytes);
+  OfParams P{};
+  P.op = *op32;
+  P.Q[0] = Q0;
+  P.Q[1] = Q1;
+  P.Z = Z;
+  P.T = cv.take<float>(op32->kind == ANCKA_HYPERGRAPH ? (size_t)op32->m * kC : 1);
+  P.c = c;
+  P.steps = steps;
+  P.gram_fx = cv.take<long long>(2 * kNP);
+  P.dq_part = cv.take<double>(of_grid_cap());
+  P.stats = stats;
+  P.tdbg = getenv("ANCKA_ORTH_TIMING") ? reinterpret_cast<unsigned long long*>(stats + 4) : nullptr;
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "orth_block: workspace too small");
+  ANCKA_CUDA(cudaMemsetAsync(P.gram_fx, 0, sizeof(long long) * 2 * kNP, as_stream(stream)));
+  int per_sm = 0, dev = 0, sms = 0;
+  ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, orth_fused_kernel, kOfThreads, 0));
+  ANCKA_CUDA(cudaGetDevice(&dev));
+  ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  ANCKA_REQUIRE(per_sm >= 1, ANCKA_ERR_UNSUPPORTED, "orth_block does not fit an SM");
+  const int64_t want = ceil_div(op32->n, 32);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
+      want, std::min<int64_t>((int64_t)per_sm * sms, of_grid_cap())));
+  void* args[] = {&P};
+  note_launch();
+  ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)orth_fused_kernel, dim3(grid), dim3(kOfThreads),
+                                         args, 0, as_stream(stream)));
+  return ANCKA_OK;
+}

@@ -375,18 +375,23 @@ def build_pipeline(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=
 class _Loop:
     """Device buffers and captured tau-block graphs of the f32 iteration."""
 
-    def __init__(self, op: WalkOperator, c: int, k: int, tau: int, use_graphs: bool):
+    def __init__(self, op: WalkOperator, c: int, k: int, tau: int, use_graphs: bool,
+                 fused: bool = True):
         self.op, self.c, self.k, self.tau = op, c, k, tau
         n = op.n
-        self.ld = ld_for(c, torch.float32)
+        # narrow blocks use the fused cooperative kernel, which wants ld == 8
+        self.fused = fused and c <= 8
+        self.ld = 8 if self.fused else ld_for(c, torch.float32)
         d = dev()
         self.Q = [torch.zeros((n, self.ld), dtype=torch.float32, device=d) for _ in range(2)]
         self.Z = torch.zeros((n, self.ld), dtype=torch.float32, device=d)
         self.Qsave = torch.zeros((n, self.ld), dtype=torch.float32, device=d)
-        self.stats = torch.zeros(4, dtype=torch.float64, device=d)
+        self.stats = torch.zeros(16, dtype=torch.float64, device=d)   # [4:12] debug timers
         self._flag_init = torch.tensor([1.0, 0.0], dtype=torch.float64, device=d)
         self.s32 = op.struct(_lib.F32)
         self.ws = WORKSPACE.get("orth", _lib.load().ancka_orth_workspace_size(self.s32, c))
+        if self.fused:
+            self.ws_fused = WORKSPACE.get("orth_block", _lib.load().ancka_orth_block_workspace_size(self.s32))
         self.cur = 0
         self.use_graphs = use_graphs
         self.graphs = {}
@@ -428,7 +433,14 @@ class _Loop:
         """Advance `steps` f32 orthogonal steps from Q[cur]."""
         start = self.cur
         self.last = (start, steps)
-        if self.use_graphs and steps == self.tau:
+        if self.fused:
+            self.Qsave.copy_(self.Q[start])
+            self.reset_flags()
+            _lib.call("ancka_orth_block_f32", self.s32, self.Q[start].data_ptr(),
+                      self.Q[1 - start].data_ptr(), self.Z.data_ptr(), self.ld, self.c, steps,
+                      self.stats.data_ptr(), self.ws_fused.data_ptr(), self.ws_fused.numel(),
+                      _lib.stream())
+        elif self.use_graphs and steps == self.tau:
             g = self.graphs.get(start)
             if g is None:
                 self._block(start, steps)          # warm-up
@@ -462,7 +474,7 @@ class _Loop:
 
 
 def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
-              early_stop: bool = True, *, use_graphs: bool = True) -> ClusterResult:
+              early_stop: bool = True, *, use_graphs: bool = True, fused: bool = True) -> ClusterResult:
     """Full clustering pipeline (engine.py:343-437): host validation and
     uploads, then the device-resident pipeline (`run_prepared`)."""
     _lib.require_device()
@@ -471,14 +483,14 @@ def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
         t0 = time.perf_counter()
         prep = prepare_network(net, params, knn_cache_dir)
         prep_ms = (time.perf_counter() - t0) * 1e3
-    res = run_prepared(prep, params, early_stop, use_graphs=use_graphs)
+    res = run_prepared(prep, params, early_stop, use_graphs=use_graphs, fused=fused)
     res.timings_ms["knn_ms"] += prep_ms
     res.warnings = [str(w.message) for w in wrec] + res.warnings
     return res
 
 
 def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool = True, *,
-                 use_graphs: bool = True) -> ClusterResult:
+                 use_graphs: bool = True, fused: bool = True) -> ClusterResult:
     """The device pipeline on HBM-resident inputs: KNN -> KNN graph ->
     operator -> init -> orthogonal iterations / discretisation / MHC."""
     _lib.require_device()
@@ -510,7 +522,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             best_mhc = float(_MhcRunner(op, k, _lib.F64)(labels0).item())
         best_labels = labels0.clone()
         history = [(0, best_mhc)]
-        loop = _Loop(op, c, k, params.tau, use_graphs)
+        loop = _Loop(op, c, k, params.tau, use_graphs, fused)
         mhc = _MhcRunner(op, k, _lib.F32)
         lab_t = torch.empty(n, dtype=torch.int32, device=dev())
         info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device=dev())

@@ -231,3 +231,22 @@ def test_tensor_core_knn_exact(shape, n, words):
     # the f64 CUDA-core path agrees up to exact ties at the K-th value
     ids_f64, _ = knn_search_exact_device(X, K, integer=0)
     assert knn_sets_match(ids_f64.cpu().numpy(), ref, X, K) == 0
+
+
+@pytest.mark.parametrize("i", [0, 2, 3])
+def test_fused_and_graph_paths_agree(golden_runs, i):
+    """The fused cooperative orthogonal block and the per-step graph path give
+    the same clustering (labels identical up to f32 rounding decisions)."""
+    z, meta = golden_runs
+    m = meta[i]
+    p = f"r{i}_"
+    S, X = load_csr(z, p + "S"), load_x(z, p + "X")
+    net = (ancka.AttributedNetwork.hypergraph(S, X) if m["kind"] == "hypergraph"
+           else ancka.AttributedNetwork.graph(S, X))
+    params = ancka.ClusterParams(k=m["k"], knn_k=10, seed=m["seed"], t_a=m["t_a"],
+                                 knn_mode=ancka.KnnMode.EXACT)
+    a = ancka.run_ancka(net, params, early_stop=m["early_stop"], fused=True)
+    b = ancka.run_ancka(net, params, early_stop=m["early_stop"], fused=False)
+    assert ari(a.y.assignment, b.y.assignment) >= 0.99
+    q = a.state.q
+    assert np.abs(q.T @ q - np.eye(q.shape[1])).max() < 1e-5   # orthonormal block
