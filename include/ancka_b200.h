@@ -98,21 +98,24 @@ int ancka_device_check(void);
  * every row's sum of squares < 2^24: the tcgen05 tensor-core path then
  * computes exact integer dot products and ranks by exact rational
  * comparison.  Otherwise an fp64 CUDA-core path runs.
- * Outputs: ids (n x K int32, -1 padded), scores (n x K f64, 0 padded,
- * min(s, 1) as knn.py:139).  Raises ANCKA_ERR_NETWORK if K >= n. */
+ * Only query rows [q_begin, q_end) are computed (against all n keys): the
+ * query-row sharding of the multi-GPU path; [0, n) is the whole matrix.
+ * Outputs: ids ((q_end-q_begin) x K int32, -1 padded), scores (same shape,
+ * f64, 0 padded, min(s, 1) as knn.py:139).  ANCKA_ERR_NETWORK if K >= n. */
 size_t ancka_knn_workspace_size(int64_t n, int64_t d, int32_t K, int32_t integer_exact);
 int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
-                    int32_t integer_exact, int32_t* ids, double* scores,
-                    void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+                    int32_t integer_exact, int64_t q_begin, int64_t q_end, int32_t* ids,
+                    double* scores, void* workspace, size_t workspace_bytes,
+                    ancka_stream_t stream);
 
 /* Same, with X given as a CSR matrix (indptr n+1, sorted indices, f64 data):
  * the quantised tensor-core operand is built directly from the nonzeros (no
  * dense f64 copy).  Integer-exact path only (integer_exact = 1 bf16, 2 fp8);
  * the workspace is ancka_knn_workspace_size(n, d, K, integer_exact). */
 int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices, const double* data,
-                        int64_t n, int64_t d, int32_t K, int32_t integer_exact, int32_t* ids,
-                        double* scores, void* workspace, size_t workspace_bytes,
-                        ancka_stream_t stream);
+                        int64_t n, int64_t d, int32_t K, int32_t integer_exact, int64_t q_begin,
+                        int64_t q_end, int32_t* ids, double* scores, void* workspace,
+                        size_t workspace_bytes, ancka_stream_t stream);
 
 /* build_knn_adjacency + knn_transition (knn.py:294-324): A_K = M + M^T as a
  * sorted CSR and P_K = D_K^-1 A_K with row sums summed exactly as numpy's
@@ -139,6 +142,29 @@ int ancka_op_apply(const ancka_operator* op, const void* Q, int64_t ldq, int32_t
  * (+ self-loops). */
 int ancka_op_apply_struct_t(const ancka_operator* op, const void* Q, int64_t ldq, int32_t c,
                             void* Z, int64_t ldz, void* scratch, ancka_stream_t stream);
+
+/* Generic two-segment SpMM, the building block of the row-partitioned
+ * multi-GPU operator (walk.py:135-190 on a row slice):
+ *   out[r] = epi( mix( S[r] . s_src (+ self), K[r] . k_src ) ),  r < rows
+ * S, K: row slices (rows x *) whose column indices address the full
+ * gathered sources; mix = (1-beta_r) s + beta_r k when beta != NULL, else s;
+ * self-loop rows add self_src[row_offset + r]; epi: scale*x + (col == tag[r]
+ * ? tagval[col] : 0) when tag != NULL.  dtype ANCKA_F32 / ANCKA_F64. */
+int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_csr* S, const void* s_src,
+                int64_t lds, const ancka_csr* K, const void* k_src, int64_t ldk, const void* beta,
+                const uint8_t* selfloop, const void* self_src, int64_t ld_self, int64_t row_offset,
+                const int32_t* tag, const void* tagval, double scale, void* out, int64_t ldo,
+                ancka_stream_t stream);
+
+/* Split Cholesky-QR for row-partitioned blocks: G = Z^T Z of the local rows
+ * (packed upper, f64, c(c+1)/2), all-reduced by the caller, then factor +
+ * Q_out = Z R^-1 + local ||Q_out - Q_prev||^2 into stats[0] (stats as
+ * ancka_orth_step_f32).  Workspace: ancka_orth_workspace_size(NULL, c). */
+int ancka_gram_f32(const float* Z, int64_t n, int64_t ld, int32_t c, double* G,
+                   void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+int ancka_cholqr_apply_f32(const float* Z, const float* Q_prev, float* Q_out, int64_t n, int64_t ld,
+                           int32_t c, const double* G, double* stats, void* workspace,
+                           size_t workspace_bytes, ancka_stream_t stream);
 
 /* ---- engine pieces (engine.py) ----------------------------------------- */
 

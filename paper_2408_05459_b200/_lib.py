@@ -46,9 +46,19 @@ _SIGS = {
     "ancka_launch_count": (c_int64, []),
     "ancka_knn_workspace_size": (c_size_t, [c_int64, c_int64, c_int32, c_int32]),
     "ancka_knn_exact": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32,
-                                  c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+                                  c_int64, c_int64, c_void_p, c_void_p, c_void_p, c_size_t,
+                                  c_void_p]),
     "ancka_knn_exact_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,
-                                      c_int32, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+                                      c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                      c_size_t, c_void_p]),
+    "ancka_spmm2": (c_int32, [c_int32, c_int64, c_int32, POINTER(CSR), c_void_p, c_int64,
+                              POINTER(CSR), c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                              c_int64, c_int64, c_void_p, c_void_p, c_double, c_void_p, c_int64,
+                              c_void_p]),
+    "ancka_gram_f32": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
+                                 c_size_t, c_void_p]),
+    "ancka_cholqr_apply_f32": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,
+                                         c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "ancka_knn_graph_workspace_size": (c_size_t, [c_int64, c_int32]),
     "ancka_knn_graph": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

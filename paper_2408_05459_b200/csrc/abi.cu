@@ -56,29 +56,33 @@ extern "C" size_t ancka_knn_workspace_size(int64_t n, int64_t d, int32_t K, int3
 }
 
 extern "C" int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
-                               int32_t integer_exact, int32_t* ids, double* scores,
-                               void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
+                               int32_t integer_exact, int64_t q_begin, int64_t q_end, int32_t* ids,
+                               double* scores, void* workspace, size_t workspace_bytes,
+                               ancka_stream_t stream) {
   ANCKA_REQUIRE(K < n, ANCKA_ERR_NETWORK, "K=%d must be smaller than n=%lld", K, (long long)n);
   ANCKA_REQUIRE(K >= 1 && d >= 1, ANCKA_ERR_ARG, "knn: bad sizes");
   auto st = as_stream(stream);
+  ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
   if (integer_exact)
-    return knn_tc(X, n, d, ldx, K, ids, scores, workspace, workspace_bytes, st, integer_exact == 2);
+    return knn_tc(X, n, d, ldx, K, q_begin, q_end, ids, scores, workspace, workspace_bytes, st,
+                  integer_exact == 2);
   Carver cv(workspace, workspace_bytes);
   double *xn, *nr;
   int64_t ldn;
   carve_knn_simt(cv, n, d, &xn, &nr, &ldn);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn: workspace too small");
   ANCKA_TRY(normalize_rows_f64(X, n, d, ldx, xn, ldn, nr, st));
-  return knn_simt(xn, n, ldn, nr, K, ids, scores, st);
+  return knn_simt(xn, n, ldn, nr, K, q_begin, q_end, ids, scores, st);
 }
 
 extern "C" int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices, const double* data,
                                    int64_t n, int64_t d, int32_t K, int32_t integer_exact,
-                                   int32_t* ids, double* scores, void* workspace,
-                                   size_t workspace_bytes, ancka_stream_t stream) {
+                                   int64_t q_begin, int64_t q_end, int32_t* ids, double* scores,
+                                   void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
   ANCKA_REQUIRE(K < n, ANCKA_ERR_NETWORK, "K=%d must be smaller than n=%lld", K, (long long)n);
   ANCKA_REQUIRE(integer_exact == 1 || integer_exact == 2, ANCKA_ERR_UNSUPPORTED,
                 "CSR attributes are supported on the integer-exact tensor-core path only");
-  return knn_tc_csr(indptr, indices, data, n, d, K, ids, scores, workspace, workspace_bytes,
-                    as_stream(stream), integer_exact == 2);
+  ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
+  return knn_tc_csr(indptr, indices, data, n, d, K, q_begin, q_end, ids, scores, workspace,
+                    workspace_bytes, as_stream(stream), integer_exact == 2);
 }

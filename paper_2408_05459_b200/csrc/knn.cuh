@@ -6,14 +6,15 @@ namespace ancka {
 int normalize_rows_f64(const double* X, int64_t n, int64_t d, int64_t ldx, double* xn, int64_t ldn,
                        double* norms, cudaStream_t st);
 size_t knn_simt_smem(int K);
-int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int K, int32_t* ids,
-             double* scores, cudaStream_t st);
+int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int K,
+             int64_t q_begin, int64_t q_end, int32_t* ids, double* scores, cudaStream_t st);
 
 // tcgen05 integer-exact path (knn_tc.cu)
 size_t knn_tc_workspace(int64_t n, int64_t d, int K);
-int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* ids, double* scores,
-           void* ws, size_t wsb, cudaStream_t st, bool fp8);
+int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
+           int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st,
+           bool fp8);
 int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t n,
-               int64_t d, int K, int32_t* ids, double* scores, void* ws, size_t wsb,
-               cudaStream_t st, bool fp8);
+               int64_t d, int K, int64_t q_begin, int64_t q_end, int32_t* ids, double* scores,
+               void* ws, size_t wsb, cudaStream_t st, bool fp8);
 }  // namespace ancka

@@ -35,7 +35,8 @@ __global__ void normalize_rows_f64_kernel(const double* __restrict__ X, int64_t 
 
 __global__ void __launch_bounds__(256)
 knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const double* __restrict__ norms,
-                int K, int32_t* __restrict__ ids, double* __restrict__ scores) {
+                int K, int64_t q_begin, int64_t q_end, int32_t* __restrict__ ids,
+                double* __restrict__ scores) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double* As = reinterpret_cast<double*>(smraw);           // BM x BK
   double* Bs = As + BM * BK;                                // BN x BK
@@ -44,11 +45,11 @@ knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const dou
   int32_t* li = reinterpret_cast<int32_t*>(lv + (size_t)BM * K);  // BM x K ids
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 4 x 4 each
-  const int64_t q0 = (int64_t)blockIdx.x * BM;
+  const int64_t q0 = q_begin + (int64_t)blockIdx.x * BM;
   int fill = 0;                            // list length (owner threads)
   for (int e = tid; e < BM * K; e += blockDim.x) { lv[e] = 0.0; li[e] = -1; }
   const int64_t qi = q0 + tid;
-  const bool owner = tid < BM && qi < n;
+  const bool owner = tid < BM && qi < q_end;
   const bool qzero = owner ? norms[qi] == 0.0 : true;
   __syncthreads();
   for (int64_t k0 = 0; k0 < n; k0 += BN) {
@@ -57,7 +58,7 @@ knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const dou
       for (int e = tid; e < BM * BK; e += blockDim.x) {
         const int r = e / BK, c = e % BK;
         const int64_t qr = q0 + r, kr = k0 + r;
-        As[e] = qr < n ? xn[qr * ldn + d0 + c] : 0.0;
+        As[e] = qr < q_end ? xn[qr * ldn + d0 + c] : 0.0;
         Bs[e] = kr < n ? xn[kr * ldn + d0 + c] : 0.0;
       }
       __syncthreads();
@@ -100,11 +101,11 @@ knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const dou
     }
     __syncthreads();
   }
-  if (tid < BM && qi < n) {
+  if (tid < BM && qi < q_end) {
     for (int t = 0; t < K; ++t) {
       const bool ok = !qzero && t < fill;
-      ids[qi * K + t] = ok ? li[tid * K + t] : -1;
-      scores[qi * K + t] = ok ? fmin(lv[tid * K + t], 1.0) : 0.0;
+      ids[(qi - q_begin) * K + t] = ok ? li[tid * K + t] : -1;
+      scores[(qi - q_begin) * K + t] = ok ? fmin(lv[tid * K + t], 1.0) : 0.0;
     }
   }
 }
@@ -114,12 +115,13 @@ size_t knn_simt_smem(int K) {
          sizeof(int32_t) * (size_t)BM * K;
 }
 
-int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int K, int32_t* ids,
-             double* scores, cudaStream_t st) {
+int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int K,
+             int64_t q_begin, int64_t q_end, int32_t* ids, double* scores, cudaStream_t st) {
   const size_t smem = knn_simt_smem(K);
   ANCKA_REQUIRE(smem <= 220 * 1024, ANCKA_ERR_UNSUPPORTED, "knn_simt: K=%d too large", K);
   ANCKA_CUDA(cudaFuncSetAttribute(knn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  knn_simt_kernel<<<(unsigned)ceil_div(n, BM), 256, smem, st>>>(xn, n, ldn, norms, K, ids, scores);
+  knn_simt_kernel<<<(unsigned)ceil_div(q_end - q_begin, BM), 256, smem, st>>>(
+      xn, n, ldn, norms, K, q_begin, q_end, ids, scores);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

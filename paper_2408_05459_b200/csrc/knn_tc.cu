@@ -158,6 +158,7 @@ struct TcParams {
   const float* inv_sqrt;    // n_pad
   int2* partial;            // n x nseg x K  (c, j)
   int debug;                // 0 normal; 1 skip epilogue math; 2 skip MMA issue
+  int64_t q_begin, q_end;   // query rows handled by this launch (row sharding)
   int* row_bound;           // n: best known K-th key per row (f32 bits, atomicMax)
 };
 
@@ -178,7 +179,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t q0 = (int64_t)blockIdx.x * BM;
+  const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
   const int seg = blockIdx.y;
   const int kt0 = seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
@@ -260,7 +261,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
       mbar_wait_sleep(&tfull[acc], acc_phase);
-      if (i < p.n) L.raise_floor(__int_as_float(__ldcg(p.row_bound + i)));
+      if (i < p.q_end) L.raise_floor(__int_as_float(__ldcg(p.row_bound + (i - p.q_begin))));
       tc_fence_after();
       const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
 #pragma unroll 1
@@ -300,16 +301,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
             L.insert(kf, cc, __ldg(p.a_norm + j), j);
             const float fk = L.f[KMAX - 1];
             if (fk > published) {        // share the row's improved bound
-              atomicMax(p.row_bound + i, __float_as_int(fk));
+              atomicMax(p.row_bound + (i - p.q_begin), __float_as_int(fk));
               published = fk;
             }
           }
         }
       }
     }
-    if (i < p.n) {
+    if (i < p.q_end) {
       const int lists = p.nseg * (EPI_WARPS / 4);
-      int2* out = p.partial + ((size_t)i * lists + seg * (EPI_WARPS / 4) + half) * p.K;
+      int2* out = p.partial + ((size_t)(i - p.q_begin) * lists + seg * (EPI_WARPS / 4) + half) * p.K;
       L.emit(p.K, [&](int r, uint32_t c, uint32_t, int32_t j) {
         out[r] = make_int2((int)c, c ? j : -1);
       });
@@ -322,16 +323,18 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
 // Merge the per-segment lists (exact order) and emit ids / f64 cosines.
 template <int KMAX>
-__global__ void knn_tc_merge_kernel(const int2* __restrict__ partial, int64_t n, int nseg, int K,
+__global__ void knn_tc_merge_kernel(const int2* __restrict__ partial, int64_t q_begin, int64_t nq,
+                                    int nseg, int K,
                                     const uint32_t* __restrict__ a_norm,
                                     const float* __restrict__ inv_sqrt, int32_t* __restrict__ ids,
                                     double* __restrict__ scores) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t li = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; li < nq;
+       li += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = q_begin + li;
     TopK<KMAX> L;
     L.clear(K);
     for (int s = 0; s < nseg; ++s) {
-      const int2* src = partial + ((size_t)i * nseg + s) * K;
+      const int2* src = partial + ((size_t)li * nseg + s) * K;
       for (int t = 0; t < K; ++t) {
         const int2 e = src[t];
         if (e.x <= 0) break;
@@ -343,8 +346,8 @@ __global__ void knn_tc_merge_kernel(const int2* __restrict__ partial, int64_t n,
     const double ai = (double)a_norm[i];
     L.emit(K, [&](int r, uint32_t c, uint32_t a, int32_t j) {
       const bool ok = c != 0;
-      ids[i * K + r] = ok ? j : -1;
-      scores[i * K + r] = ok ? fmin((double)c / sqrt(ai * (double)a), 1.0) : 0.0;
+      ids[li * K + r] = ok ? j : -1;
+      scores[li * K + r] = ok ? fmin((double)c / sqrt(ai * (double)a), 1.0) : 0.0;
     });
   }
 }
@@ -415,13 +418,13 @@ struct TcLayout {
   int nseg, tiles_per_seg, key_tiles, q_tiles;
 };
 
-static TcLayout tc_layout(int64_t n, int64_t d, bool fp8) {
+static TcLayout tc_layout(int64_t n, int64_t d, bool fp8, int64_t nq) {
   TcLayout L;
   L.fp8 = fp8;
   L.n_pad = ceil_div(n, tc::BN) * tc::BN;
   const int64_t elems_per_row = tc::ROW_BYTES / (fp8 ? 1 : 2);
   L.d_pad = ceil_div(d, elems_per_row) * elems_per_row;
-  L.q_tiles = (int)ceil_div(n, tc::BM);
+  L.q_tiles = (int)ceil_div(nq, tc::BM);
   L.key_tiles = (int)ceil_div(n, tc::BN);
   int nseg = (int)ceil_div(8 * kNumSMs, L.q_tiles);
   nseg = std::max(1, std::min(nseg, L.key_tiles));
@@ -436,13 +439,14 @@ static void carve_tc(Carver& cv, const TcLayout& L, int64_t n, int K, void** xq,
   *an = cv.take<uint32_t>(L.n_pad);
   *isq = cv.take<float>(L.n_pad);
   *rb = cv.take<int>(L.n_pad);
-  *part = cv.take<int2>((size_t)n * L.nseg * (tc::EPI_WARPS / 4) * K);
+  // nq * nseg <= n + 8 * 148 * BM for every query range (nseg ~ 8*148 / q_tiles)
+  *part = cv.take<int2>(((size_t)n + 8 * kNumSMs * tc::BM) * (tc::EPI_WARPS / 4) * K);
 }
 
 // the fp8 path is taken when the host asserts |x| <= 16 via integer_exact == 2
 size_t knn_tc_workspace(int64_t n, int64_t d, int K) {
   Carver cv(nullptr, 0);
-  TcLayout L = tc_layout(n, d, false);  // bf16 bound covers fp8
+  TcLayout L = tc_layout(n, d, false, n);  // bf16 bound covers fp8
   void* xq;
   uint32_t* an;
   float* isq;
@@ -493,14 +497,15 @@ __global__ void knn_tc_prep_csr_kernel(const int64_t* __restrict__ indptr,
 }
 
 static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, const TcLayout& L,
-                       int64_t n, int K, int32_t* ids, double* scores, cudaStream_t st, bool fp8);
+                       int64_t n, int K, int64_t q_begin, int64_t q_end, int32_t* ids,
+                       double* scores, cudaStream_t st, bool fp8);
 
 int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t n,
-               int64_t d, int K, int32_t* ids, double* scores, void* ws, size_t wsb,
-               cudaStream_t st, bool fp8) {
+               int64_t d, int K, int64_t q_begin, int64_t q_end, int32_t* ids, double* scores,
+               void* ws, size_t wsb, cudaStream_t st, bool fp8) {
   ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
   ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
-  TcLayout L = tc_layout(n, d, fp8);
+  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin);
   Carver cv(ws, wsb);
   void* xq;
   uint32_t* an;
@@ -516,14 +521,15 @@ int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data
   else
     knn_tc_prep_csr_kernel<false><<<pg, 256, 0, st>>>(indptr, indices, data, n, L.n_pad, L.d_pad, xq, an, isq);
   ANCKA_LAUNCHED();
-  return knn_tc_main(xq, an, isq, rb, part, L, n, K, ids, scores, st, fp8);
+  return knn_tc_main(xq, an, isq, rb, part, L, n, K, q_begin, q_end, ids, scores, st, fp8);
 }
 
-int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* ids, double* scores,
-           void* ws, size_t wsb, cudaStream_t st, bool fp8) {
+int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
+           int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st,
+           bool fp8) {
   ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
   ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
-  TcLayout L = tc_layout(n, d, fp8);
+  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin);
   Carver cv(ws, wsb);
   void* xq;
   uint32_t* an;
@@ -538,16 +544,19 @@ int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int32_t* i
   else
     knn_tc_prep_kernel<false><<<pg, 256, 0, st>>>(X, n, d, ldx, L.n_pad, L.d_pad, xq, an, isq);
   ANCKA_LAUNCHED();
-  return knn_tc_main(xq, an, isq, rb, part, L, n, K, ids, scores, st, fp8);
+  return knn_tc_main(xq, an, isq, rb, part, L, n, K, q_begin, q_end, ids, scores, st, fp8);
 }
 
 static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, const TcLayout& L,
-                       int64_t n, int K, int32_t* ids, double* scores, cudaStream_t st, bool fp8) {
+                       int64_t n, int K, int64_t q_begin, int64_t q_end, int32_t* ids,
+                       double* scores, cudaStream_t st, bool fp8) {
   CUtensorMap ma, mb;
   ANCKA_TRY(make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
   ANCKA_TRY(make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
   TcParams p;
   p.n = n;
+  p.q_begin = q_begin;
+  p.q_end = q_end;
   p.nkb = (int)(L.d_pad * (fp8 ? 1 : 2) / tc::ROW_BYTES);
   p.K = K;
   p.key_tiles = L.key_tiles;
@@ -557,7 +566,7 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
   p.inv_sqrt = isq;
   p.partial = part;
   p.row_bound = rb;
-  ANCKA_CUDA(cudaMemsetAsync(rb, 0, sizeof(int) * L.n_pad, st));
+  ANCKA_CUDA(cudaMemsetAsync(rb, 0, sizeof(int) * (q_end - q_begin), st));
   p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
   if (fp8) {
     if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }
@@ -566,11 +575,12 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
     if (K <= 16) { ANCKA_TRY((launch_tc<false, 16>(ma, mb, p, L, st))); }
     else { ANCKA_TRY((launch_tc<false, 32>(ma, mb, p, L, st))); }
   }
-  const int mg = (int)std::min<int64_t>(ceil_div(n, 128), 8 * kNumSMs);
+  const int64_t nq = q_end - q_begin;
+  const int mg = (int)std::min<int64_t>(ceil_div(nq, 128), 8 * kNumSMs);
   if (K <= 16)
-    knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, n, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
+    knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, q_begin, nq, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
   else
-    knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, n, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
+    knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, q_begin, nq, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

@@ -402,3 +402,62 @@ extern "C" int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double*
   }
   return ANCKA_OK;
 }
+
+// ------------------------------------------- split CholQR (multi-GPU path) ---
+// partial Gram of the local rows -> G (packed upper, f64); the caller
+// all-reduces G across ranks, then ancka_cholqr_apply_f32 factors it.
+namespace ancka {
+__global__ void gram_reduce_kernel(const double* __restrict__ partial, int nblocks, int npairs,
+                                   double* __restrict__ G) {
+  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
+    double s0 = 0.0, s1 = 0.0;
+    int b = 0;
+    for (; b + 1 < nblocks; b += 2) {
+      s0 += partial[(int64_t)b * npairs + p];
+      s1 += partial[(int64_t)(b + 1) * npairs + p];
+    }
+    if (b < nblocks) s0 += partial[(int64_t)b * npairs + p];
+    G[p] = s0 + s1;
+  }
+}
+}  // namespace ancka
+
+extern "C" int ancka_gram_f32(const float* Z, int64_t n, int64_t ld, int32_t c, double* G,
+                              void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
+  Carver cv(workspace, workspace_bytes);
+  OrthWs w;
+  carve_orth(cv, w, nullptr, c);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "gram: workspace too small");
+  auto st = as_stream(stream);
+  ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
+  gram_reduce_kernel<<<1, 256, 0, st>>>(w.gram_partial, kGramBlocks, c * (c + 1) / 2, G);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+extern "C" int ancka_cholqr_apply_f32(const float* Z, const float* Q_prev, float* Q_out, int64_t n,
+                                      int64_t ld, int32_t c, const double* G, double* stats,
+                                      void* workspace, size_t workspace_bytes,
+                                      ancka_stream_t stream) {
+  Carver cv(workspace, workspace_bytes);
+  OrthWs w;
+  carve_orth(cv, w, nullptr, c);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "cholqr_apply: workspace too small");
+  auto st = as_stream(stream);
+  const int npairs = c * (c + 1) / 2;
+  const size_t csm = 2 * (size_t)npairs * sizeof(double);
+  ANCKA_REQUIRE(csm <= 227 * 1024, ANCKA_ERR_UNSUPPORTED, "cholqr: c=%d too large", c);
+  if (csm > 48 * 1024)
+    cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+  chol_kernel<<<1, 256, csm, st>>>(G, 1, c, w.rinv32, w.rdiag, stats);
+  ANCKA_LAUNCHED();
+  const size_t asm_ = (size_t)c * c * sizeof(float);
+  if (asm_ > 48 * 1024)
+    cudaFuncSetAttribute(apply_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
+  apply_rinv_kernel<<<kApplyBlocks, 256, asm_, st>>>(Z, Q_prev, Q_out, n, ld, c, w.rinv32,
+                                                     w.dq_partial);
+  ANCKA_LAUNCHED();
+  reduce_partials_kernel<<<1, 256, 0, st>>>(w.dq_partial, kApplyBlocks, stats);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}

@@ -346,3 +346,48 @@ extern "C" int ancka_op_apply_struct_t(const ancka_operator* op, const void* Q, 
   return ancka::op_apply_struct_t_t<float>(op, (const float*)Q, ldq, c, (float*)Z, ldz,
                                            (float*)scratch, st, nullptr);
 }
+
+// Generic two-segment SpMM (the building block of the row-partitioned
+// multi-GPU operator): rows of out = epi( mix( S_rows . S_src (+ self),
+// K_rows . K_src ) ).  S/K are row slices whose column indices address the
+// full (gathered) sources; `row_offset` maps local row r to the global row
+// used for the self-loop source.  beta == NULL: structure only (no K term).
+extern "C" int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_csr* S,
+                           const void* s_src, int64_t lds, const ancka_csr* K, const void* k_src,
+                           int64_t ldk, const void* beta, const uint8_t* selfloop,
+                           const void* self_src, int64_t ld_self, int64_t row_offset,
+                           const int32_t* tag, const void* tagval, double scale, void* out,
+                           int64_t ldo, ancka_stream_t stream) {
+  using namespace ancka;
+  auto st = as_stream(stream);
+  auto fill = [&](auto* tp) -> int {
+    using T = std::remove_pointer_t<decltype(tp)>;
+    constexpr int W = sizeof(T) == 4 ? 4 : 2;
+    SpmmArgs<T> a{};
+    a.rows = rows;
+    a.c = c;
+    a.nchunk = (int)ceil_div(c, W);
+    if (S && S->rowptr) {
+      a.s.rowptr = S->rowptr; a.s.colidx = S->colidx;
+      a.s.values = static_cast<const T*>(S->values);
+      a.s.src = static_cast<const T*>(s_src); a.s.ld = lds;
+    }
+    if (K && K->rowptr) {
+      a.k.rowptr = K->rowptr; a.k.colidx = K->colidx;
+      a.k.values = static_cast<const T*>(K->values);
+      a.k.src = static_cast<const T*>(k_src); a.k.ld = ldk;
+    }
+    a.beta = static_cast<const T*>(beta);
+    a.selfloop = selfloop;
+    a.self_src = self_src ? static_cast<const T*>(self_src) + row_offset * ld_self : nullptr;
+    a.self_ld = ld_self;
+    a.tag = tag;
+    a.tagval = static_cast<const T*>(tagval);
+    a.scale = (T)scale;
+    a.out = static_cast<T*>(out);
+    a.ldo = ldo;
+    return launch_spmm<T>(a, st);
+  };
+  if (dtype == ANCKA_F64) return fill((double*)nullptr);
+  return fill((float*)nullptr);
+}

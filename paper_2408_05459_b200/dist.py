@@ -1,0 +1,484 @@
+"""Row-partitioned multi-GPU ANCKA.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank r
+owns a contiguous block of node rows [r0, r1) (balanced by operator
+nonzeros) and, for hypergraphs, a block of hyperedges [e0, e1):
+
+* KNN       query-row sharding: rank r computes the exact top-K lists of its
+            rows against all keys (every rank holds the quantised X), then the
+            lists are all-gathered and A_K / P_K are assembled on every rank.
+* operator  per apply: all-gather Q (n x c); hypergraphs compute their share
+            of T = P_E Q and all-gather T; each rank produces its rows of
+            Z = (I-B) P_struct Q + B P_K Q.
+* QR        local Gram Z_r^T Z_r -> all-reduce (c x c) -> every rank factors
+            the same R and applies R^-1 to its rows; ||dQ||^2 is all-reduced.
+* step 1    (rank deficient) Z^(1) is all-gathered in f64 and
+            the exact f64 QR with the reference's rank test and noise draw is
+            replicated, so every rank holds the reference's Q^(1).
+* init/MHC  the transposed / joint applies are row-partitioned the same way;
+            the MHC trace is all-reduced.
+* discretisation is replicated on the gathered Q (identical on every rank).
+
+The orchestration is backend-generic: `CudaBackend` drives libancka_b200
+kernels and NCCL; the CPU tests drive the same code with a numpy backend over
+gloo (tests/test_dist.py), which is how the N>1 logic is verified without
+several GPUs.
+"""
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from .network import (AttributedNetwork, BcmMatrix, ClusterParams, NetworkError, NetworkKind,
+                      default_knn_k, node_degrees, symmetrize_union, validate_network)
+
+
+# ----------------------------------------------------------------------------
+def partition_rows(cost: np.ndarray, world: int) -> np.ndarray:
+    """Contiguous row blocks with ~equal total cost: boundaries[world + 1]."""
+    n = cost.size
+    c = np.concatenate([[0.0], np.cumsum(cost, dtype=np.float64)])
+    targets = c[-1] * np.arange(1, world) / world
+    cuts = np.searchsorted(c, targets, side="left")
+    b = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    return np.maximum.accumulate(np.clip(b, 0, n))
+
+
+def _row_normalize(a: sp.csr_matrix) -> sp.csr_matrix:
+    rs = np.asarray(a.sum(axis=1)).ravel()
+    inv = np.divide(1.0, rs, out=np.zeros_like(rs), where=rs > 0)
+    p = (sp.diags(inv) @ a).tocsr()
+    p.sort_indices()
+    return p
+
+
+@dataclass
+class Plan:
+    """Ownership of rows / hyperedges for one rank."""
+    rank: int
+    world: int
+    n: int
+    m: int
+    rows: np.ndarray      # world + 1 node-row boundaries
+    edges: np.ndarray     # world + 1 hyperedge boundaries (hypergraph)
+
+    @property
+    def r0(self):
+        return int(self.rows[self.rank])
+
+    @property
+    def r1(self):
+        return int(self.rows[self.rank + 1])
+
+    @property
+    def e0(self):
+        return int(self.edges[self.rank])
+
+    @property
+    def e1(self):
+        return int(self.edges[self.rank + 1])
+
+    def row_counts(self):
+        return np.diff(self.rows)
+
+    def edge_counts(self):
+        return np.diff(self.edges)
+
+
+class HostFactors:
+    """Structural factors of the validated network, normalised on the host
+    exactly as the reference (walk.py:38-79); sliced per rank."""
+
+    def __init__(self, net: AttributedNetwork):
+        self.kind = net.kind
+        self.n = net.n
+        self.degrees = node_degrees(net)
+        if net.kind is NetworkKind.HYPERGRAPH:
+            h = net.incidence
+            self.p_v = _row_normalize(h.T.tocsr())
+            self.p_e = _row_normalize(h)
+            self.t_a = self.p_v.T.tocsr()      # P_V^T  (m x n)
+            self.t_b = self.p_e.T.tocsr()      # P_E^T  (n x m)
+            for mtx in (self.t_a, self.t_b):
+                mtx.sort_indices()
+            self.m = h.shape[0]
+        else:
+            a = symmetrize_union(net.adjacency) if net.directed else net.adjacency
+            self.p_n = _row_normalize(a)
+            self.t_a = self.p_n.T.tocsr()
+            self.t_a.sort_indices()
+            self.m = 0
+
+    def row_cost(self, K: int) -> np.ndarray:
+        s = self.p_v if self.kind is NetworkKind.HYPERGRAPH else self.p_n
+        return np.diff(s.indptr).astype(np.float64) + 2 * K + 1
+
+
+def make_plan(fac: HostFactors, K: int, rank: int, world: int) -> Plan:
+    rows = partition_rows(fac.row_cost(K), world)
+    if fac.kind is NetworkKind.HYPERGRAPH:
+        edges = partition_rows(np.diff(fac.p_e.indptr).astype(np.float64) + 1, world)
+    else:
+        edges = np.zeros(world + 1, dtype=np.int64)
+    return Plan(rank, world, fac.n, fac.m, rows, edges)
+
+
+# ----------------------------------------------------------------------------
+class DistOperator:
+    """A rank's share of the joint-walk operator (row slices, backend handles)."""
+
+    def __init__(self, B, fac: HostFactors, plan: Plan, p_k_rows, beta_full: np.ndarray,
+                 selfloop_full: np.ndarray, alpha: float, gamma: int):
+        self.B, self.plan, self.kind = B, plan, fac.kind
+        self.alpha, self.gamma = alpha, gamma
+        r0, r1 = plan.r0, plan.r1
+        if fac.kind is NetworkKind.HYPERGRAPH:
+            self.S = B.csr(fac.p_v[r0:r1])             # n_loc x m, gathers T
+            self.E = B.csr(fac.p_e[plan.e0:plan.e1])   # m_loc x n, gathers Q
+            self.TA = B.csr(fac.t_a[plan.e0:plan.e1])  # P_V^T rows: m_loc x n
+            self.TB = B.csr(fac.t_b[r0:r1])            # P_E^T rows: n_loc x m
+        else:
+            self.S = B.csr(fac.p_n[r0:r1])
+            self.TA = B.csr(fac.t_a[r0:r1])
+        self.K = p_k_rows
+        self.beta = B.vec(beta_full[r0:r1])
+        self.selfloop = B.mask(selfloop_full[r0:r1])
+
+    # -- joint apply (walk.py:177-190) on the local rows; Q_full gathered
+    def apply(self, Q_full, c, dtype, tag=None, tagval=None, scale=1.0):
+        B, pl = self.B, self.plan
+        if self.kind is NetworkKind.HYPERGRAPH:
+            T_loc = B.spmm(self.E, Q_full, None, None, None, None, None, 0, None, None, 1.0, c, dtype)
+            T_full = B.all_gather_rows(T_loc, pl.edge_counts())
+            src = T_full
+        else:
+            src = Q_full
+        return B.spmm(self.S, src, self.K, Q_full, self.beta, self.selfloop, Q_full, pl.r0,
+                      tag, tagval, scale, c, dtype)
+
+    # -- transposed structure apply (walk.py:153-174) with the init epilogue
+    def apply_t(self, P_full, c, tag, tagval, scale):
+        B, pl = self.B, self.plan
+        if self.kind is NetworkKind.HYPERGRAPH:
+            U_loc = B.spmm(self.TA, P_full, None, None, None, None, None, 0, None, None, 1.0, c, "f64")
+            U_full = B.all_gather_rows(U_loc, pl.edge_counts())
+            return B.spmm(self.TB, U_full, None, None, None, self.selfloop, P_full, pl.r0,
+                          tag, tagval, scale, c, "f64")
+        return B.spmm(self.TA, P_full, None, None, None, self.selfloop, P_full, pl.r0,
+                      tag, tagval, scale, c, "f64")
+
+
+def _centers(deg: np.ndarray, k: int) -> np.ndarray:
+    n = deg.size
+    nz = int((deg > 0).sum())
+    order = np.lexsort((np.arange(n), -deg))
+    if k > nz:
+        warnings.warn(f"only {nz} nodes have nonzero degree; filling {k - nz} center(s) in index order")
+        chosen = order[:nz]
+        mask = np.zeros(n, dtype=bool)
+        mask[chosen] = True
+        rest = np.flatnonzero(~mask)[: k - nz]
+        return np.sort(np.concatenate([chosen, rest]).astype(np.int64))
+    return np.sort(order[:k]).astype(np.int64)
+
+
+@dataclass
+class DistResult:
+    labels: np.ndarray
+    mhc: float
+    iterations: int
+    stop_reason: str
+    history: list
+    converged: bool
+    error: str | None = None
+
+
+def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop: bool = True) -> DistResult:
+    """run_ancka (engine.py:343-437) row-partitioned over the backend's ranks."""
+    rank, world = B.rank, B.world
+    net, _ = validate_network(net)
+    params.validate_for(net.n)
+    n, k = net.n, params.k
+    K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, n)
+    K = min(K, n - 1)
+    fac = HostFactors(net)
+    plan = make_plan(fac, K, rank, world)
+
+    # ---- KNN: query-row sharding, all-gather of the lists, replicated P_K
+    ids_loc, sc_loc = B.knn_rows(net.attributes, K, plan.r0, plan.r1)
+    ids = B.all_gather_rows(ids_loc, plan.row_counts())
+    scores = B.all_gather_rows(sc_loc, plan.row_counts())
+    pk_rows, zero_rows = B.knn_graph_rows(ids, scores, n, plan.r0, plan.r1)
+
+    # beta_vector / self-loops (walk.py:47-57, 121-123)
+    deg = fac.degrees
+    beta = np.full(n, float(params.beta))
+    beta[deg == 0] = 1.0
+    beta[zero_rows] = 0.0
+    selfloop = (deg == 0) & (beta == 0.0)
+    op = DistOperator(B, fac, plan, pk_rows, beta, selfloop, params.alpha, params.gamma)
+
+    # ---- greedy init (engine.py:87-127): T_i transposed restart walks
+    centers = _centers(deg, k)
+    center_of = np.full(n, -1, dtype=np.int32)
+    center_of[centers] = np.arange(k, dtype=np.int32)
+    tag_loc = B.ivec(center_of[plan.r0:plan.r1])
+    tagval = B.vec(np.full(k, params.alpha))
+    P_loc = B.tagged(tag_loc, tagval, k, "f64")
+    for _ in range(params.t_i):
+        P_full = B.all_gather_rows(P_loc, plan.row_counts())
+        P_loc = op.apply_t(P_full, k, tag_loc, tagval, 1.0 - params.alpha)
+    lab0 = B.to_host_i(B.all_gather_rows(B.argmax_rows(P_loc, k), plan.row_counts()))
+    if (np.bincount(lab0, minlength=k) == 0).any():
+        warnings.warn("greedy init left empty cluster(s); pinning centers")
+        lab0 = lab0.copy()
+        lab0[centers] = np.arange(k)
+
+    def mhc(labels: np.ndarray, dtype: str) -> float:
+        """calc_mhc (engine.py:291-299), row-partitioned."""
+        sizes = np.bincount(labels, minlength=k)
+        if (sizes == 0).any():
+            raise NetworkError("empty cluster: normalization undefined")
+        yhat = 1.0 / np.sqrt(sizes.astype(np.float64))
+        tag = B.ivec(labels[plan.r0:plan.r1].astype(np.int32))
+        tv = B.vec(params.alpha * yhat)
+        F_loc = B.tagged(tag, tv, k, dtype)
+        for _ in range(params.gamma):
+            F_full = B.all_gather_rows(F_loc, plan.row_counts())
+            F_loc = op.apply(F_full, k, dtype, tag, tv, 1.0 - params.alpha)
+        tr = B.all_reduce(np.array([B.trace_labels(F_loc, labels[plan.r0:plan.r1], yhat)]))[0]
+        return 1.0 - tr / k
+
+    rng = np.random.default_rng(params.seed)
+    c = min(k + 1, n)
+    sizes0 = np.bincount(lab0, minlength=k)
+    q0 = np.zeros((n, c))
+    q0[:, 0] = 1.0 / np.sqrt(n)
+    keep = lab0 + 1 < c
+    q0[np.flatnonzero(keep), lab0[keep] + 1] = 1.0 / np.sqrt(sizes0[lab0[keep]])
+    best_phi = mhc(lab0, "f64")
+    best = lab0.copy()
+    hist = [(0, best_phi)]
+
+    # ---- t = 1: exact f64 step, replicated on the gathered Z^(1)
+    Z1 = op.apply(B.rows_from_host(q0, "f64"), c, "f64")
+    Z1_full = B.to_host(B.all_gather_rows(Z1, plan.row_counts()))
+    q1 = B.exact_qr_step(Z1_full, rng)
+    Q_loc = B.rows_from_host(q1[plan.r0:plan.r1], "f32")
+    dq = float(np.linalg.norm(q1 - q0))
+    stop, converged, t, err = "max_iterations", False, 1, None
+    try:
+        t = 1
+        while True:
+            if t % params.tau == 0:
+                Q_full = B.all_gather_rows(Q_loc, plan.row_counts())
+                labels, info = B.discretize(Q_full, 1, k)
+                if info["empties"] > 0:
+                    raise NetworkError("cannot repair empty clusters: no movable nodes")
+                phi = mhc(labels, "f32")
+                hist.append((t, phi))
+                if phi < best_phi:
+                    best_phi, best = phi, labels.copy()
+                if dq < params.eps_q:
+                    stop, converged = "subspace_converged", True
+                    break
+                if early_stop and len(hist) >= 3 and hist[-3][1] < hist[-2][1] < hist[-1][1]:
+                    stop, converged = "mhc_rising", True
+                    break
+            if t >= params.t_a:
+                break
+            # one f32 orthogonal step (engine.py:130-149), row-partitioned
+            Q_full = B.all_gather_rows(Q_loc, plan.row_counts())
+            Z_loc = op.apply(Q_full, c, "f32")
+            G = B.all_reduce(B.gram(Z_loc, c))
+            Q_loc, dq2_loc = B.cholqr_apply(Z_loc, Q_loc, G, c)
+            dq = float(np.sqrt(B.all_reduce(np.array([dq2_loc]))[0]))
+            t += 1
+    except NetworkError as exc:
+        err, stop = str(exc), "error"
+    return DistResult(best, best_phi, t, stop, hist, converged, err)
+
+
+# ----------------------------------------------------------------------------
+class CudaBackend:
+    """libancka_b200 kernels + NCCL collectives (one rank per GPU)."""
+
+    def __init__(self, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import _lib
+        self.torch, self.dist, self._lib, self.group = torch, dist, _lib, group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        _lib.require_device()
+
+    # --- data
+    def _t(self, a, dtype):
+        return self.torch.as_tensor(a, dtype=dtype).to("cuda")
+
+    def vec(self, a):
+        return self._t(np.asarray(a, dtype=np.float64), self.torch.float64)
+
+    def ivec(self, a):
+        return self._t(np.asarray(a, dtype=np.int32), self.torch.int32)
+
+    def mask(self, a):
+        return self._t(np.asarray(a, dtype=np.uint8), self.torch.uint8)
+
+    def csr(self, m):
+        from ._device import DeviceCSR
+        return DeviceCSR.from_scipy(sp.csr_matrix(m))
+
+    def _ld(self, c, dtype):
+        from ._device import ld_for
+        return ld_for(c, self.torch.float32 if dtype == "f32" else self.torch.float64)
+
+    def rows_from_host(self, a, dtype):
+        from ._device import padded
+        return padded(self.torch.from_numpy(np.ascontiguousarray(a)),
+                      self.torch.float32 if dtype == "f32" else self.torch.float64)
+
+    def to_host(self, a):
+        return a.double().cpu().numpy()
+
+    def to_host_i(self, a):
+        return a.cpu().numpy().astype(np.int64)
+
+    def tagged(self, tag, tagval, c, dtype):
+        torch = self.torch
+        dt = torch.float32 if dtype == "f32" else torch.float64
+        out = torch.zeros((tag.numel(), self._ld(c, dtype)), dtype=dt, device="cuda")
+        rows = torch.nonzero(tag >= 0).flatten()
+        out[rows, tag[rows].long()] = tagval[tag[rows].long()].to(dt)
+        return out
+
+    # --- collectives
+    def all_gather_rows(self, x, counts):
+        torch = self.torch
+        if self.world == 1:
+            return x
+        mx = int(np.max(counts))
+        buf = torch.zeros((mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        buf[: x.shape[0]] = x
+        if self.dist.get_backend(self.group) == "nccl":
+            out = torch.empty((self.world * mx,) + tuple(x.shape[1:]), dtype=x.dtype,
+                              device=x.device)
+            self.dist.all_gather_into_tensor(out, buf, group=self.group)
+            parts = [out[r * mx: r * mx + int(counts[r])] for r in range(self.world)]
+        else:   # gloo (tests): list form
+            lst = [torch.empty_like(buf) for _ in range(self.world)]
+            self.dist.all_gather(lst, buf, group=self.group)
+            parts = [lst[r][: int(counts[r])] for r in range(self.world)]
+        return torch.cat(parts, dim=0)
+
+    def all_reduce(self, a):
+        torch = self.torch
+        t = torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
+    # --- kernels
+    def knn_rows(self, X, K, q0, q1):
+        from .knn import knn_search_exact_device
+        ids, sc = knn_search_exact_device(X, K, rows=(q0, q1))
+        return ids, sc
+
+    def knn_graph_rows(self, ids, scores, n, r0, r1):
+        from ._device import DeviceCSR
+        from .knn import build_knn_graph_device
+        A, P, zero = build_knn_graph_device(ids.int(), scores, n)
+        rp = P.rowptr[r0: r1 + 1]
+        b, e = int(rp[0]), int(rp[-1])
+        loc = DeviceCSR(r1 - r0, n, (rp - b).contiguous(), P.colidx[b:e], P.val64[b:e], P.val32[b:e])
+        return loc, zero.cpu().numpy().astype(bool)
+
+    def spmm(self, S, s_src, Kc, k_src, beta, selfloop, self_src, row_offset, tag, tagval, scale,
+             c, dtype):
+        torch, _lib = self.torch, self._lib
+        f64 = dtype == "f64"
+        dt = torch.float64 if f64 else torch.float32
+        rows = S.rows
+        out = torch.empty((rows, self._ld(c, dtype)), dtype=dt, device="cuda")
+        code = _lib.F64 if f64 else _lib.F32
+
+        def cast(x):
+            return None if x is None else (x if x.dtype == dt else x.to(dt))
+        s_src, k_src, self_src = cast(s_src), cast(k_src), cast(self_src)
+        beta_t, tagval_t = cast(beta), cast(tagval)
+        import ctypes
+        Sst = S.struct(code)
+        Kst = Kc.struct(code) if Kc is not None else None
+        _lib.call("ancka_spmm2", code, rows, c, ctypes.byref(Sst), s_src.data_ptr(),
+                  s_src.stride(0), ctypes.byref(Kst) if Kst is not None else None,
+                  k_src.data_ptr() if k_src is not None else None,
+                  k_src.stride(0) if k_src is not None else 0,
+                  beta_t.data_ptr() if beta_t is not None else None,
+                  selfloop.data_ptr() if selfloop is not None else None,
+                  self_src.data_ptr() if self_src is not None else None,
+                  self_src.stride(0) if self_src is not None else 0, row_offset,
+                  tag.data_ptr() if tag is not None else None,
+                  tagval_t.data_ptr() if tagval_t is not None else None, float(scale),
+                  out.data_ptr(), out.stride(0), _lib.stream())
+        return out
+
+    def gram(self, Z, c):
+        from ._device import WORKSPACE
+        torch, _lib = self.torch, self._lib
+        G = torch.empty(c * (c + 1) // 2, dtype=torch.float64, device="cuda")
+        ws = WORKSPACE.get("dist_orth", _lib.load().ancka_orth_workspace_size(None, c))
+        _lib.call("ancka_gram_f32", Z.data_ptr(), Z.shape[0], Z.stride(0), c, G.data_ptr(),
+                  ws.data_ptr(), ws.numel(), _lib.stream())
+        return G.cpu().numpy()
+
+    def cholqr_apply(self, Z, Qprev, G, c):
+        from ._device import WORKSPACE
+        torch, _lib = self.torch, self._lib
+        Gt = torch.as_tensor(G, device="cuda")
+        Qn = torch.empty_like(Z)
+        stats = torch.tensor([0.0, 1.0, 0.0, 0.0], dtype=torch.float64, device="cuda")
+        ws = WORKSPACE.get("dist_orth", _lib.load().ancka_orth_workspace_size(None, c))
+        _lib.call("ancka_cholqr_apply_f32", Z.data_ptr(), Qprev.data_ptr(), Qn.data_ptr(),
+                  Z.shape[0], Z.stride(0), c, Gt.data_ptr(), stats.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream())
+        return Qn, float(stats[0].item())
+
+    def argmax_rows(self, P, k):
+        return self.torch.argmax(P[:, :k], dim=1).int()
+
+    def trace_labels(self, F, labels_loc, yhat):
+        torch = self.torch
+        lab = torch.as_tensor(labels_loc, device="cuda").long()
+        vals = F[torch.arange(F.shape[0], device="cuda"), lab].double()
+        return float((vals * torch.as_tensor(yhat, device="cuda")[lab]).sum().item())
+
+    def exact_qr_step(self, Z_full, rng):
+        from ._device import padded
+        from .engine import _qr_f64_inplace
+        torch = self.torch
+        c = Z_full.shape[1]
+        z = padded(torch.from_numpy(Z_full), torch.float64)
+        q = z.clone()
+        d = _qr_f64_inplace(q, c)
+        bad = d < 1e-12 * max(1.0, d.max() if d.size else 1.0)
+        if bad.any():
+            warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
+            noise = rng.standard_normal((Z_full.shape[0], int(bad.sum())))
+            cols = torch.from_numpy(np.flatnonzero(bad)).to("cuda")
+            z[:, cols] += 1e-8 * torch.from_numpy(noise).to("cuda")
+            q = z.clone()
+            _qr_f64_inplace(q, c)
+        return q[:, :c].cpu().numpy()
+
+    def discretize(self, Q_full, col0, k):
+        from .engine import DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, _discretize_device
+        torch = self.torch
+        lab = torch.empty(Q_full.shape[0], dtype=torch.int32, device="cuda")
+        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device="cuda")
+        _discretize_device(Q_full, col0, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab, info)
+        inf = info[:8].cpu().numpy()
+        return lab.cpu().numpy().astype(np.int64), {"empties": int(inf[4]), "rounds": int(inf[1])}

@@ -150,8 +150,9 @@ def attributes_to_device(X, level: int = 0) -> DeviceAttributes:
     return DeviceAttributes(X, level)
 
 
-def knn_search_exact_device(X, K: int, integer: int | None = None):
-    """Device exact KNN: returns (ids int32 (n,K), scores f64 (n,K)) tensors.
+def knn_search_exact_device(X, K: int, integer: int | None = None, rows=None):
+    """Device exact KNN: returns (ids int32 (nq,K), scores f64 (nq,K)) tensors
+    for query rows `rows` = (q_begin, q_end) (default: all n) against all keys.
     X: numpy/scipy host matrix, DeviceAttributes, or a dense f64 CUDA tensor."""
     _lib.require_device()
     n, d = X.shape
@@ -172,16 +173,17 @@ def knn_search_exact_device(X, K: int, integer: int | None = None):
             xd = torch.sparse_csr_tensor(xa.indptr, xa.indices.long(), xa.data,
                                          size=xa.shape).to_dense()
     dv = dev()
-    ids = torch.empty((n, K), dtype=torch.int32, device=dv)
-    scores = torch.empty((n, K), dtype=torch.float64, device=dv)
+    q0, q1 = rows if rows is not None else (0, n)
+    ids = torch.empty((q1 - q0, K), dtype=torch.int32, device=dv)
+    scores = torch.empty((q1 - q0, K), dtype=torch.float64, device=dv)
     wsb = _lib.load().ancka_knn_workspace_size(n, d, K, int(integer))
     ws = WORKSPACE.get("knn", wsb)
     if xd is None:
         _lib.call("ancka_knn_exact_csr", xa.indptr.data_ptr(), xa.indices.data_ptr(),
-                  xa.data.data_ptr(), n, d, K, int(integer), ids.data_ptr(), scores.data_ptr(),
-                  ws.data_ptr(), ws.numel(), _lib.stream())
+                  xa.data.data_ptr(), n, d, K, int(integer), q0, q1, ids.data_ptr(),
+                  scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     else:
-        _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer),
+        _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer), q0, q1,
                   ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     return ids, scores
 

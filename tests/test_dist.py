@@ -1,0 +1,251 @@
+"""Multi-process (gloo, world_size 2) checks of the row-partitioned path.
+
+The distributed orchestration (paper_2408_05459_b200/dist.py) is run with a
+numpy/scipy backend on CPU ranks that talk over gloo -- the same code the
+NCCL/CUDA backend runs on GPUs.  It must reproduce the single-process oracle:
+partitioning, all-gathers of Q / T / KNN lists, all-reduced Gram / dQ / MHC
+traces and the replicated steps are all exercised.
+"""
+from __future__ import annotations
+
+import os
+import socket
+import warnings
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import ROOT  # noqa: F401  (puts the repo on sys.path)
+from paper_2408_05459_b200 import dist as D
+from paper_2408_05459_b200 import synth
+from paper_2408_05459_b200.network import AttributedNetwork, ClusterParams, KnnMode
+
+
+class NumpyBackend:
+    """CPU stand-in for CudaBackend: scipy kernels, gloo collectives (f64)."""
+
+    def __init__(self):
+        self.rank = dist.get_rank() if dist.is_initialized() else 0
+        self.world = dist.get_world_size() if dist.is_initialized() else 1
+
+    vec = staticmethod(lambda a: np.asarray(a, dtype=np.float64))
+    ivec = staticmethod(lambda a: np.asarray(a, dtype=np.int32))
+    mask = staticmethod(lambda a: np.asarray(a, dtype=bool))
+    csr = staticmethod(lambda m: sp.csr_matrix(m))
+    rows_from_host = staticmethod(lambda a, dtype: np.array(a, dtype=np.float64))
+    to_host = staticmethod(lambda a: np.asarray(a, dtype=np.float64))
+    to_host_i = staticmethod(lambda a: np.asarray(a, dtype=np.int64))
+
+    @staticmethod
+    def tagged(tag, tagval, c, dtype):
+        out = np.zeros((tag.size, c))
+        r = np.flatnonzero(tag >= 0)
+        out[r, tag[r]] = tagval[tag[r]]
+        return out
+
+    def all_gather_rows(self, x, counts):
+        if self.world == 1:
+            return x
+        x = np.asarray(x)
+        mx = int(np.max(counts))
+        buf = np.zeros((mx,) + x.shape[1:], dtype=np.float64)
+        buf[: x.shape[0]] = x
+        parts = [torch.zeros_like(torch.from_numpy(buf)) for _ in range(self.world)]
+        dist.all_gather(parts, torch.from_numpy(buf))
+        out = np.concatenate([p.numpy()[: int(counts[r])] for r, p in enumerate(parts)])
+        return out.astype(x.dtype)
+
+    def all_reduce(self, a):
+        t = torch.from_numpy(np.array(a, dtype=np.float64))
+        if self.world > 1:
+            dist.all_reduce(t)
+        return t.numpy()
+
+    @staticmethod
+    def knn_rows(X, K, q0, q1):
+        from oracle import ancka_cpu as oc
+        ids, sc = oc.knn_exact(X, K)        # the checker; rows sliced per rank
+        return ids[q0:q1], sc[q0:q1]
+
+    @staticmethod
+    def knn_graph_rows(ids, scores, n, r0, r1):
+        from oracle import ancka_cpu as oc
+        a = oc.knn_adjacency(np.asarray(ids, dtype=np.int64), np.asarray(scores))
+        p, zero = oc.row_stochastic(a)
+        return p[r0:r1], zero
+
+    @staticmethod
+    def spmm(S, s_src, K, k_src, beta, selfloop, self_src, row_offset, tag, tagval, scale, c, dtype):
+        s = S @ np.asarray(s_src)[:, :c]
+        if selfloop is not None and selfloop.any():
+            rows = np.flatnonzero(selfloop)
+            s[rows] += np.asarray(self_src)[row_offset + rows, :c]
+        out = s
+        if beta is not None:
+            b = beta[:, None]
+            out = (1.0 - b) * s + b * (K @ np.asarray(k_src)[:, :c])
+        if tag is not None:
+            add = np.zeros_like(out)
+            r = np.flatnonzero(tag >= 0)
+            add[r, tag[r]] = tagval[tag[r]]
+            out = scale * out + add
+        return out
+
+    @staticmethod
+    def gram(Z, c):
+        g = Z[:, :c].T @ Z[:, :c]
+        return g[np.triu_indices(c)]
+
+    @staticmethod
+    def cholqr_apply(Z, Qprev, G, c):
+        g = np.zeros((c, c))
+        g[np.triu_indices(c)] = G
+        g = g + np.triu(g, 1).T
+        R = np.linalg.cholesky(g).T
+        Q = Z[:, :c] @ np.linalg.inv(R)
+        return Q, float(((Q - Qprev[:, :c]) ** 2).sum())
+
+    argmax_rows = staticmethod(lambda P, k: np.argmax(P[:, :k], axis=1))
+
+    @staticmethod
+    def trace_labels(F, labels_loc, yhat):
+        return float((F[np.arange(F.shape[0]), labels_loc] * yhat[labels_loc]).sum())
+
+    @staticmethod
+    def exact_qr_step(Z, rng):
+        q, r = np.linalg.qr(Z)
+        d = np.abs(np.diag(r))
+        bad = d < 1e-12 * max(1.0, d.max())
+        if bad.any():
+            Z = Z.copy()
+            Z[:, bad] += 1e-8 * rng.standard_normal((Z.shape[0], int(bad.sum())))
+            q, r = np.linalg.qr(Z)
+        return q * np.where(np.diag(r) < 0, -1.0, 1.0)
+
+    @staticmethod
+    def discretize(Q_full, col0, k):
+        from oracle import ancka_cpu as oc
+        d = oc.discretize(np.asarray(Q_full)[:, col0: col0 + k])
+        lab = d["labels"]
+        return lab, {"empties": int((np.bincount(lab, minlength=k) == 0).sum())}
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _case(shape, n, seed):
+    inst = synth.make(shape, seed=seed, n=n)
+    net = (AttributedNetwork.hypergraph(inst.structure, inst.X) if inst.kind == "hypergraph"
+           else AttributedNetwork.graph(inst.structure, inst.X))
+    return inst, net
+
+
+def _worker(rank, world, port, shape, n, seed, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    warnings.simplefilter("ignore")
+    try:
+        inst, net = _case(shape, n, seed)
+        params = ClusterParams(k=inst.k, knn_k=10, seed=seed, knn_mode=KnnMode.EXACT)
+        res = D.run_ancka_dist(net, params, NumpyBackend())
+        out[rank] = (res.labels.tolist(), res.mhc, res.iterations, res.stop_reason)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_rows_balanced():
+    rng = np.random.default_rng(0)
+    cost = rng.integers(1, 50, size=1000).astype(float)
+    for world in (1, 2, 3, 8):
+        b = D.partition_rows(cost, world)
+        assert b[0] == 0 and b[-1] == 1000 and np.all(np.diff(b) >= 0) and b.size == world + 1
+        loads = [cost[b[r]:b[r + 1]].sum() for r in range(world)]
+        assert max(loads) <= cost.sum() / world + cost.max()
+
+
+@pytest.mark.parametrize("shape,n,seed", [("cora", 220, 0), ("dblp", 260, 2)])
+def test_world2_matches_single_process_oracle(shape, n, seed):
+    from sklearn.metrics import adjusted_rand_score
+
+    from oracle import ancka_cpu as oc
+    warnings.simplefilter("ignore")
+    port = _free_port()
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_worker, args=(2, port, shape, n, seed, out), nprocs=2, join=True)
+    inst, _ = _case(shape, n, seed)
+    ref = oc.run({"kind": inst.kind, "S": inst.structure, "X": inst.X}, inst.k, knn_k=10, seed=seed)
+    l0, phi0, it0, stop0 = out[0]
+    l1, phi1, it1, stop1 = out[1]
+    assert l0 == l1 and phi0 == phi1 and it0 == it1          # ranks agree exactly
+    assert adjusted_rand_score(ref["labels"], np.array(l0)) >= 0.99
+    assert it0 == ref["iterations"] and stop0 == ref["stop_reason"]
+    assert abs(phi0 - ref["mhc"]) < 1e-9
+
+
+# ---------------------------------------------------------------------------
+# GPU: the CUDA/NCCL backend of the same orchestration.
+def _golden_net(z, m, i):
+    from conftest import load_csr, load_x
+    p = f"r{i}_"
+    S, X = load_csr(z, p + "S"), load_x(z, p + "X")
+    net = (AttributedNetwork.hypergraph(S, X) if m["kind"] == "hypergraph"
+           else AttributedNetwork.graph(S, X))
+    params = ClusterParams(k=m["k"], knn_k=10, seed=m["seed"], t_a=m["t_a"], knn_mode=KnnMode.EXACT)
+    return net, params
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", range(6))
+def test_cuda_backend_world1_matches_reference(golden_runs, i):
+    from sklearn.metrics import adjusted_rand_score
+    z, meta = golden_runs
+    net, params = _golden_net(z, meta[i], i)
+    res = D.run_ancka_dist(net, params, D.CudaBackend(), early_stop=meta[i]["early_stop"])
+    assert res.error is None, res.error
+    a = adjusted_rand_score(z[f"r{i}_labels"], res.labels)
+    assert a >= 0.99, (i, a, res.iterations, res.stop_reason)
+    assert abs(res.mhc - float(z[f"r{i}_mhc"])) < 1e-3
+
+
+def _gpu_worker(rank, world, port, i, out):
+    import json
+    from conftest import GOLDEN
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # gloo keeps the two ranks' kernels independent on the single test GPU:
+    # the collectives are host-mediated, nothing on the device waits on a peer.
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    warnings.simplefilter("ignore")
+    try:
+        torch.cuda.set_device(0)
+        z = np.load(GOLDEN / "end_to_end.npz")
+        meta = json.loads((GOLDEN / "end_to_end.json").read_text())
+        net, params = _golden_net(z, meta[i], i)
+        res = D.run_ancka_dist(net, params, D.CudaBackend(), early_stop=meta[i]["early_stop"])
+        out[rank] = (res.labels.tolist(), res.mhc, res.iterations, res.error)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("i", [0, 3])
+def test_cuda_backend_world2_collectives(golden_runs, i):
+    from sklearn.metrics import adjusted_rand_score
+    z, meta = golden_runs
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gpu_worker, args=(2, _free_port(), i, out), nprocs=2, join=True)
+    l0, phi0, it0, e0 = out[0]
+    l1, phi1, it1, e1 = out[1]
+    assert e0 is None and e1 is None, (e0, e1)
+    assert l0 == l1 and it0 == it1 and abs(phi0 - phi1) < 1e-12
+    assert adjusted_rand_score(z[f"r{i}_labels"], np.array(l0)) >= 0.99
