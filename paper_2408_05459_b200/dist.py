@@ -265,7 +265,7 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
 
     # ---- t = 1: exact f64 step, replicated on the gathered Z^(1)
     Z1 = op.apply(B.rows_from_host(q0, "f64"), c, "f64")
-    Z1_full = B.to_host(B.all_gather_rows(Z1, plan.row_counts()))
+    Z1_full = B.to_host(B.all_gather_rows(Z1, plan.row_counts()))[:, :c]
     q1 = B.exact_qr_step(Z1_full, rng)
     Q_loc = B.rows_from_host(q1[plan.r0:plan.r1], "f32")
     dq = float(np.linalg.norm(q1 - q0))
