@@ -94,10 +94,15 @@ int ancka_device_check(void);
  * stride ldx elements, dtype f64).  Selection and order follow
  * _ordered_top_k (knn.py:83-98): strictly positive similarities only, j != i,
  * order (similarity desc, index asc); an all-zero row gets an empty list.
- * `integer_exact` != 0 declares every X entry an integer with |x| <= 256 and
- * every row's sum of squares < 2^24: the tcgen05 tensor-core path then
- * computes exact integer dot products and ranks by exact rational
- * comparison.  Otherwise an fp64 CUDA-core path runs.
+ * `integer_exact` selects the path:
+ *   2 / 1  every X entry is an integer with |x| <= 16 (e4m3) / <= 256 (bf16)
+ *          and every row's sum of squares < 2^24: tcgen05 computes exact
+ *          integer dot products, ranked by exact rational comparison;
+ *   0      real-valued X: tcgen05 split-bf16 (hi/lo) contraction with a
+ *          rigorous error bound selects candidates, which are re-ranked with
+ *          exact f64 dots; rows the bound cannot certify are recomputed by
+ *          the f64 CUDA-core scan (ancka_knn_fallback_rows reports how many);
+ *  -1      the f64 CUDA-core scan for every row.
  * Only query rows [q_begin, q_end) are computed (against all n keys): the
  * query-row sharding of the multi-GPU path; [0, n) is the whole matrix.
  * Outputs: ids ((q_end-q_begin) x K int32, -1 padded), scores (same shape,
@@ -107,6 +112,12 @@ int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t 
                     int32_t integer_exact, int64_t q_begin, int64_t q_end, int32_t* ids,
                     double* scores, void* workspace, size_t workspace_bytes,
                     ancka_stream_t stream);
+
+/* Diagnostics of the last integer_exact == 0 call that used this workspace
+ * (same sizes): number of query rows the tensor-core certificate rejected
+ * and the f64 scan recomputed.  Synchronises with the device. */
+int ancka_knn_fallback_rows(void* workspace, size_t workspace_bytes, int64_t n, int64_t d,
+                            int32_t K, int64_t q_begin, int64_t q_end, int32_t* out_rows);
 
 /* Same, with X given as a CSR matrix (indptr n+1, sorted indices, f64 data):
  * the quantised tensor-core operand is built directly from the nonzeros (no

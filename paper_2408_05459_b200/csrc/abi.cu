@@ -47,7 +47,8 @@ static void carve_knn_simt(Carver& cv, int64_t n, int64_t d, double** xn, double
 }
 
 extern "C" size_t ancka_knn_workspace_size(int64_t n, int64_t d, int32_t K, int32_t integer_exact) {
-  if (integer_exact) return knn_tc_workspace(n, d, K);
+  if (integer_exact > 0) return knn_tc_workspace(n, d, K);
+  if (integer_exact == 0) return knn_real_workspace(n, d, K);
   Carver cv(nullptr, 0);
   double *xn, *nr;
   int64_t ldn;
@@ -63,9 +64,11 @@ extern "C" int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ld
   ANCKA_REQUIRE(K >= 1 && d >= 1, ANCKA_ERR_ARG, "knn: bad sizes");
   auto st = as_stream(stream);
   ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
-  if (integer_exact)
+  if (integer_exact > 0)
     return knn_tc(X, n, d, ldx, K, q_begin, q_end, ids, scores, workspace, workspace_bytes, st,
                   integer_exact == 2);
+  if (integer_exact == 0)
+    return knn_real(X, n, d, ldx, K, q_begin, q_end, ids, scores, workspace, workspace_bytes, st);
   Carver cv(workspace, workspace_bytes);
   double *xn, *nr;
   int64_t ldn;
@@ -85,4 +88,11 @@ extern "C" int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices
   ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
   return knn_tc_csr(indptr, indices, data, n, d, K, q_begin, q_end, ids, scores, workspace,
                     workspace_bytes, as_stream(stream), integer_exact == 2);
+}
+
+extern "C" int ancka_knn_fallback_rows(void* workspace, size_t workspace_bytes, int64_t n, int64_t d,
+                                       int32_t K, int64_t q_begin, int64_t q_end,
+                                       int32_t* out_rows) {
+  ANCKA_REQUIRE(out_rows != nullptr, ANCKA_ERR_ARG, "knn_fallback_rows: null output");
+  return knn_real_flag_count(workspace, workspace_bytes, n, d, K, q_begin, q_end, out_rows);
 }

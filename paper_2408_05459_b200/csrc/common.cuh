@@ -110,54 +110,45 @@ __device__ T block_sum(T v, T* smem /* >= 32 */) {
 // numpy's pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
 // pairwise_sum) as used by np.add.reduce / reduceat: r = a[0] + pw(a[1:]).
 // Reproducing it makes row sums bit-identical to scipy's csr.sum(axis=1).
-__device__ __forceinline__ double np_pairwise_rec(const double* a, int64_t n) {
-  // iterative emulation of the recursive split for n <= a few thousand
+template <typename G>
+__device__ __forceinline__ double np_pairwise_rec_g(const G& a, int64_t o, int64_t n) {
   if (n < 8) {
     double res = 0.0;
-    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a[i]);
+    for (int64_t i = 0; i < n; ++i) res = __dadd_rn(res, a(o + i));
     return res;
   }
-  if (n <= 128) {
-    double r[8];
+  double r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = a[j];
-    int64_t i;
-    for (i = 8; i < n - (n % 8); i += 8) {
+  for (int j = 0; j < 8; ++j) r[j] = a(o + j);
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a[i + j]);
-    }
-    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-    for (; i < n; ++i) res = __dadd_rn(res, a[i]);
-    return res;
+    for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], a(o + i + j));
   }
-  return -1.0;  // handled by np_pairwise_sum
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; ++i) res = __dadd_rn(res, a(o + i));
+  return res;
 }
 
-__device__ inline double np_pairwise_sum(const double* a, int64_t n) {
-  // explicit stack for the recursive halving (depth <= 64)
-  struct Frame { const double* p; int64_t n; };
+// pairwise_sum over elements a(o .. o+n-1): the recursive halving
+//   sum(o, n) = sum(o, n2) + sum(o + n2, n - n2),  n2 = n/2 - (n/2) % 8
+// evaluated with an explicit stack; leaves of <= 128 elements use the
+// 8-accumulator loop above.
+template <typename G>
+__device__ inline double np_pairwise_sum_g(const G& a, int64_t n) {
+  struct Frame { int64_t o, n; int dep; };
   Frame stack[64];
   double vals[64];
-  int sp = 0, vp = 0;
-  // post-order evaluation: push (p, n); for n > 128 split into halves
-  // Using a simple recursion-free scheme: process leaves left-to-right and
-  // combine with a stack keyed by depth.
-  int depth_of[64];
-  stack[sp] = {a, n};
-  depth_of[sp] = 0;
-  ++sp;
-  // We evaluate in the same association as the recursion:
-  //   sum(a, n) = sum(a, n2) + sum(a + n2, n - n2),  n2 = n/2 - (n/2) % 8
-  // A leaf's value is combined with its sibling when both are done.
   int vdepth[64];
+  int sp = 0, vp = 0;
+  stack[sp++] = {0, n, 0};
   while (sp) {
     Frame f = stack[--sp];
-    int dep = depth_of[sp];
+    int dep = f.dep;
     if (f.n <= 128) {
-      double v = np_pairwise_rec(f.p, f.n);
-      // combine with completed left siblings at the same depth
-      while (vp > 0 && vdepth[vp - 1] == dep) {
+      double v = np_pairwise_rec_g(a, f.o, f.n);
+      while (vp > 0 && vdepth[vp - 1] == dep) {   // combine with finished left sibling
         v = __dadd_rn(vals[vp - 1], v);
         --vp;
         --dep;
@@ -168,16 +159,15 @@ __device__ inline double np_pairwise_sum(const double* a, int64_t n) {
     } else {
       int64_t n2 = f.n / 2;
       n2 -= n2 % 8;
-      // push right then left so the left half is evaluated first
-      stack[sp] = {f.p + n2, f.n - n2};
-      depth_of[sp] = dep + 1;
-      ++sp;
-      stack[sp] = {f.p, n2};
-      depth_of[sp] = dep + 1;
-      ++sp;
+      stack[sp++] = {f.o + n2, f.n - n2, f.dep + 1};   // right, evaluated second
+      stack[sp++] = {f.o, n2, f.dep + 1};
     }
   }
   return vals[0];
+}
+
+__device__ inline double np_pairwise_sum(const double* a, int64_t n) {
+  return np_pairwise_sum_g([a](int64_t i) { return a[i]; }, n);
 }
 
 }  // namespace ancka

@@ -41,10 +41,28 @@ struct DiscParams {
   int64_t* part_cnt;    // 2 x grid x k
   double* part_arg;     // 2 x grid x 3  (value, index, label)
   double* Rg;           // k x k f64 rotation (row l, col j), written by CTA 0
+  double* red_m;        // k x k + k: two-stage reduction target (k > 8)
   double* info;         // output info
   unsigned long long* tdbg;  // optional phase timing (ANCKA_DISC_TIMING)
   int groups;           // accumulator groups per CTA
 };
+
+// Row i of Q[:, col0:col0+k], normalised in f64 (engine.py:226-232) and
+// rounded to f32 for scoring / accumulation.
+template <int KMAX>
+__device__ __forceinline__ void load_row_f(const DiscParams& p, int64_t i, float* qf, double& nrm) {
+  const float* src = p.Q + i * p.ldq + p.col0;
+  double s = 0.0;
+#pragma unroll
+  for (int l = 0; l < KMAX; ++l) {
+    const double v = l < p.k ? (double)src[l] : 0.0;
+    s += v * v;
+  }
+  nrm = sqrt(s);
+  const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+  for (int l = 0; l < KMAX; ++l) qf[l] = l < p.k ? (float)((double)src[l] * inv) : 0.f;
+}
 
 template <int KMAX>
 __device__ __forceinline__ void load_row(const DiscParams& p, int64_t i, double* q, double& nrm) {
@@ -61,6 +79,8 @@ __device__ __forceinline__ void load_row(const DiscParams& p, int64_t i, double*
 #pragma unroll
   for (int l = 0; l < KMAX; ++l) q[l] *= inv;
 }
+
+__host__ __device__ __forceinline__ int kpad4(int k) { return (k + 3) & ~3; }
 
 struct Rows {
   int64_t r0, r1;
@@ -84,25 +104,67 @@ __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, 
   int zeros = 0;
   for (int64_t t0 = R.r0; t0 < R.r1; t0 += kDiscThreads) {
     const int64_t i = t0 + threadIdx.x;
+    if (KMAX > 8) {
+      // stage the tile's rows with coalesced loads (a warp per row) instead
+      // of k strided loads per thread
+      const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
+      const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+      for (int r = w; r < tr; r += kDiscThreads / 32) {   // async copies: no register round trip
+        const float* src = p.Q + (t0 + r) * p.ldq + p.col0;
+        for (int l = ln; l < k; l += 32)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(tile + r * k + l)),
+                       "l"(src + l)
+                       : "memory");
+      }
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      __syncthreads();
+    }
     if (i < R.r1) {
-      double q[KMAX];
       double nrm;
-      load_row<KMAX>(p, i, q, nrm);
-      if (nrm == 0.0) ++zeros;
       float qf[KMAX];
+      if (KMAX > 8) {
+        const float* row = tile + threadIdx.x * k;
+        double s = 0.0;
 #pragma unroll
-      for (int l = 0; l < KMAX; ++l) qf[l] = (float)q[l];
+        for (int l = 0; l < KMAX; ++l) {
+          const double v = l < k ? (double)row[l] : 0.0;
+          s += v * v;
+        }
+        nrm = sqrt(s);
+        const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+        for (int l = 0; l < KMAX; ++l) qf[l] = l < k ? (float)((double)row[l] * inv) : 0.f;
+      } else {
+        load_row_f<KMAX>(p, i, qf, nrm);
+      }
+      if (nrm == 0.0) ++zeros;
       int lab;
       if (score) {
+        // scores = q~ R: four columns per pass from a padded float4 rotation
+        const int kp = kpad4(k);
         float best = -INFINITY, second = -INFINITY;
         lab = 0;
-        for (int j = 0; j < k; ++j) {
-          float s = 0.f;
+        for (int j0 = 0; j0 < k; j0 += 4) {
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
           for (int l = 0; l < KMAX; ++l)
-            if (l < k) s = fmaf(qf[l], sR[l * k + j], s);
-          if (s > best) { second = best; best = s; lab = j; }
-          else if (s > second) second = s;
+            if (l < k) {
+              const float4 r = *reinterpret_cast<const float4*>(sR + l * kp + j0);
+              s0 = fmaf(qf[l], r.x, s0);
+              s1 = fmaf(qf[l], r.y, s1);
+              s2 = fmaf(qf[l], r.z, s2);
+              s3 = fmaf(qf[l], r.w, s3);
+            }
+          const float sc[4] = {s0, s1, s2, s3};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float s = sc[u];
+            if (j0 + u < k) {
+              if (s > best) { second = best; best = s; lab = j0 + u; }
+              else if (s > second) second = s;
+            }
+          }
         }
         p.labels[i] = lab;
         p.margin[i] = k >= 2 ? second : best;
@@ -203,6 +265,39 @@ __device__ void reduce_partials(const DiscParams& p, int buf, double* M, long lo
   }
   __syncthreads();
 }
+
+// k > 8: two-stage reduction.  Stage 1 (between two grid barriers): CTA b
+// reduces its slice of the k*k + k entries over all partials (fixed order,
+// block tree) into red_m; stage 2: every CTA reads the k*k + k totals.  Each
+// partial is read once instead of once per CTA.
+__device__ void reduce_stage1(const DiscParams& p, int buf, double* red) {
+  const int k = p.k, kk = k * k, nb = gridDim.x, t = threadIdx.x;
+  const double* pm = p.part_m + (size_t)buf * nb * kk;
+  const int64_t* pc = p.part_cnt + (size_t)buf * nb * k;
+  const int ne = kk + k;
+  const int per = (ne + nb - 1) / nb;
+  const int e0 = blockIdx.x * per, e1 = min(ne, e0 + per);
+  for (int e = e0; e < e1; ++e) {
+    double s = 0.0;
+    if (e < kk) {
+      for (int b = t; b < nb; b += blockDim.x) s += pm[(size_t)b * kk + e];
+    } else {
+      for (int b = t; b < nb; b += blockDim.x) s += (double)pc[(size_t)b * k + (e - kk)];
+    }
+    s = block_sum(s, red);
+    if (t == 0) p.red_m[e] = s;
+  }
+}
+
+__device__ void reduce_stage2(const DiscParams& p, double* M, long long* sizes) {
+  const int k = p.k, kk = k * k;
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) M[e] = __ldcg(p.red_m + e);
+  for (int e = threadIdx.x; e < k; e += blockDim.x) sizes[e] = (long long)__ldcg(p.red_m + kk + e);
+  __syncthreads();
+}
+
+__device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
+                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid);
 
 // Every CTA: reduce (value, index, label) partials of buffer `buf`.
 // want_max: first max (larger value, then smaller index), else first min.
@@ -340,28 +435,70 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
   const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
   for (int e = t; e < kk; e += blockDim.x) X[(e % k) * k + e / k] = A[e] * inv;  // A^T
   __syncthreads();
+  // 16 x 16 threads, each a TB x TB register block of the k x k products
+  const int TB = (k + 15) / 16;            // <= 4 for k <= 64
+  const int ty = t / 16, tx = t % 16;
   int it = 0;
   for (; it < 100; ++it) {
-    for (int e = t; e < kk; e += blockDim.x) {            // Y = X^T X
-      const int a = e / k, b = e % k;
-      double v = 0.0;
-      for (int l = 0; l < k; ++l) v += X[l * k + a] * X[l * k + b];
-      Y[e] = v;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int l = 0; l < k; ++l) {            // Y = X^T X: Y[a][b] = sum_l X[l][a] X[l][b]
+      double xa[4], xb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = ty * TB + u, b = tx * TB + u;
+        xa[u] = (u < TB && a < k) ? X[l * k + a] : 0.0;
+        xb[u] = (u < TB && b < k) ? X[l * k + b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] += xa[u] * xb[v];
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int a = ty * TB + u, b = tx * TB + v;
+        if (u < TB && v < TB && a < k && b < k) Y[a * k + b] = acc[u][v];
+      }
     __syncthreads();
     if (t == 0) *flag = 0;
-    for (int e = t; e < kk; e += blockDim.x) {            // T = X Y
-      const int a = e / k, b = e % k;
-      double v = 0.0;
-      for (int l = 0; l < k; ++l) v += X[a * k + l] * Y[l * k + b];
-      T[e] = v;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int l = 0; l < k; ++l) {            // T = X Y: T[a][b] = sum_l X[a][l] Y[l][b]
+      double xa[4], yb[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = ty * TB + u, b = tx * TB + u;
+        xa[u] = (u < TB && a < k) ? X[a * k + l] : 0.0;
+        yb[u] = (u < TB && b < k) ? Y[l * k + b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] += xa[u] * yb[v];
     }
-    __syncthreads();
-    for (int e = t; e < kk; e += blockDim.x) {
-      const double xn = 1.5 * X[e] - 0.5 * T[e];
-      if (fabs(xn - X[e]) > 1e-14 * k) *flag = 1;
-      X[e] = xn;
-    }
+    __syncthreads();                          // all reads of X done
+    bool moved = false;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int a = ty * TB + u, b = tx * TB + v;
+        if (u < TB && v < TB && a < k && b < k) {
+          const double xo = X[a * k + b];
+          const double xn = 1.5 * xo - 0.5 * acc[u][v];
+          moved |= fabs(xn - xo) > 1e-14 * k;
+          X[a * k + b] = xn;
+        }
+      }
+    if (moved) *flag = 1;
     __syncthreads();
     const bool more = *flag != 0;
     __syncthreads();
@@ -376,6 +513,17 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
   if (t == 0) *iters = it;
   __syncthreads();
   return tr;
+}
+
+__device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
+                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid) {
+  if (p.k <= 8) {
+    reduce_partials(p, buf, M, sizes, rsum, rcnt);
+    return;
+  }
+  reduce_stage1(p, buf, red);
+  grid.sync();
+  reduce_stage2(p, M, sizes);
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -399,13 +547,13 @@ discretize_kernel(DiscParams p) {
   unsigned long long t_prev = 0;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) unsigned char smraw[];
-  const int k = p.k, kk = k * k;
+  const int k = p.k, kk = k * k, kp = kpad4(k);
   const int G = p.groups;
   const int nb = gridDim.x;
-  // persistent: scoring rotation (f32) and prototype rotation (f64)
+  // persistent: scoring rotation (f32, rows padded to kp) and prototype rotation (f64)
   float* sR = reinterpret_cast<float*>(smraw);
-  double* sRp = reinterpret_cast<double*>(smraw + align_dev((size_t)kk * 4));
-  unsigned char* dyn = smraw + align_dev((size_t)kk * 4) + align_dev((size_t)kk * 8);
+  double* sRp = reinterpret_cast<double*>(smraw + align_dev((size_t)k * kp * 4));
+  unsigned char* dyn = smraw + align_dev((size_t)k * kp * 4) + align_dev((size_t)kk * 8);
   // phase-A view
   double* acc = reinterpret_cast<double*>(dyn);
   float* tile = reinterpret_cast<float*>(dyn + align_dev((size_t)G * kk * 8));
@@ -437,7 +585,7 @@ discretize_kernel(DiscParams p) {
   for (int run = 0; run < 2; ++run) {
     // ---------------------------------------------------- initial rotation
     if (run == 0) {
-      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (e / k == e % k) ? 1.f : 0.f;
+      for (int e = threadIdx.x; e < k * kp; e += blockDim.x) sR[e] = (e / kp == e % kp) ? 1.f : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = (e / k == e % k) ? 1.0 : 0.0;
     } else {
       // prototype rotation (engine.py:209-218): R[:,0] = q~[0]; greedy rows
@@ -452,16 +600,18 @@ discretize_kernel(DiscParams p) {
       for (int j = 1; j < k; ++j) {
         double best = 0.0;
         long long bi = -1;
-        for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) {
-          double q[KMAX], nrm;
-          load_row<KMAX>(p, i, q, nrm);
-          double d = 0.0;
+        {
+          for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) {
+            double q[KMAX], nrm;
+            load_row<KMAX>(p, i, q, nrm);
+            double d = 0.0;
 #pragma unroll
-          for (int l = 0; l < KMAX; ++l)
-            if (l < k) d += q[l] * sRp[l * k + (j - 1)];
-          const double a = p.proto_acc[i] + fabs(d);
-          p.proto_acc[i] = a;
-          if (bi < 0 || a < best) { best = a; bi = i; }
+            for (int l = 0; l < KMAX; ++l)
+              if (l < k) d += q[l] * sRp[l * k + (j - 1)];
+            const double a = p.proto_acc[i] + fabs(d);
+            p.proto_acc[i] = a;
+            if (bi < 0 || a < best) { best = a; bi = i; }
+          }
         }
         double* part = p.part_arg + (size_t)buf * nb * 3;
         block_arg(best, bi, 0, false, part, sv, si, sl);
@@ -479,7 +629,8 @@ discretize_kernel(DiscParams p) {
         buf ^= 1;
         __syncthreads();
       }
-      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (float)sRp[e];
+      for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
+        sR[e] = e % kp < k ? (float)sRp[(e / kp) * k + e % kp] : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = sRp[e];
     }
     __syncthreads();
@@ -502,7 +653,7 @@ discretize_kernel(DiscParams p) {
         for (int b = 0; b < nb; ++b) z += p.part_cnt[((size_t)(buf ^ 1) * nb + b) * k];
         p.info[5] = (double)z;
       }
-      reduce_partials(p, buf, M, sizes, rsum, rcnt);
+      reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid);
       TSTAMP(2);
       buf ^= 1;
       int nempty = 0;
@@ -539,7 +690,7 @@ discretize_kernel(DiscParams p) {
         }
         phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, false, nullptr);
         grid.sync();
-        reduce_partials(p, buf, M, sizes, rsum, rcnt);
+        reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid);
         buf ^= 1;
       }
       // Y~ = Y / size, polar factor and objective
@@ -566,7 +717,8 @@ discretize_kernel(DiscParams p) {
         break;
       }
       // next rotation R = V U^T (engine.py:205)
-      for (int e = threadIdx.x; e < kk; e += blockDim.x) sR[e] = (float)X[e];
+      for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
+        sR[e] = e % kp < k ? (float)X[(e / kp) * k + e % kp] : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = X[e];
       __syncthreads();
     }
@@ -613,7 +765,7 @@ static int disc_groups(int k) {
 
 static size_t disc_smem(int k, int G) {
   const size_t kk = (size_t)k * k;
-  const size_t fixed = align_dev(kk * 4) + align_dev(kk * 8);
+  const size_t fixed = align_dev((size_t)k * kpad4(k) * 4) + align_dev(kk * 8);
   const size_t a = align_dev((size_t)G * kk * 8) + align_dev((size_t)kDiscThreads * k * 4) +
                    (kDiscThreads + (size_t)G * k) * 4;
   const size_t b = 4 * kk * 8 + (size_t)k * 8;
@@ -633,6 +785,7 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   cv.take<int64_t>((size_t)2 * grid * k);
   cv.take<double>((size_t)2 * grid * 3);
   cv.take<double>((size_t)k * k);
+  cv.take<double>((size_t)k * k + k);
   return cv.used;
 }
 
@@ -677,6 +830,7 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.part_cnt = cv.take<int64_t>((size_t)2 * grid * k);
   p.part_arg = cv.take<double>((size_t)2 * grid * 3);
   p.Rg = cv.take<double>((size_t)k * k);
+  p.red_m = cv.take<double>((size_t)k * k + k);
   p.info = info;
   p.tdbg = getenv("ANCKA_DISC_TIMING") ? (unsigned long long*)(info + 8 + 2 * (size_t)max_iter + 2 * (size_t)k * k) : nullptr;
   p.groups = disc_groups(k);
@@ -686,5 +840,6 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   if (k <= 8) return launch_disc<8>(p, st);
   if (k <= 16) return launch_disc<16>(p, st);
   if (k <= 32) return launch_disc<32>(p, st);
+  if (k <= 48) return launch_disc<48>(p, st);
   return launch_disc<64>(p, st);
 }

@@ -33,86 +33,109 @@ __global__ void normalize_rows_f64_kernel(const double* __restrict__ X, int64_t 
   }
 }
 
+// Query rows are q_begin + local (qlist == nullptr) or qlist[local] for
+// local < *qcount (the uncertified rows of the tensor-core real path); CTAs
+// stride over chunks of BM query rows.
 __global__ void __launch_bounds__(256)
 knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const double* __restrict__ norms,
-                int K, int64_t q_begin, int64_t q_end, int32_t* __restrict__ ids,
-                double* __restrict__ scores) {
+                int K, int64_t q_begin, int64_t q_end, const int32_t* __restrict__ qlist,
+                const int* __restrict__ qcount, int32_t* __restrict__ ids,
+                double* __restrict__ scores, int64_t seg_len, double* __restrict__ part_v,
+                int32_t* __restrict__ part_i) {
   extern __shared__ __align__(16) unsigned char smraw[];
   double* As = reinterpret_cast<double*>(smraw);           // BM x BK
   double* Bs = As + BM * BK;                                // BN x BK
   double* S = Bs + BN * BK;                                 // BM x (BN+1)
   double* lv = S + BM * (BN + 1);                           // BM x K values
   int32_t* li = reinterpret_cast<int32_t*>(lv + (size_t)BM * K);  // BM x K ids
+  int64_t* qrow = reinterpret_cast<int64_t*>(li + (size_t)BM * K + 2);  // BM query rows
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;  // 16 x 16 threads, 4 x 4 each
-  const int64_t q0 = q_begin + (int64_t)blockIdx.x * BM;
-  int fill = 0;                            // list length (owner threads)
-  for (int e = tid; e < BM * K; e += blockDim.x) { lv[e] = 0.0; li[e] = -1; }
-  const int64_t qi = q0 + tid;
-  const bool owner = tid < BM && qi < q_end;
-  const bool qzero = owner ? norms[qi] == 0.0 : true;
-  __syncthreads();
-  for (int64_t k0 = 0; k0 < n; k0 += BN) {
-    double acc[4][4] = {};
-    for (int64_t d0 = 0; d0 < ldn; d0 += BK) {
-      for (int e = tid; e < BM * BK; e += blockDim.x) {
-        const int r = e / BK, c = e % BK;
-        const int64_t qr = q0 + r, kr = k0 + r;
-        As[e] = qr < q_end ? xn[qr * ldn + d0 + c] : 0.0;
-        Bs[e] = kr < n ? xn[kr * ldn + d0 + c] : 0.0;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int c = 0; c < BK; ++c) {
-        double a[4], b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { a[u] = As[(ty * 4 + u) * BK + c]; b[u] = Bs[(tx * 4 + u) * BK + c]; }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
-      }
-      __syncthreads();
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) S[(ty * 4 + u) * (BN + 1) + tx * 4 + v] = acc[u][v];
+  const int64_t nq = qlist ? (int64_t)*qcount : q_end - q_begin;
+  for (int64_t chunk = blockIdx.x; chunk * BM < nq; chunk += gridDim.x) {
+    const int64_t base = chunk * BM;
+    for (int r = tid; r < BM; r += blockDim.x)
+      qrow[r] = base + r < nq ? (qlist ? (int64_t)qlist[base + r] : q_begin + base + r) : -1;
+    int fill = 0;                            // list length (owner threads)
+    for (int e = tid; e < BM * K; e += blockDim.x) { lv[e] = 0.0; li[e] = -1; }
     __syncthreads();
-    if (owner && !qzero) {
-      double* myv = lv + (size_t)tid * K;
-      int32_t* myi = li + (size_t)tid * K;
-      const int jn = (int)lmin(BN, n - k0);
-      for (int jj = 0; jj < jn; ++jj) {
-        const int64_t j = k0 + jj;
-        const double s = S[tid * (BN + 1) + jj];
-        if (j == qi || !(s > 0.0)) continue;
-        if (fill == K && !(s > myv[K - 1])) continue;
-        int pos = fill < K ? fill : K - 1;
-        while (pos > 0 && myv[pos - 1] < s) {
-          myv[pos] = myv[pos - 1];
-          myi[pos] = myi[pos - 1];
-          --pos;
+    const int64_t qi = tid < BM ? qrow[tid] : -1;
+    const bool owner = qi >= 0;
+    const bool qzero = owner ? norms[qi] == 0.0 : true;
+    // key range of this CTA (blockIdx.y segments; one segment = all keys)
+    const int64_t kbeg = (int64_t)blockIdx.y * seg_len;
+    const int64_t kend = lmin(n, kbeg + seg_len);
+    for (int64_t k0 = kbeg; k0 < kend; k0 += BN) {
+      double acc[4][4] = {};
+      for (int64_t d0 = 0; d0 < ldn; d0 += BK) {
+        for (int e = tid; e < BM * BK; e += blockDim.x) {
+          const int r = e / BK, c = e % BK;
+          const int64_t qr = qrow[r], kr = k0 + r;
+          As[e] = qr >= 0 ? xn[qr * ldn + d0 + c] : 0.0;
+          Bs[e] = kr < kend ? xn[kr * ldn + d0 + c] : 0.0;
         }
-        myv[pos] = s;
-        myi[pos] = (int32_t)j;
-        if (fill < K) ++fill;
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < BK; ++c) {
+          double a[4], b[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { a[u] = As[(ty * 4 + u) * BK + c]; b[u] = Bs[(tx * 4 + u) * BK + c]; }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) acc[u][v] = fma(a[u], b[v], acc[u][v]);
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) S[(ty * 4 + u) * (BN + 1) + tx * 4 + v] = acc[u][v];
+      __syncthreads();
+      if (owner && !qzero) {
+        double* myv = lv + (size_t)tid * K;
+        int32_t* myi = li + (size_t)tid * K;
+        const int jn = (int)lmin(BN, kend - k0);
+        for (int jj = 0; jj < jn; ++jj) {
+          const int64_t j = k0 + jj;
+          const double s = S[tid * (BN + 1) + jj];
+          if (j == qi || !(s > 0.0)) continue;
+          if (fill == K && !(s > myv[K - 1])) continue;
+          int pos = fill < K ? fill : K - 1;
+          while (pos > 0 && myv[pos - 1] < s) {
+            myv[pos] = myv[pos - 1];
+            myi[pos] = myi[pos - 1];
+            --pos;
+          }
+          myv[pos] = s;
+          myi[pos] = (int32_t)j;
+          if (fill < K) ++fill;
+        }
+      }
+      __syncthreads();
+    }
+    if (owner && part_v) {                   // partial list of this key segment
+      const int64_t o = ((base + tid) * gridDim.y + blockIdx.y) * K;
+      for (int t = 0; t < K; ++t) {
+        const bool ok = !qzero && t < fill;
+        part_i[o + t] = ok ? li[tid * K + t] : -1;
+        part_v[o + t] = ok ? lv[tid * K + t] : 0.0;
+      }
+    } else if (owner) {
+      const int64_t o = qi - q_begin;
+      for (int t = 0; t < K; ++t) {
+        const bool ok = !qzero && t < fill;
+        ids[o * K + t] = ok ? li[tid * K + t] : -1;
+        scores[o * K + t] = ok ? fmin(lv[tid * K + t], 1.0) : 0.0;
       }
     }
     __syncthreads();
-  }
-  if (tid < BM && qi < q_end) {
-    for (int t = 0; t < K; ++t) {
-      const bool ok = !qzero && t < fill;
-      ids[(qi - q_begin) * K + t] = ok ? li[tid * K + t] : -1;
-      scores[(qi - q_begin) * K + t] = ok ? fmin(lv[tid * K + t], 1.0) : 0.0;
-    }
   }
 }
 
 size_t knn_simt_smem(int K) {
   return sizeof(double) * (BM * BK + BN * BK + BM * (BN + 1) + (size_t)BM * K) +
-         sizeof(int32_t) * (size_t)BM * K;
+         sizeof(int32_t) * ((size_t)BM * K + 2) + sizeof(int64_t) * BM;
 }
 
 int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int K,
@@ -121,7 +144,77 @@ int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int 
   ANCKA_REQUIRE(smem <= 220 * 1024, ANCKA_ERR_UNSUPPORTED, "knn_simt: K=%d too large", K);
   ANCKA_CUDA(cudaFuncSetAttribute(knn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   knn_simt_kernel<<<(unsigned)ceil_div(q_end - q_begin, BM), 256, smem, st>>>(
-      xn, n, ldn, norms, K, q_begin, q_end, ids, scores);
+      xn, n, ldn, norms, K, q_begin, q_end, nullptr, nullptr, ids, scores, n, nullptr, nullptr);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+// merge the per-segment lists of each listed row: order (s desc, j asc)
+__global__ void knn_simt_merge_kernel(const double* __restrict__ part_v,
+                                      const int32_t* __restrict__ part_i, int64_t nrows, int nseg,
+                                      int K, const int32_t* __restrict__ qlist, int64_t q_begin,
+                                      int32_t* __restrict__ ids, double* __restrict__ scores) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = (qlist[r] - q_begin) * K;
+    const double* v = part_v + r * nseg * K;
+    const int32_t* id = part_i + r * nseg * K;
+    int head[64];                                   // cursor per segment (nseg <= 64)
+    for (int s = 0; s < nseg; ++s) head[s] = 0;
+    for (int t = 0; t < K; ++t) {
+      int best = -1;
+      for (int s = 0; s < nseg; ++s) {
+        const int h = head[s];
+        if (h >= K || id[s * K + h] < 0) continue;
+        if (best < 0) { best = s; continue; }
+        const double a = v[s * K + h], b = v[best * K + head[best]];
+        if (a > b || (a == b && id[s * K + h] < id[best * K + head[best]])) best = s;
+      }
+      if (best < 0) { ids[o + t] = -1; scores[o + t] = 0.0; continue; }
+      ids[o + t] = id[best * K + head[best]];
+      scores[o + t] = fmin(v[best * K + head[best]], 1.0);
+      ++head[best];
+    }
+  }
+}
+
+size_t knn_simt_list_workspace(int K) {
+  return (size_t)BM * 2 * kNumSMs * K * (sizeof(double) + sizeof(int32_t)) + 1024;
+}
+
+// Exact f64 rescan of the rows in qlist[0 .. *qcount) (device count; read
+// back here, the KNN phase runs once per clustering).  Few rows are spread
+// over key segments so the rescan uses the whole GPU, then merged.
+int knn_simt_list(const double* xn, int64_t n, int64_t ldn, const double* norms, int K,
+                  int64_t q_begin, const int32_t* qlist, const int* qcount, int32_t* ids,
+                  double* scores, void* ws, size_t wsb, cudaStream_t st) {
+  const size_t smem = knn_simt_smem(K);
+  ANCKA_REQUIRE(smem <= 220 * 1024, ANCKA_ERR_UNSUPPORTED, "knn_simt: K=%d too large", K);
+  int cnt = 0;
+  ANCKA_CUDA(cudaMemcpyAsync(&cnt, qcount, sizeof(int), cudaMemcpyDeviceToHost, st));
+  ANCKA_CUDA(cudaStreamSynchronize(st));
+  if (cnt == 0) return ANCKA_OK;
+  ANCKA_CUDA(cudaFuncSetAttribute(knn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t chunks = ceil_div((int64_t)cnt, BM);
+  int64_t nseg = std::min<int64_t>(std::min<int64_t>(2 * kNumSMs / chunks, 64), ceil_div(n, 4 * BN));
+  if (nseg <= 1) {
+    knn_simt_kernel<<<(unsigned)chunks, 256, smem, st>>>(xn, n, ldn, norms, K, q_begin, 0, qlist,
+                                                        qcount, ids, scores, n, nullptr, nullptr);
+    ANCKA_LAUNCHED();
+    return ANCKA_OK;
+  }
+  const int64_t seg_len = ceil_div(ceil_div(n, nseg), BN) * BN;
+  nseg = ceil_div(n, seg_len);
+  Carver cv(ws, wsb);
+  double* pv = cv.take<double>((size_t)chunks * BM * nseg * K);
+  int32_t* pi = cv.take<int32_t>((size_t)chunks * BM * nseg * K);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_simt_list: workspace too small");
+  dim3 grid((unsigned)chunks, (unsigned)nseg);
+  knn_simt_kernel<<<grid, 256, smem, st>>>(xn, n, ldn, norms, K, q_begin, 0, qlist, qcount, ids,
+                                           scores, seg_len, pv, pi);
+  ANCKA_LAUNCHED();
+  knn_simt_merge_kernel<<<(unsigned)ceil_div(cnt, 128), 128, 0, st>>>(pv, pi, cnt, (int)nseg, K,
+                                                                      qlist, q_begin, ids, scores);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

@@ -10,14 +10,9 @@
 // order the reference's f64 arithmetic approximates.  The n x n similarity
 // matrix never leaves TMEM/registers.
 //
-// CTA = 6 warps, one 128-row query tile x one key segment:
-//   warp 0     TMA producer (A: 128 x 128B, B: 256 x 128B per stage, SW128)
-//   warp 1     TMEM allocator + single-thread MMA issuer (M=128, N=256)
-//   warps 2-5  epilogue: thread t owns query row t (TMEM lane t), streams its
-//              256 accumulator columns per key tile (double-buffered TMEM)
-//              into a register-resident exact top-K list.
-// Segments of the key range run in parallel CTAs; a merge kernel combines
-// their partial lists (same exact order) and emits ids and f64 scores.
+// Pipeline (TMA producer, tcgen05 issuer, TMEM double buffer): knn_tc.cuh.
+// Epilogue warps stream each query row's accumulator columns into a
+// register-resident exact top-K list.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp8.h>
@@ -25,23 +20,12 @@
 
 #include "common.cuh"
 #include "knn.cuh"
+#include "knn_tc.cuh"
 #include "sm100.cuh"
 
 namespace ancka {
 using namespace sm100;
 
-namespace tc {
-constexpr int BM = 128, BN = 256;
-constexpr int STAGES = 4;
-constexpr int ROW_BYTES = 128;                    // one SW128 row per stage
-constexpr int A_BYTES = BM * ROW_BYTES;           // 16 KB
-constexpr int B_BYTES = BN * ROW_BYTES;           // 32 KB
-constexpr int EPI_WARPS = 8;                      // two per TMEM lane quarter
-constexpr int THREADS = 64 + 32 * EPI_WARPS;
-constexpr int EPI_COLS = BN / (EPI_WARPS / 4);    // accumulator columns per epilogue warp
-constexpr int TMEM_COLS = 512;                    // 2 accumulators x 256 columns
-constexpr size_t SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 256 + 32 * EPI_WARPS * 33 * 4;
-}  // namespace tc
 
 struct Entry {
   uint32_t c;  // exact dot count (0 = empty slot)
@@ -168,83 +152,22 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
               TcParams p) {
   using namespace tc;
   extern __shared__ __align__(1024) unsigned char smraw[];
-  unsigned char* base = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  unsigned char* sA = base;
-  unsigned char* sB = base + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-
+  const Pipe P = setup(smraw, &tmA, &tmB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
   const int seg = blockIdx.y;
   const int kt0 = seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
   const int ntiles = kt1 - kt0;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmA);
-    tma_prefetch(&tmB);
-    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
-    fence_barrier_init();
-  }
-  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  const uint32_t tmem = P.tmem;
 
   if (warp == 0) {
-    // ------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int krow = (kt0 + t) * BN;
-        for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait_sleep(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-          tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), (int)q0);
-          tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * ROW_BYTES / (FP8 ? 1 : 2), krow);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-      }
-    }
+    if (lane == 0)
+      producer(P, &tmA, &tmB, kt0, ntiles, p.nkb, (int)q0, [](int kb, int& ca, int& cb) {
+        ca = cb = kb * ROW_BYTES / (FP8 ? 1 : 2);
+      });
   } else if (warp == 1) {
-    // ------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = make_idesc(FP8 ? 0u : 1u, BM, BN);
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = 0; t < ntiles; ++t) {
-        const int acc = t & 1;
-        const uint32_t acc_phase = (t >> 1) & 1;
-        mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t dtm = tmem + acc * BN;
-        for (int kb = 0; kb < p.nkb; ++kb) {
-          mbar_wait_sleep(&full[stage], phase);
-          tc_fence_after();
-          const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
-          const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128-byte row
-            const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
-            const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-            if (p.debug == 2) continue;
-            if (FP8) mma_f8_ss(dtm, ad, bd, idesc, (kb | k) != 0);
-            else mma_f16_ss(dtm, ad, bd, idesc, (kb | k) != 0);
-          }
-          mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
-        }
-        mma_commit(&tfull[acc]);
-      }
-    }
+    if (lane == 0) mma_issuer<FP8>(P, ntiles, p.nkb, p.debug == 2);
   } else {
     // ------------------------------------------------------ epilogue
     const int ew = warp - 2;                      // epilogue warp 0..EPI_WARPS-1
@@ -256,11 +179,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     TopK<KMAX> L;
     L.clear(p.K);
     float published = 0.f;
-    float* stash = reinterpret_cast<float*>(tmem_slot + 4) + (threadIdx.x - 64) * 33;
+    float* stash = P.stash_base + (threadIdx.x - 64) * 33;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
-      mbar_wait_sleep(&tfull[acc], acc_phase);
+      mbar_wait_sleep(&P.tfull[acc], acc_phase);
       if (i < p.q_end) L.raise_floor(__int_as_float(__ldcg(p.row_bound + (i - p.q_begin))));
       tc_fence_after();
       const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
@@ -272,11 +195,14 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         if (ch == EPI_COLS / 32 - 1) {     // this warp's share is in registers
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (lane == 0) mbar_arrive(&P.tempty[acc]);
         }
         if (p.debug == 1) continue;
         // fast filter (branch-free, unrolled): candidate bitmask against the
-        // current K-th key; the rare survivors take one out-of-line slow path
+        // current K-th key; the rare survivors take one out-of-line slow path.
+        // (A max-tree pre-test as in the real-valued kernel does not pay here:
+        // binary attributes give large exact tie groups at the K-th key, so
+        // most 32-column chunks hold a key inside the band.)
         const int64_t jb = j0 + ch * 32;
         uint32_t mask = 0;
 #pragma unroll
@@ -316,9 +242,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
       });
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+  teardown(P);
 }
 
 // Merge the per-segment lists (exact order) and emit ids / f64 cosines.
@@ -377,41 +301,6 @@ __global__ void knn_tc_prep_kernel(const double* __restrict__ X, int64_t n, int6
 }
 
 // --------------------------------------------------------------- host side
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
-static int make_map(CUtensorMap* m, void* ptr, bool fp8, int64_t rows, int64_t row_elems,
-                    int box_rows) {
-  EncodeTiledFn enc = encode_fn();
-  ANCKA_REQUIRE(enc != nullptr, ANCKA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-  const int esz = fp8 ? 1 : 2;
-  cuuint64_t gdim[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
-  cuuint64_t gstride[1] = {(cuuint64_t)(row_elems * esz)};
-  cuuint32_t box[2] = {(cuuint32_t)(tc::ROW_BYTES / esz), (cuuint32_t)box_rows};
-  cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(m, fp8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                   ptr, gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  ANCKA_REQUIRE(r == CUDA_SUCCESS, ANCKA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-  return ANCKA_OK;
-}
-
 struct TcLayout {
   bool fp8;
   int64_t n_pad, d_pad;
@@ -424,12 +313,11 @@ static TcLayout tc_layout(int64_t n, int64_t d, bool fp8, int64_t nq) {
   L.n_pad = ceil_div(n, tc::BN) * tc::BN;
   const int64_t elems_per_row = tc::ROW_BYTES / (fp8 ? 1 : 2);
   L.d_pad = ceil_div(d, elems_per_row) * elems_per_row;
-  L.q_tiles = (int)ceil_div(nq, tc::BM);
-  L.key_tiles = (int)ceil_div(n, tc::BN);
-  int nseg = (int)ceil_div(8 * kNumSMs, L.q_tiles);
-  nseg = std::max(1, std::min(nseg, L.key_tiles));
-  L.tiles_per_seg = (int)ceil_div(L.key_tiles, nseg);
-  L.nseg = (int)ceil_div(L.key_tiles, L.tiles_per_seg);
+  const TcGrid g = tc_grid(n, nq);
+  L.q_tiles = g.q_tiles;
+  L.key_tiles = g.key_tiles;
+  L.nseg = g.nseg;
+  L.tiles_per_seg = g.tiles_per_seg;
   return L;
 }
 
@@ -551,8 +439,8 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
                        int64_t n, int K, int64_t q_begin, int64_t q_end, int32_t* ids,
                        double* scores, cudaStream_t st, bool fp8) {
   CUtensorMap ma, mb;
-  ANCKA_TRY(make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
-  ANCKA_TRY(make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
+  ANCKA_TRY(tc_make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
+  ANCKA_TRY(tc_make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
   TcParams p;
   p.n = n;
   p.q_begin = q_begin;

@@ -1,0 +1,583 @@
+// Exact cosine KNN for real-valued attributes on the tensor cores, with a
+// certificate: knn.py:112-140 (blocked exact scan, strictly positive sims,
+// order (value desc, index asc), scores min(s, 1)).
+//
+// 1. prep      xn = X * (1/||X||) in f64 exactly as _normalize_rows
+//              (knn.py:62-65; the norm is numpy's pairwise sum), and its
+//              split into bf16 hi = rn(xn), lo = rn(xn - hi), stored [hi | lo].
+// 2. contract  a_ij = <hi_i,hi_j> + <hi_i,lo_j> + <lo_i,hi_j> by tcgen05 as one
+//              K = 3 d_pad contraction of [hi|hi|lo] x [hi|lo|hi] (the column
+//              map reads both operands out of the one stored [hi|lo] matrix).
+//              |a_ij - s_ij| <= eps with eps = 2^-16 (split) + 3 d_pad 2^-23
+//              (f32 accumulation), a bound on the unit-vector dot error.
+// 3. filter    each query row keeps its top-L approximate candidates (L > K)
+//              in registers, admitting only a >= max(a_(K) - 2 eps, -eps);
+//              every true top-K member passes: s_(K) >= a_(K) - eps and
+//              s_j >= s_(K) imply a_j >= a_(K) - 2 eps, and s_j > 0 implies
+//              a_j > -eps.
+// 4. rerank    the merged candidates above the threshold get their exact f64
+//              dot <xn_i, xn_j>; the top K by (s desc, j asc) with s > 0 are
+//              emitted.  The row is certified when no candidate that was
+//              dropped for lack of slots could reach the threshold; rows that
+//              are not certified (dense ties, duplicates) are recomputed by
+//              the f64 CUDA-core scan (knn_simt.cu) over all keys.
+// The n x n similarity matrix never leaves TMEM/registers.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "knn.cuh"
+#include "knn_tc.cuh"
+#include "sm100.cuh"
+
+namespace ancka {
+using namespace sm100;
+
+namespace {
+constexpr float kInf = __builtin_huge_valf();
+
+// Register-resident top-(K+E) of approximate cosines, order (a desc, j asc).
+// As in the integer kernel the list has L fixed slots: the first L-E-K hold
+// +inf padding (never displaced), the K+E live entries follow, so the K-th
+// live entry is always slot L-E-1 and the last live one slot L-1 -- no slot
+// is addressed by a runtime index and the arrays stay in registers.
+template <int L, int E>
+struct CandList {
+  static constexpr int KSLOT = L - E - 1;
+  float f[L];
+  int32_t j[L];
+  float thr;     // admission threshold
+  float floor_;  // lower bound below which no candidate can matter
+
+  __device__ __forceinline__ void clear(int K, float base) {
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+      f[t] = t < L - E - K ? kInf : -kInf;
+      j[t] = -1;
+    }
+    thr = floor_ = base;
+  }
+  __device__ __forceinline__ float kth() const { return f[KSLOT]; }
+  __device__ __forceinline__ void refresh(float band) {
+    thr = fmaxf(fmaxf(f[L - 1], f[KSLOT] - band), floor_);
+  }
+  __device__ __forceinline__ void raise_floor(float b) {
+    floor_ = fmaxf(floor_, b);
+    thr = fmaxf(thr, floor_);
+  }
+  __device__ __forceinline__ void insert(float ff, int32_t jj, float band) {
+    int pos = 0;
+#pragma unroll
+    for (int t = 0; t < L; ++t) pos += (f[t] > ff || (f[t] == ff && j[t] < jj)) ? 1 : 0;
+#pragma unroll
+    for (int t = L - 1; t > 0; --t) {
+      const bool sh = t > pos, put = t == pos;
+      f[t] = sh ? f[t - 1] : (put ? ff : f[t]);
+      j[t] = sh ? j[t - 1] : (put ? jj : j[t]);
+    }
+    if (pos == 0) { f[0] = ff; j[0] = jj; }
+    refresh(band);
+  }
+};
+
+template <int K_MAX>
+struct Slots;
+template <> struct Slots<10> { static constexpr int L = 16, E = 6; };
+template <> struct Slots<24> { static constexpr int L = 32, E = 8; };
+
+struct RealParams {
+  int64_t n;
+  int nkb_seg;        // 128-byte k-blocks per operand segment (d_pad / 64)
+  int d_pad;          // bf16 elements per segment
+  int K;
+  int key_tiles, tiles_per_seg, nseg;
+  float eps, band;    // |a - s| bound and 2 eps
+  int2* partial;      // nq x lists x L  (f32 bits, j)
+  uint32_t* row_bound;  // nq: shared pruning floor (order-mapped f32)
+  int64_t q_begin, q_end;
+  int debug;
+};
+}  // namespace
+
+// Epilogue warps (2..): thread = query row (TMEM lane), streams the
+// accumulator columns of every key tile into its candidate list.
+template <int KM>
+__device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
+                                              float* stash_base, const RealParams& p, int64_t q0,
+                                              int seg, int kt0, int ntiles) {
+  using namespace tc;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ew = warp - 2;
+  const int quarter = warp & 3;
+  const int half = ew / 4;
+  const int row = quarter * 32 + lane;
+  const int64_t i = q0 + row;
+  const bool live = i < p.q_end;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr int L = Slots<KM>::L, E = Slots<KM>::E;
+  CandList<L, E> C;
+  C.clear(p.K, -p.eps);
+  float published = -kInf;
+  float* stash = stash_base + (threadIdx.x - 64) * 33;
+  for (int t = 0; t < ntiles; ++t) {
+    const int acc = t & 1;
+    const uint32_t acc_phase = (t >> 1) & 1;
+    mbar_wait_sleep(&tfull[acc], acc_phase);
+    if (live) C.raise_floor(ord2f(__ldcg(p.row_bound + (i - p.q_begin))));
+    tc_fence_after();
+    const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
+#pragma unroll 1
+    for (int ch = 0; ch < EPI_COLS / 32; ++ch) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + ch * 32, r);
+      tmem_ld_wait();
+      if (ch == EPI_COLS / 32 - 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if (p.debug == 1) continue;
+      // common case first: one max tree over the 32 columns (~1 op/column);
+      // the per-column mask and the stash are built only when some column
+      // reaches the admission threshold
+      float mx[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) mx[u] = fmaxf(__uint_as_float(r[u]), __uint_as_float(r[u + 16]));
+#pragma unroll
+      for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+        for (int u = 0; u < w; ++u) mx[u] = fmaxf(mx[u], mx[u + w]);
+      if (mx[0] < C.thr) continue;
+      const int64_t jb = j0 + ch * 32;
+      uint32_t mask = 0;
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const float v = __uint_as_float(r[u]);
+        mask |= (uint32_t)(v >= C.thr) << u;
+        stash[u] = v;
+      }
+      if (i >= jb && i < jb + 32) mask &= ~(1u << (int)(i - jb));   // j != i
+      if (jb + 32 > p.n) mask &= p.n > jb ? (1u << (int)(p.n - jb)) - 1u : 0u;
+#pragma unroll 1
+      while (mask) {
+        const int u = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const float v = stash[u];
+        if (v < C.thr) continue;
+        C.insert(v, (int32_t)(jb + u), p.band);
+        const float b = C.kth() - p.band;
+        if (b > published && live) {
+          atomicMax(p.row_bound + (i - p.q_begin), f2ord(b));
+          published = b;
+        }
+      }
+    }
+  }
+  if (live) {
+    const int lists = p.nseg * (EPI_WARPS / 4);
+    const int live_n = p.K + E, pad = L - live_n;
+    int2* out = p.partial + ((size_t)(i - p.q_begin) * lists + seg * (EPI_WARPS / 4) + half) * live_n;
+#pragma unroll
+    for (int t = 0; t < L; ++t)
+      if (t >= pad) out[t - pad] = make_int2(__float_as_int(C.f[t]), C.j[t]);
+  }
+}
+
+// Streaming variant (any d): A = [hi|hi|lo], B = [hi|lo|hi] k-blocks both
+// streamed through the shared pipeline of knn_tc.cuh.
+template <int KM>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+knn_real_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                RealParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const Pipe P = setup(smraw, &tmA, &tmB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
+  const int seg = blockIdx.y;
+  const int kt0 = seg * p.tiles_per_seg;
+  const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
+  const int ntiles = kt1 - kt0;
+  const int nkb = 3 * p.nkb_seg;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int nks = p.nkb_seg, dp = p.d_pad;
+      producer(P, &tmA, &tmB, kt0, ntiles, nkb, (int)q0, [nks, dp](int kb, int& ca, int& cb) {
+        const int s = kb / nks, off = (kb - s * nks) * (ROW_BYTES / 2);
+        ca = (s == 2 ? dp : 0) + off;    // [hi | hi | lo]
+        cb = (s == 1 ? dp : 0) + off;    // [hi | lo | hi]
+      });
+    }
+  } else if (warp == 1) {
+    if (lane == 0) mma_issuer<false>(P, ntiles, nkb, p.debug == 2);
+  } else {
+    real_epilogue<KM>(P.tfull, P.tempty, P.tmem, P.stash_base, p, q0, seg, kt0, ntiles);
+  }
+  teardown(P);
+}
+
+// Resident-query variant (d_pad <= 192): the CTA's 128 query rows [hi|lo]
+// stay in shared memory for the whole key loop; each key tile streams its
+// [hi|lo] k-blocks once, and every hi block feeds two MMAs (A_hi B_hi,
+// A_lo B_hi), every lo block one (A_hi B_lo).  Shared-memory fill traffic per
+// key tile drops from 3 (128 + 256) d_pad to 2 * 256 d_pad elements.
+namespace res {
+constexpr int B_BYTES = tc::BN * tc::ROW_BYTES;   // 32 KB per k-block of 256 keys
+constexpr int A_BYTES = tc::BM * tc::ROW_BYTES;   // 16 KB per k-block of 128 queries
+constexpr int STASH = 32 * tc::EPI_WARPS * 33 * 4;
+__host__ __device__ constexpr int stages(int nks) { return nks <= 2 ? 4 : 3; }
+__host__ __device__ constexpr size_t smem(int nks) {
+  return 1024 + (size_t)2 * nks * A_BYTES + (size_t)stages(nks) * B_BYTES + 256 + STASH;
+}
+}  // namespace res
+
+template <int KM>
+__global__ void __launch_bounds__(tc::THREADS, 1)
+knn_real_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    RealParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int nks = p.nkb_seg, S = res::stages(nks);
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;                                    // 2 nks k-blocks: hi.., lo..
+  unsigned char* sB = sA + 2 * nks * res::A_BYTES;             // S stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * res::B_BYTES);
+  uint64_t* empty = full + 4;
+  uint64_t* tfull = empty + 4;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
+  float* stash_base = reinterpret_cast<float*>(base + 2 * nks * res::A_BYTES + S * res::B_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
+  const int seg = blockIdx.y;
+  const int kt0 = seg * p.tiles_per_seg;
+  const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
+  const int ntiles = kt1 - kt0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS); }
+    mbar_init(afull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int dp = p.d_pad;
+  constexpr int EL = ROW_BYTES / 2;    // bf16 elements per k-block
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(afull, 2 * nks * res::A_BYTES);
+      for (int kb = 0; kb < nks; ++kb) {
+        tma_load_2d(sA + kb * res::A_BYTES, &tmA, afull, kb * EL, (int)q0);
+        tma_load_2d(sA + (nks + kb) * res::A_BYTES, &tmA, afull, dp + kb * EL, (int)q0);
+      }
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int krow = (kt0 + t) * BN;
+        for (int kb = 0; kb < nks; ++kb)
+          for (int part = 0; part < 2; ++part) {          // hi, then lo
+            mbar_wait_sleep(&empty[stage], phase ^ 1);
+            mbar_arrive_expect_tx(&full[stage], res::B_BYTES);
+            tma_load_2d(sB + stage * res::B_BYTES, &tmB, &full[stage], part * dp + kb * EL, krow);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(1u, BM, BN);
+      const bool skip = p.debug == 2;
+      mbar_wait_sleep(afull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait_sleep(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + acc * BN;
+        for (int kb = 0; kb < nks; ++kb)
+          for (int part = 0; part < 2; ++part) {
+            mbar_wait_sleep(&full[stage], phase);
+            tc_fence_after();
+            const uint32_t b_addr = smem_u32(sB + stage * res::B_BYTES);
+            const uint32_t ahi = smem_u32(sA + kb * res::A_BYTES);
+            const uint32_t alo = smem_u32(sA + (nks + kb) * res::A_BYTES);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
+              if (skip) continue;
+              const bool first = kb == 0 && part == 0 && k == 0;
+              mma_f16_ss(dtm, sw128_kmajor_desc(ahi + k * 32), bd, idesc, !first);  // hi x (hi|lo)
+              if (part == 0) mma_f16_ss(dtm, sw128_kmajor_desc(alo + k * 32), bd, idesc, true);
+            }
+            mma_commit(&empty[stage]);
+            if (++stage == S) { stage = 0; phase ^= 1; }
+          }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    real_epilogue<KM>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// warp per query row: merge the partial lists, certify, rerank in f64
+template <int KM>
+__global__ void knn_real_merge_kernel(const int2* __restrict__ partial, int64_t q_begin,
+                                      int64_t nq, int lists, int K, float eps, float band,
+                                      const double* __restrict__ xn, int64_t ldn, int64_t d,
+                                      const double* __restrict__ norms, int32_t* __restrict__ ids,
+                                      double* __restrict__ scores, int32_t* __restrict__ flagged,
+                                      int* __restrict__ nflag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t li = w0; li < nq; li += nw) {
+    const int64_t i = q_begin + li;
+    int32_t* oid = ids + li * K;
+    double* osc = scores + li * K;
+    if (norms[i] == 0.0) {                       // zero row: empty list
+      for (int t = lane; t < K; t += 32) { oid[t] = -1; osc[t] = 0.0; }
+      continue;
+    }
+    constexpr int L = Slots<KM>::L, E = Slots<KM>::E;
+    const int live_n = K + E;
+    CandList<L, E> M;
+    M.clear(K, -eps);
+    float over = -kInf;                          // best candidate any list dropped
+    for (int s = 0; s < lists; ++s) {
+      const int2* src = partial + ((size_t)li * lists + s) * live_n;
+      over = fmaxf(over, __int_as_float(src[live_n - 1].x));
+      for (int t = 0; t < live_n; ++t) {
+        const int2 e = src[t];
+        if (e.y < 0) break;
+        const float f = __int_as_float(e.x);
+        if (f >= M.thr) M.insert(f, e.y, band);
+      }
+    }
+    const float theta = fmaxf(M.kth() - band, -eps);
+    over = fmaxf(over, M.f[L - 1]);
+    if (!(over < theta)) {                       // not certified: exact rescan later
+      if (lane == 0) flagged[atomicAdd(nflag, 1)] = (int32_t)i;
+      continue;
+    }
+    const double* xi = xn + i * ldn;
+    double sv[L];
+#pragma unroll
+    for (int t = 0; t < L; ++t) {
+      sv[t] = -1.0;
+      if (M.j[t] >= 0 && M.f[t] >= theta) {      // warp-uniform branch
+        const double* xj = xn + (int64_t)M.j[t] * ldn;
+        double acc = 0.0;
+        for (int64_t c = lane; c < d; c += 32) acc = fma(xi[c], xj[c], acc);
+        sv[t] = warp_sum(acc);
+      }
+    }
+    // top K of (s desc, j asc) among s > 0, by repeated selection
+    uint32_t used = 0;
+    for (int r = 0; r < K; ++r) {
+      int best = -1;
+      double bs = 0.0;
+      int32_t bj = 0;
+#pragma unroll
+      for (int t = 0; t < L; ++t) {
+        const bool ok = !((used >> t) & 1u) && sv[t] > 0.0 &&
+                        (best < 0 || sv[t] > bs || (sv[t] == bs && M.j[t] < bj));
+        best = ok ? t : best;
+        bs = ok ? sv[t] : bs;
+        bj = ok ? M.j[t] : bj;
+      }
+      if (best >= 0) used |= 1u << best;
+      if (lane == 0) {
+        oid[r] = best >= 0 ? bj : -1;
+        osc[r] = best >= 0 ? fmin(bs, 1.0) : 0.0;
+      }
+    }
+  }
+}
+
+// f64 X -> xn (f64, ldn, zero padded) + norms + [hi | lo] bf16 (n_pad x 2 d_pad)
+__global__ void knn_real_prep_kernel(const double* __restrict__ X, int64_t n, int64_t d,
+                                     int64_t ldx, int64_t n_pad, int64_t d_pad,
+                                     double* __restrict__ xn, int64_t ldn,
+                                     double* __restrict__ norms, __nv_bfloat16* __restrict__ H) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n_pad; r += nw) {
+    double inv = 0.0;
+    if (r < n) {
+      const double* x = X + r * ldx;
+      double nrm = 0.0;
+      if (lane == 0)  // np.linalg.norm(x, axis=1): sqrt of the pairwise sum of x*x
+        nrm = sqrt(np_pairwise_sum_g([x](int64_t c) { return __dmul_rn(x[c], x[c]); }, d));
+      nrm = __shfl_sync(0xffffffffu, nrm, 0);
+      inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      if (lane == 0) norms[r] = nrm;
+    }
+    __nv_bfloat16* h = H + r * 2 * d_pad;
+    for (int64_t c = lane; c < d_pad; c += 32) {
+      const double v = (r < n && c < d) ? __dmul_rn(X[r * ldx + c], inv) : 0.0;
+      if (r < n && c < ldn) xn[r * ldn + c] = v;
+      const __nv_bfloat16 hi = __double2bfloat16(v);
+      const __nv_bfloat16 lo = __double2bfloat16(v - (double)__bfloat162float(hi));
+      h[c] = hi;
+      h[d_pad + c] = lo;
+    }
+    if (r < n)
+      for (int64_t c = d_pad + lane; c < ldn; c += 32) xn[r * ldn + c] = 0.0;
+  }
+}
+
+// ----------------------------------------------------------------- host side
+namespace {
+struct RealLayout {
+  int64_t n_pad, d_pad, ldn;
+  TcGrid g;
+  int lists;
+};
+
+RealLayout real_layout(int64_t n, int64_t d, int64_t nq) {
+  RealLayout R;
+  R.n_pad = ceil_div(n, tc::BN) * tc::BN;
+  R.d_pad = ceil_div(d, 64) * 64;
+  R.ldn = ceil_div(d, 16) * 16;
+  R.g = tc_grid(n, nq);
+  R.lists = R.g.nseg * (tc::EPI_WARPS / 4);
+  return R;
+}
+
+int real_slots(int K) { return K <= 10 ? Slots<10>::L : Slots<24>::L; }
+
+struct RealWs {
+  __nv_bfloat16* H;
+  double *xn, *norms;
+  uint32_t* rb;
+  int2* part;
+  int32_t* flagged;
+  int* nflag;
+  void* simt_ws;
+  size_t simt_wsb;
+};
+
+void carve_real(Carver& cv, const RealLayout& R, int64_t n, int K, RealWs& w) {
+  const int L = real_slots(K);
+  w.H = cv.take<__nv_bfloat16>((size_t)R.n_pad * 2 * R.d_pad);
+  w.xn = cv.take<double>((size_t)n * R.ldn);
+  w.norms = cv.take<double>(n);
+  w.rb = cv.take<uint32_t>(n);
+  // nq * lists <= (n + 8 * 148 * BM) * 2 for every query range (see tc_grid)
+  w.part = cv.take<int2>(((size_t)n + 8 * kNumSMs * tc::BM) * (tc::EPI_WARPS / 4) * L);
+  w.flagged = cv.take<int32_t>(n);
+  w.nflag = cv.take<int>(1);
+  w.simt_wsb = knn_simt_list_workspace(K);
+  w.simt_ws = cv.take<unsigned char>(w.simt_wsb);
+}
+
+template <int KM>
+int launch_real(const CUtensorMap& ma, const CUtensorMap& mb, const RealParams& p,
+                const RealLayout& R, cudaStream_t st) {
+  dim3 grid(R.g.q_tiles, R.g.nseg);
+  const bool resident = p.nkb_seg <= 3 && !getenv("ANCKA_KNN_STREAM_A");
+  if (resident) {
+    auto kern = knn_real_res_kernel<KM>;
+    const size_t sm = res::smem(p.nkb_seg);
+    ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    kern<<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+  } else {
+    auto kern = knn_real_kernel<KM>;
+    ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc::SMEM));
+    kern<<<grid, tc::THREADS, tc::SMEM, st>>>(ma, mb, p);
+  }
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+}  // namespace
+
+size_t knn_real_workspace(int64_t n, int64_t d, int K) {
+  Carver cv(nullptr, 0);
+  RealWs w;
+  carve_real(cv, real_layout(n, d, n), n, K, w);
+  return cv.used;
+}
+
+int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
+             int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st) {
+  ANCKA_REQUIRE(K <= 24, ANCKA_ERR_UNSUPPORTED, "tensor-core real KNN supports K <= 24 (got %d)", K);
+  ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
+  const int64_t nq = q_end - q_begin;
+  const RealLayout R = real_layout(n, d, nq);
+  Carver cv(ws, wsb);
+  RealWs w;
+  carve_real(cv, R, n, K, w);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_real: workspace too small");
+  const int pg = (int)std::min<int64_t>(ceil_div(R.n_pad * 32, 256), 16 * kNumSMs);
+  knn_real_prep_kernel<<<pg, 256, 0, st>>>(X, n, d, ldx, R.n_pad, R.d_pad, w.xn, R.ldn, w.norms, w.H);
+  ANCKA_LAUNCHED();
+
+  CUtensorMap ma, mb;
+  ANCKA_TRY(tc_make_map(&ma, w.H, false, R.n_pad, 2 * R.d_pad, tc::BM));
+  ANCKA_TRY(tc_make_map(&mb, w.H, false, R.n_pad, 2 * R.d_pad, tc::BN));
+  RealParams p;
+  p.n = n;
+  p.nkb_seg = (int)(R.d_pad / 64);
+  p.d_pad = (int)R.d_pad;
+  p.K = K;
+  p.key_tiles = R.g.key_tiles;
+  p.tiles_per_seg = R.g.tiles_per_seg;
+  p.nseg = R.g.nseg;
+  // |a - s| <= 2^-16 (bf16 hi/lo split of two unit vectors, cross terms and
+  // the dropped lo*lo) + 3 d_pad * 2^-23 (f32 accumulation of the terms)
+  p.eps = (float)(1.6e-5 + 3.0 * (double)R.d_pad * 0x1p-23);
+  if (const char* e = getenv("ANCKA_KNN_EPS")) p.eps = (float)atof(e);
+  p.band = 2.f * p.eps;
+  p.partial = w.part;
+  p.row_bound = w.rb;
+  p.q_begin = q_begin;
+  p.q_end = q_end;
+  p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
+  ANCKA_CUDA(cudaMemsetAsync(w.rb, 0, sizeof(uint32_t) * nq, st));
+  ANCKA_CUDA(cudaMemsetAsync(w.nflag, 0, sizeof(int), st));
+  if (K <= 10) { ANCKA_TRY(launch_real<10>(ma, mb, p, R, st)); }
+  else { ANCKA_TRY(launch_real<24>(ma, mb, p, R, st)); }
+
+  const int mg = (int)std::min<int64_t>(ceil_div(nq * 32, 256), 16 * kNumSMs);
+  if (K <= 10)
+    knn_real_merge_kernel<10><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, p.band,
+                                                  w.xn, R.ldn, d, w.norms, ids, scores, w.flagged, w.nflag);
+  else
+    knn_real_merge_kernel<24><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, p.band,
+                                                  w.xn, R.ldn, d, w.norms, ids, scores, w.flagged, w.nflag);
+  ANCKA_LAUNCHED();
+  // uncertified rows: exact f64 rescan over all keys (device-side count)
+  return knn_simt_list(w.xn, n, R.ldn, w.norms, K, q_begin, w.flagged, w.nflag, ids, scores,
+                       w.simt_ws, w.simt_wsb, st);
+}
+
+int knn_real_flag_count(void* ws, size_t wsb, int64_t n, int64_t d, int K, int64_t q_begin,
+                        int64_t q_end, int* out_host) {
+  const RealLayout R = real_layout(n, d, q_end - q_begin);
+  Carver cv(ws, wsb);
+  RealWs w;
+  carve_real(cv, R, n, K, w);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_real: workspace too small");
+  ANCKA_CUDA(cudaMemcpy(out_host, w.nflag, sizeof(int), cudaMemcpyDeviceToHost));
+  return ANCKA_OK;
+}
+
+}  // namespace ancka

@@ -1,8 +1,9 @@
 """Subsystem 1: exact KNN graph on the B200 (reference: ancka/knn.py).
 
 `knn_search_exact` runs `ancka_knn_exact` (tcgen05 integer-exact path for
-integer-valued attributes such as bag-of-words, f64 CUDA-core path
-otherwise) and `build_knn_adjacency` / `knn_transition` run
+integer-valued attributes such as bag-of-words; tcgen05 split-bf16
+candidates + exact f64 re-rank with an error certificate for real-valued
+attributes, uncertified rows recomputed by the f64 CUDA-core scan) and `build_knn_adjacency` / `knn_transition` run
 `ancka_knn_graph`.  Results stay in HBM; the numpy/scipy views the reference
 API exposes (`NeighborLists.ids`, `KnnGraph.adjacency`, ...) are materialised
 lazily on first access.  Approximate search is not offered: every mode runs
@@ -23,8 +24,11 @@ from ._device import WORKSPACE, DeviceCSR, dev
 from .network import KnnMode, NetworkError
 
 _PAD = -1
-#: route integer-valued attributes to the tcgen05 kernel (knn_tc.cu)
+#: route attributes to the tcgen05 kernels (knn_tc.cu, knn_tc_real.cu); when
+#: False every row takes the f64 CUDA-core scan (level -1)
 TENSOR_CORE_KNN = True
+#: list-length limits of the tensor-core kernels (integer / real-valued)
+TC_MAX_K_INTEGER, TC_MAX_K_REAL = 32, 24
 
 
 class NeighborLists:
@@ -161,15 +165,16 @@ def knn_search_exact_device(X, K: int, integer: int | None = None, rows=None):
     if integer is None:
         integer = (X.level if isinstance(X, DeviceAttributes) else
                    0 if isinstance(X, torch.Tensor) else integer_exact(X))
-    if not (TENSOR_CORE_KNN and K <= 32):
-        integer = 0
+    if (not TENSOR_CORE_KNN or (integer > 0 and K > TC_MAX_K_INTEGER)
+            or (integer == 0 and K > TC_MAX_K_REAL)):
+        integer = -1
     if isinstance(X, torch.Tensor):
         xa = None
         xd = X
     else:
         xa = X if isinstance(X, DeviceAttributes) else DeviceAttributes(X, integer)
         xd = xa.dense
-        if xd is None and integer == 0:  # CSR held for the TC path, f64 path requested
+        if xd is None and integer <= 0:  # CSR held for the integer path, real path requested
             xd = torch.sparse_csr_tensor(xa.indptr, xa.indices.long(), xa.data,
                                          size=xa.shape).to_dense()
     dv = dev()
@@ -185,7 +190,18 @@ def knn_search_exact_device(X, K: int, integer: int | None = None, rows=None):
     else:
         _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer), q0, q1,
                   ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    if integer == 0:
+        out = np.zeros(1, dtype=np.int32)
+        _lib.call("ancka_knn_fallback_rows", ws.data_ptr(), ws.numel(), n, d, K, q0, q1,
+                  out.ctypes.data)
+        LAST_STATS["fallback_rows"] = int(out[0])
+    LAST_STATS["level"] = int(integer)
     return ids, scores
+
+
+#: diagnostics of the last device search: path level and, for real-valued
+#: attributes, how many rows the tensor-core certificate sent to the f64 scan
+LAST_STATS: dict = {}
 
 
 def knn_search_exact(X, K: int, block_rows: int | None = None) -> NeighborLists:

@@ -250,3 +250,34 @@ def test_fused_and_graph_paths_agree(golden_runs, i):
     assert ari(a.y.assignment, b.y.assignment) >= 0.99
     q = a.state.q
     assert np.abs(q.T @ q - np.eye(q.shape[1])).max() < 1e-5   # orthonormal block
+
+
+@pytest.mark.parametrize("n,d,K,dup", [(3000, 100, 10, 0), (1100, 128, 10, 40), (700, 37, 20, 0),
+                                       (257, 300, 5, 0)])
+def test_real_valued_knn_certified(n, d, K, dup):
+    """Real-valued attributes: tcgen05 split-bf16 candidates + f64 re-rank
+    (level 0) must select the reference's sets (tie-aware, f64) and agree with
+    the f64 CUDA-core scan (level -1); duplicated rows force uncertified rows
+    through the fallback scan."""
+    from paper_2408_05459_b200 import knn as kn
+    rng = np.random.default_rng(n + d)
+    lab = rng.integers(0, 7, n)
+    mu = rng.normal(0.0, 2.0, size=(7, d))
+    X = np.abs(mu[lab] + rng.standard_normal((n, d)))
+    if dup:
+        X[n - dup:] = X[0]                      # a tie group of dup+1 identical rows
+        X[5] = 0.0                              # and a zero row
+    ids0, sc0 = kn.knn_search_exact_device(X, K, integer=0)
+    fallback = kn.LAST_STATS.get("fallback_rows")
+    ids1, sc1 = kn.knn_search_exact_device(X, K, integer=-1)
+    ref_ids, ref_sc = oc.knn_exact(X, K)
+    a0 = ids0.cpu().numpy().astype(np.int64)
+    a1 = ids1.cpu().numpy().astype(np.int64)
+    assert knn_sets_match(a0, ref_ids, X, K) == 0
+    assert knn_sets_match(a1, ref_ids, X, K) == 0
+    np.testing.assert_allclose(sc0.cpu().numpy(), ref_sc, rtol=0, atol=1e-14)
+    if dup:
+        assert fallback > 0
+        assert np.all(a0[5] == -1)
+    else:
+        assert fallback == 0

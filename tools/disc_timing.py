@@ -13,12 +13,21 @@ import torch  # noqa: E402
 import paper_2408_05459_b200 as ancka  # noqa: E402
 from paper_2408_05459_b200 import engine, synth  # noqa: E402
 
-inst = synth.make("dblp", seed=0)
-net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
-params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
-res = ancka.run_ancka(net, params)
-q = res.state.q_dev
-k = inst.k
+if len(sys.argv) > 1:   # synthetic block: tools/disc_timing.py n k  (planted + noise)
+    n, k = int(sys.argv[1]), int(sys.argv[2])
+    g = torch.Generator(device="cuda").manual_seed(0)
+    lab0 = torch.randint(0, k, (n,), device="cuda", generator=g)
+    q = torch.zeros((n, 48 if k + 1 <= 48 else k + 1), dtype=torch.float32, device="cuda")
+    q[:, 0] = n ** -0.5
+    q[torch.arange(n, device="cuda"), lab0 + 1] = 1.0
+    q[:, 1:k + 1] += 0.3 * torch.randn((n, k), device="cuda", generator=g)
+else:
+    inst = synth.make("dblp", seed=0)
+    net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
+    params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
+    res = ancka.run_ancka(net, params)
+    q = res.state.q_dev
+    k = inst.k
 lab = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
 info = torch.zeros(8 + 200 + 2 * k * k + 8, dtype=torch.float64, device=q.device)
 for rep in range(3):
