@@ -16,82 +16,176 @@ namespace ancka {
 
 constexpr int kGramThreads = 256;
 constexpr int kGramBlocks = 2 * kNumSMs;
-constexpr int kGramTile = 32;
 constexpr int kApplyBlocks = 8 * kNumSMs;
 
 __device__ __forceinline__ int packed_idx(int a, int b, int c) {  // a <= b
   return a * c - (a * (a - 1)) / 2 + (b - a);
 }
 
-// Each thread owns up to PP upper-triangle pairs; groups of threads split the
-// rows of a tile when there are fewer pairs than threads.
-template <int PP>
+// Register-blocked Gram partials: thread = one 4 x 4 block (bi <= bj) of the
+// upper triangle of Z^T Z; a tile of kGT rows is staged in shared memory with
+// float4 loads (rows of Z are contiguous at stride ld), every row contributes
+// 16 FMAs per two LDS.128.  f32 sums per tile, promoted to f64 per tile; row
+// groups (when there are fewer block pairs than threads) combine in fixed
+// order.  blockIdx.y splits the block pairs for wide blocks (c > 88).
+constexpr int kGT = 64;
 __global__ void __launch_bounds__(kGramThreads)
-gram_partial_kernel(const float* __restrict__ Z, int64_t n, int64_t ld, int c,
+gram_blocked_kernel(const float* __restrict__ Z, int64_t n, int64_t ld, int c,
                     double* __restrict__ partial) {
-  extern __shared__ float tile[];  // kGramTile x c
+  extern __shared__ __align__(16) float gtile[];   // kGT x ld, then reduction scratch
+  const int nb4 = (c + 3) / 4;
+  const int nbp = nb4 * (nb4 + 1) / 2;
   const int npairs = c * (c + 1) / 2;
-  const int groups = npairs >= kGramThreads ? 1 : kGramThreads / npairs;
-  const int slots = npairs >= kGramThreads ? kGramThreads : npairs;
-  const int g = threadIdx.x / slots, slot = threadIdx.x % slots;
-  const bool active = g < groups;
-
-  int pa[PP], pb[PP];
-  float acc32[PP];
-  double acc64[PP];
-#pragma unroll
-  for (int q = 0; q < PP; ++q) {
-    pa[q] = pb[q] = -1;
-    acc64[q] = 0.0;
-    int p = slot + q * slots;
-    if (active && p < npairs) {
-      int a = 0, rem = p;
-      while (rem >= c - a) { rem -= c - a; ++a; }
-      pa[q] = a;
-      pb[q] = a + rem;
-    }
+  const int per_y = (nbp + gridDim.y - 1) / gridDim.y;
+  const int q0 = blockIdx.y * per_y, q1 = min(nbp, q0 + per_y);
+  const int nq = q1 - q0;
+  const int groups = nq >= kGramThreads ? 1 : kGramThreads / nq;
+  const int g = threadIdx.x / nq, q = q0 + threadIdx.x % nq;
+  const bool active = g < groups && threadIdx.x % nq + q0 < q1 && nq > 0;
+  int bi = 0, bj = 0;
+  if (active) {
+    int rem = q;
+    while (rem >= nb4 - bi) { rem -= nb4 - bi; ++bi; }
+    bj = bi + rem;
   }
+  float acc32[16];
+  double acc64[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) acc64[u] = 0.0;
   const int64_t rows_per_block = ceil_div(n, gridDim.x);
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = lmin(n, r0 + rows_per_block);
-  for (int64_t t0 = r0; t0 < r1; t0 += kGramTile) {
-    const int tr = (int)lmin(kGramTile, r1 - t0);
+  const int ld4 = (int)(ld / 4);
+  for (int64_t t0 = r0; t0 < r1; t0 += kGT) {
+    const int tr = (int)lmin(kGT, r1 - t0);
     __syncthreads();
-    for (int e = threadIdx.x; e < tr * c; e += blockDim.x) {
-      int r = e / c, col = e % c;
-      tile[r * c + col] = Z[(t0 + r) * ld + col];
-    }
+    const float4* src = reinterpret_cast<const float4*>(Z + t0 * ld);
+    float4* dst = reinterpret_cast<float4*>(gtile);
+    for (int e = threadIdx.x; e < tr * ld4; e += blockDim.x) dst[e] = __ldg(src + e);
     __syncthreads();
     if (!active) continue;
 #pragma unroll
-    for (int q = 0; q < PP; ++q) acc32[q] = 0.f;
+    for (int u = 0; u < 16; ++u) acc32[u] = 0.f;
     for (int r = g; r < tr; r += groups) {
-      const float* row = tile + r * c;
+      const float4 a = *reinterpret_cast<const float4*>(gtile + r * ld + 4 * bi);
+      const float4 b = *reinterpret_cast<const float4*>(gtile + r * ld + 4 * bj);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int q = 0; q < PP; ++q)
-        if (pa[q] >= 0) acc32[q] = fmaf(row[pa[q]], row[pb[q]], acc32[q]);
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc32[u * 4 + v] = fmaf(av[u], bv[v], acc32[u * 4 + v]);
     }
 #pragma unroll
-    for (int q = 0; q < PP; ++q) acc64[q] += (double)acc32[q];
+    for (int u = 0; u < 16; ++u) acc64[u] += (double)acc32[u];
   }
-  // combine groups in fixed order through shared memory
   __syncthreads();
-  double* red = reinterpret_cast<double*>(tile);  // reuse (>= groups*slots doubles)
-  if (groups > 1) {
-    if (active) red[g * slots + slot] = acc64[0];
-    __syncthreads();
-    if (threadIdx.x < npairs) {
-      double s = 0.0;
-      for (int gg = 0; gg < groups; ++gg) s += red[gg * slots + threadIdx.x];
-      partial[(int64_t)blockIdx.x * npairs + threadIdx.x] = s;
-    }
-  } else {
+  double* red = reinterpret_cast<double*>(gtile);  // groups x nq x 16 doubles
+  if (active) {
 #pragma unroll
-    for (int q = 0; q < PP; ++q) {
-      int p = slot + q * slots;
-      if (p < npairs) partial[(int64_t)blockIdx.x * npairs + p] = acc64[q];
+    for (int u = 0; u < 16; ++u) red[((size_t)g * nq + (threadIdx.x % nq)) * 16 + u] = acc64[u];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < nq * 16; e += blockDim.x) {
+    const int qq = e / 16, u = e % 16;
+    double s2 = 0.0;
+    for (int gg = 0; gg < groups; ++gg) s2 += red[((size_t)gg * nq + qq) * 16 + u];
+    int a0 = 0, rem = q0 + qq;
+    while (rem >= nb4 - a0) { rem -= nb4 - a0; ++a0; }
+    const int a = 4 * a0 + u / 4, b = 4 * (a0 + rem) + u % 4;
+    if (a < c && b < c && a <= b) partial[(int64_t)blockIdx.x * npairs + packed_idx(a, b, c)] = s2;
+  }
+}
+
+// Q = Z R^-1 with ||Q - Q_prev||^2 block partials.  A tile of kAT rows is
+// staged transposed in shared memory (zt[l][r]); a thread computes a 4 x 4
+// block (4 rows x 4 columns) per pass, so one LDS.128 of Z and one of R^-1
+// feed 16 FMAs.
+constexpr int kAT = 64;
+constexpr int kATS = kAT + 4;                     // padded stride of the transposed tile
+__global__ void __launch_bounds__(256)
+apply_rinv_tiled_kernel(const float* __restrict__ Z, const float* __restrict__ Qprev,
+                        float* __restrict__ Q, int64_t n, int64_t ld, int c,
+                        const float* __restrict__ rinv, double* __restrict__ dq_partial) {
+  extern __shared__ __align__(16) float asm_[];
+  float* rs = asm_;                               // c x ld (row l, col j), zero padded
+  float* zt = asm_ + (size_t)c * ld;              // ld x kATS (column l, row r)
+  __shared__ double red[32];
+  for (int e = threadIdx.x; e < c * (int)ld; e += blockDim.x) {
+    const int l = e / (int)ld, j = e % (int)ld;
+    rs[e] = j < c ? rinv[l * c + j] : 0.f;
+  }
+  const int nchunk = (int)(ld / 4);
+  const int npair = (kAT / 4) * nchunk;           // (row group, column chunk) pairs
+  const int ld4 = (int)(ld / 4);
+  double dq = 0.0;
+  for (int64_t t0 = (int64_t)blockIdx.x * kAT; t0 < n; t0 += (int64_t)gridDim.x * kAT) {
+    const int tr = (int)lmin(kAT, n - t0);
+    __syncthreads();
+    const float4* src = reinterpret_cast<const float4*>(Z + t0 * ld);
+    for (int e = threadIdx.x; e < tr * ld4; e += blockDim.x) {
+      const int r = e / ld4, q = e - r * ld4;
+      const float4 v = __ldg(src + e);
+      zt[(4 * q + 0) * kATS + r] = v.x;
+      zt[(4 * q + 1) * kATS + r] = v.y;
+      zt[(4 * q + 2) * kATS + r] = v.z;
+      zt[(4 * q + 3) * kATS + r] = v.w;
+    }
+    __syncthreads();
+    for (int pp = threadIdx.x; pp < npair; pp += blockDim.x) {
+      const int rg = pp / nchunk, ch = pp - rg * nchunk;
+      const int r0 = rg * 4, j0 = ch * 4;
+      if (r0 >= tr) continue;
+      float o[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) o[u][v] = 0.f;
+      const int lmax = min(c, j0 + 4);            // R^-1 is upper triangular
+      for (int l = 0; l < lmax; ++l) {
+        const float4 z = *reinterpret_cast<const float4*>(zt + l * kATS + r0);
+        const float4 w = *reinterpret_cast<const float4*>(rs + l * ld + j0);
+        const float zv[4] = {z.x, z.y, z.z, z.w}, wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) o[u][v] = fmaf(zv[u], wv[v], o[u][v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (r0 + u >= tr) break;
+        const int64_t row = t0 + r0 + u;
+        const float4 prev = *reinterpret_cast<const float4*>(Qprev + row * ld + j0);
+        const float pv[4] = {prev.x, prev.y, prev.z, prev.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const double d = (double)o[u][v] - (double)pv[v];
+          if (j0 + v < c) dq += d * d;
+        }
+        *reinterpret_cast<float4*>(Q + row * ld + j0) = make_float4(o[u][0], o[u][1], o[u][2], o[u][3]);
+      }
     }
   }
+  dq = block_sum(dq, red);
+  if (threadIdx.x == 0) dq_partial[blockIdx.x] = dq;
+}
+
+// Fixed-order reduction of per-block Gram partials, one thread per packed
+// pair (several CTAs), so the single-CTA Cholesky reads one G.
+__global__ void __launch_bounds__(256)
+gram_sum_kernel(const double* __restrict__ partial, int nblocks, int npairs,
+                double* __restrict__ G) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= npairs) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  int b = 0;
+  for (; b + 3 < nblocks; b += 4) {
+    s0 += partial[(int64_t)b * npairs + p];
+    s1 += partial[(int64_t)(b + 1) * npairs + p];
+    s2 += partial[(int64_t)(b + 2) * npairs + p];
+    s3 += partial[(int64_t)(b + 3) * npairs + p];
+  }
+  for (; b < nblocks; ++b) s0 += partial[(int64_t)b * npairs + p];
+  G[p] = (s0 + s1) + (s2 + s3);
 }
 
 // One CTA: reduce Gram partials (fixed order), Cholesky G = R^T R in packed
@@ -177,46 +271,6 @@ chol_kernel(const double* __restrict__ partial, int nblocks, int c, float* __res
   }
 }
 
-// Q = Z R^-1 with ||Q - Q_prev||^2 block partials.
-__global__ void __launch_bounds__(256)
-apply_rinv_kernel(const float* __restrict__ Z, const float* __restrict__ Qprev,
-                  float* __restrict__ Q, int64_t n, int64_t ld, int c,
-                  const float* __restrict__ rinv, double* __restrict__ dq_partial) {
-  extern __shared__ float rs[];  // c x c
-  __shared__ double red[32];
-  for (int e = threadIdx.x; e < c * c; e += blockDim.x) rs[e] = rinv[e];
-  __syncthreads();
-  const int nchunk = (int)((ld + 3) / 4);
-  const int64_t total = n * nchunk;
-  double dq = 0.0;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / nchunk;
-    const int j0 = (int)(t - row * nchunk) * 4;
-    const float* z = Z + row * ld;
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
-    const int jmax = min(c, j0 + 4);
-    for (int l = 0; l < jmax; ++l) {
-      const float zl = z[l];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int j = j0 + u;
-        if (j < c && l <= j) o[u] = fmaf(zl, rs[l * c + j], o[u]);
-      }
-    }
-    const float4 prev = *reinterpret_cast<const float4*>(Qprev + row * ld + j0);
-    const float pv[4] = {prev.x, prev.y, prev.z, prev.w};
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const double d = (double)o[u] - (double)pv[u];
-      if (j0 + u < c) dq += d * d;
-    }
-    *reinterpret_cast<float4*>(Q + row * ld + j0) = make_float4(o[0], o[1], o[2], o[3]);
-  }
-  dq = block_sum(dq, red);
-  if (threadIdx.x == 0) dq_partial[blockIdx.x] = dq;
-}
-
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, int nblocks,
                                        double* __restrict__ out) {
   __shared__ double red[32];
@@ -232,6 +286,7 @@ struct OrthWs {
   double* gram_partial;
   double* dq_partial;
   float* scratch;
+  double* gsum;
 };
 
 static size_t carve_orth(Carver& cv, OrthWs& w, const ancka_operator* op, int c) {
@@ -241,31 +296,37 @@ static size_t carve_orth(Carver& cv, OrthWs& w, const ancka_operator* op, int c)
   w.gram_partial = cv.take<double>((size_t)kGramBlocks * c * (c + 1) / 2);
   w.dq_partial = cv.take<double>(kApplyBlocks);
   w.scratch = cv.take<float>(op && op->kind == ANCKA_HYPERGRAPH ? (size_t)op->m * ld : 1);
+  w.gsum = cv.take<double>((size_t)c * (c + 1) / 2);
   return cv.used;
 }
 
 static int launch_gram(const float* Z, int64_t n, int64_t ld, int c, double* partial,
                        cudaStream_t st) {
-  const int npairs = c * (c + 1) / 2;
-  const int pp = (npairs + kGramThreads - 1) / kGramThreads;
-  const size_t smem = std::max<size_t>((size_t)kGramTile * c * sizeof(float),
-                                       (size_t)kGramThreads * sizeof(double));
-#define GRAM_CASE(P)                                                                    \
-  if (pp <= P) {                                                                        \
-    if (smem > 48 * 1024)                                                               \
-      cudaFuncSetAttribute(gram_partial_kernel<P>,                                      \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    gram_partial_kernel<P><<<kGramBlocks, kGramThreads, smem, st>>>(Z, n, ld, c, partial); \
-    ANCKA_LAUNCHED();                                                                   \
-    return ANCKA_OK;                                                                    \
-  }
-  GRAM_CASE(1)
-  GRAM_CASE(4)
-  GRAM_CASE(16)
-  GRAM_CASE(64)
-#undef GRAM_CASE
-  set_error("gram: block width c=%d too large", c);
-  return ANCKA_ERR_UNSUPPORTED;
+  const int nb4 = (c + 3) / 4;
+  const int nbp = nb4 * (nb4 + 1) / 2;
+  const int ny = (nbp + kGramThreads - 1) / kGramThreads;
+  const int nq = (nbp + ny - 1) / ny;
+  const int groups = nq >= kGramThreads ? 1 : kGramThreads / nq;
+  const size_t smem = std::max<size_t>((size_t)kGT * ld * sizeof(float),
+                                       (size_t)groups * nq * 16 * sizeof(double));
+  if (smem > 48 * 1024)
+    ANCKA_CUDA(cudaFuncSetAttribute(gram_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem));
+  gram_blocked_kernel<<<dim3(kGramBlocks, ny), kGramThreads, smem, st>>>(Z, n, ld, c, partial);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+static int launch_apply(const float* Z, const float* Qprev, float* Qout, int64_t n, int64_t ld,
+                        int c, const float* rinv, double* dq_partial, cudaStream_t st) {
+  const size_t smem = ((size_t)c * ld + (size_t)ld * kATS) * sizeof(float);
+  ANCKA_REQUIRE(smem <= 227 * 1024 && ld / 4 <= 256, ANCKA_ERR_UNSUPPORTED, "apply: c=%d too large", c);
+  if (smem > 48 * 1024)
+    ANCKA_CUDA(cudaFuncSetAttribute(apply_rinv_tiled_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  apply_rinv_tiled_kernel<<<kApplyBlocks, 256, smem, st>>>(Z, Qprev, Qout, n, ld, c, rinv, dq_partial);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
 }
 
 int cholqr_f32(const float* Z, const float* Qprev, float* Qout, int64_t n, int64_t ld, int c,
@@ -277,14 +338,11 @@ int cholqr_f32(const float* Z, const float* Qprev, float* Qout, int64_t n, int64
   ANCKA_REQUIRE(csm <= 227 * 1024, ANCKA_ERR_UNSUPPORTED, "cholqr: c=%d too large", c);
   if (csm > 48 * 1024)
     cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
-  chol_kernel<<<1, 256, csm, st>>>(w.gram_partial, kGramBlocks, c, w.rinv32, w.rdiag, stats);
+  gram_sum_kernel<<<(npairs + 255) / 256, 256, 0, st>>>(w.gram_partial, kGramBlocks, npairs, w.gsum);
   ANCKA_LAUNCHED();
-  const size_t asm_ = (size_t)c * c * sizeof(float);
-  if (asm_ > 48 * 1024)
-    cudaFuncSetAttribute(apply_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
-  apply_rinv_kernel<<<kApplyBlocks, 256, asm_, st>>>(Z, Qprev, Qout, n, ld, c, w.rinv32,
-                                                     w.dq_partial);
+  chol_kernel<<<1, 256, csm, st>>>(w.gsum, 1, c, w.rinv32, w.rdiag, stats);
   ANCKA_LAUNCHED();
+  ANCKA_TRY(launch_apply(Z, Qprev, Qout, n, ld, c, w.rinv32, w.dq_partial, st));
   reduce_partials_kernel<<<1, 256, 0, st>>>(w.dq_partial, kApplyBlocks, stats);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
@@ -406,21 +464,6 @@ extern "C" int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double*
 // ------------------------------------------- split CholQR (multi-GPU path) ---
 // partial Gram of the local rows -> G (packed upper, f64); the caller
 // all-reduces G across ranks, then ancka_cholqr_apply_f32 factors it.
-namespace ancka {
-__global__ void gram_reduce_kernel(const double* __restrict__ partial, int nblocks, int npairs,
-                                   double* __restrict__ G) {
-  for (int p = threadIdx.x; p < npairs; p += blockDim.x) {
-    double s0 = 0.0, s1 = 0.0;
-    int b = 0;
-    for (; b + 1 < nblocks; b += 2) {
-      s0 += partial[(int64_t)b * npairs + p];
-      s1 += partial[(int64_t)(b + 1) * npairs + p];
-    }
-    if (b < nblocks) s0 += partial[(int64_t)b * npairs + p];
-    G[p] = s0 + s1;
-  }
-}
-}  // namespace ancka
 
 extern "C" int ancka_gram_f32(const float* Z, int64_t n, int64_t ld, int32_t c, double* G,
                               void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
@@ -430,7 +473,8 @@ extern "C" int ancka_gram_f32(const float* Z, int64_t n, int64_t ld, int32_t c, 
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "gram: workspace too small");
   auto st = as_stream(stream);
   ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
-  gram_reduce_kernel<<<1, 256, 0, st>>>(w.gram_partial, kGramBlocks, c * (c + 1) / 2, G);
+  gram_sum_kernel<<<(c * (c + 1) / 2 + 255) / 256, 256, 0, st>>>(w.gram_partial, kGramBlocks,
+                                                                 c * (c + 1) / 2, G);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
@@ -451,12 +495,7 @@ extern "C" int ancka_cholqr_apply_f32(const float* Z, const float* Q_prev, float
     cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
   chol_kernel<<<1, 256, csm, st>>>(G, 1, c, w.rinv32, w.rdiag, stats);
   ANCKA_LAUNCHED();
-  const size_t asm_ = (size_t)c * c * sizeof(float);
-  if (asm_ > 48 * 1024)
-    cudaFuncSetAttribute(apply_rinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)asm_);
-  apply_rinv_kernel<<<kApplyBlocks, 256, asm_, st>>>(Z, Q_prev, Q_out, n, ld, c, w.rinv32,
-                                                     w.dq_partial);
-  ANCKA_LAUNCHED();
+  ANCKA_TRY(launch_apply(Z, Q_prev, Q_out, n, ld, c, w.rinv32, w.dq_partial, st));
   reduce_partials_kernel<<<1, 256, 0, st>>>(w.dq_partial, kApplyBlocks, stats);
   ANCKA_LAUNCHED();
   return ANCKA_OK;

@@ -147,15 +147,18 @@ class WalkOperator:
             self._structs[dtype] = s
         return s
 
-    # rows costing more than LONG_ROW nonzeros are cut into PIECE-long pieces
-    LONG_ROW, PIECE, MAX_LD = 64, 32, 256
+    # rows costing more than max(LONG_ROW, HUB_FACTOR x the mean row) nonzeros
+    # (hubs) are cut into PIECE-long pieces; ordinary rows stay one thread group
+    LONG_ROW, HUB_FACTOR, PIECE, MAX_LD = 64, 4, 32, 256
 
     def _split_plan(self) -> _lib.RowSplit:
         """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs)."""
         srp = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"].rowptr.cpu().numpy()
         krp = self.p_k_dev.rowptr.cpu().numpy()
         ls, lk = np.diff(srp), np.diff(krp)
-        long_rows = np.flatnonzero(ls + lk > self.LONG_ROW).astype(np.int32)
+        cost = ls + lk
+        thr = max(self.LONG_ROW, self.HUB_FACTOR * float(cost.mean()) if cost.size else 0.0)
+        long_rows = np.flatnonzero(cost > thr).astype(np.int32)
         if long_rows.size == 0:
             return _lib.RowSplit()
         P = self.PIECE
