@@ -139,6 +139,32 @@ int ancka_knn_graph(const int32_t* ids, const double* scores, int64_t n, int32_t
                     float* p_k32, uint8_t* zero_rows, int64_t* nnz_out,
                     void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
+/* ---- structural factors (walk.py:38-79, 153-174) ----------------------- */
+
+/* _row_normalize (walk.py:38-44): out = (1/rs_i) * a_ij with rs_i the row
+ * sum in numpy/scipy's order (a[b] + pairwise(a[b+1:e])); rows with rs = 0
+ * stay zero.  A is f64 (values required); inv_rows (optional, rows) gets
+ * 1/rs_i (0 for empty rows).  Bit-identical to scipy's diags(inv) @ a. */
+int ancka_csr_row_normalize(const ancka_csr* A, double* out_values, double* inv_rows,
+                            ancka_stream_t stream);
+
+/* out[p] = col_scale[colidx[p]] * values[p]: A D (e.g. P_V^T from H). */
+int ancka_csr_col_scale(const ancka_csr* A, const double* col_scale, double* out_values,
+                        ancka_stream_t stream);
+
+/* CSR transpose (scipy's a.T.tocsr()): t_rowptr (cols+1 int64), t_colidx
+ * (nnz int32, ascending within each row), t_values (nnz f64, optional). */
+size_t ancka_csr_transpose_workspace_size(int64_t rows, int64_t cols, int64_t nnz);
+int ancka_csr_transpose(const ancka_csr* A, int64_t* t_rowptr, int32_t* t_colidx,
+                        double* t_values, void* workspace, size_t workspace_bytes,
+                        ancka_stream_t stream);
+
+/* Attribute checks that select the KNN path (integer_exact levels): out3 =
+ * {1 if some entry is not an integer else 0, max |x|, max row sum of x^2}.
+ * CSR (rowptr != NULL, values = nonzeros) or dense (rowptr NULL, ld, d). */
+int ancka_attr_check(const int64_t* rowptr, const double* values, int64_t rows, int64_t ld,
+                     int64_t d, double* out3, ancka_stream_t stream);
+
 /* ---- subsystem 2: walk operator application ---------------------------- */
 
 /* apply_joint_transition (walk.py:177-190): Z = (I-B) P_struct Q + B P_K Q,

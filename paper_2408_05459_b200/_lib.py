@@ -65,6 +65,13 @@ _SIGS = {
     "ancka_knn_graph": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                   c_size_t, c_void_p]),
+    "ancka_csr_row_normalize": (c_int32, [POINTER(CSR), c_void_p, c_void_p, c_void_p]),
+    "ancka_csr_col_scale": (c_int32, [POINTER(CSR), c_void_p, c_void_p, c_void_p]),
+    "ancka_csr_transpose_workspace_size": (c_size_t, [c_int64, c_int64, c_int64]),
+    "ancka_csr_transpose": (c_int32, [POINTER(CSR), c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_size_t, c_void_p]),
+    "ancka_attr_check": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                   c_void_p]),
     "ancka_op_apply": (c_int32, [_OP, c_void_p, c_int64, c_int32, c_void_p, c_int64, c_void_p,
                                  c_void_p]),
     "ancka_op_apply_struct_t": (c_int32, [_OP, c_void_p, c_int64, c_int32, c_void_p, c_int64,

@@ -335,9 +335,8 @@ def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir
     cache_path = None
     if knn_cache_dir is not None:
         cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
-    level = integer_exact(net.attributes) if K <= 32 else 0
-    return PreparedNetwork(net, K, attributes_to_device(net.attributes, level), level,
-                           StructureFactors(net), cache_path)
+    xd = attributes_to_device(net.attributes, None if K <= 32 else 0)
+    return PreparedNetwork(net, K, xd, xd.level, StructureFactors(net), cache_path)
 
 
 def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):

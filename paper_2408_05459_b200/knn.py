@@ -126,31 +126,51 @@ def integer_exact(X) -> int:
     return 2 if vmax <= 16 else 1
 
 
-class DeviceAttributes:
-    """Attributes resident in HBM: CSR (integer-exact sparse input, fed to the
-    tensor-core kernel as is) or dense f64."""
+def _level_from_checks(nonint: float, vmax: float, sqmax: float) -> int:
+    """integer_exact's rule applied to the device-side checks."""
+    if nonint or vmax > 256 or sqmax >= 2 ** 24:
+        return 0
+    return 2 if vmax <= 16 else 1
 
-    def __init__(self, X, level: int):
+
+class DeviceAttributes:
+    """Attributes resident in HBM: CSR (sparse input on an integer-exact
+    path, fed to the tensor-core kernel as is) or dense f64.  With
+    `level=None` the integer-exact level is decided on the device after the
+    upload (ancka_attr_check), so the host never scans X."""
+
+    def __init__(self, X, level: int | None):
         self.shape = X.shape
-        self.level = level
         d = dev()
-        if sp.issparse(X) and level > 0:
+        self.dense = None
+        if sp.issparse(X):
             x = sp.csr_matrix(X)
             self.indptr = torch.from_numpy(x.indptr.astype(np.int64)).to(d)
             self.indices = torch.from_numpy(x.indices.astype(np.int32)).to(d)
             self.data = torch.from_numpy(x.data.astype(np.float64)).to(d)
-            self.dense = None
-        elif sp.issparse(X):
-            x = sp.csr_matrix(X)
-            t = torch.sparse_csr_tensor(torch.from_numpy(x.indptr.astype(np.int64)),
-                                        torch.from_numpy(x.indices.astype(np.int64)),
-                                        torch.from_numpy(x.data.astype(np.float64)), size=x.shape)
-            self.dense = t.to(d).to_dense().contiguous()
+            if level is None:
+                level = self._check(self.indptr.data_ptr(), self.data.data_ptr(), 0, 0)
+            if level <= 0:
+                t = torch.sparse_csr_tensor(self.indptr, self.indices.long(), self.data,
+                                            size=x.shape)
+                self.dense = t.to_dense().contiguous()
+                self.indptr = self.indices = self.data = None
         else:
             self.dense = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(d)
+            if level is None:
+                level = self._check(None, self.dense.data_ptr(), self.dense.stride(0),
+                                    self.dense.shape[1])
+        self.level = int(level)
+
+    def _check(self, rowptr, values, ld, ncols) -> int:
+        out = torch.empty(3, dtype=torch.float64, device=dev())
+        _lib.call("ancka_attr_check", rowptr, values, self.shape[0], ld, ncols, out.data_ptr(),
+                  _lib.stream())
+        nonint, vmax, sqmax = out.cpu().tolist()
+        return _level_from_checks(nonint, vmax, sqmax)
 
 
-def attributes_to_device(X, level: int = 0) -> DeviceAttributes:
+def attributes_to_device(X, level: int | None = None) -> DeviceAttributes:
     return DeviceAttributes(X, level)
 
 

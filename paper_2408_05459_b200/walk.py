@@ -1,7 +1,8 @@
 """Subsystem 2: the joint-walk operator on the B200 (reference: ancka/walk.py).
 
-Structural factors are normalised on the host with the same scipy calls as
-the reference (O(nnz), once per network) and uploaded; the KNN factor P_K is
+Structural factors are built on the device from the uploaded structure
+(`ancka_csr_row_normalize` / `ancka_csr_transpose` / `ancka_csr_col_scale`,
+bit-identical to the reference's scipy normalisation); the KNN factor P_K is
 produced on the device by `ancka_knn_graph`.  `apply_joint_transition` and
 `apply_structure_rowvec` run `ancka_op_apply` / `ancka_op_apply_struct_t`;
 in f64 they are bit-identical to scipy's csr_matvecs.
@@ -53,9 +54,42 @@ def multiplex_transition(net: AttributedNetwork):
     raise NetworkError("multiplex networks are outside the B200 hot path (SURVEY.md §8f)")
 
 
+def _upload(m: sp.csr_matrix) -> DeviceCSR:
+    d = dev()
+    rp = torch.from_numpy(np.ascontiguousarray(m.indptr, dtype=np.int64)).to(d)
+    ci = torch.from_numpy(np.ascontiguousarray(m.indices, dtype=np.int32)).to(d)
+    v = torch.from_numpy(np.ascontiguousarray(m.data, dtype=np.float64)).to(d)
+    return DeviceCSR(m.shape[0], m.shape[1], rp, ci, v, None)
+
+
+def _with_values(a: DeviceCSR, vals: torch.Tensor) -> DeviceCSR:
+    return DeviceCSR(a.rows, a.cols, a.rowptr, a.colidx, vals, vals.to(torch.float32))
+
+
+def _row_normalize_dev(a: DeviceCSR, want_inv: bool = False):
+    out = torch.empty_like(a.val64)
+    inv = torch.empty(a.rows, dtype=torch.float64, device=out.device) if want_inv else None
+    _lib.call("ancka_csr_row_normalize", a.struct(_lib.F64), out.data_ptr(),
+              None if inv is None else inv.data_ptr(), _lib.stream())
+    return _with_values(a, out), inv
+
+
+def _transpose_dev(a: DeviceCSR) -> DeviceCSR:
+    d = a.colidx.device
+    rp = torch.empty(a.cols + 1, dtype=torch.int64, device=d)
+    ci = torch.empty(a.nnz, dtype=torch.int32, device=d)
+    v = torch.empty(a.nnz, dtype=torch.float64, device=d)
+    wsb = _lib.load().ancka_csr_transpose_workspace_size(a.rows, a.cols, a.nnz)
+    ws = WORKSPACE.get("csr_transpose", wsb)
+    _lib.call("ancka_csr_transpose", a.struct(_lib.F64), rp.data_ptr(), ci.data_ptr(),
+              v.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+    return DeviceCSR(a.cols, a.rows, rp, ci, v, v.to(torch.float32))
+
+
 class StructureFactors:
-    """Host-normalised structural factors uploaded once (walk.py:60-79), plus
-    the init transposes (walk.py:163-165) and the pattern degrees."""
+    """Structural factors (walk.py:60-79), the init transposes (walk.py:163-165)
+    and the pattern degrees, built on the device from one upload of the
+    structure.  Host scipy views (`host_view`) are materialised on access."""
 
     def __init__(self, net: AttributedNetwork):
         if net.kind is NetworkKind.MULTIPLEX:
@@ -64,24 +98,33 @@ class StructureFactors:
         self.degrees = node_degrees(net)
         self.host, self.dev = {}, {}
         if net.kind is NetworkKind.HYPERGRAPH:
-            p_v, p_e = hypergraph_factors(net)
-            self.host.update(p_v=p_v, p_e=p_e)
-            self.dev["p_v"], self.dev["p_e"] = DeviceCSR.from_scipy(p_v), DeviceCSR.from_scipy(p_e)
-            # init_bcm transposes: (p_e^T @ (p_v^T @ m)), walk.py:163
-            self.dev["t_a"] = DeviceCSR.from_scipy(p_v.T.tocsr())
-            self.dev["t_b"] = DeviceCSR.from_scipy(p_e.T.tocsr())
-            self.m = p_e.shape[0]
+            h = _upload(net.incidence)                      # H  (m x n)
+            ht = _transpose_dev(h)                          # H^T (n x m)
+            p_e, _ = _row_normalize_dev(h)                  # P_E = D_E^-1 H
+            p_v, inv_v = _row_normalize_dev(ht, True)       # P_V = D_V^-1 H^T
+            t_a = torch.empty_like(h.val64)                 # P_V^T = H D_V^-1
+            _lib.call("ancka_csr_col_scale", h.struct(_lib.F64), inv_v.data_ptr(),
+                      t_a.data_ptr(), _lib.stream())
+            self.dev.update(p_v=p_v, p_e=p_e, t_a=_with_values(h, t_a), t_b=_transpose_dev(p_e))
+            self.m = h.rows
+            self._up = h.rowptr.numel() * 8 + h.colidx.numel() * 4 + h.val64.numel() * 8
         else:
-            p_n = graph_transition(net)
-            self.host["p_n"] = p_n
-            self.dev["p_n"] = DeviceCSR.from_scipy(p_n)
-            self.dev["t_a"] = DeviceCSR.from_scipy(p_n.T.tocsr())
+            a = symmetrize_union(net.adjacency) if net.directed else net.adjacency
+            A = _upload(a)
+            p_n, _ = _row_normalize_dev(A)
+            self.dev.update(p_n=p_n, t_a=_transpose_dev(p_n))
             self.m = 0
+            self._up = A.rowptr.numel() * 8 + A.colidx.numel() * 4 + A.val64.numel() * 8
         self.degrees_dev = torch.from_numpy(self.degrees).to(dev())
 
+    def host_view(self, name: str):
+        """scipy CSR of a device factor (p_n, p_v, p_e), materialised once."""
+        if name not in self.host and name in self.dev and name in ("p_n", "p_v", "p_e"):
+            self.host[name] = self.dev[name].to_scipy()
+        return self.host.get(name)
+
     def h2d_bytes(self) -> int:
-        return int(sum(m.rowptr.numel() * 8 + m.colidx.numel() * 4 + m.val64.numel() * 8
-                       for m in self.dev.values()) + self.degrees.nbytes)
+        return int(self._up + self.degrees.nbytes)
 
 
 class WalkOperator:
@@ -118,15 +161,15 @@ class WalkOperator:
 
     @property
     def p_n(self):
-        return self._fac.host.get("p_n")
+        return self._fac.host_view("p_n")
 
     @property
     def p_v(self):
-        return self._fac.host.get("p_v")
+        return self._fac.host_view("p_v")
 
     @property
     def p_e(self):
-        return self._fac.host.get("p_e")
+        return self._fac.host_view("p_e")
 
     layer_p = None
 

@@ -22,8 +22,7 @@ for it in range(8):
     net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
     T["construct"] = time.perf_counter() - t0
     t = time.perf_counter(); vnet, _ = network.validate_network(net); T["validate"] = time.perf_counter() - t
-    t = time.perf_counter(); lvl = knn.integer_exact(vnet.attributes); T["integer_exact"] = time.perf_counter() - t
-    t = time.perf_counter(); xd = knn.attributes_to_device(vnet.attributes, lvl); torch.cuda.synchronize(); T["x_to_dev"] = time.perf_counter() - t
+    t = time.perf_counter(); xd = knn.attributes_to_device(vnet.attributes, None); lvl = xd.level; torch.cuda.synchronize(); T["x_to_dev+level"] = time.perf_counter() - t
     t = time.perf_counter(); fac = walk.StructureFactors(vnet); torch.cuda.synchronize(); T["factors"] = time.perf_counter() - t
     prep = engine.PreparedNetwork(vnet, 10, xd, lvl, fac)
     t = time.perf_counter(); res = ancka.run_prepared(prep, params); lab = res.y.assignment; T["run"] = time.perf_counter() - t
