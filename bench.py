@@ -24,7 +24,6 @@ import json
 import os
 import subprocess
 import sys
-import threading
 import time
 import warnings
 from pathlib import Path
@@ -70,55 +69,49 @@ def workload_config(inst, K):
 
 
 # ------------------------------------------------------------------ clocks --
-class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+_SAMPLER = r"""
+import sys, time
+try:
+    import pynvml as nv
+    nv.nvmlInit()
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[1]))
+    bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+            nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+    print("ready", flush=True)
+    while True:
+        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        print(",".join([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]),
+              flush=True)
+        time.sleep(0.05)
+except Exception as exc:
+    print("ready", flush=True)
+    print("error", exc, flush=True)
+"""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+
+class ClockSampler:
+    """SM clocks and clock-event (throttle) reasons sampled by NVML in a
+    separate process during the timed region: no thread of the benchmark
+    process competes for its interpreter lock while kernels are enqueued."""
 
     def __init__(self, index=0):
-        self.index, self.samples, self._stop = index, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _nvml(self):
-        """In-process NVML sampler (no subprocess spawning during timing)."""
-        import pynvml as nv
-        nv.nvmlInit()
-        h = nv.nvmlDeviceGetHandleByIndex(self.index)
-        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        while not self._stop.is_set():
-            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-            self.samples.append([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits])
-            self._stop.wait(0.05)
-
-    def _run(self):
-        try:
-            self._nvml()
-            return
-        except Exception:
-            pass
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([v.strip() for v in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.index, self.samples, self._p = index, [], None
 
     def __enter__(self):
-        self._t.start()
+        self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index)],
+                                   stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self._p.stdout.readline()            # wait until NVML is initialised
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self._p.terminate()                  # this exact child process
+        out, _ = self._p.communicate(timeout=10)
+        for line in out.splitlines():
+            v = [x.strip() for x in line.split(",")]
+            if len(v) == 6:
+                self.samples.append(v)
 
     def summary(self):
         import numpy as np
@@ -256,7 +249,8 @@ def run_ours(args):
             b.synchronize()
             step_ms.append(a.elapsed_time(b))
             launches += res.gpu_launches
-            results.append(res)
+            results = [res]                   # keep one: retained device buffers would
+                                              # force fresh allocations inside timed steps
         gc.enable()
         barrier()
     t_step = float(np.mean(step_ms))

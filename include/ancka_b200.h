@@ -60,6 +60,9 @@ typedef struct {
   const int64_t* piece_end;
   void* partial;              /* n_pieces x max_ld f32 scratch            */
   int64_t max_ld;
+  const int32_t* row_order;   /* n rows by descending cost (optional): the
+                                 fused narrow-block kernel deals rows to its
+                                 lane groups in this order (balanced tails) */
 } ancka_row_split;
 
 /* Device-resident WalkOperator (walk.py:89-104).  Index arrays are shared by

@@ -28,7 +28,7 @@ class RowSplit(ctypes.Structure):
     _fields_ = [("n_long", c_int64), ("n_pieces", c_int64), ("is_long", c_void_p),
                 ("long_rows", c_void_p), ("piece_ptr", c_void_p), ("piece_seg", c_void_p),
                 ("piece_begin", c_void_p), ("piece_end", c_void_p), ("partial", c_void_p),
-                ("max_ld", c_int64)]
+                ("max_ld", c_int64), ("row_order", c_void_p)]
 
 
 class Operator(ctypes.Structure):

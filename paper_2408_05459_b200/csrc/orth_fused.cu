@@ -194,6 +194,7 @@ orth_fused_kernel(OfParams P) {
   const int nb = gridDim.x;
 
   __shared__ double red[(kOfThreads / 32) * kNP];
+  __shared__ float gsm[kOfThreads * (kNP + 1)];
   __shared__ double G[kNP];
   __shared__ float Rinv[kC * kC];
   __shared__ double s_stat[2];
@@ -228,8 +229,9 @@ orth_fused_kernel(OfParams P) {
     const float* Ssrc = hyper ? P.T : Qp;
     // ---- P2: rows (Z + Gram): regular rows by 8-lane groups ...
     const int64_t nround = ((n + noct - 1) / noct) * noct;
-    for (int64_t i = goct; i < nround; i += noct) {
-      const bool live = i < n && !(sp.is_long && sp.is_long[i]);
+    for (int64_t i0 = goct; i0 < nround; i0 += noct) {
+      const int64_t i = (sp.row_order && i0 < n) ? (int64_t)sp.row_order[i0] : i0;
+      const bool live = i0 < n && !(sp.is_long && sp.is_long[i]);
       float s[kC] = {}, kk[kC] = {};
       if (live) {
         seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, 8, s);
@@ -255,38 +257,41 @@ orth_fused_kernel(OfParams P) {
     }
     OF_STAMP(2);
     grid.sync();
-    // ---- P3: Gram partial of this CTA's rows of Z (lane = row, shuffle sums)
+    OF_STAMP(8);
+    // ---- P3: Gram partial of this CTA's rows of Z: thread = row, its 36
+    // f32 products go to shared memory, then 7 threads per entry sum fixed
+    // row subsets in f64 and combine in fixed order; one fixed-point atomic
+    // per entry and CTA (integer sums: order independent, bit-reproducible)
     {
-      const int warp_in = threadIdx.x >> 5;
-      double gq0 = 0.0, gq1 = 0.0;   // lane owns Gram entries lane and lane + 32
       const int64_t rows_per_cta = (n + nb - 1) / nb;
       const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
       const int64_t r1 = lmin(n, r0 + rows_per_cta);
-      for (int64_t base = r0 + warp_in * 32; base < r1; base += (int64_t)blockDim.x) {
-        const int64_t i = base + lane;
-        float z[kC] = {};
-        if (i < r1) f8_load(P.Z + i * kC, z);
-        int q = 0;
+      constexpr int kGS = 7;                       // summing threads per entry
+      const int q = threadIdx.x % kNP, g = threadIdx.x / kNP;
+      double acc = 0.0;
+      for (int64_t base = r0; base < r1; base += kOfThreads) {
+        const int tr = (int)lmin(kOfThreads, r1 - base);
+        __syncthreads();
+        if (threadIdx.x < tr) {
+          float z[kC];
+          f8_load(P.Z + (base + threadIdx.x) * kC, z);
+          int qq = 0;
 #pragma unroll
-        for (int a = 0; a < kC; ++a)
+          for (int a = 0; a < kC; ++a)
 #pragma unroll
-          for (int b2 = a; b2 < kC; ++b2, ++q) {
-            float v = z[a] * z[b2];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == q) gq0 += (double)v;
-            if (lane + 32 == q) gq1 += (double)v;
-          }
+            for (int b2 = a; b2 < kC; ++b2, ++qq) gsm[threadIdx.x * (kNP + 1) + qq] = z[a] * z[b2];
+        }
+        __syncthreads();
+        if (g < kGS)
+          for (int r = g; r < tr; r += kGS) acc += (double)gsm[r * (kNP + 1) + q];
       }
-      red[warp_in * kNP + lane] = gq0;
-      if (lane + 32 < kNP) red[warp_in * kNP + lane + 32] = gq1;
       __syncthreads();
-      for (int q = threadIdx.x; q < kNP; q += blockDim.x) {
+      if (g < kGS) red[g * kNP + q] = acc;
+      __syncthreads();
+      for (int qq = threadIdx.x; qq < kNP; qq += blockDim.x) {
         double v = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) v += red[w * kNP + q];
-        // 64-bit fixed point: integer sums are order independent, so the
-        // grid-wide Gram is bit-reproducible without a partials pass
-        atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + q),
+        for (int gg = 0; gg < kGS; ++gg) v += red[gg * kNP + qq];
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + qq),
                   (unsigned long long)(long long)llrint(v * kFx));
       }
       __syncthreads();
@@ -301,7 +306,7 @@ orth_fused_kernel(OfParams P) {
     if (threadIdx.x == 0) {
       // Cholesky of the padded 8 x 8 Gram (identity on padding), fully
       // unrolled so the factor lives in registers
-      double R[kC][kC], X[kC][kC];
+      double R[kC][kC], X[kC][kC], Rd[kC];
 #pragma unroll
       for (int a2 = 0; a2 < kC; ++a2)
 #pragma unroll
@@ -322,26 +327,28 @@ orth_fused_kernel(OfParams P) {
           if (!(ratio > 1e-9)) { ++bad; piv = fmax(piv, 1e-30 + 1e-9 * fmax(gjj, 0.0)); }
         }
         const double rjj = sqrt(piv);
+        const double irjj = 1.0 / rjj;          // one division per column
         R[j][j] = rjj;
+        Rd[j] = irjj;
 #pragma unroll
         for (int q = j + 1; q < kC; ++q) {
           double v = R[j][q];
 #pragma unroll
           for (int l = 0; l < j; ++l) v -= R[l][j] * R[l][q];
-          R[j][q] = v / rjj;
+          R[j][q] = v * irjj;
         }
       }
 #pragma unroll
       for (int bcol = 0; bcol < kC; ++bcol) {
 #pragma unroll
         for (int a2 = 0; a2 < kC; ++a2) X[a2][bcol] = 0.0;
-        X[bcol][bcol] = 1.0 / R[bcol][bcol];
+        X[bcol][bcol] = Rd[bcol];
 #pragma unroll
         for (int a2 = bcol - 1; a2 >= 0; --a2) {
           double v = 0.0;
 #pragma unroll
           for (int l = a2 + 1; l <= bcol; ++l) v += R[a2][l] * X[l][bcol];
-          X[a2][bcol] = -v / R[a2][a2];
+          X[a2][bcol] = -v * Rd[a2];
         }
       }
 #pragma unroll
@@ -431,7 +438,8 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
   ANCKA_CUDA(cudaGetDevice(&dev));
   ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   ANCKA_REQUIRE(per_sm >= 1, ANCKA_ERR_UNSUPPORTED, "orth_block does not fit an SM");
-  const int64_t want = ceil_div(op32->n, 32);
+  int64_t want = ceil_div(op32->n, 32);
+  if (const char* g = getenv("ANCKA_ORTH_GRID")) want = std::max(1, atoi(g));
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
       want, std::min<int64_t>((int64_t)per_sm * sms, of_grid_cap())));
   void* args[] = {&P};

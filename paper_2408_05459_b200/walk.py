@@ -202,8 +202,14 @@ class WalkOperator:
         cost = ls + lk
         thr = max(self.LONG_ROW, self.HUB_FACTOR * float(cost.mean()) if cost.size else 0.0)
         long_rows = np.flatnonzero(cost > thr).astype(np.int32)
+        d = dev()
+        # regular rows by descending cost (stable): the fused kernel deals them
+        # round-robin to its lane groups, so every group gets a similar load
+        order = np.argsort(-cost, kind="stable").astype(np.int32)
+        self._order = torch.from_numpy(order).to(d)
         if long_rows.size == 0:
-            return _lib.RowSplit()
+            return _lib.RowSplit(0, 0, None, None, None, None, None, None, None, 0,
+                                 self._order.data_ptr())
         P = self.PIECE
         ns = -(-ls[long_rows] // P)                   # structural pieces per long row
         nk = -(-lk[long_rows] // P)                   # KNN pieces per long row
@@ -219,7 +225,6 @@ class WalkOperator:
         begins = rb + qq * P
         ends = np.minimum(re, begins + P)
         segs = is_k.astype(np.int32)
-        d = dev()
         mask = np.zeros(self.n, dtype=np.uint8)
         mask[long_rows] = 1
         self._plan = {
@@ -235,7 +240,8 @@ class WalkOperator:
         return _lib.RowSplit(long_rows.size, len(segs), p["is_long"].data_ptr(),
                              p["long_rows"].data_ptr(), p["piece_ptr"].data_ptr(),
                              p["piece_seg"].data_ptr(), p["piece_begin"].data_ptr(),
-                             p["piece_end"].data_ptr(), p["partial"].data_ptr(), self.MAX_LD)
+                             p["piece_end"].data_ptr(), p["partial"].data_ptr(), self.MAX_LD,
+                             self._order.data_ptr())
 
     def scratch(self, c: int, dtype: torch.dtype, key: str = "op_scratch") -> torch.Tensor:
         rows = max(self.m, 1)
