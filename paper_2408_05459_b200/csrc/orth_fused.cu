@@ -22,6 +22,7 @@ namespace cg = cooperative_groups;
 namespace ancka {
 
 constexpr int kOfThreads = 256;
+constexpr int kGW = 4;                      // lanes per regular row / hyperedge
 constexpr int kC = 8;                       // padded block width
 constexpr int kNP = kC * (kC + 1) / 2;      // Gram upper-triangle entries
 constexpr double kFx = 1125899906842624.0;  // 2^50 fixed-point scale of Gram sums
@@ -207,9 +208,9 @@ orth_fused_kernel(OfParams P) {
     const int buf = step & 1;
     // row groups: 8 lanes per regular row, a whole warp per long row
     const int lane = threadIdx.x & 31;
-    const int sub = lane & 7;
+    const int sub = lane & (kGW - 1);
     const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
-    const int64_t goct = gtid >> 3, noct = gsz >> 3;
+    const int64_t goct = gtid / kGW, noct = gsz / kGW;
     // ---- P1: T = P_E Q (hypergraph)
     if (hyper) {
       const float* Eval = static_cast<const float*>(op.p_e.values);
@@ -218,8 +219,8 @@ orth_fused_kernel(OfParams P) {
         const int64_t e = e0;
         float acc[kC] = {};
         if (e < m) seg8_strided(op.p_e.colidx, Eval, Qp, op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
-                                sub, 8, acc);
-        group_sum(acc, 8);
+                                sub, kGW, acc);
+        group_sum(acc, kGW);
         if (e < m && sub == 0) f8_store(P.T + e * kC, acc);
       }
       OF_STAMP(0);
@@ -227,6 +228,8 @@ orth_fused_kernel(OfParams P) {
       OF_STAMP(1);
     }
     const float* Ssrc = hyper ? P.T : Qp;
+    unsigned long long p2_t0 = 0;
+    if (P.tdbg && threadIdx.x == 0) p2_t0 = of_timer();
     // ---- P2: rows (Z + Gram): regular rows by 8-lane groups ...
     const int64_t nround = ((n + noct - 1) / noct) * noct;
     for (int64_t i0 = goct; i0 < nround; i0 += noct) {
@@ -234,11 +237,11 @@ orth_fused_kernel(OfParams P) {
       const bool live = i0 < n && !(sp.is_long && sp.is_long[i]);
       float s[kC] = {}, kk[kC] = {};
       if (live) {
-        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, 8, s);
-        seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], sub, 8, kk);
+        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, kGW, s);
+        seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], sub, kGW, kk);
       }
-      group_sum(s, 8);
-      group_sum(kk, 8);
+      group_sum(s, kGW);
+      group_sum(kk, kGW);
       if (live && sub == 0) finish8(P, i, Qp, s, kk);
     }
     // ... and long rows (KNN hubs) by whole warps
@@ -256,6 +259,14 @@ orth_fused_kernel(OfParams P) {
       if (live && lane == 0) finish8(P, i, Qp, s, kk);
     }
     OF_STAMP(2);
+    if (P.tdbg) {                        // per-CTA P2 duration: max and sum over CTAs
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long dt = of_timer() - p2_t0;
+        atomicMax(P.tdbg + 9, dt);
+        atomicAdd(P.tdbg + 10, dt);
+      }
+    }
     grid.sync();
     OF_STAMP(8);
     // ---- P3: Gram partial of this CTA's rows of Z: thread = row, its 36

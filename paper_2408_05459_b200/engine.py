@@ -147,8 +147,15 @@ def _init_labels_device(op: WalkOperator, k: int, t_i: int, alpha: float):
     n = op.n
     if k > n:
         raise NetworkError(f"k={k} exceeds node count n={n}")
-    centers = _centers(op.degrees, k)
-    cdev = torch.from_numpy(centers).to(dev())
+    cache = op._fac.__dict__.setdefault("_centers_cache", {})   # degrees are per network
+    if k not in cache:
+        with warnings.catch_warnings(record=True) as wr:
+            warnings.simplefilter("always")
+            c_host = _centers(op.degrees, k)
+        cache[k] = (c_host, torch.from_numpy(c_host).to(dev()), [str(w.message) for w in wr])
+    centers, cdev, msgs = cache[k]
+    for m in msgs:
+        warnings.warn(m)
     labels = torch.empty(n, dtype=torch.int32, device=dev())
     s64 = op.struct(_lib.F64)
     wsb = _lib.load().ancka_init_workspace_size(s64, k)
@@ -187,7 +194,35 @@ def _qr_f64_inplace(z: torch.Tensor, c: int) -> np.ndarray:
     return rdiag.cpu().numpy()
 
 
-def _exact_step(op: WalkOperator, q64: torch.Tensor, c: int, rng: np.random.Generator):
+class _NoisePrefetch:
+    """The first draw of the reference's rank-deficiency noise
+    (default_rng(seed).standard_normal((n, 1)), engine.py:141-146) computed on
+    a host thread while the device runs the KNN phase: step 1 always flags one
+    column.  The generator state after the draw is kept so the
+    caller's rng continues exactly as if it had drawn itself."""
+
+    def __init__(self, seed: int, n: int):
+        import threading
+        self.seed, self.n, self.noise, self.state = seed, n, None, None
+        self.fresh = np.random.default_rng(seed).bit_generator.state
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def _run(self):
+        g = np.random.default_rng(self.seed)
+        self.noise = g.standard_normal((self.n, 1))
+        self.state = g.bit_generator.state
+
+    def take(self, rng: np.random.Generator, n: int, cols: int):
+        if cols != 1 or n != self.n or rng.bit_generator.state != self.fresh:
+            return None
+        self._t.join()
+        rng.bit_generator.state = self.state
+        return self.noise
+
+
+def _exact_step(op: WalkOperator, q64: torch.Tensor, c: int, rng: np.random.Generator,
+                prefetch: "_NoisePrefetch | None" = None):
     """orthogonal_step (engine.py:130-149) in f64: apply, QR, the reference's
     rank test on |R_jj|, seeded noise on bad columns, re-QR.  Returns the new
     f64 block (diag R > 0 by construction) and Z."""
@@ -201,7 +236,9 @@ def _exact_step(op: WalkOperator, q64: torch.Tensor, c: int, rng: np.random.Gene
     bad = d < 1e-12 * max(1.0, d.max() if d.size else 1.0)
     if bad.any():
         warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
-        noise = rng.standard_normal((n, int(bad.sum())))
+        noise = prefetch.take(rng, n, int(bad.sum())) if prefetch is not None else None
+        if noise is None:
+            noise = rng.standard_normal((n, int(bad.sum())))
         cols = torch.from_numpy(np.flatnonzero(bad)).to(z.device)
         z[:, cols] += 1e-8 * torch.from_numpy(noise).to(z.device)
         q = z.clone()
@@ -495,6 +532,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
     _lib.require_device()
     timer = _PhaseTimer()
     launches0 = _lib.load().ancka_launch_count()
+    prefetch = _NoisePrefetch(params.seed, prep.net.n)
     with warnings.catch_warnings(record=True) as wrec:
         warnings.simplefilter("always")
         with timer.span("knn_ms"):
@@ -527,7 +565,11 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device=dev())
         readback = torch.zeros(4, dtype=torch.float64, device=dev())
         error, stop_reason, converged, t = None, "max_iterations", False, 0
-        def sample(t_now, dq_first):
+        host_info = torch.empty(8, dtype=torch.float64, pin_memory=True)
+        host_rb = torch.empty(4, dtype=torch.float64, pin_memory=True)
+        rb_ready = torch.cuda.Event()
+
+        def sample_issue(t_now, dq_first):
             qt = loop.q
             with timer.span("discretize_ms"):
                 _discretize_device(qt, 1, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
@@ -539,24 +581,58 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             else:
                 readback[1] = loop.stats[0]
                 readback[2] = loop.stats[2]
-            return info[:8].cpu().numpy(), readback.cpu().numpy()[:3]
+            host_info.copy_(info[:8], non_blocking=True)
+            host_rb.copy_(readback, non_blocking=True)
+            rb_ready.record()
 
+        def sample_collect():
+            rb_ready.synchronize()
+            return host_info.numpy().copy(), host_rb.numpy()[:3].copy()
+
+        def sample(t_now, dq_first):
+            sample_issue(t_now, dq_first)
+            return sample_collect()
+
+        Qsave_prev = torch.empty_like(loop.Qsave)
+
+        spec = None
         try:
             # ---- t = 1: exact f64 step on the rank-deficient block
             t = 1
             with timer.span("ortho_ms"):
-                q1, _ = _exact_step(op, q0, c, rng)
+                q1, _ = _exact_step(op, q0, c, rng, prefetch)
                 loop.Q[0][:, :c] = q1[:, :c].to(torch.float32)
                 loop.cur = 0
                 dq1 = torch.linalg.vector_norm(q1[:, :c] - q0[:, :c])
             t_done = 1
             sample_needed = params.tau == 1
+            # spec: a tau-block enqueued while the sample is read back
+
+            def undo_spec():
+                # return to the iterate at t_done: the speculative block saved it
+                start, prev_last = spec[1], spec[2]
+                loop.Q[start].copy_(loop.Qsave)
+                loop.cur = start
+                loop.Qsave.copy_(Qsave_prev)
+                loop.last = prev_last
+
             while True:
                 if sample_needed:
                     t = t_done
-                    inf, (phi, dq2, nbad) = sample(t_done, dq1 if t_done == 1 else None)
+                    sample_issue(t_done, dq1 if t_done == 1 else None)
+                    if t_done < params.t_a:
+                        # overlap the host decision with the next block (discarded on stop)
+                        nxt_s = min(params.t_a, (t_done // params.tau + 1) * params.tau)
+                        Qsave_prev.copy_(loop.Qsave)
+                        spec = (nxt_s, loop.cur, getattr(loop, "last", None))
+                        with timer.span("ortho_ms"):
+                            loop.run(nxt_s - t_done)
+                    inf, (phi, dq2, nbad) = sample_collect()
                     if nbad > 0:
                         # a suspect Cholesky pivot: replay the block with exact f64 steps
+                        if spec is not None:
+                            undo_spec()
+                            spec = None
                         warnings.warn("ill-conditioned iterate; replaying tau-block in f64")
                         with timer.span("ortho_ms"):
                             loop.replay_exact(rng)
@@ -572,24 +648,33 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                         best_labels.copy_(lab_t)
                     if float(np.sqrt(dq2)) < params.eps_q:
                         stop_reason, converged = "subspace_converged", True
+                        if spec is not None:
+                            undo_spec()
                         break
                     if early_stop and len(history) >= 3:
                         p = [v for _, v in history[-3:]]
                         if p[0] < p[1] < p[2]:
                             stop_reason, converged = "mhc_rising", True
+                            if spec is not None:
+                                undo_spec()
                             break
                     timer.flush()
                 if t_done >= params.t_a:
                     t = t_done
                     break
-                nxt = min(params.t_a, (t_done // params.tau + 1) * params.tau)
-                with timer.span("ortho_ms"):
-                    loop.run(nxt - t_done)
+                if spec is not None:            # the next block already ran
+                    nxt, spec = spec[0], None
+                else:
+                    nxt = min(params.t_a, (t_done // params.tau + 1) * params.tau)
+                    with timer.span("ortho_ms"):
+                        loop.run(nxt - t_done)
                 t_done = nxt
                 t = t_done
                 sample_needed = t_done % params.tau == 0
         except NetworkError as exc:
             error, stop_reason = str(exc), "error"
+            if spec is not None:
+                undo_spec()
         timer.flush()
         caught = [str(w.message) for w in wrec]
     best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)

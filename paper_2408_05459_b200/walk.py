@@ -195,49 +195,55 @@ class WalkOperator:
     LONG_ROW, HUB_FACTOR, PIECE, MAX_LD = 64, 4, 32, 256
 
     def _split_plan(self) -> _lib.RowSplit:
-        """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs)."""
-        srp = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"].rowptr.cpu().numpy()
-        krp = self.p_k_dev.rowptr.cpu().numpy()
-        ls, lk = np.diff(srp), np.diff(krp)
+        """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs),
+        computed with device tensor ops (two scalar read-backs)."""
+        srp = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"].rowptr
+        krp = self.p_k_dev.rowptr
+        d = srp.device
+        ls, lk = srp[1:] - srp[:-1], krp[1:] - krp[:-1]
         cost = ls + lk
-        thr = max(self.LONG_ROW, self.HUB_FACTOR * float(cost.mean()) if cost.size else 0.0)
-        long_rows = np.flatnonzero(cost > thr).astype(np.int32)
-        d = dev()
+        mean = float(cost.double().mean().item()) if cost.numel() else 0.0
+        thr = max(self.LONG_ROW, self.HUB_FACTOR * mean)
         # regular rows by descending cost (stable): the fused kernel deals them
         # round-robin to its lane groups, so every group gets a similar load
-        order = np.argsort(-cost, kind="stable").astype(np.int32)
-        self._order = torch.from_numpy(order).to(d)
-        if long_rows.size == 0:
+        self._order = torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
+        long_rows = torch.nonzero(cost > thr).flatten()
+        n_long = int(long_rows.numel())
+        if n_long == 0:
             return _lib.RowSplit(0, 0, None, None, None, None, None, None, None, 0,
                                  self._order.data_ptr())
         P = self.PIECE
-        ns = -(-ls[long_rows] // P)                   # structural pieces per long row
-        nk = -(-lk[long_rows] // P)                   # KNN pieces per long row
+        ns = (ls[long_rows] + P - 1) // P             # structural pieces per long row
+        nk = (lk[long_rows] + P - 1) // P             # KNN pieces per long row
         per = ns + nk
-        ptr = np.concatenate([[0], np.cumsum(per)])
+        ptr = torch.zeros(n_long + 1, dtype=torch.int64, device=d)
+        ptr[1:] = torch.cumsum(per, 0)
+        total = int(ptr[-1].item())
         # within-row piece ordinal q and its segment (structural pieces first)
-        q = np.arange(ptr[-1]) - np.repeat(ptr[:-1], per)
-        rrep = np.repeat(long_rows, per)
-        is_k = q >= np.repeat(ns, per)
-        qq = np.where(is_k, q - np.repeat(ns, per), q)
-        rb = np.where(is_k, krp[rrep], srp[rrep])
-        re = np.where(is_k, krp[rrep + 1], srp[rrep + 1])
+        rows_of_piece = torch.repeat_interleave(torch.arange(n_long, device=d), per,
+                                                output_size=total)
+        q = torch.arange(total, device=d) - ptr[:-1][rows_of_piece]
+        rrep = long_rows[rows_of_piece]
+        nsr = ns[rows_of_piece]
+        is_k = q >= nsr
+        qq = torch.where(is_k, q - nsr, q)
+        rb = torch.where(is_k, krp[rrep], srp[rrep])
+        re = torch.where(is_k, krp[rrep + 1], srp[rrep + 1])
         begins = rb + qq * P
-        ends = np.minimum(re, begins + P)
-        segs = is_k.astype(np.int32)
-        mask = np.zeros(self.n, dtype=np.uint8)
+        ends = torch.minimum(re, begins + P)
+        mask = torch.zeros(self.n, dtype=torch.uint8, device=d)
         mask[long_rows] = 1
         self._plan = {
-            "is_long": torch.from_numpy(mask).to(d),
-            "long_rows": torch.from_numpy(long_rows).to(d),
-            "piece_ptr": torch.from_numpy(ptr.astype(np.int64)).to(d),
-            "piece_seg": torch.from_numpy(segs).to(d),
-            "piece_begin": torch.from_numpy(begins.astype(np.int64)).to(d),
-            "piece_end": torch.from_numpy(ends.astype(np.int64)).to(d),
-            "partial": torch.empty(len(segs) * self.MAX_LD, dtype=torch.float32, device=d),
+            "is_long": mask,
+            "long_rows": long_rows.to(torch.int32),
+            "piece_ptr": ptr,
+            "piece_seg": is_k.to(torch.int32),
+            "piece_begin": begins.contiguous(),
+            "piece_end": ends.contiguous(),
+            "partial": torch.empty(total * self.MAX_LD, dtype=torch.float32, device=d),
         }
         p = self._plan
-        return _lib.RowSplit(long_rows.size, len(segs), p["is_long"].data_ptr(),
+        return _lib.RowSplit(n_long, total, p["is_long"].data_ptr(),
                              p["long_rows"].data_ptr(), p["piece_ptr"].data_ptr(),
                              p["piece_seg"].data_ptr(), p["piece_begin"].data_ptr(),
                              p["piece_end"].data_ptr(), p["partial"].data_ptr(), self.MAX_LD,
