@@ -206,6 +206,25 @@ int ancka_cholqr_apply_f32(const float* Z, const float* Q_prev, float* Q_out, in
                            int32_t c, const double* G, double* stats, void* workspace,
                            size_t workspace_bytes, ancka_stream_t stream);
 
+/* ---- wide-block discretisation (k > 16; engine.py:183-263) ------------- */
+/* The n-sized per-round work of _alternate_rounding on the device; the host
+ * runs the k x k SVD (np.linalg.svd, as the reference) between rounds.
+ * q~ = q / ||q|| (numpy's pairwise norm) as f32 rows of stride ldt >= k;
+ * zero_rows (device int32) counts all-zero rows. */
+int ancka_disc_normalize(const float* Q, int64_t ldq, int64_t col0, int64_t n, int32_t k,
+                         float* qt, int64_t ldt, int32_t* zero_rows, ancka_stream_t stream);
+/* labels = first argmax_j (q~ R)[i, j], margin = second-largest score. */
+int ancka_disc_score(const float* qt, int64_t ldt, int64_t n, int32_t k, const float* R,
+                     int64_t ldr, int32_t* labels, float* margin, ancka_stream_t stream);
+/* S[l*k + j] = sum over rows with label l of llrint(q~[i][j] * scale) (int64),
+ * counts[l] = cluster sizes.  Integer sums: bit-reproducible. */
+int ancka_disc_accumulate(const float* qt, int64_t ldt, int64_t n, int32_t k,
+                          const int32_t* labels, double scale, int64_t* S, int64_t* counts,
+                          ancka_stream_t stream);
+/* acc[i] += |q~_i . rcol| (f64): one greedy pass of _prototype_rotation. */
+int ancka_disc_proto_pass(const float* qt, int64_t ldt, int64_t n, int32_t k,
+                          const double* rcol, double* acc, ancka_stream_t stream);
+
 /* ---- engine pieces (engine.py) ----------------------------------------- */
 
 /* init_bcm (engine.py:87-127) after centre selection: t_i restart-walk steps

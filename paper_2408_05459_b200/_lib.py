@@ -91,6 +91,14 @@ _SIGS = {
     "ancka_discretize_workspace_size": (c_size_t, [c_int64, c_int32, c_int32]),
     "ancka_discretize": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32,
                                    c_double, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_disc_normalize": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_void_p,
+                                       c_int64, c_void_p, c_void_p]),
+    "ancka_disc_score": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_int64,
+                                   c_void_p, c_void_p, c_void_p]),
+    "ancka_disc_accumulate": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_double,
+                                        c_void_p, c_void_p, c_void_p]),
+    "ancka_disc_proto_pass": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
+                                        c_void_p]),
     "ancka_mhc_workspace_size": (c_size_t, [_OP, c_int32]),
     "ancka_mhc": (c_int32, [_OP, c_void_p, c_int32, c_double, c_int32, c_void_p, c_void_p,
                             c_void_p, c_size_t, c_void_p]),

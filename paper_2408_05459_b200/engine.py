@@ -259,9 +259,126 @@ def orthogonal_step(op: WalkOperator, q_prev, rng: np.random.Generator):
 
 
 # --------------------------------------------------------- discretize -------
+#: blocks wider than this use the host-driven wide path (per-round n-sized
+#: work on the device, the k x k SVD on the host as np.linalg.svd); narrower
+#: ones the single cooperative kernel (discretize.cu), which is faster there
+WIDE_DISCRETIZE_K = 64
+
+
+class _WideDiscretizer:
+    """_alternate_rounding / _prototype_rotation (engine.py:183-218) for k > 16.
+    Buffers are per (n, k) and reused across calls."""
+
+    def __init__(self, n: int, k: int):
+        d = dev()
+        self.n, self.k = n, k
+        self.ldt = ld_for(k, torch.float32)
+        self.qt = torch.empty((n, self.ldt), dtype=torch.float32, device=d)
+        self.zero = torch.zeros(1, dtype=torch.int32, device=d)
+        self.lab = [torch.empty(n, dtype=torch.int32, device=d) for _ in range(2)]
+        self.margin = torch.empty(n, dtype=torch.float32, device=d)
+        self.R = torch.zeros((k, self.ldt), dtype=torch.float32, device=d)
+        self.S = torch.empty(k * k, dtype=torch.int64, device=d)
+        self.cnt = torch.empty(k, dtype=torch.int64, device=d)
+        self.acc = torch.empty(n, dtype=torch.float64, device=d)
+        self.rcol = torch.empty(k, dtype=torch.float64, device=d)
+        bits = int(np.ceil(np.log2(n + 1)))
+        self.shift = 61 - bits                  # |sum| <= n: no int64 overflow
+        self.scale = float(2.0 ** self.shift)
+
+    def _sizes(self, lab):
+        _lib.call("ancka_cluster_sizes", lab.data_ptr(), self.n, self.k, self.cnt.data_ptr(),
+                  _lib.stream())
+        return self.cnt
+
+    def _reseed(self, lab):
+        """_reseed_empty_columns (engine.py:162-180) with device tensor ops."""
+        k = self.k
+        sizes = self._sizes(lab).cpu().numpy()
+        empties = np.flatnonzero(sizes == 0)
+        if not empties.size or k < 2:
+            return
+        for c in empties:
+            sz = torch.bincount(lab.long(), minlength=k)
+            movable = sz[lab.long()] >= 2
+            if not bool(movable.any()):
+                break
+            cand = torch.where(movable, self.margin, torch.full_like(self.margin, -np.inf))
+            lab[int(torch.argmax(cand))] = int(c)
+
+    def run(self, R0: np.ndarray, lab, max_iter: int, tol: float):
+        n, k = self.n, self.k
+        objs, conv, R = [], False, R0
+        for _ in range(max_iter):
+            R_used = R                            # rotation behind this round's scores
+            self.R[:, :k] = torch.from_numpy(R.astype(np.float32)).to(self.R.device)
+            _lib.call("ancka_disc_score", self.qt.data_ptr(), self.ldt, n, k, self.R.data_ptr(),
+                      self.ldt, lab.data_ptr(), self.margin.data_ptr(), _lib.stream())
+            self._reseed(lab)
+            _lib.call("ancka_disc_accumulate", self.qt.data_ptr(), self.ldt, n, k, lab.data_ptr(),
+                      self.scale, self.S.data_ptr(), self.cnt.data_ptr(), _lib.stream())
+            S = self.S.cpu().numpy().reshape(k, k).astype(np.float64) / self.scale
+            sizes = self.cnt.cpu().numpy().astype(np.float64)
+            M = np.divide(S, sizes[:, None], out=np.zeros_like(S), where=sizes[:, None] > 0)
+            u, omega, vh = np.linalg.svd(M)     # Y~^T Q~ (engine.py:199-200)
+            objs.append(n - 2.0 * float(omega.sum()))
+            if len(objs) >= 2 and abs(objs[-1] - objs[-2]) < tol:
+                conv = True
+                break
+            R = vh.T @ u.T
+        return objs, conv, R_used, int((sizes == 0).sum())
+
+    def prototype(self) -> np.ndarray:
+        """_prototype_rotation (engine.py:209-218): k - 1 greedy passes."""
+        n, k = self.n, self.k
+        R = np.zeros((k, k))
+        R[:, 0] = self.qt[0, :k].double().cpu().numpy()
+        self.acc.zero_()
+        for j in range(1, k):
+            self.rcol.copy_(torch.from_numpy(R[:, j - 1]))
+            _lib.call("ancka_disc_proto_pass", self.qt.data_ptr(), self.ldt, n, k,
+                      self.rcol.data_ptr(), self.acc.data_ptr(), _lib.stream())
+            i = int(torch.argmin(self.acc))      # first minimum, as np.argmin
+            R[:, j] = self.qt[i, :k].double().cpu().numpy()
+        return R
+
+    def __call__(self, q32, col0, max_iter, tol, labels_out, info):
+        n, k = self.n, self.k
+        _lib.call("ancka_disc_normalize", q32.data_ptr(), q32.stride(0), col0, n, k,
+                  self.qt.data_ptr(), self.ldt, self.zero.data_ptr(), _lib.stream())
+        results = []
+        for r, R0 in enumerate((np.eye(k), None)):
+            if R0 is None:
+                R0 = self.prototype()
+            results.append(self.run(R0, self.lab[r], max_iter, tol))
+        # identity wins unless the prototype run is lower by more than 1e-15
+        win = 1 if results[1][0][-1] < results[0][0][-1] - 1e-15 else 0
+        objs, conv, R, empties = results[win]
+        labels_out.copy_(self.lab[win])
+        head = [objs[-1], len(objs), 1.0 if conv else 0.0, win, empties,
+                float(self.zero.item()), len(results[0][0]), len(results[1][0])]
+        host = np.zeros(info.numel())
+        host[:8] = head
+        for r in range(2):
+            o = results[r][0]
+            host[8 + r * max_iter: 8 + r * max_iter + len(o)] = o
+            host[8 + 2 * max_iter + r * k * k: 8 + 2 * max_iter + (r + 1) * k * k] = \
+                results[r][2].ravel()
+        info.copy_(torch.from_numpy(host))
+
+
+_WIDE = {}
+
+
 def _discretize_device(q32: torch.Tensor, col0: int, k: int, max_iter: int, tol: float,
                        labels_out: torch.Tensor, info: torch.Tensor):
     n = q32.shape[0]
+    if k > WIDE_DISCRETIZE_K:
+        w = _WIDE.get((n, k))
+        if w is None:
+            w = _WIDE[(n, k)] = _WideDiscretizer(n, k)
+        w(q32, col0, max_iter, tol, labels_out, info)
+        return
     wsb = _lib.load().ancka_discretize_workspace_size(n, k, max_iter)
     ws = WORKSPACE.get("disc", wsb)
     _lib.call("ancka_discretize", q32.data_ptr(), q32.stride(0), col0, n, k, max_iter, float(tol),

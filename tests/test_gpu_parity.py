@@ -281,3 +281,27 @@ def test_real_valued_knn_certified(n, d, K, dup):
         assert np.all(a0[5] == -1)
     else:
         assert fallback == 0
+
+
+@pytest.mark.parametrize("n,k,noise", [(3000, 20, 0.25), (2500, 47, 0.2), (3000, 72, 0.1),
+                                       (4000, 172, 0.05)])
+def test_wide_discretize_matches_oracle(n, k, noise, monkeypatch):
+    """Host-driven wide rounds (device scoring / fixed-point accumulation, host
+    SVD; the path for k > 64, forced here for every k) against the oracle
+    restatement of engine.py:221-263."""
+    from sklearn.metrics import adjusted_rand_score as ari_
+
+    from paper_2408_05459_b200 import engine
+    monkeypatch.setattr(engine, "WIDE_DISCRETIZE_K", 16)
+    rng = np.random.default_rng(k)
+    lab = rng.integers(0, k, n)
+    q = np.zeros((n, k))
+    q[np.arange(n), lab] = 1.0
+    q += noise * rng.standard_normal((n, k))
+    q[7] = 0.0                                    # an all-zero row -> cluster 0
+    q32 = q.astype(np.float32).astype(np.float64)   # the device sees f32 input
+    d = ancka.discretize(q32)
+    ref = oc.discretize(q32)
+    assert ari_(ref["labels"], d.y.assignment) >= 0.99
+    assert d.y.assignment[7] == ref["labels"][7]
+    assert abs(d.objectives[-1] - ref["objs"][-1]) <= 1e-5 * max(1.0, abs(ref["objs"][-1]))
