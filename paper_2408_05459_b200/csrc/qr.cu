@@ -17,6 +17,7 @@ namespace ancka {
 constexpr int kGramThreads = 256;
 constexpr int kGramBlocks = 2 * kNumSMs;
 constexpr int kApplyBlocks = 8 * kNumSMs;
+constexpr int kMaxC = 256;     // widest block (Papers100M: c = 173)
 
 __device__ __forceinline__ int packed_idx(int a, int b, int c) {  // a <= b
   return a * c - (a * (a - 1)) / 2 + (b - a);
@@ -196,7 +197,6 @@ chol_kernel(const double* __restrict__ partial, int nblocks, int c, float* __res
   extern __shared__ double sm[];
   const int npairs = c * (c + 1) / 2;
   double* R = sm;               // packed upper, npairs
-  double* X = sm + npairs;      // packed upper inverse, npairs
   __shared__ double s_minratio;
   __shared__ int s_bad;
   __shared__ double gsum[256];
@@ -250,20 +250,19 @@ chol_kernel(const double* __restrict__ partial, int nblocks, int c, float* __res
     }
     __syncthreads();
   }
-  // inverse of upper-triangular R, one column per thread
+  // inverse of upper-triangular R, one column per thread (the column lives in
+  // a per-thread local array, so only R occupies shared memory)
   for (int b = threadIdx.x; b < c; b += blockDim.x) {
-    X[packed_idx(b, b, c)] = 1.0 / R[packed_idx(b, b, c)];
+    double xc[kMaxC];
+    xc[b] = 1.0 / R[packed_idx(b, b, c)];
     for (int a = b - 1; a >= 0; --a) {
       double s = 0.0;
-      for (int l = a + 1; l <= b; ++l) s += R[packed_idx(a, l, c)] * X[packed_idx(l, b, c)];
-      X[packed_idx(a, b, c)] = -s / R[packed_idx(a, a, c)];
+      for (int l = a + 1; l <= b; ++l) s += R[packed_idx(a, l, c)] * xc[l];
+      xc[a] = -s / R[packed_idx(a, a, c)];
     }
+    for (int a = 0; a < c; ++a) rinv32[a * c + b] = a <= b ? (float)xc[a] : 0.f;
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < c * c; e += blockDim.x) {
-    int a = e / c, b = e % c;
-    rinv32[e] = a <= b ? (float)X[packed_idx(a, b, c)] : 0.f;
-  }
   for (int j = threadIdx.x; j < c; j += blockDim.x) rdiag[j] = R[packed_idx(j, j, c)];
   if (threadIdx.x == 0) {  // accumulated across steps until the host resets them
     stats[1] = fmin(stats[1], s_minratio);
@@ -334,7 +333,7 @@ int cholqr_f32(const float* Z, const float* Qprev, float* Qout, int64_t n, int64
   ANCKA_REQUIRE(c >= 1 && c <= 256 && ld % 4 == 0, ANCKA_ERR_ARG, "cholqr: bad c/ld");
   ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
   const int npairs = c * (c + 1) / 2;
-  const size_t csm = 2 * (size_t)npairs * sizeof(double);
+  const size_t csm = (size_t)npairs * sizeof(double);
   ANCKA_REQUIRE(csm <= 227 * 1024, ANCKA_ERR_UNSUPPORTED, "cholqr: c=%d too large", c);
   if (csm > 48 * 1024)
     cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
@@ -489,7 +488,7 @@ extern "C" int ancka_cholqr_apply_f32(const float* Z, const float* Q_prev, float
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "cholqr_apply: workspace too small");
   auto st = as_stream(stream);
   const int npairs = c * (c + 1) / 2;
-  const size_t csm = 2 * (size_t)npairs * sizeof(double);
+  const size_t csm = (size_t)npairs * sizeof(double);
   ANCKA_REQUIRE(csm <= 227 * 1024, ANCKA_ERR_UNSUPPORTED, "cholqr: c=%d too large", c);
   if (csm > 48 * 1024)
     cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);

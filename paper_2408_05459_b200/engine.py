@@ -320,7 +320,11 @@ class _WideDiscretizer:
             S = self.S.cpu().numpy().reshape(k, k).astype(np.float64) / self.scale
             sizes = self.cnt.cpu().numpy().astype(np.float64)
             M = np.divide(S, sizes[:, None], out=np.zeros_like(S), where=sizes[:, None] > 0)
-            u, omega, vh = np.linalg.svd(M)     # Y~^T Q~ (engine.py:199-200)
+            try:
+                u, omega, vh = np.linalg.svd(M)     # Y~^T Q~ (engine.py:199-200)
+            except np.linalg.LinAlgError:       # gesdd non-convergence: QR-iteration SVD
+                import scipy.linalg
+                u, omega, vh = scipy.linalg.svd(M, lapack_driver="gesvd")
             objs.append(n - 2.0 * float(omega.sum()))
             if len(objs) >= 2 and abs(objs[-1] - objs[-2]) < tol:
                 conv = True

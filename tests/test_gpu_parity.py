@@ -305,3 +305,34 @@ def test_wide_discretize_matches_oracle(n, k, noise, monkeypatch):
     assert ari_(ref["labels"], d.y.assignment) >= 0.99
     assert d.y.assignment[7] == ref["labels"][7]
     assert abs(d.objectives[-1] - ref["objs"][-1]) <= 1e-5 * max(1.0, abs(ref["objs"][-1]))
+
+
+def test_run_ancka_wide_k_matches_oracle():
+    """k = 70 (c = 71 > 64): CholQR on wide blocks, the wide discretisation,
+    MHC and init at large k, end to end against the oracle on a
+    well-separated planted instance."""
+    from sklearn.metrics import adjusted_rand_score as ari_
+    rng = np.random.default_rng(11)
+    k, per, d = 70, 60, 32
+    n = k * per
+    lab = np.repeat(np.arange(k), per)
+    rows, cols = [], []
+    for b in range(k):
+        idx = np.arange(b * per, (b + 1) * per)
+        e = rng.integers(0, per, size=(6 * per, 2))
+        rows += list(idx[e[:, 0]])
+        cols += list(idx[e[:, 1]])
+    a = sp.csr_matrix((np.ones(len(rows)), (rows, cols)), shape=(n, n))
+    a = ((a + a.T) > 0).astype(np.float64)
+    a.setdiag(0)
+    a.eliminate_zeros()
+    mu = rng.normal(0, 2.0, size=(k, d))
+    X = np.abs(mu[lab] + 0.5 * rng.standard_normal((n, d)))
+    net = ancka.AttributedNetwork.graph(sp.csr_matrix(a), X)
+    params = ancka.ClusterParams(k=k, knn_k=10, seed=3, knn_mode=ancka.KnnMode.EXACT)
+    res = ancka.run_ancka(net, params)
+    assert res.error is None, res.error
+    ref = oc.run({"kind": "graph", "S": sp.csr_matrix(a), "X": X}, k, knn_k=10, seed=3)
+    assert ari_(ref["labels"], res.y.assignment) >= 0.99, (ari_(lab, res.y.assignment),
+                                                           ari_(lab, ref["labels"]))
+    assert abs(res.mhc - ref["mhc"]) < 1e-3
