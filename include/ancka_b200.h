@@ -34,7 +34,8 @@ enum ancka_status {
 };
 
 enum ancka_dtype { ANCKA_F32 = 0, ANCKA_F64 = 1 };
-enum ancka_kind { ANCKA_GRAPH = 0, ANCKA_HYPERGRAPH = 1 };
+enum ancka_kind { ANCKA_GRAPH = 0, ANCKA_HYPERGRAPH = 1, ANCKA_MULTIPLEX = 2 };
+#define ANCKA_MAX_LAYERS 8
 
 /* Sparse row matrix on the device.  values == NULL means every stored entry
  * is 1 (index-only storage of an unweighted factor). */
@@ -81,6 +82,11 @@ typedef struct {
   const void* beta;       /* n, beta_vector (walk.py:47-57)              */
   const uint8_t* selfloop;/* n, 1 where walk.py:123 adds a self-loop     */
   ancka_row_split split;  /* f32 load balancing of the n-row pass         */
+  int32_t n_layers;       /* multiplex: L <= ANCKA_MAX_LAYERS (0 otherwise) */
+  const ancka_csr* layers;   /* multiplex: host array of L CSR views of
+                                P_l = D_l^-1 A_l (walk.py:82-86); the
+                                structural term is (sum_l P_l M) / L     */
+  const ancka_csr* layers_t; /* multiplex: P_l^T, for the rowvec apply    */
 } ancka_operator;
 
 const char* ancka_last_error(void);

@@ -18,8 +18,8 @@ checks this restatement against every one of them (bit-exact for integer
 outputs, <=1e-12 for floating point).
 
 Data model: plain arrays.  A network is a dict
-    {"kind": "graph"|"hypergraph", "S": csr (A n x n, or H m x n),
-     "directed": bool, "X": ndarray or csr}
+    {"kind": "graph"|"hypergraph"|"multiplex", "S": csr (A n x n, or H m x n),
+     "layers": [csr n x n, ...] (multiplex), "directed": bool, "X": ndarray or csr}
 """
 from __future__ import annotations
 
@@ -61,8 +61,12 @@ def sym_union(a):
 
 
 def clean_network(net):
-    """validate_network (network.py:266-313), structural cleanup only."""
+    """validate_network (network.py:266-313), structural cleanup only
+    (multiplex layers are only canonicalised, network.py:107-126)."""
     net = dict(net)
+    if net["kind"] == "multiplex":
+        net["layers"] = [canon_csr(a, f"layer {i}") for i, a in enumerate(net["layers"])]
+        return net
     s = canon_csr(net["S"], "structure")
     if net["kind"] == "hypergraph":
         keep = np.diff(s.indptr) >= 2
@@ -81,7 +85,11 @@ def clean_network(net):
 
 
 def structural_degree(net):
-    """node_degrees (network.py:316-328): pattern counts."""
+    """node_degrees (network.py:316-328): pattern counts (multiplex: summed
+    over layers, layer_degrees network.py:331-337)."""
+    if net["kind"] == "multiplex":
+        return np.sum([np.asarray((a != 0).sum(axis=1)).ravel().astype(np.float64)
+                       for a in net["layers"]], axis=0)
     s = net["S"]
     if net["kind"] == "hypergraph":
         return np.asarray((s != 0).sum(axis=0)).ravel().astype(np.float64)
@@ -184,6 +192,9 @@ def make_operator(net, p_k, knn_zero, alpha=ALPHA, beta=BETA, gamma=GAMMA):
     op = {"kind": net["kind"], "n": n, "alpha": float(alpha), "gamma": int(gamma),
           "beta": b, "p_k": p_k, "degrees": deg,
           "selfloop": np.flatnonzero((deg == 0) & (b == 0.0))}
+    if net["kind"] == "multiplex":   # multiplex_transition (walk.py:82-86)
+        op["layers"] = [row_stochastic(a)[0] for a in net["layers"]]
+        return op
     s = net["S"]
     if net["kind"] == "hypergraph":
         op["p_v"], _ = row_stochastic(s.T.tocsr())
@@ -197,7 +208,15 @@ def structure_apply(op, m):
     """apply_structure (walk.py:135-150)."""
     if m.shape[0] != op["n"]:
         raise OracleError("block/operator size mismatch")
-    out = op["p_v"] @ (op["p_e"] @ m) if op["kind"] == "hypergraph" else op["p_n"] @ m
+    if op["kind"] == "multiplex":   # layer average (walk.py:143-147)
+        out = op["layers"][0] @ m
+        for p in op["layers"][1:]:
+            out += p @ m
+        out /= len(op["layers"])
+    elif op["kind"] == "hypergraph":
+        out = op["p_v"] @ (op["p_e"] @ m)
+    else:
+        out = op["p_n"] @ m
     sl = op["selfloop"]
     if sl.size:
         out[sl] += m[sl]
@@ -207,7 +226,12 @@ def structure_apply(op, m):
 def structure_apply_t(op, m):
     """apply_structure_rowvec (walk.py:153-174): (c x n) block times P_struct."""
     mt = np.ascontiguousarray(m.T)
-    if op["kind"] == "hypergraph":
+    if op["kind"] == "multiplex":   # walk.py:168-172
+        acc = op["layers"][0].T @ mt
+        for p in op["layers"][1:]:
+            acc += p.T @ mt
+        out = acc.T / len(op["layers"])
+    elif op["kind"] == "hypergraph":
         out = (op["p_e"].T @ (op["p_v"].T @ mt)).T
     else:
         out = (op["p_n"].T @ mt).T
@@ -231,7 +255,9 @@ def joint_apply(op, m):
 
 def dense_P(op):
     """dense_transition (walk.py:193-208), small n only."""
-    if op["kind"] == "hypergraph":
+    if op["kind"] == "multiplex":
+        pn = sum(p.toarray() for p in op["layers"]) / len(op["layers"])
+    elif op["kind"] == "hypergraph":
         pn = (op["p_v"] @ op["p_e"]).toarray()
     else:
         pn = op["p_n"].toarray()

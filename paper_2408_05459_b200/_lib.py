@@ -16,7 +16,8 @@ LIB_PATH = Path(__file__).resolve().parent / "libancka_b200.so"
 
 ANCKA_OK, ANCKA_ERR_ARG, ANCKA_ERR_CUDA, ANCKA_ERR_NETWORK, ANCKA_ERR_UNSUPPORTED = range(5)
 F32, F64 = 0, 1
-GRAPH, HYPERGRAPH = 0, 1
+GRAPH, HYPERGRAPH, MULTIPLEX = 0, 1, 2
+MAX_LAYERS = 8
 
 
 class CSR(ctypes.Structure):
@@ -34,7 +35,8 @@ class RowSplit(ctypes.Structure):
 class Operator(ctypes.Structure):
     _fields_ = [("kind", c_int32), ("dtype", c_int32), ("n", c_int64), ("m", c_int64),
                 ("p_n", CSR), ("p_e", CSR), ("p_v", CSR), ("p_k", CSR), ("t_a", CSR),
-                ("t_b", CSR), ("beta", c_void_p), ("selfloop", c_void_p), ("split", RowSplit)]
+                ("t_b", CSR), ("beta", c_void_p), ("selfloop", c_void_p), ("split", RowSplit),
+                ("n_layers", c_int32), ("layers", c_void_p), ("layers_t", c_void_p)]
 
 
 _OP = POINTER(Operator)

@@ -425,6 +425,8 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
                                     int64_t ld, int32_t c, int32_t steps, double* stats,
                                     void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
   ANCKA_REQUIRE(op32 && op32->dtype == ANCKA_F32, ANCKA_ERR_ARG, "orth_block needs the f32 operator");
+  ANCKA_REQUIRE(op32->kind != ANCKA_MULTIPLEX, ANCKA_ERR_UNSUPPORTED,
+                "fused orthogonal block: graph and hypergraph operators only");
   ANCKA_REQUIRE(ld == kC && c >= 1 && c <= kC, ANCKA_ERR_UNSUPPORTED,
                 "fused orthogonal block supports c <= 8 with ld == 8");
   ANCKA_REQUIRE(op32->split.n_pieces == 0 || op32->split.max_ld >= kC, ANCKA_ERR_ARG,

@@ -36,6 +36,12 @@ __device__ __forceinline__ void add_acc(float4& acc, float4 x) {
 __device__ __forceinline__ void add_acc(double2& acc, double2 x) {
   acc.x = __dadd_rn(acc.x, x.x); acc.y = __dadd_rn(acc.y, x.y);
 }
+__device__ __forceinline__ void div_acc(float4& acc, float d) {
+  acc.x /= d; acc.y /= d; acc.z /= d; acc.w /= d;
+}
+__device__ __forceinline__ void div_acc(double2& acc, double d) {
+  acc.x = __ddiv_rn(acc.x, d); acc.y = __ddiv_rn(acc.y, d);
+}
 
 template <typename T, typename VT>
 __device__ __forceinline__ VT seg_sum(const SegArgs<T>& s, int64_t row, int64_t coloff) {
@@ -132,6 +138,10 @@ spmm_kernel(SpmmArgs<T> a) {
   const int chunk = (int)(gid - row * a.nchunk);
   const int64_t coloff = (int64_t)chunk * W;
   VT s = seg_sum<T, VT>(a.s, row, coloff);
+  if (a.nl > 1) {   // multiplex: (sum_l P_l M) / L, layers added in order (walk.py:143-147)
+    for (int l = 0; l < a.nl - 1; ++l) add_acc(s, seg_sum<T, VT>(a.lay[l], row, coloff));
+    div_acc(s, T(a.nl));
+  }
   VT k;
   if (a.beta) k = seg_sum<T, VT>(a.k, row, coloff);
   else memset(&k, 0, sizeof(k));
@@ -227,6 +237,16 @@ static SegArgs<T> seg_of(const ancka_csr& m, const T* src, int64_t ld) {
 }
 
 template <typename T>
+static int set_layers(SpmmArgs<T>& a, int nl, const ancka_csr* layers, const T* src, int64_t ld) {
+  ANCKA_REQUIRE(nl >= 1 && nl <= ANCKA_MAX_LAYERS && layers != nullptr, ANCKA_ERR_ARG,
+                "multiplex operator needs 1..%d layers (got %d)", ANCKA_MAX_LAYERS, nl);
+  a.s = seg_of<T>(layers[0], src, ld);
+  for (int l = 1; l < nl; ++l) a.lay[l - 1] = seg_of<T>(layers[l], src, ld);
+  a.nl = nl;
+  return ANCKA_OK;
+}
+
+template <typename T>
 int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, int64_t ldz,
                T* scratch, cudaStream_t st, const EpilogueTag<T>* epi) {
   constexpr int W = Vec<T>::W;
@@ -248,6 +268,8 @@ int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, i
     s1.ldo = ldq;
     ANCKA_TRY(launch_spmm<T>(s1, st));
     a.s = seg_of<T>(op->p_v, scratch, ldq);
+  } else if (op->kind == ANCKA_MULTIPLEX) {
+    ANCKA_TRY(set_layers<T>(a, op->n_layers, op->layers, Q, ldq));
   } else {
     a.s = seg_of<T>(op->p_n, Q, ldq);
   }
@@ -295,6 +317,8 @@ int op_apply_struct_t_t(const ancka_operator* op, const T* Q, int64_t ldq, int c
     s1.ldo = ldq;
     ANCKA_TRY(launch_spmm<T>(s1, st));
     a.s = seg_of<T>(op->t_b, scratch, ldq);
+  } else if (op->kind == ANCKA_MULTIPLEX) {
+    ANCKA_TRY(set_layers<T>(a, op->n_layers, op->layers_t, Q, ldq));
   } else {
     a.s = seg_of<T>(op->t_a, Q, ldq);
   }

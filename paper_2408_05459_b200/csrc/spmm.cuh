@@ -21,6 +21,8 @@ struct SpmmArgs {
   int64_t rows = 0;
   int c = 0, nchunk = 0;
   SegArgs<T> s, k;
+  int nl = 0;                       // multiplex: layers (s = layer 0, lay[] = 1..nl-1)
+  SegArgs<T> lay[ANCKA_MAX_LAYERS - 1];
   const uint8_t* selfloop = nullptr;
   const T* self_src = nullptr;
   int64_t self_ld = 0;

@@ -200,6 +200,8 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     """run_ancka (engine.py:343-437) row-partitioned over the backend's ranks."""
     rank, world = B.rank, B.world
     net, _ = validate_network(net)
+    if net.kind is NetworkKind.MULTIPLEX:
+        raise NetworkError("the row-partitioned path covers graphs and hypergraphs")
     params.validate_for(net.n)
     n, k = net.n, params.k
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, n)

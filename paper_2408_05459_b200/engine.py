@@ -30,7 +30,7 @@ from .knn import (KnnGraph, NeighborLists, attributes_to_device, build_knn_graph
                   cache_key, integer_exact, knn_search_exact_device, load_neighbor_cache,
                   save_neighbor_cache)
 from .network import (AttributedNetwork, BcmMatrix, ClusterParams, KnnMode, NetworkError,
-                      default_knn_k, validate_network)
+                      default_knn_k, validate_network, NetworkKind)
 from .walk import StructureFactors, WalkOperator, build_walk_operator
 
 DISCRETIZE_MAX_ITER = 100
@@ -537,7 +537,7 @@ class _Loop:
         self.op, self.c, self.k, self.tau = op, c, k, tau
         n = op.n
         # narrow blocks use the fused cooperative kernel, which wants ld == 8
-        self.fused = fused and c <= 8
+        self.fused = fused and c <= 8 and op.kind is not NetworkKind.MULTIPLEX
         self.ld = 8 if self.fused else ld_for(c, torch.float32)
         d = dev()
         self.Q = [torch.zeros((n, self.ld), dtype=torch.float32, device=d) for _ in range(2)]

@@ -9,6 +9,8 @@ in f64 they are bit-identical to scipy's csr_matvecs.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -51,7 +53,10 @@ def graph_transition(net: AttributedNetwork) -> sp.csr_matrix:
 
 
 def multiplex_transition(net: AttributedNetwork):
-    raise NetworkError("multiplex networks are outside the B200 hot path (SURVEY.md §8f)")
+    """Per-layer transitions P_l = D_l^-1 A_l (walk.py:82-86), host scipy."""
+    if net.kind is not NetworkKind.MULTIPLEX:
+        raise NetworkError("multiplex_transition requires a multiplex network")
+    return [_row_normalize(a) for a in net.layers]
 
 
 def _upload(m: sp.csr_matrix) -> DeviceCSR:
@@ -92,8 +97,6 @@ class StructureFactors:
     structure.  Host scipy views (`host_view`) are materialised on access."""
 
     def __init__(self, net: AttributedNetwork):
-        if net.kind is NetworkKind.MULTIPLEX:
-            multiplex_transition(net)
         self.kind, self.n = net.kind, net.n
         self.degrees = node_degrees(net)
         self.host, self.dev = {}, {}
@@ -108,6 +111,18 @@ class StructureFactors:
             self.dev.update(p_v=p_v, p_e=p_e, t_a=_with_values(h, t_a), t_b=_transpose_dev(p_e))
             self.m = h.rows
             self._up = h.rowptr.numel() * 8 + h.colidx.numel() * 4 + h.val64.numel() * 8
+        elif net.kind is NetworkKind.MULTIPLEX:
+            if len(net.layers) > _lib.MAX_LAYERS:
+                raise NetworkError(f"multiplex networks support at most {_lib.MAX_LAYERS} layers")
+            layers, layers_t, self._up = [], [], 0
+            for a in net.layers:                       # P_l = D_l^-1 A_l (walk.py:82-86)
+                A = _upload(a)
+                p_l, _ = _row_normalize_dev(A)
+                layers.append(p_l)
+                layers_t.append(_transpose_dev(p_l))
+                self._up += A.rowptr.numel() * 8 + A.colidx.numel() * 4 + A.val64.numel() * 8
+            self.dev.update(layers=layers, layers_t=layers_t)
+            self.m = 0
         else:
             a = symmetrize_union(net.adjacency) if net.directed else net.adjacency
             A = _upload(a)
@@ -171,22 +186,37 @@ class WalkOperator:
     def p_e(self):
         return self._fac.host_view("p_e")
 
-    layer_p = None
+    @property
+    def layer_p(self):
+        """multiplex: per-layer P_l (walk.py:100), host views."""
+        if self.kind is not NetworkKind.MULTIPLEX:
+            return None
+        return tuple(m.to_scipy() for m in self._f["layers"])
 
     def struct(self, dtype: int) -> _lib.Operator:
         """ctypes ancka_operator for f32 (`_lib.F32`) or f64 values."""
         s = self._structs.get(dtype)
         if s is None:
             f = self._f
+            kind = {NetworkKind.HYPERGRAPH: _lib.HYPERGRAPH, NetworkKind.GRAPH: _lib.GRAPH,
+                    NetworkKind.MULTIPLEX: _lib.MULTIPLEX}[self.kind]
+            nl, lay, lay_t = 0, None, None
+            if self.kind is NetworkKind.MULTIPLEX:
+                nl = len(f["layers"])
+                lay = (_lib.CSR * nl)(*[m.struct(dtype) for m in f["layers"]])
+                lay_t = (_lib.CSR * nl)(*[m.struct(dtype) for m in f["layers_t"]])
+                self._keep = getattr(self, "_keep", []) + [lay, lay_t]   # ctypes arrays stay alive
+            split = (self._split_plan() if dtype == _lib.F32 and self.kind is not NetworkKind.MULTIPLEX
+                     else _lib.RowSplit())
             s = _lib.Operator(
-                _lib.HYPERGRAPH if self.kind is NetworkKind.HYPERGRAPH else _lib.GRAPH, dtype,
-                self.n, self.m,
+                kind, dtype, self.n, self.m,
                 csr_struct(f.get("p_n"), dtype), csr_struct(f.get("p_e"), dtype),
                 csr_struct(f.get("p_v"), dtype), csr_struct(self.p_k_dev, dtype),
                 csr_struct(f.get("t_a"), dtype), csr_struct(f.get("t_b"), dtype),
                 (self.beta64 if dtype == _lib.F64 else self.beta32).data_ptr(),
-                self.selfloop_dev.data_ptr(),
-                self._split_plan() if dtype == _lib.F32 else _lib.RowSplit())
+                self.selfloop_dev.data_ptr(), split, nl,
+                ctypes.cast(lay, ctypes.c_void_p) if lay is not None else None,
+                ctypes.cast(lay_t, ctypes.c_void_p) if lay_t is not None else None)
             self._structs[dtype] = s
         return s
 

@@ -51,7 +51,21 @@ def random_seeds(z):
     return sorted({int(k[1:].split("_")[0]) for k in z.files if k.startswith("s")})
 
 
+def load_layers(z, p):
+    return [load_csr(z, p + f"L{i}") for i in range(int(z[p + "n_layers"]))]
+
+
 def oracle_net(z, p):
     kind = str(z[p + "kind"])
+    if kind == "multiplex":
+        return {"kind": kind, "layers": load_layers(z, p), "directed": False,
+                "X": load_x(z, p + "X")}
     return {"kind": kind, "S": load_csr(z, p + "S"), "directed": bool(z[p + "directed"]),
             "X": load_x(z, p + "X")}
+
+
+@pytest.fixture(scope="session")
+def golden_multiplex():
+    z = np.load(GOLDEN / "multiplex.npz")
+    meta = json.loads((GOLDEN / "multiplex.json").read_text())
+    return z, meta

@@ -78,13 +78,14 @@ def random_instances(n_seeds=60):
         out[p + "beta"] = np.array((0.0, 0.5, 1.0)[(seed // 3) % 3])   # conftest.py:80
         out[p + "beta_vec"] = op.beta
         out[p + "gamma"] = np.array(op.gamma)
-        struct = net.incidence if net.kind is ancka.NetworkKind.HYPERGRAPH else (
-            net.adjacency if net.kind is ancka.NetworkKind.GRAPH else None)
-        if struct is None:                      # multiplex: out of scope
-            out[p + "skip"] = np.array(True)
-            continue
         out[p + "skip"] = np.array(False)
-        _csr(p + "S", struct, out)
+        if net.kind is ancka.NetworkKind.MULTIPLEX:
+            out[p + "n_layers"] = np.array(len(net.layers))
+            for li, a in enumerate(net.layers):
+                _csr(p + f"L{li}", a, out)
+        else:
+            struct = net.incidence if net.kind is ancka.NetworkKind.HYPERGRAPH else net.adjacency
+            _csr(p + "S", struct, out)
         _x(p + "X", net.attributes, out)
         out[p + "knn_ids"] = g.neighbors.ids
         out[p + "knn_scores"] = g.neighbors.scores
@@ -133,6 +134,60 @@ RUNS = [  # (shape, seed, n, p_in, words, early_stop)
 ]
 
 
+def multiplex_split(inst, seed):
+    """Two-layer multiplex from a graph instance: each edge goes to layer 0 or
+    1 at random, and each layer gets a few extra intra-block edges."""
+    rng = np.random.default_rng(seed)
+    a = sp.triu(sp.csr_matrix(inst.structure), 1).tocoo()
+    side = rng.random(a.nnz) < 0.55
+    n = inst.structure.shape[0]
+    layers = []
+    for want in (True, False):
+        keep = side == want
+        r, c = a.row[keep], a.col[keep]
+        extra = rng.integers(0, n, size=(n // 4, 2))
+        same = inst.labels[extra[:, 0]] == inst.labels[extra[:, 1]]
+        r = np.concatenate([r, extra[same, 0]])
+        c = np.concatenate([c, extra[same, 1]])
+        m = sp.csr_matrix((np.ones(r.size), (r, c)), shape=(n, n))
+        m = ((m + m.T) > 0).astype(np.float64)
+        m.setdiag(0)
+        m.eliminate_zeros()
+        layers.append(sp.csr_matrix(m))
+    return layers
+
+
+MPX_RUNS = [  # (shape, seed, n, early_stop)
+    ("cora", 5, 300, True),
+    ("amazon2m", 6, 300, True),
+]
+
+
+def end_to_end_multiplex():
+    out, meta = {}, []
+    for i, (shape, seed, n, early) in enumerate(MPX_RUNS):
+        inst = synth.make(shape, seed=seed, n=n)
+        layers = multiplex_split(inst, seed)
+        p = f"m{i}_"
+        out[p + "n_layers"] = np.array(len(layers))
+        for li, a in enumerate(layers):
+            _csr(p + f"L{li}", a, out)
+        _x(p + "X", inst.X, out)
+        params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=seed, knn_mode=ancka.KnnMode.EXACT)
+        net = ancka.AttributedNetwork.multiplex(layers, inst.X)
+        res = ancka.run_ancka(net, params, early_stop=early)
+        out[p + "labels"] = res.y.assignment
+        out[p + "mhc"] = np.array(res.mhc)
+        out[p + "iterations"] = np.array(res.iterations)
+        out[p + "planted"] = inst.labels
+        meta.append({"shape": shape, "seed": seed, "n": n, "kind": "multiplex",
+                     "n_layers": len(layers), "k": inst.k, "stop_reason": res.stop_reason,
+                     "early_stop": early, "t_a": params.t_a,
+                     "ari_vs_planted": float(ancka.ari(inst.labels, res.y.assignment))})
+    np.savez_compressed(HERE / "multiplex.npz", **out)
+    (HERE / "multiplex.json").write_text(json.dumps(meta, indent=1))
+
+
 def end_to_end():
     out, meta = {}, []
     for i, (shape, seed, n, p_in, words, early) in enumerate(RUNS):
@@ -164,5 +219,6 @@ if __name__ == "__main__":
     spec_examples()
     random_instances()
     end_to_end()
+    end_to_end_multiplex()
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)

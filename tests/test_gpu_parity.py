@@ -33,7 +33,11 @@ def ari(a, b):
 
 def _net(z, p):
     kind = str(z[p + "kind"])
-    S, X = load_csr(z, p + "S"), load_x(z, p + "X")
+    X = load_x(z, p + "X")
+    if kind == "multiplex":
+        from conftest import load_layers
+        return ancka.AttributedNetwork.multiplex(load_layers(z, p), X)
+    S = load_csr(z, p + "S")
     if kind == "hypergraph":
         return ancka.AttributedNetwork.hypergraph(S, X)
     return ancka.AttributedNetwork.graph(S, X, directed=bool(z[p + "directed"]))
@@ -336,3 +340,20 @@ def test_run_ancka_wide_k_matches_oracle():
     assert ari_(ref["labels"], res.y.assignment) >= 0.99, (ari_(lab, res.y.assignment),
                                                            ari_(lab, ref["labels"]))
     assert abs(res.mhc - ref["mhc"]) < 1e-3
+
+
+@pytest.mark.parametrize("i", range(2))
+def test_run_ancka_multiplex_matches_reference(golden_multiplex, i):
+    """multiplex networks (layer-averaged structural
+    walk) end to end against the reference's golden runs."""
+    from conftest import load_layers
+    z, meta = golden_multiplex
+    m = meta[i]
+    p = f"m{i}_"
+    net = ancka.AttributedNetwork.multiplex(load_layers(z, p), load_x(z, p + "X"))
+    params = ancka.ClusterParams(k=m["k"], knn_k=10, seed=m["seed"], t_a=m["t_a"],
+                                 knn_mode=ancka.KnnMode.EXACT)
+    res = ancka.run_ancka(net, params, early_stop=m["early_stop"])
+    assert res.error is None, res.error
+    assert ari(res.y.assignment, z[p + "labels"]) >= 0.99
+    assert abs(res.mhc - float(z[p + "mhc"])) < 1e-3

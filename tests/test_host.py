@@ -52,11 +52,14 @@ def test_validate_and_degrees_match_oracle(golden_random):
         if bool(z[p + "skip"]):
             continue
         on = oc.clean_network(oracle_net(z, p))
-        S = load_csr(z, p + "S")
-        if str(z[p + "kind"]) == "hypergraph":
-            net = ancka.AttributedNetwork.hypergraph(S, on["X"])
+        kind = str(z[p + "kind"])
+        if kind == "multiplex":
+            net = ancka.AttributedNetwork.multiplex(on["layers"], on["X"])
+        elif kind == "hypergraph":
+            net = ancka.AttributedNetwork.hypergraph(load_csr(z, p + "S"), on["X"])
         else:
-            net = ancka.AttributedNetwork.graph(S, on["X"], directed=bool(z[p + "directed"]))
+            net = ancka.AttributedNetwork.graph(load_csr(z, p + "S"), on["X"],
+                                                directed=bool(z[p + "directed"]))
         net, _ = ancka.validate_network(net)
         np.testing.assert_array_equal(ancka.node_degrees(net), oc.structural_degree(on))
 
