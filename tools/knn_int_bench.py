@@ -12,7 +12,8 @@ from paper_2408_05459_b200 import synth  # noqa: E402
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "dblp"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-inst = synth.make(shape, seed=0)
+scale = float(sys.argv[3]) if len(sys.argv) > 3 else 1.0
+inst = synth.make(shape, seed=0, scale=scale)
 X = inst.X
 xa = kn.DeviceAttributes(X, kn.integer_exact(X))
 n, d = X.shape
