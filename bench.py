@@ -161,7 +161,7 @@ def run_reference(args):
         return
     inst = make_instance(args.seed)
     oracle_run(make_small(), 0)                     # warm-up: imports, page-in
-    steps = max(1, min(args.steps, 3))
+    steps = max(1, min(args.steps, 2))          # ~100 s per full CPU clustering
     times = [oracle_run(inst, args.seed)[0] for _ in range(steps)]
     v = sum(times) / len(times)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "s",
