@@ -135,7 +135,7 @@ __device__ __forceinline__ void gram_add(const float (&z)[kC], double (&g)[kNP])
 
 // z = mix(s, k) for row i, store, add to the Gram partial
 __device__ __forceinline__ void finish8(const OfParams& P, int64_t i, const float* Qp,
-                                        float (&s)[kC], float (&kk)[kC]) {
+                                        float (&s)[kC], float (&kk)[kC], float (&z)[kC]) {
   const ancka_operator& op = P.op;
   if (op.selfloop[i]) {
     float x[kC];
@@ -145,10 +145,18 @@ __device__ __forceinline__ void finish8(const OfParams& P, int64_t i, const floa
   }
   const float b = __ldg(static_cast<const float*>(op.beta) + i);
   const float omb = 1.f - b;
-  float z[kC];
 #pragma unroll
   for (int u = 0; u < kC; ++u) z[u] = u < P.c ? omb * s[u] + b * kk[u] : 0.f;
   f8_store(P.Z + i * kC, z);
+}
+
+// this row's 36 Gram products (f32) into shared-memory slot `slot`
+__device__ __forceinline__ void gram_stage(float* gsm, int slot, const float (&z)[kC]) {
+  int qq = 0;
+#pragma unroll
+  for (int a = 0; a < kC; ++a)
+#pragma unroll
+    for (int b2 = a; b2 < kC; ++b2, ++qq) gsm[slot * (kNP + 1) + qq] = z[a] * z[b2];
 }
 
 // deterministic CTA reduction of the per-thread Gram partial -> global slot
@@ -230,33 +238,60 @@ orth_fused_kernel(OfParams P) {
     const float* Ssrc = hyper ? P.T : Qp;
     unsigned long long p2_t0 = 0;
     if (P.tdbg && threadIdx.x == 0) p2_t0 = of_timer();
-    // ---- P2: rows (Z + Gram): regular rows by 8-lane groups ...
+    // ---- P2: rows of Z with their Gram contributions: regular rows by
+    // kGW-lane groups (cost-ordered), long rows (KNN hubs) by whole warps.
+    // Each produced row's 36 products are staged in shared memory (one slot
+    // per lane group) and summed into per-thread f64 partials after every
+    // round, so the Gram needs no second pass over Z and no extra barrier.
+    constexpr int kGS = 7;                         // summing threads per entry
+    const int gq = threadIdx.x % kNP, gg = threadIdx.x / kNP;
+    constexpr int kSlots = kOfThreads / kGW;       // regular-row slots per round
+    double gacc = 0.0;
+    auto gram_round = [&](int nslots) {
+      __syncthreads();
+      if (gg < kGS)
+        for (int r = gg; r < nslots; r += kGS) gacc += (double)gsm[r * (kNP + 1) + gq];
+      __syncthreads();
+    };
     const int64_t nround = ((n + noct - 1) / noct) * noct;
     for (int64_t i0 = goct; i0 < nround; i0 += noct) {
       const int64_t i = (sp.row_order && i0 < n) ? (int64_t)sp.row_order[i0] : i0;
       const bool live = i0 < n && !(sp.is_long && sp.is_long[i]);
-      float s[kC] = {}, kk[kC] = {};
+      float s[kC] = {}, kk[kC] = {}, z[kC] = {};
       if (live) {
         seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, kGW, s);
         seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], sub, kGW, kk);
       }
       group_sum(s, kGW);
       group_sum(kk, kGW);
-      if (live && sub == 0) finish8(P, i, Qp, s, kk);
+      if (live && sub == 0) finish8(P, i, Qp, s, kk, z);
+      if (sub == 0) gram_stage(gsm, threadIdx.x / kGW, z);   // zeros when not live
+      gram_round(kSlots);
     }
-    // ... and long rows (KNN hubs) by whole warps
     const int64_t lround = ((sp.n_long + nwarps - 1) / nwarps) * nwarps;
     for (int64_t li = gwarp; li < lround; li += nwarps) {
       const bool live = li < sp.n_long;
       const int64_t i = live ? sp.long_rows[li] : 0;
-      float s[kC] = {}, kk[kC] = {};
+      float s[kC] = {}, kk[kC] = {}, z[kC] = {};
       if (live) {
         seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], lane, 32, s);
         seg8_strided(K_ci, Kval, Qp, K_rp[i], K_rp[i + 1], lane, 32, kk);
       }
       group_sum(s, 32);
       group_sum(kk, 32);
-      if (live && lane == 0) finish8(P, i, Qp, s, kk);
+      if (live && lane == 0) finish8(P, i, Qp, s, kk, z);
+      if (lane == 0) gram_stage(gsm, threadIdx.x >> 5, z);
+      gram_round(kOfThreads / 32);
+    }
+    // CTA total of the Gram partials -> one fixed-point atomic per entry
+    // (integer sums are order independent: bit-reproducible)
+    if (gg < kGS) red[gg * kNP + gq] = gacc;
+    __syncthreads();
+    for (int qq = threadIdx.x; qq < kNP; qq += blockDim.x) {
+      double v = 0.0;
+      for (int g2 = 0; g2 < kGS; ++g2) v += red[g2 * kNP + qq];
+      atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + qq),
+                (unsigned long long)(long long)llrint(v * kFx));
     }
     OF_STAMP(2);
     if (P.tdbg) {                        // per-CTA P2 duration: max and sum over CTAs
@@ -267,48 +302,7 @@ orth_fused_kernel(OfParams P) {
         atomicAdd(P.tdbg + 10, dt);
       }
     }
-    grid.sync();
-    OF_STAMP(8);
-    // ---- P3: Gram partial of this CTA's rows of Z: thread = row, its 36
-    // f32 products go to shared memory, then 7 threads per entry sum fixed
-    // row subsets in f64 and combine in fixed order; one fixed-point atomic
-    // per entry and CTA (integer sums: order independent, bit-reproducible)
-    {
-      const int64_t rows_per_cta = (n + nb - 1) / nb;
-      const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
-      const int64_t r1 = lmin(n, r0 + rows_per_cta);
-      constexpr int kGS = 7;                       // summing threads per entry
-      const int q = threadIdx.x % kNP, g = threadIdx.x / kNP;
-      double acc = 0.0;
-      for (int64_t base = r0; base < r1; base += kOfThreads) {
-        const int tr = (int)lmin(kOfThreads, r1 - base);
-        __syncthreads();
-        if (threadIdx.x < tr) {
-          float z[kC];
-          f8_load(P.Z + (base + threadIdx.x) * kC, z);
-          int qq = 0;
-#pragma unroll
-          for (int a = 0; a < kC; ++a)
-#pragma unroll
-            for (int b2 = a; b2 < kC; ++b2, ++qq) gsm[threadIdx.x * (kNP + 1) + qq] = z[a] * z[b2];
-        }
-        __syncthreads();
-        if (g < kGS)
-          for (int r = g; r < tr; r += kGS) acc += (double)gsm[r * (kNP + 1) + q];
-      }
-      __syncthreads();
-      if (g < kGS) red[g * kNP + q] = acc;
-      __syncthreads();
-      for (int qq = threadIdx.x; qq < kNP; qq += blockDim.x) {
-        double v = 0.0;
-        for (int gg = 0; gg < kGS; ++gg) v += red[gg * kNP + qq];
-        atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + qq),
-                  (unsigned long long)(long long)llrint(v * kFx));
-      }
-      __syncthreads();
-    }
-    OF_STAMP(3);
-    grid.sync();
+    grid.sync();                        // Z and the Gram complete
     OF_STAMP(4);
     // ---- P4: every CTA: Gram (fixed-point sums), Cholesky, R^-1 (identical)
     if (threadIdx.x < kNP) G[threadIdx.x] = (double)P.gram_fx[buf * kNP + threadIdx.x] * kFxInv;

@@ -29,6 +29,6 @@ for rep in range(3):
     b.record()
     b.synchronize()
     t = loop.stats[4:15].cpu().numpy().view(np.uint64)
-    names = ["P1", "sync1", "P2", "gram", "sync2", "chol", "apply", "sync3", "syncP2",
+    names = ["P1", "sync1", "P2+gram", "-", "sync2", "chol", "apply", "sync3", "-",
              "P2max_sum_over_steps", "P2sum_all_ctas"]
     print(f"20 steps {a.elapsed_time(b)*1e3:.0f} us:", {nm: int(v) // 1000 for nm, v in zip(names, t)}, "us")
