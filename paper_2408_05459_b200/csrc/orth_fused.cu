@@ -300,6 +300,7 @@ orth_fused_kernel(OfParams P) {
         const unsigned long long dt = of_timer() - p2_t0;
         atomicMax(P.tdbg + 9, dt);
         atomicAdd(P.tdbg + 10, dt);
+        atomicMax(P.tdbg + 11, (dt << 20) | (unsigned long long)blockIdx.x);
       }
     }
     grid.sync();                        // Z and the Gram complete
@@ -447,8 +448,12 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
   ANCKA_REQUIRE(per_sm >= 1, ANCKA_ERR_UNSUPPORTED, "orth_block does not fit an SM");
   int64_t want = ceil_div(op32->n, 32);
   if (const char* g = getenv("ANCKA_ORTH_GRID")) want = std::max(1, atoi(g));
+  // two CTAs per SM: more CTAs shorten each CTA's row share but lengthen the
+  // grid barriers and the tail (measured at the DBLP shape: 2/SM 861 us per
+  // 20 steps, 4/SM 975 us)
+  const int64_t cap = getenv("ANCKA_ORTH_GRID") ? of_grid_cap() : 2 * (int64_t)sms;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
-      want, std::min<int64_t>((int64_t)per_sm * sms, of_grid_cap())));
+      want, std::min<int64_t>((int64_t)per_sm * sms, std::min<int64_t>(cap, of_grid_cap()))));
   void* args[] = {&P};
   note_launch();
   ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)orth_fused_kernel, dim3(grid), dim3(kOfThreads),

@@ -28,7 +28,8 @@ for rep in range(3):
     loop.run(20)
     b.record()
     b.synchronize()
-    t = loop.stats[4:15].cpu().numpy().view(np.uint64)
+    t = loop.stats[4:16].cpu().numpy().view(np.uint64)
+    print("slowest P2 CTA:", int(t[11]) & 0xFFFFF, "dt us", (int(t[11]) >> 20) / 1000)
     names = ["P1", "sync1", "P2+gram", "-", "sync2", "chol", "apply", "sync3", "-",
              "P2max_sum_over_steps", "P2sum_all_ctas"]
     print(f"20 steps {a.elapsed_time(b)*1e3:.0f} us:", {nm: int(v) // 1000 for nm, v in zip(names, t)}, "us")
