@@ -4,9 +4,13 @@ One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank r
 owns a contiguous block of node rows [r0, r1) (balanced by operator
 nonzeros) and, for hypergraphs, a block of hyperedges [e0, e1):
 
-* KNN       query-row sharding: rank r computes the exact top-K lists of its
-            rows against all keys (every rank holds the quantised X), then the
-            lists are all-gathered and A_K / P_K are assembled on every rank.
+* KNN       query-stationary ring: rank r keeps its rows [r0, r1) as queries
+            and as its first key block; the other key shards travel around
+            the ring (P2P send/recv, overlapped with the kernel).  Each step
+            ranks (own rows + visiting shard) and merges the lists exactly
+            (score desc, index asc), so every rank ends with its rows' global
+            top-K holding only 2 shards of X at a time; the lists are then
+            all-gathered and A_K / P_K are assembled on every rank.
 * operator  per apply: all-gather Q (n x c); hypergraphs compute their share
             of T = P_E Q and all-gather T; each rank produces its rows of
             Z = (I-B) P_struct Q + B P_K Q.
@@ -171,6 +175,29 @@ class DistOperator:
                       tag, tagval, scale, c, "f64")
 
 
+def knn_ring(B, X, K: int, plan: Plan):
+    """Exact top-K of rows [r0, r1) against all n keys, with only the own shard
+    and one visiting shard of X resident (SURVEY.md §8(e) KNN ring).
+
+    Step 0 ranks the own rows; step s ranks (own rows + the shard of rank
+    r - s).  Every key of shard b that belongs to a row's global top-K is in
+    that row's top-K over (own rows + shard b) -- its rank there cannot exceed
+    its global rank -- so merging the step lists by (score desc, index asc)
+    and keeping K gives the global lists exactly."""
+    rank, world = plan.rank, plan.world
+    r0, r1 = plan.r0, plan.r1
+    mine = B.x_shard(X, r0, r1)
+    ids, sc = B.knn_local(mine, None, K, r0, 0)
+    block, src = mine, rank
+    pending = B.ring_start(block) if world > 1 else None
+    for _step in range(1, world):
+        block, src = B.ring_finish(pending), (src - 1) % world
+        pending = B.ring_start(block) if _step < world - 1 else None   # overlaps the kernel
+        i2, s2 = B.knn_local(mine, block, K, r0, int(plan.rows[src]))
+        ids, sc = B.merge_lists(ids, sc, i2, s2, K)
+    return ids, sc
+
+
 def _centers(deg: np.ndarray, k: int) -> np.ndarray:
     n = deg.size
     nz = int((deg > 0).sum())
@@ -209,8 +236,8 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     fac = HostFactors(net)
     plan = make_plan(fac, K, rank, world)
 
-    # ---- KNN: query-row sharding, all-gather of the lists, replicated P_K
-    ids_loc, sc_loc = B.knn_rows(net.attributes, K, plan.r0, plan.r1)
+    # ---- KNN: query-stationary key ring, all-gather of the lists, replicated P_K
+    ids_loc, sc_loc = knn_ring(B, net.attributes, K, plan)
     ids = B.all_gather_rows(ids_loc, plan.row_counts())
     scores = B.all_gather_rows(sc_loc, plan.row_counts())
     pk_rows, zero_rows = B.knn_graph_rows(ids, scores, n, plan.r0, plan.r1)
@@ -389,6 +416,117 @@ class CudaBackend:
         from .knn import knn_search_exact_device
         ids, sc = knn_search_exact_device(X, K, rows=(q0, q1))
         return ids, sc
+
+    # --- KNN key ring: shards are ("csr", indptr, indices, data, d) or ("dense", X)
+    def x_shard(self, X, r0, r1):
+        torch = self.torch
+        if sp.issparse(X):
+            x = sp.csr_matrix(X)[r0:r1]
+            return ("csr", torch.from_numpy(x.indptr.astype(np.int64)).cuda(),
+                    torch.from_numpy(x.indices.astype(np.int32)).cuda(),
+                    torch.from_numpy(x.data.astype(np.float64)).cuda(), X.shape[1])
+        return ("dense", torch.from_numpy(np.ascontiguousarray(X[r0:r1], dtype=np.float64)).cuda())
+
+    def _concat(self, a, b):
+        torch = self.torch
+        if b is None:
+            return a
+        if a[0] == "csr":
+            ip = torch.cat([a[1], b[1][1:] + a[1][-1]])
+            return ("csr", ip, torch.cat([a[2], b[2]]), torch.cat([a[3], b[3]]), a[4])
+        return ("dense", torch.cat([a[1], b[1]]))
+
+    def knn_local(self, mine, block, K, r0, boff):
+        """Top-K of the own rows over (own rows + block), global indices.  The
+        two shards are concatenated in global row order, so the kernel's
+        index tie-break is the global one."""
+        from .knn import DeviceAttributes, knn_search_exact_device
+        torch = self.torch
+        rows_of = (lambda t: int(t[1].numel() - 1)) if mine[0] == "csr" else (lambda t: int(t[1].shape[0]))
+        nq = rows_of(mine)
+        first = block is not None and boff < r0
+        x = self._concat(block, mine) if first else self._concat(mine, block)
+        nb = rows_of(block) if first else 0
+        if x[0] == "csr":
+            xa = DeviceAttributes.from_device_csr(x[1], x[2], x[3], (int(x[1].numel() - 1), x[4]))
+        else:
+            xa = DeviceAttributes.from_device_dense(x[1])
+        kk = min(K, xa.shape[0] - 1)
+        ids, sc = knn_search_exact_device(xa, kk, rows=(nb, nb + nq))
+        ids = ids.long()
+        if first:
+            g = torch.where(ids < nb, ids + boff, ids - nb + r0)
+        else:
+            g = torch.where(ids < nq, ids + r0, ids - nq + boff)
+        g = torch.where(ids < 0, torch.full_like(ids, -1), g)
+        if kk < K:
+            pad = K - kk
+            g = torch.cat([g, torch.full((nq, pad), -1, dtype=g.dtype, device=g.device)], 1)
+            sc = torch.cat([sc, torch.zeros((nq, pad), dtype=sc.dtype, device=sc.device)], 1)
+        return g, sc
+
+    def merge_lists(self, ia, sa, ib, sb, K):
+        """Per row: union, dedup, order (score desc, index asc), first K."""
+        torch = self.torch
+        ids = torch.cat([ia, ib], 1)
+        sc = torch.cat([sa, sb], 1)
+        big = torch.iinfo(torch.int64).max
+        key_i = torch.where(ids < 0, torch.full_like(ids, big), ids)
+        o = torch.argsort(key_i, dim=1, stable=True)               # index asc
+        ids, sc, key_i = ids.gather(1, o), sc.gather(1, o), key_i.gather(1, o)
+        dup = torch.zeros_like(ids, dtype=torch.bool)
+        dup[:, 1:] = (key_i[:, 1:] == key_i[:, :-1]) & (ids[:, 1:] >= 0)
+        s_key = torch.where((ids < 0) | dup, torch.full_like(sc, -np.inf), sc)
+        o = torch.argsort(-s_key, dim=1, stable=True)               # score desc, ties keep index asc
+        ids, s_key = ids.gather(1, o)[:, :K], s_key.gather(1, o)[:, :K]
+        ok = s_key > -np.inf
+        return torch.where(ok, ids, torch.full_like(ids, -1)), torch.where(ok, s_key, torch.zeros_like(s_key))
+
+    def _p2p(self, send_tensors, recv_tensors):
+        """Send to rank+1 and receive from rank-1.  NCCL moves device tensors
+        over NVLink; other backends (gloo in the tests) go through host copies."""
+        dist = self.dist
+        nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        if dist.get_backend(self.group) != "nccl":
+            host_recv = [t.cpu() for t in recv_tensors]
+            ops = [dist.P2POp(dist.isend, t.cpu(), nxt, group=self.group) for t in send_tensors]
+            ops += [dist.P2POp(dist.irecv, t, prv, group=self.group) for t in host_recv]
+            reqs = dist.batch_isend_irecv(ops)
+            for r in reqs:
+                r.wait()
+            for dst, src in zip(recv_tensors, host_recv):
+                dst.copy_(src)
+            return []
+        ops = [dist.P2POp(dist.isend, t, nxt, group=self.group) for t in send_tensors]
+        ops += [dist.P2POp(dist.irecv, t, prv, group=self.group) for t in recv_tensors]
+        return dist.batch_isend_irecv(ops)
+
+    def ring_start(self, block):
+        torch = self.torch
+        arrays = list(block[1:4]) if block[0] == "csr" else [block[1]]
+        hdr = torch.tensor([a.numel() for a in arrays] + ([block[4]] if block[0] == "csr"
+                                                          else list(block[1].shape)),
+                           dtype=torch.int64, device="cuda")
+        rh = torch.empty_like(hdr)
+        for r in self._p2p([hdr], [rh]):
+            r.wait()
+        sizes = rh.cpu().tolist()
+        if block[0] == "csr":
+            bufs = [torch.empty(sizes[0], dtype=torch.int64, device="cuda"),
+                    torch.empty(sizes[1], dtype=torch.int32, device="cuda"),
+                    torch.empty(sizes[2], dtype=torch.float64, device="cuda")]
+            meta = ("csr", sizes[3])
+        else:
+            bufs = [torch.empty((sizes[1], sizes[2]), dtype=torch.float64, device="cuda")]
+            meta = ("dense",)
+        reqs = self._p2p(arrays, bufs)
+        return reqs, bufs, meta
+
+    def ring_finish(self, pending):
+        reqs, bufs, meta = pending
+        for r in reqs:
+            r.wait()
+        return ("csr", bufs[0], bufs[1], bufs[2], meta[1]) if meta[0] == "csr" else ("dense", bufs[0])
 
     def knn_graph_rows(self, ids, scores, n, r0, r1):
         from ._device import DeviceCSR

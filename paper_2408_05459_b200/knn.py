@@ -162,6 +162,29 @@ class DeviceAttributes:
                                     self.dense.shape[1])
         self.level = int(level)
 
+    @classmethod
+    def from_device_csr(cls, indptr, indices, data, shape) -> "DeviceAttributes":
+        """CSR already in HBM (e.g. a shard received over the KNN ring)."""
+        self = cls.__new__(cls)
+        self.shape, self.dense = tuple(shape), None
+        self.indptr, self.indices, self.data = indptr, indices, data
+        level = self._check(indptr.data_ptr(), data.data_ptr(), 0, 0)
+        if level <= 0:
+            t = torch.sparse_csr_tensor(indptr, indices.long(), data, size=self.shape)
+            self.dense = t.to_dense().contiguous()
+            self.indptr = self.indices = self.data = None
+        self.level = int(level)
+        return self
+
+    @classmethod
+    def from_device_dense(cls, x) -> "DeviceAttributes":
+        self = cls.__new__(cls)
+        self.shape, self.dense = tuple(x.shape), x.contiguous()
+        self.indptr = self.indices = self.data = None
+        self.level = int(self._check(None, self.dense.data_ptr(), self.dense.stride(0),
+                                     self.dense.shape[1]))
+        return self
+
     def _check(self, rowptr, values, ld, ncols) -> int:
         out = torch.empty(3, dtype=torch.float64, device=dev())
         _lib.call("ancka_attr_check", rowptr, values, self.shape[0], ld, ncols, out.data_ptr(),

@@ -71,6 +71,67 @@ class NumpyBackend:
         ids, sc = oc.knn_exact(X, K)        # the checker; rows sliced per rank
         return ids[q0:q1], sc[q0:q1]
 
+    # --- KNN key ring over gloo
+    @staticmethod
+    def x_shard(X, r0, r1):
+        return sp.csr_matrix(X)[r0:r1] if sp.issparse(X) else np.asarray(X, dtype=np.float64)[r0:r1]
+
+    @staticmethod
+    def knn_local(mine, block, K, r0, boff):
+        from oracle import ancka_cpu as oc
+        nq = mine.shape[0]
+        first = block is not None and boff < r0          # concatenate in global order
+        parts = [mine] if block is None else ([block, mine] if first else [mine, block])
+        x = sp.vstack(parts).tocsr() if sp.issparse(mine) else np.vstack(parts)
+        nb = block.shape[0] if first else 0
+        kk = min(K, x.shape[0] - 1)
+        ids, sc = oc.knn_exact(x, kk)
+        ids, sc = ids[nb:nb + nq], sc[nb:nb + nq]
+        if first:
+            g = np.where(ids < nb, ids + boff, ids - nb + r0)
+        else:
+            g = np.where(ids < nq, ids + r0, ids - nq + boff)
+        g = np.where(ids < 0, -1, g)
+        if kk < K:
+            g = np.hstack([g, np.full((nq, K - kk), -1)])
+            sc = np.hstack([sc, np.zeros((nq, K - kk))])
+        return g, sc
+
+    @staticmethod
+    def merge_lists(ia, sa, ib, sb, K):
+        ids, sc = np.hstack([ia, ib]), np.hstack([sa, sb])
+        out_i = np.full((ids.shape[0], K), -1, dtype=np.int64)
+        out_s = np.zeros((ids.shape[0], K))
+        for r in range(ids.shape[0]):
+            best = {}
+            for j, v in zip(ids[r], sc[r]):
+                if j >= 0:
+                    best[int(j)] = v
+            order = sorted(best.items(), key=lambda t: (-t[1], t[0]))[:K]
+            for c, (j, v) in enumerate(order):
+                out_i[r, c], out_s[r, c] = j, v
+        return out_i, out_s
+
+    def ring_start(self, block):
+        import pickle
+        data = np.frombuffer(pickle.dumps(block), dtype=np.uint8)
+        n_out = torch.tensor([data.size], dtype=torch.int64)
+        n_in = torch.empty(1, dtype=torch.int64)
+        nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
+        for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, n_out, nxt),
+                                         dist.P2POp(dist.irecv, n_in, prv)]):
+            r.wait()
+        buf = torch.empty(int(n_in.item()), dtype=torch.uint8)
+        for r in dist.batch_isend_irecv([dist.P2POp(dist.isend, torch.from_numpy(data.copy()), nxt),
+                                         dist.P2POp(dist.irecv, buf, prv)]):
+            r.wait()
+        return buf
+
+    @staticmethod
+    def ring_finish(buf):
+        import pickle
+        return pickle.loads(buf.numpy().tobytes())
+
     @staticmethod
     def knn_graph_rows(ids, scores, n, r0, r1):
         from oracle import ancka_cpu as oc
@@ -172,8 +233,9 @@ def test_partition_rows_balanced():
         assert max(loads) <= cost.sum() / world + cost.max()
 
 
-@pytest.mark.parametrize("shape,n,seed", [("cora", 220, 0), ("dblp", 260, 2)])
-def test_world2_matches_single_process_oracle(shape, n, seed):
+@pytest.mark.parametrize("shape,n,seed,world", [("cora", 220, 0, 2), ("dblp", 260, 2, 2),
+                                               ("amazon2m", 240, 1, 3)])
+def test_world2_matches_single_process_oracle(shape, n, seed, world):
     from sklearn.metrics import adjusted_rand_score
 
     from oracle import ancka_cpu as oc
@@ -181,7 +243,7 @@ def test_world2_matches_single_process_oracle(shape, n, seed):
     port = _free_port()
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, port, shape, n, seed, out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, port, shape, n, seed, out), nprocs=world, join=True)
     inst, _ = _case(shape, n, seed)
     ref = oc.run({"kind": inst.kind, "S": inst.structure, "X": inst.X}, inst.k, knn_k=10, seed=seed)
     l0, phi0, it0, stop0 = out[0]
@@ -237,7 +299,7 @@ def _gpu_worker(rank, world, port, i, out):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("i", [0, 3])
+@pytest.mark.parametrize("i", [0, 3, 4])          # binary graph, hypergraph, real-valued
 def test_cuda_backend_world2_collectives(golden_runs, i):
     from sklearn.metrics import adjusted_rand_score
     z, meta = golden_runs
