@@ -198,6 +198,77 @@ def knn_ring(B, X, K: int, plan: Plan):
     return ids, sc
 
 
+def discretize_dist(B, Q_loc, k: int, plan: Plan, max_iter: int = 100, tol: float = 1e-10):
+    """discretize (engine.py:183-263) row-partitioned:
+    argmax and the cluster sums are local; per round the k x k sums and the
+    k counts are all-reduced and every rank runs the same k x k SVD.  The
+    empty-cluster reseed and the prototype start use global (value, index)
+    reductions.  Returns (local labels as numpy, global empties count)."""
+    n = plan.n
+    qt = B.disc_prepare(Q_loc, 1, k)
+
+    def gather_best(v, gidx, extra=0.0, want_max=True):
+        rows = B.all_gather_small(np.array([v, float(gidx), float(extra)]))
+        ok = [r for r in rows if r[1] >= 0]
+        if not ok:
+            return None
+        key = (lambda r: (-r[0], r[1])) if want_max else (lambda r: (r[0], r[1]))
+        return min(ok, key=key)
+
+    def run(R0):
+        objs, conv, R = [], False, R0
+        lab = None
+        empties_left = 0
+        for _ in range(max_iter):
+            R_used = R
+            lab, margin = B.disc_score(qt, R)
+            sizes = B.all_reduce(B.disc_counts(lab, k).astype(np.float64)).astype(np.int64)
+            for c in np.flatnonzero(sizes == 0):            # _reseed_empty_columns
+                if k < 2:
+                    break
+                v, li, old = B.disc_best_movable(lab, margin, sizes)
+                best = gather_best(v, plan.r0 + li if li >= 0 else -1, old)
+                if best is None:
+                    break
+                g, old = int(best[1]), int(best[2])
+                if plan.r0 <= g < plan.r1:
+                    B.disc_set_label(lab, g - plan.r0, int(c))
+                sizes[old] -= 1
+                sizes[c] += 1
+            S, cnt = B.disc_cluster_sums(qt, lab, k)
+            M = np.divide(S, cnt[:, None], out=np.zeros_like(S), where=cnt[:, None] > 0)
+            try:
+                u, omega, vh = np.linalg.svd(M)
+            except np.linalg.LinAlgError:
+                import scipy.linalg
+                u, omega, vh = scipy.linalg.svd(M, lapack_driver="gesvd")
+            objs.append(n - 2.0 * float(omega.sum()))
+            empties_left = int((cnt == 0).sum())
+            if len(objs) >= 2 and abs(objs[-1] - objs[-2]) < tol:
+                conv = True
+                break
+            R = vh.T @ u.T
+        return objs, conv, R_used, lab, empties_left
+
+    def prototype():
+        R = np.zeros((k, k))
+        R[:, 0] = B.all_reduce(B.disc_row(qt, 0) if plan.r0 == 0 < plan.r1 else np.zeros(k))
+        B.disc_proto_reset(qt)
+        for j in range(1, k):
+            v, li = B.disc_proto_pass(qt, R[:, j - 1])
+            best = gather_best(v, plan.r0 + li if li >= 0 else -1, want_max=False)
+            g = int(best[1])
+            R[:, j] = B.all_reduce(B.disc_row(qt, g - plan.r0) if plan.r0 <= g < plan.r1
+                                   else np.zeros(k))
+        return R
+
+    r0_res = run(np.eye(k))
+    r1_res = run(prototype())
+    win = 1 if r1_res[0][-1] < r0_res[0][-1] - 1e-15 else 0
+    res = (r0_res, r1_res)[win]
+    return B.disc_labels_host(res[3]), res[4]
+
+
 def _centers(deg: np.ndarray, k: int) -> np.ndarray:
     n = deg.size
     nz = int((deg > 0).sum())
@@ -303,10 +374,10 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
         t = 1
         while True:
             if t % params.tau == 0:
-                Q_full = B.all_gather_rows(Q_loc, plan.row_counts())
-                labels, info = B.discretize(Q_full, 1, k)
-                if info["empties"] > 0:
+                lab_loc, empties = discretize_dist(B, Q_loc, k, plan)
+                if empties > 0:
                     raise NetworkError("cannot repair empty clusters: no movable nodes")
+                labels = B.all_gather_labels(lab_loc, plan.row_counts())
                 phi = mhc(labels, "f32")
                 hist.append((t, phi))
                 if phi < best_phi:
@@ -614,11 +685,100 @@ class CudaBackend:
             _qr_f64_inplace(q, c)
         return q[:, :c].cpu().numpy()
 
-    def discretize(self, Q_full, col0, k):
-        from .engine import DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, _discretize_device
+    # --- row-partitioned discretisation primitives (discretize_dist)
+    def disc_prepare(self, Q_loc, col0, k):
+        torch, _lib = self.torch, self._lib
+        from ._device import ld_for
+        n = Q_loc.shape[0]
+        ldt = ld_for(k, torch.float32)
+        st = {"k": k, "ldt": ldt, "n": n,
+              "qt": torch.empty((n, ldt), dtype=torch.float32, device="cuda"),
+              "zero": torch.zeros(1, dtype=torch.int32, device="cuda"),
+              "R": torch.zeros((k, ldt), dtype=torch.float32, device="cuda"),
+              "acc": torch.zeros(max(n, 1), dtype=torch.float64, device="cuda"),
+              "rcol": torch.zeros(k, dtype=torch.float64, device="cuda"),
+              "S": torch.empty(k * k, dtype=torch.int64, device="cuda"),
+              "cnt": torch.empty(k, dtype=torch.int64, device="cuda")}
+        bits = int(np.ceil(np.log2(max(self.all_reduce(np.array([float(n)]))[0], 1) + 1)))
+        st["scale"] = float(2.0 ** (61 - bits))
+        if n:
+            _lib.call("ancka_disc_normalize", Q_loc.data_ptr(), Q_loc.stride(0), col0, n, k,
+                      st["qt"].data_ptr(), ldt, st["zero"].data_ptr(), _lib.stream())
+        return st
+
+    def disc_score(self, st, R):
+        torch, _lib = self.torch, self._lib
+        k, n = st["k"], st["n"]
+        st["R"][:, :k] = torch.from_numpy(R.astype(np.float32)).cuda()
+        lab = torch.zeros(max(n, 1), dtype=torch.int32, device="cuda")
+        margin = torch.zeros(max(n, 1), dtype=torch.float32, device="cuda")
+        if n:
+            _lib.call("ancka_disc_score", st["qt"].data_ptr(), st["ldt"], n, k, st["R"].data_ptr(),
+                      st["ldt"], lab.data_ptr(), margin.data_ptr(), _lib.stream())
+        return lab[:n], margin[:n]
+
+    def disc_counts(self, lab, k):
+        return self.torch.bincount(lab.long(), minlength=k).cpu().numpy()
+
+    def disc_best_movable(self, lab, margin, sizes):
         torch = self.torch
-        lab = torch.empty(Q_full.shape[0], dtype=torch.int32, device="cuda")
-        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device="cuda")
-        _discretize_device(Q_full, col0, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab, info)
-        inf = info[:8].cpu().numpy()
-        return lab.cpu().numpy().astype(np.int64), {"empties": int(inf[4]), "rounds": int(inf[1])}
+        if lab.numel() == 0:
+            return -np.inf, -1, 0
+        sz = torch.from_numpy(sizes).cuda()
+        movable = sz[lab.long()] >= 2
+        if not bool(movable.any()):
+            return -np.inf, -1, 0
+        cand = torch.where(movable, margin.double(), torch.full_like(margin, -np.inf).double())
+        i = int(torch.argmax(cand))                      # first maximum
+        return float(cand[i]), i, int(lab[i])
+
+    def disc_set_label(self, lab, i, c):
+        lab[i] = c
+
+    def disc_cluster_sums(self, st, lab, k):
+        torch, _lib = self.torch, self._lib
+        n = st["n"]
+        if n:
+            _lib.call("ancka_disc_accumulate", st["qt"].data_ptr(), st["ldt"], n, k, lab.data_ptr(),
+                      st["scale"], st["S"].data_ptr(), st["cnt"].data_ptr(), _lib.stream())
+        else:
+            st["S"].zero_()
+            st["cnt"].zero_()
+        both = torch.cat([st["S"], st["cnt"]])
+        if self.world > 1:                               # int64 sums: exact, order free
+            self.dist.all_reduce(both, group=self.group)
+        h = both.cpu().numpy()
+        return h[:k * k].reshape(k, k).astype(np.float64) / st["scale"], h[k * k:].astype(np.float64)
+
+    def disc_proto_reset(self, st):
+        st["acc"].zero_()
+
+    def disc_proto_pass(self, st, rcol):
+        torch, _lib = self.torch, self._lib
+        n, k = st["n"], st["k"]
+        if n == 0:
+            return np.inf, -1
+        st["rcol"].copy_(torch.from_numpy(rcol))
+        _lib.call("ancka_disc_proto_pass", st["qt"].data_ptr(), st["ldt"], n, k,
+                  st["rcol"].data_ptr(), st["acc"].data_ptr(), _lib.stream())
+        i = int(torch.argmin(st["acc"][:n]))             # first minimum
+        return float(st["acc"][i]), i
+
+    def disc_row(self, st, i):
+        return st["qt"][i, :st["k"]].double().cpu().numpy()
+
+    def disc_labels_host(self, lab):
+        return lab.cpu().numpy().astype(np.int64)
+
+    def all_gather_small(self, a):
+        torch = self.torch
+        t = torch.as_tensor(np.asarray(a, dtype=np.float64), device="cuda")
+        if self.world == 1:
+            return [t.cpu().numpy()]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return [o.cpu().numpy() for o in out]
+
+    def all_gather_labels(self, lab_loc, counts):
+        t = self.torch.as_tensor(lab_loc.astype(np.float64), device="cuda")[:, None]
+        return self.all_gather_rows(t, counts)[:, 0].cpu().numpy().astype(np.int64)

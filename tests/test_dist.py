@@ -187,12 +187,75 @@ class NumpyBackend:
             q, r = np.linalg.qr(Z)
         return q * np.where(np.diag(r) < 0, -1.0, 1.0)
 
+    # --- row-partitioned discretisation primitives (f64, as the reference)
     @staticmethod
-    def discretize(Q_full, col0, k):
-        from oracle import ancka_cpu as oc
-        d = oc.discretize(np.asarray(Q_full)[:, col0: col0 + k])
-        lab = d["labels"]
-        return lab, {"empties": int((np.bincount(lab, minlength=k) == 0).sum())}
+    def disc_prepare(Q_loc, col0, k):
+        q = np.asarray(Q_loc, dtype=np.float64)[:, col0:col0 + k]
+        nrm = np.linalg.norm(q, axis=1)
+        qt = np.divide(q, nrm[:, None], out=np.zeros_like(q), where=nrm[:, None] > 0)
+        return {"qt": qt, "k": k, "acc": np.zeros(q.shape[0])}
+
+    @staticmethod
+    def disc_score(st, R):
+        sc = st["qt"] @ R
+        lab = np.argmax(sc, axis=1)
+        margin = np.partition(sc, -2, axis=1)[:, -2] if st["k"] >= 2 else sc[:, 0]
+        return lab, margin
+
+    @staticmethod
+    def disc_counts(lab, k):
+        return np.bincount(lab, minlength=k)
+
+    @staticmethod
+    def disc_best_movable(lab, margin, sizes):
+        movable = sizes[lab] >= 2
+        if lab.size == 0 or not movable.any():
+            return -np.inf, -1, 0
+        cand = np.where(movable, margin, -np.inf)
+        i = int(np.argmax(cand))
+        return float(cand[i]), i, int(lab[i])
+
+    @staticmethod
+    def disc_set_label(lab, i, c):
+        lab[i] = c
+
+    def disc_cluster_sums(self, st, lab, k):
+        S = np.zeros((k, k))
+        np.add.at(S, lab, st["qt"])
+        cnt = np.bincount(lab, minlength=k).astype(np.float64)
+        both = self.all_reduce(np.concatenate([S.ravel(), cnt]))
+        return both[:k * k].reshape(k, k), both[k * k:]
+
+    @staticmethod
+    def disc_proto_reset(st):
+        st["acc"][:] = 0.0
+
+    @staticmethod
+    def disc_proto_pass(st, rcol):
+        st["acc"] += np.abs(st["qt"] @ rcol)
+        if st["acc"].size == 0:
+            return np.inf, -1
+        i = int(np.argmin(st["acc"]))
+        return float(st["acc"][i]), i
+
+    @staticmethod
+    def disc_row(st, i):
+        return st["qt"][i].copy()
+
+    @staticmethod
+    def disc_labels_host(lab):
+        return np.asarray(lab, dtype=np.int64)
+
+    def all_gather_small(self, a):
+        t = torch.from_numpy(np.asarray(a, dtype=np.float64))
+        if self.world == 1:
+            return [t.numpy()]
+        out = [torch.empty_like(t) for _ in range(self.world)]
+        dist.all_gather(out, t)
+        return [o.numpy() for o in out]
+
+    def all_gather_labels(self, lab_loc, counts):
+        return self.all_gather_rows(lab_loc.astype(np.float64)[:, None], counts)[:, 0].astype(np.int64)
 
 
 def _free_port():
