@@ -133,6 +133,7 @@ struct TopK {
 
 struct TcParams {
   int64_t n;
+  int d;              // attribute columns: MMA k-steps past d are skipped
   int nkb;            // k-blocks of 128 bytes along d
   int K;
   int key_tiles;      // total key tiles of BN
@@ -167,7 +168,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         ca = cb = kb * ROW_BYTES / (FP8 ? 1 : 2);
       });
   } else if (warp == 1) {
-    if (lane == 0) mma_issuer<FP8>(P, ntiles, p.nkb, p.debug == 2);
+    if (lane == 0) mma_issuer<FP8>(P, ntiles, p.nkb, p.debug == 2, p.d);
   } else {
     // ------------------------------------------------------ epilogue
     const int ew = warp - 2;                      // epilogue warp 0..EPI_WARPS-1
@@ -303,7 +304,7 @@ __global__ void knn_tc_prep_kernel(const double* __restrict__ X, int64_t n, int6
 // --------------------------------------------------------------- host side
 struct TcLayout {
   bool fp8;
-  int64_t n_pad, d_pad;
+  int64_t n_pad, d_pad, d;
   int nseg, tiles_per_seg, key_tiles, q_tiles;
 };
 
@@ -313,6 +314,7 @@ static TcLayout tc_layout(int64_t n, int64_t d, bool fp8, int64_t nq) {
   L.n_pad = ceil_div(n, tc::BN) * tc::BN;
   const int64_t elems_per_row = tc::ROW_BYTES / (fp8 ? 1 : 2);
   L.d_pad = ceil_div(d, elems_per_row) * elems_per_row;
+  L.d = d;
   const TcGrid g = tc_grid(n, nq);
   L.q_tiles = g.q_tiles;
   L.key_tiles = g.key_tiles;
@@ -443,6 +445,7 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
   ANCKA_TRY(tc_make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
   TcParams p;
   p.n = n;
+  p.d = (int)L.d;
   p.q_begin = q_begin;
   p.q_end = q_end;
   p.nkb = (int)(L.d_pad * (fp8 ? 1 : 2) / tc::ROW_BYTES);

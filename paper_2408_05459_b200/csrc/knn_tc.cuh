@@ -92,7 +92,8 @@ __device__ __forceinline__ void producer(const Pipe& P, const CUtensorMap* ma,
 
 // warp 1, lane 0: one 128 x 256 accumulator per key tile, alternating halves
 template <bool FP8>
-__device__ __forceinline__ void mma_issuer(const Pipe& P, int ntiles, int nkb, bool skip) {
+__device__ __forceinline__ void mma_issuer(const Pipe& P, int ntiles, int nkb, bool skip,
+                                           int k_elems = 1 << 30) {
   using namespace sm100;
   constexpr uint32_t idesc = make_idesc(FP8 ? 0u : 1u, BM, BN);
   int stage = 0;
@@ -112,7 +113,8 @@ __device__ __forceinline__ void mma_issuer(const Pipe& P, int ntiles, int nkb, b
       for (int k = 0; k < 4; ++k) {  // 4 x 32 bytes of K per 128-byte row
         const uint64_t ad = sw128_kmajor_desc(a_addr + k * 32);
         const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-        if (skip) continue;
+        // k-steps entirely in the zero padding past the last column are skipped
+        if (skip || (kb * 4 + k) * (FP8 ? 32 : 16) >= k_elems) continue;
         if (FP8) mma_f8_ss(dtm, ad, bd, idesc, (kb | k) != 0);
         else mma_f16_ss(dtm, ad, bd, idesc, (kb | k) != 0);
       }

@@ -90,6 +90,7 @@ struct RealParams {
   int64_t n;
   int nkb_seg;        // 128-byte k-blocks per operand segment (d_pad / 64)
   int d_pad;          // bf16 elements per segment
+  int d;              // attribute columns (MMA k-steps past d are all zeros: skipped)
   int K;
   int key_tiles, tiles_per_seg, nseg;
   float eps, band;    // |a - s| bound and 2 eps
@@ -317,7 +318,7 @@ knn_real_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint64_t bd = sw128_kmajor_desc(b_addr + k * 32);
-              if (skip) continue;
+              if (skip || kb * 64 + k * 16 >= p.d) continue;   // zero padding past d
               const bool first = kb == 0 && part == 0 && k == 0;
               mma_f16_ss(dtm, sw128_kmajor_desc(ahi + k * 32), bd, idesc, !first);  // hi x (hi|lo)
               if (part == 0) mma_f16_ss(dtm, sw128_kmajor_desc(alo + k * 32), bd, idesc, true);
@@ -537,6 +538,7 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
   p.n = n;
   p.nkb_seg = (int)(R.d_pad / 64);
   p.d_pad = (int)R.d_pad;
+  p.d = (int)d;
   p.K = K;
   p.key_tiles = R.g.key_tiles;
   p.tiles_per_seg = R.g.tiles_per_seg;
