@@ -365,16 +365,62 @@ __device__ void block_arg(double v, long long id, int lab, bool want_max, double
 //
 // k <= 8: warp 0 keeps X and Y in registers (entries lane and lane+32) and
 // forms the products with shuffles -- no barriers inside the iteration.
-__device__ __forceinline__ double wget(double v0, double v1, int e) {
-  const double a = __shfl_sync(0xffffffffu, v0, e & 31);
-  const double b = __shfl_sync(0xffffffffu, v1, e & 31);
+// Entry e of a warp-distributed k x k matrix (entry e in lane e, entry
+// e + 32 in the second register); TWO == false when k*k <= 32.
+template <bool TWO, typename T>
+__device__ __forceinline__ T wget(T v0, T v1, int e) {
+  const T a = __shfl_sync(0xffffffffu, v0, e & 31);
+  if (!TWO) return a;
+  const T b = __shfl_sync(0xffffffffu, v1, e & 31);
   return e < 32 ? a : b;
 }
 
-__device__ double polar_ns_small(const double* A, double* X, int k, int* iters) {
+// Newton-Schulz sweeps X <- 1.5 X - 0.5 X X^T X until no entry moves by
+// more than tol (or maxit sweeps); returns the sweeps done.
+template <bool TWO, typename T>
+__device__ __forceinline__ int ns_sweeps(T& x0, T& x1, int k, bool v0ok, bool v1ok, int r0,
+                                         int c0, int r1, int c1, T tol, int maxit) {
+  int it = 0;
+  for (; it < maxit; ++it) {
+    T y0 = 0, y1 = 0;                                   // Y = X^T X
+    for (int l = 0; l < k; ++l) {
+      const T p0 = wget<TWO>(x0, x1, l * k + (v0ok ? r0 : 0));
+      const T q0 = wget<TWO>(x0, x1, l * k + (v0ok ? c0 : 0));
+      y0 += p0 * q0;
+      if (TWO) {
+        const T p1 = wget<TWO>(x0, x1, l * k + (v1ok ? r1 : 0));
+        const T q1 = wget<TWO>(x0, x1, l * k + (v1ok ? c1 : 0));
+        y1 += p1 * q1;
+      }
+    }
+    T t0 = 0, t1 = 0;                                   // T = X Y
+    for (int l = 0; l < k; ++l) {
+      const T p0 = wget<TWO>(x0, x1, (v0ok ? r0 : 0) * k + l);
+      const T q0 = wget<TWO>(y0, y1, l * k + (v0ok ? c0 : 0));
+      t0 += p0 * q0;
+      if (TWO) {
+        const T p1 = wget<TWO>(x0, x1, (v1ok ? r1 : 0) * k + l);
+        const T q1 = wget<TWO>(y0, y1, l * k + (v1ok ? c1 : 0));
+        t1 += p1 * q1;
+      }
+    }
+    const T n0 = T(1.5) * x0 - T(0.5) * t0, n1 = T(1.5) * x1 - T(0.5) * t1;
+    const bool moved = (v0ok && fabs(n0 - x0) > tol) || (v1ok && fabs(n1 - x1) > tol);
+    x0 = v0ok ? n0 : T(0);
+    x1 = v1ok ? n1 : T(0);
+    if (!__any_sync(0xffffffffu, moved)) { ++it; break; }
+  }
+  return it;
+}
+
+// Polar factor for k <= 8, warp 0: the slow, linear first phase of the
+// iteration runs in f32 (one 32-bit shuffle per operand instead of two),
+// then f64 sweeps converge quadratically to the f64 fixed point.
+template <bool TWO>
+__device__ double polar_ns_small_t(const double* A, double* X, int k, int* iters) {
   const int kk = k * k, lane = threadIdx.x & 31;
   const int e0 = lane, e1 = lane + 32;
-  const bool v0ok = e0 < kk, v1ok = e1 < kk;
+  const bool v0ok = e0 < kk, v1ok = TWO && e1 < kk;
   double a0 = v0ok ? A[e0] : 0.0, a1 = v1ok ? A[e1] : 0.0;
   double s = warp_sum(a0 * a0 + a1 * a1);
   const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
@@ -382,32 +428,11 @@ __device__ double polar_ns_small(const double* A, double* X, int k, int* iters) 
   double x0 = v0ok ? A[(e0 % k) * k + e0 / k] * inv : 0.0;
   double x1 = v1ok ? A[(e1 % k) * k + e1 / k] * inv : 0.0;
   const int r0 = e0 / k, c0 = e0 % k, r1 = e1 / k, c1 = e1 % k;
-  int it = 0;
-  for (; it < 100; ++it) {
-    double y0 = 0.0, y1 = 0.0;                          // Y = X^T X
-    for (int l = 0; l < k; ++l) {
-      const double p0 = wget(x0, x1, l * k + (v0ok ? r0 : 0));
-      const double q0 = wget(x0, x1, l * k + (v0ok ? c0 : 0));
-      const double p1 = wget(x0, x1, l * k + (v1ok ? r1 : 0));
-      const double q1 = wget(x0, x1, l * k + (v1ok ? c1 : 0));
-      y0 += p0 * q0;
-      y1 += p1 * q1;
-    }
-    double t0 = 0.0, t1 = 0.0;                          // T = X Y
-    for (int l = 0; l < k; ++l) {
-      const double p0 = wget(x0, x1, (v0ok ? r0 : 0) * k + l);
-      const double q0 = wget(y0, y1, l * k + (v0ok ? c0 : 0));
-      const double p1 = wget(x0, x1, (v1ok ? r1 : 0) * k + l);
-      const double q1 = wget(y0, y1, l * k + (v1ok ? c1 : 0));
-      t0 += p0 * q0;
-      t1 += p1 * q1;
-    }
-    const double n0 = 1.5 * x0 - 0.5 * t0, n1 = 1.5 * x1 - 0.5 * t1;
-    const bool moved = (v0ok && fabs(n0 - x0) > 1e-14 * k) || (v1ok && fabs(n1 - x1) > 1e-14 * k);
-    x0 = v0ok ? n0 : 0.0;
-    x1 = v1ok ? n1 : 0.0;
-    if (!__any_sync(0xffffffffu, moved)) { ++it; break; }
-  }
+  float f0 = (float)x0, f1 = (float)x1;
+  int it = ns_sweeps<TWO, float>(f0, f1, k, v0ok, v1ok, r0, c0, r1, c1, 1e-4f, 60);
+  x0 = f0;
+  x1 = f1;
+  it += ns_sweeps<TWO, double>(x0, x1, k, v0ok, v1ok, r0, c0, r1, c1, 1e-14 * k, 100);
   if (v0ok) X[e0] = x0;
   if (v1ok) X[e1] = x1;
   // tr(X A) = sum_{a,b} X[a][b] A[b][a]
@@ -415,6 +440,11 @@ __device__ double polar_ns_small(const double* A, double* X, int k, int* iters) 
   tr = warp_sum(tr);
   if (lane == 0) *iters = it;
   return tr;
+}
+
+__device__ double polar_ns_small(const double* A, double* X, int k, int* iters) {
+  return k * k <= 32 ? polar_ns_small_t<false>(A, X, k, iters)
+                     : polar_ns_small_t<true>(A, X, k, iters);
 }
 
 __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int k, int* flag,
