@@ -42,6 +42,8 @@ struct DiscParams {
   double* part_arg;     // 2 x grid x 3  (value, index, label)
   double* Rg;           // k x k f64 rotation (row l, col j), written by CTA 0
   double* red_m;        // k x k + k: two-stage reduction target (k > 8)
+  unsigned long long* gfx;  // 3 x (k x k + k) fixed-point totals (k <= 8), rotating
+  double fx_scale;          // 2^s with n * 2^s < 2^62
   double* info;         // output info
   unsigned long long* tdbg;  // optional phase timing (ANCKA_DISC_TIMING)
   int groups;           // accumulator groups per CTA
@@ -94,7 +96,8 @@ __device__ __forceinline__ Rows my_rows(int64_t n) {
 // Phase A.  score=true: labels + margins from R; false: keep labels.
 template <int KMAX>
 __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, float* tile,
-                                 int* tlab, double* acc, int* cnt, bool score, int* zeros_out) {
+                                 int* tlab, double* acc, int* cnt, bool score, int* zeros_out,
+                                 unsigned long long* gdst = nullptr) {
   const int k = p.k;
   const int G = p.groups;
   for (int e = threadIdx.x; e < G * k * k; e += blockDim.x) acc[e] = 0.0;
@@ -191,17 +194,30 @@ __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, 
     }
     __syncthreads();
   }
-  double* pm = p.part_m + ((size_t)buf * gridDim.x + blockIdx.x) * k * k;
-  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-    double s = 0.0;
-    for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
-    pm[e] = s;
-  }
-  int64_t* pc = p.part_cnt + ((size_t)buf * gridDim.x + blockIdx.x) * k;
-  for (int e = threadIdx.x; e < k; e += blockDim.x) {
-    int s = 0;
-    for (int g = 0; g < G; ++g) s += cnt[g * k + e];
-    pc[e] = s;
+  if (gdst) {   // k <= 8: one fixed-point atomic per entry (integer sums: order free)
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      double s = 0.0;
+      for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
+      atomicAdd(gdst + e, (unsigned long long)(long long)llrint(s * p.fx_scale));
+    }
+    for (int e = threadIdx.x; e < k; e += blockDim.x) {
+      int s = 0;
+      for (int g = 0; g < G; ++g) s += cnt[g * k + e];
+      atomicAdd(gdst + k * k + e, (unsigned long long)s);
+    }
+  } else {
+    double* pm = p.part_m + ((size_t)buf * gridDim.x + blockIdx.x) * k * k;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      double s = 0.0;
+      for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
+      pm[e] = s;
+    }
+    int64_t* pc = p.part_cnt + ((size_t)buf * gridDim.x + blockIdx.x) * k;
+    for (int e = threadIdx.x; e < k; e += blockDim.x) {
+      int s = 0;
+      for (int g = 0; g < G; ++g) s += cnt[g * k + e];
+      pc[e] = s;
+    }
   }
   if (zeros_out) {
     __shared__ int zsum;
@@ -297,7 +313,8 @@ __device__ void reduce_stage2(const DiscParams& p, double* M, long long* sizes) 
 }
 
 __device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
-                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid);
+                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid,
+                           int ri);
 
 // Every CTA: reduce (value, index, label) partials of buffer `buf`.
 // want_max: first max (larger value, then smaller index), else first min.
@@ -581,9 +598,20 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
 }
 
 __device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
-                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid) {
+                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid,
+                           int ri) {
   if (p.k <= 8) {
-    reduce_partials(p, buf, M, sizes, rsum, rcnt);
+    // totals accumulated by the atomics of phase A (buffer ri % 3); CTA 0
+    // clears buffer (ri + 2) % 3, whose next use is two barriers away
+    const int k = p.k, ne = k * k + k;
+    const unsigned long long* src = p.gfx + (size_t)(ri % 3) * ne;
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x)
+      M[e] = (double)(long long)__ldcg(src + e) / p.fx_scale;
+    for (int e = threadIdx.x; e < k; e += blockDim.x) sizes[e] = (long long)__ldcg(src + k * k + e);
+    if (blockIdx.x == 0)
+      for (int e = threadIdx.x; e < ne; e += blockDim.x) p.gfx[(size_t)((ri + 2) % 3) * ne + e] = 0ull;
+    __syncthreads();
+    (void)rsum; (void)rcnt;
     return;
   }
   reduce_stage1(p, buf, red);
@@ -642,6 +670,7 @@ discretize_kernel(DiscParams p) {
   const bool cta0 = blockIdx.x == 0;
   const Rows rows = my_rows(p.n);
   int buf = 0;                 // partial-buffer parity (advances per barrier)
+  int ri = 0;                  // accumulate/reduce counter (rotating fixed-point totals)
   double final_obj[2] = {0.0, 0.0};
   int final_rounds[2] = {0, 0};
   double final_conv[2] = {0.0, 0.0};
@@ -707,7 +736,8 @@ discretize_kernel(DiscParams p) {
     for (int it = 0; it < p.max_iter; ++it) {
       TSTAMP(0);
       phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, true,
-                             (run == 0 && it == 0) ? &s_zero : nullptr);
+                             (run == 0 && it == 0) ? &s_zero : nullptr,
+                             p.k <= 8 ? p.gfx + (size_t)(ri % 3) * (kk + k) : nullptr);
       if (run == 0 && it == 0 && threadIdx.x == 0)   // fold the zero-row count into the
         p.part_cnt[((size_t)(buf ^ 1) * nb + blockIdx.x) * k] = s_zero;  // idle buffer
       TSTAMP(6);
@@ -718,7 +748,8 @@ discretize_kernel(DiscParams p) {
         for (int b = 0; b < nb; ++b) z += p.part_cnt[((size_t)(buf ^ 1) * nb + b) * k];
         p.info[5] = (double)z;
       }
-      reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid);
+      reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid, ri);
+      ++ri;
       TSTAMP(2);
       buf ^= 1;
       int nempty = 0;
@@ -753,9 +784,11 @@ discretize_kernel(DiscParams p) {
           }
           __syncthreads();
         }
-        phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, false, nullptr);
+        phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, false, nullptr,
+                               p.k <= 8 ? p.gfx + (size_t)(ri % 3) * (kk + k) : nullptr);
         grid.sync();
-        reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid);
+        reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid, ri);
+        ++ri;
         buf ^= 1;
       }
       // Y~ = Y / size, polar factor and objective
@@ -851,6 +884,7 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   cv.take<double>((size_t)2 * grid * 3);
   cv.take<double>((size_t)k * k);
   cv.take<double>((size_t)k * k + k);
+  cv.take<unsigned long long>((size_t)3 * (k * k + k));
   return cv.used;
 }
 
@@ -896,12 +930,19 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.part_arg = cv.take<double>((size_t)2 * grid * 3);
   p.Rg = cv.take<double>((size_t)k * k);
   p.red_m = cv.take<double>((size_t)k * k + k);
+  p.gfx = cv.take<unsigned long long>((size_t)3 * (k * k + k));
+  {
+    int bits = 1;
+    while ((1ll << bits) <= n) ++bits;
+    p.fx_scale = std::ldexp(1.0, 61 - bits);
+  }
   p.info = info;
   p.tdbg = getenv("ANCKA_DISC_TIMING") ? (unsigned long long*)(info + 8 + 2 * (size_t)max_iter + 2 * (size_t)k * k) : nullptr;
   p.groups = disc_groups(k);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize: workspace too small");
   auto st = as_stream(stream);
   ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 8 : 0)), st));
+  ANCKA_CUDA(cudaMemsetAsync(p.gfx, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
   if (k <= 8) return launch_disc<8>(p, st);
   if (k <= 16) return launch_disc<16>(p, st);
   if (k <= 32) return launch_disc<32>(p, st);
