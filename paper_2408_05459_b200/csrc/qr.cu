@@ -9,8 +9,13 @@
 // (CGS2), used for the parity-critical first step whose block is rank
 // deficient by construction: it reports |R_jj| so the host
 // applies the reference's rank test (engine.py:141-142) exactly.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "spmm.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace ancka {
 
@@ -399,6 +404,77 @@ __global__ void cgs_update_kernel(double* __restrict__ Z, int64_t n, int64_t ld,
   }
 }
 
+// One cooperative kernel for the whole f64 CGS2 (the step-1 QR): CTA b owns
+// rows [b*rpb, (b+1)*rpb).  Per column: two projection passes and the norm,
+// each a CTA-local partial sum -> grid barrier -> fixed-order reduction of
+// the partials by every CTA (identical, deterministic) -> local update.
+// Three barriers per column instead of nine kernel launches.
+__global__ void __launch_bounds__(256)
+cgs2_fused_kernel(double* __restrict__ Z, int64_t n, int64_t ld, int c,
+                  double* __restrict__ partial, double* __restrict__ rdiag) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
+  __shared__ double proj[kMaxC];
+  const int nb = gridDim.x;
+  const int64_t rpb = ceil_div(n, (int64_t)nb);
+  const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = lmin(n, r0 + rpb);
+  int buf = 0;
+  for (int j = 0; j < c; ++j) {
+    for (int pass = 0; pass < 2 && j > 0; ++pass) {
+      double* part = partial + (size_t)buf * nb * kMaxC;
+      for (int l = 0; l < j; ++l) {          // partial dots <Q[:,l], Z[:,j]> of own rows
+        double s = 0.0;
+        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+          s = fma(Z[i * ld + l], Z[i * ld + j], s);
+        s = block_sum(s, red);
+        if (threadIdx.x == 0) part[(size_t)blockIdx.x * kMaxC + l] = s;
+      }
+      grid.sync();
+      for (int l = threadIdx.x; l < j; l += blockDim.x) {
+        double s0 = 0.0, s1 = 0.0;
+        int b = 0;
+        for (; b + 1 < nb; b += 2) {
+          s0 += __ldcg(part + (size_t)b * kMaxC + l);
+          s1 += __ldcg(part + (size_t)(b + 1) * kMaxC + l);
+        }
+        if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC + l);
+        proj[l] = s0 + s1;
+      }
+      __syncthreads();
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+        double v = Z[i * ld + j];
+        for (int l = 0; l < j; ++l) v -= Z[i * ld + l] * proj[l];
+        Z[i * ld + j] = v;
+      }
+      buf ^= 1;
+      __syncthreads();
+    }
+    double* part = partial + (size_t)buf * nb * kMaxC;
+    double s = 0.0;
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) s = fma(Z[i * ld + j], Z[i * ld + j], s);
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) part[(size_t)blockIdx.x * kMaxC] = s;
+    grid.sync();
+    if (threadIdx.x == 0) {
+      double s0 = 0.0, s1 = 0.0;
+      int b = 0;
+      for (; b + 1 < nb; b += 2) {
+        s0 += __ldcg(part + (size_t)b * kMaxC);
+        s1 += __ldcg(part + (size_t)(b + 1) * kMaxC);
+      }
+      if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC);
+      proj[0] = sqrt(s0 + s1);
+    }
+    __syncthreads();
+    const double nrm = proj[0];
+    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
+      Z[i * ld + j] = nrm > 0 ? Z[i * ld + j] / nrm : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) rdiag[j] = nrm;
+    buf ^= 1;
+    __syncthreads();
+  }
+}
+
 }  // namespace ancka
 
 using namespace ancka;
@@ -428,6 +504,7 @@ extern "C" size_t ancka_qr_f64_workspace_size(int64_t n, int32_t c) {
   Carver cv(nullptr, 0);
   cv.take<double>((size_t)kQrBlocks * (c + 1));
   cv.take<double>(c + 1);
+  cv.take<double>((size_t)2 * 2 * kNumSMs * kMaxC);   // fused CGS2 partials
   return cv.used;
 }
 
@@ -436,8 +513,22 @@ extern "C" int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double*
   Carver cv(workspace, workspace_bytes);
   double* partial = cv.take<double>((size_t)kQrBlocks * (c + 1));
   double* proj = cv.take<double>(c + 1);
+  double* fpart = cv.take<double>((size_t)2 * 2 * kNumSMs * kMaxC);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "qr_f64: workspace too small");
   auto st = as_stream(stream);
+  if (c <= kMaxC && !getenv("ANCKA_QR_UNFUSED")) {    // one cooperative launch
+    int per_sm = 0, dev = 0, sms = 0;
+    ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_fused_kernel, 256, 0));
+    ANCKA_CUDA(cudaGetDevice(&dev));
+    ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int grid = (int)std::min<int64_t>(ceil_div(n, 256), std::min(per_sm, 2) * (int64_t)sms);
+    grid = std::max(grid, 1);
+    void* args[] = {&Z, &n, &ld, &c, &fpart, &rdiag};
+    note_launch();
+    ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)cgs2_fused_kernel, dim3(grid), dim3(256), args,
+                                           0, st));
+    return ANCKA_OK;
+  }
   const int ub = 256;
   const int ug = (int)std::min<int64_t>(ceil_div(n, ub), 4 * kNumSMs);
   for (int j = 0; j < c; ++j) {
