@@ -18,6 +18,7 @@ replays it with the exact f64 step.
 from __future__ import annotations
 
 import time
+import os
 import warnings
 from dataclasses import dataclass, field
 
@@ -537,7 +538,8 @@ class _Loop:
         self.op, self.c, self.k, self.tau = op, c, k, tau
         n = op.n
         # narrow blocks use the fused cooperative kernel, which wants ld == 8
-        self.fused = fused and c <= 8 and op.kind is not NetworkKind.MULTIPLEX
+        self.fused = (fused and c <= 8 and op.kind is not NetworkKind.MULTIPLEX
+                      and not os.environ.get("ANCKA_ORTH_UNFUSED"))
         self.ld = 8 if self.fused else ld_for(c, torch.float32)
         d = dev()
         self.Q = [torch.zeros((n, self.ld), dtype=torch.float32, device=d) for _ in range(2)]
