@@ -460,15 +460,21 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
   ANCKA_CUDA(cudaMemsetAsync(rb, 0, sizeof(int) * (q_end - q_begin), st));
   p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
   if (fp8) {
-    if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }
+    if (K <= 10) { ANCKA_TRY((launch_tc<true, 10>(ma, mb, p, L, st))); }
+    else if (K <= 12) { ANCKA_TRY((launch_tc<true, 12>(ma, mb, p, L, st))); }
+    else if (K <= 16) { ANCKA_TRY((launch_tc<true, 16>(ma, mb, p, L, st))); }
     else { ANCKA_TRY((launch_tc<true, 32>(ma, mb, p, L, st))); }
   } else {
-    if (K <= 16) { ANCKA_TRY((launch_tc<false, 16>(ma, mb, p, L, st))); }
+    if (K <= 10) { ANCKA_TRY((launch_tc<false, 10>(ma, mb, p, L, st))); }
+    else if (K <= 12) { ANCKA_TRY((launch_tc<false, 12>(ma, mb, p, L, st))); }
+    else if (K <= 16) { ANCKA_TRY((launch_tc<false, 16>(ma, mb, p, L, st))); }
     else { ANCKA_TRY((launch_tc<false, 32>(ma, mb, p, L, st))); }
   }
   const int64_t nq = q_end - q_begin;
   const int mg = (int)std::min<int64_t>(ceil_div(nq, 128), 8 * kNumSMs);
-  if (K <= 16)
+  if (K <= 10)
+    knn_tc_merge_kernel<10><<<mg, 128, 0, st>>>(part, q_begin, nq, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
+  else if (K <= 16)
     knn_tc_merge_kernel<16><<<mg, 128, 0, st>>>(part, q_begin, nq, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
   else
     knn_tc_merge_kernel<32><<<mg, 128, 0, st>>>(part, q_begin, nq, L.nseg * (tc::EPI_WARPS / 4), K, an, isq, ids, scores);
