@@ -483,11 +483,6 @@ class CudaBackend:
         return t.cpu().numpy()
 
     # --- kernels
-    def knn_rows(self, X, K, q0, q1):
-        from .knn import knn_search_exact_device
-        ids, sc = knn_search_exact_device(X, K, rows=(q0, q1))
-        return ids, sc
-
     # --- KNN key ring: shards are ("csr", indptr, indices, data, d) or ("dense", X)
     def x_shard(self, X, r0, r1):
         torch = self.torch

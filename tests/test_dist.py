@@ -65,12 +65,6 @@ class NumpyBackend:
             dist.all_reduce(t)
         return t.numpy()
 
-    @staticmethod
-    def knn_rows(X, K, q0, q1):
-        from oracle import ancka_cpu as oc
-        ids, sc = oc.knn_exact(X, K)        # the checker; rows sliced per rank
-        return ids[q0:q1], sc[q0:q1]
-
     # --- KNN key ring over gloo
     @staticmethod
     def x_shard(X, r0, r1):
