@@ -405,68 +405,87 @@ __global__ void cgs_update_kernel(double* __restrict__ Z, int64_t n, int64_t ld,
 }
 
 // One cooperative kernel for the whole f64 CGS2 (the step-1 QR): CTA b owns
-// rows [b*rpb, (b+1)*rpb).  Per column: two projection passes and the norm,
-// each a CTA-local partial sum -> grid barrier -> fixed-order reduction of
+// rows [b*rpb, (b+1)*rpb).  Per column j: two projection passes and the
+// norm, each a CTA-local partial -> grid barrier -> fixed-order reduction of
 // the partials by every CTA (identical, deterministic) -> local update.
-// Three barriers per column instead of nine kernel launches.
-__global__ void __launch_bounds__(256)
+// Rows are read warp-wide (lane = column), so every pass streams the
+// row-major block coalesced.
+constexpr int kCgsWarps = 8;
+__global__ void __launch_bounds__(32 * kCgsWarps)
 cgs2_fused_kernel(double* __restrict__ Z, int64_t n, int64_t ld, int c,
                   double* __restrict__ partial, double* __restrict__ rdiag) {
   cg::grid_group grid = cg::this_grid();
-  __shared__ double red[32];
+  __shared__ double wpart[kCgsWarps][kMaxC];
   __shared__ double proj[kMaxC];
   const int nb = gridDim.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t rpb = ceil_div(n, (int64_t)nb);
   const int64_t r0 = (int64_t)blockIdx.x * rpb, r1 = lmin(n, r0 + rpb);
   int buf = 0;
+  auto reduce_cols = [&](int cnt, double* part) {   // warp partials -> CTA partial[blk]
+    __syncthreads();
+    for (int l = threadIdx.x; l < cnt; l += blockDim.x) {
+      double s = 0.0;
+      for (int ww = 0; ww < kCgsWarps; ++ww) s += wpart[ww][l];
+      part[(size_t)blockIdx.x * kMaxC + l] = s;
+    }
+  };
+  auto total_cols = [&](int cnt, const double* part) {   // all CTAs' partials -> proj
+    for (int l = threadIdx.x; l < cnt; l += blockDim.x) {
+      double s0 = 0.0, s1 = 0.0;
+      int b = 0;
+      for (; b + 1 < nb; b += 2) {
+        s0 += __ldcg(part + (size_t)b * kMaxC + l);
+        s1 += __ldcg(part + (size_t)(b + 1) * kMaxC + l);
+      }
+      if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC + l);
+      proj[l] = s0 + s1;
+    }
+    __syncthreads();
+  };
   for (int j = 0; j < c; ++j) {
     for (int pass = 0; pass < 2 && j > 0; ++pass) {
       double* part = partial + (size_t)buf * nb * kMaxC;
-      for (int l = 0; l < j; ++l) {          // partial dots <Q[:,l], Z[:,j]> of own rows
-        double s = 0.0;
-        for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
-          s = fma(Z[i * ld + l], Z[i * ld + j], s);
-        s = block_sum(s, red);
-        if (threadIdx.x == 0) part[(size_t)blockIdx.x * kMaxC + l] = s;
-      }
-      grid.sync();
-      for (int l = threadIdx.x; l < j; l += blockDim.x) {
-        double s0 = 0.0, s1 = 0.0;
-        int b = 0;
-        for (; b + 1 < nb; b += 2) {
-          s0 += __ldcg(part + (size_t)b * kMaxC + l);
-          s1 += __ldcg(part + (size_t)(b + 1) * kMaxC + l);
+      double acc[kMaxC / 32];
+#pragma unroll
+      for (int t = 0; t < kMaxC / 32; ++t) acc[t] = 0.0;
+      for (int64_t i = r0 + w; i < r1; i += kCgsWarps) {     // <Q[:,l], Z[:,j]>, l < j
+        const double* row = Z + i * ld;
+        const double zj = row[j];
+#pragma unroll
+        for (int t = 0; t < kMaxC / 32; ++t) {
+          const int l = lane + 32 * t;
+          if (l < j) acc[t] = fma(row[l], zj, acc[t]);
         }
-        if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC + l);
-        proj[l] = s0 + s1;
       }
-      __syncthreads();
-      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-        double v = Z[i * ld + j];
-        for (int l = 0; l < j; ++l) v -= Z[i * ld + l] * proj[l];
-        Z[i * ld + j] = v;
+#pragma unroll
+      for (int t = 0; t < kMaxC / 32; ++t)
+        if (lane + 32 * t < j) wpart[w][lane + 32 * t] = acc[t];
+      reduce_cols(j, part);
+      grid.sync();
+      total_cols(j, part);
+      for (int64_t i = r0 + w; i < r1; i += kCgsWarps) {     // Z[:,j] -= Q[:, :j] proj
+        double* row = Z + i * ld;
+        double s = 0.0;
+        for (int l = lane; l < j; l += 32) s += row[l] * proj[l];
+        s = warp_sum(s);
+        if (lane == 0) row[j] -= s;
       }
       buf ^= 1;
       __syncthreads();
     }
     double* part = partial + (size_t)buf * nb * kMaxC;
     double s = 0.0;
-    for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) s = fma(Z[i * ld + j], Z[i * ld + j], s);
-    s = block_sum(s, red);
-    if (threadIdx.x == 0) part[(size_t)blockIdx.x * kMaxC] = s;
-    grid.sync();
-    if (threadIdx.x == 0) {
-      double s0 = 0.0, s1 = 0.0;
-      int b = 0;
-      for (; b + 1 < nb; b += 2) {
-        s0 += __ldcg(part + (size_t)b * kMaxC);
-        s1 += __ldcg(part + (size_t)(b + 1) * kMaxC);
-      }
-      if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC);
-      proj[0] = sqrt(s0 + s1);
+    for (int64_t i = r0 + w * 32 + lane; i < r1; i += 32 * kCgsWarps) {
+      const double v = Z[i * ld + j];
+      s = fma(v, v, s);
     }
-    __syncthreads();
-    const double nrm = proj[0];
+    s = warp_sum(s);
+    if (lane == 0) wpart[w][0] = s;
+    reduce_cols(1, part);
+    grid.sync();
+    total_cols(1, part);
+    const double nrm = sqrt(proj[0]);
     for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x)
       Z[i * ld + j] = nrm > 0 ? Z[i * ld + j] / nrm : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0) rdiag[j] = nrm;
@@ -518,15 +537,16 @@ extern "C" int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double*
   auto st = as_stream(stream);
   if (c <= kMaxC && !getenv("ANCKA_QR_UNFUSED")) {    // one cooperative launch
     int per_sm = 0, dev = 0, sms = 0;
-    ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_fused_kernel, 256, 0));
+    ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cgs2_fused_kernel,
+                                                             32 * kCgsWarps, 0));
     ANCKA_CUDA(cudaGetDevice(&dev));
     ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     int grid = (int)std::min<int64_t>(ceil_div(n, 256), std::min(per_sm, 2) * (int64_t)sms);
     grid = std::max(grid, 1);
     void* args[] = {&Z, &n, &ld, &c, &fpart, &rdiag};
     note_launch();
-    ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)cgs2_fused_kernel, dim3(grid), dim3(256), args,
-                                           0, st));
+    ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)cgs2_fused_kernel, dim3(grid),
+                                           dim3(32 * kCgsWarps), args, 0, st));
     return ANCKA_OK;
   }
   const int ub = 256;

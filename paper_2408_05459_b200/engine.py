@@ -287,15 +287,9 @@ class _WideDiscretizer:
         self.shift = 61 - bits                  # |sum| <= n: no int64 overflow
         self.scale = float(2.0 ** self.shift)
 
-    def _sizes(self, lab):
-        _lib.call("ancka_cluster_sizes", lab.data_ptr(), self.n, self.k, self.cnt.data_ptr(),
-                  _lib.stream())
-        return self.cnt
-
-    def _reseed(self, lab):
+    def _reseed(self, lab, sizes):
         """_reseed_empty_columns (engine.py:162-180) with device tensor ops."""
         k = self.k
-        sizes = self._sizes(lab).cpu().numpy()
         empties = np.flatnonzero(sizes == 0)
         if not empties.size or k < 2:
             return
@@ -310,16 +304,29 @@ class _WideDiscretizer:
     def run(self, R0: np.ndarray, lab, max_iter: int, tol: float):
         n, k = self.n, self.k
         objs, conv, R = [], False, R0
+        Rh = torch.empty((k, self.ldt), dtype=torch.float32, pin_memory=True)
+        out = torch.empty(k * k + k, dtype=torch.int64, pin_memory=True)
+        SC = torch.empty(k * k + k, dtype=torch.int64, device=self.S.device)
+
+        def accumulate():
+            # one read-back per round: the k x k fixed-point sums and the sizes
+            _lib.call("ancka_disc_accumulate", self.qt.data_ptr(), self.ldt, n, k, lab.data_ptr(),
+                      self.scale, SC.data_ptr(), SC[k * k:].data_ptr(), _lib.stream())
+            out.copy_(SC)
+            return out.numpy()
+
         for _ in range(max_iter):
             R_used = R                            # rotation behind this round's scores
-            self.R[:, :k] = torch.from_numpy(R.astype(np.float32)).to(self.R.device)
+            Rh[:, :k] = torch.from_numpy(R.astype(np.float32))
+            self.R.copy_(Rh, non_blocking=True)
             _lib.call("ancka_disc_score", self.qt.data_ptr(), self.ldt, n, k, self.R.data_ptr(),
                       self.ldt, lab.data_ptr(), self.margin.data_ptr(), _lib.stream())
-            self._reseed(lab)
-            _lib.call("ancka_disc_accumulate", self.qt.data_ptr(), self.ldt, n, k, lab.data_ptr(),
-                      self.scale, self.S.data_ptr(), self.cnt.data_ptr(), _lib.stream())
-            S = self.S.cpu().numpy().reshape(k, k).astype(np.float64) / self.scale
-            sizes = self.cnt.cpu().numpy().astype(np.float64)
+            h = accumulate()
+            if (h[k * k:] == 0).any() and k >= 2:  # reseed empties, then recount
+                self._reseed(lab, h[k * k:].copy())
+                h = accumulate()
+            S = h[:k * k].reshape(k, k).astype(np.float64) / self.scale
+            sizes = h[k * k:].astype(np.float64)
             M = np.divide(S, sizes[:, None], out=np.zeros_like(S), where=sizes[:, None] > 0)
             try:
                 u, omega, vh = np.linalg.svd(M)     # Y~^T Q~ (engine.py:199-200)
