@@ -209,14 +209,17 @@ def canonical_knn(X, K):
     return ids
 
 
-@pytest.mark.parametrize("shape,n,words", [("cora", 1500, 18), ("dblp", 2100, 20), ("citeseer", 700, 32)])
-def test_tensor_core_knn_exact(shape, n, words):
+@pytest.mark.parametrize("shape,n,words,K", [("cora", 1500, 18, 10), ("dblp", 2100, 20, 10),
+                                             ("citeseer", 700, 32, 10), ("cora", 900, 18, 12),
+                                             ("dblp", 800, 20, 16), ("cora", 600, 18, 24)])
+def test_tensor_core_knn_exact(shape, n, words, K):
+    """Every list-slot instantiation (K <= 10, 12, 16, 32) of the integer
+    tcgen05 kernel against exact rational top-K."""
     from paper_2408_05459_b200 import synth
     from paper_2408_05459_b200.knn import integer_exact, knn_search_exact_device
     inst = synth.make(shape, seed=3, n=n, words=words)
     X = inst.X
     assert integer_exact(X) == 2
-    K = 10
     ids_fp8, sc_fp8 = knn_search_exact_device(X, K, integer=2)
     ids_bf16, sc_bf16 = knn_search_exact_device(X, K, integer=1)
     ref = canonical_knn(X, K)
