@@ -209,6 +209,21 @@ orth_fused_kernel(OfParams P) {
   __shared__ double s_stat[2];
 
   unsigned long long t_prev = 0;
+  const int lane0 = threadIdx.x & 31;
+  const int sub0 = lane0 & (kGW - 1);
+  const int64_t goct0 = gtid / kGW, noct0 = gsz / kGW;
+  if (hyper) {     // T = P_E Q0 for the first step
+    const float* Eval = static_cast<const float*>(op.p_e.values);
+    const int64_t m = op.m;
+    for (int64_t e = goct0; e < ((m + noct0 - 1) / noct0) * noct0; e += noct0) {
+      float acc[kC] = {};
+      if (e < m) seg8_strided(op.p_e.colidx, Eval, P.Q[0], op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
+                              sub0, kGW, acc);
+      group_sum(acc, kGW);
+      if (e < m && sub0 == 0) f8_store(P.T + e * kC, acc);
+    }
+    grid.sync();
+  }
   for (int step = 0; step < P.steps; ++step) {
     OF_STAMP(-1);
     const float* Qp = P.Q[step & 1];
@@ -219,22 +234,8 @@ orth_fused_kernel(OfParams P) {
     const int sub = lane & (kGW - 1);
     const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
     const int64_t goct = gtid / kGW, noct = gsz / kGW;
-    // ---- P1: T = P_E Q (hypergraph)
-    if (hyper) {
-      const float* Eval = static_cast<const float*>(op.p_e.values);
-      const int64_t m = op.m;
-      for (int64_t e0 = goct; e0 < ((m + noct - 1) / noct) * noct; e0 += noct) {
-        const int64_t e = e0;
-        float acc[kC] = {};
-        if (e < m) seg8_strided(op.p_e.colidx, Eval, Qp, op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
-                                sub, kGW, acc);
-        group_sum(acc, kGW);
-        if (e < m && sub == 0) f8_store(P.T + e * kC, acc);
-      }
-      OF_STAMP(0);
-      grid.sync();
-      OF_STAMP(1);
-    }
+    // T = P_E Q of this step was produced at the end of the previous step
+    // (or before the loop), already multiplied by R^-1
     const float* Ssrc = hyper ? P.T : Qp;
     unsigned long long p2_t0 = 0;
     if (P.tdbg && threadIdx.x == 0) p2_t0 = of_timer();
@@ -370,6 +371,30 @@ orth_fused_kernel(OfParams P) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       P.stats[1] = fmin(P.stats[1], s_stat[0]);
       P.stats[2] += s_stat[1];
+    }
+    // ---- next step's T = P_E Q_{t+1} = (P_E Z) R^-1: Z is complete (barrier
+    // above) and R^-1 is known, so the hyperedge stage needs no barrier of
+    // its own; every group applies R^-1 to the hyperedges it produced
+    if (hyper) {
+      const float* Eval = static_cast<const float*>(op.p_e.values);
+      const int64_t m = op.m;
+      for (int64_t e = goct; e < ((m + noct - 1) / noct) * noct; e += noct) {
+        float acc[kC] = {};
+        if (e < m) seg8_strided(op.p_e.colidx, Eval, P.Z, op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
+                                sub, kGW, acc);
+        group_sum(acc, kGW);
+        if (e < m && sub == 0) {
+          float tv[kC];
+#pragma unroll
+          for (int b2 = 0; b2 < kC; ++b2) {
+            float v = 0.f;
+#pragma unroll
+            for (int a = 0; a <= b2; ++a) v = fmaf(acc[a], Rinv[a * kC + b2], v);
+            tv[b2] = v;
+          }
+          f8_store(P.T + e * kC, tv);
+        }
+      }
     }
     // ---- P5: Q = Z R^-1 and ||Q - Q_prev||^2
     double dq = 0.0;
