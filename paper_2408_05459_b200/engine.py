@@ -686,9 +686,12 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             if (sizes0 == 0).any():
                 raise NetworkError(f"empty cluster(s) {np.flatnonzero(sizes0 == 0).tolist()}: "
                                    "normalization undefined")
-            best_mhc = float(_MhcRunner(op, k, _lib.F64)(labels0).item())
+            # phi(Y0) stays on the device; it rides along with the first sample's
+            # read-back (no synchronisation here)
+            mhc0_dev = _MhcRunner(op, k, _lib.F64)(labels0)
+        best_mhc = None
         best_labels = labels0.clone()
-        history = [(0, best_mhc)]
+        history = [(0, None)]
         loop = _Loop(op, c, k, params.tau, use_graphs, fused)
         mhc = _MhcRunner(op, k, _lib.F32)
         lab_t = torch.empty(n, dtype=torch.int32, device=dev())
@@ -711,12 +714,17 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             else:
                 readback[1] = loop.stats[0]
                 readback[2] = loop.stats[2]
+            readback[3:4].copy_(mhc0_dev)
             host_info.copy_(info[:8], non_blocking=True)
             host_rb.copy_(readback, non_blocking=True)
             rb_ready.record()
 
         def sample_collect():
+            nonlocal best_mhc
             rb_ready.synchronize()
+            if best_mhc is None:                    # phi(Y0) (engine.py:373)
+                best_mhc = float(host_rb[3])
+                history[0] = (0, best_mhc)
             return host_info.numpy().copy(), host_rb.numpy()[:3].copy()
 
         def sample(t_now, dq_first):
@@ -806,6 +814,9 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             if spec is not None:
                 undo_spec()
         timer.flush()
+        if best_mhc is None:                        # no sample was taken
+            best_mhc = float(mhc0_dev.item())
+            history[0] = (0, best_mhc)
         caught = [str(w.message) for w in wrec]
     best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)
     state = EngineState(loop.q, best_y, best_mhc, history, t, c=c)
