@@ -430,46 +430,44 @@ cgs2_fused_kernel(double* __restrict__ Z, int64_t n, int64_t ld, int c,
       part[(size_t)blockIdx.x * kMaxC + l] = s;
     }
   };
-  auto total_cols = [&](int cnt, const double* part) {   // all CTAs' partials -> proj
-    for (int l = threadIdx.x; l < cnt; l += blockDim.x) {
-      double s0 = 0.0, s1 = 0.0;
-      int b = 0;
-      for (; b + 1 < nb; b += 2) {
-        s0 += __ldcg(part + (size_t)b * kMaxC + l);
-        s1 += __ldcg(part + (size_t)(b + 1) * kMaxC + l);
-      }
-      if (b < nb) s0 += __ldcg(part + (size_t)b * kMaxC + l);
-      proj[l] = s0 + s1;
+  // all CTAs' partials -> proj: per column, the CTA's threads load the
+  // partials in parallel and sum them with the fixed block tree
+  // (deterministic, and no serial chain of L2 loads)
+  auto total_cols = [&](int cnt, const double* part) {
+    __shared__ double tred[32];
+    for (int l = 0; l < cnt; ++l) {
+      double v = 0.0;
+      for (int b = threadIdx.x; b < nb; b += blockDim.x) v += __ldcg(part + (size_t)b * kMaxC + l);
+      v = block_sum(v, tred);
+      if (threadIdx.x == 0) proj[l] = v;
     }
     __syncthreads();
   };
   for (int j = 0; j < c; ++j) {
     for (int pass = 0; pass < 2 && j > 0; ++pass) {
       double* part = partial + (size_t)buf * nb * kMaxC;
-      double acc[kMaxC / 32];
-#pragma unroll
-      for (int t = 0; t < kMaxC / 32; ++t) acc[t] = 0.0;
-      for (int64_t i = r0 + w; i < r1; i += kCgsWarps) {     // <Q[:,l], Z[:,j]>, l < j
-        const double* row = Z + i * ld;
-        const double zj = row[j];
-#pragma unroll
-        for (int t = 0; t < kMaxC / 32; ++t) {
-          const int l = lane + 32 * t;
-          if (l < j) acc[t] = fma(row[l], zj, acc[t]);
+      // thread per row (independent loads in flight across the CTA); the
+      // j products of a 32-row batch are summed across the warp per column
+      for (int l = threadIdx.x; l < kCgsWarps * kMaxC; l += blockDim.x) (&wpart[0][0])[l] = 0.0;
+      __syncthreads();
+      for (int64_t i0 = r0 + (int64_t)w * 32; i0 < r1; i0 += 32 * kCgsWarps) {
+        const int64_t i = i0 + lane;
+        const bool ok = i < r1;
+        const double zj = ok ? Z[i * ld + j] : 0.0;
+        for (int l = 0; l < j; ++l) {
+          double v = ok ? Z[i * ld + l] * zj : 0.0;
+          v = warp_sum(v);
+          if (lane == 0) wpart[w][l] += v;
         }
       }
-#pragma unroll
-      for (int t = 0; t < kMaxC / 32; ++t)
-        if (lane + 32 * t < j) wpart[w][lane + 32 * t] = acc[t];
       reduce_cols(j, part);
       grid.sync();
       total_cols(j, part);
-      for (int64_t i = r0 + w; i < r1; i += kCgsWarps) {     // Z[:,j] -= Q[:, :j] proj
+      for (int64_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {   // Z[:,j] -= Q[:, :j] proj
         double* row = Z + i * ld;
-        double s = 0.0;
-        for (int l = lane; l < j; l += 32) s += row[l] * proj[l];
-        s = warp_sum(s);
-        if (lane == 0) row[j] -= s;
+        double v = row[j];
+        for (int l = 0; l < j; ++l) v -= row[l] * proj[l];
+        row[j] = v;
       }
       buf ^= 1;
       __syncthreads();
