@@ -796,7 +796,8 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                             if spec is not None:
                                 undo_spec()
                             break
-                    timer.flush()
+                    # (span events are resolved once at the end: resolving them here
+                    # would wait for the speculative block and idle the device)
                 if t_done >= params.t_a:
                     t = t_done
                     break

@@ -27,11 +27,12 @@ with profile(activities=[ProfilerActivity.CUDA]) as prof:
 ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
 ev.sort(key=lambda e: e.time_range.start)
 t0, t1 = ev[0].time_range.start, max(e.time_range.end for e in ev)
-busy, last_end, gaps = 0.0, t0, []
+busy, last_end, gaps, prev = 0.0, t0, [], "-"
 for e in ev:
     s, f = e.time_range.start, e.time_range.end
     if s > last_end:
-        gaps.append((s - last_end, e.name[:70]))
+        gaps.append((s - last_end, prev[:45] + "  ->  " + e.name[:45]))
+    prev = e.name
     busy += max(0, f - max(s, last_end))
     last_end = max(last_end, f)
 print(f"span {(t1 - t0) / 1e3:.2f} ms  busy {busy / 1e3:.2f} ms  idle {(t1 - t0 - busy) / 1e3:.2f} ms  events {len(ev)}")
