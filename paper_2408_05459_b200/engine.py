@@ -113,6 +113,67 @@ class _PhaseTimer:
         self._open.clear()
 
 
+class _LazyTimings(dict):
+    """ClusterResult.timings_ms: a plain dict once read.  The CUDA-event spans
+    are resolved on first access instead of at the end of the run, so the
+    ~2 event reads per span stay out of the clustering's own wall time."""
+
+    def __init__(self, timer: "_PhaseTimer"):
+        super().__init__()
+        self._timer = timer
+
+    def _resolve(self):
+        if self._timer is not None:
+            t, self._timer = self._timer, None
+            t.flush()
+            for k2, v in t.totals.items():
+                super().__setitem__(k2, super().get(k2, 0.0) + v)
+
+    def __getitem__(self, key):
+        self._resolve()
+        return super().__getitem__(key)
+
+    def __setitem__(self, key, value):
+        self._resolve()
+        super().__setitem__(key, value)
+
+    def __iter__(self):
+        self._resolve()
+        return super().__iter__()
+
+    def __len__(self):
+        self._resolve()
+        return super().__len__()
+
+    def __contains__(self, key):
+        self._resolve()
+        return super().__contains__(key)
+
+    def __repr__(self):
+        self._resolve()
+        return super().__repr__()
+
+    def get(self, key, default=None):
+        self._resolve()
+        return super().get(key, default)
+
+    def items(self):
+        self._resolve()
+        return super().items()
+
+    def keys(self):
+        self._resolve()
+        return super().keys()
+
+    def values(self):
+        self._resolve()
+        return super().values()
+
+    def copy(self):
+        self._resolve()
+        return dict(self)
+
+
 # ----------------------------------------------------------------------------
 def normalize_bcm(y: BcmMatrix) -> np.ndarray:
     """Column-orthonormal membership (engine.py:75-84)."""
@@ -814,14 +875,13 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             error, stop_reason = str(exc), "error"
             if spec is not None:
                 undo_spec()
-        timer.flush()
         if best_mhc is None:                        # no sample was taken
             best_mhc = float(mhc0_dev.item())
             history[0] = (0, best_mhc)
         caught = [str(w.message) for w in wrec]
     best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)
     state = EngineState(loop.q, best_y, best_mhc, history, t, c=c)
-    res = ClusterResult(y=best_y, mhc=best_mhc, iterations=t, timings_ms=dict(timer.totals),
+    res = ClusterResult(y=best_y, mhc=best_mhc, iterations=t, timings_ms=_LazyTimings(timer),
                         state=state, knn=g, operator=op, converged=converged,
                         stop_reason=stop_reason, warnings=caught, error=error)
     # kernels of this library executed by the run (graph captures excluded,
