@@ -6,14 +6,17 @@
 // returning to the host.  Per round:
 //   A  every CTA: row-normalise its rows of Q[:, col0:col0+k], score them
 //      against R (k x k, shared-memory broadcast), first-max argmax and
-//      second-best margin, and accumulate per-cluster column sums of Q~
-//      deterministically (each thread owns one column of one accumulator
-//      group, fixed row order) into a double-buffered per-CTA partial.
+//      second-best margin, and add per-cluster column sums of Q~ into a
+//      rotating global total in 64-bit fixed point (integer atomics: the sum
+//      is independent of order, hence bit-reproducible).  k <= 8: thread per
+//      row with direct loads, per-group f64 sums, one atomic per entry and
+//      CTA; k > 8: rows staged through shared memory as aligned column
+//      windows, per-CTA split 32-bit fixed-point shared atomics.
 //   -- one grid barrier --
-//   B  every CTA, redundantly and identically: fixed-order reduction of the
-//      partials -> M (k x k, f64) and the cluster sizes; Y~ = Y/size (the
-//      reference's 1/size, engine.py:194-198); polar factor R = V U^T of
-//      (Y~^T Q~)^T by Newton-Schulz (the SVD's V U^T, engine.py:199-205) and
+//   B  every CTA, redundantly and identically: read M (k x k) and the
+//      cluster sizes from the totals; Y~ = Y/size (the reference's 1/size,
+//      engine.py:194-198); polar factor R = V U^T of (Y~^T Q~)^T by
+//      Newton-Schulz (the SVD's V U^T, engine.py:199-205) and
 //      sum(sigma) = tr(R Y~^T Q~); obj = n - 2 sum(sigma); |d obj| < tol.
 // Empty clusters (rare) take a slower path with the reference's margin rule
 // (engine.py:162-180).  No float atomics: results are bit-reproducible.
@@ -37,12 +40,10 @@ struct DiscParams {
   int32_t* labels_run0; // saved labels of run 0
   float* margin;        // n, second-best score
   double* proto_acc;    // n, prototype accumulator
-  double* part_m;       // 2 x grid x k x k
   int64_t* part_cnt;    // 2 x grid x k
   double* part_arg;     // 2 x grid x 3  (value, index, label)
   double* Rg;           // k x k f64 rotation (row l, col j), written by CTA 0
-  double* red_m;        // k x k + k: two-stage reduction target (k > 8)
-  unsigned long long* gfx;  // 3 x (k x k + k) fixed-point totals (k <= 8), rotating
+  unsigned long long* gfx;  // 3 x (k x k + k) fixed-point totals, rotating
   double fx_scale;          // 2^s with n * 2^s < 2^62
   double* info;         // output info
   unsigned long long* tdbg;  // optional phase timing (ANCKA_DISC_TIMING)
@@ -93,11 +94,13 @@ __device__ __forceinline__ Rows my_rows(int64_t n) {
   return {r0, lmin(n, r0 + rpb)};
 }
 
-// Phase A.  score=true: labels + margins from R; false: keep labels.
+// Phase A for k <= 8.  score=true: labels + margins from R; false: keep
+// labels.  Thread per row (direct loads), per-group f64 column sums in fixed
+// row order, then one fixed-point atomic per entry into `gdst`.
 template <int KMAX>
-__device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, float* tile,
-                                 int* tlab, double* acc, int* cnt, bool score, int* zeros_out,
-                                 unsigned long long* gdst = nullptr) {
+__device__ void phase_accumulate(const DiscParams& p, const float* sR, float* tile, int* tlab,
+                                 double* acc, int* cnt, bool score, int* zeros_out,
+                                 unsigned long long* gdst) {
   const int k = p.k;
   const int G = p.groups;
   for (int e = threadIdx.x; e < G * k * k; e += blockDim.x) acc[e] = 0.0;
@@ -107,40 +110,10 @@ __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, 
   int zeros = 0;
   for (int64_t t0 = R.r0; t0 < R.r1; t0 += kDiscThreads) {
     const int64_t i = t0 + threadIdx.x;
-    if (KMAX > 8) {
-      // stage the tile's rows with coalesced loads (a warp per row) instead
-      // of k strided loads per thread
-      const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
-      const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
-      for (int r = w; r < tr; r += kDiscThreads / 32) {   // async copies: no register round trip
-        const float* src = p.Q + (t0 + r) * p.ldq + p.col0;
-        for (int l = ln; l < k; l += 32)
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                           (uint32_t)__cvta_generic_to_shared(tile + r * k + l)),
-                       "l"(src + l)
-                       : "memory");
-      }
-      asm volatile("cp.async.wait_all;" ::: "memory");
-      __syncthreads();
-    }
     if (i < R.r1) {
       double nrm;
       float qf[KMAX];
-      if (KMAX > 8) {
-        const float* row = tile + threadIdx.x * k;
-        double s = 0.0;
-#pragma unroll
-        for (int l = 0; l < KMAX; ++l) {
-          const double v = l < k ? (double)row[l] : 0.0;
-          s += v * v;
-        }
-        nrm = sqrt(s);
-        const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
-#pragma unroll
-        for (int l = 0; l < KMAX; ++l) qf[l] = l < k ? (float)((double)row[l] * inv) : 0.f;
-      } else {
-        load_row_f<KMAX>(p, i, qf, nrm);
-      }
+      load_row_f<KMAX>(p, i, qf, nrm);
       if (nrm == 0.0) ++zeros;
       int lab;
       if (score) {
@@ -194,30 +167,16 @@ __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, 
     }
     __syncthreads();
   }
-  if (gdst) {   // k <= 8: one fixed-point atomic per entry (integer sums: order free)
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-      double s = 0.0;
-      for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
-      atomicAdd(gdst + e, (unsigned long long)(long long)llrint(s * p.fx_scale));
-    }
-    for (int e = threadIdx.x; e < k; e += blockDim.x) {
-      int s = 0;
-      for (int g = 0; g < G; ++g) s += cnt[g * k + e];
-      atomicAdd(gdst + k * k + e, (unsigned long long)s);
-    }
-  } else {
-    double* pm = p.part_m + ((size_t)buf * gridDim.x + blockIdx.x) * k * k;
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-      double s = 0.0;
-      for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
-      pm[e] = s;
-    }
-    int64_t* pc = p.part_cnt + ((size_t)buf * gridDim.x + blockIdx.x) * k;
-    for (int e = threadIdx.x; e < k; e += blockDim.x) {
-      int s = 0;
-      for (int g = 0; g < G; ++g) s += cnt[g * k + e];
-      pc[e] = s;
-    }
+  // one fixed-point atomic per entry (integer sums: order free)
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    double s = 0.0;
+    for (int g = 0; g < G; ++g) s += acc[(size_t)g * k * k + e];
+    atomicAdd(gdst + e, (unsigned long long)(long long)llrint(s * p.fx_scale));
+  }
+  for (int e = threadIdx.x; e < k; e += blockDim.x) {
+    int s = 0;
+    for (int g = 0; g < G; ++g) s += cnt[g * k + e];
+    atomicAdd(gdst + k * k + e, (unsigned long long)s);
   }
   if (zeros_out) {
     __shared__ int zsum;
@@ -230,91 +189,221 @@ __device__ void phase_accumulate(const DiscParams& p, int buf, const float* sR, 
   __syncthreads();
 }
 
-// Every CTA: fixed-order reduction of buffer `buf` -> M (smem f64), sizes.
-__device__ void reduce_partials(const DiscParams& p, int buf, double* M, long long* sizes,
-                                double* rsum, long long* rcnt) {
-  const int k = p.k, kk = k * k, nb = gridDim.x, t = threadIdx.x;
-  const double* pm = p.part_m + (size_t)buf * nb * kk;
-  const int64_t* pc = p.part_cnt + (size_t)buf * nb * k;
-  if (kk >= kDiscThreads) {
-    for (int e = t; e < kk; e += blockDim.x) {
-      double s0 = 0.0, s1 = 0.0;
-      int b = 0;
-      for (; b + 1 < nb; b += 2) { s0 += pm[(size_t)b * kk + e]; s1 += pm[(size_t)(b + 1) * kk + e]; }
-      if (b < nb) s0 += pm[(size_t)b * kk + e];
-      M[e] = s0 + s1;
+// kernel instance: k <= 8, else the column window width (>= off + k)
+__host__ __device__ constexpr int disc_kmax(int k, int off) {
+  return k <= 8 ? 8 : off + k <= 16 ? 16 : off + k <= 32 ? 32 : off + k <= 48 ? 48
+                    : off + k <= 64 ? 64 : 68;
+}
+__host__ __device__ constexpr int win_kw(int kmax) { return kmax; }
+__host__ __device__ constexpr int win_sw(int kmax) {
+  return ((win_kw(kmax) / 4) % 2 == 1) ? win_kw(kmax) : win_kw(kmax) + 4;
+}
+// scoring-rotation and row-tile bytes of the k (<= 8 : > 8) layouts
+__host__ __device__ inline size_t disc_rot_bytes(int k, int off) {
+  return k <= 8 ? (size_t)k * kpad4(k) * 4 : (size_t)((k + 3) / 4) * win_kw(disc_kmax(k, off)) * 16;
+}
+__host__ __device__ inline size_t disc_tile_bytes(int k, int off) {
+  return (size_t)kDiscThreads * 4 * (k <= 8 ? k : win_sw(disc_kmax(k, off)));
+}
+
+// ---- k > 8 layout.  A thread owns one row and reads it from a staged tile
+// as float4s: the window of KW = KMAX columns starting at the aligned column
+// c0 = col0 & ~3 holds Q[i, col0:col0+k] at offset off = col0 - c0 (the
+// instance is chosen with off + k <= KMAX).
+// Tile rows are SW floats apart with SW / 4 odd, so the eight 16-byte reads
+// of a quarter warp hit distinct bank groups.  The scoring rotation is
+// stored shifted by `off` in the same window coordinates (zero outside the
+// k valid rows), so no runtime column index reaches a register array.
+template <int KMAX>
+struct Win {
+  static constexpr int KW = win_kw(KMAX);
+  static constexpr int SW = win_sw(KMAX);
+};
+
+// sR4[jb * KW + m] = R[m - off][4 jb .. 4 jb + 3] (zero outside), R from get(l, j)
+template <int KMAX, typename Get>
+__device__ __forceinline__ void store_rot_win(float* sR, int k, int off, Get get) {
+  constexpr int KW = Win<KMAX>::KW;
+  const int nb = (k + 3) >> 2;
+  for (int e = threadIdx.x; e < nb * KW * 4; e += blockDim.x) {
+    const int jb = e / (KW * 4), rem = e % (KW * 4), m = rem >> 2, j = jb * 4 + (rem & 3);
+    const int l = m - off;
+    sR[e] = (l >= 0 && l < k && j < k) ? (float)get(l, j) : 0.f;
+  }
+}
+
+// Stage rows [t0, t0 + tr) of Q's column window into tile (async copies).
+__device__ __forceinline__ void stage_window(const DiscParams& p, int64_t t0, int tr, float* tile,
+                                             int SW, bool vec) {
+  const int k = p.k, off = (int)(p.col0 & 3);
+  const int64_t c0 = p.col0 - off;
+  if (vec) {   // 16-byte chunks of the aligned window
+    const int w4 = (off + k + 3) >> 2, ne = tr * w4;
+    const int dr = kDiscThreads / w4, dc = kDiscThreads % w4;
+    int r = threadIdx.x / w4, c = threadIdx.x % w4;
+    for (int e = threadIdx.x; e < ne; e += kDiscThreads) {
+      const float* src = p.Q + (t0 + r) * p.ldq + c0 + 4 * c;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(tile + r * SW + 4 * c)),
+                   "l"(src)
+                   : "memory");
+      r += dr;
+      c += dc;
+      if (c >= w4) { c -= w4; ++r; }
     }
-  } else {
-    const int G = kDiscThreads / kk, g = t / kk, e = t % kk;
-    if (g < G) {  // 4 independent accumulators (memory-level parallelism), fixed order
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-      int b = g;
-      for (; b + 3 * G < nb; b += 4 * G) {
-        s0 += pm[(size_t)b * kk + e];
-        s1 += pm[(size_t)(b + G) * kk + e];
-        s2 += pm[(size_t)(b + 2 * G) * kk + e];
-        s3 += pm[(size_t)(b + 3 * G) * kk + e];
-      }
-      for (; b < nb; b += G) s0 += pm[(size_t)b * kk + e];
-      rsum[g * kk + e] = (s0 + s1) + (s2 + s3);
+  } else {     // unaligned rows: 4-byte copies of the k valid columns
+    const int ne = tr * k, dr = kDiscThreads / k, dl = kDiscThreads % k;
+    int r = threadIdx.x / k, l = threadIdx.x % k;
+    for (int e = threadIdx.x; e < ne; e += kDiscThreads) {
+      const float* src = p.Q + (t0 + r) * p.ldq + p.col0 + l;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(tile + r * SW + off + l)),
+                   "l"(src)
+                   : "memory");
+      r += dr;
+      l += dl;
+      if (l >= k) { l -= k; ++r; }
     }
-    __syncthreads();
-    if (t < kk) {
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  __syncthreads();
+}
+
+// This thread's row from the staged tile: raw[m] = Q[i, c0 + m] inside the
+// valid window [off, off + k), zero elsewhere.
+template <int KMAX>
+__device__ __forceinline__ void load_window(const float* rowp, int off, int k,
+                                            float (&raw)[Win<KMAX>::KW]) {
+  constexpr int KW = Win<KMAX>::KW;
+#pragma unroll
+  for (int m4 = 0; m4 < KW / 4; ++m4) {
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * m4 < off + k) v = *reinterpret_cast<const float4*>(rowp + 4 * m4);
+    raw[4 * m4 + 0] = v.x;
+    raw[4 * m4 + 1] = v.y;
+    raw[4 * m4 + 2] = v.z;
+    raw[4 * m4 + 3] = v.w;
+  }
+#pragma unroll
+  for (int m = 0; m < KW; ++m) raw[m] = (m >= off && m < off + k) ? raw[m] : 0.f;
+}
+
+// Phase A for k > 8.  Thread per row scores against R; the normalised tile is
+// then folded into per-CTA fixed-point totals [(label, column)] by integer
+// shared-memory atomics over the flat (row, column) index: the 32 entries a
+// warp touches span at most two rows with disjoint column ranges, so the
+// addresses never collide.  Shared-memory 64-bit atomic add is a CAS loop on
+// sm_100, so each 64-bit value v = hi * 2^32 + lo is added as two native
+// 32-bit atomics, the carry out of the low word detected from its returned
+// old value.  Integer sums are order-free (bit-reproducible); the CTA totals
+// then go to the rotating global buffer `gdst` (same scheme as the k <= 8
+// path, one grid barrier per round).
+// acc layout: lo[k*k] (u32) | hi[k*k] (i32) | count[k] (u32)
+template <int KMAX>
+__device__ void phase_accumulate_wide(const DiscParams& p, const float* sR, float* tile, int* tlab,
+                                      unsigned int* acc, bool score, int* zeros_out,
+                                      unsigned long long* gdst, bool vec) {
+  constexpr int KW = Win<KMAX>::KW, SW = Win<KMAX>::SW;
+  const int k = p.k, kk = k * k, off = (int)(p.col0 & 3);
+  unsigned int* acc_lo = acc;
+  int* acc_hi = reinterpret_cast<int*>(acc + kk);
+  unsigned int* acc_n = acc + 2 * kk;
+  for (int e = threadIdx.x; e < 2 * kk + k; e += blockDim.x) acc[e] = 0u;
+  const float fsc = (float)p.fx_scale;   // power of two: v * fsc is exact in f32
+  const float4* R4 = reinterpret_cast<const float4*>(sR);
+  const Rows R = my_rows(p.n);
+  int zeros = 0;
+  for (int64_t t0 = R.r0; t0 < R.r1; t0 += kDiscThreads) {
+    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
+    stage_window(p, t0, tr, tile, SW, vec);
+    const int64_t i = t0 + threadIdx.x;
+    if (threadIdx.x < tr) {
+      float* rowp = tile + threadIdx.x * SW;
+      float qf[KW];
+      load_window<KMAX>(rowp, off, k, qf);
       double s = 0.0;
-      for (int gg = 0; gg < G; ++gg) s += rsum[gg * kk + t];
-      M[t] = s;
-    }
-  }
-  {
-    const int G = kDiscThreads / k, g = t / k, e = t % k;
-    if (g < G) {
-      long long s = 0;
-      for (int b = g; b < nb; b += G) s += pc[(size_t)b * k + e];
-      rcnt[g * k + e] = s;
+#pragma unroll
+      for (int m = 0; m < KW; ++m) s += (double)qf[m] * (double)qf[m];
+      const double nrm = sqrt(s);
+      const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+      for (int m = 0; m < KW; ++m) qf[m] = (float)((double)qf[m] * inv);
+      if (nrm == 0.0) ++zeros;
+      int lab = 0;
+      if (score) {
+        // scores = q~ R, four columns per pass; a uniform exit per 8 window columns
+        float best = -INFINITY, second = -INFINITY;
+        for (int jb = 0; jb * 4 < k; ++jb) {
+          const float4* c = R4 + jb * KW;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int m0 = 0; m0 < KW; m0 += 4) {
+            if (m0 >= off + k) break;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4 r = c[m0 + u];
+              s0 = fmaf(qf[m0 + u], r.x, s0);
+              s1 = fmaf(qf[m0 + u], r.y, s1);
+              s2 = fmaf(qf[m0 + u], r.z, s2);
+              s3 = fmaf(qf[m0 + u], r.w, s3);
+            }
+          }
+          const float sc[4] = {s0, s1, s2, s3};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float sv = sc[u];
+            if (jb * 4 + u < k) {
+              if (sv > best) { second = best; best = sv; lab = jb * 4 + u; }
+              else if (sv > second) second = sv;
+            }
+          }
+        }
+        p.labels[i] = lab;
+        p.margin[i] = second;
+      } else {
+        lab = p.labels[i];
+      }
+#pragma unroll
+      for (int m4 = 0; m4 < KW / 4; ++m4)
+        if (4 * m4 < off + k)
+          *reinterpret_cast<float4*>(rowp + 4 * m4) =
+              make_float4(qf[4 * m4], qf[4 * m4 + 1], qf[4 * m4 + 2], qf[4 * m4 + 3]);
+      tlab[threadIdx.x] = lab;
     }
     __syncthreads();
-    if (t < k) {
-      long long s = 0;
-      for (int gg = 0; gg < G; ++gg) s += rcnt[gg * k + t];
-      sizes[t] = s;
+    {
+      const int ne = tr * k, dr = kDiscThreads / k, dl = kDiscThreads % k;
+      int r = threadIdx.x / k, l = threadIdx.x % k;
+      for (int e = threadIdx.x; e < ne; e += kDiscThreads) {
+        const int lab = tlab[r], a = lab * k + l;
+        const long long v = __float2ll_rn(tile[r * SW + off + l] * fsc);
+        const unsigned int lo = (unsigned int)v;
+        const unsigned int old = atomicAdd(acc_lo + a, lo);
+        atomicAdd(acc_hi + a, (int)(v >> 32) + (old + lo < old ? 1 : 0));
+        if (l == 0) atomicAdd(acc_n + lab, 1u);
+        r += dr;
+        l += dl;
+        if (l >= k) { l -= k; ++r; }
+      }
     }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    const long long v = (long long)((unsigned long long)(long long)acc_hi[e] << 32) + acc_lo[e];
+    if (v != 0) atomicAdd(gdst + e, (unsigned long long)v);
+  }
+  for (int e = threadIdx.x; e < k; e += blockDim.x)
+    if (acc_n[e] != 0u) atomicAdd(gdst + kk + e, (unsigned long long)acc_n[e]);
+  if (zeros_out) {
+    __shared__ int zsum;
+    if (threadIdx.x == 0) zsum = 0;
+    __syncthreads();
+    atomicAdd(&zsum, zeros);
+    __syncthreads();
+    if (threadIdx.x == 0) *zeros_out = zsum;
   }
   __syncthreads();
 }
-
-// k > 8: two-stage reduction.  Stage 1 (between two grid barriers): CTA b
-// reduces its slice of the k*k + k entries over all partials (fixed order,
-// block tree) into red_m; stage 2: every CTA reads the k*k + k totals.  Each
-// partial is read once instead of once per CTA.
-__device__ void reduce_stage1(const DiscParams& p, int buf, double* red) {
-  const int k = p.k, kk = k * k, nb = gridDim.x, t = threadIdx.x;
-  const double* pm = p.part_m + (size_t)buf * nb * kk;
-  const int64_t* pc = p.part_cnt + (size_t)buf * nb * k;
-  const int ne = kk + k;
-  const int per = (ne + nb - 1) / nb;
-  const int e0 = blockIdx.x * per, e1 = min(ne, e0 + per);
-  for (int e = e0; e < e1; ++e) {
-    double s = 0.0;
-    if (e < kk) {
-      for (int b = t; b < nb; b += blockDim.x) s += pm[(size_t)b * kk + e];
-    } else {
-      for (int b = t; b < nb; b += blockDim.x) s += (double)pc[(size_t)b * k + (e - kk)];
-    }
-    s = block_sum(s, red);
-    if (t == 0) p.red_m[e] = s;
-  }
-}
-
-__device__ void reduce_stage2(const DiscParams& p, double* M, long long* sizes) {
-  const int k = p.k, kk = k * k;
-  for (int e = threadIdx.x; e < kk; e += blockDim.x) M[e] = __ldcg(p.red_m + e);
-  for (int e = threadIdx.x; e < k; e += blockDim.x) sizes[e] = (long long)__ldcg(p.red_m + kk + e);
-  __syncthreads();
-}
-
-__device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
-                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid,
-                           int ri);
 
 // Every CTA: reduce (value, index, label) partials of buffer `buf`.
 // want_max: first max (larger value, then smaller index), else first min.
@@ -460,6 +549,34 @@ __device__ __forceinline__ void ns_quintic(float& x0, float& x1, int k, bool v0o
   x1 = v1ok ? qa * x1 + t1 : 0.f;
 }
 
+// Upper bound on sigma_max(A) (k x k, shared memory), called by one full
+// warp: min(||A||_F, sqrt(||A||_1 ||A||_inf)).  Scaling the Newton-Schulz
+// start by it instead of ||A||_F alone puts the singular values of a
+// well-conditioned A near 1 (||A||_F overestimates sigma_max by up to
+// sqrt(k)), so the linear phase of the iteration is short.
+__device__ __forceinline__ double sigma_bound_warp(const double* A, int k, bool tight) {
+  const int lane = threadIdx.x & 31;
+  double f = 0.0, rmax = 0.0, cmax = 0.0;
+  for (int e = lane; e < k * k; e += 32) f += A[e] * A[e];
+  f = warp_sum(f);
+  if (!tight) return sqrt(f);
+  for (int r = lane; r < k; r += 32) {
+    double rs = 0.0, cs = 0.0;
+    for (int c = 0; c < k; ++c) {
+      rs += fabs(A[r * k + c]);
+      cs += fabs(A[c * k + r]);
+    }
+    rmax = fmax(rmax, rs);
+    cmax = fmax(cmax, cs);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  }
+  return fmin(sqrt(f), sqrt(rmax * cmax));
+}
+
 // Polar factor for k <= 8, warp 0: the slow, linear first phase of the
 // iteration runs in f32 (one 32-bit shuffle per operand instead of two),
 // then f64 sweeps converge quadratically to the f64 fixed point.
@@ -468,9 +585,10 @@ __device__ double polar_ns_small_t(const double* A, double* X, int k, int* iters
   const int kk = k * k, lane = threadIdx.x & 31;
   const int e0 = lane, e1 = lane + 32;
   const bool v0ok = e0 < kk, v1ok = TWO && e1 < kk;
-  double a0 = v0ok ? A[e0] : 0.0, a1 = v1ok ? A[e1] : 0.0;
-  double s = warp_sum(a0 * a0 + a1 * a1);
-  const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
+  // Frobenius start: measured faster here than the tight bound, which leaves
+  // the quintic sweeps overshooting on the (ill-conditioned) small-k blocks
+  const double sb = sigma_bound_warp(A, k, false);
+  const double inv = sb > 0 ? 1.0 / sb : 0.0;
   // X = A^T * inv: X[e] = A[(e % k) * k + e / k]
   double x0 = v0ok ? A[(e0 % k) * k + e0 / k] * inv : 0.0;
   double x1 = v1ok ? A[(e1 % k) * k + e1 / k] * inv : 0.0;
@@ -511,10 +629,13 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
     return s_tr;
   }
   const int kk = k * k, t = threadIdx.x;
-  double s = 0.0;
-  for (int e = t; e < kk; e += blockDim.x) s += A[e] * A[e];
-  s = block_sum(s, red);
-  const double inv = s > 0 ? 1.0 / sqrt(s) : 0.0;
+  if (t < 32) {
+    const double sb = sigma_bound_warp(A, k, true);   // k = 47: 11.6 -> 7.1 sweeps per round
+    if (t == 0) s_tr = sb;
+  }
+  __syncthreads();
+  const double inv = s_tr > 0 ? 1.0 / s_tr : 0.0;
+  __syncthreads();
   for (int e = t; e < kk; e += blockDim.x) X[(e % k) * k + e / k] = A[e] * inv;  // A^T
   __syncthreads();
   // 16 x 16 threads, each a TB x TB register block of the k x k products
@@ -597,26 +718,17 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
   return tr;
 }
 
-__device__ void reduce_all(const DiscParams& p, int buf, double* M, long long* sizes,
-                           double* rsum, long long* rcnt, double* red, cg::grid_group& grid,
-                           int ri) {
-  if (p.k <= 8) {
-    // totals accumulated by the atomics of phase A (buffer ri % 3); CTA 0
-    // clears buffer (ri + 2) % 3, whose next use is two barriers away
-    const int k = p.k, ne = k * k + k;
-    const unsigned long long* src = p.gfx + (size_t)(ri % 3) * ne;
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x)
-      M[e] = (double)(long long)__ldcg(src + e) / p.fx_scale;
-    for (int e = threadIdx.x; e < k; e += blockDim.x) sizes[e] = (long long)__ldcg(src + k * k + e);
-    if (blockIdx.x == 0)
-      for (int e = threadIdx.x; e < ne; e += blockDim.x) p.gfx[(size_t)((ri + 2) % 3) * ne + e] = 0ull;
-    __syncthreads();
-    (void)rsum; (void)rcnt;
-    return;
-  }
-  reduce_stage1(p, buf, red);
-  grid.sync();
-  reduce_stage2(p, M, sizes);
+// Totals accumulated by the fixed-point atomics of phase A (buffer ri % 3);
+// CTA 0 clears buffer (ri + 2) % 3, whose next use is two barriers away.
+__device__ void reduce_all(const DiscParams& p, double* M, long long* sizes, int ri) {
+  const int k = p.k, ne = k * k + k;
+  const unsigned long long* src = p.gfx + (size_t)(ri % 3) * ne;
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x)
+    M[e] = (double)(long long)__ldcg(src + e) / p.fx_scale;
+  for (int e = threadIdx.x; e < k; e += blockDim.x) sizes[e] = (long long)__ldcg(src + k * k + e);
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < ne; e += blockDim.x) p.gfx[(size_t)((ri + 2) % 3) * ne + e] = 0ull;
+  __syncthreads();
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -635,7 +747,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 template <int KMAX>
-__global__ void __launch_bounds__(kDiscThreads)
+__global__ void __launch_bounds__(kDiscThreads, (KMAX > 8 && KMAX <= 48) ? 2 : 1)
 discretize_kernel(DiscParams p) {
   unsigned long long t_prev = 0;
   cg::grid_group grid = cg::this_grid();
@@ -645,13 +757,15 @@ discretize_kernel(DiscParams p) {
   const int nb = gridDim.x;
   // persistent: scoring rotation (f32, rows padded to kp) and prototype rotation (f64)
   float* sR = reinterpret_cast<float*>(smraw);
-  double* sRp = reinterpret_cast<double*>(smraw + align_dev((size_t)k * kp * 4));
-  unsigned char* dyn = smraw + align_dev((size_t)k * kp * 4) + align_dev((size_t)kk * 8);
-  // phase-A view
+  double* sRp = reinterpret_cast<double*>(smraw + align_dev(disc_rot_bytes(k, (int)(p.col0 & 3))));
+  unsigned char* dyn = smraw + align_dev(disc_rot_bytes(k, (int)(p.col0 & 3))) + align_dev((size_t)kk * 8);
+  // phase-A view (k <= 8: G f64 accumulator groups; k > 8: split fixed-point totals)
   double* acc = reinterpret_cast<double*>(dyn);
-  float* tile = reinterpret_cast<float*>(dyn + align_dev((size_t)G * kk * 8));
+  unsigned int* accx = reinterpret_cast<unsigned int*>(dyn);
+  float* tile = reinterpret_cast<float*>(
+      dyn + align_dev(KMAX > 8 ? (2 * (size_t)kk + k) * 4 : (size_t)G * kk * 8));
   int* tlab = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(tile) +
-                                     align_dev((size_t)kDiscThreads * k * 4));
+                                     align_dev(disc_tile_bytes(k, (int)(p.col0 & 3))));
   int* cnt = tlab + kDiscThreads;
   // phase-B view (aliases phase A)
   double* M = reinterpret_cast<double*>(dyn);
@@ -659,13 +773,13 @@ discretize_kernel(DiscParams p) {
   double* Y = X + kk;
   double* T = Y + kk;
   long long* sizes = reinterpret_cast<long long*>(T + kk);
-  __shared__ double rsum[kDiscThreads];
-  __shared__ long long rcnt[kDiscThreads];
   __shared__ double sv[kDiscThreads];
   __shared__ long long si[kDiscThreads];
   __shared__ int sl[kDiscThreads];
   __shared__ double red[32];
   __shared__ int s_flag, s_zero;
+  __shared__ double s_pcol[KMAX > 8 ? Win<KMAX>::KW : 1];
+  const bool vec = (p.ldq % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.Q) & 15) == 0);
 
   const bool cta0 = blockIdx.x == 0;
   const Rows rows = my_rows(p.n);
@@ -679,7 +793,10 @@ discretize_kernel(DiscParams p) {
   for (int run = 0; run < 2; ++run) {
     // ---------------------------------------------------- initial rotation
     if (run == 0) {
-      for (int e = threadIdx.x; e < k * kp; e += blockDim.x) sR[e] = (e / kp == e % kp) ? 1.f : 0.f;
+      if (KMAX > 8)
+        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [](int l, int j) { return l == j ? 1.0 : 0.0; });
+      else
+        for (int e = threadIdx.x; e < k * kp; e += blockDim.x) sR[e] = (e / kp == e % kp) ? 1.f : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = (e / k == e % k) ? 1.0 : 0.0;
     } else {
       // prototype rotation (engine.py:209-218): R[:,0] = q~[0]; greedy rows
@@ -694,7 +811,38 @@ discretize_kernel(DiscParams p) {
       for (int j = 1; j < k; ++j) {
         double best = 0.0;
         long long bi = -1;
-        {
+        if (KMAX > 8) {
+          // staged window tiles (coalesced reads); column j-1 of the
+          // prototype rotation shifted into window coordinates
+          constexpr int KW = Win<KMAX>::KW, SW = Win<KMAX>::SW;
+          const int off = (int)(p.col0 & 3);
+          for (int m = threadIdx.x; m < KW; m += blockDim.x) {
+            const int l = m - off;
+            s_pcol[m] = (l >= 0 && l < k) ? sRp[l * k + (j - 1)] : 0.0;
+          }
+          __syncthreads();
+          for (int64_t t0 = rows.r0; t0 < rows.r1; t0 += kDiscThreads) {
+            const int tr = (int)lmin(kDiscThreads, rows.r1 - t0);
+            stage_window(p, t0, tr, tile, SW, vec);
+            if (threadIdx.x < tr) {
+              const int64_t i = t0 + threadIdx.x;
+              float raw[KW];
+              load_window<KMAX>(tile + threadIdx.x * SW, off, k, raw);
+              double s2 = 0.0;
+#pragma unroll
+              for (int m = 0; m < KW; ++m) s2 += (double)raw[m] * (double)raw[m];
+              const double nrm = sqrt(s2);
+              const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+              double d = 0.0;
+#pragma unroll
+              for (int m = 0; m < KW; ++m) d += ((double)raw[m] * inv) * s_pcol[m];
+              const double a = p.proto_acc[i] + fabs(d);
+              p.proto_acc[i] = a;
+              if (bi < 0 || a < best) { best = a; bi = i; }
+            }
+            __syncthreads();
+          }
+        } else {
           for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x) {
             double q[KMAX], nrm;
             load_row<KMAX>(p, i, q, nrm);
@@ -723,8 +871,11 @@ discretize_kernel(DiscParams p) {
         buf ^= 1;
         __syncthreads();
       }
-      for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
-        sR[e] = e % kp < k ? (float)sRp[(e / kp) * k + e % kp] : 0.f;
+      if (KMAX > 8)
+        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [&](int l, int j) { return sRp[l * k + j]; });
+      else
+        for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
+          sR[e] = e % kp < k ? (float)sRp[(e / kp) * k + e % kp] : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = sRp[e];
     }
     __syncthreads();
@@ -735,9 +886,14 @@ discretize_kernel(DiscParams p) {
     int rounds = 0;
     for (int it = 0; it < p.max_iter; ++it) {
       TSTAMP(0);
-      phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, true,
-                             (run == 0 && it == 0) ? &s_zero : nullptr,
-                             p.k <= 8 ? p.gfx + (size_t)(ri % 3) * (kk + k) : nullptr);
+      if (KMAX > 8)
+        phase_accumulate_wide<KMAX>(p, sR, tile, tlab, accx, true,
+                                    (run == 0 && it == 0) ? &s_zero : nullptr,
+                                    p.gfx + (size_t)(ri % 3) * (kk + k), vec);
+      else
+        phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, true,
+                               (run == 0 && it == 0) ? &s_zero : nullptr,
+                               p.gfx + (size_t)(ri % 3) * (kk + k));
       if (run == 0 && it == 0 && threadIdx.x == 0)   // fold the zero-row count into the
         p.part_cnt[((size_t)(buf ^ 1) * nb + blockIdx.x) * k] = s_zero;  // idle buffer
       TSTAMP(6);
@@ -748,7 +904,7 @@ discretize_kernel(DiscParams p) {
         for (int b = 0; b < nb; ++b) z += p.part_cnt[((size_t)(buf ^ 1) * nb + b) * k];
         p.info[5] = (double)z;
       }
-      reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid, ri);
+      reduce_all(p, M, sizes, ri);
       ++ri;
       TSTAMP(2);
       buf ^= 1;
@@ -784,10 +940,14 @@ discretize_kernel(DiscParams p) {
           }
           __syncthreads();
         }
-        phase_accumulate<KMAX>(p, buf, sR, tile, tlab, acc, cnt, false, nullptr,
-                               p.k <= 8 ? p.gfx + (size_t)(ri % 3) * (kk + k) : nullptr);
+        if (KMAX > 8)
+          phase_accumulate_wide<KMAX>(p, sR, tile, tlab, accx, false, nullptr,
+                                      p.gfx + (size_t)(ri % 3) * (kk + k), vec);
+        else
+          phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, false, nullptr,
+                                 p.gfx + (size_t)(ri % 3) * (kk + k));
         grid.sync();
-        reduce_all(p, buf, M, sizes, rsum, rcnt, red, grid, ri);
+        reduce_all(p, M, sizes, ri);
         ++ri;
         buf ^= 1;
       }
@@ -815,8 +975,11 @@ discretize_kernel(DiscParams p) {
         break;
       }
       // next rotation R = V U^T (engine.py:205)
-      for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
-        sR[e] = e % kp < k ? (float)X[(e / kp) * k + e % kp] : 0.f;
+      if (KMAX > 8)
+        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [&](int l, int j) { return X[l * k + j]; });
+      else
+        for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
+          sR[e] = e % kp < k ? (float)X[(e / kp) * k + e % kp] : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = X[e];
       __syncthreads();
     }
@@ -861,10 +1024,11 @@ static int disc_groups(int k) {
   return g < 1 ? 1 : g;
 }
 
-static size_t disc_smem(int k, int G) {
+static size_t disc_smem(int k, int G, int off) {
   const size_t kk = (size_t)k * k;
-  const size_t fixed = align_dev((size_t)k * kpad4(k) * 4) + align_dev(kk * 8);
-  const size_t a = align_dev((size_t)G * kk * 8) + align_dev((size_t)kDiscThreads * k * 4) +
+  const size_t fixed = align_dev(disc_rot_bytes(k, off)) + align_dev(kk * 8);
+  const size_t acc = k > 8 ? (2 * kk + k) * 4 : (size_t)G * kk * 8;
+  const size_t a = align_dev(acc) + align_dev(disc_tile_bytes(k, off)) +
                    (kDiscThreads + (size_t)G * k) * 4;
   const size_t b = 4 * kk * 8 + (size_t)k * 8;
   return fixed + std::max(a, b) + 64;
@@ -879,11 +1043,9 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   cv.take<int32_t>(n);              // labels_run0
   cv.take<float>(n);                // margin
   cv.take<double>(n);               // proto_acc
-  cv.take<double>((size_t)2 * grid * k * k);
   cv.take<int64_t>((size_t)2 * grid * k);
   cv.take<double>((size_t)2 * grid * 3);
   cv.take<double>((size_t)k * k);
-  cv.take<double>((size_t)k * k + k);
   cv.take<unsigned long long>((size_t)3 * (k * k + k));
   return cv.used;
 }
@@ -891,7 +1053,7 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
 template <int KMAX>
 static int launch_disc(DiscParams& p, cudaStream_t st) {
   auto kern = discretize_kernel<KMAX>;
-  const size_t smem = disc_smem(p.k, p.groups);
+  const size_t smem = disc_smem(p.k, p.groups, (int)(p.col0 & 3));
   ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDiscThreads, smem));
@@ -925,11 +1087,9 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.labels_run0 = cv.take<int32_t>(n);
   p.margin = cv.take<float>(n);
   p.proto_acc = cv.take<double>(n);
-  p.part_m = cv.take<double>((size_t)2 * grid * k * k);
   p.part_cnt = cv.take<int64_t>((size_t)2 * grid * k);
   p.part_arg = cv.take<double>((size_t)2 * grid * 3);
   p.Rg = cv.take<double>((size_t)k * k);
-  p.red_m = cv.take<double>((size_t)k * k + k);
   p.gfx = cv.take<unsigned long long>((size_t)3 * (k * k + k));
   {
     int bits = 1;
@@ -943,9 +1103,12 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   auto st = as_stream(stream);
   ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 8 : 0)), st));
   ANCKA_CUDA(cudaMemsetAsync(p.gfx, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
-  if (k <= 8) return launch_disc<8>(p, st);
-  if (k <= 16) return launch_disc<16>(p, st);
-  if (k <= 32) return launch_disc<32>(p, st);
-  if (k <= 48) return launch_disc<48>(p, st);
-  return launch_disc<64>(p, st);
+  switch (disc_kmax(k, (int)(col0 & 3))) {
+    case 8: return launch_disc<8>(p, st);
+    case 16: return launch_disc<16>(p, st);
+    case 32: return launch_disc<32>(p, st);
+    case 48: return launch_disc<48>(p, st);
+    case 64: return launch_disc<64>(p, st);
+    default: return launch_disc<68>(p, st);
+  }
 }

@@ -314,6 +314,42 @@ def test_wide_discretize_matches_oracle(n, k, noise, monkeypatch):
     assert abs(d.objectives[-1] - ref["objs"][-1]) <= 1e-5 * max(1.0, abs(ref["objs"][-1]))
 
 
+@pytest.mark.parametrize("k", [12, 20, 47, 62])
+def test_discretize_kernel_windows(k):
+    """Cooperative kernel for 8 < k <= 64 against the oracle, and bit-identical
+    across the column offset of the block inside Q (the kernel stages an
+    aligned column window) and across aligned / unaligned row strides
+    (16-byte vs 4-byte staging)."""
+    from paper_2408_05459_b200 import engine
+    n = 3000
+    rng = np.random.default_rng(100 + k)
+    lab = rng.integers(0, k, n)
+    q = np.zeros((n, k))
+    q[np.arange(n), lab] = 1.0
+    q += 0.25 * rng.standard_normal((n, k))
+    q[5] = 0.0
+    q32 = q.astype(np.float32).astype(np.float64)
+    d = ancka.discretize(q32)
+    ref = oc.discretize(q32)
+    assert ari(ref["labels"], d.y.assignment) >= 0.99
+    assert abs(d.objectives[-1] - ref["objs"][-1]) <= 1e-5 * max(1.0, abs(ref["objs"][-1]))
+    base = None
+    for col0 in (0, 1, 2, 3):
+        for ld in (((col0 + k + 3) // 4) * 4, col0 + k + (1 if (col0 + k) % 4 == 0 else 0)):
+            Q = torch.zeros((n, ld), dtype=torch.float32, device="cuda")
+            Q[:, col0:col0 + k] = torch.as_tensor(q32, dtype=torch.float32, device="cuda")
+            labels = torch.empty(n, dtype=torch.int32, device="cuda")
+            info = torch.zeros(8 + 2 * 100 + 2 * k * k, dtype=torch.float64, device="cuda")
+            engine._discretize_device(Q, col0, k, 100, 1e-10, labels, info)
+            got = (labels.cpu().numpy(), info[:8].cpu().numpy())
+            if base is None:
+                base = got
+                assert ari(ref["labels"], got[0]) >= 0.99
+                continue
+            np.testing.assert_array_equal(got[0], base[0], err_msg=f"col0={col0} ld={ld}")
+            np.testing.assert_array_equal(got[1], base[1], err_msg=f"col0={col0} ld={ld}")
+
+
 def test_run_ancka_wide_k_matches_oracle():
     """k = 70 (c = 71 > 64): CholQR on wide blocks, the wide discretisation,
     MHC and init at large k, end to end against the oracle on a
