@@ -215,10 +215,39 @@ def end_to_end():
     (HERE / "end_to_end.json").write_text(json.dumps(meta, indent=1))
 
 
+def aknn_cache():
+    """The .aknn neighbour-cache wire format (knn.py:327-382): files written
+    by the reference's save_neighbor_cache for its own exact lists, and its
+    cache_key for each input, so the B200 reader/writer/key are pinned."""
+    rng = np.random.default_rng(5)
+    xs = {
+        "binary_csr": sp.csr_matrix((rng.random((300, 120)) < 0.06).astype(np.float64)),
+        "dense": np.abs(rng.normal(size=(250, 16))),
+    }
+    out, meta = {}, {}
+    for name, x in xs.items():
+        _x(name, x, out)
+        nl = knn.knn_search_exact(x, 7)
+        f = HERE / f"aknn_{name}.aknn"
+        knn.save_neighbor_cache(f, nl, ancka.KnnMode.EXACT)
+        meta[name] = {"K": 7, "file": f.name,
+                      "key_exact": knn.cache_key(x, 7, ancka.KnnMode.EXACT),
+                      "key_approx": knn.cache_key(x, 7, ancka.KnnMode.APPROX)}
+    np.savez_compressed(HERE / "aknn.npz", **out)
+    (HERE / "aknn.json").write_text(json.dumps(meta, indent=1))
+
+
 if __name__ == "__main__":
-    spec_examples()
-    random_instances()
-    end_to_end()
-    end_to_end_multiplex()
+    which = set(sys.argv[1:])
+    if not which or "spec" in which:
+        spec_examples()
+    if not which or "random" in which:
+        random_instances()
+    if not which or "e2e" in which:
+        end_to_end()
+    if not which or "multiplex" in which:
+        end_to_end_multiplex()
+    if not which or "aknn" in which:
+        aknn_cache()
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)
