@@ -293,6 +293,30 @@ int ancka_mhc(const ancka_operator* op, const int32_t* labels, int32_t k, double
               int32_t gamma, double* phi_out, int64_t* sizes_out,
               void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
+/* Load-balancing plan (ancka_row_split) of the f32 operator pass, from the
+ * structural row pointers `srp` (P_N, or P_V for hypergraphs) and the KNN
+ * row pointers `krp`.  No reference counterpart: the reference's scipy SpMM
+ * is sequential per row (walk.py:135-190); this only schedules the same sums.
+ * plan: row_order (n, descending cost, stable), is_long (n), long_rows
+ * (capacity n, ascending) and counts_out[2] = (n_long, n_pieces) on the
+ * device; pieces: after the caller read the counts, the piece arrays of the
+ * n_long long rows (structural pieces of a row first). */
+size_t ancka_row_split_workspace_size(int64_t n);
+int ancka_row_split_plan(const int64_t* srp, const int64_t* krp, int64_t n, double thr,
+                         int32_t piece, int32_t* order_out, uint8_t* is_long_out,
+                         int32_t* long_rows_out, int64_t* counts_out, void* workspace,
+                         size_t workspace_bytes, ancka_stream_t stream);
+int ancka_row_split_pieces(const int64_t* srp, const int64_t* krp, const int32_t* long_rows,
+                           int64_t n, int64_t n_long, int32_t piece, int64_t* piece_ptr,
+                           int32_t* piece_seg, int64_t* piece_begin, int64_t* piece_end,
+                           void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+
+/* The first iterate Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371, Yhat by
+ * normalize_bcm, engine.py:75-84) as an n x ldq f64 block, from device labels
+ * and cluster sizes; first_col = 1/sqrt(n); columns past c are zero. */
+int ancka_bcm_block(const int32_t* labels, int64_t n, int32_t c, const int64_t* sizes,
+                    double first_col, double* q, int64_t ldq, ancka_stream_t stream);
+
 /* Cluster sizes (BcmMatrix.cluster_sizes, network.py:176-177). */
 int ancka_cluster_sizes(const int32_t* labels, int64_t n, int32_t k, int64_t* sizes_out,
                         ancka_stream_t stream);

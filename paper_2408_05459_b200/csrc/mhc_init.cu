@@ -190,6 +190,38 @@ static void carve_init(Carver& cv, InitWs& w, const ancka_operator* op, int k) {
 
 using namespace ancka;
 
+namespace ancka {
+// Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371): row i gets first_col in
+// column 0 and 1/sqrt(|C_l|) in column l+1 (l = label, l + 1 < c); every other
+// entry of the n x ld block is zero
+__global__ void bcm_block_kernel(const int32_t* __restrict__ labels, int64_t n, int c,
+                                 const int64_t* __restrict__ sizes, double first_col,
+                                 double* __restrict__ q, int64_t ldq) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n * ldq;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / ldq;
+    const int j = (int)(e - i * ldq);
+    double v = 0.0;
+    if (j == 0) {
+      v = first_col;
+    } else if (j < c) {
+      const int l = labels[i];
+      if (l + 1 == j && sizes[l] > 0) v = 1.0 / sqrt((double)sizes[l]);
+    }
+    q[e] = v;
+  }
+}
+}  // namespace ancka
+
+extern "C" int ancka_bcm_block(const int32_t* labels, int64_t n, int32_t c, const int64_t* sizes,
+                               double first_col, double* q, int64_t ldq, ancka_stream_t stream) {
+  ANCKA_REQUIRE(n >= 1 && c >= 1 && ldq >= c, ANCKA_ERR_ARG, "bcm_block: bad sizes");
+  const int grid = (int)std::min<int64_t>(ceil_div(n * ldq, 256), 16 * kNumSMs);
+  bcm_block_kernel<<<grid, 256, 0, as_stream(stream)>>>(labels, n, c, sizes, first_col, q, ldq);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
 extern "C" int ancka_cluster_sizes(const int32_t* labels, int64_t n, int32_t k, int64_t* sizes_out,
                                    ancka_stream_t stream) {
   return cluster_sizes(labels, n, k, sizes_out, as_stream(stream));

@@ -206,6 +206,12 @@ def _centers(deg: np.ndarray, k: int) -> np.ndarray:
 
 
 def _init_labels_device(op: WalkOperator, k: int, t_i: int, alpha: float):
+    labels, centers, _, _ = _init_labels_sizes(op, k, t_i, alpha)
+    return labels, centers
+
+
+def _init_labels_sizes(op: WalkOperator, k: int, t_i: int, alpha: float):
+    """init_bcm on the device: (labels, centers, device sizes, host sizes)."""
     n = op.n
     if k > n:
         raise NetworkError(f"k={k} exceeds node count n={n}")
@@ -224,18 +230,22 @@ def _init_labels_device(op: WalkOperator, k: int, t_i: int, alpha: float):
     ws = WORKSPACE.get("init", wsb)
     _lib.call("ancka_init_bcm", s64, cdev.data_ptr(), k, t_i, float(alpha), labels.data_ptr(),
               ws.data_ptr(), ws.numel(), _lib.stream())
-    sizes = _cluster_sizes(labels, k)
+    sizes_dev = _cluster_sizes_dev(labels, k)
+    sizes = sizes_dev.cpu().numpy()
     if (sizes == 0).any():
         warnings.warn("greedy init left empty cluster(s); pinning centers")
         labels[cdev] = torch.arange(k, dtype=torch.int32, device=dev())
-    return labels, centers
+        sizes_dev = _cluster_sizes_dev(labels, k)
+        sizes = sizes_dev.cpu().numpy()
+    return labels, centers, sizes_dev, sizes
 
 
-def _cluster_sizes(labels: torch.Tensor, k: int) -> np.ndarray:
+def _cluster_sizes_dev(labels: torch.Tensor, k: int) -> torch.Tensor:
     sizes = torch.empty(k, dtype=torch.int64, device=labels.device)
     _lib.call("ancka_cluster_sizes", labels.data_ptr(), labels.numel(), k, sizes.data_ptr(),
               _lib.stream())
-    return sizes.cpu().numpy()
+    return sizes
+
 
 
 def init_bcm(op: WalkOperator, k: int, t_i: int, alpha: float) -> BcmMatrix:
@@ -730,19 +740,14 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             op, g = build_pipeline_device(prep, params)
         n, k = op.n, params.k
         with timer.span("init_ms"):
-            labels0, _ = _init_labels_device(op, k, params.t_i, params.alpha)
+            labels0, _, sizes0_dev, sizes0 = _init_labels_sizes(op, k, params.t_i, params.alpha)
         rng = np.random.default_rng(params.seed)
         c = min(k + 1, n)
         # Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371), f64 for the exact first step
-        sizes0 = _cluster_sizes(labels0, k)
         ld64 = ld_for(c, torch.float64)
-        q0 = torch.zeros((n, ld64), dtype=torch.float64, device=dev())
-        q0[:, 0] = 1.0 / np.sqrt(n)
-        yval = torch.from_numpy(np.where(sizes0 > 0, 1.0 / np.sqrt(np.maximum(sizes0, 1)), 0.0)).to(dev())
-        rows = torch.arange(n, device=dev())
-        lab0 = labels0.long()
-        keep = (lab0 + 1) < c
-        q0[rows[keep], lab0[keep] + 1] = yval[lab0[keep]]
+        q0 = torch.empty((n, ld64), dtype=torch.float64, device=dev())
+        _lib.call("ancka_bcm_block", labels0.data_ptr(), n, c, sizes0_dev.data_ptr(),
+                  1.0 / np.sqrt(n), q0.data_ptr(), ld64, _lib.stream())
         with timer.span("mhc_ms"):
             if (sizes0 == 0).any():
                 raise NetworkError(f"empty cluster(s) {np.flatnonzero(sizes0 == 0).tolist()}: "

@@ -226,53 +226,41 @@ class WalkOperator:
 
     def _split_plan(self) -> _lib.RowSplit:
         """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs),
-        computed with device tensor ops (two scalar read-backs)."""
-        srp = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"].rowptr
-        krp = self.p_k_dev.rowptr
-        d = srp.device
-        ls, lk = srp[1:] - srp[:-1], krp[1:] - krp[:-1]
-        cost = ls + lk
-        mean = float(cost.double().mean().item()) if cost.numel() else 0.0
+        built on the device by plan.cu (one read-back of the two counts)."""
+        sf = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"]
+        srp, krp = sf.rowptr, self.p_k_dev.rowptr
+        d, n = srp.device, self.n
+        # mean row cost = (structural + KNN nonzeros) / n, known on the host
+        mean = (sf.nnz + self.p_k_dev.nnz) / n if n else 0.0
         thr = max(self.LONG_ROW, self.HUB_FACTOR * mean)
-        # regular rows by descending cost (stable): the fused kernel deals them
-        # round-robin to its lane groups, so every group gets a similar load
-        self._order = torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
-        long_rows = torch.nonzero(cost > thr).flatten()
-        n_long = int(long_rows.numel())
+        P = self.PIECE
+        lib = _lib.load()
+        ws = WORKSPACE.get("row_split", lib.ancka_row_split_workspace_size(n))
+        self._order = torch.empty(n, dtype=torch.int32, device=d)
+        is_long = torch.empty(n, dtype=torch.uint8, device=d)
+        long_rows = torch.empty(n, dtype=torch.int32, device=d)
+        counts = torch.empty(2, dtype=torch.int64, device=d)
+        _lib.call("ancka_row_split_plan", srp.data_ptr(), krp.data_ptr(), n, float(thr), P,
+                  self._order.data_ptr(), is_long.data_ptr(), long_rows.data_ptr(),
+                  counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+        n_long, total = (int(v) for v in counts.cpu().tolist())
         if n_long == 0:
             return _lib.RowSplit(0, 0, None, None, None, None, None, None, None, 0,
                                  self._order.data_ptr())
-        P = self.PIECE
-        ns = (ls[long_rows] + P - 1) // P             # structural pieces per long row
-        nk = (lk[long_rows] + P - 1) // P             # KNN pieces per long row
-        per = ns + nk
-        ptr = torch.zeros(n_long + 1, dtype=torch.int64, device=d)
-        ptr[1:] = torch.cumsum(per, 0)
-        total = int(ptr[-1].item())
-        # within-row piece ordinal q and its segment (structural pieces first)
-        rows_of_piece = torch.repeat_interleave(torch.arange(n_long, device=d), per,
-                                                output_size=total)
-        q = torch.arange(total, device=d) - ptr[:-1][rows_of_piece]
-        rrep = long_rows[rows_of_piece]
-        nsr = ns[rows_of_piece]
-        is_k = q >= nsr
-        qq = torch.where(is_k, q - nsr, q)
-        rb = torch.where(is_k, krp[rrep], srp[rrep])
-        re = torch.where(is_k, krp[rrep + 1], srp[rrep + 1])
-        begins = rb + qq * P
-        ends = torch.minimum(re, begins + P)
-        mask = torch.zeros(self.n, dtype=torch.uint8, device=d)
-        mask[long_rows] = 1
         self._plan = {
-            "is_long": mask,
-            "long_rows": long_rows.to(torch.int32),
-            "piece_ptr": ptr,
-            "piece_seg": is_k.to(torch.int32),
-            "piece_begin": begins.contiguous(),
-            "piece_end": ends.contiguous(),
+            "is_long": is_long,
+            "long_rows": long_rows,
+            "piece_ptr": torch.empty(n_long + 1, dtype=torch.int64, device=d),
+            "piece_seg": torch.empty(total, dtype=torch.int32, device=d),
+            "piece_begin": torch.empty(total, dtype=torch.int64, device=d),
+            "piece_end": torch.empty(total, dtype=torch.int64, device=d),
             "partial": torch.empty(total * self.MAX_LD, dtype=torch.float32, device=d),
         }
         p = self._plan
+        _lib.call("ancka_row_split_pieces", srp.data_ptr(), krp.data_ptr(), long_rows.data_ptr(),
+                  n, n_long, P, p["piece_ptr"].data_ptr(), p["piece_seg"].data_ptr(),
+                  p["piece_begin"].data_ptr(), p["piece_end"].data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream())
         return _lib.RowSplit(n_long, total, p["is_long"].data_ptr(),
                              p["long_rows"].data_ptr(), p["piece_ptr"].data_ptr(),
                              p["piece_seg"].data_ptr(), p["piece_begin"].data_ptr(),

@@ -396,3 +396,65 @@ def test_run_ancka_multiplex_matches_reference(golden_multiplex, i):
     assert res.error is None, res.error
     assert ari(res.y.assignment, z[p + "labels"]) >= 0.99
     assert abs(res.mhc - float(z[p + "mhc"])) < 1e-3
+
+
+def _split_plan_torch(srp, krp, n, thr, P):
+    """Torch restatement of the row-split plan (the former host-side builder)."""
+    ls, lk = srp[1:] - srp[:-1], krp[1:] - krp[:-1]
+    cost = ls + lk
+    order = torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
+    long_rows = torch.nonzero(cost > thr).flatten()
+    if long_rows.numel() == 0:
+        return order, long_rows, None
+    ns = (ls[long_rows] + P - 1) // P
+    nk = (lk[long_rows] + P - 1) // P
+    per = ns + nk
+    ptr = torch.zeros(long_rows.numel() + 1, dtype=torch.int64, device=srp.device)
+    ptr[1:] = torch.cumsum(per, 0)
+    segs, begins, ends = [], [], []
+    for j, r in enumerate(long_rows.tolist()):
+        for s, rp in ((0, srp), (1, krp)):
+            b, e = int(rp[r]), int(rp[r + 1])
+            for p in range(b, e, P):
+                segs.append(s)
+                begins.append(p)
+                ends.append(min(p + P, e))
+    return order, long_rows.to(torch.int32), (ptr, segs, begins, ends)
+
+
+@pytest.mark.parametrize("hubs", [0, 7])
+def test_row_split_plan_matches_torch(hubs):
+    """plan.cu (cost order, long rows, pieces) against the torch restatement
+    on a graph with `hubs` star nodes (long structural rows) and KNN hubs."""
+    from paper_2408_05459_b200 import walk
+    rng = np.random.default_rng(hubs)
+    n = 3000
+    a = sp.random(n, n, density=0.002, random_state=rng, format="csr")
+    a.data[:] = 1.0
+    for h in range(hubs):
+        a[h * 11, rng.choice(n, 400, replace=False)] = 1.0
+    a = ((a + a.T) > 0).astype(np.float64).tocsr()
+    a.setdiag(0)
+    a.eliminate_zeros()
+    X = np.abs(rng.normal(size=(n, 8)))
+    X[: n // 2] += 3.0 * np.eye(8)[0]
+    net = ancka.AttributedNetwork.graph(a, X)
+    params = ancka.ClusterParams(k=4, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
+    from paper_2408_05459_b200.engine import build_pipeline
+    op, _, _ = build_pipeline(net, params)
+    split = op._split_plan()
+    sf = op._f["p_n"]
+    thr = max(op.LONG_ROW, op.HUB_FACTOR * (sf.nnz + op.p_k_dev.nnz) / n)
+    order, long_rows, pieces = _split_plan_torch(sf.rowptr, op.p_k_dev.rowptr, n, thr, op.PIECE)
+    assert torch.equal(op._order.cpu(), order.cpu())
+    assert split.n_long == long_rows.numel()
+    if pieces is None:
+        return
+    assert hubs == 0 or split.n_long >= hubs
+    p = op._plan
+    ptr, segs, begins, ends = pieces
+    assert torch.equal(p["long_rows"][: split.n_long].cpu(), long_rows.cpu())
+    assert torch.equal(p["piece_ptr"].cpu(), ptr.cpu())
+    assert p["piece_seg"].cpu().tolist() == segs
+    assert p["piece_begin"].cpu().tolist() == begins
+    assert p["piece_end"].cpu().tolist() == ends

@@ -48,3 +48,37 @@ print("largest idle gaps (us, next event):")
 for g, name in gaps[:12]:
     print(f"  {g:8.1f}  {name}")
 print(f"gaps > 20us: {sum(1 for g, _ in gaps if g > 20)} totalling {sum(g for g, _ in gaps if g > 20) / 1e3:.2f} ms")
+# idle time attributed to where it happens: before the first orth_fused launch
+# (KNN / operator / init) vs inside the iteration loop, by (prev -> next) pair
+first_loop = next((e.time_range.start for e in ev if "orth_fused" in e.name or "cgs2" in e.name), t1)
+pre = sum(g for g, _ in [(x, 0) for x in []])
+idle_pre, idle_loop, pairs = 0.0, 0.0, {}
+last_end, prev = t0, "-"
+for e in ev:
+    s, f = e.time_range.start, e.time_range.end
+    if s > last_end:
+        g = s - last_end
+        if s < first_loop:
+            idle_pre += g
+        else:
+            idle_loop += g
+            key = prev[:40] + " -> " + e.name[:40]
+            a = pairs.setdefault(key, [0, 0.0])
+            a[0] += 1
+            a[1] += g
+    prev = e.name
+    last_end = max(last_end, f)
+print(f"idle before loop {idle_pre / 1e3:.2f} ms, in loop {idle_loop / 1e3:.2f} ms "
+      f"(loop span {(t1 - first_loop) / 1e3:.2f} ms)")
+for key, (cnt, tot) in sorted(pairs.items(), key=lambda x: -x[1][1])[:25]:
+    print(f"  {tot:8.1f} us  x{cnt:3d}  {key}")
+print("pre-loop gaps > 8 us in order (t_ms, gap_us, prev -> next):")
+last_end, prev = t0, "-"
+for e in ev:
+    s, f = e.time_range.start, e.time_range.end
+    if s >= first_loop:
+        break
+    if s - last_end > 8:
+        print(f"  {(s - t0) / 1e3:7.3f} {s - last_end:7.1f}  {prev[:50]} -> {e.name[:50]}")
+    prev = e.name
+    last_end = max(last_end, f)
