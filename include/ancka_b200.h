@@ -317,6 +317,13 @@ int ancka_row_split_pieces(const int64_t* srp, const int64_t* krp, const int32_t
 int ancka_bcm_block(const int32_t* labels, int64_t n, int32_t c, const int64_t* sizes,
                     double first_col, double* q, int64_t ldq, ancka_stream_t stream);
 
+/* beta_vector (walk.py:47-57: beta, 1 for degree-0 nodes, 0 for empty KNN
+ * rows) in f64 and f32, and the self-loop flags of walk.py:123 (degree 0 and
+ * beta_i = 0), from the node degrees and the KNN zero-row flags. */
+int ancka_beta_vector(const double* degrees, const uint8_t* knn_zero_rows, int64_t n, double beta,
+                      double* beta64_out, float* beta32_out, uint8_t* selfloop_out,
+                      ancka_stream_t stream);
+
 /* Cluster sizes (BcmMatrix.cluster_sizes, network.py:176-177). */
 int ancka_cluster_sizes(const int32_t* labels, int64_t n, int32_t k, int64_t* sizes_out,
                         ancka_stream_t stream);

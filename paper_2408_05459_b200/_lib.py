@@ -106,6 +106,8 @@ _SIGS = {
                             c_void_p, c_size_t, c_void_p]),
     "ancka_cluster_sizes": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "ancka_row_split_workspace_size": (c_size_t, [c_int64]),
+    "ancka_beta_vector": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p,
+                                    c_void_p, c_void_p]),
     "ancka_bcm_block": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_double, c_void_p,
                                   c_int64, c_void_p]),
     "ancka_row_split_plan": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_int32, c_void_p,

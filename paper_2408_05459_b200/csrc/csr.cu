@@ -218,3 +218,32 @@ extern "C" int ancka_attr_check(const int64_t* rowptr, const double* values, int
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
+
+namespace ancka {
+// beta_vector (walk.py:47-57) and the self-loop flags (walk.py:123)
+__global__ void beta_vector_kernel(const double* __restrict__ degrees,
+                                   const uint8_t* __restrict__ knn_zero, int64_t n, double beta,
+                                   double* __restrict__ b64, float* __restrict__ b32,
+                                   uint8_t* __restrict__ selfloop) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool isolated = degrees[i] == 0.0;
+    double b = isolated ? 1.0 : beta;
+    if (knn_zero[i]) b = 0.0;
+    b64[i] = b;
+    b32[i] = (float)b;
+    selfloop[i] = (isolated && b == 0.0) ? 1 : 0;
+  }
+}
+}  // namespace ancka
+
+extern "C" int ancka_beta_vector(const double* degrees, const uint8_t* knn_zero_rows, int64_t n,
+                                 double beta, double* beta64_out, float* beta32_out,
+                                 uint8_t* selfloop_out, ancka_stream_t stream) {
+  ANCKA_REQUIRE(n >= 1, ANCKA_ERR_ARG, "beta_vector: empty");
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), 4 * kNumSMs);
+  beta_vector_kernel<<<grid, 256, 0, as_stream(stream)>>>(degrees, knn_zero_rows, n, beta,
+                                                          beta64_out, beta32_out, selfloop_out);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}

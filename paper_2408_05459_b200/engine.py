@@ -762,36 +762,37 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         mhc = _MhcRunner(op, k, _lib.F32)
         lab_t = torch.empty(n, dtype=torch.int32, device=dev())
         info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device=dev())
-        readback = torch.zeros(4, dtype=torch.float64, device=dev())
         error, stop_reason, converged, t = None, "max_iterations", False, 0
         host_info = torch.empty(8, dtype=torch.float64, pin_memory=True)
         host_rb = torch.empty(4, dtype=torch.float64, pin_memory=True)
+        host_rb0 = torch.empty(1, dtype=torch.float64, pin_memory=True)
         rb_ready = torch.cuda.Event()
 
         def sample_issue(t_now, dq_first):
+            # loop.stats = [dq^2, min pivot ratio, suspect pivots, phi]: one
+            # read-back per sample next to the discretisation info
             qt = loop.q
             with timer.span("discretize_ms"):
                 _discretize_device(qt, 1, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
             with timer.span("mhc_ms"):
-                mhc(lab_t, readback[0:1])
+                mhc(lab_t, loop.stats[3:4])
             if dq_first is not None:
-                readback[1] = dq_first * dq_first
-                readback[2] = 0.0
-            else:
-                readback[1] = loop.stats[0]
-                readback[2] = loop.stats[2]
-            readback[3:4].copy_(mhc0_dev)
+                loop.stats[0] = dq_first * dq_first
+                loop.stats[2] = 0.0
+            if best_mhc is None:
+                host_rb0.copy_(mhc0_dev, non_blocking=True)
             host_info.copy_(info[:8], non_blocking=True)
-            host_rb.copy_(readback, non_blocking=True)
+            host_rb.copy_(loop.stats[:4], non_blocking=True)
             rb_ready.record()
 
         def sample_collect():
             nonlocal best_mhc
             rb_ready.synchronize()
             if best_mhc is None:                    # phi(Y0) (engine.py:373)
-                best_mhc = float(host_rb[3])
+                best_mhc = float(host_rb0[0])
                 history[0] = (0, best_mhc)
-            return host_info.numpy().copy(), host_rb.numpy()[:3].copy()
+            rb = host_rb.numpy()
+            return host_info.numpy().copy(), (float(rb[3]), float(rb[0]), float(rb[2]))
 
         def sample(t_now, dq_first):
             sample_issue(t_now, dq_first)
@@ -812,12 +813,27 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             sample_needed = params.tau == 1
             # spec: a tau-block enqueued while the sample is read back
 
+            # the fused path holds no captured pointer to loop.Qsave, so the
+            # save of the previous block start is a buffer swap, not a copy
+            swap_saves = loop.fused or not loop.use_graphs
+
+            def save_prev():
+                nonlocal Qsave_prev
+                if swap_saves:
+                    Qsave_prev, loop.Qsave = loop.Qsave, Qsave_prev
+                else:
+                    Qsave_prev.copy_(loop.Qsave)
+
             def undo_spec():
                 # return to the iterate at t_done: the speculative block saved it
+                nonlocal Qsave_prev
                 start, prev_last = spec[1], spec[2]
                 loop.Q[start].copy_(loop.Qsave)
                 loop.cur = start
-                loop.Qsave.copy_(Qsave_prev)
+                if swap_saves:
+                    Qsave_prev, loop.Qsave = loop.Qsave, Qsave_prev
+                else:
+                    loop.Qsave.copy_(Qsave_prev)
                 loop.last = prev_last
 
             while True:
@@ -827,7 +843,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                     if t_done < params.t_a:
                         # overlap the host decision with the next block (discarded on stop)
                         nxt_s = min(params.t_a, (t_done // params.tau + 1) * params.tau)
-                        Qsave_prev.copy_(loop.Qsave)
+                        save_prev()
                         spec = (nxt_s, loop.cur, getattr(loop, "last", None))
                         with timer.span("ortho_ms"):
                             loop.run(nxt_s - t_done)

@@ -147,16 +147,15 @@ class WalkOperator:
     attributes of the reference (`p_k`, `p_n`, `p_v`, `p_e`, `beta`,
     `selfloop`) are host views materialised on access."""
 
-    def __init__(self, factors: StructureFactors, p_k_dev: DeviceCSR, beta_dev, alpha, gamma):
+    def __init__(self, factors: StructureFactors, p_k_dev: DeviceCSR, beta_vecs, alpha, gamma):
         self.kind, self.n, self.m = factors.kind, factors.n, factors.m
         self.alpha, self.gamma = float(alpha), int(gamma)
         self.degrees = factors.degrees
         self._fac = factors
         self._f = factors.dev
         self.p_k_dev = p_k_dev
-        self.beta64 = beta_dev
-        self.beta32 = beta_dev.to(torch.float32)
-        self.selfloop_dev = ((factors.degrees_dev == 0) & (beta_dev == 0)).to(torch.uint8)
+        # (beta f64, beta f32, self-loop flags) from beta_device
+        self.beta64, self.beta32, self.selfloop_dev = beta_vecs
         self._structs = {}
         self._beta_host = None
 
@@ -272,13 +271,19 @@ class WalkOperator:
         return WORKSPACE.get(f"{key}_{dtype}", rows * ld_for(c, dtype) * (4 if dtype == torch.float32 else 8))
 
 
-def beta_device(factors: StructureFactors, knn_zero_rows, beta: float) -> torch.Tensor:
-    """beta_vector (walk.py:47-57) on the device."""
+def beta_device(factors: StructureFactors, knn_zero_rows, beta: float):
+    """beta_vector (walk.py:47-57) on the device: (beta f64, beta f32,
+    self-loop flags of walk.py:123), one kernel."""
     z = knn_zero_rows if isinstance(knn_zero_rows, torch.Tensor) else \
         torch.from_numpy(np.asarray(knn_zero_rows, dtype=bool)).to(dev())
-    b = torch.full((factors.n,), float(beta), dtype=torch.float64, device=dev())
-    b = torch.where(factors.degrees_dev == 0, torch.ones_like(b), b)
-    return torch.where(z.bool(), torch.zeros_like(b), b)
+    z = z.to(torch.uint8) if z.dtype != torch.uint8 else z
+    n = factors.n
+    b64 = torch.empty(n, dtype=torch.float64, device=dev())
+    b32 = torch.empty(n, dtype=torch.float32, device=dev())
+    loops = torch.empty(n, dtype=torch.uint8, device=dev())
+    _lib.call("ancka_beta_vector", factors.degrees_dev.data_ptr(), z.data_ptr(), n, float(beta),
+              b64.data_ptr(), b32.data_ptr(), loops.data_ptr(), _lib.stream())
+    return b64, b32, loops
 
 
 def build_walk_operator(net: AttributedNetwork, p_k, knn_zero_rows, alpha: float, beta: float,
