@@ -6,8 +6,11 @@
 * t = 1 (rank-deficient by construction) -> f64 apply +
   f64 CGS2 QR with the reference's rank test and its exact numpy noise
   draw (engine.py:139-149), so Q^(1) matches the reference to rounding
-* t >= 2               -> ancka_orth_step_f32 (fused SpMM + Cholesky-QR),
-  captured in a CUDA graph per tau-block
+* t >= 2               -> c <= 8: ancka_orth_block_f32 (one cooperative
+  kernel per tau-block); wider blocks: ancka_orth_step_f32 per step.  CUDA
+  graphs per tau-block are available (use_graphs=True) but off by default:
+  a capture costs 17 ms (DBLP) to 110 ms (Amazon2M) of host time per run
+  and saves ~0.1 ms per replayed block, which a single run never recovers
 * every tau            -> ancka_discretize (one cooperative kernel) and
   ancka_mhc; one small device->host read of (phi, ||dQ||, flags) drives the
   reference's stop rules on the host (engine.py:402-418).
@@ -711,7 +714,7 @@ class _Loop:
 
 
 def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
-              early_stop: bool = True, *, use_graphs: bool = True, fused: bool = True) -> ClusterResult:
+              early_stop: bool = True, *, use_graphs: bool = False, fused: bool = True) -> ClusterResult:
     """Full clustering pipeline (engine.py:343-437): host validation and
     uploads, then the device-resident pipeline (`run_prepared`)."""
     _lib.require_device()
@@ -727,7 +730,7 @@ def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
 
 
 def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool = True, *,
-                 use_graphs: bool = True, fused: bool = True) -> ClusterResult:
+                 use_graphs: bool = False, fused: bool = True) -> ClusterResult:
     """The device pipeline on HBM-resident inputs: KNN -> KNN graph ->
     operator -> init -> orthogonal iterations / discretisation / MHC."""
     _lib.require_device()

@@ -458,3 +458,30 @@ def test_row_split_plan_matches_torch(hubs):
     assert p["piece_seg"].cpu().tolist() == segs
     assert p["piece_begin"].cpu().tolist() == begins
     assert p["piece_end"].cpu().tolist() == ends
+
+
+def test_graph_replay_matches_eager():
+    """The tau-block CUDA-graph path of the unfused loop (c > 8) replays the
+    same kernels: labels and iteration count identical to eager launches."""
+    rng = np.random.default_rng(21)
+    k, per = 12, 80
+    n = k * per
+    lab = np.repeat(np.arange(k), per)
+    rows, cols = [], []
+    for b in range(k):
+        idx = np.arange(b * per, (b + 1) * per)
+        e = rng.integers(0, per, size=(5 * per, 2))
+        rows += list(idx[e[:, 0]])
+        cols += list(idx[e[:, 1]])
+    a = sp.csr_matrix((np.ones(len(rows)), (rows, cols)), shape=(n, n))
+    a = ((a + a.T) > 0).astype(np.float64)
+    a.setdiag(0)
+    a.eliminate_zeros()
+    X = np.abs(rng.normal(0, 2.0, size=(k, 16))[lab] + 0.7 * rng.standard_normal((n, 16)))
+    net = ancka.AttributedNetwork.graph(sp.csr_matrix(a), X)
+    params = ancka.ClusterParams(k=k, knn_k=10, seed=2, knn_mode=ancka.KnnMode.EXACT)
+    r0 = ancka.run_ancka(net, params, use_graphs=False)
+    r1 = ancka.run_ancka(net, params, use_graphs=True)
+    assert r0.iterations == r1.iterations
+    assert np.array_equal(r0.y.assignment, r1.y.assignment)
+    assert r0.mhc == r1.mhc

@@ -34,4 +34,6 @@ for rep in range(2):
     print(f"run {rep}: {dt:.2f}s iters={res.iterations} stop={res.stop_reason} "
           f"err={res.error} ari_planted={adjusted_rand_score(inst.labels, res.y.assignment):.4f} "
           f"timings={ {k: round(v, 1) for k, v in res.timings_ms.items()} }", flush=True)
+    if res.warnings:
+        print("   warnings:", sorted(set(res.warnings)), flush=True)
 print("max mem GB", torch.cuda.max_memory_allocated() / 1e9)
