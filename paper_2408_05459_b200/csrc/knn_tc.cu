@@ -181,11 +181,16 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
     L.clear(p.K);
     float published = 0.f;
     float* stash = P.stash_base + (threadIdx.x - 64) * 33;
+    // shared floor read one tile ahead (the L2 round trip overlaps the tile)
+    int floor_next = i < p.q_end ? __ldcg(p.row_bound + (i - p.q_begin)) : 0;
     for (int t = 0; t < ntiles; ++t) {
       const int acc = t & 1;
       const uint32_t acc_phase = (t >> 1) & 1;
       mbar_wait_sleep(&P.tfull[acc], acc_phase);
-      if (i < p.q_end) L.raise_floor(__int_as_float(__ldcg(p.row_bound + (i - p.q_begin))));
+      if (i < p.q_end) {
+        L.raise_floor(__int_as_float(floor_next));
+        floor_next = __ldcg(p.row_bound + (i - p.q_begin));
+      }
       tc_fence_after();
       const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
 #pragma unroll 1

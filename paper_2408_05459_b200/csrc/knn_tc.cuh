@@ -13,6 +13,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "sm100.cuh"
 
@@ -190,7 +192,8 @@ inline TcGrid tc_grid(int64_t n, int64_t nq) {
   TcGrid g;
   g.q_tiles = (int)ceil_div(nq, tc::BM);
   g.key_tiles = (int)ceil_div(n, tc::BN);
-  int nseg = (int)ceil_div(8 * kNumSMs, g.q_tiles);
+  static const int waves = getenv("ANCKA_KNN_WAVES") ? atoi(getenv("ANCKA_KNN_WAVES")) : 8;
+  int nseg = (int)ceil_div((int64_t)waves * kNumSMs, g.q_tiles);
   nseg = std::max(1, std::min(nseg, g.key_tiles));
   g.tiles_per_seg = (int)ceil_div(g.key_tiles, nseg);
   g.nseg = (int)ceil_div(g.key_tiles, g.tiles_per_seg);

@@ -121,11 +121,18 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
   C.clear(p.K, -p.eps);
   float published = -kInf;
   float* stash = stash_base + (threadIdx.x - 64) * 33;
+  // the shared floor is read one tile ahead: the L2 round trip overlaps the
+  // current tile instead of stalling every tile start (a staler floor is
+  // still a valid lower bound)
+  uint32_t floor_next = live ? __ldcg(p.row_bound + (i - p.q_begin)) : 0u;
   for (int t = 0; t < ntiles; ++t) {
     const int acc = t & 1;
     const uint32_t acc_phase = (t >> 1) & 1;
     mbar_wait_sleep(&tfull[acc], acc_phase);
-    if (live) C.raise_floor(ord2f(__ldcg(p.row_bound + (i - p.q_begin))));
+    if (live) {
+      C.raise_floor(ord2f(floor_next));
+      floor_next = __ldcg(p.row_bound + (i - p.q_begin));
+    }
     tc_fence_after();
     const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
 #pragma unroll 1
