@@ -82,12 +82,17 @@ struct TopK {
     thr_lo = fmaxf(thr_lo, floor_lo);
   }
 
-  // does the candidate rank before entry t?
-  __device__ __forceinline__ static bool above(float ff, uint32_t cc, uint32_t aa, int32_t jj,
-                                               float f2, uint32_t c2, uint32_t a2, int32_t j2) {
+  // does the candidate rank before entry t?  ff_lo / ff_hi = ff (1 -/+ 2 kBand)
+  // bracket the band once per insert: f2 < ff_lo implies ff > f2 (1 + kBand),
+  // f2 > ff_hi implies ff < f2 (1 - kBand); equal (c, a) -- the common exact
+  // tie of binary attributes -- is decided by the index without products
+  __device__ __forceinline__ static bool above(float ff_lo, float ff_hi, uint32_t cc, uint32_t aa,
+                                               int32_t jj, float f2, uint32_t c2, uint32_t a2,
+                                               int32_t j2) {
     if (f2 == 0.f) return true;                       // empty slot
-    if (ff > f2 * (1.f + kBand)) return true;
-    if (ff < f2 * (1.f - kBand)) return false;        // includes +inf padding
+    if (f2 < ff_lo) return true;
+    if (f2 > ff_hi) return false;                     // includes +inf padding
+    if (cc == c2 && aa == a2) return jj < j2;
     return better(cc, aa, jj, c2, a2, j2);
   }
 
@@ -106,8 +111,9 @@ struct TopK {
   // fixed-index selects
   __device__ __forceinline__ void insert(float ff, uint32_t cc, uint32_t aa, int32_t jj) {
     int pos = 0;
+    const float ff_lo = ff * (1.f - 2.f * kBand), ff_hi = ff * (1.f + 2.f * kBand);
 #pragma unroll
-    for (int t = 0; t < KMAX; ++t) pos += above(ff, cc, aa, jj, f[t], c[t], a[t], j[t]) ? 0 : 1;
+    for (int t = 0; t < KMAX; ++t) pos += above(ff_lo, ff_hi, cc, aa, jj, f[t], c[t], a[t], j[t]) ? 0 : 1;
 #pragma unroll
     for (int t = KMAX - 1; t > 0; --t) {
       const bool sh = t > pos, put = t == pos;
@@ -211,16 +217,27 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
         // most 32-column chunks hold a key inside the band.)
         const int64_t jb = j0 + ch * 32;
         uint32_t mask = 0;
+        // the 32 key scales as eight 16-byte loads (jb is a multiple of 32;
+        // inv_sqrt is padded to n_pad), the same addresses for the whole warp
+        const float4* is4 = reinterpret_cast<const float4*>(p.inv_sqrt + jb);
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const float v = __uint_as_float(r[u]);
-          const float kf = v * __ldg(p.inv_sqrt + jb + u);
-          const bool keep = (v > 0.5f) & (kf >= L.thr_lo);
-          mask |= (uint32_t)keep << u;
-          stash[u] = v;
+        for (int q = 0; q < 8; ++q) {
+          const float4 sc = __ldg(is4 + q);
+          const float s4[4] = {sc.x, sc.y, sc.z, sc.w};
+#pragma unroll
+          for (int w = 0; w < 4; ++w) {
+            const int u = 4 * q + w;
+            const float v = __uint_as_float(r[u]);
+            const bool keep = (v > 0.5f) & (v * s4[w] >= L.thr_lo);
+            mask |= (uint32_t)keep << u;
+          }
         }
         if (i >= jb && i < jb + 32) mask &= ~(1u << (int)(i - jb));   // j != i
         if (jb + 32 > p.n) mask &= p.n > jb ? (1u << (int)(p.n - jb)) - 1u : 0u;
+        if (mask) {
+#pragma unroll
+          for (int u = 0; u < 32; ++u) stash[u] = __uint_as_float(r[u]);
+        }
 #pragma unroll 1
         while (mask) {
           const int u = __ffs(mask) - 1;
