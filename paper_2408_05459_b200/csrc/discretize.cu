@@ -466,88 +466,12 @@ __device__ void block_arg(double v, long long id, int lab, bool want_max, double
 }
 
 // Polar factor of A^T (A = M~ = U S V^T):  X -> V U^T by Newton-Schulz
-// X <- 1.5 X - 0.5 X X^T X from X0 = A^T / ||A||_F (all singular values in
-// (0, 1]).  Returns sum(sigma) = tr(X A).  Identical arithmetic in every CTA.
-//
-// k <= 8: warp 0 keeps X and Y in registers (entries lane and lane+32) and
-// forms the products with shuffles -- no barriers inside the iteration.
-// Entry e of a warp-distributed k x k matrix (entry e in lane e, entry
-// e + 32 in the second register); TWO == false when k*k <= 32.
-template <bool TWO, typename T>
-__device__ __forceinline__ T wget(T v0, T v1, int e) {
-  const T a = __shfl_sync(0xffffffffu, v0, e & 31);
-  if (!TWO) return a;
-  const T b = __shfl_sync(0xffffffffu, v1, e & 31);
-  return e < 32 ? a : b;
-}
-
-// Newton-Schulz sweeps X <- 1.5 X - 0.5 X X^T X until no entry moves by
-// more than tol (or maxit sweeps); returns the sweeps done.
-template <bool TWO, typename T>
-__device__ __forceinline__ int ns_sweeps(T& x0, T& x1, int k, bool v0ok, bool v1ok, int r0,
-                                         int c0, int r1, int c1, T tol, int maxit) {
-  int it = 0;
-  for (; it < maxit; ++it) {
-    T y0 = 0, y1 = 0;                                   // Y = X^T X
-    for (int l = 0; l < k; ++l) {
-      const T p0 = wget<TWO>(x0, x1, l * k + (v0ok ? r0 : 0));
-      const T q0 = wget<TWO>(x0, x1, l * k + (v0ok ? c0 : 0));
-      y0 += p0 * q0;
-      if (TWO) {
-        const T p1 = wget<TWO>(x0, x1, l * k + (v1ok ? r1 : 0));
-        const T q1 = wget<TWO>(x0, x1, l * k + (v1ok ? c1 : 0));
-        y1 += p1 * q1;
-      }
-    }
-    T t0 = 0, t1 = 0;                                   // T = X Y
-    for (int l = 0; l < k; ++l) {
-      const T p0 = wget<TWO>(x0, x1, (v0ok ? r0 : 0) * k + l);
-      const T q0 = wget<TWO>(y0, y1, l * k + (v0ok ? c0 : 0));
-      t0 += p0 * q0;
-      if (TWO) {
-        const T p1 = wget<TWO>(x0, x1, (v1ok ? r1 : 0) * k + l);
-        const T q1 = wget<TWO>(y0, y1, l * k + (v1ok ? c1 : 0));
-        t1 += p1 * q1;
-      }
-    }
-    const T n0 = T(1.5) * x0 - T(0.5) * t0, n1 = T(1.5) * x1 - T(0.5) * t1;
-    const bool moved = (v0ok && fabs(n0 - x0) > tol) || (v1ok && fabs(n1 - x1) > tol);
-    x0 = v0ok ? n0 : T(0);
-    x1 = v1ok ? n1 : T(0);
-    if (!__any_sync(0xffffffffu, moved)) { ++it; break; }
-  }
-  return it;
-}
-
+// X <- 1.5 X - 0.5 X X^T X from X0 = A^T / s with s >= sigma_max(A) (all
+// singular values in (0, 1]).  Returns sum(sigma) = tr(X A).  Identical
+// arithmetic in every CTA.  k <= 8 first runs quintic sweeps
+// X <- X (a I + b Y + c Y^2) (small singular values grow ~3.4x per sweep and
+// all stay in (0, 1.13], the basin of the cubic iteration).
 constexpr int kQuinticSweeps = 5;
-
-template <bool TWO>
-__device__ __forceinline__ void ns_quintic(float& x0, float& x1, int k, bool v0ok, bool v1ok,
-                                           int r0, int c0, int r1, int c1) {
-  constexpr float qa = 3.4445f, qb = -4.7750f, qc = 2.0315f;
-  float y0 = 0.f, y1 = 0.f;                             // Y = X^T X
-  for (int l = 0; l < k; ++l) {
-    y0 += wget<TWO>(x0, x1, l * k + (v0ok ? r0 : 0)) * wget<TWO>(x0, x1, l * k + (v0ok ? c0 : 0));
-    if (TWO)
-      y1 += wget<TWO>(x0, x1, l * k + (v1ok ? r1 : 0)) * wget<TWO>(x0, x1, l * k + (v1ok ? c1 : 0));
-  }
-  float z0 = 0.f, z1 = 0.f;                             // P = b Y + c Y^2
-  for (int l = 0; l < k; ++l) {
-    z0 += wget<TWO>(y0, y1, (v0ok ? r0 : 0) * k + l) * wget<TWO>(y0, y1, l * k + (v0ok ? c0 : 0));
-    if (TWO)
-      z1 += wget<TWO>(y0, y1, (v1ok ? r1 : 0) * k + l) * wget<TWO>(y0, y1, l * k + (v1ok ? c1 : 0));
-  }
-  z0 = qb * y0 + qc * z0;
-  z1 = qb * y1 + qc * z1;
-  float t0 = 0.f, t1 = 0.f;                             // T = X P
-  for (int l = 0; l < k; ++l) {
-    t0 += wget<TWO>(x0, x1, (v0ok ? r0 : 0) * k + l) * wget<TWO>(z0, z1, l * k + (v0ok ? c0 : 0));
-    if (TWO)
-      t1 += wget<TWO>(x0, x1, (v1ok ? r1 : 0) * k + l) * wget<TWO>(z0, z1, l * k + (v1ok ? c1 : 0));
-  }
-  x0 = v0ok ? qa * x0 + t0 : 0.f;
-  x1 = v1ok ? qa * x1 + t1 : 0.f;
-}
 
 // Upper bound on sigma_max(A) (k x k, shared memory), called by one full
 // warp: min(||A||_F, sqrt(||A||_1 ||A||_inf)).  Scaling the Newton-Schulz
@@ -577,57 +501,104 @@ __device__ __forceinline__ double sigma_bound_warp(const double* A, int k, bool 
   return fmin(sqrt(f), sqrt(rmax * cmax));
 }
 
-// Polar factor for k <= 8, warp 0: the slow, linear first phase of the
-// iteration runs in f32 (one 32-bit shuffle per operand instead of two),
-// then f64 sweeps converge quadratically to the f64 fixed point.
-template <bool TWO>
-__device__ double polar_ns_small_t(const double* A, double* X, int k, int* iters) {
-  const int kk = k * k, lane = threadIdx.x & 31;
-  const int e0 = lane, e1 = lane + 32;
-  const bool v0ok = e0 < kk, v1ok = TWO && e1 < kk;
-  // Frobenius start: measured faster here than the tight bound, which leaves
-  // the quintic sweeps overshooting on the (ill-conditioned) small-k blocks
-  const double sb = sigma_bound_warp(A, k, false);
-  const double inv = sb > 0 ? 1.0 / sb : 0.0;
-  // X = A^T * inv: X[e] = A[(e % k) * k + e / k]
-  double x0 = v0ok ? A[(e0 % k) * k + e0 / k] * inv : 0.0;
-  double x1 = v1ok ? A[(e1 % k) * k + e1 / k] * inv : 0.0;
-  const int r0 = e0 / k, c0 = e0 % k, r1 = e1 / k, c1 = e1 % k;
-  float f0 = (float)x0, f1 = (float)x1;
-  // quintic sweeps X <- X (a I + b Y + c Y^2): small singular values grow ~3.4x
-  // per sweep and all stay in (0, 1.13] -- the basin of the cubic iteration
-  for (int q = 0; q < kQuinticSweeps; ++q)
-    ns_quintic<TWO>(f0, f1, k, v0ok, v1ok, r0, c0, r1, c1);
-  int it = kQuinticSweeps;
-  it += ns_sweeps<TWO, float>(f0, f1, k, v0ok, v1ok, r0, c0, r1, c1, 1e-4f, 60);
-  x0 = f0;
-  x1 = f1;
-  it += ns_sweeps<TWO, double>(x0, x1, k, v0ok, v1ok, r0, c0, r1, c1, 1e-14 * k, 100);
-  if (v0ok) X[e0] = x0;
-  if (v1ok) X[e1] = x1;
-  // tr(X A) = sum_{a,b} X[a][b] A[b][a]
-  double tr = (v0ok ? x0 * A[c0 * k + r0] : 0.0) + (v1ok ? x1 * A[c1 * k + r1] : 0.0);
-  tr = warp_sum(tr);
-  if (lane == 0) *iters = it;
-  return tr;
+// Polar factor for k <= 8 with the whole CTA: the k x k blocks are padded
+// to 8 x 8 in shared memory (zeros outside k, so padded terms vanish) and
+// each product C = op(A) B is 64 entries x 8 terms = 512 products on 256
+// threads, summed over aligned 8-lane groups by three shuffles -- one
+// barrier per product instead of a k-long dependent shuffle chain per entry
+// in one warp (4x shorter per sweep).  Same recipe as the warp version:
+// quintic f32 sweeps, cubic f32 sweeps to 1e-4, cubic f64 to the fixed point.
+template <typename T>
+__device__ __forceinline__ T seg8_sum(T v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  return v;
 }
 
-__device__ double polar_ns_small(const double* A, double* X, int k, int* iters) {
-  return k * k <= 32 ? polar_ns_small_t<false>(A, X, k, iters)
-                     : polar_ns_small_t<true>(A, X, k, iters);
+// C[r][c] = sum_l op(A)[r][l] B[l][c] on 8 x 8 blocks; TA: op(A) = A^T
+template <typename T, bool TA>
+__device__ __forceinline__ void mm8(const T* A, const T* B, T* C) {
+  const int t = threadIdx.x, l = t & 7;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = (t >> 3) + 32 * h, r = e >> 3, c = e & 7;
+    T v = (TA ? A[l * 8 + r] : A[r * 8 + l]) * B[l * 8 + c];
+    v = seg8_sum(v);
+    if (l == 0) C[e] = v;
+  }
+  __syncthreads();
+}
+
+// cubic sweeps X <- 1.5 X - 0.5 X (X^T X) until no entry moves more than tol
+template <typename T>
+__device__ int ns_sweeps_cta(T* X, T* Y, T* Tm, T tol, int max_it) {
+  int it = 0;
+  for (; it < max_it; ++it) {
+    mm8<T, true>(X, X, Y);
+    mm8<T, false>(X, Y, Tm);
+    bool moved = false;
+    if (threadIdx.x < 64) {
+      const T xo = X[threadIdx.x];
+      const T xn = T(1.5) * xo - T(0.5) * Tm[threadIdx.x];
+      moved = fabs(xn - xo) > tol;
+      X[threadIdx.x] = xn;
+    }
+    if (!__syncthreads_or(moved)) { ++it; break; }
+  }
+  return it;
+}
+
+__device__ double polar_ns_small_cta(const double* A, double* X, int k, int* iters, double* red) {
+  __shared__ float xf[64], yf[64], zf[64], tf[64];
+  __shared__ double xd[64], yd[64], td[64];
+  __shared__ double s_inv;
+  const int t = threadIdx.x;
+  // Frobenius start (measured faster here than the tight bound, which leaves
+  // the quintic sweeps overshooting on the ill-conditioned small-k blocks)
+  if (t < 32) {
+    const double sb = sigma_bound_warp(A, k, false);
+    if (t == 0) s_inv = sb > 0 ? 1.0 / sb : 0.0;
+  }
+  __syncthreads();
+  if (t < 64) {   // X = A^T / sb, padded
+    const int r = t >> 3, c = t & 7;
+    xf[t] = (r < k && c < k) ? (float)(A[c * k + r] * s_inv) : 0.f;
+  }
+  __syncthreads();
+  constexpr float qa = 3.4445f, qb = -4.7750f, qc = 2.0315f;
+  for (int q = 0; q < kQuinticSweeps; ++q) {   // X <- X (a I + b Y + c Y^2)
+    mm8<float, true>(xf, xf, yf);
+    mm8<float, false>(yf, yf, zf);
+    if (t < 64) zf[t] = qb * yf[t] + qc * zf[t];
+    __syncthreads();
+    mm8<float, false>(xf, zf, tf);
+    if (t < 64) xf[t] = qa * xf[t] + tf[t];
+    __syncthreads();
+  }
+  int it = kQuinticSweeps;
+  it += ns_sweeps_cta<float>(xf, yf, tf, 1e-4f, 60);
+  if (t < 64) xd[t] = (double)xf[t];
+  __syncthreads();
+  it += ns_sweeps_cta<double>(xd, yd, td, 1e-14 * k, 100);
+  double tr = 0.0;   // tr(X A) = sum_{a,b} X[a][b] A[b][a]
+  if (t < 64) {
+    const int r = t >> 3, c = t & 7;
+    if (r < k && c < k) {
+      X[r * k + c] = xd[t];
+      tr = xd[t] * A[c * k + r];
+    }
+  }
+  tr = block_sum(tr, red);
+  if (t == 0) *iters = it;
+  __syncthreads();
+  return tr;
 }
 
 __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int k, int* flag,
                            double* red, int* iters) {
   __shared__ double s_tr;
-  if (k <= 8) {
-    if (threadIdx.x < 32) {
-      const double tr = polar_ns_small(A, X, k, iters);
-      if (threadIdx.x == 0) s_tr = tr;
-    }
-    __syncthreads();
-    return s_tr;
-  }
+  if (k <= 8) return polar_ns_small_cta(A, X, k, iters, red);
   const int kk = k * k, t = threadIdx.x;
   if (t < 32) {
     const double sb = sigma_bound_warp(A, k, true);   // k = 47: 11.6 -> 7.1 sweeps per round

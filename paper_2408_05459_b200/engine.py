@@ -566,7 +566,7 @@ def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir
     from pathlib import Path
 
     _lib.require_device()
-    net, _ = validate_network(net)
+    net, report = validate_network(net)
     params.validate_for(net.n)
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, net.n)
     if K >= net.n:
@@ -576,7 +576,7 @@ def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir
     if knn_cache_dir is not None:
         cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
     xd = attributes_to_device(net.attributes, None if K <= 32 else 0)
-    return PreparedNetwork(net, K, xd, xd.level, StructureFactors(net), cache_path)
+    return PreparedNetwork(net, K, xd, xd.level, StructureFactors(net, report.degrees), cache_path)
 
 
 def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):

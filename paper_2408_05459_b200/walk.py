@@ -96,9 +96,9 @@ class StructureFactors:
     and the pattern degrees, built on the device from one upload of the
     structure.  Host scipy views (`host_view`) are materialised on access."""
 
-    def __init__(self, net: AttributedNetwork):
+    def __init__(self, net: AttributedNetwork, degrees=None):
         self.kind, self.n = net.kind, net.n
-        self.degrees = node_degrees(net)
+        self.degrees = node_degrees(net) if degrees is None else degrees
         self.host, self.dev = {}, {}
         if net.kind is NetworkKind.HYPERGRAPH:
             h = _upload(net.incidence)                      # H  (m x n)
