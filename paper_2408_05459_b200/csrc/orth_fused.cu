@@ -64,11 +64,27 @@ __device__ __forceinline__ void f8_store(float* p, const float (&v)[kC]) {
   reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
 }
 
-// acc += sum_{p in [b, e)} w_p * src[col_p]   (sequential, 2-way unrolled)
+// acc += sum_{p in [b, e)} w_p * src[col_p]   (sequential order, 4-way batched loads)
 __device__ __forceinline__ void seg8(const int32_t* __restrict__ ci, const float* __restrict__ val,
                                      const float* __restrict__ src, int64_t b, int64_t e,
                                      float (&acc)[kC]) {
   int64_t p = b;
+  for (; p + 4 <= e; p += 4) {   // four index loads, then four row loads in flight
+    int32_t j[4];
+    float w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      j[q] = __ldg(ci + p + q);
+      w[q] = val ? __ldg(val + p + q) : 1.f;
+    }
+    float x[4][kC];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f8_load(src + (int64_t)j[q] * kC, x[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < kC; ++u) acc[u] = fmaf(w[q], x[q][u], acc[u]);
+  }
   for (; p + 2 <= e; p += 2) {
     const int32_t j0 = __ldg(ci + p), j1 = __ldg(ci + p + 1);
     const float w0 = val ? __ldg(val + p) : 1.f, w1 = val ? __ldg(val + p + 1) : 1.f;
@@ -97,6 +113,24 @@ __device__ __forceinline__ void seg8_strided(const int32_t* __restrict__ ci,
                                              const float* __restrict__ src, int64_t b, int64_t e,
                                              int lane, int gw, float (&acc)[kC]) {
   int64_t p = b + lane;
+  // four nonzeros per round: their index loads, then their row loads, are
+  // in flight together (the rows are L2 hits; latency, not bandwidth, binds)
+  for (; p + 3 * gw < e; p += 4 * gw) {
+    int32_t j[4];
+    float w[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      j[q] = __ldg(ci + p + q * gw);
+      w[q] = val ? __ldg(val + p + q * gw) : 1.f;
+    }
+    float x[4][kC];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f8_load(src + (int64_t)j[q] * kC, x[q]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int u = 0; u < kC; ++u) acc[u] = fmaf(w[q], x[q][u], acc[u]);
+  }
   for (; p + gw < e; p += 2 * gw) {
     const int32_t j0 = __ldg(ci + p), j1 = __ldg(ci + p + gw);
     const float w0 = val ? __ldg(val + p) : 1.f, w1 = val ? __ldg(val + p + gw) : 1.f;
@@ -183,7 +217,7 @@ __device__ __forceinline__ int pidx(int a, int b) {  // a <= b, packed upper of 
   return a * kC - (a * (a - 1)) / 2 + (b - a);
 }
 
-__global__ void __launch_bounds__(kOfThreads, 4)
+__global__ void __launch_bounds__(kOfThreads, 2)
 orth_fused_kernel(OfParams P) {
   cg::grid_group grid = cg::this_grid();
   const ancka_operator& op = P.op;
@@ -232,8 +266,12 @@ orth_fused_kernel(OfParams P) {
     // row groups: 8 lanes per regular row, a whole warp per long row
     const int lane = threadIdx.x & 31;
     const int sub = lane & (kGW - 1);
-    const int64_t gwarp = gtid >> 5, nwarps = gsz >> 5;
-    const int64_t goct = gtid / kGW, noct = gsz / kGW;
+    // lane groups / warps numbered CTA-fastest, so consecutive rows of the
+    // cost order (and consecutive long rows) land on different CTAs: every
+    // CTA gets an equal share of the heavy rows and the barrier after P2
+    // waits less for the slowest CTA
+    const int64_t gwarp = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x, nwarps = gsz >> 5;
+    const int64_t goct = (int64_t)(threadIdx.x / kGW) * gridDim.x + blockIdx.x, noct = gsz / kGW;
     // T = P_E Q of this step was produced at the end of the previous step
     // (or before the loop), already multiplied by R^-1
     const float* Ssrc = hyper ? P.T : Qp;
