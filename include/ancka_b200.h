@@ -48,19 +48,14 @@ typedef struct {
 
 /* Load-balancing plan for the f32 operator application: rows whose
  * structural + KNN nonzeros exceed a threshold ("long" rows, e.g. KNN hubs)
- * are cut into pieces of bounded length that are summed by separate threads
- * and combined in a fixed order (deterministic).  All pointers NULL / counts 0
- * disable it.  The f64 path ignores it (it keeps scipy's sequential order). */
+ * are summed by a whole warp each (lanes strided over the nonzeros, fixed
+ * butterfly combine: deterministic) in the same launch as the regular rows.
+ * All pointers NULL / n_long 0 disable it.  The f64 path ignores it (it keeps
+ * scipy's sequential order). */
 typedef struct {
-  int64_t n_long, n_pieces;
+  int64_t n_long;
   const uint8_t* is_long;     /* n                                        */
   const int32_t* long_rows;   /* n_long                                   */
-  const int64_t* piece_ptr;   /* n_long + 1: pieces of each long row      */
-  const int32_t* piece_seg;   /* n_pieces: 0 structural, 1 KNN segment    */
-  const int64_t* piece_begin; /* n_pieces: nonzero range [begin, end)     */
-  const int64_t* piece_end;
-  void* partial;              /* n_pieces x max_ld f32 scratch            */
-  int64_t max_ld;
   const int32_t* row_order;   /* n rows by descending cost (optional): the
                                  fused narrow-block kernel deals rows to its
                                  lane groups in this order (balanced tails) */
@@ -297,19 +292,13 @@ int ancka_mhc(const ancka_operator* op, const int32_t* labels, int32_t k, double
  * structural row pointers `srp` (P_N, or P_V for hypergraphs) and the KNN
  * row pointers `krp`.  No reference counterpart: the reference's scipy SpMM
  * is sequential per row (walk.py:135-190); this only schedules the same sums.
- * plan: row_order (n, descending cost, stable), is_long (n), long_rows
- * (capacity n, ascending) and counts_out[2] = (n_long, n_pieces) on the
- * device; pieces: after the caller read the counts, the piece arrays of the
- * n_long long rows (structural pieces of a row first). */
+ * Writes row_order (n, descending cost, stable), is_long (n, cost > thr),
+ * long_rows (capacity n, ascending) and *n_long_out (device int64). */
 size_t ancka_row_split_workspace_size(int64_t n);
 int ancka_row_split_plan(const int64_t* srp, const int64_t* krp, int64_t n, double thr,
-                         int32_t piece, int32_t* order_out, uint8_t* is_long_out,
-                         int32_t* long_rows_out, int64_t* counts_out, void* workspace,
-                         size_t workspace_bytes, ancka_stream_t stream);
-int ancka_row_split_pieces(const int64_t* srp, const int64_t* krp, const int32_t* long_rows,
-                           int64_t n, int64_t n_long, int32_t piece, int64_t* piece_ptr,
-                           int32_t* piece_seg, int64_t* piece_begin, int64_t* piece_end,
-                           void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+                         int32_t* order_out, uint8_t* is_long_out, int32_t* long_rows_out,
+                         int64_t* n_long_out, void* workspace, size_t workspace_bytes,
+                         ancka_stream_t stream);
 
 /* The first iterate Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371, Yhat by
  * normalize_bcm, engine.py:75-84) as an n x ldq f64 block, from device labels

@@ -26,10 +26,8 @@ class CSR(ctypes.Structure):
 
 
 class RowSplit(ctypes.Structure):
-    _fields_ = [("n_long", c_int64), ("n_pieces", c_int64), ("is_long", c_void_p),
-                ("long_rows", c_void_p), ("piece_ptr", c_void_p), ("piece_seg", c_void_p),
-                ("piece_begin", c_void_p), ("piece_end", c_void_p), ("partial", c_void_p),
-                ("max_ld", c_int64), ("row_order", c_void_p)]
+    _fields_ = [("n_long", c_int64), ("is_long", c_void_p), ("long_rows", c_void_p),
+                ("row_order", c_void_p)]
 
 
 class Operator(ctypes.Structure):
@@ -110,12 +108,9 @@ _SIGS = {
                                     c_void_p, c_void_p]),
     "ancka_bcm_block": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_double, c_void_p,
                                   c_int64, c_void_p]),
-    "ancka_row_split_plan": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_int32, c_void_p,
+    "ancka_row_split_plan": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p,
                                        c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                        c_void_p]),
-    "ancka_row_split_pieces": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,
-                                         c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
-                                         c_size_t, c_void_p]),
 }
 
 _lib = None

@@ -487,8 +487,6 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
                 "fused orthogonal block: graph and hypergraph operators only");
   ANCKA_REQUIRE(ld == kC && c >= 1 && c <= kC, ANCKA_ERR_UNSUPPORTED,
                 "fused orthogonal block supports c <= 8 with ld == 8");
-  ANCKA_REQUIRE(op32->split.n_pieces == 0 || op32->split.max_ld >= kC, ANCKA_ERR_ARG,
-                "row-split scratch too narrow");
   Carver cv(workspace, workspace_bytes);
   OfParams P{};
   P.op = *op32;

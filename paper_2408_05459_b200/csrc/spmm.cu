@@ -126,15 +126,77 @@ __device__ __forceinline__ void finish_row(const SpmmArgs<T>& a, int64_t row, in
   *reinterpret_cast<VT*>(a.out + row * a.ldo + coloff) = out;
 }
 
+// A long row summed by a whole warp.  Lanes are (slot, chunk) with `lpr`
+// lanes per nonzero (the column chunks, rounded up to a power of two), so the
+// lanes reading one gathered row read its consecutive 16-byte chunks
+// (coalesced), and 32 / lpr nonzeros are in flight per step.  The slot
+// partial sums are combined by a fixed butterfly (deterministic).
+__device__ __forceinline__ float4 warp_rows_sum(const SegArgs<float>& s, int64_t row,
+                                                int64_t coloff, int slot, int nslot, bool act) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (s.rowptr == nullptr) return acc;
+  const int64_t b = __ldg(s.rowptr + row), e = __ldg(s.rowptr + row + 1);
+  const float* src = s.src + coloff;
+  int64_t p = b + slot;
+  for (; p + nslot < e; p += 2 * nslot) {
+    const int32_t j0 = __ldg(s.colidx + p), j1 = __ldg(s.colidx + p + nslot);
+    const float w0 = s.values ? __ldg(s.values + p) : 1.f;
+    const float w1 = s.values ? __ldg(s.values + p + nslot) : 1.f;
+    if (act) {
+      const float4 x0 = ldv(src + (int64_t)j0 * s.ld), x1 = ldv(src + (int64_t)j1 * s.ld);
+      fma_acc(acc, w0, x0);
+      fma_acc(acc, w1, x1);
+    }
+  }
+  if (p < e && act)
+    fma_acc(acc, s.values ? __ldg(s.values + p) : 1.f, ldv(src + (int64_t)__ldg(s.colidx + p) * s.ld));
+  return acc;
+}
+
+__device__ __forceinline__ void slot_reduce(float4& v, int lpr) {
+  for (int o = lpr; o < 32; o <<= 1) {
+    v.x += __shfl_xor_sync(0xffffffffu, v.x, o);
+    v.y += __shfl_xor_sync(0xffffffffu, v.y, o);
+    v.z += __shfl_xor_sync(0xffffffffu, v.z, o);
+    v.w += __shfl_xor_sync(0xffffffffu, v.w, o);
+  }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256)
 spmm_kernel(SpmmArgs<T> a) {
   using VT = typename Vec<T>::type;
   constexpr int W = Vec<T>::W;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // long rows (KNN / graph hubs) take the first blocks, a warp per row, so
+  // the heaviest rows start first instead of forming the tail
+  const int64_t long_blocks = ceil_div(a.n_long, (int64_t)(blockDim.x >> 5));
+  if constexpr (std::is_same<T, float>::value) {
+    if (blockIdx.x < long_blocks) {
+      const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+      if (w >= a.n_long) return;
+      const int lane = threadIdx.x & 31;
+      const int64_t row = a.long_rows[w];
+      for (int cb = 0; cb < a.nchunk; cb += 32) {      // column chunks in blocks of <= 32
+        const int nc = min(32, a.nchunk - cb);
+        int lpr = 1;
+        while (lpr < nc) lpr <<= 1;
+        const int sub = lane & (lpr - 1), slot = lane / lpr, nslot = 32 / lpr;
+        const bool act = sub < nc;
+        const int64_t coloff = (int64_t)(cb + sub) * W;
+        float4 s = warp_rows_sum(a.s, row, coloff, slot, nslot, act);
+        float4 k = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (a.beta) k = warp_rows_sum(a.k, row, coloff, slot, nslot, act);
+        slot_reduce(s, lpr);
+        slot_reduce(k, lpr);
+        if (act && slot == 0) finish_row<T, VT>(a, row, coloff, s, k);
+      }
+      return;
+    }
+  }
+  const int64_t gid = (int64_t)(blockIdx.x - long_blocks) * blockDim.x + threadIdx.x;
   const int64_t row = gid / a.nchunk;
   if (row >= a.rows) return;
-  if (a.skip && a.skip[row]) return;            // long row: pieces + combine
+  if (a.skip && a.skip[row]) return;            // long row: the warp path
   const int chunk = (int)(gid - row * a.nchunk);
   const int64_t coloff = (int64_t)chunk * W;
   VT s = seg_sum<T, VT>(a.s, row, coloff);
@@ -148,74 +210,15 @@ spmm_kernel(SpmmArgs<T> a) {
   finish_row<T, VT>(a, row, coloff, s, k);
 }
 
-// one bounded nonzero range of a long row -> partial[piece]
-__global__ void __launch_bounds__(256)
-spmm_piece_kernel(SpmmArgs<float> a, ancka_row_split sp) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t pc = gid / a.nchunk;
-  if (pc >= sp.n_pieces) return;
-  const int64_t coloff = (int64_t)(gid - pc * a.nchunk) * 4;
-  // select scalar fields (not a reference into the parameter struct, which
-  // would force a local-memory copy of the kernel parameters)
-  const bool kseg = sp.piece_seg[pc] != 0;
-  SegArgs<float> g;
-  g.colidx = kseg ? a.k.colidx : a.s.colidx;
-  g.values = kseg ? a.k.values : a.s.values;
-  g.src = kseg ? a.k.src : a.s.src;
-  g.ld = kseg ? a.k.ld : a.s.ld;
-  const int64_t e = sp.piece_end[pc];
-  const float* src = g.src + coloff;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  int64_t p = sp.piece_begin[pc];
-  for (; p + 4 <= e; p += 4) {
-    const int32_t j0 = __ldg(g.colidx + p), j1 = __ldg(g.colidx + p + 1);
-    const int32_t j2 = __ldg(g.colidx + p + 2), j3 = __ldg(g.colidx + p + 3);
-    const float w0 = g.values ? __ldg(g.values + p) : 1.f, w1 = g.values ? __ldg(g.values + p + 1) : 1.f;
-    const float w2 = g.values ? __ldg(g.values + p + 2) : 1.f, w3 = g.values ? __ldg(g.values + p + 3) : 1.f;
-    const float4 x0 = ldv(src + (int64_t)j0 * g.ld), x1 = ldv(src + (int64_t)j1 * g.ld);
-    const float4 x2 = ldv(src + (int64_t)j2 * g.ld), x3 = ldv(src + (int64_t)j3 * g.ld);
-    fma_acc(acc, w0, x0); fma_acc(acc, w1, x1); fma_acc(acc, w2, x2); fma_acc(acc, w3, x3);
-  }
-  for (; p < e; ++p)
-    fma_acc(acc, g.values ? __ldg(g.values + p) : 1.f, ldv(src + (int64_t)__ldg(g.colidx + p) * g.ld));
-  *reinterpret_cast<float4*>(static_cast<float*>(sp.partial) + pc * sp.max_ld + coloff) = acc;
-}
-
-// fixed-order combination of the pieces of each long row + the row epilogue
-__global__ void __launch_bounds__(256)
-spmm_combine_kernel(SpmmArgs<float> a, ancka_row_split sp) {
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t li = gid / a.nchunk;
-  if (li >= sp.n_long) return;
-  const int64_t coloff = (int64_t)(gid - li * a.nchunk) * 4;
-  const int64_t row = sp.long_rows[li];
-  float4 s = make_float4(0.f, 0.f, 0.f, 0.f), k = s;
-  const float* part = static_cast<const float*>(sp.partial);
-  for (int64_t pc = sp.piece_ptr[li]; pc < sp.piece_ptr[li + 1]; ++pc) {
-    const float4 v = *reinterpret_cast<const float4*>(part + pc * sp.max_ld + coloff);
-    if (sp.piece_seg[pc]) add_acc(k, v); else add_acc(s, v);
-  }
-  finish_row<float, float4>(a, row, coloff, s, k);
-}
-
 template <typename T>
 int launch_spmm(const SpmmArgs<T>& args, cudaStream_t st) {
   if (args.rows == 0) return ANCKA_OK;
   const int64_t threads = args.rows * args.nchunk;
   const int bs = 256;
-  const int64_t grid = ceil_div(threads, bs);
+  // blocks of 8 long-row warps, then the regular blocks
+  const int64_t grid = ceil_div(threads, bs) + ceil_div(args.n_long, (int64_t)(bs / 32));
   ANCKA_REQUIRE(grid < (1ll << 31), ANCKA_ERR_ARG, "spmm grid too large");
   spmm_kernel<T><<<(unsigned)grid, bs, 0, st>>>(args);
-  ANCKA_LAUNCHED();
-  return ANCKA_OK;
-}
-
-static int launch_split(const SpmmArgs<float>& a, const ancka_row_split& sp, cudaStream_t st) {
-  ANCKA_REQUIRE(a.nchunk * 4 <= sp.max_ld, ANCKA_ERR_ARG, "row split scratch narrower than block");
-  const int64_t t1 = sp.n_pieces * a.nchunk, t2 = sp.n_long * a.nchunk;
-  spmm_piece_kernel<<<(unsigned)ceil_div(t1, 256), 256, 0, st>>>(a, sp);
-  ANCKA_LAUNCHED();
-  spmm_combine_kernel<<<(unsigned)ceil_div(t2, 256), 256, 0, st>>>(a, sp);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
@@ -287,10 +290,10 @@ int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, i
     a.scale = epi->scale;
   }
   if constexpr (std::is_same<T, float>::value) {
-    if (op->split.n_long > 0) {
+    if (op->split.n_long > 0) {   // long rows by whole warps in the same launch
       a.skip = op->split.is_long;
-      ANCKA_TRY(launch_spmm<T>(a, st));
-      return launch_split(a, op->split, st);
+      a.long_rows = op->split.long_rows;
+      a.n_long = op->split.n_long;
     }
   }
   return launch_spmm<T>(a, st);

@@ -220,50 +220,32 @@ class WalkOperator:
         return s
 
     # rows costing more than max(LONG_ROW, HUB_FACTOR x the mean row) nonzeros
-    # (hubs) are cut into PIECE-long pieces; ordinary rows stay one thread group
-    LONG_ROW, HUB_FACTOR, PIECE, MAX_LD = 64, 4, 32, 256
+    # (hubs) get a whole warp; ordinary rows stay one thread (group)
+    LONG_ROW, HUB_FACTOR = 64, 4
 
     def _split_plan(self) -> _lib.RowSplit:
-        """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs),
-        built on the device by plan.cu (one read-back of the two counts)."""
+        """Load-balancing plan of the f32 n-row pass (KNN hubs, graph hubs):
+        cost order and long rows, built on the device by plan.cu."""
         sf = self._f["p_v" if self.kind is NetworkKind.HYPERGRAPH else "p_n"]
         srp, krp = sf.rowptr, self.p_k_dev.rowptr
         d, n = srp.device, self.n
         # mean row cost = (structural + KNN nonzeros) / n, known on the host
         mean = (sf.nnz + self.p_k_dev.nnz) / n if n else 0.0
         thr = max(self.LONG_ROW, self.HUB_FACTOR * mean)
-        P = self.PIECE
         lib = _lib.load()
         ws = WORKSPACE.get("row_split", lib.ancka_row_split_workspace_size(n))
         self._order = torch.empty(n, dtype=torch.int32, device=d)
         is_long = torch.empty(n, dtype=torch.uint8, device=d)
         long_rows = torch.empty(n, dtype=torch.int32, device=d)
-        counts = torch.empty(2, dtype=torch.int64, device=d)
-        _lib.call("ancka_row_split_plan", srp.data_ptr(), krp.data_ptr(), n, float(thr), P,
+        n_long_dev = torch.zeros(1, dtype=torch.int64, device=d)
+        _lib.call("ancka_row_split_plan", srp.data_ptr(), krp.data_ptr(), n, float(thr),
                   self._order.data_ptr(), is_long.data_ptr(), long_rows.data_ptr(),
-                  counts.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
-        n_long, total = (int(v) for v in counts.cpu().tolist())
+                  n_long_dev.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
+        n_long = int(n_long_dev.item())
+        self._plan = {"is_long": is_long, "long_rows": long_rows}
         if n_long == 0:
-            return _lib.RowSplit(0, 0, None, None, None, None, None, None, None, 0,
-                                 self._order.data_ptr())
-        self._plan = {
-            "is_long": is_long,
-            "long_rows": long_rows,
-            "piece_ptr": torch.empty(n_long + 1, dtype=torch.int64, device=d),
-            "piece_seg": torch.empty(total, dtype=torch.int32, device=d),
-            "piece_begin": torch.empty(total, dtype=torch.int64, device=d),
-            "piece_end": torch.empty(total, dtype=torch.int64, device=d),
-            "partial": torch.empty(total * self.MAX_LD, dtype=torch.float32, device=d),
-        }
-        p = self._plan
-        _lib.call("ancka_row_split_pieces", srp.data_ptr(), krp.data_ptr(), long_rows.data_ptr(),
-                  n, n_long, P, p["piece_ptr"].data_ptr(), p["piece_seg"].data_ptr(),
-                  p["piece_begin"].data_ptr(), p["piece_end"].data_ptr(), ws.data_ptr(),
-                  ws.numel(), _lib.stream())
-        return _lib.RowSplit(n_long, total, p["is_long"].data_ptr(),
-                             p["long_rows"].data_ptr(), p["piece_ptr"].data_ptr(),
-                             p["piece_seg"].data_ptr(), p["piece_begin"].data_ptr(),
-                             p["piece_end"].data_ptr(), p["partial"].data_ptr(), self.MAX_LD,
+            return _lib.RowSplit(0, None, None, self._order.data_ptr())
+        return _lib.RowSplit(n_long, is_long.data_ptr(), long_rows.data_ptr(),
                              self._order.data_ptr())
 
     def scratch(self, c: int, dtype: torch.dtype, key: str = "op_scratch") -> torch.Tensor:

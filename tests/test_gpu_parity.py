@@ -398,35 +398,19 @@ def test_run_ancka_multiplex_matches_reference(golden_multiplex, i):
     assert abs(res.mhc - float(z[p + "mhc"])) < 1e-3
 
 
-def _split_plan_torch(srp, krp, n, thr, P):
+def _split_plan_torch(srp, krp, thr):
     """Torch restatement of the row-split plan (the former host-side builder)."""
-    ls, lk = srp[1:] - srp[:-1], krp[1:] - krp[:-1]
-    cost = ls + lk
+    cost = (srp[1:] - srp[:-1]) + (krp[1:] - krp[:-1])
     order = torch.sort(cost, descending=True, stable=True).indices.to(torch.int32)
-    long_rows = torch.nonzero(cost > thr).flatten()
-    if long_rows.numel() == 0:
-        return order, long_rows, None
-    ns = (ls[long_rows] + P - 1) // P
-    nk = (lk[long_rows] + P - 1) // P
-    per = ns + nk
-    ptr = torch.zeros(long_rows.numel() + 1, dtype=torch.int64, device=srp.device)
-    ptr[1:] = torch.cumsum(per, 0)
-    segs, begins, ends = [], [], []
-    for j, r in enumerate(long_rows.tolist()):
-        for s, rp in ((0, srp), (1, krp)):
-            b, e = int(rp[r]), int(rp[r + 1])
-            for p in range(b, e, P):
-                segs.append(s)
-                begins.append(p)
-                ends.append(min(p + P, e))
-    return order, long_rows.to(torch.int32), (ptr, segs, begins, ends)
+    long_rows = torch.nonzero(cost > thr).flatten().to(torch.int32)
+    return order, long_rows
 
 
 @pytest.mark.parametrize("hubs", [0, 7])
-def test_row_split_plan_matches_torch(hubs):
-    """plan.cu (cost order, long rows, pieces) against the torch restatement
-    on a graph with `hubs` star nodes (long structural rows) and KNN hubs."""
-    from paper_2408_05459_b200 import walk
+def test_row_split_plan_and_hub_rows(hubs):
+    """plan.cu (cost order, long rows) against the torch restatement on a
+    graph with `hubs` star nodes, and the f32 apply with hub rows summed by
+    whole warps against the oracle (1e-5 relative)."""
     rng = np.random.default_rng(hubs)
     n = 3000
     a = sp.random(n, n, density=0.002, random_state=rng, format="csr")
@@ -445,19 +429,26 @@ def test_row_split_plan_matches_torch(hubs):
     split = op._split_plan()
     sf = op._f["p_n"]
     thr = max(op.LONG_ROW, op.HUB_FACTOR * (sf.nnz + op.p_k_dev.nnz) / n)
-    order, long_rows, pieces = _split_plan_torch(sf.rowptr, op.p_k_dev.rowptr, n, thr, op.PIECE)
+    order, long_rows = _split_plan_torch(sf.rowptr, op.p_k_dev.rowptr, thr)
     assert torch.equal(op._order.cpu(), order.cpu())
     assert split.n_long == long_rows.numel()
-    if pieces is None:
-        return
     assert hubs == 0 or split.n_long >= hubs
-    p = op._plan
-    ptr, segs, begins, ends = pieces
-    assert torch.equal(p["long_rows"][: split.n_long].cpu(), long_rows.cpu())
-    assert torch.equal(p["piece_ptr"].cpu(), ptr.cpu())
-    assert p["piece_seg"].cpu().tolist() == segs
-    assert p["piece_begin"].cpu().tolist() == begins
-    assert p["piece_end"].cpu().tolist() == ends
+    if split.n_long:
+        assert torch.equal(op._plan["long_rows"][: split.n_long].cpu(), long_rows.cpu())
+    # the f32 apply (hub rows by warps) against the f64 oracle apply
+    c = 5
+    m = rng.standard_normal((n, c))
+    q = padded(torch.from_numpy(m), torch.float32)
+    out = torch.empty_like(q)
+    scr = op.scratch(c, torch.float32)
+    _lib.call("ancka_op_apply", op.struct(_lib.F32), q.data_ptr(), q.stride(0), c,
+              out.data_ptr(), out.stride(0), scr.data_ptr(), _lib.stream())
+    got = out[:, :c].double().cpu().numpy()
+    ref = ancka.apply_joint_transition(op, m)
+    rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
+    assert rel <= 1e-5, rel
+    floor = np.sqrt(np.mean(ref ** 2))
+    assert np.all(np.abs(got - ref) <= 1e-5 * (np.abs(ref) + floor))
 
 
 def test_graph_replay_matches_eager():
