@@ -552,8 +552,22 @@ class PreparedNetwork:
     K: int
     x_dev: object           # knn.DeviceAttributes
     x_level: int            # 2 fp8-exact, 1 bf16-exact, 0 general (knn.integer_exact)
-    factors: StructureFactors
+    factors: StructureFactors | None   # None: structure not validated / uploaded yet
     cache_path: object = None
+
+    def finish_structure(self) -> None:
+        """Host validation of the structure (network.py:266-313) and the
+        structural uploads on a side stream.  run_ancka calls it after the
+        KNN launch, so this host work overlaps the KNN on the device (the
+        attributes -- all the KNN reads -- are not changed by validation)."""
+        if self.factors is not None:
+            return
+        main = torch.cuda.current_stream()
+        side = _structure_stream()
+        with torch.cuda.stream(side):
+            self.net, report = validate_network(self.net)
+            self.factors = StructureFactors(self.net, report.degrees)
+        main.wait_stream(side)
 
     def h2d_bytes(self, x) -> int:
         import scipy.sparse as sp
@@ -561,12 +575,29 @@ class PreparedNetwork:
         return int(xb + self.factors.h2d_bytes())
 
 
-def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None) -> PreparedNetwork:
-    """Host validation (network.py:266-313) and the one-time uploads."""
+_SIDE_STREAMS: dict = {}
+
+
+def _structure_stream() -> torch.cuda.Stream:
+    """One persistent side stream per device (the caching allocator keeps
+    per-stream pools: a fresh stream per run would miss them every time)."""
+    d = torch.cuda.current_device()
+    if d not in _SIDE_STREAMS:
+        _SIDE_STREAMS[d] = torch.cuda.Stream(device=d)
+    return _SIDE_STREAMS[d]
+
+
+def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None, *,
+                    defer_structure: bool = False) -> PreparedNetwork:
+    """Host validation (network.py:266-313) and the one-time uploads.
+    defer_structure: upload the attributes only; the structure is validated
+    and uploaded by PreparedNetwork.finish_structure (after the KNN launch)."""
     from pathlib import Path
 
     _lib.require_device()
-    net, report = validate_network(net)
+    report = None
+    if not defer_structure:
+        net, report = validate_network(net)
     params.validate_for(net.n)
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, net.n)
     if K >= net.n:
@@ -576,7 +607,8 @@ def prepare_network(net: AttributedNetwork, params: ClusterParams, knn_cache_dir
     if knn_cache_dir is not None:
         cache_path = Path(knn_cache_dir) / f"{cache_key(net.attributes, K, params.knn_mode)}.aknn"
     xd = attributes_to_device(net.attributes, None if K <= 32 else 0)
-    return PreparedNetwork(net, K, xd, xd.level, StructureFactors(net, report.degrees), cache_path)
+    factors = None if report is None else StructureFactors(net, report.degrees)
+    return PreparedNetwork(net, K, xd, xd.level, factors, cache_path)
 
 
 def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):
@@ -593,6 +625,7 @@ def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):
         if prep.cache_path is not None:
             prep.cache_path.parent.mkdir(parents=True, exist_ok=True)
             save_neighbor_cache(prep.cache_path, neighbors, mode_used)
+    prep.finish_structure()          # host work overlapping the KNN kernel
     ids, scores = neighbors.device()
     A, P, zero = build_knn_graph_device(ids, scores, n)
     g = KnnGraph(A, P, zero, neighbors, mode_used)
@@ -721,7 +754,7 @@ def run_ancka(net: AttributedNetwork, params: ClusterParams, knn_cache_dir=None,
     with warnings.catch_warnings(record=True) as wrec:
         warnings.simplefilter("always")
         t0 = time.perf_counter()
-        prep = prepare_network(net, params, knn_cache_dir)
+        prep = prepare_network(net, params, knn_cache_dir, defer_structure=True)
         prep_ms = (time.perf_counter() - t0) * 1e3
     res = run_prepared(prep, params, early_stop, use_graphs=use_graphs, fused=fused)
     res.timings_ms["knn_ms"] += prep_ms
