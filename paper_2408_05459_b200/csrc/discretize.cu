@@ -48,6 +48,8 @@ struct DiscParams {
   double* info;         // output info
   unsigned long long* tdbg;  // optional phase timing (ANCKA_DISC_TIMING)
   int groups;           // accumulator groups per CTA
+  int run_lo, run_hi;   // alternating-rounding starts handled by this launch
+  double* fin;          // split launches: per-run (obj, rounds, conv, empties)
 };
 
 // Row i of Q[:, col0:col0+k], normalised in f64 (engine.py:226-232) and
@@ -761,7 +763,7 @@ discretize_kernel(DiscParams p) {
   double final_conv[2] = {0.0, 0.0};
   int empties_left[2] = {0, 0};
 
-  for (int run = 0; run < 2; ++run) {
+  for (int run = p.run_lo; run < p.run_hi; ++run) {
     // ---------------------------------------------------- initial rotation
     if (run == 0) {
       if (KMAX > 8)
@@ -963,10 +965,20 @@ discretize_kernel(DiscParams p) {
       for (int e = threadIdx.x; e < kk; e += blockDim.x)
         p.info[8 + 2 * p.max_iter + run * kk + e] = p.Rg[e];
     }
-    if (run == 0)
+    if (run == 0 && p.run_hi == 2)
       for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x)
         p.labels_run0[i] = p.labels[i];
     __syncthreads();
+  }
+  if (p.run_hi - p.run_lo == 1) {   // split launch: the finish kernel picks the winner
+    if (cta0 && threadIdx.x == 0) {
+      const int r = p.run_lo;
+      p.fin[r * 4 + 0] = final_obj[r];
+      p.fin[r * 4 + 1] = final_rounds[r];
+      p.fin[r * 4 + 2] = final_conv[r];
+      p.fin[r * 4 + 3] = empties_left[r];
+    }
+    return;
   }
   // identity wins unless the prototype run is lower by more than 1e-15
   const int win = final_obj[1] < final_obj[0] - 1e-15 ? 1 : 0;
@@ -982,6 +994,27 @@ discretize_kernel(DiscParams p) {
   if (win == 0)
     for (int64_t i = rows.r0 + threadIdx.x; i < rows.r1; i += blockDim.x)
       p.labels[i] = p.labels_run0[i];
+}
+
+// Split launches: pick the winning start (same rule as the fused tail) and
+// move the identity run's labels into the output when it wins.
+__global__ void discretize_finish_kernel(const double* __restrict__ fin, double* __restrict__ info,
+                                         const int32_t* __restrict__ labels_run0,
+                                         int32_t* __restrict__ labels, int64_t n) {
+  const int win = fin[4] < fin[0] - 1e-15 ? 1 : 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    info[0] = fin[win * 4 + 0];
+    info[1] = fin[win * 4 + 1];
+    info[2] = fin[win * 4 + 2];
+    info[3] = win;
+    info[4] = fin[win * 4 + 3];
+    info[6] = fin[1];
+    info[7] = fin[5];
+  }
+  if (win == 0)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+      labels[i] = labels_run0[i];
 }
 
 }  // namespace ancka
@@ -1012,17 +1045,20 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   Carver cv(nullptr, 0);
   const int grid = disc_grid_cap();
   cv.take<int32_t>(n);              // labels_run0
-  cv.take<float>(n);                // margin
   cv.take<double>(n);               // proto_acc
-  cv.take<int64_t>((size_t)2 * grid * k);
-  cv.take<double>((size_t)2 * grid * 3);
-  cv.take<double>((size_t)k * k);
-  cv.take<unsigned long long>((size_t)3 * (k * k + k));
+  cv.take<double>(8);               // fin
+  for (int r = 0; r < 2; ++r) {     // per start (split launches run concurrently)
+    cv.take<float>(n);              // margin
+    cv.take<int64_t>((size_t)2 * grid * k);
+    cv.take<double>((size_t)2 * grid * 3);
+    cv.take<double>((size_t)k * k);
+    cv.take<unsigned long long>((size_t)3 * (k * k + k));
+  }
   return cv.used;
 }
 
 template <int KMAX>
-static int launch_disc(DiscParams& p, cudaStream_t st) {
+static int launch_disc(DiscParams& p, cudaStream_t st, int sm_share) {
   auto kern = discretize_kernel<KMAX>;
   const size_t smem = disc_smem(p.k, p.groups, (int)(p.col0 & 3));
   ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1036,13 +1072,55 @@ static int launch_disc(DiscParams& p, cudaStream_t st) {
   static const int64_t min_rows =
       getenv("ANCKA_DISC_ROWS") ? atoll(getenv("ANCKA_DISC_ROWS")) : kDiscThreads;
   int64_t want = ceil_div(p.n, std::max<int64_t>(kDiscThreads, min_rows));
-  int64_t grid = std::min(want, std::min((int64_t)per_sm * sms, (int64_t)disc_grid_cap()));
+  int64_t grid = std::min(want, std::min((int64_t)per_sm * sms / sm_share, (int64_t)disc_grid_cap()));
   if (grid < 1) grid = 1;
   void* args[] = {&p};
   note_launch();
   ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)grid), dim3(kDiscThreads),
                                          args, smem, st));
   return ANCKA_OK;
+}
+
+static int launch_disc_k(DiscParams& p, int k, int64_t col0, cudaStream_t st, int sm_share) {
+  switch (disc_kmax(k, (int)(col0 & 3))) {
+    case 8: return launch_disc<8>(p, st, sm_share);
+    case 16: return launch_disc<16>(p, st, sm_share);
+    case 32: return launch_disc<32>(p, st, sm_share);
+    case 48: return launch_disc<48>(p, st, sm_share);
+    case 64: return launch_disc<64>(p, st, sm_share);
+    default: return launch_disc<68>(p, st, sm_share);
+  }
+}
+
+// Second stream + fork/join events for the split launches (one per device,
+// created on first use; legal inside stream capture).
+struct DiscSide {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static int disc_side(DiscSide** out) {
+  static DiscSide sides[16];
+  int dev = 0;
+  ANCKA_CUDA(cudaGetDevice(&dev));
+  DiscSide& d = sides[dev & 15];
+  if (!d.s) {
+    ANCKA_CUDA(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking));
+    ANCKA_CUDA(cudaEventCreateWithFlags(&d.fork, cudaEventDisableTiming));
+    ANCKA_CUDA(cudaEventCreateWithFlags(&d.join, cudaEventDisableTiming));
+  }
+  *out = &d;
+  return ANCKA_OK;
+}
+
+// The two alternating-rounding starts are independent until the final
+// comparison (engine.py:247-253).  Small blocks (latency-bound rounds: a grid
+// barrier, a tiny polar factor) run them as two concurrent cooperative
+// launches on half the SMs each, the prototype start on a side stream; large
+// blocks (bandwidth/issue-bound rounds) keep one launch over the whole GPU.
+static bool disc_split(int64_t n, int k) {
+  static const int force = getenv("ANCKA_DISC_SPLIT") ? atoi(getenv("ANCKA_DISC_SPLIT")) : -1;
+  if (force >= 0) return force != 0;
+  return k <= 8 && n <= (1 << 20);
 }
 
 extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64_t n, int32_t k,
@@ -1056,12 +1134,17 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.Q = Q; p.ldq = ldq; p.col0 = col0; p.n = n; p.k = k; p.max_iter = max_iter; p.tol = tol;
   p.labels = labels_out;
   p.labels_run0 = cv.take<int32_t>(n);
-  p.margin = cv.take<float>(n);
   p.proto_acc = cv.take<double>(n);
-  p.part_cnt = cv.take<int64_t>((size_t)2 * grid * k);
-  p.part_arg = cv.take<double>((size_t)2 * grid * 3);
-  p.Rg = cv.take<double>((size_t)k * k);
-  p.gfx = cv.take<unsigned long long>((size_t)3 * (k * k + k));
+  p.fin = cv.take<double>(8);
+  DiscParams pr[2];
+  for (int r = 0; r < 2; ++r) {
+    pr[r] = p;
+    pr[r].margin = cv.take<float>(n);
+    pr[r].part_cnt = cv.take<int64_t>((size_t)2 * grid * k);
+    pr[r].part_arg = cv.take<double>((size_t)2 * grid * 3);
+    pr[r].Rg = cv.take<double>((size_t)k * k);
+    pr[r].gfx = cv.take<unsigned long long>((size_t)3 * (k * k + k));
+  }
   {
     int bits = 1;
     while ((1ll << bits) <= n) ++bits;
@@ -1073,13 +1156,33 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize: workspace too small");
   auto st = as_stream(stream);
   ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 8 : 0)), st));
-  ANCKA_CUDA(cudaMemsetAsync(p.gfx, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
-  switch (disc_kmax(k, (int)(col0 & 3))) {
-    case 8: return launch_disc<8>(p, st);
-    case 16: return launch_disc<16>(p, st);
-    case 32: return launch_disc<32>(p, st);
-    case 48: return launch_disc<48>(p, st);
-    case 64: return launch_disc<64>(p, st);
-    default: return launch_disc<68>(p, st);
+  for (int r = 0; r < 2; ++r) {
+    ANCKA_CUDA(cudaMemsetAsync(pr[r].gfx, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
+    pr[r].fx_scale = p.fx_scale;
+    pr[r].info = p.info;
+    pr[r].tdbg = p.tdbg;
+    pr[r].groups = p.groups;
   }
+  if (!disc_split(n, k)) {
+    DiscParams q = pr[0];
+    q.run_lo = 0;
+    q.run_hi = 2;
+    return launch_disc_k(q, k, col0, st, 1);
+  }
+  DiscSide* side = nullptr;
+  ANCKA_TRY(disc_side(&side));
+  // run 0 (identity start) writes labels_run0, run 1 (prototype) the output
+  DiscParams a = pr[0], b = pr[1];
+  a.run_lo = 0; a.run_hi = 1; a.labels = p.labels_run0;
+  b.run_lo = 1; b.run_hi = 2;
+  ANCKA_CUDA(cudaEventRecord(side->fork, st));
+  ANCKA_CUDA(cudaStreamWaitEvent(side->s, side->fork, 0));
+  ANCKA_TRY(launch_disc_k(b, k, col0, side->s, 2));
+  ANCKA_TRY(launch_disc_k(a, k, col0, st, 2));
+  ANCKA_CUDA(cudaEventRecord(side->join, side->s));
+  ANCKA_CUDA(cudaStreamWaitEvent(st, side->join, 0));
+  const int fg = (int)std::min<int64_t>(ceil_div(n, 256), 2 * kNumSMs);
+  discretize_finish_kernel<<<fg, 256, 0, st>>>(p.fin, info, p.labels_run0, labels_out, n);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
 }
