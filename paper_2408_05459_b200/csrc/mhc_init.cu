@@ -94,18 +94,32 @@ struct MhcWs {
   T* tagval;
   double* yhat;
   double* partial;
+  unsigned long long* hist;
 };
+
+// one cooperative kernel for narrow f32 blocks on graph / hypergraph walks
+template <typename T>
+static bool mhc_fused(const ancka_operator* op, int k) {
+  static const bool off = getenv("ANCKA_MHC_UNFUSED") != nullptr;
+  return sizeof(T) == 4 && k <= 8 && op->kind != ANCKA_MULTIPLEX && !off;
+}
+
+template <typename T>
+static int64_t mhc_ld(const ancka_operator* op, int k) {
+  const int W = sizeof(T) == 4 ? 4 : 2;
+  return mhc_fused<T>(op, k) ? 8 : (k + W - 1) / W * W;
+}
 
 template <typename T>
 static void carve_mhc(Carver& cv, MhcWs<T>& w, const ancka_operator* op, int k) {
-  const int W = sizeof(T) == 4 ? 4 : 2;
-  const int64_t ld = (k + W - 1) / W * W;
+  const int64_t ld = mhc_ld<T>(op, k);
   w.F0 = cv.take<T>((size_t)op->n * ld);
   w.F1 = cv.take<T>((size_t)op->n * ld);
   w.scratch = cv.take<T>(op->kind == ANCKA_HYPERGRAPH ? (size_t)op->m * ld : 1);
   w.tagval = cv.take<T>(k);
   w.yhat = cv.take<double>(k);
-  w.partial = cv.take<double>(kTraceBlocks);
+  w.partial = cv.take<double>(std::max(kTraceBlocks, mhc_fused_grid_cap()));
+  w.hist = cv.take<unsigned long long>(k);
 }
 
 template <typename T>
@@ -115,9 +129,13 @@ static int mhc_t(const ancka_operator* op, const int32_t* labels, int k, double 
   MhcWs<T> w;
   carve_mhc<T>(cv, w, op, k);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "mhc: workspace too small");
-  const int W = sizeof(T) == 4 ? 4 : 2;
-  const int64_t ld = (k + W - 1) / W * W;
+  const int64_t ld = mhc_ld<T>(op, k);
   const int64_t n = op->n;
+  if constexpr (sizeof(T) == 4) {
+    if (mhc_fused<T>(op, k))
+      return mhc_fused_f32(op, labels, k, alpha, gamma, phi, sizes, w.F0, w.F1, w.scratch, w.hist,
+                           w.partial, st);
+  }
   ANCKA_TRY(cluster_sizes(labels, n, k, sizes, st));
   mhc_tagval_kernel<T><<<1, 256, 0, st>>>(sizes, k, alpha, w.tagval, w.yhat);
   ANCKA_LAUNCHED();

@@ -16,6 +16,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "spmm.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -463,6 +464,248 @@ orth_fused_kernel(OfParams P) {
     s = block_sum(s, red);
     if (threadIdx.x == 0) P.stats[0] = s;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// Fused multi-hop conductance (engine.py:291-299) for k <= 8: one cooperative
+// kernel replaces the cluster-size histogram, the tag fill, gamma x (P_E pass
+// + row pass) SpMM launches and the two trace kernels.  Rows are walked in the
+// same cost order and lane layout as the orthogonal block above.
+//   F0 = alpha Yhat;  F <- (1 - alpha) apply(F) + F0  (gamma times);
+//   phi = 1 - <Yhat, F> / k   (NaN when a cluster is empty)
+struct MhcParams {
+  ancka_operator op;
+  const int32_t* labels;
+  int k, gamma;
+  double alpha;
+  float scale;                 // 1 - alpha
+  float* F[2];                 // n x 8 ping-pong
+  float* T;                    // m x 8 (hypergraph)
+  unsigned long long* hist;    // k, zeroed by the host
+  int64_t* sizes;              // k (output)
+  double* part;                // grid trace partials
+  double* phi;
+  unsigned long long* tdbg;    // optional (ANCKA_MHC_TIMING): per phase CTA-0 work, max CTA work
+};
+
+__global__ void __launch_bounds__(kOfThreads, 2)
+mhc_fused_kernel(MhcParams P) {
+  cg::grid_group grid = cg::this_grid();
+  const ancka_operator& op = P.op;
+  const bool hyper = op.kind == ANCKA_HYPERGRAPH;
+  const int64_t* S_rp = hyper ? op.p_v.rowptr : op.p_n.rowptr;
+  const int32_t* S_ci = hyper ? op.p_v.colidx : op.p_n.colidx;
+  const float* Sval = static_cast<const float*>(hyper ? op.p_v.values : op.p_n.values);
+  const int64_t* K_rp = op.p_k.rowptr;
+  const int32_t* K_ci = op.p_k.colidx;
+  const float* Kval = static_cast<const float*>(op.p_k.values);
+  const ancka_row_split& sp = op.split;
+  const int64_t n = op.n;
+  const int k = P.k;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gsz = (int64_t)gridDim.x * blockDim.x;
+  __shared__ unsigned int h[kC];
+  __shared__ float tv[kC];
+  __shared__ double yh[kC];
+  __shared__ double red[32];
+  __shared__ int s_empty;
+  int ph = 0;
+  unsigned long long t_ph = of_timer();
+  // phase work time before a grid barrier: CTA 0's and the max over CTAs
+  auto stamp = [&]() {
+    if (P.tdbg) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const unsigned long long now = of_timer(), dt = now - t_ph;
+        if (blockIdx.x == 0) P.tdbg[2 * ph] += dt;
+        atomicMax(P.tdbg + 2 * ph + 1, dt);
+        if (ph < 8) P.tdbg[64 + ph * 1024 + blockIdx.x] = dt;   // last call, per CTA
+      }
+    }
+  };
+  auto after = [&]() { ++ph; if (P.tdbg && threadIdx.x == 0) t_ph = of_timer(); };
+
+  // ---- cluster sizes (integer atomics: order-free)
+  if (threadIdx.x < kC) h[threadIdx.x] = 0u;
+  __syncthreads();
+  for (int64_t i = gtid; i < n; i += gsz) {
+    const int l = P.labels[i];
+    if (l >= 0 && l < k) atomicAdd(&h[l], 1u);
+  }
+  __syncthreads();
+  if (threadIdx.x < k && h[threadIdx.x]) atomicAdd(P.hist + threadIdx.x, (unsigned long long)h[threadIdx.x]);
+  stamp();
+  grid.sync();
+  after();
+  if (threadIdx.x == 0) s_empty = 0;
+  __syncthreads();
+  if (threadIdx.x < kC) {
+    const int c = threadIdx.x;
+    const unsigned long long sz = c < k ? __ldcg(P.hist + c) : 0ull;
+    const double y = sz > 0 ? 1.0 / sqrt((double)sz) : 0.0;   // mhc_tagval_kernel
+    yh[c] = y;
+    tv[c] = c < k ? (float)(P.alpha * y) : 0.f;
+    if (c < k && sz == 0) s_empty = 1;
+    if (blockIdx.x == 0 && c < k) P.sizes[c] = (int64_t)sz;
+  }
+  __syncthreads();
+  // ---- F0 = alpha Yhat (fill_tag_kernel)
+  for (int64_t i = gtid; i < n; i += gsz) {
+    const int l = P.labels[i];
+    float f[kC];
+#pragma unroll
+    for (int u = 0; u < kC; ++u) f[u] = (u == l && u < k) ? tv[u] : 0.f;
+    f8_store(P.F[0] + i * kC, f);
+  }
+  stamp();
+  grid.sync();
+  after();
+
+  const int lane = threadIdx.x & 31;
+  const int sub = lane & (kGW - 1);
+  const int64_t gwarp = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x, nwarps = gsz >> 5;
+  const int64_t goct = (int64_t)(threadIdx.x / kGW) * gridDim.x + blockIdx.x, noct = gsz / kGW;
+  double tr = 0.0;
+  for (int g = 0; g < P.gamma; ++g) {
+    const float* src = P.F[g & 1];
+    float* dst = P.F[(g + 1) & 1];
+    const bool last = g + 1 == P.gamma;
+    if (hyper) {   // T = P_E F
+      const float* Eval = static_cast<const float*>(op.p_e.values);
+      const int64_t m = op.m;
+      for (int64_t e = goct; e < ((m + noct - 1) / noct) * noct; e += noct) {
+        float acc[kC] = {};
+        if (e < m) seg8_strided(op.p_e.colidx, Eval, src, op.p_e.rowptr[e], op.p_e.rowptr[e + 1],
+                                sub, kGW, acc);
+        group_sum(acc, kGW);
+        if (e < m && sub == 0) f8_store(P.T + e * kC, acc);
+      }
+      stamp();
+  grid.sync();
+  after();
+    }
+    const float* Ssrc = hyper ? P.T : src;
+    // out = (1 - alpha) ((1 - b) (S + self) + b K) + tag   (finish_row with the tag epilogue)
+    auto finish = [&](int64_t i, float (&s)[kC], float (&kk)[kC]) {
+      if (op.selfloop[i]) {
+        float x[kC];
+        f8_load(src + i * kC, x);
+#pragma unroll
+        for (int u = 0; u < kC; ++u) s[u] += x[u];
+      }
+      const float b = __ldg(static_cast<const float*>(op.beta) + i);
+      const float omb = 1.f - b;
+      const int l = __ldg(P.labels + i);
+      float z[kC];
+#pragma unroll
+      for (int u = 0; u < kC; ++u) {
+        const float v = P.scale * (omb * s[u] + b * kk[u]);
+        z[u] = u < k ? v + ((u == l) ? tv[u] : 0.f) : 0.f;
+      }
+      f8_store(dst + i * kC, z);
+      if (last) {
+#pragma unroll
+        for (int u = 0; u < kC; ++u)
+          if (u == l) tr += yh[u] * (double)z[u];
+      }
+    };
+    const int64_t nround = ((n + noct - 1) / noct) * noct;
+    for (int64_t i0 = goct; i0 < nround; i0 += noct) {
+      const int64_t i = (sp.row_order && i0 < n) ? (int64_t)sp.row_order[i0] : i0;
+      const bool live = i0 < n && !(sp.is_long && sp.is_long[i]);
+      float s[kC] = {}, kk[kC] = {};
+      if (live) {
+        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], sub, kGW, s);
+        seg8_strided(K_ci, Kval, src, K_rp[i], K_rp[i + 1], sub, kGW, kk);
+        if (P.tdbg && sub == 0)
+          atomicAdd(P.tdbg + 64 + 8 * 1024 + blockIdx.x,
+                    (unsigned long long)(S_rp[i + 1] - S_rp[i] + K_rp[i + 1] - K_rp[i]));
+      }
+      group_sum(s, kGW);
+      group_sum(kk, kGW);
+      if (live && sub == 0) finish(i, s, kk);
+    }
+    const int64_t lround = ((sp.n_long + nwarps - 1) / nwarps) * nwarps;
+    for (int64_t li = gwarp; li < lround; li += nwarps) {
+      const bool live = li < sp.n_long;
+      const int64_t i = live ? sp.long_rows[li] : 0;
+      float s[kC] = {}, kk[kC] = {};
+      if (live) {
+        seg8_strided(S_ci, Sval, Ssrc, S_rp[i], S_rp[i + 1], lane, 32, s);
+        seg8_strided(K_ci, Kval, src, K_rp[i], K_rp[i + 1], lane, 32, kk);
+      }
+      group_sum(s, 32);
+      group_sum(kk, 32);
+      if (live && lane == 0) finish(i, s, kk);
+    }
+    if (last) {
+      tr = block_sum(tr, red);
+      if (threadIdx.x == 0) P.part[blockIdx.x] = tr;
+    }
+    stamp();
+  grid.sync();
+  after();
+  }
+  if (blockIdx.x == 0) {   // fixed-order sum of the CTA partials (mhc_finish_kernel)
+    double s = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) s += P.part[b];
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) *P.phi = s_empty ? nan("") : 1.0 - s / (double)k;
+  }
+}
+
+constexpr int kMhcTimingWords = 64 + 9 * 1024;
+static unsigned long long* mhc_timing_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (!buf) {
+    cudaMalloc(&buf, kMhcTimingWords * sizeof(unsigned long long));
+    cudaMemset(buf, 0, kMhcTimingWords * sizeof(unsigned long long));
+  }
+  return buf;
+}
+
+extern "C" void ancka_mhc_timing(unsigned long long* out, int reset) {
+  unsigned long long* b = mhc_timing_buffer();
+  cudaDeviceSynchronize();
+  if (out) cudaMemcpy(out, b, kMhcTimingWords * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (reset) cudaMemset(b, 0, kMhcTimingWords * sizeof(unsigned long long));
+  cudaDeviceSynchronize();
+}
+
+int mhc_fused_f32(const ancka_operator* op, const int32_t* labels, int k, double alpha, int gamma,
+                  double* phi, int64_t* sizes, float* F0, float* F1, float* T,
+                  unsigned long long* hist, double* part, cudaStream_t st) {
+  ANCKA_REQUIRE(k >= 1 && k <= kC && gamma >= 1, ANCKA_ERR_UNSUPPORTED, "fused mhc: k <= 8");
+  MhcParams P{};
+  P.op = *op;
+  P.labels = labels;
+  P.k = k;
+  P.gamma = gamma;
+  P.alpha = alpha;
+  P.scale = (float)(1.0 - alpha);
+  P.F[0] = F0;
+  P.F[1] = F1;
+  P.T = T;
+  P.hist = hist;
+  P.sizes = sizes;
+  P.part = part;
+  P.phi = phi;
+  P.tdbg = getenv("ANCKA_MHC_TIMING") ? mhc_timing_buffer() : nullptr;
+  ANCKA_CUDA(cudaMemsetAsync(hist, 0, sizeof(unsigned long long) * k, st));
+  int per_sm = 0, dev = 0, sms = 0;
+  ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mhc_fused_kernel, kOfThreads, 0));
+  ANCKA_CUDA(cudaGetDevice(&dev));
+  ANCKA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  ANCKA_REQUIRE(per_sm >= 1, ANCKA_ERR_UNSUPPORTED, "fused mhc does not fit an SM");
+  const int64_t want = ceil_div(op->n, 32);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
+      want, std::min<int64_t>((int64_t)std::min(per_sm, 2) * sms, mhc_fused_grid_cap())));
+  void* args[] = {&P};
+  note_launch();
+  ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)mhc_fused_kernel, dim3(grid), dim3(kOfThreads),
+                                         args, 0, st));
+  return ANCKA_OK;
 }
 
 }  // namespace ancka
