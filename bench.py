@@ -154,6 +154,14 @@ def oracle_run(inst, seed):
         return time.perf_counter() - t0, res
 
 
+def per_call(tm, calls):
+    """Per-kernel timings: one orthogonal step (apply + QR),
+    one discretisation, one MHC."""
+    return {"ortho_step": round(tm["ortho_ms"] / max(calls["ortho"], 1), 4),
+            "discretize": round(tm["discretize_ms"] / max(calls["discretize"], 1), 4),
+            "mhc": round(tm["mhc_ms"] / max(calls["mhc"], 1), 4)}
+
+
 def run_reference(args):
     """--impl reference: the reference algorithm (oracle port) on the host."""
     ws, rank, _ = dist_env()
@@ -284,6 +292,8 @@ def run_ours(args):
     spmm_ms = time_kernel(apply, 50)
     spmm_bytes = spmm_gbytes_model(op, c, op.p_k_dev.nnz)
     phases = {k: round(v, 3) for k, v in res.timings_ms.items()}
+    gpu_calls = {"ortho": res.iterations, "discretize": res.iterations // 5,
+                 "mhc": res.iterations // 5 + 1}
     traffic = None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
@@ -361,7 +371,10 @@ def run_ours(args):
                "sample": f"one full {SHAPE}-shaped clustering with the numpy/scipy restatement "
                          f"of the reference (oracle/ancka_cpu.py), same instance",
                "ari_vs_gpu": round(float(adjusted_rand_score(ref["labels"], res.y.assignment)), 4),
-               "iterations": ref["iterations"]}
+               "iterations": ref["iterations"],
+               "phases_ms": {k2: round(v, 1) for k2, v in ref["timings_ms"].items()},
+               "per_call_ms": per_call(ref["timings_ms"], ref["calls"]),
+               "gpu_per_call_ms": per_call(phases, gpu_calls)}
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 5), "unit": "s", "n_gpus": ws,
                 "steps": args.steps, "warmup": max(args.warmup, 3),

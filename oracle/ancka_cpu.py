@@ -451,13 +451,23 @@ def run(net, k, knn_k=None, alpha=ALPHA, beta=BETA, gamma=GAMMA, eps_q=0.005,
         t_a=1000, t_i=25, tau=5, seed=0, early_stop=True, knn=None):
     """run_ancka (engine.py:343-437).  Returns a dict with labels, mhc,
     iterations, stop_reason, history and the operator."""
+    import time
+    tm = {"knn_ms": 0.0, "init_ms": 0.0, "ortho_ms": 0.0, "discretize_ms": 0.0, "mhc_ms": 0.0}
+    calls = {"ortho": 0, "discretize": 0, "mhc": 0}
+    t0 = time.perf_counter()
     op, knn_out = build(net, k, knn_k, alpha, beta, gamma, knn)
+    t1 = time.perf_counter()
+    tm["knn_ms"] = (t1 - t0) * 1e3
     labels0, _ = greedy_init(op, k, t_i, alpha)
+    tm["init_ms"] = (time.perf_counter() - t1) * 1e3
     rng = np.random.default_rng(seed)
     n = op["n"]
     q = np.concatenate([np.full((n, 1), 1.0 / np.sqrt(n)), unit_membership(labels0, k)], axis=1)
     q = q[:, :n]
+    t1 = time.perf_counter()
     best_phi = mhc(op, labels0, k)
+    tm["mhc_ms"] += (time.perf_counter() - t1) * 1e3
+    calls["mhc"] += 1
     best = labels0
     hist = [(0, best_phi)]
     stop, it, err = "max_iterations", 0, None
@@ -465,12 +475,21 @@ def run(net, k, knn_k=None, alpha=ALPHA, beta=BETA, gamma=GAMMA, eps_q=0.005,
         for t in range(1, t_a + 1):
             it = t
             q_prev = q
+            t1 = time.perf_counter()
             q, _ = qr_step(op, q_prev, rng)
+            tm["ortho_ms"] += (time.perf_counter() - t1) * 1e3
+            calls["ortho"] += 1
             if t % tau:
                 continue
+            t1 = time.perf_counter()
             d = discretize(q[:, 1:])
             lab = repair(d["labels"], d["scores"], k)
+            t2 = time.perf_counter()
             phi = mhc(op, lab, k)
+            tm["discretize_ms"] += (t2 - t1) * 1e3
+            tm["mhc_ms"] += (time.perf_counter() - t2) * 1e3
+            calls["discretize"] += 1
+            calls["mhc"] += 1
             hist.append((t, phi))
             if phi < best_phi:
                 best_phi, best = phi, lab
@@ -484,4 +503,4 @@ def run(net, k, knn_k=None, alpha=ALPHA, beta=BETA, gamma=GAMMA, eps_q=0.005,
         err, stop = str(exc), "error"
     return {"labels": best, "mhc": best_phi, "iterations": it, "stop_reason": stop,
             "history": hist, "q": q, "op": op, "knn": knn_out, "labels0": labels0,
-            "error": err}
+            "error": err, "timings_ms": tm, "calls": calls}
