@@ -218,7 +218,10 @@ __device__ __forceinline__ int pidx(int a, int b) {  // a <= b, packed upper of 
   return a * kC - (a * (a - 1)) / 2 + (b - a);
 }
 
-__global__ void __launch_bounds__(kOfThreads, 2)
+#ifndef ANCKA_ORTH_CTAS
+#define ANCKA_ORTH_CTAS 2
+#endif
+__global__ void __launch_bounds__(kOfThreads, ANCKA_ORTH_CTAS)
 orth_fused_kernel(OfParams P) {
   cg::grid_group grid = cg::this_grid();
   const ancka_operator& op = P.op;
@@ -489,7 +492,10 @@ struct MhcParams {
   unsigned long long* tdbg;    // optional (ANCKA_MHC_TIMING): per phase CTA-0 work, max CTA work
 };
 
-__global__ void __launch_bounds__(kOfThreads, 2)
+#ifndef ANCKA_MHC_CTAS
+#define ANCKA_MHC_CTAS 3
+#endif
+__global__ void __launch_bounds__(kOfThreads, ANCKA_MHC_CTAS)
 mhc_fused_kernel(MhcParams P) {
   cg::grid_group grid = cg::this_grid();
   const ancka_operator& op = P.op;
@@ -700,7 +706,7 @@ int mhc_fused_f32(const ancka_operator* op, const int32_t* labels, int k, double
   ANCKA_REQUIRE(per_sm >= 1, ANCKA_ERR_UNSUPPORTED, "fused mhc does not fit an SM");
   const int64_t want = ceil_div(op->n, 32);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
-      want, std::min<int64_t>((int64_t)std::min(per_sm, 2) * sms, mhc_fused_grid_cap())));
+      want, std::min<int64_t>((int64_t)std::min(per_sm, ANCKA_MHC_CTAS) * sms, mhc_fused_grid_cap())));
   void* args[] = {&P};
   note_launch();
   ANCKA_CUDA(cudaLaunchCooperativeKernel((void*)mhc_fused_kernel, dim3(grid), dim3(kOfThreads),
@@ -755,7 +761,7 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
   // two CTAs per SM: more CTAs shorten each CTA's row share but lengthen the
   // grid barriers and the tail (measured at the DBLP shape: 2/SM 861 us per
   // 20 steps, 4/SM 975 us)
-  const int64_t cap = getenv("ANCKA_ORTH_GRID") ? of_grid_cap() : 2 * (int64_t)sms;
+  const int64_t cap = getenv("ANCKA_ORTH_GRID") ? of_grid_cap() : ANCKA_ORTH_CTAS * (int64_t)sms;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(
       want, std::min<int64_t>((int64_t)per_sm * sms, std::min<int64_t>(cap, of_grid_cap()))));
   void* args[] = {&P};

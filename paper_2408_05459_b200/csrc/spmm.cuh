@@ -54,7 +54,7 @@ int op_apply_struct_t_t(const ancka_operator* op, const T* Q, int64_t ldq, int c
                         int64_t ldz, T* scratch, cudaStream_t st, const EpilogueTag<T>* epi);
 
 // fused multi-hop conductance for k <= 8 (orth_fused.cu); F0/F1 n x 8, T m x 8
-constexpr int mhc_fused_grid_cap() { return 2 * kNumSMs; }
+constexpr int mhc_fused_grid_cap() { return 4 * kNumSMs; }
 int mhc_fused_f32(const ancka_operator* op, const int32_t* labels, int k, double alpha, int gamma,
                   double* phi, int64_t* sizes, float* F0, float* F1, float* T,
                   unsigned long long* hist, double* part, cudaStream_t st);
