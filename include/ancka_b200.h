@@ -288,6 +288,13 @@ int ancka_mhc(const ancka_operator* op, const int32_t* labels, int32_t k, double
               int32_t gamma, double* phi_out, int64_t* sizes_out,
               void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
+/* Diagnostics of the fused MHC kernel (k <= 8, set ANCKA_MHC_TIMING=1 before
+ * the first call): copies the phase timers (host u64[64 + 9 * 1024]: per
+ * phase CTA-0 ns and max-over-CTAs ns, per-CTA ns, per-CTA nonzeros) and
+ * optionally resets them.  Synchronises the device.  Not used on the
+ * clustering path. */
+void ancka_mhc_timing(unsigned long long* out, int reset);
+
 /* Load-balancing plan (ancka_row_split) of the f32 operator pass, from the
  * structural row pointers `srp` (P_N, or P_V for hypergraphs) and the KNN
  * row pointers `krp`.  No reference counterpart: the reference's scipy SpMM

@@ -18,7 +18,7 @@ warnings.simplefilter("ignore")
 
 def _header_symbols():
     text = (ROOT / "include" / "ancka_b200.h").read_text()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int|int64_t|size_t)\s+(ancka_\w+)\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int|int64_t|size_t|void)\s+(ancka_\w+)\(", text, re.M)))
 
 
 def test_library_builds_and_exports():

@@ -37,10 +37,10 @@ import os  # noqa: E402
 if os.environ.get("ANCKA_MHC_TIMING"):
     lib = _lib.load()
     buf = (ctypes.c_ulonglong * (64 + 9 * 1024))()
-    lib.ancka_mhc_timing(buf, 1)
+    lib.ancka_mhc_timing(ctypes.cast(buf, ctypes.c_void_p), 1)
     for rep in range(reps):
         run(labels)
-    lib.ancka_mhc_timing(buf, 1)
+    lib.ancka_mhc_timing(ctypes.cast(buf, ctypes.c_void_p), 1)
     names = ["hist", "F0"] + [f"{x}{g}" for g in range(3) for x in ("T", "rows")]
     print("per call, us (CTA0 work / max CTA work):",
           {nm: (round(buf[2 * q] / reps / 1e3, 1), round(buf[2 * q + 1] / 1e3, 1)) for q, nm in enumerate(names)})
