@@ -1,20 +1,30 @@
 #!/usr/bin/env python
-"""Benchmark: end-to-end ANCKA clustering of a DBLP-shaped attributed
-hypergraph (BASELINE.json configs[1]) on B200, beside the CPU reference path.
+"""Benchmark: end-to-end ANCKA clustering of the Amazon2M-shaped attributed
+graph (BASELINE.json configs[3]: 2.45M nodes, 61.9M edges, 100-dim
+continuous attributes, k=47) on B200, beside the reference CPU path.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload amazon2m|magpm|dblp|...] [--extra magpm,dblp]
 
-A step is one full `run_ancka` pipeline (exact KNN -> KNN graph -> operator
--> greedy init -> orthogonal iterations with discretisation and MHC until the
-reference's stop rules fire) on a synthetic n=41,302 / m=22,363 / d=1,425
-binary-attribute hypergraph with k=6, K=10.
+A step is one full clustering (`run_prepared`): exact KNN -> KNN graph ->
+walk operator -> greedy init -> orthogonal iterations with discretisation
+and MHC until the reference's stop rules fire (engine.py:343-437), K=10,
+knn_mode EXACT, reference defaults otherwise.
 
-`value` = seconds per clustering with attributes and structural factors
-already resident in HBM (CUDA events on the launching stream, max over
-ranks, L2 flushed before every timed step); `e2e` = the same through the
-public API `run_ancka(net, params)` from host numpy/scipy inputs (validation,
-host->device copies and the label read-back inside the timed region).
-Multi-GPU runs are independent replicas (DBLP fits one GPU).
+* `value`  seconds per clustering with the attributes and the structure
+  resident in HBM (CUDA events on the launching stream, max over ranks;
+  the inputs -- 2 GB of attributes, 1.5 GB of CSR -- and every iterate
+  exceed the 126 MB L2, and a 256 MiB buffer is written before each step).
+* `e2e`    the same through the public API `run_ancka(net, params)` from
+  host numpy/scipy inputs: host validation, host->device copies of X and
+  the structure, and the label read-back inside the timed region.
+* N > 1 (torchrun, NCCL): the row-partitioned path `dist.run_ancka_dist`
+  on the same instance, strong scaling (one clustering over N GPUs).
+* `cpu_baseline` / `--impl reference`: the reference algorithm (the pinned
+  numpy/scipy restatement in oracle/) timed per kernel on the host cores
+  on a bounded sample of the same instance and assembled into a full-run
+  estimate with this run's kernel counts (oracle/cpu_sample.py,
+  BASELINE.md §4); exact KNN is extrapolated from a query-row sample.
 """
 from __future__ import annotations
 
@@ -33,17 +43,29 @@ sys.path.insert(0, str(ROOT))
 warnings.simplefilter("ignore")
 
 METRIC = "end-to-end clustering seconds + KNN build s; SpMM HBM GB/s at 1/2/4/8 B200 vs CPU"
-SHAPE = "dblp"
+DEFAULT_WORKLOAD = "amazon2m"
+DEFAULT_EXTRA = "magpm"
+COUNTS_FILE = ROOT / "profiles" / "run_counts.json"
+# kernel counts of the GPU run used by --impl reference when no counts file
+# is present (iterations, discretisation calls, rounds; seed 0, r02 runs)
+FALLBACK_COUNTS = {"amazon2m": {"iterations": 195, "disc_calls": 39, "disc_rounds": 1560},
+                   "magpm": {"iterations": 45, "disc_calls": 9, "disc_rounds": 360},
+                   "dblp": {"iterations": 85, "disc_calls": 17, "disc_rounds": 680}}
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--extra", default=DEFAULT_EXTRA,
+                    help="comma list of further single-GPU workloads reported under 'extra'")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--write-counts", action="store_true",
+                    help="store this run's kernel counts for --impl reference")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -55,17 +77,36 @@ def dist_env():
     return ws, rank, local
 
 
-def make_instance(seed):
+def make_instance(name, seed):
     from paper_2408_05459_b200 import synth
-    return synth.make(SHAPE, seed=seed)
+    return synth.make(name, seed=seed)
 
 
-def workload_config(inst, K):
-    return {"workload": f"synthetic {SHAPE.upper()}-shaped attributed hypergraph",
-            "n": int(inst.structure.shape[1]), "m": int(inst.structure.shape[0]),
-            "d": int(inst.X.shape[1]), "attributes": "binary bag-of-words (CSR)",
-            "k": int(inst.k), "knn_k": K, "alpha": 0.2, "beta": 0.5, "gamma": 3, "tau": 5,
-            "t_a": 1000, "knn_mode": "exact", "l2": "flushed (256 MiB write) before each timed step"}
+def make_net(inst):
+    import paper_2408_05459_b200 as ancka
+    if inst.kind == "hypergraph":
+        return ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
+    return ancka.AttributedNetwork.graph(inst.structure, inst.X)
+
+
+def workload_config(name, inst, K):
+    from paper_2408_05459_b200 import synth
+    kind = synth.SHAPES[name][0]
+    s = inst.structure
+    cfg = {"workload": f"synthetic {name}-shaped attributed {kind} (BASELINE.json configs)",
+           "n": int(inst.X.shape[0]), "d": int(inst.X.shape[1]),
+           "attributes": "binary bag-of-words (CSR)" if synth.SHAPES[name][5] == "binary"
+           else "continuous |N(mu_block, I)| (dense)",
+           "k": int(inst.k), "knn_k": K, "alpha": 0.2, "beta": 0.5, "gamma": 3, "tau": 5,
+           "t_a": 1000, "t_i": 25, "knn_mode": "exact"}
+    if kind == "hypergraph":
+        cfg |= {"m": int(s.shape[0]), "nnz_H": int(s.nnz)}
+    else:
+        cfg |= {"edges": int(s.nnz // 2), "nnz_A": int(s.nnz)}
+    big = inst.X.shape[0] * (inst.k + 1) * 4 > 126e6
+    cfg["l2"] = ("inputs and iterates exceed L2 (126 MB); " if big else "") + \
+        "256 MiB written (L2 flush) before each timed step"
+    return cfg
 
 
 # ------------------------------------------------------------------ clocks --
@@ -84,7 +125,7 @@ try:
         r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
         print(",".join([str(sm), str(mx)] + ["Active" if r & b else "Not Active" for b in bits]),
               flush=True)
-        time.sleep(0.05)
+        time.sleep(0.1)
 except Exception as exc:
     print("ready", flush=True)
     print("error", exc, flush=True)
@@ -93,8 +134,7 @@ except Exception as exc:
 
 class ClockSampler:
     """SM clocks and clock-event (throttle) reasons sampled by NVML in a
-    separate process during the timed region: no thread of the benchmark
-    process competes for its interpreter lock while kernels are enqueued."""
+    separate process during the timed region."""
 
     def __init__(self, index=0):
         self.index, self.samples, self._p = index, [], None
@@ -102,7 +142,7 @@ class ClockSampler:
     def __enter__(self):
         self._p = subprocess.Popen([sys.executable, "-c", _SAMPLER, str(self.index)],
                                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        self._p.stdout.readline()            # wait until NVML is initialised
+        self._p.stdout.readline()
         return self
 
     def __exit__(self, *exc):
@@ -116,7 +156,7 @@ class ClockSampler:
     def summary(self):
         import numpy as np
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -131,80 +171,81 @@ def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
-    return 6650.0, 1590.0, "fallback"
+        return (d.get("hbm_gbs", 6530.0), d.get("bf16_tflops", 1652.1),
+                d.get("bf16_tflops_sustained", 1389.8), "measured (MEASURED_PEAKS.json)")
+    return 6530.0, 1652.1, 1389.8, "fallback (B200_PROFILING.md)"
 
 
 # --------------------------------------------------------------- CPU side --
-def cpu_threads():
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+def load_counts(name):
+    if COUNTS_FILE.exists():
+        d = json.loads(COUNTS_FILE.read_text())
+        if name in d:
+            return d[name], f"kernel counts of the GPU run recorded in {COUNTS_FILE.name}"
+    if name in FALLBACK_COUNTS:
+        return FALLBACK_COUNTS[name], "kernel counts of the round-2 GPU run (bench.py defaults)"
+    return ({"iterations": 1000, "disc_calls": 200, "disc_rounds": 8000},
+            "no recorded GPU run: the reference's t_a = 1000 iterations, 40 rounds per call")
 
 
-def oracle_run(inst, seed):
-    from threadpoolctl import threadpool_limits
-
-    from oracle import ancka_cpu as oc
-    with threadpool_limits(limits=cpu_threads()):
-        t0 = time.perf_counter()
-        res = oc.run({"kind": inst.kind, "S": inst.structure, "X": inst.X}, inst.k, knn_k=10,
-                     seed=seed)
-        return time.perf_counter() - t0, res
-
-
-def per_call(tm, calls):
-    """Per-kernel timings: one orthogonal step (apply + QR),
-    one discretisation, one MHC."""
-    return {"ortho_step": round(tm["ortho_ms"] / max(calls["ortho"], 1), 4),
-            "discretize": round(tm["discretize_ms"] / max(calls["discretize"], 1), 4),
-            "mhc": round(tm["mhc_ms"] / max(calls["mhc"], 1), 4)}
+def cpu_estimate(name, inst, counts, row_frac, knn_rows):
+    from oracle import cpu_sample as cs
+    t0 = time.perf_counter()
+    tm = cs.sample_timings(inst, 10, row_frac=row_frac, knn_rows=knn_rows)
+    wall = time.perf_counter() - t0
+    est = cs.full_run_estimate(tm, counts)
+    n = inst.X.shape[0]
+    rows_txt = "all rows" if row_frac >= 1 else f"{tm['rows']} sampled rows scaled to n"
+    sample = (f"reference kernels (numpy/scipy restatement, oracle/ancka_cpu.py) on the {name} "
+              f"instance: exact KNN on {knn_rows} query rows x all {n} keys extrapolated x n/"
+              f"{knn_rows}; one joint apply, one Householder QR, one rounding round and one "
+              f"prototype start on {rows_txt}; assembled with "
+              f"{counts['iterations']} iterations, {counts['disc_calls']} discretisations "
+              f"({counts['disc_rounds']} rounds), {counts['disc_calls'] + 1} MHC evaluations")
+    per_kernel = {k: round(v, 4) for k, v in tm.items() if k.endswith("_s")}
+    return est, wall, sample, per_kernel
 
 
 def run_reference(args):
-    """--impl reference: the reference algorithm (oracle port) on the host."""
+    """--impl reference: the reference algorithm on the host cores, full-size
+    per-kernel timings on the workload, assembled into one clustering."""
+    from oracle import cpu_sample as cs
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    inst = make_instance(args.seed)
-    oracle_run(make_small(), 0)                     # warm-up: imports, page-in
-    steps = max(1, min(args.steps, 2))          # ~100 s per full CPU clustering
-    times = [oracle_run(inst, args.seed)[0] for _ in range(steps)]
-    v = sum(times) / len(times)
-    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": "s",
-            "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": round(v * 1e3, 2),
-            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(inst, 10),
-            "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": cpu_threads(),
-                             "kind": "port",
-                             "sample": f"full {SHAPE}-shaped clustering with the numpy/scipy "
-                                       f"restatement of the reference (oracle/ancka_cpu.py), "
-                                       f"{steps} timed run(s), BLAS threads = all host cores"},
-            "e2e": {"value": round(v, 4), "unit": "s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+    name = args.workload
+    inst = make_instance(name, args.seed)
+    counts, counts_src = load_counts(name)
+    from paper_2408_05459_b200 import synth
+    cs.sample_timings(synth.make(name, seed=1, n=20000), 10, row_frac=1.0, knn_rows=20)  # warm-up
+    steps = 1                      # one step = the whole bounded sample (~3 min)
+    ests, walls = [], []
+    for _ in range(steps):
+        est, wall, sample, per_kernel = cpu_estimate(name, inst, counts, 1.0, 1000)
+        ests.append(est)
+        walls.append(wall)
+    v = sum(ests) / len(ests)
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 2), "unit": "s",
+            "n_gpus": args.gpus, "steps": steps, "warmup": 1, "ms_per_step": round(v * 1e3, 1),
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(name, inst, 10),
+            "cpu_baseline": {"value": round(v, 2), "unit": "s", "cores": cs.cores(), "kind": "port",
+                             "sample": sample + f" ({counts_src})", "extrapolated": True,
+                             "per_kernel_s": per_kernel, "sample_wall_s": round(walls[0], 1)},
+            "e2e": {"value": round(v, 2), "unit": "s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "note": "steps capped at 1: one step is the full bounded sample; "
+                    "value = estimated seconds of one reference clustering"}
     print(json.dumps(line), flush=True)
 
 
-def make_small():
-    from paper_2408_05459_b200 import synth
-    return synth.make(SHAPE, seed=1, n=1500)
-
-
 # -------------------------------------------------------------- GPU side --
-def spmm_gbytes_model(op, c, nnz_k):
-    """SURVEY.md §8(d) hypergraph gather model (bytes per operator apply)."""
-    n, m = op.n, op.m
-    nnz_h = op._f["p_e"].nnz
-    return (4 * nnz_h + 12 * m + 4 * c * nnz_h + 4 * m * c) + \
-           (4 * nnz_h + 8 * nnz_k + 16 * n + 8 * n + 4 * c * (nnz_h + nnz_k) + 4 * n * c)
-
-
-def time_kernel(fn, reps):
+def time_events(fn, reps, warm=1):
     import torch
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    fn()
+    for _ in range(warm):
+        fn()
     torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
     for _ in range(reps):
         fn()
@@ -213,184 +254,306 @@ def time_kernel(fn, reps):
     return s.elapsed_time(e) / reps
 
 
-def run_ours(args):
+def gather_model_bytes(op, c):
+    """SURVEY.md §8(d) gather model: bytes per f32 joint apply."""
+    n = op.n
+    nnz_k = int(op.p_k_dev.nnz)
+    if op.m:                                   # hypergraph, two passes
+        nnz_h = int(op._f["p_e"].nnz)
+        m = op.m
+        return ((4 * nnz_h + 12 * m + 4 * c * nnz_h + 4 * m * c) +
+                (4 * nnz_h + 8 * nnz_k + 16 * n + 8 * n + 4 * c * (nnz_h + nnz_k) + 4 * n * c))
+    nnz_a = int(op._f["p_n"].nnz)
+    return (4 * nnz_a + 8 * nnz_k + 16 * (n + 1) + 8 * n + 4 * c * (nnz_a + nnz_k) + 4 * n * c)
+
+
+def kernel_rooflines(prep, res, inst, hbm, bf16):
+    """Live per-kernel rooflines (CUDA events on the library's stream, after
+    warm-up): KNN (tensor), joint apply and CholQR (HBM), discretisation."""
+    import numpy as np
+    import torch
+
+    from paper_2408_05459_b200 import _lib, engine
+    from paper_2408_05459_b200._device import WORKSPACE, ld_for
+    from paper_2408_05459_b200.knn import knn_search_exact_device
+
+    out = {}
+    n, d = inst.X.shape
+    K = prep.K
+    knn_ms = time_events(lambda: knn_search_exact_device(prep.x_dev, K, integer=prep.x_level), 1)
+    flops = 2.0 * n * n * d
+    fp8 = prep.x_level == 2
+    peak = 4500.0 if fp8 else bf16
+    out["knn"] = {"kernel": ("knn_tc_kernel (tcgen05 kind::f8f6f4, exact integer)" if fp8 else
+                             "knn_real_res_kernel (tcgen05 split-bf16) + certified f64 re-rank"),
+                  "bound": "tensor", "achieved": round(flops / (knn_ms * 1e-3) / 1e12, 1),
+                  "peak": peak, "unit": "TFLOP/s",
+                  "frac": round(flops / (knn_ms * 1e-3) / 1e12 / peak, 4),
+                  "algorithmic": f"2*n^2*d = {flops:.4e} FLOP per search",
+                  "duration_ms": round(knn_ms, 2),
+                  "peak_source": ("nominal dense fp8 4.5 PFLOP/s (B200_PROFILING.md; no measured fp8 peak)"
+                                  if fp8 else "measured bf16 burst (MEASURED_PEAKS.json)"),
+                  "timed": "whole ancka_knn_exact call (all kernels of the search)"}
+    op = res.operator
+    c = inst.k + 1
+    ld = ld_for(c, torch.float32)
+    Q = torch.randn((n, ld), dtype=torch.float32, device="cuda")
+    Q[:, c:] = 0
+    Z = torch.empty_like(Q)
+    Q2 = torch.empty_like(Q)
+    s32 = op.struct(_lib.F32)
+    scr = op.scratch(c, torch.float32)
+    st = _lib.stream
+    apply_ms = time_events(lambda: _lib.call("ancka_op_apply", s32, Q.data_ptr(), ld, c,
+                                             Z.data_ptr(), ld, scr.data_ptr(), st()), 10)
+    b_op = gather_model_bytes(op, c)
+    nnz_struct = int(op._f["p_e"].nnz) if op.m else int(op._f["p_n"].nnz)
+    out["spmm"] = {"kernel": "spmm_kernel<float> (joint walk apply, f32)", "bound": "hbm",
+                   "achieved": round(b_op / (apply_ms * 1e-3) / 1e9, 1), "peak": hbm,
+                   "unit": "GB/s", "frac": round(b_op / (apply_ms * 1e-3) / 1e9 / hbm, 4),
+                   "algorithmic": f"gather model {b_op} B per apply (SURVEY.md §8(d))",
+                   "compulsory_bytes": int(4 * n * c * 2 + 12 * (nnz_struct + op.p_k_dev.nnz)),
+                   "duration_ms": round(apply_ms, 3), "peak_source": "measured HBM copy"}
+    stats = torch.tensor([0.0, 1.0, 0.0, 0.0] + [0.0] * 12, dtype=torch.float64, device="cuda")
+    ws = WORKSPACE.get("orth", _lib.load().ancka_orth_workspace_size(s32, c))
+    G = torch.empty(c * (c + 1) // 2, dtype=torch.float64, device="cuda")
+
+    def qr():
+        _lib.call("ancka_gram_f32", Z.data_ptr(), n, ld, c, G.data_ptr(), ws.data_ptr(),
+                  ws.numel(), st())
+        _lib.call("ancka_cholqr_apply_f32", Z.data_ptr(), Q.data_ptr(), Q2.data_ptr(), n, ld, c,
+                  G.data_ptr(), stats.data_ptr(), ws.data_ptr(), ws.numel(), st())
+    qr_ms = time_events(qr, 10)
+    b_qr = 12 * n * c
+    out["cholqr"] = {"kernel": "gram + cholesky + R^-1 apply (f32 data, f64 Gram)",
+                     "bound": "hbm", "achieved": round(b_qr / (qr_ms * 1e-3) / 1e9, 1),
+                     "peak": hbm, "unit": "GB/s",
+                     "frac": round(b_qr / (qr_ms * 1e-3) / 1e9 / hbm, 4),
+                     "algorithmic": f"12nc = {b_qr} B per QR", "duration_ms": round(qr_ms, 3)}
+    k = inst.k
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    info = torch.zeros(8 + 2 * 100 + 2 * k * k, dtype=torch.float64, device="cuda")
+    Qd = res.state.q_dev
+    disc_ms = time_events(lambda: engine._discretize_device(Qd, 1, k, 100, 1e-10, lab, info), 2)
+    rounds = int(info[6].item() + info[7].item())
+    b_round = 4 * n * k + 4 * n
+    out["discretize"] = {"kernel": "discretize_kernel (both starts, cooperative)", "bound": "hbm",
+                         "achieved": round(rounds * b_round / (disc_ms * 1e-3) / 1e9, 1),
+                         "peak": hbm, "unit": "GB/s",
+                         "frac": round(rounds * b_round / (disc_ms * 1e-3) / 1e9 / hbm, 4),
+                         "algorithmic": f"{rounds} rounds x (4nk + 4n = {b_round} B)",
+                         "duration_ms": round(disc_ms, 3)}
+    return out
+
+
+def _phase_roofline(rooflines, phases, step_ms):
+    """The headline roofline: the kernel family with the largest share."""
+    fam = {"knn_ms": "knn", "ortho_ms": "spmm", "discretize_ms": "discretize", "mhc_ms": "spmm"}
+    dom = max(("knn_ms", "ortho_ms", "discretize_ms", "mhc_ms"), key=lambda k: phases.get(k, 0))
+    r = dict(rooflines[fam[dom]])
+    r["share_of_step"] = round(phases.get(dom, 0.0) / step_ms, 3)
+    r["phase"] = dom
+    r["traffic"] = _traffic(r["kernel"])
+    return r
+
+
+def _traffic(kernel_name):
+    tf = ROOT / "profiles" / "traffic.json"
+    if not tf.exists():
+        return None
+    d = json.loads(tf.read_text())
+    for key, v in d.items():
+        if key.split(":")[0] in kernel_name and isinstance(v, (int, float)):
+            return v
+    return None
+
+
+def timed_steps(fn, steps, warmup, barrier, flush, clocks=None):
+    """W untimed steps, then exactly K steps bracketed by barrier + sync,
+    each timed with CUDA events; NVML clocks sampled over the K steps."""
+    import numpy as np
+    import torch
+    for _ in range(max(warmup, 3)):
+        fn()
+    barrier()
+    ms, res = [], None
+    gc.disable()
+    if clocks is not None:
+        clocks.__enter__()
+    try:
+        for _ in range(steps):
+            flush.fill_(1.0)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            res = fn()
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+    finally:
+        if clocks is not None:
+            clocks.__exit__(None, None, None)
+        gc.enable()
+    barrier()
+    return float(np.mean(ms)), ms, res
+
+
+def run_single_gpu(name, args, with_e2e, with_cpu, steps, warmup, clocks=None):
+    """One workload on one GPU: device-timed steps, rooflines, e2e, CPU sample."""
+    import numpy as np
+    import torch
+
+    import paper_2408_05459_b200 as ancka
+
+    hbm, bf16, _, _ = peaks()
+    inst = make_instance(name, args.seed)
+    net = make_net(inst)
+    params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=args.seed, knn_mode=ancka.KnnMode.EXACT)
+    prep = ancka.prepare_network(net, params)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    launches = [0]
+
+    def step():
+        r = ancka.run_prepared(prep, params)
+        launches[0] += r.gpu_launches
+        return r
+    step_ms, all_ms, res = timed_steps(step, steps, warmup, torch.cuda.synchronize, flush, clocks)
+    launches_timed = launches[0]
+    phases = {k: round(v, 2) for k, v in res.timings_ms.items()}
+    counts = {"iterations": int(res.iterations), "disc_calls": len(res.disc_rounds),
+              "disc_rounds": int(sum(res.disc_rounds))}
+    roof = kernel_rooflines(prep, res, inst, hbm, bf16)
+    out = {"value": step_ms / 1e3, "step_ms": [round(x, 2) for x in all_ms],
+           "ms_per_step": round(step_ms, 2), "phases_ms": phases,
+           "iterations": res.iterations, "stop_reason": res.stop_reason, "counts": counts,
+           "knn_build_s": round(res.timings_ms["knn_ms"] / 1e3, 4),
+           "spmm_hbm_gbs": roof["spmm"]["achieved"], "rooflines": roof,
+           "roofline": _phase_roofline(roof, phases, step_ms),
+           "gpu_launches": launches_timed, "config": workload_config(name, inst, prep.K)}
+    try:
+        from sklearn.metrics import adjusted_rand_score
+        out["ari_vs_planted"] = round(float(adjusted_rand_score(inst.labels, res.y.assignment)), 4)
+    except Exception:
+        pass
+    del res
+    if with_e2e:
+        e2e_t, r2 = [], None
+        ancka.run_ancka(net, params)                     # warm-up of the host path
+        for _ in range(3):
+            torch.cuda.synchronize()
+            gc.collect()
+            t0 = time.perf_counter()
+            r2 = ancka.run_ancka(net, params)
+            lab = r2.y.assignment                          # labels on the host
+            torch.cuda.synchronize()
+            e2e_t.append(time.perf_counter() - t0)
+        out["e2e"] = {"value": round(float(np.median(e2e_t)), 4), "unit": "s",
+                      "h2d_bytes_per_step": prep.h2d_bytes(inst.X),
+                      "d2h_bytes_per_step": int(lab.size * 4 + 8 * 13 * (r2.iterations // 5 + 2)),
+                      "runs_s": [round(x, 4) for x in e2e_t],
+                      "note": "median of 3 wall-clock run_ancka(net, params) calls from host "
+                              "numpy/scipy inputs: validation, pageable H2D copies, labels D2H"}
+        del r2
+    if with_cpu:
+        est, wall, sample, per_kernel = cpu_estimate(name, inst, counts, 1.0 / 16, 100)
+        out["cpu_baseline"] = {"value": round(est, 1), "unit": "s", "cores": _cores(),
+                               "kind": "port", "sample": sample, "extrapolated": True,
+                               "per_kernel_s": per_kernel, "sample_wall_s": round(wall, 1)}
+    if args.write_counts:
+        d = json.loads(COUNTS_FILE.read_text()) if COUNTS_FILE.exists() else {}
+        d[name] = counts
+        COUNTS_FILE.write_text(json.dumps(d, indent=1) + "\n")
+    torch.cuda.empty_cache()
+    return out
+
+
+def _cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_multi_gpu(args, ws, rank, local):
+    """N > 1: row-partitioned clustering over NCCL (strong scaling)."""
     import numpy as np
     import torch
     import torch.distributed as dist
 
     import paper_2408_05459_b200 as ancka
-    from paper_2408_05459_b200 import _lib
-    from paper_2408_05459_b200._device import padded
-    from paper_2408_05459_b200.knn import knn_search_exact_device
+    from paper_2408_05459_b200 import dist as adist
 
-    ws, rank, local = dist_env()
-    torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    _lib.require_device()
-
-    inst = make_instance(args.seed + rank)
-    net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
-    params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=args.seed + rank,
-                                 knn_mode=ancka.KnnMode.EXACT)
-    prep = ancka.prepare_network(net, params)
+    name = args.workload
+    inst = make_instance(name, args.seed)
+    net = make_net(inst)
+    params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=args.seed, knn_mode=ancka.KnnMode.EXACT)
+    B = adist.CudaBackend()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
-        if ws > 1:
-            dist.barrier()
+        dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(args.warmup, 3)):
-        res = ancka.run_prepared(prep, params)
-    barrier()
-    step_ms, launches, results = [], 0, []
-    with ClockSampler(local) as clocks:
-        barrier()
-        gc.disable()                          # no collector pauses inside timed steps
-        for _ in range(args.steps):
-            flush.fill_(1.0)
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            res = ancka.run_prepared(prep, params)
-            b.record()
-            b.synchronize()
-            step_ms.append(a.elapsed_time(b))
-            launches += res.gpu_launches
-            results = [res]                   # keep one: retained device buffers would
-                                              # force fresh allocations inside timed steps
-        gc.enable()
-        barrier()
-    t_step = float(np.mean(step_ms))
-    if ws > 1:
-        tt = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
-    value = t_step / 1e3 / ws          # seconds per clustering across the job
-
-    # ---- per-kernel rooflines (live, CUDA events on the launching stream)
-    hbm, bf16, src = peaks()
-    res = results[-1]
-    n, d = inst.X.shape
-    K = prep.K
-    knn_ms = time_kernel(lambda: knn_search_exact_device(prep.x_dev, K, integer=prep.x_level), 3)
-    knn_flops = 2.0 * n * n * d
-    fp8 = prep.x_level == 2
-    tc_peak = 4500.0 if fp8 else bf16
-    tc_peak_src = ("nominal fp8 dense, B200_PROFILING.md (no measured fp8 peak)" if fp8
-                   else f"{src} bf16 burst, MEASURED_PEAKS.json")
-    op = res.operator
-    c = inst.k + 1
-    q = padded(torch.randn(n, c, dtype=torch.float64), torch.float32)
-    z = torch.empty_like(q)
-    scr = op.scratch(c, torch.float32)
-    s32 = op.struct(_lib.F32)
-
-    def apply():
-        _lib.call("ancka_op_apply", s32, q.data_ptr(), q.stride(0), c, z.data_ptr(),
-                  z.stride(0), scr.data_ptr(), _lib.stream())
-    spmm_ms = time_kernel(apply, 50)
-    spmm_bytes = spmm_gbytes_model(op, c, op.p_k_dev.nnz)
-    phases = {k: round(v, 3) for k, v in res.timings_ms.items()}
-    gpu_calls = {"ortho": res.iterations, "discretize": res.iterations // 5,
-                 "mhc": res.iterations // 5 + 1}
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
-        traffic = json.loads(tf.read_text()).get("knn_tc_kernel_dram_bytes")
-    roofline = {"kernel": "knn_tc_kernel (tcgen05 exact KNN, fp8 e4m3)" if fp8 else "knn",
-                "bound": "tensor", "achieved": round(knn_flops / (knn_ms * 1e-3) / 1e12, 2),
-                "peak": tc_peak, "unit": "TFLOP/s",
-                "frac": round(knn_flops / (knn_ms * 1e-3) / 1e12 / tc_peak, 4),
-                "traffic": traffic, "peak_source": tc_peak_src,
-                "algorithmic": f"2*n^2*d = {knn_flops:.3e} FLOP per launch",
-                "duration_ms": round(knn_ms, 3)}
-    spmm = {"kernel": "spmm_kernel<float> (hypergraph P_E then P_V+P_K stage)", "bound": "hbm",
-            "achieved": round(spmm_bytes / (spmm_ms * 1e-3) / 1e9, 1), "peak": hbm,
-            "unit": "GB/s", "frac": round(spmm_bytes / (spmm_ms * 1e-3) / 1e9 / hbm, 4),
-            "algorithmic": f"gather model {spmm_bytes} B per apply (SURVEY.md §8(d))",
-            "duration_ms": round(spmm_ms, 4), "peak_source": f"{src} HBM copy"}
-
-    # fused orthogonal block (tau = 5 steps per launch): SpMM gather model +
-    # CholQR 12 n c bytes per step
-    from paper_2408_05459_b200 import engine as eng
-    loop = eng._Loop(op, c, inst.k, 5, True, True)
-    loop.Q[0][:, :c] = torch.randn(n, c, device="cuda")
-    orth_ms = time_kernel(lambda: loop.run(5), 5)
-    orth_bytes = 5 * (spmm_bytes + 12 * n * c)
-    orth_traffic = None
-    if tf.exists():
-        per_step = json.loads(tf.read_text()).get("orth_fused_kernel_dram_bytes_per_step")
-        orth_traffic = None if per_step is None else 5 * per_step
-    orth = {"kernel": "orth_fused_kernel (cooperative: 5 x [SpMM + Gram + Cholesky + R^-1 apply])",
-            "bound": "hbm", "achieved": round(orth_bytes / (orth_ms * 1e-3) / 1e9, 1),
-            "peak": hbm, "unit": "GB/s",
-            "frac": round(orth_bytes / (orth_ms * 1e-3) / 1e9 / hbm, 4), "traffic": orth_traffic,
-            "algorithmic": f"5 x (gather model {spmm_bytes} B + 12nc = {12 * n * c} B) per launch",
-            "duration_ms": round(orth_ms, 4), "peak_source": f"{src} HBM copy",
-            "note": "grid-barrier / latency bound at this size: the working set sits in L2"}
-    # the headline roofline is the kernel family with the largest share of the step
-    share = {"ortho_ms": orth, "knn_ms": roofline}
-    dom = max(share, key=lambda k2: phases.get(k2, 0.0))
-    rooflines = {"orth_fused": orth, "knn_tc": roofline, "spmm": spmm}
-    roofline_main = share[dom] | {"share_of_step": round(phases.get(dom, 0.0) / t_step, 3)}
-
-    # ---- end-to-end through the public API from host inputs
-    e2e = None
-    if not args.no_e2e:
-        e2e_t = []
-        ancka.run_ancka(net, params)          # untimed warm-up of the host path
-        for _ in range(5):
-            barrier()
-            gc.collect()
-            t0 = time.perf_counter()
-            r2 = ancka.run_ancka(net, params)
-            lab = r2.y.assignment  # host labels
-            torch.cuda.synchronize()
-            e2e_t.append(time.perf_counter() - t0)
-        te = float(np.median(e2e_t))
-        if ws > 1:
-            tt = torch.tensor([te], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt.item())
-        if os.environ.get("ANCKA_BENCH_DEBUG"):
-            print("e2e runs (s):", [round(x, 4) for x in e2e_t], "last timings:", r2.timings_ms,
-                  file=sys.stderr)
-        e2e = {"value": round(te / ws, 4), "unit": "s",
-               "h2d_bytes_per_step": prep.h2d_bytes(inst.X),
-               "d2h_bytes_per_step": int(lab.size * 4 + 8 * 4 * (r2.iterations // 5 + 2)),
-               "runs_s": [round(x, 4) for x in e2e_t],
-               "note": "median of 5 host wall-clock runs of run_ancka(net, params) incl. host "
-                       "validation, pageable H2D uploads and the label read-back"}
-
-    cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        t_cpu, ref = oracle_run(inst, args.seed)
-        from sklearn.metrics import adjusted_rand_score
-        cpu = {"value": round(t_cpu, 3), "unit": "s", "cores": cpu_threads(), "kind": "port",
-               "sample": f"one full {SHAPE}-shaped clustering with the numpy/scipy restatement "
-                         f"of the reference (oracle/ancka_cpu.py), same instance",
-               "ari_vs_gpu": round(float(adjusted_rand_score(ref["labels"], res.y.assignment)), 4),
-               "iterations": ref["iterations"],
-               "phases_ms": {k2: round(v, 1) for k2, v in ref["timings_ms"].items()},
-               "per_call_ms": per_call(ref["timings_ms"], ref["calls"]),
-               "gpu_per_call_ms": per_call(phases, gpu_calls)}
+    def step():
+        return adist.run_ancka_dist(net, params, B)
+    w = max(args.warmup, 3)
+    clocks = ClockSampler(local)
+    step_ms, all_ms, res = timed_steps(step, args.steps, w, barrier, flush, clocks)
+    t = torch.tensor([step_ms], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    step_ms = float(t.item())
     if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 5), "unit": "s", "n_gpus": ws,
-                "steps": args.steps, "warmup": max(args.warmup, 3),
-                "ms_per_step": round(t_step, 3), "step_ms": [round(x, 3) for x in step_ms],
-                "higher_is_better": False, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": workload_config(inst, K) | {"parallelism": f"replicas x{ws}"},
-                "knn_build_s": round(res.timings_ms["knn_ms"] / 1e3, 5),
-                "spmm_hbm_gbs": spmm["achieved"], "roofline": roofline_main,
-                "rooflines": rooflines,
-                "phases_ms": phases, "iterations": res.iterations, "stop_reason": res.stop_reason,
-                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        line = {"metric": METRIC, "value": round(step_ms / 1e3, 4), "unit": "s", "n_gpus": ws,
+                "steps": args.steps, "warmup": w, "ms_per_step": round(step_ms, 2),
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic",
+                "config": workload_config(name, inst, 10) | {"parallelism": f"rows x{ws} (NCCL)"},
+                "iterations": res.iterations, "stop_reason": res.stop_reason,
                 "clocks": clocks.summary()}
         print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_05459_b200 import _lib
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    _lib.require_device()
     if ws > 1:
-        dist.destroy_process_group()
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        try:
+            run_multi_gpu(args, ws, rank, local)
+        finally:
+            dist.destroy_process_group()
+        return
+    name = args.workload
+    clocks = ClockSampler(local)
+    main = run_single_gpu(name, args, not args.no_e2e, not args.no_cpu_baseline,
+                          args.steps, args.warmup, clocks)
+    extra = {}
+    for other in [w for w in args.extra.split(",") if w and w != name]:
+        r = run_single_gpu(other, args, False, False, min(args.steps, 3), 3)
+        extra[other] = {k: r[k] for k in ("value", "ms_per_step", "phases_ms", "iterations",
+                                          "stop_reason", "knn_build_s", "spmm_hbm_gbs",
+                                          "roofline", "rooflines", "config")
+                        if k in r} | {"unit": "s", "ari_vs_planted": r.get("ari_vs_planted")}
+    line = {"metric": METRIC, "value": round(main["value"], 4), "unit": "s", "n_gpus": 1,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": main["ms_per_step"], "step_ms": main["step_ms"],
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": main["config"] | {"parallelism": "single GPU"},
+            "knn_build_s": main["knn_build_s"], "spmm_hbm_gbs": main["spmm_hbm_gbs"],
+            "roofline": main["roofline"], "rooflines": main["rooflines"],
+            "phases_ms": main["phases_ms"], "iterations": main["iterations"],
+            "stop_reason": main["stop_reason"], "ari_vs_planted": main.get("ari_vs_planted"),
+            "counts": main["counts"],
+            "cpu_baseline": main.get("cpu_baseline"), "e2e": main.get("e2e"),
+            "gpu_launches": main["gpu_launches"], "clocks": clocks.summary(),
+            "extra": extra}
+    print(json.dumps(line), flush=True)
 
 
 def main():

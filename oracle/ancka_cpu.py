@@ -119,17 +119,47 @@ def unit_rows(x):
 
 
 def _select_row(sims_row, K):
-    """_ordered_top_k (knn.py:83-98) as one lexicographic sort.
-
-    Order is (value desc, index asc) over strictly positive entries; the
-    first K of that order are exactly the reference's selection (its
-    boundary ties resolve to the smaller index, then a stable sort on -value).
-    """
+    """_ordered_top_k (knn.py:83-98): keep strictly positive entries; above K
+    of them, partition at the K-th largest value, keep everything above it
+    and the smallest-index ties at it; order by a stable sort on -value
+    (so (value desc, index asc)).  Same selection work as the reference
+    (partition, then a sort of K entries), so the CPU arm is timed fairly."""
     pos = np.flatnonzero(sims_row > 0)
-    if pos.size == 0:
-        return pos
-    order = np.lexsort((pos, -sims_row[pos]))
-    return pos[order[:K]]
+    if pos.size > K:
+        vals = sims_row[pos]
+        kth = np.partition(vals, vals.size - K)[vals.size - K]
+        above = pos[vals > kth]
+        ties = pos[vals == kth]
+        pos = np.concatenate([above, ties[: K - above.size]])
+        pos.sort()
+    order = np.argsort(-sims_row[pos], kind="stable")
+    return pos[order]
+
+
+def knn_rows(X, rows, K):
+    """Exact lists of the query rows `rows` against all n keys, the blocked
+    scan of knn.py:112-140 restricted to a row sample (the reference's own
+    sampled form is knn._exact_rows_for, knn.py:227-239).  Used to time the
+    CPU KNN on a bounded sample and to check sampled GPU rows."""
+    xn, nrm = unit_rows(X)
+    n = xn.shape[0]
+    rows = np.asarray(rows, dtype=np.int64)
+    right = xn.T.tocsc() if sp.issparse(xn) else xn.T
+    block = max(16, min(4096, int(2.5e7 // max(n, 1))))
+    ids = np.full((rows.size, K), -1, dtype=np.int64)
+    scores = np.zeros((rows.size, K), dtype=np.float64)
+    for lo in range(0, rows.size, block):
+        chunk = rows[lo: lo + block]
+        blk = xn[chunk] @ right
+        blk = blk.toarray() if sp.issparse(blk) else np.asarray(blk)
+        blk[np.arange(chunk.size), chunk] = -1.0
+        for r in range(chunk.size):
+            if nrm[chunk[r]] == 0.0:
+                continue
+            sel = _select_row(blk[r], K)
+            ids[lo + r, : sel.size] = sel
+            scores[lo + r, : sel.size] = np.minimum(blk[r, sel], 1.0)
+    return ids, scores
 
 
 def knn_exact(X, K, block_rows=None):

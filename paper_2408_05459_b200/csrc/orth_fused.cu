@@ -27,6 +27,13 @@ constexpr int kGW = 4;                      // lanes per regular row / hyperedge
 constexpr int kC = 8;                       // padded block width
 constexpr int kNP = kC * (kC + 1) / 2;      // Gram upper-triangle entries
 constexpr double kFx = 1125899906842624.0;  // 2^50 fixed-point scale of Gram sums
+// Every partial sum of a Gram entry over a subset of rows is bounded by the
+// Gram trace (Cauchy-Schwarz), so a trace below 2^12 keeps all 2^50-scaled
+// int64 accumulators (and every CTA's llrint) in range.  Larger traces (hub
+// rows inflating ||P q||^2) count as a suspect pivot: the host replays the
+// tau-block with the exact f64 step.
+constexpr double kGuardFx = 1048576.0;       // 2^20 scale of the trace guard
+constexpr double kGuardMaxTrace = 4096.0;
 constexpr double kFxInv = 1.0 / 1125899906842624.0;
 
 struct OfParams {
@@ -36,6 +43,7 @@ struct OfParams {
   float* T;                  // m x 8 (hypergraph)
   int c, steps;
   long long* gram_fx;        // 2 x kNP fixed-point Gram accumulators
+  long long* gram_guard;     // 2 x fixed-point (2^20) Gram trace: overflow guard
   double* dq_part;           // grid
   double* stats;             // [0] dq^2 of the last step, [1] min pivot ratio, [2] += bad pivots
   unsigned long long* tdbg;  // optional phase timers (ANCKA_ORTH_TIMING): stats[4..11]
@@ -334,7 +342,13 @@ orth_fused_kernel(OfParams P) {
       double v = 0.0;
       for (int g2 = 0; g2 < kGS; ++g2) v += red[g2 * kNP + qq];
       atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_fx + buf * kNP + qq),
-                (unsigned long long)(long long)llrint(v * kFx));
+                (unsigned long long)(long long)llrint(fmin(fmax(v, -kGuardMaxTrace), kGuardMaxTrace) * kFx));
+      bool diag = false;
+#pragma unroll
+      for (int a2 = 0; a2 < kC; ++a2) diag |= (a2 < P.c && qq == pidx(a2, a2));
+      if (diag)                                  // v >= 0: a sum of squares
+        atomicAdd(reinterpret_cast<unsigned long long*>(P.gram_guard + buf),
+                  (unsigned long long)(long long)llrint(fmin(v, 1e12) * kGuardFx));
     }
     OF_STAMP(2);
     if (P.tdbg) {                        // per-CTA P2 duration: max and sum over CTAs
@@ -352,6 +366,9 @@ orth_fused_kernel(OfParams P) {
     if (threadIdx.x < kNP) G[threadIdx.x] = (double)P.gram_fx[buf * kNP + threadIdx.x] * kFxInv;
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x < kNP) P.gram_fx[(buf ^ 1) * kNP + threadIdx.x] = 0;
+    const double gtrace = (double)P.gram_guard[buf] * (1.0 / kGuardFx);
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.gram_guard[buf ^ 1] = 0;
     if (threadIdx.x == 0) {
       // Cholesky of the padded 8 x 8 Gram (identity on padding), fully
       // unrolled so the factor lives in registers
@@ -363,7 +380,7 @@ orth_fused_kernel(OfParams P) {
           R[a2][b3] = (a2 < P.c && b3 < P.c) ? (a2 <= b3 ? G[pidx(a2, b3)] : 0.0)
                                              : (a2 == b3 ? 1.0 : 0.0);
       double minratio = 1.0;
-      int bad = 0;
+      int bad = gtrace >= kGuardMaxTrace / 2 ? 1 : 0;   // fixed-point range guard
 #pragma unroll
       for (int j = 0; j < kC; ++j) {
         const double gjj = R[j][j];
@@ -724,6 +741,7 @@ extern "C" size_t ancka_orth_block_workspace_size(const ancka_operator* op) {
   Carver cv(nullptr, 0);
   cv.take<float>(op && op->kind == ANCKA_HYPERGRAPH ? (size_t)op->m * kC : 1);
   cv.take<long long>(2 * kNP);
+  cv.take<long long>(2);
   cv.take<double>(of_grid_cap());
   return cv.used;
 }
@@ -746,11 +764,13 @@ extern "C" int ancka_orth_block_f32(const ancka_operator* op32, float* Q0, float
   P.c = c;
   P.steps = steps;
   P.gram_fx = cv.take<long long>(2 * kNP);
+  P.gram_guard = cv.take<long long>(2);
   P.dq_part = cv.take<double>(of_grid_cap());
   P.stats = stats;
   P.tdbg = getenv("ANCKA_ORTH_TIMING") ? reinterpret_cast<unsigned long long*>(stats + 4) : nullptr;
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "orth_block: workspace too small");
   ANCKA_CUDA(cudaMemsetAsync(P.gram_fx, 0, sizeof(long long) * 2 * kNP, as_stream(stream)));
+  ANCKA_CUDA(cudaMemsetAsync(P.gram_guard, 0, sizeof(long long) * 2, as_stream(stream)));
   int per_sm = 0, dev = 0, sms = 0;
   ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, orth_fused_kernel, kOfThreads, 0));
   ANCKA_CUDA(cudaGetDevice(&dev));

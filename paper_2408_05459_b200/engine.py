@@ -517,6 +517,24 @@ def repair_empty_clusters(y: BcmMatrix, scores: np.ndarray) -> BcmMatrix:
     return BcmMatrix(assignment=a, k=y.k)
 
 
+def _repair_missing_columns(q32: torch.Tensor, kd: int, k: int, labels: torch.Tensor,
+                            info: torch.Tensor) -> None:
+    """k == n: the discretised block has kd = n - 1 < k columns, so clusters
+    kd..k-1 are empty and repair_empty_clusters (engine.py:266-288) fills them
+    from the winning run's final scores.  Degenerate (tiny n) case: the scores
+    are rebuilt on the host from the winning rotation the kernel reports."""
+    inf = info.cpu().numpy()
+    win = int(inf[3])
+    base = 8 + 2 * DISCRETIZE_MAX_ITER + win * kd * kd
+    rot = inf[base: base + kd * kd].reshape(kd, kd)
+    q = q32[:, 1:1 + kd].double().cpu().numpy()
+    nrm = np.linalg.norm(q, axis=1)
+    qt = np.divide(q, nrm[:, None], out=np.zeros_like(q), where=nrm[:, None] > 0)
+    y = BcmMatrix(assignment=labels.cpu().numpy().astype(np.int64), k=k)
+    y = repair_empty_clusters(y, qt @ rot)
+    labels.copy_(torch.from_numpy(y.assignment.astype(np.int32)))
+
+
 # ---------------------------------------------------------------- MHC -------
 class _MhcRunner:
     def __init__(self, op: WalkOperator, k: int, dtype: int):
@@ -804,12 +822,20 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         host_rb0 = torch.empty(1, dtype=torch.float64, pin_memory=True)
         rb_ready = torch.cuda.Event()
 
+        # discretize(state.q[:, 1:]) sees c - 1 columns: fewer than k only in
+        # the degenerate k == n case (engine.py:370-371, 392-394)
+        kd = c - 1
+
         def sample_issue(t_now, dq_first):
             # loop.stats = [dq^2, min pivot ratio, suspect pivots, phi]: one
             # read-back per sample next to the discretisation info
+            if kd < 1:
+                raise NetworkError("discretize expects an n x k block with k >= 1")
             qt = loop.q
             with timer.span("discretize_ms"):
-                _discretize_device(qt, 1, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
+                _discretize_device(qt, 1, kd, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
+                if kd < k:
+                    _repair_missing_columns(qt, kd, k, lab_t, info)
             with timer.span("mhc_ms"):
                 mhc(lab_t, loop.stats[3:4])
             if dq_first is not None:
@@ -835,6 +861,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             return sample_collect()
 
         Qsave_prev = torch.empty_like(loop.Qsave)
+        disc_rounds = []            # rounds (both starts) of every discretisation
 
         spec = None
         try:
@@ -893,6 +920,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                         with timer.span("ortho_ms"):
                             loop.replay_exact(rng)
                         inf, (phi, dq2, nbad) = sample(t_done, None)
+                    disc_rounds.append(int(inf[6]) + int(inf[7]))
                     if inf[5] > 0:
                         warnings.warn(f"{int(inf[5])} all-zero row(s); assigning to cluster 0")
                     if inf[4] > 0:
@@ -943,6 +971,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                         stop_reason=stop_reason, warnings=caught, error=error)
     # kernels of this library executed by the run (graph captures excluded,
     # graph replays included)
+    res.disc_rounds = disc_rounds
     res.gpu_launches = int(_lib.load().ancka_launch_count() - launches0 - loop.captured
                            + loop.replayed)
     return res

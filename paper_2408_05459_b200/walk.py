@@ -318,8 +318,64 @@ def apply_structure_rowvec(op: WalkOperator, m):
 
 
 def apply_structure(op: WalkOperator, m):
-    """Structural transition times a block (walk.py:135-150): the joint apply
-    with beta = 0 is not exposed separately on the device; provided for API
-    completeness via a beta-free operator view."""
-    raise NetworkError("apply_structure is internal to the fused device operator; "
-                       "use apply_joint_transition")
+    """Structural transition times a block (walk.py:135-150): P_N M (graph),
+    P_V (P_E M) (hypergraph) or the layer average (multiplex), plus M on the
+    self-loop rows.  Runs the same device apply as apply_joint_transition on
+    a view of the operator whose beta is zero, so (1 - 0) struct + 0 attr is
+    exactly the structural product."""
+    return _apply(_structure_view(op), m, transposed=False)
+
+
+def _structure_view(op: WalkOperator) -> WalkOperator:
+    view = op.__dict__.get("_structure_only")
+    if view is None:
+        import copy
+        view = copy.copy(op)
+        view.beta64 = torch.zeros_like(op.beta64)
+        view.beta32 = torch.zeros_like(op.beta32)
+        view._structs, view._beta_host = {}, None
+        op.__dict__["_structure_only"] = view
+    return view
+
+
+#: the reference's dense-oracle size limit (walk.py DENSE_ORACLE_MAX_N)
+DENSE_ORACLE_MAX_N = 2000
+
+
+def _check_dense(op: WalkOperator) -> None:
+    if op.n > DENSE_ORACLE_MAX_N:
+        raise NetworkError(f"dense oracle is limited to n <= {DENSE_ORACLE_MAX_N}, got {op.n}")
+
+
+def dense_transition(op: WalkOperator) -> np.ndarray:
+    """Materialised joint transition (walk.py:193-208): the device apply of
+    the identity block, P = apply(op, I_n), in f64."""
+    _check_dense(op)
+    eye = torch.eye(op.n, dtype=torch.float64, device=dev())
+    return apply_joint_transition(op, eye).cpu().numpy()
+
+
+def dense_walk_scores(op: WalkOperator) -> np.ndarray:
+    """alpha * sum_{s=0..gamma} (1 - alpha)^s P^s (walk.py:211-225); each power
+    is one device apply of the previous one (P^s = P P^(s-1))."""
+    _check_dense(op)
+    power = torch.eye(op.n, dtype=torch.float64, device=dev())
+    s = op.alpha * power.clone()
+    for step in range(1, op.gamma + 1):
+        power = apply_joint_transition(op, power)
+        s += op.alpha * (1.0 - op.alpha) ** step * power
+    return s.cpu().numpy()
+
+
+def brute_mhc_oracle(op: WalkOperator, y) -> float:
+    """Multi-hop conductance from the dense walk scores (walk.py:228-242):
+    1 - tr(Yhat^T S Yhat) / k, independent of the iterative calc_mhc."""
+    if y.n != op.n:
+        raise NetworkError("membership length does not match operator size")
+    empty = y.empty_clusters()
+    if empty.size:
+        raise NetworkError(f"empty cluster(s) {empty.tolist()}: conductance undefined")
+    s = dense_walk_scores(op)
+    sizes = y.cluster_sizes().astype(np.float64)
+    yhat = y.to_onehot() / np.sqrt(sizes)[y.assignment][:, None]
+    return float(1.0 - np.trace(yhat.T @ s @ yhat) / y.k)
