@@ -136,12 +136,12 @@ def _select_row(sims_row, K):
     return pos[order]
 
 
-def knn_rows(X, rows, K):
+def knn_rows(X, rows, K, normalized=None):
     """Exact lists of the query rows `rows` against all n keys, the blocked
     scan of knn.py:112-140 restricted to a row sample (the reference's own
     sampled form is knn._exact_rows_for, knn.py:227-239).  Used to time the
     CPU KNN on a bounded sample and to check sampled GPU rows."""
-    xn, nrm = unit_rows(X)
+    xn, nrm = unit_rows(X) if normalized is None else normalized
     n = xn.shape[0]
     rows = np.asarray(rows, dtype=np.int64)
     right = xn.T.tocsc() if sp.issparse(xn) else xn.T

@@ -862,6 +862,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
 
         Qsave_prev = torch.empty_like(loop.Qsave)
         disc_rounds = []            # rounds (both starts) of every discretisation
+        best_sampled = False        # best labels from a sample (phi in f32) or Y0 (f64)
 
         spec = None
         try:
@@ -930,6 +931,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                     if phi < best_mhc:
                         best_mhc = float(phi)
                         best_labels.copy_(lab_t)
+                        best_sampled = True
                     if float(np.sqrt(dq2)) < params.eps_q:
                         stop_reason, converged = "subspace_converged", True
                         if spec is not None:
@@ -963,6 +965,11 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         if best_mhc is None:                        # no sample was taken
             best_mhc = float(mhc0_dev.item())
             history[0] = (0, best_mhc)
+        if best_sampled:
+            # the loop compares f32 phi values (engine.py:403); the returned
+            # phi of the best labels is the f64 calc_mhc, as the reference's
+            with timer.span("mhc_ms"):
+                best_mhc = float(_MhcRunner(op, k, _lib.F64)(best_labels).item())
         caught = [str(w.message) for w in wrec]
     best_y = BcmMatrix(assignment=best_labels.cpu().numpy().astype(np.int64), k=k)
     state = EngineState(loop.q, best_y, best_mhc, history, t, c=c)
