@@ -24,6 +24,7 @@
 // The n x n similarity matrix never leaves TMEM/registers.
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -81,10 +82,16 @@ struct CandList {
   }
 };
 
+template <int L_, int E_>
+struct SlotCfg { static constexpr int L = L_, E = E_; };
+// split-bf16 path (eps ~ 2^-16): few near-K candidates per row
 template <int K_MAX>
 struct Slots;
-template <> struct Slots<10> { static constexpr int L = 16, E = 6; };
-template <> struct Slots<24> { static constexpr int L = 32, E = 8; };
+template <> struct Slots<10> : SlotCfg<16, 6> {};
+template <> struct Slots<24> : SlotCfg<32, 8> {};
+// single-product fp16 path (eps ~ 2 ||x - fp16(x)|| ~ 6e-4): K <= 10 live
+// entries plus 22 spare slots for the wider admission band
+using SlotsF16 = SlotCfg<32, 22>;
 
 struct RealParams {
   int64_t n;
@@ -93,7 +100,11 @@ struct RealParams {
   int d;              // attribute columns (MMA k-steps past d are all zeros: skipped)
   int K;
   int key_tiles, tiles_per_seg, nseg;
-  float eps, band;    // |a - s| bound and 2 eps
+  float eps, band;    // |a - s| bound and 2 eps (global)
+  const float* row_eps;  // per-query-row bound (fp16 path) or nullptr
+  int spin;              // producer / MMA threads spin on mbarriers instead of suspending
+  int resume;            // lists continue from `partial` (key-segment launches > 0)
+  int kt_base;           // first key tile of this launch
   int2* partial;      // nq x lists x L  (f32 bits, j)
   uint32_t* row_bound;  // nq: shared pruning floor (order-mapped f32)
   int64_t q_begin, q_end;
@@ -103,7 +114,7 @@ struct RealParams {
 
 // Epilogue warps (2..): thread = query row (TMEM lane), streams the
 // accumulator columns of every key tile into its candidate list.
-template <int KM>
+template <class SL>
 __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty, uint32_t tmem,
                                               float* stash_base, const RealParams& p, int64_t q0,
                                               int seg, int kt0, int ntiles) {
@@ -116,9 +127,25 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
   const int64_t i = q0 + row;
   const bool live = i < p.q_end;
   const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-  constexpr int L = Slots<KM>::L, E = Slots<KM>::E;
+  constexpr int L = SL::L, E = SL::E;
+  const float eps_i = (live && p.row_eps) ? p.row_eps[i] : p.eps;
+  const float band_i = 2.f * eps_i;
   CandList<L, E> C;
-  C.clear(p.K, -p.eps);
+  C.clear(p.K, -eps_i);
+  if (p.resume && live) {
+    // key-segment launches after the first continue the row's list
+    const int lists = p.nseg * (EPI_WARPS / 4);
+    const int live_n = p.K + E, pad = L - live_n;
+    const int2* in = p.partial + ((size_t)(i - p.q_begin) * lists + seg * (EPI_WARPS / 4) + half) * live_n;
+#pragma unroll
+    for (int t = 0; t < L; ++t)
+      if (t >= pad) {
+        const int2 e = in[t - pad];
+        C.f[t] = __int_as_float(e.x);
+        C.j[t] = e.y;
+      }
+    C.refresh(band_i);
+  }
   float published = -kInf;
   float* stash = stash_base + (threadIdx.x - 64) * 33;
   // the shared floor is read one tile ahead: the L2 round trip overlaps the
@@ -173,8 +200,8 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
         mask &= mask - 1;
         const float v = stash[u];
         if (v < C.thr) continue;
-        C.insert(v, (int32_t)(jb + u), p.band);
-        const float b = C.kth() - p.band;
+        C.insert(v, (int32_t)(jb + u), band_i);
+        const float b = C.kth() - band_i;
         if (b > published && live) {
           atomicMax(p.row_bound + (i - p.q_begin), f2ord(b));
           published = b;
@@ -189,6 +216,138 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
 #pragma unroll
     for (int t = 0; t < L; ++t)
       if (t >= pad) out[t - pad] = make_int2(__float_as_int(C.f[t]), C.j[t]);
+  }
+}
+
+// Epilogue of the single-product path.  Same admission rule and outputs as
+// real_epilogue, restructured for a warp of 32 independent rows:
+// * two 32-column chunks per TMEM wait (64 accumulator registers in flight);
+// * candidates that pass the admission threshold are appended to a small
+//   per-thread buffer (register selects, ~20 instructions) instead of being
+//   inserted into the sorted list at once; when any lane's buffer is half
+//   full the whole warp drains its buffers in lockstep.  A sorted insert is
+//   ~450 instructions, and unbatched the warp executes one per lane per event
+//   (lanes hit candidates at independent times); batched, the lanes insert
+//   together.  The threshold is refreshed at each drain, so between drains it
+//   is a (valid, lower) stale bound.
+template <class SL>
+__device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t* tempty,
+                                                      uint32_t tmem, float* stash_base,
+                                                      const RealParams& p, int64_t q0, int seg,
+                                                      int kt0, int ntiles) {
+  using namespace tc;
+  constexpr int PB = 8, DRAIN = 4;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ew = warp - 2;
+  const int quarter = warp & 3;
+  const int half = ew / 4;
+  const int row = quarter * 32 + lane;
+  const int64_t i = q0 + row;
+  const bool live = i < p.q_end;
+  const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+  constexpr int L = SL::L, E = SL::E;
+  const float eps_i = (live && p.row_eps) ? p.row_eps[i] : p.eps;
+  const float band_i = 2.f * eps_i;
+  CandList<L, E> C;
+  C.clear(p.K, -eps_i);
+  const int lists = p.nseg * (EPI_WARPS / 4);
+  const int live_n = p.K + E, pad = L - live_n;
+  int2* slot = p.partial + ((size_t)(live ? i - p.q_begin : 0) * lists + seg * (EPI_WARPS / 4) + half) * live_n;
+  if (p.resume && live) {
+#pragma unroll
+    for (int t = 0; t < L; ++t)
+      if (t >= pad) {
+        const int2 e = slot[t - pad];
+        C.f[t] = __int_as_float(e.x);
+        C.j[t] = e.y;
+      }
+    C.refresh(band_i);
+  }
+  if (!live) C.raise_floor(kInf);          // padding rows admit nothing
+  float pf[PB];
+  int32_t pj[PB];
+  int pc = 0;
+  float published = -kInf;
+  float* stash = stash_base + (threadIdx.x - 64) * 33;
+  auto drain = [&]() {
+#pragma unroll
+    for (int t = 0; t < PB; ++t)
+      if (t < pc && pf[t] >= C.thr) C.insert(pf[t], pj[t], band_i);
+    pc = 0;
+    const float b = C.kth() - band_i;
+    if (b > published && live) {
+      atomicMax(p.row_bound + (i - p.q_begin), f2ord(b));
+      published = b;
+    }
+  };
+  uint32_t floor_next = live ? __ldcg(p.row_bound + (i - p.q_begin)) : 0u;
+  for (int t = 0; t < ntiles; ++t) {
+    const int acc = t & 1;
+    const uint32_t acc_phase = (t >> 1) & 1;
+    mbar_wait_sleep(&tfull[acc], acc_phase);
+    if (live) {
+      C.raise_floor(ord2f(floor_next));
+      floor_next = __ldcg(p.row_bound + (i - p.q_begin));
+    }
+    tc_fence_after();
+    const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
+#pragma unroll 1
+    for (int ch = 0; ch < EPI_COLS / 32; ch += 2) {
+      uint32_t r[2][32];
+      tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + ch * 32, r[0]);
+      tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + (ch + 1) * 32, r[1]);
+      tmem_ld_wait();
+      if (ch + 2 == EPI_COLS / 32) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+      if (p.debug == 1) continue;
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        float mx[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          mx[u] = fmaxf(__uint_as_float(r[h2][u]), __uint_as_float(r[h2][u + 16]));
+#pragma unroll
+        for (int w = 8; w > 0; w >>= 1)
+#pragma unroll
+          for (int u = 0; u < w; ++u) mx[u] = fmaxf(mx[u], mx[u + w]);
+        if (mx[0] >= C.thr) {
+          const int64_t jb = j0 + (ch + h2) * 32;
+          uint32_t mask = 0;
+#pragma unroll
+          for (int u = 0; u < 32; ++u) {
+            const float v = __uint_as_float(r[h2][u]);
+            mask |= (uint32_t)(v >= C.thr) << u;
+            stash[u] = v;
+          }
+          if (i >= jb && i < jb + 32) mask &= ~(1u << (int)(i - jb));   // j != i
+          if (jb + 32 > p.n) mask &= p.n > jb ? (1u << (int)(p.n - jb)) - 1u : 0u;
+#pragma unroll 1
+          while (mask) {
+            const int u = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const float v = stash[u];
+            if (pc == PB) drain();                 // overflow (early in a row's stream)
+            if (v < C.thr) continue;
+#pragma unroll
+            for (int q = 0; q < PB; ++q) {
+              pf[q] = q == pc ? v : pf[q];
+              pj[q] = q == pc ? (int32_t)(jb + u) : pj[q];
+            }
+            ++pc;
+          }
+        }
+      }
+      if (__any_sync(0xffffffffu, pc >= DRAIN)) drain();
+    }
+  }
+  drain();
+  if (live) {
+#pragma unroll
+    for (int t = 0; t < L; ++t)
+      if (t >= pad) slot[t - pad] = make_int2(__float_as_int(C.f[t]), C.j[t]);
   }
 }
 
@@ -221,7 +380,7 @@ knn_real_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   } else if (warp == 1) {
     if (lane == 0) mma_issuer<false>(P, ntiles, nkb, p.debug == 2);
   } else {
-    real_epilogue<KM>(P.tfull, P.tempty, P.tmem, P.stash_base, p, q0, seg, kt0, ntiles);
+    real_epilogue<Slots<KM>>(P.tfull, P.tempty, P.tmem, P.stash_base, p, q0, seg, kt0, ntiles);
   }
   teardown(P);
 }
@@ -337,7 +496,117 @@ knn_real_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
       }
     }
   } else {
-    real_epilogue<KM>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
+    real_epilogue<Slots<KM>>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
+}
+
+// Single-product fp16 variant (d_pad <= 256, K <= 10): a_ij = <h_i, h_j>
+// with h = fp16(xn) (subnormals flushed to 0 in the prep, so the MMA sees
+// exactly the stored values).  |a_ij - s_ij| <= l_i + l_j + 3 l_i l_j +
+// d_pad 2^-23 with l = ||xn - h|| (per row, measured in f64): the bound is
+// ~6e-4 instead of the split path's ~2e-5, so each row keeps K + 22
+// candidates, but each key tile costs one MMA per k-step instead of three.
+// The CTA's 128 query rows stay resident in shared memory; key tiles stream.
+namespace res16 {
+constexpr int B_BYTES = tc::BN * tc::ROW_BYTES;
+constexpr int A_BYTES = tc::BM * tc::ROW_BYTES;
+constexpr int STASH = 32 * tc::EPI_WARPS * 33 * 4;
+__host__ __device__ constexpr int stages(int nks) { return nks <= 2 ? 5 : 4; }
+__host__ __device__ constexpr size_t smem(int nks) {
+  return 1024 + (size_t)nks * A_BYTES + (size_t)stages(nks) * B_BYTES + 256 + STASH;
+}
+}  // namespace res16
+
+__global__ void __launch_bounds__(tc::THREADS, 1)
+knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  RealParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int nks = p.nkb_seg, S = res16::stages(nks);
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;                                    // nks k-blocks of h
+  unsigned char* sB = sA + nks * res16::A_BYTES;               // S stages
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * res16::B_BYTES);
+  uint64_t* empty = full + 6;
+  uint64_t* tfull = empty + 6;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
+  float* stash_base = reinterpret_cast<float*>(base + nks * res16::A_BYTES + S * res16::B_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
+  const int seg = blockIdx.y;
+  const int kt0 = p.kt_base + seg * p.tiles_per_seg;
+  const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
+  const int ntiles = kt1 - kt0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s2 = 0; s2 < S; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
+    for (int s2 = 0; s2 < 2; ++s2) { mbar_init(&tfull[s2], 1); mbar_init(&tempty[s2], EPI_WARPS); }
+    mbar_init(afull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr int EL = ROW_BYTES / 2;    // fp16 elements per k-block
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(afull, nks * res16::A_BYTES);
+      for (int kb = 0; kb < nks; ++kb) tma_load_2d(sA + kb * res16::A_BYTES, &tmA, afull, kb * EL, (int)q0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int krow = (kt0 + t) * BN;
+        for (int kb = 0; kb < nks; ++kb) {
+          mbar_wait_backoff(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], res16::B_BYTES);
+          tma_load_2d(sB + stage * res16::B_BYTES, &tmB, &full[stage], kb * EL, krow);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(0u, BM, BN);     // kind::f16, F16 inputs
+      const bool skip = p.debug == 2;
+      mbar_wait_sleep(afull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait_backoff(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + acc * BN;
+        for (int kb = 0; kb < nks; ++kb) {
+          mbar_wait_backoff(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t b_addr = smem_u32(sB + stage * res16::B_BYTES);
+          const uint32_t a_addr = smem_u32(sA + kb * res16::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (skip || kb * 64 + k * 16 >= p.d) continue;     // zero padding past d
+            mma_f16_ss(dtm, sw128_kmajor_desc(a_addr + k * 32), sw128_kmajor_desc(b_addr + k * 32),
+                       idesc, (kb | k) != 0);
+          }
+          mma_commit(&empty[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    real_epilogue_batched<SlotsF16>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
   }
   tc_fence_before();
   __syncthreads();
@@ -345,9 +614,10 @@ knn_real_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
 }
 
 // warp per query row: merge the partial lists, certify, rerank in f64
-template <int KM>
+template <class SL>
 __global__ void knn_real_merge_kernel(const int2* __restrict__ partial, int64_t q_begin,
-                                      int64_t nq, int lists, int K, float eps, float band,
+                                      int64_t nq, int lists, int K, float eps_g,
+                                      const float* __restrict__ row_eps,
                                       const double* __restrict__ xn, int64_t ldn, int64_t d,
                                       const double* __restrict__ norms, int32_t* __restrict__ ids,
                                       double* __restrict__ scores, int32_t* __restrict__ flagged,
@@ -363,7 +633,9 @@ __global__ void knn_real_merge_kernel(const int2* __restrict__ partial, int64_t 
       for (int t = lane; t < K; t += 32) { oid[t] = -1; osc[t] = 0.0; }
       continue;
     }
-    constexpr int L = Slots<KM>::L, E = Slots<KM>::E;
+    constexpr int L = SL::L, E = SL::E;
+    const float eps = row_eps ? row_eps[i] : eps_g;
+    const float band = 2.f * eps;
     const int live_n = K + E;
     CandList<L, E> M;
     M.clear(K, -eps);
@@ -452,6 +724,61 @@ __global__ void knn_real_prep_kernel(const double* __restrict__ X, int64_t n, in
   }
 }
 
+// f64 X -> xn (f64) + norms + h = fp16(xn) (n_pad x d_pad, subnormals
+// flushed to zero) + lo[i] = ||xn_i - h_i|| (rounded up) + max_i lo[i]
+__global__ void knn_real16_prep_kernel(const double* __restrict__ X, int64_t n, int64_t d,
+                                       int64_t ldx, int64_t n_pad, int64_t d_pad,
+                                       double* __restrict__ xn, int64_t ldn,
+                                       double* __restrict__ norms, __half* __restrict__ H,
+                                       float* __restrict__ lo, uint32_t* __restrict__ lo_max) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = w0; r < n_pad; r += nw) {
+    double inv = 0.0;
+    if (r < n) {
+      const double* x = X + r * ldx;
+      double nrm = 0.0;
+      if (lane == 0)  // np.linalg.norm(x, axis=1): sqrt of the pairwise sum of x*x
+        nrm = sqrt(np_pairwise_sum_g([x](int64_t c) { return __dmul_rn(x[c], x[c]); }, d));
+      nrm = __shfl_sync(0xffffffffu, nrm, 0);
+      inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+      if (lane == 0) norms[r] = nrm;
+    }
+    __half* h = H + r * d_pad;
+    double l2 = 0.0;
+    for (int64_t c = lane; c < d_pad; c += 32) {
+      const double v = (r < n && c < d) ? __dmul_rn(X[r * ldx + c], inv) : 0.0;
+      if (r < n && c < ldn) xn[r * ldn + c] = v;
+      __half hv = __double2half(v);
+      if (fabs(v) < 0x1p-14) hv = __double2half(0.0);      // no fp16 subnormals
+      h[c] = hv;
+      const double e = v - (double)__half2float(hv);
+      l2 = fma(e, e, l2);
+    }
+    if (r < n) {
+      for (int64_t c = d_pad + lane; c < ldn; c += 32) xn[r * ldn + c] = 0.0;
+      l2 = warp_sum(l2);
+      if (lane == 0) {
+        const float l = (float)(sqrt(l2) * (1.0 + 1e-6)) + 1e-30f;
+        lo[r] = l;
+        atomicMax(lo_max, __float_as_uint(l));             // l >= 0: bit order = value order
+      }
+    }
+  }
+}
+
+// per-row certificate bound eps_i = l_i + l_max + 3 l_i l_max + d_pad 2^-23
+__global__ void knn_real16_eps_kernel(const float* __restrict__ lo, const uint32_t* __restrict__ lo_max,
+                                      int64_t n, float acc_eps, float* __restrict__ row_eps) {
+  const float lm = __uint_as_float(*lo_max);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float l = lo[i];
+    row_eps[i] = (l + lm + 3.f * l * lm + acc_eps) * (1.f + 1e-5f);
+  }
+}
+
 // ----------------------------------------------------------------- host side
 namespace {
 struct RealLayout {
@@ -470,7 +797,12 @@ RealLayout real_layout(int64_t n, int64_t d, int64_t nq) {
   return R;
 }
 
-int real_slots(int K) { return K <= 10 ? Slots<10>::L : Slots<24>::L; }
+// partial-list slots per list: the fp16 path (K <= 10) keeps K + 22 live
+int real_slots(int K) { return K <= 10 ? SlotsF16::L : Slots<24>::L; }
+bool use_f16_path(int K, int64_t d_pad) {
+  static const bool split = getenv("ANCKA_KNN_SPLIT") != nullptr;
+  return !split && K <= 10 && d_pad <= 256;
+}
 
 struct RealWs {
   __nv_bfloat16* H;
@@ -481,6 +813,8 @@ struct RealWs {
   int* nflag;
   void* simt_ws;
   size_t simt_wsb;
+  float *lo, *row_eps;
+  uint32_t* lo_max;
 };
 
 void carve_real(Carver& cv, const RealLayout& R, int64_t n, int K, RealWs& w) {
@@ -495,6 +829,9 @@ void carve_real(Carver& cv, const RealLayout& R, int64_t n, int K, RealWs& w) {
   w.nflag = cv.take<int>(1);
   w.simt_wsb = knn_simt_list_workspace(K);
   w.simt_ws = cv.take<unsigned char>(w.simt_wsb);
+  w.lo = cv.take<float>(n);
+  w.row_eps = cv.take<float>(n);
+  w.lo_max = cv.take<uint32_t>(1);
 }
 
 template <int KM>
@@ -517,6 +854,86 @@ int launch_real(const CUtensorMap& ma, const CUtensorMap& mb, const RealParams& 
 }
 }  // namespace
 
+namespace {
+int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
+               int64_t q_end, int32_t* ids, double* scores, const RealLayout& R, const RealWs& w,
+               cudaStream_t st) {
+  const int64_t nq = q_end - q_begin;
+  __half* H = reinterpret_cast<__half*>(w.H);       // n_pad x d_pad fits the [hi|lo] buffer
+  ANCKA_CUDA(cudaMemsetAsync(w.lo_max, 0, sizeof(uint32_t), st));
+  const int pg = (int)std::min<int64_t>(ceil_div(R.n_pad * 32, 256), 16 * kNumSMs);
+  knn_real16_prep_kernel<<<pg, 256, 0, st>>>(X, n, d, ldx, R.n_pad, R.d_pad, w.xn, R.ldn, w.norms,
+                                             H, w.lo, w.lo_max);
+  ANCKA_LAUNCHED();
+  const float acc_eps = (float)((double)R.d_pad * 0x1p-23);
+  knn_real16_eps_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 8 * kNumSMs), 256, 0, st>>>(
+      w.lo, w.lo_max, n, acc_eps, w.row_eps);
+  ANCKA_LAUNCHED();
+  CUtensorMap ma, mb;
+  ANCKA_TRY(tc_make_map(&ma, H, false, R.n_pad, R.d_pad, tc::BM));
+  ANCKA_TRY(tc_make_map(&mb, H, false, R.n_pad, R.d_pad, tc::BN));
+  RealParams p;
+  p.n = n;
+  p.nkb_seg = (int)(R.d_pad / 64);
+  p.d_pad = (int)R.d_pad;
+  p.d = (int)d;
+  p.K = K;
+  p.key_tiles = R.g.key_tiles;
+  p.tiles_per_seg = R.g.tiles_per_seg;
+  p.nseg = R.g.nseg;
+  p.eps = 0.f;
+  p.band = 0.f;
+  p.row_eps = w.row_eps;
+  p.resume = 0;
+  p.kt_base = 0;
+  p.partial = w.part;
+  p.row_bound = w.rb;
+  p.q_begin = q_begin;
+  p.q_end = q_end;
+  p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
+  p.spin = getenv("ANCKA_KNN_SPIN") ? atoi(getenv("ANCKA_KNN_SPIN")) : 0;
+  ANCKA_CUDA(cudaMemsetAsync(w.rb, 0, sizeof(uint32_t) * nq, st));
+  ANCKA_CUDA(cudaMemsetAsync(w.nflag, 0, sizeof(int), st));
+  // Key segments as successive launches over all query tiles: the CTAs in
+  // flight all stream the same <= ~40 MB of keys, which stays in L2 (one
+  // launch over all n keys re-reads the key matrix from HBM once CTAs drift
+  // apart: 6.8 TB of DRAM reads at Amazon2M).  Row lists carry across
+  // launches through `partial`.
+  const int64_t key_bytes = (int64_t)tc::BN * R.d_pad * 2;
+  int seg_tiles = (int)std::max<int64_t>(1, (40ll << 20) / key_bytes);
+  if (const char* e = getenv("ANCKA_KNN_SEG_TILES")) seg_tiles = std::max(1, atoi(e));
+  const int nlaunch = (int)ceil_div(R.g.key_tiles, seg_tiles);
+  int lists = R.lists;
+  {
+    const size_t sm = res16::smem(p.nkb_seg);
+    ANCKA_CUDA(cudaFuncSetAttribute(knn_real16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sm));
+    if (nlaunch <= 1) {
+      dim3 grid(R.g.q_tiles, R.g.nseg);
+      knn_real16_kernel<<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+      ANCKA_LAUNCHED();
+    } else {
+      p.nseg = 1;
+      p.tiles_per_seg = seg_tiles;
+      lists = tc::EPI_WARPS / 4;
+      for (int l = 0; l < nlaunch; ++l) {
+        p.kt_base = l * seg_tiles;
+        p.resume = l > 0;
+        knn_real16_kernel<<<dim3(R.g.q_tiles, 1), tc::THREADS, sm, st>>>(ma, mb, p);
+        ANCKA_LAUNCHED();
+      }
+    }
+  }
+  const int mg = (int)std::min<int64_t>(ceil_div(nq * 32, 256), 16 * kNumSMs);
+  knn_real_merge_kernel<SlotsF16><<<mg, 256, 0, st>>>(w.part, q_begin, nq, lists, K, 0.f,
+                                                      w.row_eps, w.xn, R.ldn, d, w.norms, ids,
+                                                      scores, w.flagged, w.nflag);
+  ANCKA_LAUNCHED();
+  return knn_simt_list(w.xn, n, R.ldn, w.norms, K, q_begin, w.flagged, w.nflag, ids, scores,
+                       w.simt_ws, w.simt_wsb, st);
+}
+}  // namespace
+
 size_t knn_real_workspace(int64_t n, int64_t d, int K) {
   Carver cv(nullptr, 0);
   RealWs w;
@@ -535,6 +952,8 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
   carve_real(cv, R, n, K, w);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_real: workspace too small");
   const int pg = (int)std::min<int64_t>(ceil_div(R.n_pad * 32, 256), 16 * kNumSMs);
+  if (use_f16_path(K, R.d_pad))
+    return knn_real16(X, n, d, ldx, K, q_begin, q_end, ids, scores, R, w, st);
   knn_real_prep_kernel<<<pg, 256, 0, st>>>(X, n, d, ldx, R.n_pad, R.d_pad, w.xn, R.ldn, w.norms, w.H);
   ANCKA_LAUNCHED();
 
@@ -555,6 +974,10 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
   p.eps = (float)(1.6e-5 + 3.0 * (double)R.d_pad * 0x1p-23);
   if (const char* e = getenv("ANCKA_KNN_EPS")) p.eps = (float)atof(e);
   p.band = 2.f * p.eps;
+  p.row_eps = nullptr;
+  p.spin = 0;
+  p.resume = 0;
+  p.kt_base = 0;
   p.partial = w.part;
   p.row_bound = w.rb;
   p.q_begin = q_begin;
@@ -567,10 +990,10 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
 
   const int mg = (int)std::min<int64_t>(ceil_div(nq * 32, 256), 16 * kNumSMs);
   if (K <= 10)
-    knn_real_merge_kernel<10><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, p.band,
+    knn_real_merge_kernel<Slots<10>><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, nullptr,
                                                   w.xn, R.ldn, d, w.norms, ids, scores, w.flagged, w.nflag);
   else
-    knn_real_merge_kernel<24><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, p.band,
+    knn_real_merge_kernel<Slots<24>><<<mg, 256, 0, st>>>(w.part, q_begin, nq, R.lists, K, p.eps, nullptr,
                                                   w.xn, R.ldn, d, w.norms, ids, scores, w.flagged, w.nflag);
   ANCKA_LAUNCHED();
   // uncertified rows: exact f64 rescan over all keys (device-side count)

@@ -25,7 +25,7 @@ import numpy as np
 import pytest
 import scipy.sparse as sp
 
-from conftest import load_csr, random_seeds
+from conftest import load_csr, oracle_net, random_seeds
 from oracle import ancka_cpu as oc
 
 pytestmark = pytest.mark.gpu
@@ -187,8 +187,7 @@ def test_dense_oracles_match_golden(golden_random):
         assert abs(b - float(z[p + "mhc_brute"])) < 1e-9, s
         assert abs(b - ancka.calc_mhc(op, y)) < 1e-9, s
         m = z[p + "M"]
-        onet = oc.clean_network({"kind": str(z[p + "kind"]), "S": load_csr(z, p + "S"),
-                                 "directed": bool(z[p + "directed"]), "X": None})
+        onet = oc.clean_network(oracle_net(z, p))
         pk = load_csr(z, p + "PK")
         zero = np.asarray(pk.sum(axis=1)).ravel() == 0
         oop = oc.make_operator(onet, pk, zero, 0.2, float(z[p + "beta"]), int(z[p + "gamma"]))
