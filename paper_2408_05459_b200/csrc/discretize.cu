@@ -23,6 +23,8 @@
 #include <cooperative_groups.h>
 #include <cstdlib>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -50,6 +52,9 @@ struct DiscParams {
   int groups;           // accumulator groups per CTA
   int run_lo, run_hi;   // alternating-rounding starts handled by this launch
   double* fin;          // split launches: per-run (obj, rounds, conv, empties)
+  float* qn;            // k > 8: normalised block q~ (n x kq, f32, zero padded)
+  double* qinv;         // k > 8: 1 / ||q_i|| (0 for all-zero rows)
+  int dbuf;             // k > 8: double-buffered row tiles (when shared memory allows)
 };
 
 // Row i of Q[:, col0:col0+k], normalised in f64 (engine.py:226-232) and
@@ -202,7 +207,18 @@ __host__ __device__ constexpr int win_sw(int kmax) {
 }
 // scoring-rotation and row-tile bytes of the k (<= 8 : > 8) layouts
 __host__ __device__ inline size_t disc_rot_bytes(int k, int off) {
-  return k <= 8 ? (size_t)k * kpad4(k) * 4 : (size_t)((k + 3) / 4) * win_kw(disc_kmax(k, off)) * 16;
+  (void)off;
+  return k <= 8 ? (size_t)k * kpad4(k) * 4
+                : align_dev((size_t)((k + 15) / 16) * (((k + 15) & ~15) / 8) * 32 * 16) + (size_t)k * k * 8;
+}
+// k > 8 phase-A layout: group accumulators | group counts | tile | tile labels
+__host__ __device__ inline size_t disc_tc_tile_bytes(int k, int off, int dbuf = 1) {
+  const size_t tc = (dbuf ? 2 : 1) * (size_t)kDiscThreads * (((k + 15) & ~15) + 4) * 4;
+  const size_t win = (size_t)kDiscThreads * 4 * win_sw(disc_kmax(k, off));
+  return tc > win ? tc : win;
+}
+__host__ __device__ inline size_t disc_tc_acc_bytes(int k, int G) {
+  return (size_t)G * k * ((k + 15) & ~15) * 8;
 }
 __host__ __device__ inline size_t disc_tile_bytes(int k, int off) {
   return (size_t)kDiscThreads * 4 * (k <= 8 ? k : win_sw(disc_kmax(k, off)));
@@ -403,6 +419,427 @@ __device__ void phase_accumulate_wide(const DiscParams& p, const float* sR, floa
     atomicAdd(&zsum, zeros);
     __syncthreads();
     if (threadIdx.x == 0) *zeros_out = zsum;
+  }
+  __syncthreads();
+}
+
+// ---- k > 8: tensor-core scoring.  The block is normalised once per call
+// into q~ (f32, kq = 8 ceil(k / 8) columns, zero padded); each round scores a
+// staged 256-row tile against R with warp-level TF32 MMAs in three products
+// (q_hi R_hi + q_hi R_lo + q_lo R_hi, hi = rna_tf32(x), lo = x - hi), which
+// carries the f32 scoring error of the SIMT path (~2^-22 relative per
+// product, f32 accumulation).  A quad of lanes owns a row; the first-max
+// argmax and the second-best margin are merged by two shuffles.  The
+// cluster sums M[label][j] go to NG group-private 64-bit fixed-point
+// accumulators in shared memory (plain adds: each (label, column) cell of a
+// group has one owner thread), folded into the global totals by integer
+// atomics (order-free: bit-reproducible).
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], float b0, float b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(__float_as_uint(b0)),
+        "r"(__float_as_uint(b1)));
+}
+// q~ columns padded to the MMA K step (16); n-blocks of 8 output columns
+__device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__host__ __device__ constexpr int disc_kq(int k) { return (k + 15) & ~15; }
+__host__ __device__ constexpr int disc_nbmax(int kmax) { return disc_kq(kmax >= 64 ? 64 : kmax) / 8; }
+
+// R as per-lane FP16 B fragments (m16n8k16), split R = hi + lo:
+// sRf[(ks * nb8 + nb) * 32 + lane] = (hi pair 0, hi pair 1, lo pair 0, lo pair 1),
+// pair 0 = (R[16ks+2t][8nb+g], R[16ks+2t+1][8nb+g]), pair 1 = rows + 8,
+// g = lane / 4, t = lane % 4; followed by R in f64 (row l, col j).
+__host__ __device__ inline size_t disc_frag_bytes(int k) {
+  return align_dev((size_t)(disc_kq(k) / 16) * (disc_kq(k) / 8) * 32 * 16);
+}
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+// x = hi + lo with hi = fp16(x), lo = fp16(x - hi) for an element pair
+__device__ __forceinline__ void split_half2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack_half2(a - hf.x, b - hf.y);
+}
+template <typename Get>
+__device__ __forceinline__ void store_rot_frag(unsigned char* base, int k, Get get) {
+  const int ks16 = disc_kq(k) / 16, nb8 = disc_kq(k) / 8;
+  uint4* sRf = reinterpret_cast<uint4*>(base);
+  double* sR64 = reinterpret_cast<double*>(base + disc_frag_bytes(k));
+  for (int e = threadIdx.x; e < ks16 * nb8 * 32; e += blockDim.x) {
+    const int lane = e & 31, f = e >> 5, ks = f / nb8, nb = f % nb8;
+    const int g = lane >> 2, t = lane & 3, j = nb * 8 + g;
+    float r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int l = ks * 16 + 2 * t + (q & 1) + ((q & 2) ? 8 : 0);
+      r[q] = (l < k && j < k) ? (float)get(l, j) : 0.f;
+    }
+    uint4 v;
+    split_half2(r[0], r[1], v.x, v.z);
+    split_half2(r[2], r[3], v.y, v.w);
+    sRf[e] = v;
+  }
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) sR64[e] = get(e / k, e % k);
+}
+
+// q~ = Q[:, col0:col0+k] / ||.|| for this CTA's rows (warp per row, lanes
+// over columns), 1/||q_i|| kept for the prototype start; returns zero rows.
+__device__ int normalize_rows(const DiscParams& p) {
+  const int k = p.k, kq = disc_kq(k);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const Rows R = my_rows(p.n);
+  int zeros = 0;
+  for (int64_t i = R.r0 + warp; i < R.r1; i += nw) {
+    const float* src = p.Q + i * p.ldq + p.col0;
+    const double v0 = lane < k ? (double)src[lane] : 0.0;
+    const double v1 = lane + 32 < k ? (double)src[lane + 32] : 0.0;
+    const double nrm = sqrt(warp_sum(v0 * v0 + v1 * v1));
+    const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+    float* dst = p.qn + i * kq;
+    if (lane < kq) dst[lane] = (float)(v0 * inv);
+    if (lane + 32 < kq) dst[lane + 32] = (float)(v1 * inv);
+    if (lane == 0) {
+      p.qinv[i] = inv;
+      zeros += nrm == 0.0;
+    }
+  }
+  return zeros;
+}
+
+// Certified argmax.  Scores are 3xTF32 products (q_hi R_hi + q_hi R_lo +
+// q_lo R_hi, hi = rna_tf32(x), lo = x - hi truncated by the MMA): per
+// product error <= 2^-20 |q||R|, plus f32 accumulation of 3k terms, so for a
+// unit row and an orthogonal R every score is within 1e-5 of the f64 score
+// of the same f32 iterate.  When the winner beats the runner-up by more than
+// kCert = 2e-5 the f64 winner is the same column; rows below the margin
+// (exact ties, near-ties) are rescored in f64 by one warp each: q~ = Q_i /
+// ||Q_i||, R in f64, first max -- the reference's f64 argmax (engine.py:192)
+// on this iterate.  Margins (second-best scores) of certified rows stay
+// 3xTF32 values; the rare empty-cluster reseed rescores every row first.
+constexpr float kCert = 2e-5f;
+
+// One warp: f64 scores of row i against R, first-max argmax and the
+// second-best value (all lanes return them).  qw: 64 doubles of scratch.
+__device__ __forceinline__ void score_row_exact_warp(const DiscParams& p, const double* sR64,
+                                                     int64_t i, double* qw, int& lab,
+                                                     float& second_out) {
+  const int k = p.k, lane = threadIdx.x & 31;
+  const float* src = p.Q + i * p.ldq + p.col0;
+  const double inv = p.qinv[i];
+  if (lane < k) qw[lane] = (double)src[lane] * inv;
+  if (lane + 32 < k) qw[lane + 32] = (double)src[lane + 32] * inv;
+  __syncwarp();
+  double s0 = 0.0, s1 = 0.0;
+  for (int l = 0; l < k; ++l) {
+    const double ql = qw[l];
+    if (lane < k) s0 = fma(ql, sR64[l * k + lane], s0);
+    if (lane + 32 < k) s1 = fma(ql, sR64[l * k + lane + 32], s1);
+  }
+  double best = lane < k ? s0 : -INFINITY, second = -INFINITY;
+  int bi = lane;
+  if (lane + 32 < k) {
+    if (s1 > best) { second = best; best = s1; bi = lane + 32; }
+    else second = s1;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const double os = __shfl_xor_sync(0xffffffffu, second, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    const bool take = ob > best || (ob == best && oi < bi);
+    second = fmax(fmax(second, os), take ? best : ob);
+    best = take ? ob : best;
+    bi = take ? oi : bi;
+  }
+  lab = bi;
+  second_out = (float)second;
+  __syncwarp();
+}
+
+// round(x * 2^sh) to int64 (round half to even, as __float2ll_rn of the
+// exact product) with integer operations only: the 64-bit float->int
+// conversion is a slow path on sm_100.  |x| <= 1 and sh <= 61.
+__device__ __forceinline__ long long fx_round(float x, int sh) {
+  const uint32_t b = __float_as_uint(x);
+  const int e = (int)((b >> 23) & 0xffu);
+  const uint32_t m = (b & 0x7fffffu) | 0x800000u;
+  const int s = e - 150 + sh;                // x * 2^sh = m * 2^s (normal x)
+  long long v;
+  if (e == 0 || s <= -25) {
+    v = 0;                                   // |x * 2^sh| < 1/2 (or zero / subnormal x)
+  } else if (s >= 0) {
+    v = (long long)m << s;
+  } else {
+    const int r = -s;
+    const uint32_t q = m >> r, rem = m & ((1u << r) - 1u), half = 1u << (r - 1);
+    v = (long long)(q + ((rem > half || (rem == half && (q & 1u))) ? 1u : 0u));
+  }
+  return (b >> 31) ? -v : v;
+}
+
+template <int KMAX>
+__device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const double* sR64,
+                                    float* tile, int* tlab, long long* gacc, int* gcnt, bool score,
+                                    unsigned long long* gdst) {
+  constexpr int NBM = disc_nbmax(KMAX);
+  const int k = p.k, kk = k * k, kq = disc_kq(k), ks16 = kq / 16, nb8 = kq / 8;
+  const int SWQ = kq + 4;
+  const size_t tile_floats = p.dbuf ? (size_t)kDiscThreads * SWQ : 0;
+  // tile labels, within-bucket ranks, row permutation, bucket offsets and
+  // counts, rows to rescore exactly
+  int* trank = tlab + kDiscThreads;
+  int* perm = trank + kDiscThreads;
+  int* boff = perm + kDiscThreads;        // k + 1 (68 slots)
+  int* bcnt = boff + 68;                  // k (64 slots)
+  int* flagged = bcnt + 64;               // kDiscThreads
+  double* wq = reinterpret_cast<double*>(flagged + kDiscThreads);   // 8 warps x 64, 16-B aligned
+  __shared__ int s_nflag;
+  double* gsum = reinterpret_cast<double*>(gacc);    // CTA cluster sums (f64)
+  int* wcnt = flagged + kDiscThreads + 2 * 8 * 64;    // 8 warps x 64 labels (after wq)
+  for (int e = threadIdx.x; e < k * kq; e += blockDim.x) gsum[e] = 0.0;
+  for (int e = threadIdx.x; e < k; e += blockDim.x) gcnt[e] = 0;
+  for (int e = threadIdx.x; e < 8 * 64; e += blockDim.x) wcnt[e] = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int ngb = kDiscThreads / kq, grp = threadIdx.x / kq, col = threadIdx.x % kq;
+  const Rows R = my_rows(p.n);
+  const int ntile = (int)ceil_div(R.r1 - R.r0, (int64_t)kDiscThreads);
+  const int c4 = kq / 4;
+  auto stage = [&](int ti) {   // 16-byte async copies of tile ti into buffer ti & 1
+    const int64_t t0 = R.r0 + (int64_t)ti * kDiscThreads;
+    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
+    float* dst = tile + (ti & 1) * tile_floats;
+    const int ne = tr * c4, dr = kDiscThreads / c4, dc = kDiscThreads % c4;
+    int r = threadIdx.x / c4, c = threadIdx.x % c4;
+    for (int e = threadIdx.x; e < ne; e += kDiscThreads) {
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst + r * SWQ + 4 * c)),
+                   "l"(p.qn + (t0 + r) * kq + 4 * c)
+                   : "memory");
+      r += dr;
+      c += dc;
+      if (c >= c4) { c -= c4; ++r; }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const bool dbg = p.tdbg && blockIdx.x == 0 && threadIdx.x == 0;
+  long long c_prev = dbg ? clock64() : 0;
+#define SUBSTAMP(slot)                                  \
+  do {                                                  \
+    if (dbg) {                                          \
+      const long long _c = clock64();                   \
+      p.tdbg[(slot)] += (unsigned long long)(_c - c_prev); \
+      c_prev = _c;                                      \
+    }                                                   \
+  } while (0)
+  if (ntile > 0 && p.dbuf) stage(0);
+  for (int ti = 0; ti < ntile; ++ti) {
+    const int64_t t0 = R.r0 + (int64_t)ti * kDiscThreads;
+    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
+    if (!p.dbuf) {
+      stage(ti);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    } else if (ti + 1 < ntile) {
+      stage(ti + 1);                       // overlaps this tile's work
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    for (int e = threadIdx.x; e < 8 * 64; e += blockDim.x) wcnt[e] = 0;
+    if (threadIdx.x == 0) s_nflag = 0;
+    __syncthreads();
+    SUBSTAMP(8);
+    const float* tl = tile + (ti & 1) * tile_floats;
+    if (score) {
+      if (warp * 32 < tr) {
+        float acc[2][NBM][4];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+          for (int nb = 0; nb < NBM; ++nb)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[mb][nb][c] = 0.f;
+        const float* wt = tl + warp * 32 * SWQ;
+#pragma unroll 1
+        for (int ks = 0; ks < ks16; ++ks) {
+          uint32_t ah[2][4], al[2][4];
+#pragma unroll
+          for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float2 x = *reinterpret_cast<const float2*>(
+                  wt + (mb * 16 + g + ((q & 1) ? 8 : 0)) * SWQ + ks * 16 + 2 * t + ((q & 2) ? 8 : 0));
+              split_half2(x.x, x.y, ah[mb][q], al[mb][q]);
+            }
+#pragma unroll
+          for (int nb = 0; nb < NBM; ++nb) {
+            if (nb < nb8) {
+              const uint4 b = sRf[(ks * nb8 + nb) * 32 + lane];
+#pragma unroll
+              for (int mb = 0; mb < 2; ++mb) {
+                mma_f16(acc[mb][nb], ah[mb], b.x, b.y);
+                mma_f16(acc[mb][nb], ah[mb], b.z, b.w);
+                mma_f16(acc[mb][nb], al[mb], b.x, b.y);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float best = -INFINITY, second = -INFINITY;
+            int bi = 0x7fffffff;
+#pragma unroll
+            for (int nb = 0; nb < NBM; ++nb)
+#pragma unroll
+              for (int c = 0; c < 2; ++c) {
+                const int j = nb * 8 + 2 * t + c;
+                const float v = (nb < nb8 && j < k) ? acc[mb][nb][h * 2 + c] : -INFINITY;
+                second = fmaxf(second, fminf(best, v));
+                bi = v > best ? j : bi;
+                best = fmaxf(best, v);
+              }
+#pragma unroll
+            for (int o = 1; o <= 2; o <<= 1) {
+              const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+              const float os = __shfl_xor_sync(0xffffffffu, second, o);
+              const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+              const bool take = ob > best || (ob == best && oi < bi);
+              second = fmaxf(fmaxf(second, os), take ? best : ob);
+              best = take ? ob : best;
+              bi = take ? oi : bi;
+            }
+            const int row = warp * 32 + mb * 16 + g + h * 8;
+            if (t == 0 && row < tr) {
+              if (!(best - second > kCert)) flagged[atomicAdd(&s_nflag, 1)] = row;
+              p.labels[t0 + row] = bi;
+              p.margin[t0 + row] = second;
+              tlab[row] = bi;
+            }
+          }
+      }
+      __syncthreads();
+      SUBSTAMP(9);
+      if (dbg) p.tdbg[14] += s_nflag;
+      // exact f64 rescoring (a warp per row) of the rows the margin does not certify
+      for (int f = warp; f < s_nflag; f += kDiscThreads / 32) {
+        const int row = flagged[f];
+        int lab;
+        float second;
+        score_row_exact_warp(p, sR64, t0 + row, wq + warp * 64, lab, second);
+        if (lane == 0) {
+          p.labels[t0 + row] = lab;
+          p.margin[t0 + row] = second;
+          tlab[row] = lab;
+        }
+      }
+    } else {
+      for (int r = threadIdx.x; r < tr; r += blockDim.x) tlab[r] = p.labels[t0 + r];
+    }
+    __syncthreads();
+    SUBSTAMP(10);
+    // rows grouped by label with a stable counting sort (ranks from warp
+    // matches + per-warp label counts), so every bucket lists its rows in
+    // row order and the f64 sums below have a fixed order
+    {
+      const int r = threadIdx.x;
+      const int lab = r < tr ? tlab[r] : 0x40000000 + r;       // unique sentinel
+      const unsigned match = __match_any_sync(0xffffffffu, lab);
+      const unsigned lt = (1u << lane) - 1u;
+      trank[r] = __popc(match & lt);
+      if (r < tr && (match & lt) == 0) wcnt[warp * 64 + lab] = __popc(match);
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {                // per label: warp bases, bucket size
+      const int l = threadIdx.x;
+      int run = 0;
+#pragma unroll
+      for (int w = 0; w < kDiscThreads / 32; ++w) {
+        const int c = wcnt[w * 64 + l];
+        wcnt[w * 64 + l] = run;
+        run += c;
+      }
+      bcnt[l] = run;
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const int c0 = lane < k ? bcnt[lane] : 0, c1 = lane + 32 < k ? bcnt[lane + 32] : 0;
+      int x0 = c0, x1 = c1;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
+        if (lane >= o) { x0 += y0; x1 += y1; }
+      }
+      const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
+      if (lane < k) boff[lane] = x0 - c0;
+      if (lane + 32 < k) boff[lane + 32] = tot0 + x1 - c1;
+      if (lane == 0) boff[k] = tr;
+    }
+    __syncthreads();
+    if (threadIdx.x < tr) {
+      const int lab = tlab[threadIdx.x];
+      perm[boff[lab] + wcnt[warp * 64 + lab] + trank[threadIdx.x]] = threadIdx.x;
+    }
+    __syncthreads();
+    SUBSTAMP(11);
+    // a warp per bucket, lanes over columns: f64 sums in row order, one
+    // update of the CTA accumulator per (bucket, column)
+    for (int b = warp; b < k; b += kDiscThreads / 32) {
+      const int q0 = boff[b], q1 = boff[b + 1];
+      if (q0 == q1) continue;
+      double s0 = 0.0, s1 = 0.0;
+      const bool c0ok = lane < k, c1ok = lane + 32 < k;
+      for (int q = q0; q < q1; ++q) {
+        const float* row = tl + perm[q] * SWQ;
+        if (c0ok) s0 += (double)row[lane];
+        if (c1ok) s1 += (double)row[lane + 32];
+      }
+      if (c0ok) gsum[b * kq + lane] += s0;
+      if (c1ok) gsum[b * kq + lane + 32] += s1;
+      if (lane == 0) gcnt[b] += q1 - q0;
+    }
+    __syncthreads();
+    SUBSTAMP(12);
+  }
+#undef SUBSTAMP
+  // CTA sums -> 64-bit fixed point -> global totals (integer atomics: order free)
+  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
+    const int l = e / k, j = e - l * k;
+    const long long v = __double2ll_rn(gsum[l * kq + j] * p.fx_scale);
+    if (v != 0) atomicAdd(gdst + e, (unsigned long long)v);
+  }
+  for (int e = threadIdx.x; e < k; e += blockDim.x)
+    if (gcnt[e] != 0) atomicAdd(gdst + kk + e, (unsigned long long)gcnt[e]);
+  __syncthreads();
+}
+
+// Exact (f64) second-best scores of every row of this CTA, before the rare
+// empty-cluster reseed picks the largest margin (engine.py:170-179).
+template <int KMAX>
+__device__ void exact_margins(const DiscParams& p, const double* sR64, double* wq) {
+  const Rows R = my_rows(p.n);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t i = R.r0 + warp; i < R.r1; i += kDiscThreads / 32) {
+    int lab;
+    float second;
+    score_row_exact_warp(p, sR64, i, wq + warp * 64, lab, second);
+    if (lane == 0) p.margin[i] = second;
   }
   __syncthreads();
 }
@@ -720,7 +1157,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 
 template <int KMAX>
-__global__ void __launch_bounds__(kDiscThreads, (KMAX > 8 && KMAX <= 48) ? 2 : 1)
+__global__ void __launch_bounds__(kDiscThreads, 1)
 discretize_kernel(DiscParams p) {
   unsigned long long t_prev = 0;
   cg::grid_group grid = cg::this_grid();
@@ -728,17 +1165,24 @@ discretize_kernel(DiscParams p) {
   const int k = p.k, kk = k * k, kp = kpad4(k);
   const int G = p.groups;
   const int nb = gridDim.x;
-  // persistent: scoring rotation (f32, rows padded to kp) and prototype rotation (f64)
+  // persistent: scoring rotation (f32, rows padded to kp; k > 8: TF32 B
+  // fragments) and prototype rotation (f64)
   float* sR = reinterpret_cast<float*>(smraw);
+  const uint4* sRf = reinterpret_cast<const uint4*>(smraw);
+  const double* sR64 = reinterpret_cast<const double*>(smraw + (KMAX > 8 ? disc_frag_bytes(k) : 0));
   double* sRp = reinterpret_cast<double*>(smraw + align_dev(disc_rot_bytes(k, (int)(p.col0 & 3))));
   unsigned char* dyn = smraw + align_dev(disc_rot_bytes(k, (int)(p.col0 & 3))) + align_dev((size_t)kk * 8);
   // phase-A view (k <= 8: G f64 accumulator groups; k > 8: split fixed-point totals)
   double* acc = reinterpret_cast<double*>(dyn);
   unsigned int* accx = reinterpret_cast<unsigned int*>(dyn);
+  long long* gacc = reinterpret_cast<long long*>(dyn);
+  int* gcnt = reinterpret_cast<int*>(dyn + align_dev(disc_tc_acc_bytes(k, G)));
   float* tile = reinterpret_cast<float*>(
-      dyn + align_dev(KMAX > 8 ? (2 * (size_t)kk + k) * 4 : (size_t)G * kk * 8));
+      KMAX > 8 ? dyn + align_dev(disc_tc_acc_bytes(k, G)) + align_dev((size_t)G * k * 4)
+               : dyn + align_dev((size_t)G * kk * 8));
   int* tlab = reinterpret_cast<int*>(reinterpret_cast<unsigned char*>(tile) +
-                                     align_dev(disc_tile_bytes(k, (int)(p.col0 & 3))));
+                                     align_dev(KMAX > 8 ? disc_tc_tile_bytes(k, (int)(p.col0 & 3), p.dbuf)
+                                                        : disc_tile_bytes(k, (int)(p.col0 & 3))));
   int* cnt = tlab + kDiscThreads;
   // phase-B view (aliases phase A)
   double* M = reinterpret_cast<double*>(dyn);
@@ -762,12 +1206,20 @@ discretize_kernel(DiscParams p) {
   int final_rounds[2] = {0, 0};
   double final_conv[2] = {0.0, 0.0};
   int empties_left[2] = {0, 0};
+  (void)accx;
+  if (KMAX > 8) {            // q~ once per call (the rounds read the f32 copy)
+    const int z = normalize_rows(p);
+    if (threadIdx.x == 0) s_zero = 0;
+    __syncthreads();
+    if (z) atomicAdd(&s_zero, z);
+    __syncthreads();
+  }
 
   for (int run = p.run_lo; run < p.run_hi; ++run) {
     // ---------------------------------------------------- initial rotation
     if (run == 0) {
       if (KMAX > 8)
-        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [](int l, int j) { return l == j ? 1.0 : 0.0; });
+        store_rot_frag(smraw, k, [](int l, int j) { return l == j ? 1.0 : 0.0; });
       else
         for (int e = threadIdx.x; e < k * kp; e += blockDim.x) sR[e] = (e / kp == e % kp) ? 1.f : 0.f;
       if (cta0) for (int e = threadIdx.x; e < kk; e += blockDim.x) p.Rg[e] = (e / k == e % k) ? 1.0 : 0.0;
@@ -845,7 +1297,7 @@ discretize_kernel(DiscParams p) {
         __syncthreads();
       }
       if (KMAX > 8)
-        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [&](int l, int j) { return sRp[l * k + j]; });
+        store_rot_frag(smraw, k, [&](int l, int j) { return sRp[l * k + j]; });
       else
         for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
           sR[e] = e % kp < k ? (float)sRp[(e / kp) * k + e % kp] : 0.f;
@@ -860,9 +1312,8 @@ discretize_kernel(DiscParams p) {
     for (int it = 0; it < p.max_iter; ++it) {
       TSTAMP(0);
       if (KMAX > 8)
-        phase_accumulate_wide<KMAX>(p, sR, tile, tlab, accx, true,
-                                    (run == 0 && it == 0) ? &s_zero : nullptr,
-                                    p.gfx + (size_t)(ri % 3) * (kk + k), vec);
+        phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, true,
+                                  p.gfx + (size_t)(ri % 3) * (kk + k));
       else
         phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, true,
                                (run == 0 && it == 0) ? &s_zero : nullptr,
@@ -884,6 +1335,8 @@ discretize_kernel(DiscParams p) {
       int nempty = 0;
       for (int c = 0; c < k; ++c) nempty += sizes[c] == 0;
       if (nempty > 0 && k >= 2) {
+        if (KMAX > 8)
+          exact_margins<KMAX>(p, sR64, reinterpret_cast<double*>(tlab + 4 * kDiscThreads + 68 + 64));
         // _reseed_empty_columns (engine.py:162-180): every CTA tracks sizes
         for (int c = 0; c < k; ++c) {
           if (sizes[c] != 0) continue;
@@ -914,8 +1367,8 @@ discretize_kernel(DiscParams p) {
           __syncthreads();
         }
         if (KMAX > 8)
-          phase_accumulate_wide<KMAX>(p, sR, tile, tlab, accx, false, nullptr,
-                                      p.gfx + (size_t)(ri % 3) * (kk + k), vec);
+          phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, false,
+                                    p.gfx + (size_t)(ri % 3) * (kk + k));
         else
           phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, false, nullptr,
                                  p.gfx + (size_t)(ri % 3) * (kk + k));
@@ -949,7 +1402,7 @@ discretize_kernel(DiscParams p) {
       }
       // next rotation R = V U^T (engine.py:205)
       if (KMAX > 8)
-        store_rot_win<KMAX>(sR, k, (int)(p.col0 & 3), [&](int l, int j) { return X[l * k + j]; });
+        store_rot_frag(smraw, k, [&](int l, int j) { return X[l * k + j]; });
       else
         for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
           sR[e] = e % kp < k ? (float)X[(e / kp) * k + e % kp] : 0.f;
@@ -1021,21 +1474,29 @@ __global__ void discretize_finish_kernel(const double* __restrict__ fin, double*
 
 using namespace ancka;
 
-static int disc_groups(int k) {
-  int g = kDiscThreads / k;
-  const int cap = (int)((96 * 1024) / ((size_t)k * k * 8));
-  if (g > cap) g = cap;
-  return g < 1 ? 1 : g;
-}
-
-static size_t disc_smem(int k, int G, int off) {
+static size_t disc_smem(int k, int G, int off, int dbuf = 1) {
   const size_t kk = (size_t)k * k;
   const size_t fixed = align_dev(disc_rot_bytes(k, off)) + align_dev(kk * 8);
-  const size_t acc = k > 8 ? (2 * kk + k) * 4 : (size_t)G * kk * 8;
-  const size_t a = align_dev(acc) + align_dev(disc_tile_bytes(k, off)) +
-                   (kDiscThreads + (size_t)G * k) * 4;
+  const size_t a = k > 8 ? align_dev(disc_tc_acc_bytes(k, G)) + align_dev((size_t)G * k * 4) +
+                               align_dev(disc_tc_tile_bytes(k, off, dbuf)) +
+                               (4 * kDiscThreads + 68 + 64) * 4 + 8 * 64 * 8 + 8 * 64 * 4
+                         : align_dev((size_t)G * kk * 8) + align_dev(disc_tile_bytes(k, off)) +
+                               (kDiscThreads + (size_t)G * k) * 4;
   const size_t b = 4 * kk * 8 + (size_t)k * 8;
   return fixed + std::max(a, b) + 64;
+}
+
+// accumulator groups: k <= 8 f64 groups of k x k; k > 8 fixed-point groups
+// of k x kq, as many as the threads and ~210 KB of shared memory allow
+static int disc_groups(int k, int off) {
+  if (k <= 8) {
+    int g = kDiscThreads / k;
+    const int cap = (int)((96 * 1024) / ((size_t)k * k * 8));
+    if (g > cap) g = cap;
+    return g < 1 ? 1 : g;
+  }
+  (void)off;
+  return 1;          // one accumulator: buckets give each (label, column) one owner
 }
 
 static int disc_grid_cap() { return 4 * kNumSMs; }
@@ -1047,6 +1508,10 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   cv.take<int32_t>(n);              // labels_run0
   cv.take<double>(n);               // proto_acc
   cv.take<double>(8);               // fin
+  if (k > 8) {
+    cv.take<float>((size_t)n * disc_kq(k));   // qn
+    cv.take<double>(n);                       // qinv
+  }
   for (int r = 0; r < 2; ++r) {     // per start (split launches run concurrently)
     cv.take<float>(n);              // margin
     cv.take<int64_t>((size_t)2 * grid * k);
@@ -1060,7 +1525,7 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
 template <int KMAX>
 static int launch_disc(DiscParams& p, cudaStream_t st, int sm_share) {
   auto kern = discretize_kernel<KMAX>;
-  const size_t smem = disc_smem(p.k, p.groups, (int)(p.col0 & 3));
+  const size_t smem = disc_smem(p.k, p.groups, (int)(p.col0 & 3), p.dbuf);
   ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
   ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kDiscThreads, smem));
@@ -1136,6 +1601,10 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   p.labels_run0 = cv.take<int32_t>(n);
   p.proto_acc = cv.take<double>(n);
   p.fin = cv.take<double>(8);
+  if (k > 8) {
+    p.qn = cv.take<float>((size_t)n * disc_kq(k));
+    p.qinv = cv.take<double>(n);
+  }
   DiscParams pr[2];
   for (int r = 0; r < 2; ++r) {
     pr[r] = p;
@@ -1152,16 +1621,18 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   }
   p.info = info;
   p.tdbg = getenv("ANCKA_DISC_TIMING") ? (unsigned long long*)(info + 8 + 2 * (size_t)max_iter + 2 * (size_t)k * k) : nullptr;
-  p.groups = disc_groups(k);
+  p.groups = disc_groups(k, (int)(col0 & 3));
+  p.dbuf = disc_smem(k, p.groups, (int)(col0 & 3), 1) <= 200 * 1024 ? 1 : 0;
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize: workspace too small");
   auto st = as_stream(stream);
-  ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 8 : 0)), st));
+  ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k + (p.tdbg ? 16 : 0)), st));
   for (int r = 0; r < 2; ++r) {
     ANCKA_CUDA(cudaMemsetAsync(pr[r].gfx, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
     pr[r].fx_scale = p.fx_scale;
     pr[r].info = p.info;
     pr[r].tdbg = p.tdbg;
     pr[r].groups = p.groups;
+    pr[r].dbuf = p.dbuf;
   }
   if (!disc_split(n, k)) {
     DiscParams q = pr[0];

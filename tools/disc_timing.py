@@ -29,7 +29,7 @@ else:
     q = res.state.q_dev
     k = inst.k
 lab = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
-info = torch.zeros(8 + 200 + 2 * k * k + 8, dtype=torch.float64, device=q.device)
+info = torch.zeros(8 + 200 + 2 * k * k + 16, dtype=torch.float64, device=q.device)
 for rep in range(3):
     info.zero_()
     torch.cuda.synchronize()
@@ -43,3 +43,7 @@ for rep in range(3):
     inf = info[:8].cpu().numpy()
     print(f"total {a.elapsed_time(b)*1e3:.0f} us rounds={inf[6]:.0f}+{inf[7]:.0f}",
           {names[i]: int(t[i]) // 1000 for i in (1, 2, 4, 5, 6)}, "us; NS iterations", int(t[7]))
+    if len(t) > 8:
+        sub = ["wait+stage", "score+argmax", "rescore", "sort", "accumulate"]
+        print("   CTA0 clocks (M):", {sub[j]: round(int(t[8 + j]) / 1e6, 2) for j in range(5)},
+              "flagged rows (CTA0):", int(t[14]))
