@@ -10,8 +10,10 @@
 //      rotating global total in 64-bit fixed point (integer atomics: the sum
 //      is independent of order, hence bit-reproducible).  k <= 8: thread per
 //      row with direct loads, per-group f64 sums, one atomic per entry and
-//      CTA; k > 8: rows staged through shared memory as aligned column
-//      windows, per-CTA split 32-bit fixed-point shared atomics.
+//      CTA; k > 8: q~ normalised once per call, 3xFP16 warp-MMA scores with
+//      a certified margin (uncertified rows rescored exactly in f64), a
+//      stable per-tile bucket sort by label and f64 cluster sums per CTA
+//      (see phase_accumulate_tc).
 //   -- one grid barrier --
 //   B  every CTA, redundantly and identically: read M (k x k) and the
 //      cluster sizes from the totals; Y~ = Y/size (the reference's 1/size,
@@ -238,18 +240,6 @@ struct Win {
   static constexpr int SW = win_sw(KMAX);
 };
 
-// sR4[jb * KW + m] = R[m - off][4 jb .. 4 jb + 3] (zero outside), R from get(l, j)
-template <int KMAX, typename Get>
-__device__ __forceinline__ void store_rot_win(float* sR, int k, int off, Get get) {
-  constexpr int KW = Win<KMAX>::KW;
-  const int nb = (k + 3) >> 2;
-  for (int e = threadIdx.x; e < nb * KW * 4; e += blockDim.x) {
-    const int jb = e / (KW * 4), rem = e % (KW * 4), m = rem >> 2, j = jb * 4 + (rem & 3);
-    const int l = m - off;
-    sR[e] = (l >= 0 && l < k && j < k) ? (float)get(l, j) : 0.f;
-  }
-}
-
 // Stage rows [t0, t0 + tr) of Q's column window into tile (async copies).
 __device__ __forceinline__ void stage_window(const DiscParams& p, int64_t t0, int tr, float* tile,
                                              int SW, bool vec) {
@@ -306,122 +296,6 @@ __device__ __forceinline__ void load_window(const float* rowp, int off, int k,
   for (int m = 0; m < KW; ++m) raw[m] = (m >= off && m < off + k) ? raw[m] : 0.f;
 }
 
-// Phase A for k > 8.  Thread per row scores against R; the normalised tile is
-// then folded into per-CTA fixed-point totals [(label, column)] by integer
-// shared-memory atomics over the flat (row, column) index: the 32 entries a
-// warp touches span at most two rows with disjoint column ranges, so the
-// addresses never collide.  Shared-memory 64-bit atomic add is a CAS loop on
-// sm_100, so each 64-bit value v = hi * 2^32 + lo is added as two native
-// 32-bit atomics, the carry out of the low word detected from its returned
-// old value.  Integer sums are order-free (bit-reproducible); the CTA totals
-// then go to the rotating global buffer `gdst` (same scheme as the k <= 8
-// path, one grid barrier per round).
-// acc layout: lo[k*k] (u32) | hi[k*k] (i32) | count[k] (u32)
-template <int KMAX>
-__device__ void phase_accumulate_wide(const DiscParams& p, const float* sR, float* tile, int* tlab,
-                                      unsigned int* acc, bool score, int* zeros_out,
-                                      unsigned long long* gdst, bool vec) {
-  constexpr int KW = Win<KMAX>::KW, SW = Win<KMAX>::SW;
-  const int k = p.k, kk = k * k, off = (int)(p.col0 & 3);
-  unsigned int* acc_lo = acc;
-  int* acc_hi = reinterpret_cast<int*>(acc + kk);
-  unsigned int* acc_n = acc + 2 * kk;
-  for (int e = threadIdx.x; e < 2 * kk + k; e += blockDim.x) acc[e] = 0u;
-  const float fsc = (float)p.fx_scale;   // power of two: v * fsc is exact in f32
-  const float4* R4 = reinterpret_cast<const float4*>(sR);
-  const Rows R = my_rows(p.n);
-  int zeros = 0;
-  for (int64_t t0 = R.r0; t0 < R.r1; t0 += kDiscThreads) {
-    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
-    stage_window(p, t0, tr, tile, SW, vec);
-    const int64_t i = t0 + threadIdx.x;
-    if (threadIdx.x < tr) {
-      float* rowp = tile + threadIdx.x * SW;
-      float qf[KW];
-      load_window<KMAX>(rowp, off, k, qf);
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < KW; ++m) s += (double)qf[m] * (double)qf[m];
-      const double nrm = sqrt(s);
-      const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
-#pragma unroll
-      for (int m = 0; m < KW; ++m) qf[m] = (float)((double)qf[m] * inv);
-      if (nrm == 0.0) ++zeros;
-      int lab = 0;
-      if (score) {
-        // scores = q~ R, four columns per pass; a uniform exit per 8 window columns
-        float best = -INFINITY, second = -INFINITY;
-        for (int jb = 0; jb * 4 < k; ++jb) {
-          const float4* c = R4 + jb * KW;
-          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-#pragma unroll
-          for (int m0 = 0; m0 < KW; m0 += 4) {
-            if (m0 >= off + k) break;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4 r = c[m0 + u];
-              s0 = fmaf(qf[m0 + u], r.x, s0);
-              s1 = fmaf(qf[m0 + u], r.y, s1);
-              s2 = fmaf(qf[m0 + u], r.z, s2);
-              s3 = fmaf(qf[m0 + u], r.w, s3);
-            }
-          }
-          const float sc[4] = {s0, s1, s2, s3};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float sv = sc[u];
-            if (jb * 4 + u < k) {
-              if (sv > best) { second = best; best = sv; lab = jb * 4 + u; }
-              else if (sv > second) second = sv;
-            }
-          }
-        }
-        p.labels[i] = lab;
-        p.margin[i] = second;
-      } else {
-        lab = p.labels[i];
-      }
-#pragma unroll
-      for (int m4 = 0; m4 < KW / 4; ++m4)
-        if (4 * m4 < off + k)
-          *reinterpret_cast<float4*>(rowp + 4 * m4) =
-              make_float4(qf[4 * m4], qf[4 * m4 + 1], qf[4 * m4 + 2], qf[4 * m4 + 3]);
-      tlab[threadIdx.x] = lab;
-    }
-    __syncthreads();
-    {
-      const int ne = tr * k, dr = kDiscThreads / k, dl = kDiscThreads % k;
-      int r = threadIdx.x / k, l = threadIdx.x % k;
-      for (int e = threadIdx.x; e < ne; e += kDiscThreads) {
-        const int lab = tlab[r], a = lab * k + l;
-        const long long v = __float2ll_rn(tile[r * SW + off + l] * fsc);
-        const unsigned int lo = (unsigned int)v;
-        const unsigned int old = atomicAdd(acc_lo + a, lo);
-        atomicAdd(acc_hi + a, (int)(v >> 32) + (old + lo < old ? 1 : 0));
-        if (l == 0) atomicAdd(acc_n + lab, 1u);
-        r += dr;
-        l += dl;
-        if (l >= k) { l -= k; ++r; }
-      }
-    }
-    __syncthreads();
-  }
-  for (int e = threadIdx.x; e < kk; e += blockDim.x) {
-    const long long v = (long long)((unsigned long long)(long long)acc_hi[e] << 32) + acc_lo[e];
-    if (v != 0) atomicAdd(gdst + e, (unsigned long long)v);
-  }
-  for (int e = threadIdx.x; e < k; e += blockDim.x)
-    if (acc_n[e] != 0u) atomicAdd(gdst + kk + e, (unsigned long long)acc_n[e]);
-  if (zeros_out) {
-    __shared__ int zsum;
-    if (threadIdx.x == 0) zsum = 0;
-    __syncthreads();
-    atomicAdd(&zsum, zeros);
-    __syncthreads();
-    if (threadIdx.x == 0) *zeros_out = zsum;
-  }
-  __syncthreads();
-}
 
 // ---- k > 8: tensor-core scoring.  The block is normalised once per call
 // into q~ (f32, kq = 8 ceil(k / 8) columns, zero padded); each round scores a
@@ -1174,7 +1048,6 @@ discretize_kernel(DiscParams p) {
   unsigned char* dyn = smraw + align_dev(disc_rot_bytes(k, (int)(p.col0 & 3))) + align_dev((size_t)kk * 8);
   // phase-A view (k <= 8: G f64 accumulator groups; k > 8: split fixed-point totals)
   double* acc = reinterpret_cast<double*>(dyn);
-  unsigned int* accx = reinterpret_cast<unsigned int*>(dyn);
   long long* gacc = reinterpret_cast<long long*>(dyn);
   int* gcnt = reinterpret_cast<int*>(dyn + align_dev(disc_tc_acc_bytes(k, G)));
   float* tile = reinterpret_cast<float*>(
@@ -1206,7 +1079,6 @@ discretize_kernel(DiscParams p) {
   int final_rounds[2] = {0, 0};
   double final_conv[2] = {0.0, 0.0};
   int empties_left[2] = {0, 0};
-  (void)accx;
   if (KMAX > 8) {            // q~ once per call (the rounds read the f32 copy)
     const int z = normalize_rows(p);
     if (threadIdx.x == 0) s_zero = 0;

@@ -22,8 +22,10 @@ if len(sys.argv) > 1:   # synthetic block: tools/disc_timing.py n k  (planted + 
     q[torch.arange(n, device="cuda"), lab0 + 1] = 1.0
     q[:, 1:k + 1] += 0.3 * torch.randn((n, k), device="cuda", generator=g)
 else:
-    inst = synth.make("dblp", seed=0)
-    net = ancka.AttributedNetwork.hypergraph(inst.structure, inst.X)
+    shape = os.environ.get("SHAPE", "dblp")
+    inst = synth.make(shape, seed=0)
+    net = (ancka.AttributedNetwork.hypergraph(inst.structure, inst.X) if inst.kind == "hypergraph"
+           else ancka.AttributedNetwork.graph(inst.structure, inst.X))
     params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
     res = ancka.run_ancka(net, params)
     q = res.state.q_dev
