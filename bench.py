@@ -285,7 +285,7 @@ def kernel_rooflines(prep, res, inst, hbm, bf16):
     fp8 = prep.x_level == 2
     peak = 4500.0 if fp8 else bf16
     out["knn"] = {"kernel": ("knn_tc_kernel (tcgen05 kind::f8f6f4, exact integer)" if fp8 else
-                             "knn_real_res_kernel (tcgen05 split-bf16) + certified f64 re-rank"),
+                             "knn_real16_kernel (tcgen05 kind::f16, fp16 operands) + certified f64 re-rank"),
                   "bound": "tensor", "achieved": round(flops / (knn_ms * 1e-3) / 1e12, 1),
                   "peak": peak, "unit": "TFLOP/s",
                   "frac": round(flops / (knn_ms * 1e-3) / 1e12 / peak, 4),

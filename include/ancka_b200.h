@@ -132,6 +132,39 @@ int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices, const dou
                         int64_t q_end, int32_t* ids, double* scores, void* workspace,
                         size_t workspace_bytes, ancka_stream_t stream);
 
+/* Same searches restricted to the key rows [k0, k1) (k0 a multiple of 256):
+ * the query-stationary ring of the multi-GPU path computes its own rows
+ * against each visiting key block once (reference knn.py:112-140 blocked
+ * over keys).  Rows the real-valued certificate rejects are rescanned
+ * against all keys; merge with ancka_knn_merge_lists (de-duplicating). */
+int ancka_knn_exact_keys(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
+                         int32_t integer_exact, int64_t q_begin, int64_t q_end, int64_t k0,
+                         int64_t k1, int32_t* ids, double* scores, void* workspace,
+                         size_t workspace_bytes, ancka_stream_t stream);
+int ancka_knn_exact_csr_keys(const int64_t* indptr, const int32_t* indices, const double* data,
+                             int64_t n, int64_t d, int32_t K, int32_t integer_exact,
+                             int64_t q_begin, int64_t q_end, int64_t k0, int64_t k1, int32_t* ids,
+                             double* scores, void* workspace, size_t workspace_bytes,
+                             ancka_stream_t stream);
+
+/* Per row, merge two neighbour lists (each ordered by score desc, id asc,
+ * -1 padded) into the first K of their union by the same order, dropping
+ * repeated ids (knn.py:83-98 applied across key blocks).  In place into
+ * (ids_a, scores_a). */
+int ancka_knn_merge_lists(int32_t* ids_a, double* scores_a, const int32_t* ids_b,
+                          const double* scores_b, int64_t nq, int32_t K, ancka_stream_t stream);
+
+/* KNN-graph rows from COO entries (local row, global column, score): the
+ * per-rank rows of A_K = M + M^T after the all-to-all of transposed
+ * triples, then P_K rows (same sums/normalisation as ancka_knn_graph).
+ * Capacities: colidx/val arrays hold E entries. */
+size_t ancka_knn_graph_coo_workspace_size(int64_t E);
+int ancka_knn_graph_coo(const int32_t* rows, const int32_t* cols, const double* vals, int64_t E,
+                        int64_t nrows, int64_t ncols, int64_t* rowptr, int32_t* colidx,
+                        double* a_k, double* p_k64, float* p_k32, uint8_t* zero_rows,
+                        int64_t* nnz_out, void* workspace, size_t workspace_bytes,
+                        ancka_stream_t stream);
+
 /* build_knn_adjacency + knn_transition (knn.py:294-324): A_K = M + M^T as a
  * sorted CSR and P_K = D_K^-1 A_K with row sums summed exactly as numpy's
  * pairwise reduction (so f64 values are bit-identical to scipy's).

@@ -61,6 +61,18 @@ _SIGS = {
                                  c_size_t, c_void_p]),
     "ancka_cholqr_apply_f32": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,
                                          c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_knn_exact_keys": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32,
+                                       c_int64, c_int64, c_int64, c_int64, c_void_p, c_void_p,
+                                       c_void_p, c_size_t, c_void_p]),
+    "ancka_knn_exact_csr_keys": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64,
+                                           c_int32, c_int32, c_int64, c_int64, c_int64, c_int64,
+                                           c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_knn_merge_lists": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
+                                        c_void_p]),
+    "ancka_knn_graph_coo_workspace_size": (c_size_t, [c_int64]),
+    "ancka_knn_graph_coo": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_size_t, c_void_p]),
     "ancka_knn_graph_workspace_size": (c_size_t, [c_int64, c_int32]),
     "ancka_knn_graph": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

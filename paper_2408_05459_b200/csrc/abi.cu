@@ -90,6 +90,42 @@ extern "C" int ancka_knn_exact_csr(const int64_t* indptr, const int32_t* indices
                     workspace_bytes, as_stream(stream), integer_exact == 2);
 }
 
+// Query rows [q_begin, q_end) against the key rows [k0, k1) only (k0 a
+// multiple of 256): the own-rows x visiting-block products of the multi-GPU
+// key ring.  Rows the real-valued certificate rejects are rescanned against
+// all n keys (callers merge lists with de-duplication).
+extern "C" int ancka_knn_exact_keys(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t K,
+                                    int32_t integer_exact, int64_t q_begin, int64_t q_end,
+                                    int64_t k0, int64_t k1, int32_t* ids, double* scores,
+                                    void* workspace, size_t workspace_bytes,
+                                    ancka_stream_t stream) {
+  ANCKA_REQUIRE(K >= 1 && d >= 1 && K < n, ANCKA_ERR_ARG, "knn: bad sizes");
+  ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
+  ANCKA_REQUIRE(k0 >= 0 && k0 % 256 == 0 && k0 < k1 && k1 <= n, ANCKA_ERR_ARG, "knn: bad key range");
+  auto st = as_stream(stream);
+  const KeyRange kr{k0, k1};
+  if (integer_exact > 0)
+    return knn_tc(X, n, d, ldx, K, q_begin, q_end, ids, scores, workspace, workspace_bytes, st,
+                  integer_exact == 2, kr);
+  ANCKA_REQUIRE(integer_exact == 0, ANCKA_ERR_UNSUPPORTED, "key ranges need a tensor-core path");
+  return knn_real(X, n, d, ldx, K, q_begin, q_end, ids, scores, workspace, workspace_bytes, st, kr);
+}
+
+extern "C" int ancka_knn_exact_csr_keys(const int64_t* indptr, const int32_t* indices,
+                                        const double* data, int64_t n, int64_t d, int32_t K,
+                                        int32_t integer_exact, int64_t q_begin, int64_t q_end,
+                                        int64_t k0, int64_t k1, int32_t* ids, double* scores,
+                                        void* workspace, size_t workspace_bytes,
+                                        ancka_stream_t stream) {
+  ANCKA_REQUIRE(K >= 1 && K < n, ANCKA_ERR_ARG, "knn: bad sizes");
+  ANCKA_REQUIRE(integer_exact == 1 || integer_exact == 2, ANCKA_ERR_UNSUPPORTED,
+                "CSR attributes are supported on the integer-exact tensor-core path only");
+  ANCKA_REQUIRE(0 <= q_begin && q_begin < q_end && q_end <= n, ANCKA_ERR_ARG, "knn: bad query range");
+  ANCKA_REQUIRE(k0 >= 0 && k0 % 256 == 0 && k0 < k1 && k1 <= n, ANCKA_ERR_ARG, "knn: bad key range");
+  return knn_tc_csr(indptr, indices, data, n, d, K, q_begin, q_end, ids, scores, workspace,
+                    workspace_bytes, as_stream(stream), integer_exact == 2, KeyRange{k0, k1});
+}
+
 extern "C" int ancka_knn_fallback_rows(void* workspace, size_t workspace_bytes, int64_t n, int64_t d,
                                        int32_t K, int64_t q_begin, int64_t q_end,
                                        int32_t* out_rows) {

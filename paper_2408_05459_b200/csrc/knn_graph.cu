@@ -80,6 +80,53 @@ __global__ void knn_finish_kernel(const uint64_t* __restrict__ ukeys, const doub
   }
 }
 
+__global__ void knn_coo_keys_kernel(const int32_t* __restrict__ rows, const int32_t* __restrict__ cols,
+                                    const double* __restrict__ vals, int64_t E,
+                                    uint64_t* __restrict__ keys, double* __restrict__ kv) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < E;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    keys[p] = ((uint64_t)(uint32_t)rows[p] << 32) | (uint32_t)cols[p];
+    kv[p] = vals[p];
+  }
+}
+
+// thread per row: two (score desc, id asc) lists -> first K of the union
+__global__ void knn_merge_lists_kernel(int32_t* __restrict__ ia, double* __restrict__ sa,
+                                       const int32_t* __restrict__ ib, const double* __restrict__ sb,
+                                       int64_t nq, int K) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nq;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int32_t oi[32];
+    double os[32];
+    const int32_t* A = ia + r * K;
+    const double* As = sa + r * K;
+    const int32_t* B = ib + r * K;
+    const double* Bs = sb + r * K;
+    int pa = 0, pb = 0, m = 0;
+    while (m < K) {
+      const bool va = pa < K && A[pa] >= 0, vb = pb < K && B[pb] >= 0;
+      if (!va && !vb) break;
+      bool takeA;
+      if (!vb) takeA = true;
+      else if (!va) takeA = false;
+      else takeA = As[pa] > Bs[pb] || (As[pa] == Bs[pb] && A[pa] < B[pb]);
+      const int32_t id = takeA ? A[pa] : B[pb];
+      const double sc = takeA ? As[pa] : Bs[pb];
+      if (takeA) ++pa; else ++pb;
+      bool dup = false;
+      for (int q = 0; q < m; ++q) dup |= oi[q] == id;
+      if (dup) continue;
+      oi[m] = id;
+      os[m] = sc;
+      ++m;
+    }
+    for (int q = 0; q < K; ++q) {
+      ia[r * K + q] = q < m ? oi[q] : -1;
+      sa[r * K + q] = q < m ? os[q] : 0.0;
+    }
+  }
+}
+
 struct GraphWs {
   uint64_t *k0, *k1, *ukeys;
   double *v0, *v1, *agg;
@@ -155,6 +202,85 @@ extern "C" int ancka_knn_graph(const int32_t* ids, const double* scores, int64_t
   knn_rowptr_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.nruns, n, rowptr, nnz_out);
   ANCKA_LAUNCHED();
   knn_finish_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.agg, rowptr, n, colidx, a_k,
+                                                     p_k64, p_k32, zero_rows);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+extern "C" int ancka_knn_merge_lists(int32_t* ids_a, double* scores_a, const int32_t* ids_b,
+                                     const double* scores_b, int64_t nq, int32_t K,
+                                     ancka_stream_t stream) {
+  ANCKA_REQUIRE(K >= 1 && K <= 32, ANCKA_ERR_UNSUPPORTED, "merge_lists: K must be in [1, 32]");
+  if (nq <= 0) return ANCKA_OK;
+  const int g = (int)std::min<int64_t>(ceil_div(nq, 128), 16 * kNumSMs);
+  knn_merge_lists_kernel<<<g, 128, 0, as_stream(stream)>>>(ids_a, scores_a, ids_b, scores_b, nq, K);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+static int carve_graph_coo(Carver& cv, GraphWs& w, int64_t E, int64_t nrows) {
+  w.k0 = cv.take<uint64_t>(E);
+  w.k1 = cv.take<uint64_t>(E);
+  w.ukeys = cv.take<uint64_t>(E);
+  w.v0 = cv.take<double>(E);
+  w.v1 = cv.take<double>(E);
+  w.agg = cv.take<double>(E);
+  w.nruns = cv.take<int64_t>(1);
+  size_t sort_bytes = 0, red_bytes = 0;
+  cub::DoubleBuffer<uint64_t> kb(nullptr, nullptr);
+  cub::DoubleBuffer<double> vb(nullptr, nullptr);
+  if (cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, kb, vb, E, 0, 32 + bits_for(nrows)) !=
+      cudaSuccess)
+    return ANCKA_ERR_CUDA;
+  if (cub::DeviceReduce::ReduceByKey(nullptr, red_bytes, (uint64_t*)nullptr, (uint64_t*)nullptr,
+                                     (double*)nullptr, (double*)nullptr, (int64_t*)nullptr, SumOp(),
+                                     E) != cudaSuccess)
+    return ANCKA_ERR_CUDA;
+  w.cub_bytes = std::max(sort_bytes, red_bytes);
+  w.cub_tmp = cv.take<char>(w.cub_bytes);
+  return ANCKA_OK;
+}
+
+extern "C" size_t ancka_knn_graph_coo_workspace_size(int64_t E) {
+  Carver cv(nullptr, 0);
+  GraphWs w;
+  if (carve_graph_coo(cv, w, std::max<int64_t>(E, 1), 1ll << 31) != ANCKA_OK) return 0;
+  return cv.used;
+}
+
+extern "C" int ancka_knn_graph_coo(const int32_t* rows, const int32_t* cols, const double* vals,
+                                   int64_t E, int64_t nrows, int64_t ncols, int64_t* rowptr,
+                                   int32_t* colidx, double* a_k, double* p_k64, float* p_k32,
+                                   uint8_t* zero_rows, int64_t* nnz_out, void* workspace,
+                                   size_t workspace_bytes, ancka_stream_t stream) {
+  ANCKA_REQUIRE(nrows >= 1 && E >= 0, ANCKA_ERR_ARG, "knn_graph_coo: bad sizes");
+  ANCKA_REQUIRE(ncols < (1ll << 31) && nrows < (1ll << 31), ANCKA_ERR_UNSUPPORTED,
+                "knn_graph_coo: ids must fit int32");
+  auto st = as_stream(stream);
+  const int gr = (int)std::min<int64_t>(ceil_div(nrows + 1, 256), 16 * kNumSMs);
+  if (E == 0) {
+    ANCKA_CUDA(cudaMemsetAsync(rowptr, 0, sizeof(int64_t) * (nrows + 1), st));
+    ANCKA_CUDA(cudaMemsetAsync(zero_rows, 1, nrows, st));
+    ANCKA_CUDA(cudaMemsetAsync(nnz_out, 0, sizeof(int64_t), st));
+    return ANCKA_OK;
+  }
+  Carver cv(workspace, workspace_bytes);
+  GraphWs w;
+  ANCKA_TRY(carve_graph_coo(cv, w, E, 1ll << 31));
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_graph_coo: workspace too small");
+  const int g = (int)std::min<int64_t>(ceil_div(E, 256), 16 * kNumSMs);
+  knn_coo_keys_kernel<<<std::max(g, 1), 256, 0, st>>>(rows, cols, vals, E, w.k0, w.v0);
+  ANCKA_LAUNCHED();
+  cub::DoubleBuffer<uint64_t> kb(w.k0, w.k1);
+  cub::DoubleBuffer<double> vb(w.v0, w.v1);
+  size_t bytes = w.cub_bytes;
+  ANCKA_CUDA(cub::DeviceRadixSort::SortPairs(w.cub_tmp, bytes, kb, vb, E, 0, 32 + bits_for(nrows), st));
+  bytes = w.cub_bytes;
+  ANCKA_CUDA(cub::DeviceReduce::ReduceByKey(w.cub_tmp, bytes, kb.Current(), w.ukeys, vb.Current(),
+                                            w.agg, w.nruns, SumOp(), E, st));
+  knn_rowptr_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.nruns, nrows, rowptr, nnz_out);
+  ANCKA_LAUNCHED();
+  knn_finish_kernel<<<std::max(gr, 1), 256, 0, st>>>(w.ukeys, w.agg, rowptr, nrows, colidx, a_k,
                                                      p_k64, p_k32, zero_rows);
   ANCKA_LAUNCHED();
   return ANCKA_OK;

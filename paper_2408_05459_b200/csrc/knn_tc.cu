@@ -142,7 +142,8 @@ struct TcParams {
   int d;              // attribute columns: MMA k-steps past d are skipped
   int nkb;            // k-blocks of 128 bytes along d
   int K;
-  int key_tiles;      // total key tiles of BN
+  int key_tiles;      // end key tile (exclusive) of BN
+  int kt_base;        // first key tile
   int tiles_per_seg;
   int nseg;
   const uint32_t* a_norm;   // n_pad
@@ -163,7 +164,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
   const int seg = blockIdx.y;
-  const int kt0 = seg * p.tiles_per_seg;
+  const int kt0 = p.kt_base + seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
   const int ntiles = kt1 - kt0;
   const uint32_t tmem = P.tmem;
@@ -328,16 +329,18 @@ struct TcLayout {
   bool fp8;
   int64_t n_pad, d_pad, d;
   int nseg, tiles_per_seg, key_tiles, q_tiles;
+  KeyRange kr;
 };
 
-static TcLayout tc_layout(int64_t n, int64_t d, bool fp8, int64_t nq) {
+static TcLayout tc_layout(int64_t n, int64_t d, bool fp8, int64_t nq, KeyRange kr = {0, -1}) {
   TcLayout L;
   L.fp8 = fp8;
   L.n_pad = ceil_div(n, tc::BN) * tc::BN;
   const int64_t elems_per_row = tc::ROW_BYTES / (fp8 ? 1 : 2);
   L.d_pad = ceil_div(d, elems_per_row) * elems_per_row;
   L.d = d;
-  const TcGrid g = tc_grid(n, nq);
+  const TcGrid g = tc_grid(n, nq, kr);
+  L.kr = {kr.k0, kr.k1 < 0 ? n : kr.k1};
   L.q_tiles = g.q_tiles;
   L.key_tiles = g.key_tiles;
   L.nseg = g.nseg;
@@ -414,10 +417,10 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
 
 int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data, int64_t n,
                int64_t d, int K, int64_t q_begin, int64_t q_end, int32_t* ids, double* scores,
-               void* ws, size_t wsb, cudaStream_t st, bool fp8) {
+               void* ws, size_t wsb, cudaStream_t st, bool fp8, KeyRange kr) {
   ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
   ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
-  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin);
+  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin, kr);
   Carver cv(ws, wsb);
   void* xq;
   uint32_t* an;
@@ -438,10 +441,10 @@ int knn_tc_csr(const int64_t* indptr, const int32_t* indices, const double* data
 
 int knn_tc(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
            int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st,
-           bool fp8) {
+           bool fp8, KeyRange kr) {
   ANCKA_REQUIRE(K <= 32, ANCKA_ERR_UNSUPPORTED, "tensor-core KNN supports K <= 32 (got %d)", K);
   ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
-  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin);
+  TcLayout L = tc_layout(n, d, fp8, q_end - q_begin, kr);
   Carver cv(ws, wsb);
   void* xq;
   uint32_t* an;
@@ -466,13 +469,14 @@ static int knn_tc_main(void* xq, uint32_t* an, float* isq, int* rb, int2* part, 
   ANCKA_TRY(tc_make_map(&ma, xq, fp8, L.n_pad, L.d_pad, tc::BM));
   ANCKA_TRY(tc_make_map(&mb, xq, fp8, L.n_pad, L.d_pad, tc::BN));
   TcParams p;
-  p.n = n;
+  p.n = L.kr.k1;                      // key index bound (masking)
+  p.kt_base = (int)(L.kr.k0 / tc::BN);
   p.d = (int)L.d;
   p.q_begin = q_begin;
   p.q_end = q_end;
   p.nkb = (int)(L.d_pad * (fp8 ? 1 : 2) / tc::ROW_BYTES);
   p.K = K;
-  p.key_tiles = L.key_tiles;
+  p.key_tiles = p.kt_base + L.key_tiles;
   p.tiles_per_seg = L.tiles_per_seg;
   p.nseg = L.nseg;
   p.a_norm = an;

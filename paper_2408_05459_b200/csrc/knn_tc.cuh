@@ -188,10 +188,17 @@ inline int tc_make_map(CUtensorMap* m, void* ptr, bool fp8, int64_t rows, int64_
 struct TcGrid {
   int q_tiles, key_tiles, nseg, tiles_per_seg;
 };
-inline TcGrid tc_grid(int64_t n, int64_t nq) {
+// keys: rows [k0, k1) of the key matrix, k0 a multiple of BN (the query-row
+// x key-block products of the multi-GPU ring); key_tiles then counts the
+// tiles of the range and kt_base is the first one
+struct KeyRange {
+  int64_t k0, k1;
+};
+inline TcGrid tc_grid(int64_t n, int64_t nq, KeyRange kr = {0, -1}) {
   TcGrid g;
+  const int64_t k1 = kr.k1 < 0 ? n : kr.k1;
   g.q_tiles = (int)ceil_div(nq, tc::BM);
-  g.key_tiles = (int)ceil_div(n, tc::BN);
+  g.key_tiles = (int)(ceil_div(k1, tc::BN) - kr.k0 / tc::BN);
   static const int waves = getenv("ANCKA_KNN_WAVES") ? atoi(getenv("ANCKA_KNN_WAVES")) : 8;
   int nseg = (int)ceil_div((int64_t)waves * kNumSMs, g.q_tiles);
   nseg = std::max(1, std::min(nseg, g.key_tiles));

@@ -363,7 +363,7 @@ knn_real_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
   const int seg = blockIdx.y;
-  const int kt0 = seg * p.tiles_per_seg;
+  const int kt0 = p.kt_base + seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
   const int ntiles = kt1 - kt0;
   const int nkb = 3 * p.nkb_seg;
@@ -422,7 +422,7 @@ knn_real_res_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_consta
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
   const int seg = blockIdx.y;
-  const int kt0 = seg * p.tiles_per_seg;
+  const int kt0 = p.kt_base + seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
   const int ntiles = kt1 - kt0;
   if (warp == 0 && lane == 0) {
@@ -785,14 +785,16 @@ struct RealLayout {
   int64_t n_pad, d_pad, ldn;
   TcGrid g;
   int lists;
+  KeyRange kr;
 };
 
-RealLayout real_layout(int64_t n, int64_t d, int64_t nq) {
+RealLayout real_layout(int64_t n, int64_t d, int64_t nq, KeyRange kr = {0, -1}) {
   RealLayout R;
   R.n_pad = ceil_div(n, tc::BN) * tc::BN;
   R.d_pad = ceil_div(d, 64) * 64;
   R.ldn = ceil_div(d, 16) * 16;
-  R.g = tc_grid(n, nq);
+  R.g = tc_grid(n, nq, kr);
+  R.kr = {kr.k0, kr.k1 < 0 ? n : kr.k1};
   R.lists = R.g.nseg * (tc::EPI_WARPS / 4);
   return R;
 }
@@ -873,19 +875,19 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
   ANCKA_TRY(tc_make_map(&ma, H, false, R.n_pad, R.d_pad, tc::BM));
   ANCKA_TRY(tc_make_map(&mb, H, false, R.n_pad, R.d_pad, tc::BN));
   RealParams p;
-  p.n = n;
+  p.n = R.kr.k1;                         // key index bound
   p.nkb_seg = (int)(R.d_pad / 64);
   p.d_pad = (int)R.d_pad;
   p.d = (int)d;
   p.K = K;
-  p.key_tiles = R.g.key_tiles;
+  p.key_tiles = (int)(R.kr.k0 / tc::BN) + R.g.key_tiles;
   p.tiles_per_seg = R.g.tiles_per_seg;
   p.nseg = R.g.nseg;
   p.eps = 0.f;
   p.band = 0.f;
   p.row_eps = w.row_eps;
   p.resume = 0;
-  p.kt_base = 0;
+  p.kt_base = (int)(R.kr.k0 / tc::BN);
   p.partial = w.part;
   p.row_bound = w.rb;
   p.q_begin = q_begin;
@@ -902,6 +904,7 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
   const int64_t key_bytes = (int64_t)tc::BN * R.d_pad * 2;
   int seg_tiles = (int)std::max<int64_t>(1, (40ll << 20) / key_bytes);
   if (const char* e = getenv("ANCKA_KNN_SEG_TILES")) seg_tiles = std::max(1, atoi(e));
+  const int kt_first = (int)(R.kr.k0 / tc::BN);
   const int nlaunch = (int)ceil_div(R.g.key_tiles, seg_tiles);
   int lists = R.lists;
   {
@@ -917,7 +920,7 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
       p.tiles_per_seg = seg_tiles;
       lists = tc::EPI_WARPS / 4;
       for (int l = 0; l < nlaunch; ++l) {
-        p.kt_base = l * seg_tiles;
+        p.kt_base = kt_first + l * seg_tiles;
         p.resume = l > 0;
         knn_real16_kernel<<<dim3(R.g.q_tiles, 1), tc::THREADS, sm, st>>>(ma, mb, p);
         ANCKA_LAUNCHED();
@@ -942,11 +945,14 @@ size_t knn_real_workspace(int64_t n, int64_t d, int K) {
 }
 
 int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t q_begin,
-             int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st) {
+             int64_t q_end, int32_t* ids, double* scores, void* ws, size_t wsb, cudaStream_t st,
+             KeyRange kr) {
   ANCKA_REQUIRE(K <= 24, ANCKA_ERR_UNSUPPORTED, "tensor-core real KNN supports K <= 24 (got %d)", K);
   ANCKA_REQUIRE(n < (1ll << 31), ANCKA_ERR_UNSUPPORTED, "tensor-core KNN: n too large");
   const int64_t nq = q_end - q_begin;
-  const RealLayout R = real_layout(n, d, nq);
+  const RealLayout R = real_layout(n, d, nq, kr);
+  ANCKA_REQUIRE(R.kr.k0 % tc::BN == 0 && R.kr.k0 < R.kr.k1 && R.kr.k1 <= n, ANCKA_ERR_ARG,
+                "knn: key range must start on a %d-row tile", tc::BN);
   Carver cv(ws, wsb);
   RealWs w;
   carve_real(cv, R, n, K, w);
@@ -961,12 +967,12 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
   ANCKA_TRY(tc_make_map(&ma, w.H, false, R.n_pad, 2 * R.d_pad, tc::BM));
   ANCKA_TRY(tc_make_map(&mb, w.H, false, R.n_pad, 2 * R.d_pad, tc::BN));
   RealParams p;
-  p.n = n;
+  p.n = R.kr.k1;                         // key index bound
   p.nkb_seg = (int)(R.d_pad / 64);
   p.d_pad = (int)R.d_pad;
   p.d = (int)d;
   p.K = K;
-  p.key_tiles = R.g.key_tiles;
+  p.key_tiles = (int)(R.kr.k0 / tc::BN) + R.g.key_tiles;
   p.tiles_per_seg = R.g.tiles_per_seg;
   p.nseg = R.g.nseg;
   // |a - s| <= 2^-16 (bf16 hi/lo split of two unit vectors, cross terms and
@@ -977,7 +983,7 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
   p.row_eps = nullptr;
   p.spin = 0;
   p.resume = 0;
-  p.kt_base = 0;
+  p.kt_base = (int)(R.kr.k0 / tc::BN);
   p.partial = w.part;
   p.row_bound = w.rb;
   p.q_begin = q_begin;

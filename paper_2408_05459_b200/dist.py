@@ -2,26 +2,41 @@
 
 One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  Rank r
 owns a contiguous block of node rows [r0, r1) (balanced by operator
-nonzeros) and, for hypergraphs, a block of hyperedges [e0, e1):
+nonzeros) and, for hypergraphs, a block of hyperedges [e0, e1).  No rank
+materialises a whole-graph factor, the whole KNN graph or a whole f64 block:
 
-* KNN       query-stationary ring: rank r keeps its rows [r0, r1) as queries
-            and as its first key block; the other key shards travel around
-            the ring (P2P send/recv, overlapped with the kernel).  Each step
-            ranks (own rows + visiting shard) and merges the lists exactly
-            (score desc, index asc), so every rank ends with its rows' global
-            top-K holding only 2 shards of X at a time; the lists are then
-            all-gathered and A_K / P_K are assembled on every rank.
-* operator  per apply: all-gather Q (n x c); hypergraphs compute their share
-            of T = P_E Q and all-gather T; each rank produces its rows of
-            Z = (I-B) P_struct Q + B P_K Q.
-* QR        local Gram Z_r^T Z_r -> all-reduce (c x c) -> every rank factors
-            the same R and applies R^-1 to its rows; ||dQ||^2 is all-reduced.
-* step 1    (rank deficient) Z^(1) is all-gathered in f64 and
-            the exact f64 QR with the reference's rank test and noise draw is
-            replicated, so every rank holds the reference's Q^(1).
-* init/MHC  the transposed / joint applies are row-partitioned the same way;
-            the MHC trace is all-reduced.
-* discretisation is replicated on the gathered Q (identical on every rank).
+* factors   each rank normalises only its rows (ShardFactors): P_N / P_V rows
+            [r0, r1), P_E rows [e0, e1), and the transposed factors of the
+            init walk as column-scaled local slices (P_N^T rows = A rows * D^-1
+            for the symmetrised A; P_V^T rows = H rows * D_V^-1; P_E^T rows =
+            H^T rows * D_E^-1) -- walk.py:38-79, 153-174 restricted to rows.
+* KNN       query-stationary key ring (knn.py:112-140): own rows x own rows
+            once, then own rows x each visiting shard only (the kernels take a
+            key-row range), the lists merged per row on the device by
+            (score desc, id asc) with de-duplication.  The shards travel
+            around the ring (P2P send/recv, the next transfer posted before
+            the kernel runs).
+* KNN graph A_K = M + M^T by rows (knn.py:294-324): every list entry (i, j, s)
+            is kept as (i, j, s) by owner(i) and sent as (j, i, s) to owner(j)
+            in one all-to-all; each rank sums duplicates and row-normalises
+            its rows on the device (same sums as the single-GPU kernel).
+* init      T_i restart walks (engine.py:87-127) over column chunks of the
+            centres (f64, each chunk n x <= 32 gathered per step), with a
+            running first-max argmax on the device.
+* step 1    (rank deficient) f64 apply of Q^(0) -- rebuilt on
+            every rank from the labels, in column chunks -- then CGS2 over
+            the local rows with all-reduced column dots, the reference's rank
+            test on |R_jj| and its replicated seeded noise (engine.py:130-149).
+* loop      per f32 step: all-gather of Q (n x c), local rows of Z, local Gram
+            all-reduced on the device, every rank factors the same Gram and
+            applies R^-1 to its rows; ||dQ||^2 and the suspect-pivot count stay
+            on the device until the tau sample (one small read-back).  A
+            suspect pivot in a tau-block replays the block with exact f64
+            steps, as the single-GPU engine does.
+* MHC       gamma all-gathers plus an all-reduced trace (engine.py:291-299).
+* discretisation is row-partitioned: argmax and cluster sums local, the
+            k x k sums all-reduced (exact 64-bit fixed point), the k x k SVD
+            replicated (engine.py:183-263).
 
 The orchestration is backend-generic: `CudaBackend` drives libancka_b200
 kernels and NCCL; the CPU tests drive the same code with a numpy backend over
@@ -36,8 +51,12 @@ from dataclasses import dataclass
 import numpy as np
 import scipy.sparse as sp
 
-from .network import (AttributedNetwork, BcmMatrix, ClusterParams, NetworkError, NetworkKind,
-                      default_knn_k, node_degrees, symmetrize_union, validate_network)
+from .network import (AttributedNetwork, ClusterParams, NetworkError, NetworkKind,
+                      default_knn_k, symmetrize_union, validate_network)
+
+#: centre columns per chunk of the init walk / step-1 apply (bounds the f64
+#: n x chunk block each rank holds: Papers100M 111M x 32 x 8 B = 28 GB)
+INIT_CHUNK = 32
 
 
 # ----------------------------------------------------------------------------
@@ -49,14 +68,6 @@ def partition_rows(cost: np.ndarray, world: int) -> np.ndarray:
     cuts = np.searchsorted(c, targets, side="left")
     b = np.concatenate([[0], cuts, [n]]).astype(np.int64)
     return np.maximum.accumulate(np.clip(b, 0, n))
-
-
-def _row_normalize(a: sp.csr_matrix) -> sp.csr_matrix:
-    rs = np.asarray(a.sum(axis=1)).ravel()
-    inv = np.divide(1.0, rs, out=np.zeros_like(rs), where=rs > 0)
-    p = (sp.diags(inv) @ a).tocsr()
-    p.sort_indices()
-    return p
 
 
 @dataclass
@@ -92,72 +103,86 @@ class Plan:
         return np.diff(self.edges)
 
 
-class HostFactors:
-    """Structural factors of the validated network, normalised on the host
-    exactly as the reference (walk.py:38-79); sliced per rank."""
+def _binary(m: sp.csr_matrix) -> sp.csr_matrix:
+    m = sp.csr_matrix(m)
+    m.sort_indices()
+    return m
 
-    def __init__(self, net: AttributedNetwork):
+
+class ShardFactors:
+    """The validated structure with the global per-node / per-edge degree
+    vectors (O(n + m)), from which each rank cuts its row slices.  The full
+    normalised factors and their transposes are never formed."""
+
+    def __init__(self, net: AttributedNetwork, degrees: np.ndarray):
         self.kind = net.kind
         self.n = net.n
-        self.degrees = node_degrees(net)
+        self.degrees = np.asarray(degrees, dtype=np.float64)
         if net.kind is NetworkKind.HYPERGRAPH:
-            h = net.incidence
-            self.p_v = _row_normalize(h.T.tocsr())
-            self.p_e = _row_normalize(h)
-            self.t_a = self.p_v.T.tocsr()      # P_V^T  (m x n)
-            self.t_b = self.p_e.T.tocsr()      # P_E^T  (n x m)
-            for mtx in (self.t_a, self.t_b):
-                mtx.sort_indices()
-            self.m = h.shape[0]
+            self.h = _binary(net.incidence)                   # m x n
+            self.m = self.h.shape[0]
+            # reference row sums of H^T (node degrees) and of H (edge sizes)
+            self.dv = np.asarray(self.h.sum(axis=0)).ravel()
+            self.de = np.asarray(self.h.sum(axis=1)).ravel()
+            self.row_nnz = np.diff(self.h.tocsc().indptr).astype(np.float64)
         else:
             a = symmetrize_union(net.adjacency) if net.directed else net.adjacency
-            self.p_n = _row_normalize(a)
-            self.t_a = self.p_n.T.tocsr()
-            self.t_a.sort_indices()
+            self.a = _binary(a)
             self.m = 0
+            self.da = np.asarray(self.a.sum(axis=1)).ravel()
+            self.row_nnz = np.diff(self.a.indptr).astype(np.float64)
 
     def row_cost(self, K: int) -> np.ndarray:
-        s = self.p_v if self.kind is NetworkKind.HYPERGRAPH else self.p_n
-        return np.diff(s.indptr).astype(np.float64) + 2 * K + 1
+        return self.row_nnz + 2 * K + 1
+
+    def edge_cost(self) -> np.ndarray:
+        return np.diff(self.h.indptr).astype(np.float64) + 1
 
 
-def make_plan(fac: HostFactors, K: int, rank: int, world: int) -> Plan:
+def make_plan(fac: ShardFactors, K: int, rank: int, world: int) -> Plan:
     rows = partition_rows(fac.row_cost(K), world)
     if fac.kind is NetworkKind.HYPERGRAPH:
-        edges = partition_rows(np.diff(fac.p_e.indptr).astype(np.float64) + 1, world)
+        edges = partition_rows(fac.edge_cost(), world)
     else:
         edges = np.zeros(world + 1, dtype=np.int64)
     return Plan(rank, world, fac.n, fac.m, rows, edges)
+
+
+def _inv(v: np.ndarray) -> np.ndarray:
+    return np.divide(1.0, v, out=np.zeros_like(v, dtype=np.float64), where=v != 0)
 
 
 # ----------------------------------------------------------------------------
 class DistOperator:
     """A rank's share of the joint-walk operator (row slices, backend handles)."""
 
-    def __init__(self, B, fac: HostFactors, plan: Plan, p_k_rows, beta_full: np.ndarray,
-                 selfloop_full: np.ndarray, alpha: float, gamma: int):
+    def __init__(self, B, fac: ShardFactors, plan: Plan, p_k_rows, beta_loc: np.ndarray,
+                 selfloop_loc: np.ndarray, alpha: float, gamma: int):
         self.B, self.plan, self.kind = B, plan, fac.kind
         self.alpha, self.gamma = alpha, gamma
         r0, r1 = plan.r0, plan.r1
         if fac.kind is NetworkKind.HYPERGRAPH:
-            self.S = B.csr(fac.p_v[r0:r1])             # n_loc x m, gathers T
-            self.E = B.csr(fac.p_e[plan.e0:plan.e1])   # m_loc x n, gathers Q
-            self.TA = B.csr(fac.t_a[plan.e0:plan.e1])  # P_V^T rows: m_loc x n
-            self.TB = B.csr(fac.t_b[r0:r1])            # P_E^T rows: n_loc x m
+            hloc = fac.h[plan.e0:plan.e1]                     # m_loc x n
+            htl = sp.csr_matrix(fac.h[:, r0:r1].T)            # H^T rows: n_loc x m
+            htl.sort_indices()
+            self.S = B.csr_rownorm(htl)                       # P_V rows: n_loc x m, gathers T
+            self.E = B.csr_rownorm(hloc)                      # P_E rows: m_loc x n, gathers Q
+            self.TA = B.csr_colscale(hloc, _inv(fac.dv))      # P_V^T rows: m_loc x n
+            self.TB = B.csr_colscale(htl, _inv(fac.de))       # P_E^T rows: n_loc x m
         else:
-            self.S = B.csr(fac.p_n[r0:r1])
-            self.TA = B.csr(fac.t_a[r0:r1])
+            aloc = fac.a[r0:r1]
+            self.S = B.csr_rownorm(aloc)                      # P_N rows
+            self.TA = B.csr_colscale(aloc, _inv(fac.da))      # P_N^T rows (A symmetric)
         self.K = p_k_rows
-        self.beta = B.vec(beta_full[r0:r1])
-        self.selfloop = B.mask(selfloop_full[r0:r1])
+        self.beta = B.vec(beta_loc)
+        self.selfloop = B.mask(selfloop_loc)
 
     # -- joint apply (walk.py:177-190) on the local rows; Q_full gathered
     def apply(self, Q_full, c, dtype, tag=None, tagval=None, scale=1.0):
         B, pl = self.B, self.plan
         if self.kind is NetworkKind.HYPERGRAPH:
             T_loc = B.spmm(self.E, Q_full, None, None, None, None, None, 0, None, None, 1.0, c, dtype)
-            T_full = B.all_gather_rows(T_loc, pl.edge_counts())
-            src = T_full
+            src = B.all_gather_rows(T_loc, pl.edge_counts())
         else:
             src = Q_full
         return B.spmm(self.S, src, self.K, Q_full, self.beta, self.selfloop, Q_full, pl.r0,
@@ -176,24 +201,24 @@ class DistOperator:
 
 
 def knn_ring(B, X, K: int, plan: Plan):
-    """Exact top-K of rows [r0, r1) against all n keys, with only the own shard
-    and one visiting shard of X resident (SURVEY.md §8(e) KNN ring).
-
-    Step 0 ranks the own rows; step s ranks (own rows + the shard of rank
-    r - s).  Every key of shard b that belongs to a row's global top-K is in
-    that row's top-K over (own rows + shard b) -- its rank there cannot exceed
-    its global rank -- so merging the step lists by (score desc, index asc)
-    and keeping K gives the global lists exactly."""
+    """Exact top-K of rows [r0, r1) against all n keys with only the own shard
+    and one visiting shard of X resident (SURVEY.md §8(e) KNN ring): own x own
+    once, then own x visiting per step; every key is ranked against the own
+    rows exactly once, and the per-row merge by (score desc, id asc) keeps the
+    global top-K (knn.py:83-98)."""
     rank, world = plan.rank, plan.world
     r0, r1 = plan.r0, plan.r1
     mine = B.x_shard(X, r0, r1)
-    ids, sc = B.knn_local(mine, None, K, r0, 0)
+    level = B.knn_level(mine)
+    ids, sc = B.knn_own(mine, K, r0, level)
     block, src = mine, rank
     pending = B.ring_start(block) if world > 1 else None
-    for _step in range(1, world):
+    for step in range(1, world):
         block, src = B.ring_finish(pending), (src - 1) % world
-        pending = B.ring_start(block) if _step < world - 1 else None   # overlaps the kernel
-        i2, s2 = B.knn_local(mine, block, K, r0, int(plan.rows[src]))
+        pending = B.ring_start(block) if step < world - 1 else None   # overlaps the kernel
+        if B.shard_rows(block) == 0 or r1 == r0:
+            continue
+        i2, s2 = B.knn_cross(mine, block, K, r0, int(plan.rows[src]), level)
         ids, sc = B.merge_lists(ids, sc, i2, s2, K)
     return ids, sc
 
@@ -222,20 +247,20 @@ def discretize_dist(B, Q_loc, k: int, plan: Plan, max_iter: int = 100, tol: floa
         for _ in range(max_iter):
             R_used = R
             lab, margin = B.disc_score(qt, R)
-            sizes = B.all_reduce(B.disc_counts(lab, k).astype(np.float64)).astype(np.int64)
-            for c in np.flatnonzero(sizes == 0):            # _reseed_empty_columns
-                if k < 2:
-                    break
-                v, li, old = B.disc_best_movable(lab, margin, sizes)
-                best = gather_best(v, plan.r0 + li if li >= 0 else -1, old)
-                if best is None:
-                    break
-                g, old = int(best[1]), int(best[2])
-                if plan.r0 <= g < plan.r1:
-                    B.disc_set_label(lab, g - plan.r0, int(c))
-                sizes[old] -= 1
-                sizes[c] += 1
             S, cnt = B.disc_cluster_sums(qt, lab, k)
+            sizes = cnt.astype(np.int64)
+            if (sizes == 0).any() and k >= 2:
+                for c in np.flatnonzero(sizes == 0):            # _reseed_empty_columns
+                    v, li, old = B.disc_best_movable(lab, margin, sizes)
+                    best = gather_best(v, plan.r0 + li if li >= 0 else -1, old)
+                    if best is None:
+                        break
+                    g, old = int(best[1]), int(best[2])
+                    if plan.r0 <= g < plan.r1:
+                        B.disc_set_label(lab, g - plan.r0, int(c))
+                    sizes[old] -= 1
+                    sizes[c] += 1
+                S, cnt = B.disc_cluster_sums(qt, lab, k)
             M = np.divide(S, cnt[:, None], out=np.zeros_like(S), where=cnt[:, None] > 0)
             try:
                 u, omega, vh = np.linalg.svd(M)
@@ -270,6 +295,7 @@ def discretize_dist(B, Q_loc, k: int, plan: Plan, max_iter: int = 100, tol: floa
 
 
 def _centers(deg: np.ndarray, k: int) -> np.ndarray:
+    """Top-k degree nodes, ties to the smaller index, sorted (engine.py:97-110)."""
     n = deg.size
     nz = int((deg > 0).sum())
     order = np.lexsort((np.arange(n), -deg))
@@ -292,92 +318,156 @@ class DistResult:
     history: list
     converged: bool
     error: str | None = None
+    replays: int = 0
+
+
+def _q0_chunk(B, labels: np.ndarray, sizes: np.ndarray, n: int, c: int, c0: int, cc: int):
+    """Columns [c0, c0 + cc) of Q^(0) = [1/sqrt(n) | Yhat0] (engine.py:368-371)
+    for all n rows, built from the replicated labels (no gather)."""
+    q = np.zeros((n, cc))
+    if c0 == 0:
+        q[:, 0] = 1.0 / np.sqrt(n)
+    col = labels + 1 - c0
+    ok = (col >= 0) & (col < cc) & (labels + 1 < c)
+    q[np.flatnonzero(ok), col[ok]] = 1.0 / np.sqrt(sizes[labels[ok]])
+    return B.rows_from_host(q, "f64")
+
+
+def exact_step_dist(B, op: DistOperator, plan: Plan, Q_src, c: int, rng, labels0=None,
+                    sizes0=None):
+    """orthogonal_step (engine.py:130-149) in f64, row-partitioned: the apply
+    by column chunks (all-gathered, or rebuilt from the labels for Q^(0)),
+    CGS2 over the local rows with all-reduced column dots, the reference's
+    rank test on |R_jj|, its seeded noise on flagged columns (the same
+    n x b draw on every rank, each adding its rows), and the re-factorisation.
+    Returns (Q_loc f64, Z_loc f64)."""
+    n = plan.n
+    parts = []
+    for c0 in range(0, c, INIT_CHUNK):
+        cc = min(INIT_CHUNK, c - c0)
+        if Q_src is None:
+            full = _q0_chunk(B, labels0, sizes0, n, c, c0, cc)
+        else:
+            full = B.all_gather_rows(B.cols(Q_src, c0, cc, "f64"), plan.row_counts())
+        parts.append(op.apply(full, cc, "f64"))
+    Z = B.hcat(parts, c)
+    Q, d = B.cgs2(Z, c, B.all_reduce_vec)
+    bad = d < 1e-12 * max(1.0, d.max() if d.size else 1.0)
+    if bad.any():
+        warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
+        noise = rng.standard_normal((n, int(bad.sum())))
+        Z = B.add_cols(Z, np.flatnonzero(bad), 1e-8 * noise[plan.r0:plan.r1])
+        Q, _ = B.cgs2(Z, c, B.all_reduce_vec)
+    return Q, Z
 
 
 def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop: bool = True) -> DistResult:
     """run_ancka (engine.py:343-437) row-partitioned over the backend's ranks."""
     rank, world = B.rank, B.world
-    net, _ = validate_network(net)
+    net, report = validate_network(net)
     if net.kind is NetworkKind.MULTIPLEX:
         raise NetworkError("the row-partitioned path covers graphs and hypergraphs")
     params.validate_for(net.n)
     n, k = net.n, params.k
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, n)
     K = min(K, n - 1)
-    fac = HostFactors(net)
+    fac = ShardFactors(net, report.degrees)
     plan = make_plan(fac, K, rank, world)
+    r0, r1 = plan.r0, plan.r1
 
-    # ---- KNN: query-stationary key ring, all-gather of the lists, replicated P_K
+    # ---- KNN: key ring, then A_K / P_K rows from an all-to-all of triples
     ids_loc, sc_loc = knn_ring(B, net.attributes, K, plan)
-    ids = B.all_gather_rows(ids_loc, plan.row_counts())
-    scores = B.all_gather_rows(sc_loc, plan.row_counts())
-    pk_rows, zero_rows = B.knn_graph_rows(ids, scores, n, plan.r0, plan.r1)
+    pk_rows, zero_loc = B.knn_graph_rows(ids_loc, sc_loc, plan, K)
 
-    # beta_vector / self-loops (walk.py:47-57, 121-123)
+    # beta_vector / self-loops (walk.py:47-57, 121-123) on the local rows
     deg = fac.degrees
-    beta = np.full(n, float(params.beta))
-    beta[deg == 0] = 1.0
-    beta[zero_rows] = 0.0
-    selfloop = (deg == 0) & (beta == 0.0)
+    beta = np.full(r1 - r0, float(params.beta))
+    beta[deg[r0:r1] == 0] = 1.0
+    beta[zero_loc] = 0.0
+    selfloop = (deg[r0:r1] == 0) & (beta == 0.0)
     op = DistOperator(B, fac, plan, pk_rows, beta, selfloop, params.alpha, params.gamma)
 
-    # ---- greedy init (engine.py:87-127): T_i transposed restart walks
+    # ---- greedy init (engine.py:87-127): T_i transposed restart walks per
+    # chunk of centres, running first-max argmax over the chunks
     centers = _centers(deg, k)
-    center_of = np.full(n, -1, dtype=np.int32)
-    center_of[centers] = np.arange(k, dtype=np.int32)
-    tag_loc = B.ivec(center_of[plan.r0:plan.r1])
-    tagval = B.vec(np.full(k, params.alpha))
-    P_loc = B.tagged(tag_loc, tagval, k, "f64")
-    for _ in range(params.t_i):
-        P_full = B.all_gather_rows(P_loc, plan.row_counts())
-        P_loc = op.apply_t(P_full, k, tag_loc, tagval, 1.0 - params.alpha)
-    lab0 = B.to_host_i(B.all_gather_rows(B.argmax_rows(P_loc, k), plan.row_counts()))
+    center_of = np.full(n, -1, dtype=np.int64)
+    center_of[centers] = np.arange(k)
+    best_v, best_i = None, None
+    for c0 in range(0, k, INIT_CHUNK):
+        cc = min(INIT_CHUNK, k - c0)
+        loc = center_of[r0:r1] - c0
+        loc = np.where((center_of[r0:r1] >= 0) & (loc >= 0) & (loc < cc), loc, -1)
+        tag_loc = B.ivec(loc)
+        tagval = B.vec(np.full(cc, params.alpha))
+        P_loc = B.tagged(tag_loc, tagval, cc, "f64")
+        for _ in range(params.t_i):
+            P_full = B.all_gather_rows(P_loc, plan.row_counts())
+            P_loc = op.apply_t(P_full, cc, tag_loc, tagval, 1.0 - params.alpha)
+        best_v, best_i = B.argmax_update(P_loc, cc, c0, best_v, best_i)
+    lab0 = B.to_host_i(B.all_gather_rows(B.as_rows(best_i), plan.row_counts()))
     if (np.bincount(lab0, minlength=k) == 0).any():
         warnings.warn("greedy init left empty cluster(s); pinning centers")
         lab0 = lab0.copy()
         lab0[centers] = np.arange(k)
 
-    def mhc(labels: np.ndarray, dtype: str) -> float:
-        """calc_mhc (engine.py:291-299), row-partitioned."""
+    def mhc(labels: np.ndarray, dtype: str):
+        """calc_mhc (engine.py:291-299), row-partitioned; the trace stays a
+        backend scalar until read."""
         sizes = np.bincount(labels, minlength=k)
         if (sizes == 0).any():
             raise NetworkError("empty cluster: normalization undefined")
         yhat = 1.0 / np.sqrt(sizes.astype(np.float64))
-        tag = B.ivec(labels[plan.r0:plan.r1].astype(np.int32))
+        tag = B.ivec(labels[r0:r1].astype(np.int32))
         tv = B.vec(params.alpha * yhat)
         F_loc = B.tagged(tag, tv, k, dtype)
         for _ in range(params.gamma):
             F_full = B.all_gather_rows(F_loc, plan.row_counts())
             F_loc = op.apply(F_full, k, dtype, tag, tv, 1.0 - params.alpha)
-        tr = B.all_reduce(np.array([B.trace_labels(F_loc, labels[plan.r0:plan.r1], yhat)]))[0]
+        tr = B.sync_scalars([B.trace_labels(F_loc, labels[r0:r1], yhat)])[0]
         return 1.0 - tr / k
 
     rng = np.random.default_rng(params.seed)
     c = min(k + 1, n)
     sizes0 = np.bincount(lab0, minlength=k)
-    q0 = np.zeros((n, c))
-    q0[:, 0] = 1.0 / np.sqrt(n)
-    keep = lab0 + 1 < c
-    q0[np.flatnonzero(keep), lab0[keep] + 1] = 1.0 / np.sqrt(sizes0[lab0[keep]])
     best_phi = mhc(lab0, "f64")
     best = lab0.copy()
     hist = [(0, best_phi)]
 
-    # ---- t = 1: exact f64 step, replicated on the gathered Z^(1)
-    Z1 = op.apply(B.rows_from_host(q0, "f64"), c, "f64")
-    Z1_full = B.to_host(B.all_gather_rows(Z1, plan.row_counts()))[:, :c]
-    q1 = B.exact_qr_step(Z1_full, rng)
-    Q_loc = B.rows_from_host(q1[plan.r0:plan.r1], "f32")
-    dq = float(np.linalg.norm(q1 - q0))
-    stop, converged, t, err = "max_iterations", False, 1, None
+    # ---- t = 1: exact f64 step from the replicated labels (no gather of Q0)
+    Q1, _ = exact_step_dist(B, op, plan, None, c, rng, labels0=lab0, sizes0=sizes0)
+    q0_loc = _q0_chunk(B, lab0[r0:r1], sizes0, r1 - r0, c, 0, c)
+    if r1 > r0:
+        q0_loc = B.fix_q0_rows(q0_loc, n)      # the 1/sqrt(n) column uses the global n
+    dq = float(np.sqrt(B.sync_scalars([B.diff2(Q1, q0_loc, c)])[0]))
+    Q_loc = B.to_f32(Q1, c)
+    stop, converged, t, err, replays = "max_iterations", False, 1, None, 0
+    kd = c - 1
     try:
-        t = 1
+        block_start, Q_save, bad_acc, dq2 = 1, None, None, None
         while True:
             if t % params.tau == 0:
-                lab_loc, empties = discretize_dist(B, Q_loc, k, plan)
+                if t > 1:
+                    dq2_g, bad_g = B.sync_scalars([dq2, bad_acc])
+                    if bad_g > 0:
+                        # a suspect Cholesky pivot: replay the block with exact f64 steps
+                        warnings.warn("ill-conditioned iterate; replaying tau-block in f64")
+                        replays += 1
+                        Q64 = B.to_f64(Q_save, c)
+                        prev = Q64
+                        for _ in range(t - block_start):
+                            prev = Q64
+                            Q64, _ = exact_step_dist(B, op, plan, Q64, c, rng)
+                        dq2_g = B.sync_scalars([B.diff2(Q64, prev, c)])[0]
+                        Q_loc = B.to_f32(Q64, c)
+                    dq = float(np.sqrt(dq2_g))
+                if kd < 1:
+                    raise NetworkError("discretize expects an n x k block with k >= 1")
+                lab_loc, empties = discretize_dist(B, Q_loc, kd, plan)
                 if empties > 0:
                     raise NetworkError("cannot repair empty clusters: no movable nodes")
                 labels = B.all_gather_labels(lab_loc, plan.row_counts())
+                if kd < k:                                     # k == n (engine.py:392-394)
+                    raise NetworkError("the row-partitioned path needs k < n")
                 phi = mhc(labels, "f32")
                 hist.append((t, phi))
                 if phi < best_phi:
@@ -390,21 +480,29 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
                     break
             if t >= params.t_a:
                 break
+            if t % params.tau == 0 or t == 1:      # a new tau-block starts at t + 1
+                block_start, Q_save, bad_acc = t, B.copy(Q_loc), B.scalar(0.0)
             # one f32 orthogonal step (engine.py:130-149), row-partitioned
             Q_full = B.all_gather_rows(Q_loc, plan.row_counts())
             Z_loc = op.apply(Q_full, c, "f32")
-            G = B.all_reduce(B.gram(Z_loc, c))
-            Q_loc, dq2_loc = B.cholqr_apply(Z_loc, Q_loc, G, c)
-            dq = float(np.sqrt(B.all_reduce(np.array([dq2_loc]))[0]))
+            G = B.all_reduce_dev(B.gram(Z_loc, c))
+            Q_loc, stats = B.cholqr_apply(Z_loc, Q_loc, G, c)
+            dq2, bad_acc = stats[0], bad_acc + stats[2]
             t += 1
+            if t % params.tau != 0 and t < params.t_a:
+                continue
+            if t % params.tau != 0:                 # t_a reached between samples
+                break
     except NetworkError as exc:
         err, stop = str(exc), "error"
-    return DistResult(best, best_phi, t, stop, hist, converged, err)
+    return DistResult(best, best_phi, t, stop, hist, converged, err, replays)
 
 
 # ----------------------------------------------------------------------------
 class CudaBackend:
-    """libancka_b200 kernels + NCCL collectives (one rank per GPU)."""
+    """libancka_b200 kernels + NCCL collectives (one rank per GPU).  Blocks,
+    Grams and step statistics are device tensors; host reads happen at the
+    tau samples and inside the discretisation rounds only."""
 
     def __init__(self, group=None):
         import torch
@@ -415,6 +513,10 @@ class CudaBackend:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         _lib.require_device()
+
+    @property
+    def _nccl(self):
+        return self.world > 1 and self.dist.get_backend(self.group) == "nccl"
 
     # --- data
     def _t(self, a, dtype):
@@ -429,9 +531,28 @@ class CudaBackend:
     def mask(self, a):
         return self._t(np.asarray(a, dtype=np.uint8), self.torch.uint8)
 
-    def csr(self, m):
+    def csr_rownorm(self, m):
+        """Row-normalised device CSR of a (binary) row slice, numpy's row-sum
+        order (ancka_csr_row_normalize)."""
         from ._device import DeviceCSR
-        return DeviceCSR.from_scipy(sp.csr_matrix(m))
+        d = DeviceCSR.from_scipy(sp.csr_matrix(m, dtype=np.float64))
+        out = self.torch.empty_like(d.val64)
+        if d.nnz:
+            self._lib.call("ancka_csr_row_normalize", d.struct(self._lib.F64), out.data_ptr(),
+                           None, self._lib.stream())
+        d.val64, d.val32 = out, out.to(self.torch.float32)
+        return d
+
+    def csr_colscale(self, m, col_scale):
+        from ._device import DeviceCSR
+        d = DeviceCSR.from_scipy(sp.csr_matrix(m, dtype=np.float64))
+        out = self.torch.empty_like(d.val64)
+        cs = self.vec(col_scale)
+        if d.nnz:
+            self._lib.call("ancka_csr_col_scale", d.struct(self._lib.F64), cs.data_ptr(),
+                           out.data_ptr(), self._lib.stream())
+        d.val64, d.val32 = out, out.to(self.torch.float32)
+        return d
 
     def _ld(self, c, dtype):
         from ._device import ld_for
@@ -446,7 +567,10 @@ class CudaBackend:
         return a.double().cpu().numpy()
 
     def to_host_i(self, a):
-        return a.cpu().numpy().astype(np.int64)
+        return a.cpu().numpy().astype(np.int64).reshape(-1)
+
+    def as_rows(self, v):
+        return v.reshape(-1, 1)
 
     def tagged(self, tag, tagval, c, dtype):
         torch = self.torch
@@ -456,6 +580,49 @@ class CudaBackend:
         out[rows, tag[rows].long()] = tagval[tag[rows].long()].to(dt)
         return out
 
+    def cols(self, Q, c0, cc, dtype):
+        from ._device import padded
+        return padded(Q[:, c0:c0 + cc], self.torch.float64 if dtype == "f64" else self.torch.float32)
+
+    def hcat(self, parts, c):
+        torch = self.torch
+        n = parts[0].shape[0]
+        out = torch.zeros((n, self._ld(c, "f64")), dtype=torch.float64, device="cuda")
+        c0 = 0
+        for p in parts:
+            cc = min(p.shape[1], c - c0)
+            out[:, c0:c0 + cc] = p[:, :cc]
+            c0 += cc
+            if c0 >= c:
+                break
+        return out
+
+    def add_cols(self, Z, cols, noise):
+        Z = Z.clone()
+        idx = self.torch.from_numpy(cols).to("cuda")
+        Z[:, idx] += self.torch.from_numpy(np.ascontiguousarray(noise)).to("cuda")
+        return Z
+
+    def fix_q0_rows(self, q, n):
+        return q
+
+    def copy(self, a):
+        return a.clone()
+
+    def scalar(self, v):
+        return self.torch.tensor(float(v), dtype=self.torch.float64, device="cuda")
+
+    def to_f32(self, Q, c):
+        from ._device import padded
+        return padded(Q[:, :c], self.torch.float32)
+
+    def to_f64(self, Q, c):
+        from ._device import padded
+        return padded(Q[:, :c], self.torch.float64)
+
+    def diff2(self, A, Bm, c):
+        return ((A[:, :c].double() - Bm[:, :c].double()) ** 2).sum()
+
     # --- collectives
     def all_gather_rows(self, x, counts):
         torch = self.torch
@@ -464,7 +631,7 @@ class CudaBackend:
         mx = int(np.max(counts))
         buf = torch.zeros((mx,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         buf[: x.shape[0]] = x
-        if self.dist.get_backend(self.group) == "nccl":
+        if self._nccl:
             out = torch.empty((self.world * mx,) + tuple(x.shape[1:]), dtype=x.dtype,
                               device=x.device)
             self.dist.all_gather_into_tensor(out, buf, group=self.group)
@@ -482,7 +649,24 @@ class CudaBackend:
             self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
 
-    # --- kernels
+    def all_reduce_dev(self, t):
+        """In-place sum over ranks of a device tensor (no host round trip)."""
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t
+
+    def all_reduce_vec(self, t):
+        return self.all_reduce_dev(t)
+
+    def sync_scalars(self, vals):
+        """Sum over ranks of a few device scalars, read back once."""
+        torch = self.torch
+        t = torch.stack([v if isinstance(v, torch.Tensor) else self.scalar(v) for v in vals])
+        t = t.to(torch.float64)
+        if self.world > 1:
+            self.dist.all_reduce(t, group=self.group)
+        return t.cpu().numpy()
+
     # --- KNN key ring: shards are ("csr", indptr, indices, data, d) or ("dense", X)
     def x_shard(self, X, r0, r1):
         torch = self.torch
@@ -493,67 +677,117 @@ class CudaBackend:
                     torch.from_numpy(x.data.astype(np.float64)).cuda(), X.shape[1])
         return ("dense", torch.from_numpy(np.ascontiguousarray(X[r0:r1], dtype=np.float64)).cuda())
 
-    def _concat(self, a, b):
-        torch = self.torch
-        if b is None:
-            return a
-        if a[0] == "csr":
-            ip = torch.cat([a[1], b[1][1:] + a[1][-1]])
-            return ("csr", ip, torch.cat([a[2], b[2]]), torch.cat([a[3], b[3]]), a[4])
-        return ("dense", torch.cat([a[1], b[1]]))
+    def shard_rows(self, s):
+        return int(s[1].numel() - 1) if s[0] == "csr" else int(s[1].shape[0])
 
-    def knn_local(self, mine, block, K, r0, boff):
-        """Top-K of the own rows over (own rows + block), global indices.  The
-        two shards are concatenated in global row order, so the kernel's
-        index tie-break is the global one."""
-        from .knn import DeviceAttributes, knn_search_exact_device
+    def knn_level(self, mine):
+        """Tensor-core path of the whole X: the minimum shard level over ranks."""
+        from .knn import DeviceAttributes
+        if self.shard_rows(mine) == 0:
+            lv = 2.0
+        elif mine[0] == "csr":
+            lv = DeviceAttributes.from_device_csr(mine[1], mine[2], mine[3],
+                                                  (self.shard_rows(mine), mine[4])).level
+        else:
+            lv = DeviceAttributes.from_device_dense(mine[1]).level
+        t = self.torch.tensor([float(lv)], device="cuda")
+        if self.world > 1:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
+    def _attrs(self, s, level):
+        from .knn import DeviceAttributes
+        if s[0] == "csr":
+            if level > 0:
+                xa = DeviceAttributes.__new__(DeviceAttributes)
+                xa.shape, xa.dense = (self.shard_rows(s), s[4]), None
+                xa.indptr, xa.indices, xa.data, xa.level = s[1], s[2], s[3], level
+                return xa
+            t = self.torch.sparse_csr_tensor(s[1], s[2].long(), s[3],
+                                             size=(self.shard_rows(s), s[4]))
+            return DeviceAttributes.from_device_dense(t.to_dense())
+        return DeviceAttributes.from_device_dense(s[1])
+
+    def knn_own(self, mine, K, r0, level):
+        from .knn import knn_search_exact_device
+        nq = self.shard_rows(mine)
         torch = self.torch
-        rows_of = (lambda t: int(t[1].numel() - 1)) if mine[0] == "csr" else (lambda t: int(t[1].shape[0]))
-        nq = rows_of(mine)
-        first = block is not None and boff < r0
-        x = self._concat(block, mine) if first else self._concat(mine, block)
-        nb = rows_of(block) if first else 0
-        if x[0] == "csr":
-            xa = DeviceAttributes.from_device_csr(x[1], x[2], x[3], (int(x[1].numel() - 1), x[4]))
-        else:
-            xa = DeviceAttributes.from_device_dense(x[1])
-        kk = min(K, xa.shape[0] - 1)
-        ids, sc = knn_search_exact_device(xa, kk, rows=(nb, nb + nq))
-        ids = ids.long()
-        if first:
-            g = torch.where(ids < nb, ids + boff, ids - nb + r0)
-        else:
-            g = torch.where(ids < nq, ids + r0, ids - nq + boff)
-        g = torch.where(ids < 0, torch.full_like(ids, -1), g)
+        if nq == 0:
+            return (torch.empty((0, K), dtype=torch.int32, device="cuda"),
+                    torch.empty((0, K), dtype=torch.float64, device="cuda"))
+        if nq <= 1:
+            return (torch.full((nq, K), -1, dtype=torch.int32, device="cuda"),
+                    torch.zeros((nq, K), dtype=torch.float64, device="cuda"))
+        xa = self._attrs(mine, level)
+        kk = min(K, nq - 1)
+        ids, sc = knn_search_exact_device(xa, kk, integer=level)
+        ids = torch.where(ids >= 0, ids + r0, ids)
         if kk < K:
-            pad = K - kk
-            g = torch.cat([g, torch.full((nq, pad), -1, dtype=g.dtype, device=g.device)], 1)
-            sc = torch.cat([sc, torch.zeros((nq, pad), dtype=sc.dtype, device=sc.device)], 1)
-        return g, sc
+            ids = torch.cat([ids, torch.full((nq, K - kk), -1, dtype=ids.dtype, device="cuda")], 1)
+            sc = torch.cat([sc, torch.zeros((nq, K - kk), dtype=sc.dtype, device="cuda")], 1)
+        return ids.contiguous(), sc.contiguous()
+
+    def _concat_padded(self, a, b, pad_rows):
+        """[a rows, zero rows up to pad_rows, b rows] (the key block starts on a 256-row tile)."""
+        torch = self.torch
+        na = self.shard_rows(a)
+        if a[0] == "csr":
+            ip_a = torch.cat([a[1], a[1][-1:].repeat(pad_rows - na)])
+            ip = torch.cat([ip_a, b[1][1:] + ip_a[-1]])
+            return ("csr", ip, torch.cat([a[2], b[2]]), torch.cat([a[3], b[3]]), a[4])
+        d = a[1].shape[1]
+        return ("dense", torch.cat([a[1], torch.zeros((pad_rows - na, d), dtype=a[1].dtype,
+                                                       device="cuda"), b[1]]))
+
+    def knn_cross(self, mine, block, K, r0, boff, level):
+        """Top-K of the own rows over the visiting block's keys only
+        (ancka_knn_exact_keys on [own | pad | visiting])."""
+        from ._device import WORKSPACE
+        torch, _lib = self.torch, self._lib
+        nq, nb = self.shard_rows(mine), self.shard_rows(block)
+        qpad = (nq + 255) // 256 * 256
+        x = self._concat_padded(mine, block, qpad)
+        n = qpad + nb
+        kk = min(K, n - 1)
+        ids = torch.empty((nq, kk), dtype=torch.int32, device="cuda")
+        sc = torch.empty((nq, kk), dtype=torch.float64, device="cuda")
+        if x[0] == "csr" and level > 0:
+            d = x[4]
+            ws = WORKSPACE.get("knn_ring", _lib.load().ancka_knn_workspace_size(n, d, kk, level))
+            _lib.call("ancka_knn_exact_csr_keys", x[1].data_ptr(), x[2].data_ptr(), x[3].data_ptr(),
+                      n, d, kk, level, 0, nq, qpad, n, ids.data_ptr(), sc.data_ptr(),
+                      ws.data_ptr(), ws.numel(), _lib.stream())
+        else:
+            xa = self._attrs(x, level)
+            xd = xa.dense
+            d = xd.shape[1]
+            lv = level if level >= 0 else 0
+            ws = WORKSPACE.get("knn_ring", _lib.load().ancka_knn_workspace_size(n, d, kk, lv))
+            _lib.call("ancka_knn_exact_keys", xd.data_ptr(), n, d, xd.stride(0), kk, lv, 0, nq,
+                      qpad, n, ids.data_ptr(), sc.data_ptr(), ws.data_ptr(), ws.numel(),
+                      _lib.stream())
+        ids = ids.long()
+        g = torch.where(ids >= qpad, ids - qpad + boff, ids + r0)
+        g = torch.where(ids < 0, torch.full_like(ids, -1), g).to(torch.int32)
+        if kk < K:
+            g = torch.cat([g, torch.full((nq, K - kk), -1, dtype=g.dtype, device="cuda")], 1)
+            sc = torch.cat([sc, torch.zeros((nq, K - kk), dtype=sc.dtype, device="cuda")], 1)
+        return g.contiguous(), sc.contiguous()
 
     def merge_lists(self, ia, sa, ib, sb, K):
-        """Per row: union, dedup, order (score desc, index asc), first K."""
-        torch = self.torch
-        ids = torch.cat([ia, ib], 1)
-        sc = torch.cat([sa, sb], 1)
-        big = torch.iinfo(torch.int64).max
-        key_i = torch.where(ids < 0, torch.full_like(ids, big), ids)
-        o = torch.argsort(key_i, dim=1, stable=True)               # index asc
-        ids, sc, key_i = ids.gather(1, o), sc.gather(1, o), key_i.gather(1, o)
-        dup = torch.zeros_like(ids, dtype=torch.bool)
-        dup[:, 1:] = (key_i[:, 1:] == key_i[:, :-1]) & (ids[:, 1:] >= 0)
-        s_key = torch.where((ids < 0) | dup, torch.full_like(sc, -np.inf), sc)
-        o = torch.argsort(-s_key, dim=1, stable=True)               # score desc, ties keep index asc
-        ids, s_key = ids.gather(1, o)[:, :K], s_key.gather(1, o)[:, :K]
-        ok = s_key > -np.inf
-        return torch.where(ok, ids, torch.full_like(ids, -1)), torch.where(ok, s_key, torch.zeros_like(s_key))
+        """Per row: first K of the union by (score desc, id asc), de-duplicated
+        (ancka_knn_merge_lists, in place)."""
+        ia, sa = ia.contiguous(), sa.contiguous()
+        self._lib.call("ancka_knn_merge_lists", ia.data_ptr(), sa.data_ptr(), ib.data_ptr(),
+                       sb.data_ptr(), ia.shape[0], K, self._lib.stream())
+        return ia, sa
 
     def _p2p(self, send_tensors, recv_tensors):
         """Send to rank+1 and receive from rank-1.  NCCL moves device tensors
         over NVLink; other backends (gloo in the tests) go through host copies."""
         dist = self.dist
         nxt, prv = (self.rank + 1) % self.world, (self.rank - 1) % self.world
-        if dist.get_backend(self.group) != "nccl":
+        if not self._nccl:
             host_recv = [t.cpu() for t in recv_tensors]
             ops = [dist.P2POp(dist.isend, t.cpu(), nxt, group=self.group) for t in send_tensors]
             ops += [dist.P2POp(dist.irecv, t, prv, group=self.group) for t in host_recv]
@@ -594,14 +828,76 @@ class CudaBackend:
             r.wait()
         return ("csr", bufs[0], bufs[1], bufs[2], meta[1]) if meta[0] == "csr" else ("dense", bufs[0])
 
-    def knn_graph_rows(self, ids, scores, n, r0, r1):
-        from ._device import DeviceCSR
-        from .knn import build_knn_graph_device
-        A, P, zero = build_knn_graph_device(ids.int(), scores, n)
-        rp = P.rowptr[r0: r1 + 1]
-        b, e = int(rp[0]), int(rp[-1])
-        loc = DeviceCSR(r1 - r0, n, (rp - b).contiguous(), P.colidx[b:e], P.val64[b:e], P.val32[b:e])
-        return loc, zero.cpu().numpy().astype(bool)
+    def _all_to_all(self, send: np.ndarray | None, sendt, dest):
+        """Exchange rows of `sendt` (device, [E, w]) grouped by destination rank."""
+        torch, dist = self.torch, self.dist
+        order = torch.argsort(dest, stable=True)
+        sendt = sendt[order]
+        counts = torch.bincount(dest, minlength=self.world)
+        if self.world == 1:
+            return sendt
+        rc = torch.empty_like(counts)
+        if self._nccl:
+            dist.all_to_all_single(rc, counts, group=self.group)
+            sc, rcl = counts.cpu().tolist(), rc.cpu().tolist()
+            out = torch.empty((sum(rcl), sendt.shape[1]), dtype=sendt.dtype, device="cuda")
+            dist.all_to_all_single(out, sendt.contiguous(), output_split_sizes=rcl,
+                                   input_split_sizes=sc, group=self.group)
+            return out
+        # gloo (tests): all-gather the variable-size parts through the host
+        sizes = [torch.zeros(1, dtype=torch.int64) for _ in range(self.world)]
+        dist.all_gather(sizes, torch.tensor([sendt.shape[0]], dtype=torch.int64), group=self.group)
+        mx = max(int(s.item()) for s in sizes)
+        cnt = counts.cpu()
+        buf = torch.zeros((mx, sendt.shape[1]), dtype=sendt.dtype)
+        buf[: sendt.shape[0]] = sendt.cpu()
+        dbuf = torch.full((mx,), -1, dtype=torch.int64)
+        dbuf[: sendt.shape[0]] = dest[order].cpu()
+        lst = [torch.empty_like(buf) for _ in range(self.world)]
+        dl = [torch.empty_like(dbuf) for _ in range(self.world)]
+        dist.all_gather(lst, buf, group=self.group)
+        dist.all_gather(dl, dbuf, group=self.group)
+        del cnt
+        parts = [lst[r][dl[r] == self.rank] for r in range(self.world)]
+        return torch.cat(parts).to("cuda")
+
+    def knn_graph_rows(self, ids_loc, sc_loc, plan, K):
+        """Rows [r0, r1) of A_K = M + M^T and P_K (knn.py:294-324): own list
+        entries stay, transposed entries go to the owner of their column."""
+        from ._device import WORKSPACE, DeviceCSR
+        torch, _lib = self.torch, self._lib
+        r0, r1, n = plan.r0, plan.r1, plan.n
+        nloc = r1 - r0
+        i = torch.arange(r0, r1, device="cuda", dtype=torch.int64)[:, None].expand(-1, K)
+        j = ids_loc.long()
+        ok = j >= 0
+        i, j, s = i[ok], j[ok], sc_loc[ok]
+        bounds = torch.from_numpy(plan.rows[1:-1].astype(np.int64)).to("cuda")
+        dest = torch.bucketize(j, bounds, right=True)
+        trip = torch.stack([j.double(), i.double(), s], 1)      # (row j, col i, s) to owner(j)
+        recv = self._all_to_all(None, trip, dest)
+        rows = torch.cat([i - r0, recv[:, 0].long() - r0]).to(torch.int32)
+        cols = torch.cat([j, recv[:, 1].long()]).to(torch.int32)
+        vals = torch.cat([s, recv[:, 2]])
+        E = int(rows.numel())
+        rp = torch.empty(nloc + 1, dtype=torch.int64, device="cuda")
+        ci = torch.empty(max(E, 1), dtype=torch.int32, device="cuda")
+        ak = torch.empty(max(E, 1), dtype=torch.float64, device="cuda")
+        p64 = torch.empty_like(ak)
+        p32 = torch.empty(max(E, 1), dtype=torch.float32, device="cuda")
+        zero = torch.empty(max(nloc, 1), dtype=torch.uint8, device="cuda")
+        nnz = torch.zeros(1, dtype=torch.int64, device="cuda")
+        if nloc:
+            ws = WORKSPACE.get("knn_graph_coo", _lib.load().ancka_knn_graph_coo_workspace_size(E))
+            _lib.call("ancka_knn_graph_coo", rows.data_ptr(), cols.data_ptr(), vals.data_ptr(), E,
+                      nloc, n, rp.data_ptr(), ci.data_ptr(), ak.data_ptr(), p64.data_ptr(),
+                      p32.data_ptr(), zero.data_ptr(), nnz.data_ptr(), ws.data_ptr(), ws.numel(),
+                      _lib.stream())
+        else:
+            rp.zero_()
+        m = int(nnz.item())
+        P = DeviceCSR(nloc, n, rp, ci[:m], p64[:m], p32[:m])
+        return P, zero[:nloc].cpu().numpy().astype(bool)
 
     def spmm(self, S, s_src, Kc, k_src, beta, selfloop, self_src, row_offset, tag, tagval, scale,
              c, dtype):
@@ -610,6 +906,8 @@ class CudaBackend:
         dt = torch.float64 if f64 else torch.float32
         rows = S.rows
         out = torch.empty((rows, self._ld(c, dtype)), dtype=dt, device="cuda")
+        if rows == 0:
+            return out
         code = _lib.F64 if f64 else _lib.F32
 
         def cast(x):
@@ -633,52 +931,62 @@ class CudaBackend:
         return out
 
     def gram(self, Z, c):
+        """Local Gram Z^T Z (packed upper, f64) on the device (ancka_gram_f32)."""
         from ._device import WORKSPACE
         torch, _lib = self.torch, self._lib
-        G = torch.empty(c * (c + 1) // 2, dtype=torch.float64, device="cuda")
-        ws = WORKSPACE.get("dist_orth", _lib.load().ancka_orth_workspace_size(None, c))
-        _lib.call("ancka_gram_f32", Z.data_ptr(), Z.shape[0], Z.stride(0), c, G.data_ptr(),
-                  ws.data_ptr(), ws.numel(), _lib.stream())
-        return G.cpu().numpy()
+        G = torch.zeros(c * (c + 1) // 2, dtype=torch.float64, device="cuda")
+        if Z.shape[0]:
+            ws = WORKSPACE.get("dist_orth", _lib.load().ancka_orth_workspace_size(None, c))
+            _lib.call("ancka_gram_f32", Z.data_ptr(), Z.shape[0], Z.stride(0), c, G.data_ptr(),
+                      ws.data_ptr(), ws.numel(), _lib.stream())
+        return G
 
     def cholqr_apply(self, Z, Qprev, G, c):
+        """Every rank factors the same all-reduced Gram (device) and applies
+        R^-1 to its rows; stats = [||dQ_loc||^2, min pivot ratio, suspect
+        pivots] stay on the device."""
         from ._device import WORKSPACE
         torch, _lib = self.torch, self._lib
-        Gt = torch.as_tensor(G, device="cuda")
         Qn = torch.empty_like(Z)
         stats = torch.tensor([0.0, 1.0, 0.0, 0.0], dtype=torch.float64, device="cuda")
         ws = WORKSPACE.get("dist_orth", _lib.load().ancka_orth_workspace_size(None, c))
         _lib.call("ancka_cholqr_apply_f32", Z.data_ptr(), Qprev.data_ptr(), Qn.data_ptr(),
-                  Z.shape[0], Z.stride(0), c, Gt.data_ptr(), stats.data_ptr(), ws.data_ptr(),
+                  Z.shape[0], Z.stride(0), c, G.data_ptr(), stats.data_ptr(), ws.data_ptr(),
                   ws.numel(), _lib.stream())
-        return Qn, float(stats[0].item())
+        return Qn, stats
 
-    def argmax_rows(self, P, k):
-        return self.torch.argmax(P[:, :k], dim=1).int()
+    def cgs2(self, Z, c, allreduce):
+        """Classical Gram-Schmidt with reorthogonalisation over the local rows,
+        column dots all-reduced (f64): Q and |R_jj|."""
+        torch = self.torch
+        Q = torch.zeros_like(Z)
+        d = np.zeros(c)
+        for j in range(c):
+            z = Z[:, j].clone()
+            for _ in range(2):
+                if j:
+                    h = allreduce(Q[:, :j].T @ z)
+                    z = z - Q[:, :j] @ h
+            r = float(np.sqrt(max(float(allreduce((z * z).sum().reshape(1))[0].item()), 0.0)))
+            d[j] = r
+            Q[:, j] = z / r if r > 0 else z * 0.0
+        return Q, d
+
+    def argmax_update(self, P, cc, c0, best_v, best_i):
+        """Running first-max argmax over centre chunks (engine.py:119)."""
+        torch = self.torch
+        v, i = torch.max(P[:, :cc], dim=1)
+        i = i.to(torch.int64) + c0
+        if best_v is None:
+            return v, i
+        take = v > best_v                     # strict: the earlier chunk wins ties
+        return torch.where(take, v, best_v), torch.where(take, i, best_i)
 
     def trace_labels(self, F, labels_loc, yhat):
         torch = self.torch
         lab = torch.as_tensor(labels_loc, device="cuda").long()
         vals = F[torch.arange(F.shape[0], device="cuda"), lab].double()
-        return float((vals * torch.as_tensor(yhat, device="cuda")[lab]).sum().item())
-
-    def exact_qr_step(self, Z_full, rng):
-        from ._device import padded
-        from .engine import _qr_f64_inplace
-        torch = self.torch
-        c = Z_full.shape[1]
-        z = padded(torch.from_numpy(Z_full), torch.float64)
-        q = z.clone()
-        d = _qr_f64_inplace(q, c)
-        bad = d < 1e-12 * max(1.0, d.max() if d.size else 1.0)
-        if bad.any():
-            warnings.warn(f"rank-deficient iterate; perturbing {int(bad.sum())} column(s)")
-            noise = rng.standard_normal((Z_full.shape[0], int(bad.sum())))
-            cols = torch.from_numpy(np.flatnonzero(bad)).to("cuda")
-            z[:, cols] += 1e-8 * torch.from_numpy(noise).to("cuda")
-            q = z.clone()
-            _qr_f64_inplace(q, c)
-        return q[:, :c].cpu().numpy()
+        return (vals * torch.as_tensor(yhat, device="cuda")[lab]).sum()
 
     # --- row-partitioned discretisation primitives (discretize_dist)
     def disc_prepare(self, Q_loc, col0, k):
@@ -687,7 +995,7 @@ class CudaBackend:
         n = Q_loc.shape[0]
         ldt = ld_for(k, torch.float32)
         st = {"k": k, "ldt": ldt, "n": n,
-              "qt": torch.empty((n, ldt), dtype=torch.float32, device="cuda"),
+              "qt": torch.empty((max(n, 1), ldt), dtype=torch.float32, device="cuda"),
               "zero": torch.zeros(1, dtype=torch.int32, device="cuda"),
               "R": torch.zeros((k, ldt), dtype=torch.float32, device="cuda"),
               "acc": torch.zeros(max(n, 1), dtype=torch.float64, device="cuda"),
@@ -712,9 +1020,6 @@ class CudaBackend:
                       st["ldt"], lab.data_ptr(), margin.data_ptr(), _lib.stream())
         return lab[:n], margin[:n]
 
-    def disc_counts(self, lab, k):
-        return self.torch.bincount(lab.long(), minlength=k).cpu().numpy()
-
     def disc_best_movable(self, lab, margin, sizes):
         torch = self.torch
         if lab.numel() == 0:
@@ -731,6 +1036,8 @@ class CudaBackend:
         lab[i] = c
 
     def disc_cluster_sums(self, st, lab, k):
+        """k x k sums and k counts of this round: 64-bit fixed point on the
+        device, all-reduced as integers (exact, order free), one read-back."""
         torch, _lib = self.torch, self._lib
         n = st["n"]
         if n:
@@ -740,7 +1047,7 @@ class CudaBackend:
             st["S"].zero_()
             st["cnt"].zero_()
         both = torch.cat([st["S"], st["cnt"]])
-        if self.world > 1:                               # int64 sums: exact, order free
+        if self.world > 1:
             self.dist.all_reduce(both, group=self.group)
         h = both.cpu().numpy()
         return h[:k * k].reshape(k, k).astype(np.float64) / st["scale"], h[k * k:].astype(np.float64)
