@@ -67,6 +67,8 @@ def parse():
     ap.add_argument("--write-counts", action="store_true",
                     help="store this run's kernel counts for --impl reference")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--dist", action="store_true",
+                    help="run the row-partitioned path (dist.run_ancka_dist) also at N=1")
     return ap.parse_args()
 
 
@@ -490,7 +492,8 @@ def run_multi_gpu(args, ws, rank, local):
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
 
     def barrier():
-        dist.barrier()
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize()
 
     def step():
@@ -521,7 +524,10 @@ def run_ours(args):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     _lib.require_device()
-    if ws > 1:
+    if ws > 1 or args.dist:
+        for key, val in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"),
+                         ("WORLD_SIZE", "1")):
+            os.environ.setdefault(key, val)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         try:
             run_multi_gpu(args, ws, rank, local)
