@@ -13,6 +13,7 @@ from paper_2408_05459_b200 import synth  # noqa: E402
 
 shape = sys.argv[1] if len(sys.argv) > 1 else "magpm"
 scale = float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 t0 = time.perf_counter()
 inst = synth.make(shape, seed=0, scale=scale)
 print(f"generated {shape} n={inst.structure.shape[1]} nnz={inst.structure.nnz} "
@@ -24,7 +25,7 @@ t0 = time.perf_counter()
 prep = ancka.prepare_network(net, params)
 torch.cuda.synchronize()
 print(f"prepare {time.perf_counter() - t0:.2f}s level={prep.x_level}", flush=True)
-for rep in range(2):
+for rep in range(reps):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     res = ancka.run_prepared(prep, params)
@@ -36,4 +37,5 @@ for rep in range(2):
           f"timings={ {k: round(v, 1) for k, v in res.timings_ms.items()} }", flush=True)
     if res.warnings:
         print("   warnings:", sorted(set(res.warnings)), flush=True)
-print("max mem GB", torch.cuda.max_memory_allocated() / 1e9)
+print("max mem GB", torch.cuda.max_memory_allocated() / 1e9,
+      "reserved GB", torch.cuda.max_memory_reserved() / 1e9, flush=True)
