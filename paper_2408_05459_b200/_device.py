@@ -63,6 +63,12 @@ class Workspace:
     def __init__(self):
         self._bufs: dict[str, torch.Tensor] = {}
 
+    def release(self, *keys: str) -> None:
+        """Drop phase-specific buffers (the caching allocator keeps the
+        memory for the next phase's tensors)."""
+        for k in keys:
+            self._bufs.pop(k, None)
+
     def get(self, key: str, nbytes: int) -> torch.Tensor:
         nbytes = max(int(nbytes), 256)
         b = self._bufs.get(key)

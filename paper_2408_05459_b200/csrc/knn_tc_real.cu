@@ -269,10 +269,14 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   int pc = 0;
   float published = -kInf;
   float* stash = stash_base + (threadIdx.x - 64) * 33;
-  auto drain = [&]() {
+  // drain(upto): insert the buffered candidates; upto bounds the loop (the
+  // warp-wide maximum of pc when all lanes drain together, PB otherwise)
+  auto drain = [&](int upto) {
 #pragma unroll
-    for (int t = 0; t < PB; ++t)
+    for (int t = 0; t < PB; ++t) {
+      if (t >= upto) break;
       if (t < pc && pf[t] >= C.thr) C.insert(pf[t], pj[t], band_i);
+    }
     pc = 0;
     const float b = C.kth() - band_i;
     if (b > published && live) {
@@ -284,7 +288,7 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   for (int t = 0; t < ntiles; ++t) {
     const int acc = t & 1;
     const uint32_t acc_phase = (t >> 1) & 1;
-    mbar_wait_sleep(&tfull[acc], acc_phase);
+    mbar_wait_backoff(&tfull[acc], acc_phase);
     if (live) {
       C.raise_floor(ord2f(floor_next));
       floor_next = __ldcg(p.row_bound + (i - p.q_begin));
@@ -329,7 +333,7 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
             const int u = __ffs(mask) - 1;
             mask &= mask - 1;
             const float v = stash[u];
-            if (pc == PB) drain();                 // overflow (early in a row's stream)
+            if (pc == PB) drain(PB);               // overflow (divergent: no warp sync)
             if (v < C.thr) continue;
 #pragma unroll
             for (int q = 0; q < PB; ++q) {
@@ -340,10 +344,10 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
           }
         }
       }
-      if (__any_sync(0xffffffffu, pc >= DRAIN)) drain();
+      if (__any_sync(0xffffffffu, pc >= DRAIN)) drain(__reduce_max_sync(0xffffffffu, pc));
     }
   }
-  drain();
+  drain(__reduce_max_sync(0xffffffffu, pc));
   if (live) {
 #pragma unroll
     for (int t = 0; t < L; ++t)

@@ -793,8 +793,12 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         with timer.span("knn_ms"):
             op, g = build_pipeline_device(prep, params)
         n, k = op.n, params.k
+        # KNN / graph-assembly buffers are dead from here on (tens of GB at
+        # 1e7+ nodes); the allocator reuses the memory for the loop's blocks
+        WORKSPACE.release("knn", "knn_graph", "csr_transpose", "row_split")
         with timer.span("init_ms"):
             labels0, _, sizes0_dev, sizes0 = _init_labels_sizes(op, k, params.t_i, params.alpha)
+        WORKSPACE.release("init")
         rng = np.random.default_rng(params.seed)
         c = min(k + 1, n)
         # Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371), f64 for the exact first step
@@ -809,6 +813,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             # phi(Y0) stays on the device; it rides along with the first sample's
             # read-back (no synchronisation here)
             mhc0_dev = _MhcRunner(op, k, _lib.F64)(labels0)
+        WORKSPACE.release(f"mhc{_lib.F64}")          # 2 n k f64: re-acquired at the end
         best_mhc = None
         best_labels = labels0.clone()
         history = [(0, None)]
@@ -873,6 +878,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                 loop.Q[0][:, :c] = q1[:, :c].to(torch.float32)
                 loop.cur = 0
                 dq1 = torch.linalg.vector_norm(q1[:, :c] - q0[:, :c])
+                del q1, q0
             t_done = 1
             sample_needed = params.tau == 1
             # spec: a tau-block enqueued while the sample is read back
