@@ -333,22 +333,10 @@ static int launch_apply(const float* Z, const float* Qprev, float* Qout, int64_t
   return ANCKA_OK;
 }
 
-int gram_tc(const float* Z, int64_t n, int64_t ld, int c, double* partial, int nblocks,
-            cudaStream_t st);
-int apply_tc(const float* Z, const float* Qprev, float* Qout, int64_t n, int64_t ld, int c,
-             const float* rinv, double* dq_partial, int nblocks, cudaStream_t st);
-
-// tensor-core Gram / apply (qr_tc.cu); ANCKA_QR_SIMT=1 selects the SIMT kernels
-static bool qr_use_tc() {
-  static const bool simt = getenv("ANCKA_QR_SIMT") != nullptr;
-  return !simt;
-}
-
 int cholqr_f32(const float* Z, const float* Qprev, float* Qout, int64_t n, int64_t ld, int c,
                double* stats, OrthWs& w, cudaStream_t st) {
   ANCKA_REQUIRE(c >= 1 && c <= 256 && ld % 4 == 0, ANCKA_ERR_ARG, "cholqr: bad c/ld");
-  if (qr_use_tc()) ANCKA_TRY(gram_tc(Z, n, ld, c, w.gram_partial, kGramBlocks, st));
-  else ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
+  ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
   const int npairs = c * (c + 1) / 2;
   const size_t csm = (size_t)npairs * sizeof(double);
   ANCKA_REQUIRE(csm <= 227 * 1024, ANCKA_ERR_UNSUPPORTED, "cholqr: c=%d too large", c);
@@ -358,10 +346,7 @@ int cholqr_f32(const float* Z, const float* Qprev, float* Qout, int64_t n, int64
   ANCKA_LAUNCHED();
   chol_kernel<<<1, 256, csm, st>>>(w.gsum, 1, c, w.rinv32, w.rdiag, stats);
   ANCKA_LAUNCHED();
-  if (qr_use_tc())
-    ANCKA_TRY(apply_tc(Z, Qprev, Qout, n, ld, c, w.rinv32, w.dq_partial, kApplyBlocks, st));
-  else
-    ANCKA_TRY(launch_apply(Z, Qprev, Qout, n, ld, c, w.rinv32, w.dq_partial, st));
+  ANCKA_TRY(launch_apply(Z, Qprev, Qout, n, ld, c, w.rinv32, w.dq_partial, st));
   reduce_partials_kernel<<<1, 256, 0, st>>>(w.dq_partial, kApplyBlocks, stats);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
@@ -595,8 +580,7 @@ extern "C" int ancka_gram_f32(const float* Z, int64_t n, int64_t ld, int32_t c, 
   carve_orth(cv, w, nullptr, c);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "gram: workspace too small");
   auto st = as_stream(stream);
-  if (qr_use_tc()) ANCKA_TRY(gram_tc(Z, n, ld, c, w.gram_partial, kGramBlocks, st));
-  else ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
+  ANCKA_TRY(launch_gram(Z, n, ld, c, w.gram_partial, st));
   gram_sum_kernel<<<(c * (c + 1) / 2 + 255) / 256, 256, 0, st>>>(w.gram_partial, kGramBlocks,
                                                                  c * (c + 1) / 2, G);
   ANCKA_LAUNCHED();

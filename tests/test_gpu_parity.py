@@ -502,8 +502,10 @@ def test_cholqr_wide_blocks(c):
     _lib.call("ancka_gram_f32", Z.data_ptr(), n, ld, c, G.data_ptr(), ws.data_ptr(), ws.numel(),
               _lib.stream())
     zd = z.astype(np.float64)
-    g_ref = (zd.T @ zd)[np.triu_indices(c)]
-    np.testing.assert_allclose(G.cpu().numpy(), g_ref, rtol=2e-6, atol=1e-9 * np.abs(g_ref).max())
+    gfull = zd.T @ zd
+    g_ref = gfull[np.triu_indices(c)]
+    scale = np.sqrt(np.outer(np.diag(gfull), np.diag(gfull)))[np.triu_indices(c)]
+    assert np.all(np.abs(G.cpu().numpy() - g_ref) <= 1e-6 * scale)   # f32-data Gram accuracy
     _lib.call("ancka_cholqr_apply_f32", Z.data_ptr(), Qp.data_ptr(), Qn.data_ptr(), n, ld, c,
               G.data_ptr(), stats.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
     q = Qn[:, :c].double().cpu().numpy()
