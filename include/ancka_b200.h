@@ -59,6 +59,11 @@ typedef struct {
   const int32_t* row_order;   /* n rows by descending cost (optional): the
                                  fused narrow-block kernel deals rows to its
                                  lane groups in this order (balanced tails) */
+  const int32_t* locality_order; /* n rows grouped by cluster (optional, graph
+                                 operators): the f32 apply processes rows in
+                                 this order, so the rows in flight share their
+                                 neighbours' gathered rows in L2; results are
+                                 unchanged (each row's sum is the same) */
 } ancka_row_split;
 
 /* Device-resident WalkOperator (walk.py:89-104).  Index arrays are shared by
@@ -339,6 +344,11 @@ int ancka_row_split_plan(const int64_t* srp, const int64_t* krp, int64_t n, doub
                          int32_t* order_out, uint8_t* is_long_out, int32_t* long_rows_out,
                          int64_t* n_long_out, void* workspace, size_t workspace_bytes,
                          ancka_stream_t stream);
+
+/* Rows sorted by (label, row): the locality order of ancka_row_split. */
+size_t ancka_locality_order_workspace_size(int64_t n);
+int ancka_locality_order(const int32_t* labels, int64_t n, int32_t k, int32_t* order_out,
+                         void* workspace, size_t workspace_bytes, ancka_stream_t stream);
 
 /* The first iterate Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371, Yhat by
  * normalize_bcm, engine.py:75-84) as an n x ldq f64 block, from device labels

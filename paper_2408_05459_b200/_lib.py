@@ -27,7 +27,7 @@ class CSR(ctypes.Structure):
 
 class RowSplit(ctypes.Structure):
     _fields_ = [("n_long", c_int64), ("is_long", c_void_p), ("long_rows", c_void_p),
-                ("row_order", c_void_p)]
+                ("row_order", c_void_p), ("locality_order", c_void_p)]
 
 
 class Operator(ctypes.Structure):
@@ -73,6 +73,9 @@ _SIGS = {
     "ancka_knn_graph_coo": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int64,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_locality_order_workspace_size": (c_size_t, [c_int64]),
+    "ancka_locality_order": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_size_t,
+                                       c_void_p]),
     "ancka_knn_graph_workspace_size": (c_size_t, [c_int64, c_int32]),
     "ancka_knn_graph": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
                                   c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,

@@ -10,6 +10,8 @@
 // instantiation accumulates sequentially with non-contracted mul/add, i.e.
 // in exactly scipy csr_matvecs' order, giving bit-identical results.
 #include "common.cuh"
+#include <cub/device/device_radix_sort.cuh>
+
 #include "spmm.cuh"
 
 namespace ancka {
@@ -194,10 +196,13 @@ spmm_kernel(SpmmArgs<T> a) {
     }
   }
   const int64_t gid = (int64_t)(blockIdx.x - long_blocks) * blockDim.x + threadIdx.x;
-  const int64_t row = gid / a.nchunk;
-  if (row >= a.rows) return;
+  const int64_t slot = gid / a.nchunk;
+  if (slot >= a.rows) return;
+  // rows in a locality order (grouped by cluster): the rows in flight share
+  // their neighbours' gathered rows in L2.  Each row's sum is unchanged.
+  const int64_t row = a.order ? (int64_t)__ldg(a.order + slot) : slot;
   if (a.skip && a.skip[row]) return;            // long row: the warp path
-  const int chunk = (int)(gid - row * a.nchunk);
+  const int chunk = (int)(gid - slot * a.nchunk);
   const int64_t coloff = (int64_t)chunk * W;
   VT s = seg_sum<T, VT>(a.s, row, coloff);
   if (a.nl > 1) {   // multiplex: (sum_l P_l M) / L, layers added in order (walk.py:143-147)
@@ -295,6 +300,7 @@ int op_apply_t(const ancka_operator* op, const T* Q, int64_t ldq, int c, T* Z, i
       a.long_rows = op->split.long_rows;
       a.n_long = op->split.n_long;
     }
+    if (op->kind == ANCKA_GRAPH) a.order = op->split.locality_order;
   }
   return launch_spmm<T>(a, st);
 }
@@ -417,4 +423,50 @@ extern "C" int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_c
   };
   if (dtype == ANCKA_F64) return fill((double*)nullptr);
   return fill((float*)nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// rows grouped by label: order = rows sorted by (label, row) (radix sort)
+using namespace ancka;
+
+extern "C" size_t ancka_locality_order_workspace_size(int64_t n) {
+  size_t bytes = 0;
+  cub::DoubleBuffer<int32_t> kb(nullptr, nullptr), vb(nullptr, nullptr);
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, (int)n, 0, 32);
+  return bytes + 3 * (size_t)n * sizeof(int32_t) + 1024;
+}
+
+static __global__ void iota_labels_kernel(const int32_t* __restrict__ labels, int64_t n,
+                                   int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = labels[i];
+    vals[i] = (int32_t)i;
+  }
+}
+
+extern "C" int ancka_locality_order(const int32_t* labels, int64_t n, int32_t k, int32_t* order_out,
+                                    void* workspace, size_t workspace_bytes,
+                                    ancka_stream_t stream) {
+  ANCKA_REQUIRE(n >= 1 && n < (1ll << 31) && k >= 1, ANCKA_ERR_ARG, "locality_order: bad sizes");
+  Carver cv(workspace, workspace_bytes);
+  int32_t* k0 = cv.take<int32_t>(n);
+  int32_t* k1 = cv.take<int32_t>(n);
+  int32_t* v0 = cv.take<int32_t>(n);
+  size_t bytes = 0;
+  cub::DoubleBuffer<int32_t> kb(k0, k1), vb(v0, order_out);
+  ANCKA_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kb, vb, (int)n, 0, 32));
+  void* tmp = cv.take<char>(bytes);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "locality_order: workspace too small");
+  auto st = as_stream(stream);
+  int bits = 1;
+  while ((1 << bits) <= k) ++bits;
+  iota_labels_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 16 * kNumSMs), 256, 0, st>>>(
+      labels, n, k0, v0);
+  ANCKA_LAUNCHED();
+  ANCKA_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, kb, vb, (int)n, 0, bits, st));
+  if (vb.Current() != order_out)
+    ANCKA_CUDA(cudaMemcpyAsync(order_out, vb.Current(), sizeof(int32_t) * n,
+                               cudaMemcpyDeviceToDevice, st));
+  return ANCKA_OK;
 }

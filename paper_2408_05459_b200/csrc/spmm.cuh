@@ -28,6 +28,7 @@ struct SpmmArgs {
   int64_t self_ld = 0;
   const T* beta = nullptr;          // nullptr: no mix (structure only)
   const uint8_t* skip = nullptr;    // long rows: handled by the warp path below
+  const int32_t* order = nullptr;   // regular rows processed in this order (locality)
   const int32_t* long_rows = nullptr;  // f32: rows done by a warp per (row, column chunk)
   int64_t n_long = 0;
   const int32_t* tag = nullptr;     // epilogue: out = scale*out + (col==tag ? tagval[col] : 0)

@@ -799,6 +799,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         with timer.span("init_ms"):
             labels0, _, sizes0_dev, sizes0 = _init_labels_sizes(op, k, params.t_i, params.alpha)
         WORKSPACE.release("init")
+        op.set_locality(labels0, k)       # row order of the f32 graph applies (L2 reuse)
         rng = np.random.default_rng(params.seed)
         c = min(k + 1, n)
         # Q0 = [1/sqrt(n) | Yhat0] (engine.py:368-371), f64 for the exact first step
@@ -843,6 +844,7 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                     _repair_missing_columns(qt, kd, k, lab_t, info)
             with timer.span("mhc_ms"):
                 mhc(lab_t, loop.stats[3:4])
+            op.set_locality(lab_t, k)     # regroup the apply's rows by the current clusters
             if dq_first is not None:
                 loop.stats[0] = dq_first * dq_first
                 loop.stats[2] = 0.0
