@@ -82,6 +82,95 @@ struct CandList {
   }
 };
 
+// Top-K list plus a band pool (single-product path).  The K best (a desc,
+// j asc) sit in a sorted register array; candidates within `band` below the
+// current K-th sit unsorted in a pool of P slots.  Admission is a >= K-th -
+// band (not the 32nd best of a 32-slot sorted list), so a stream of n keys
+// costs ~K ln(n/K) sorted inserts instead of ~(K+P) ln(n/(K+P)), and band
+// candidates are appends.  A full pool evicts its minimum; `ovf` keeps the
+// largest value dropped for lack of room, which the merge's certificate
+// compares with the final threshold (dead entries, below a later K-th -
+// band, are evicted first and never matter).
+template <int KT, int P>
+struct TopPool {
+  float f[KT];
+  int32_t j[KT];
+  float pf[P];
+  int32_t pj[P];
+  int pcnt;
+  float ovf, thr, floor_;
+
+  __device__ __forceinline__ void clear(int K, float base) {
+#pragma unroll
+    for (int t = 0; t < KT; ++t) {
+      f[t] = t < KT - K ? kInf : -kInf;
+      j[t] = -1;
+    }
+#pragma unroll
+    for (int t = 0; t < P; ++t) { pf[t] = -kInf; pj[t] = -1; }
+    pcnt = 0;
+    ovf = -kInf;
+    thr = floor_ = base;
+  }
+  __device__ __forceinline__ float kth() const { return f[KT - 1]; }
+  __device__ __forceinline__ void refresh(float band) { thr = fmaxf(f[KT - 1] - band, floor_); }
+  __device__ __forceinline__ void raise_floor(float b) {
+    floor_ = fmaxf(floor_, b);
+    thr = fmaxf(thr, floor_);
+  }
+  __device__ __forceinline__ void pool_add(float v, int32_t jj) {
+    if (pcnt < P) {
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        pf[t] = t == pcnt ? v : pf[t];
+        pj[t] = t == pcnt ? jj : pj[t];
+      }
+      ++pcnt;
+      return;
+    }
+    int mi = 0;
+    float mv = pf[0];
+    int32_t mj = pj[0];
+#pragma unroll
+    for (int t = 1; t < P; ++t) {
+      const bool worse = pf[t] < mv || (pf[t] == mv && pj[t] > mj);
+      mi = worse ? t : mi;
+      mv = worse ? pf[t] : mv;
+      mj = worse ? pj[t] : mj;
+    }
+    if (v > mv || (v == mv && jj < mj)) {
+      ovf = fmaxf(ovf, mv);
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        pf[t] = t == mi ? v : pf[t];
+        pj[t] = t == mi ? jj : pj[t];
+      }
+    } else {
+      ovf = fmaxf(ovf, v);
+    }
+  }
+  __device__ __forceinline__ void insert(float v, int32_t jj, float band) {
+    if (v > f[KT - 1] || (v == f[KT - 1] && jj < j[KT - 1])) {
+      const float dv = f[KT - 1];
+      const int32_t dj = j[KT - 1];
+      int pos = 0;
+#pragma unroll
+      for (int t = 0; t < KT; ++t) pos += (f[t] > v || (f[t] == v && j[t] < jj)) ? 1 : 0;
+#pragma unroll
+      for (int t = KT - 1; t > 0; --t) {
+        const bool sh = t > pos, put = t == pos;
+        f[t] = sh ? f[t - 1] : (put ? v : f[t]);
+        j[t] = sh ? j[t - 1] : (put ? jj : j[t]);
+      }
+      if (pos == 0) { f[0] = v; j[0] = jj; }
+      v = dv;
+      jj = dj;
+    }
+    if (jj >= 0 && v >= f[KT - 1] - band) pool_add(v, jj);
+    refresh(band);
+  }
+};
+
 template <int L_, int E_>
 struct SlotCfg { static constexpr int L = L_, E = E_; };
 // split-bf16 path (eps ~ 2^-16): few near-K candidates per row
@@ -246,21 +335,34 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   const bool live = i < p.q_end;
   const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
   constexpr int L = SL::L, E = SL::E;
+  constexpr int KT = L - E, P = E - 1;   // top list (K <= KT), pool, 1 overflow slot
   const float eps_i = (live && p.row_eps) ? p.row_eps[i] : p.eps;
   const float band_i = 2.f * eps_i;
-  CandList<L, E> C;
+  TopPool<KT, P> C;
   C.clear(p.K, -eps_i);
   const int lists = p.nseg * (EPI_WARPS / 4);
-  const int live_n = p.K + E, pad = L - live_n;
+  // list layout (live_n = K + E int2): K top entries (a desc), the pool
+  // (compact, unsorted), padding (-inf, -1), and in the last slot
+  // (ovf, -1): the merge stops at the first id < 0 and reads the last slot
+  // as the bound on dropped candidates
+  const int live_n = p.K + E, padk = KT - p.K;
   int2* slot = p.partial + ((size_t)(live ? i - p.q_begin : 0) * lists + seg * (EPI_WARPS / 4) + half) * live_n;
   if (p.resume && live) {
 #pragma unroll
-    for (int t = 0; t < L; ++t)
-      if (t >= pad) {
-        const int2 e = slot[t - pad];
+    for (int t = 0; t < KT; ++t)
+      if (t >= padk) {
+        const int2 e = slot[t - padk];
         C.f[t] = __int_as_float(e.x);
         C.j[t] = e.y;
       }
+#pragma unroll
+    for (int t = 0; t < P; ++t) {
+      const int2 e = slot[p.K + t];
+      C.pf[t] = __int_as_float(e.x);
+      C.pj[t] = e.y;
+      C.pcnt += e.y >= 0 ? 1 : 0;
+    }
+    C.ovf = __int_as_float(slot[live_n - 1].x);
     C.refresh(band_i);
   }
   if (!live) C.raise_floor(kInf);          // padding rows admit nothing
@@ -317,7 +419,8 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
         for (int w = 8; w > 0; w >>= 1)
 #pragma unroll
           for (int u = 0; u < w; ++u) mx[u] = fmaxf(mx[u], mx[u + w]);
-        if (mx[0] >= C.thr) {
+        if (mx[0] >= C.thr && p.debug != 3) {   // debug 3: the scan without admissions
+
           const int64_t jb = j0 + (ch + h2) * 32;
           uint32_t mask = 0;
 #pragma unroll
@@ -350,8 +453,11 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   drain(__reduce_max_sync(0xffffffffu, pc));
   if (live) {
 #pragma unroll
-    for (int t = 0; t < L; ++t)
-      if (t >= pad) slot[t - pad] = make_int2(__float_as_int(C.f[t]), C.j[t]);
+    for (int t = 0; t < KT; ++t)
+      if (t >= padk) slot[t - padk] = make_int2(__float_as_int(C.f[t]), C.j[t]);
+#pragma unroll
+    for (int t = 0; t < P; ++t) slot[p.K + t] = make_int2(__float_as_int(C.pf[t]), C.pj[t]);
+    slot[live_n - 1] = make_int2(__float_as_int(C.ovf), -1);
   }
 }
 
