@@ -319,7 +319,7 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
 //   (lanes hit candidates at independent times); batched, the lanes insert
 //   together.  The threshold is refreshed at each drain, so between drains it
 //   is a (valid, lower) stale bound.
-template <class SL>
+template <class SL, bool PAIR = false>
 __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t* tempty,
                                                       uint32_t tmem, float* stash_base,
                                                       const RealParams& p, int64_t q0, int seg,
@@ -406,7 +406,10 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
       if (ch + 2 == EPI_COLS / 32) {
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_remote(mapa_rank(&tempty[acc], 0));   // leader's
+          else mbar_arrive(&tempty[acc]);
+        }
       }
       if (p.debug == 1) continue;
 #pragma unroll
@@ -723,6 +726,123 @@ knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   if (warp == 1) tmem_dealloc<TMEM_COLS>(tmem);
 }
 
+// CTA-pair variant of knn_real16_kernel: a (2,1,1) cluster covers 256
+// query rows with one M=256 N=256 MMA per k-step (tcgen05 cta_group::2).
+// Each CTA stages its own 128 query rows and HALF of every 256-key tile
+// (keys [0,128) in rank 0, [128,256) in rank 1), so each SM pulls half the
+// key bytes from L2 per tile that the 1-CTA kernel does -- the 1-CTA
+// kernel streams 12 TB of keys from L2 per Amazon2M search and is bound by
+// that (~9.6 TB/s), not by the tensor cores.  The accumulator layout in
+// each CTA's TMEM (its 128 rows x 256 columns) and the epilogue are the
+// 1-CTA ones; only the accumulator-free handshake goes to the leader.
+namespace pair16 {
+constexpr int HB_BYTES = (tc::BN / 2) * tc::ROW_BYTES;    // half key tile per k-block (16 KB)
+constexpr int A_BYTES = tc::BM * tc::ROW_BYTES;
+constexpr int STASH = 32 * tc::EPI_WARPS * 33 * 4;
+constexpr int MAXS = 10;
+__host__ __device__ constexpr int stages(int nks) { return nks <= 2 ? 8 : (nks <= 3 ? 7 : 6); }
+__host__ __device__ constexpr size_t smem(int nks) {
+  return 1024 + (size_t)nks * A_BYTES + (size_t)stages(nks) * HB_BYTES + 256 + STASH;
+}
+}  // namespace pair16
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc::THREADS, 1)
+knn_real16_pair_kernel(const __grid_constant__ CUtensorMap tmA, RealParams p) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  const int nks = p.nkb_seg, S = pair16::stages(nks);
+  unsigned char* base = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+  unsigned char* sA = base;
+  unsigned char* sB = sA + nks * pair16::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * pair16::HB_BYTES);
+  uint64_t* empty = full + pair16::MAXS;
+  uint64_t* tfull = empty + pair16::MAXS;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* afull = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
+  float* stash_base =
+      reinterpret_cast<float*>(base + nks * pair16::A_BYTES + S * pair16::HB_BYTES + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_ctarank();
+  const int64_t q0 = p.q_begin + (int64_t)blockIdx.x * BM;
+  const int seg = blockIdx.y;
+  const int kt0 = p.kt_base + seg * p.tiles_per_seg;
+  const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
+  const int ntiles = kt1 - kt0;
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    for (int s2 = 0; s2 < S; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
+    for (int s2 = 0; s2 < 2; ++s2) { mbar_init(&tfull[s2], 1); mbar_init(&tempty[s2], 2 * EPI_WARPS); }
+    mbar_init(afull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();                 // barriers of both CTAs initialised, TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  constexpr int EL = ROW_BYTES / 2;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t afull_l = mapa_rank(afull, 0);
+      if (rank == 0) mbar_arrive_expect_tx(afull, 2 * nks * pair16::A_BYTES);
+      for (int kb = 0; kb < nks; ++kb)
+        tma_load_2d_pair(sA + kb * pair16::A_BYTES, &tmA, afull_l, kb * EL, (int)q0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int krow = (kt0 + t) * BN + (int)rank * (BN / 2);
+        for (int kb = 0; kb < nks; ++kb) {
+          mbar_wait_backoff(&empty[stage], phase ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * pair16::HB_BYTES);
+          tma_load_2d_pair(sB + stage * pair16::HB_BYTES, &tmA, mapa_rank(&full[stage], 0),
+                           kb * EL, krow);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = make_idesc(0u, 2 * BM, BN);   // kind::f16, F16, M=256
+      const bool skip = p.debug == 2;
+      mbar_wait_sleep(afull, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = 0; t < ntiles; ++t) {
+        const int acc = t & 1;
+        const uint32_t acc_phase = (t >> 1) & 1;
+        mbar_wait_backoff(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + acc * BN;
+        for (int kb = 0; kb < nks; ++kb) {
+          mbar_wait_backoff(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t b_addr = smem_u32(sB + stage * pair16::HB_BYTES);
+          const uint32_t a_addr = smem_u32(sA + kb * pair16::A_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            if (skip || kb * 64 + k * 16 >= p.d) continue;
+            mma_f16_ss_pair(dtm, sw128_kmajor_desc(a_addr + k * 32),
+                            sw128_kmajor_desc(b_addr + k * 32), idesc, (kb | k) != 0);
+          }
+          mma_commit_pair(&empty[stage]);
+          if (++stage == S) { stage = 0; phase ^= 1; }
+        }
+        mma_commit_pair(&tfull[acc]);
+      }
+    }
+  } else {
+    real_epilogue_batched<SlotsF16, true>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
+  }
+  tc_fence_before();
+  cluster_sync();                 // no remote arrivals or MMA writes still in flight
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc_pair<TMEM_COLS>(tmem);
+}
+
 // warp per query row: merge the partial lists, certify, rerank in f64
 template <class SL>
 __global__ void knn_real_merge_kernel(const int2* __restrict__ partial, int64_t q_begin,
@@ -1017,24 +1137,32 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
   const int kt_first = (int)(R.kr.k0 / tc::BN);
   const int nlaunch = (int)ceil_div(R.g.key_tiles, seg_tiles);
   int lists = R.lists;
-  {
-    const size_t sm = res16::smem(p.nkb_seg);
+  // CTA pairs (cta_group::2) unless ANCKA_KNN_PAIR=0
+  const bool pair = !getenv("ANCKA_KNN_PAIR") || atoi(getenv("ANCKA_KNN_PAIR")) != 0;
+  const size_t sm = pair ? pair16::smem(p.nkb_seg) : res16::smem(p.nkb_seg);
+  const int qt = pair ? (int)((R.g.q_tiles + 1) & ~1) : R.g.q_tiles;
+  if (pair)
+    ANCKA_CUDA(cudaFuncSetAttribute(knn_real16_pair_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+  else
     ANCKA_CUDA(cudaFuncSetAttribute(knn_real16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sm));
-    if (nlaunch <= 1) {
-      dim3 grid(R.g.q_tiles, R.g.nseg);
-      knn_real16_kernel<<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+  auto launch = [&](dim3 grid) {
+    if (pair) knn_real16_pair_kernel<<<grid, tc::THREADS, sm, st>>>(ma, p);
+    else knn_real16_kernel<<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+  };
+  if (nlaunch <= 1) {
+    launch(dim3(qt, R.g.nseg));
+    ANCKA_LAUNCHED();
+  } else {
+    p.nseg = 1;
+    p.tiles_per_seg = seg_tiles;
+    lists = tc::EPI_WARPS / 4;
+    for (int l = 0; l < nlaunch; ++l) {
+      p.kt_base = kt_first + l * seg_tiles;
+      p.resume = l > 0;
+      launch(dim3(qt, 1));
       ANCKA_LAUNCHED();
-    } else {
-      p.nseg = 1;
-      p.tiles_per_seg = seg_tiles;
-      lists = tc::EPI_WARPS / 4;
-      for (int l = 0; l < nlaunch; ++l) {
-        p.kt_base = kt_first + l * seg_tiles;
-        p.resume = l > 0;
-        knn_real16_kernel<<<dim3(R.g.q_tiles, 1), tc::THREADS, sm, st>>>(ma, mb, p);
-        ANCKA_LAUNCHED();
-      }
     }
   }
   const int mg = (int)std::min<int64_t>(ceil_div(nq * 32, 256), 16 * kNumSMs);
