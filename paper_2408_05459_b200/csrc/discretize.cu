@@ -216,7 +216,7 @@ __host__ __device__ inline size_t disc_rot_bytes(int k, int off) {
 // k > 8 phase-A layout: group accumulators | group counts | tile | tile labels
 __host__ __device__ inline size_t disc_tc_tile_bytes(int k, int off, int dbuf = 1) {
   const size_t tc = (dbuf ? 2 : 1) * (size_t)kDiscThreads * (((k + 15) & ~15) + 4) * 4;
-  const size_t win = (size_t)kDiscThreads * 4 * win_sw(disc_kmax(k, off));
+  const size_t win = (dbuf ? 2 : 1) * (size_t)kDiscThreads * 4 * win_sw(disc_kmax(k, off));
   return tc > win ? tc : win;
 }
 __host__ __device__ inline size_t disc_tc_acc_bytes(int k, int G) {
@@ -240,9 +240,10 @@ struct Win {
   static constexpr int SW = win_sw(KMAX);
 };
 
-// Stage rows [t0, t0 + tr) of Q's column window into tile (async copies).
-__device__ __forceinline__ void stage_window(const DiscParams& p, int64_t t0, int tr, float* tile,
-                                             int SW, bool vec) {
+// Stage rows [t0, t0 + tr) of Q's column window into tile (async copies,
+// one commit group).
+__device__ __forceinline__ void stage_window_issue(const DiscParams& p, int64_t t0, int tr,
+                                                   float* tile, int SW, bool vec) {
   const int k = p.k, off = (int)(p.col0 & 3);
   const int64_t c0 = p.col0 - off;
   if (vec) {   // 16-byte chunks of the aligned window
@@ -273,8 +274,7 @@ __device__ __forceinline__ void stage_window(const DiscParams& p, int64_t t0, in
       if (l >= k) { l -= k; ++r; }
     }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  __syncthreads();
+  asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
 // This thread's row from the staged tile: raw[m] = Q[i, c0 + m] inside the
@@ -467,30 +467,57 @@ __device__ __forceinline__ long long fx_round(float x, int sh) {
   return (b >> 31) ? -v : v;
 }
 
+// 64-bit add to a shared-memory cell (lo, hi words) with two native 32-bit
+// atomics: the low-word atomic's old value gives this add's carry, so the
+// cell is exact mod 2^64 under any interleaving (the 64-bit shared atomic
+// is a compare-and-swap loop on sm_100)
+__device__ __forceinline__ void sadd64(unsigned* cell, long long v) {
+  const unsigned lo = (unsigned)v, hi = (unsigned)((unsigned long long)v >> 32);
+  const unsigned old = atomicAdd(cell, lo);
+  const unsigned h = hi + ((old + lo < old) ? 1u : 0u);
+  if (h) atomicAdd(cell + 1, h);
+}
+
 template <int KMAX>
 __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const double* sR64,
                                     float* tile, int* tlab, long long* gacc, int* gcnt, bool score,
-                                    unsigned long long* gdst) {
+                                    unsigned long long* gdst, const unsigned long long* gprev) {
   constexpr int NBM = disc_nbmax(KMAX);
   const int k = p.k, kk = k * k, kq = disc_kq(k), ks16 = kq / 16, nb8 = kq / 8;
   const int SWQ = kq + 4;
   const size_t tile_floats = p.dbuf ? (size_t)kDiscThreads * SWQ : 0;
-  // tile labels, within-bucket ranks, row permutation, bucket offsets and
-  // counts, rows to rescore exactly
+  int* flagged = tlab + 3 * kDiscThreads + 68 + 64;   // kDiscThreads
+  double* wq = reinterpret_cast<double*>(flagged + kDiscThreads);   // 8 warps x 64, 16-B aligned
+  int* wcnt = flagged + kDiscThreads + 2 * 8 * 64;    // 8 warps x 64 labels (after wq)
+  int* told = wcnt + 8 * 64;                          // kDiscThreads
+  __shared__ int s_nflag;
+  // Cluster sums in 64-bit fixed point, element by element (fx_round: the
+  // same integer for the same q~ entry every round), so totals can be
+  // carried: a round after the first adds only the rows whose label moved
+  // (-fx to the old cluster, +fx to the new one) to the previous round's
+  // totals, and the result is the exact integer a full recount gives.
+  // gprev == nullptr: full recount (first round of a start, after a reseed).
+  const bool full = gprev == nullptr;
+  const int sh = ilogb(p.fx_scale);
+  // tile labels, within-bucket ranks, entry permutation, bucket offsets and
+  // sizes, rows to rescore exactly, rescoring scratch, per-warp counts,
+  // labels before this round's scoring
   int* trank = tlab + kDiscThreads;
   int* perm = trank + kDiscThreads;
   int* boff = perm + kDiscThreads;        // k + 1 (68 slots)
   int* bcnt = boff + 68;                  // k (64 slots)
-  int* flagged = bcnt + 64;               // kDiscThreads
-  double* wq = reinterpret_cast<double*>(flagged + kDiscThreads);   // 8 warps x 64, 16-B aligned
-  __shared__ int s_nflag;
-  double* gsum = reinterpret_cast<double*>(gacc);    // CTA cluster sums (f64)
-  int* wcnt = flagged + kDiscThreads + 2 * 8 * 64;    // 8 warps x 64 labels (after wq)
-  for (int e = threadIdx.x; e < k * kq; e += blockDim.x) gsum[e] = 0.0;
+  (void)bcnt;
+  __shared__ int s_nchg;
+  for (int e = threadIdx.x; e < k * kq; e += blockDim.x) gacc[e] = 0;
   for (int e = threadIdx.x; e < k; e += blockDim.x) gcnt[e] = 0;
-  for (int e = threadIdx.x; e < 8 * 64; e += blockDim.x) wcnt[e] = 0;
+  if (!full)   // carry: this CTA's slice of the previous totals
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kk + k;
+         e += (int64_t)gridDim.x * blockDim.x) {
+      const unsigned long long v = __ldcg(gprev + e);
+      if (v) atomicAdd(gdst + e, v);
+    }
+  __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int ngb = kDiscThreads / kq, grp = threadIdx.x / kq, col = threadIdx.x % kq;
   const Rows R = my_rows(p.n);
   const int ntile = (int)ceil_div(R.r1 - R.r0, (int64_t)kDiscThreads);
   const int c4 = kq / 4;
@@ -522,9 +549,14 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     }                                                   \
   } while (0)
   if (ntile > 0 && p.dbuf) stage(0);
+  // labels before this round, read one tile ahead (latency off the scoring path)
+  int old_next = (!full && threadIdx.x < R.r1 - R.r0) ? __ldcg(p.labels + R.r0 + threadIdx.x) : -1;
   for (int ti = 0; ti < ntile; ++ti) {
     const int64_t t0 = R.r0 + (int64_t)ti * kDiscThreads;
     const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
+    told[threadIdx.x] = old_next;
+    old_next = (!full && t0 + kDiscThreads + threadIdx.x < R.r1)
+                   ? __ldcg(p.labels + t0 + kDiscThreads + threadIdx.x) : -1;
     if (!p.dbuf) {
       stage(ti);
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -534,7 +566,6 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
-    for (int e = threadIdx.x; e < 8 * 64; e += blockDim.x) wcnt[e] = 0;
     if (threadIdx.x == 0) s_nflag = 0;
     __syncthreads();
     SUBSTAMP(8);
@@ -603,7 +634,6 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
             if (t == 0 && row < tr) {
               if (!(best - second > kCert)) flagged[atomicAdd(&s_nflag, 1)] = row;
               p.labels[t0 + row] = bi;
-              p.margin[t0 + row] = second;
               tlab[row] = bi;
             }
           }
@@ -619,7 +649,6 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
         score_row_exact_warp(p, sR64, t0 + row, wq + warp * 64, lab, second);
         if (lane == 0) {
           p.labels[t0 + row] = lab;
-          p.margin[t0 + row] = second;
           tlab[row] = lab;
         }
       }
@@ -628,78 +657,53 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     }
     __syncthreads();
     SUBSTAMP(10);
-    // rows grouped by label with a stable counting sort (ranks from warp
-    // matches + per-warp label counts), so every bucket lists its rows in
-    // row order and the f64 sums below have a fixed order
-    {
-      const int r = threadIdx.x;
-      const int lab = r < tr ? tlab[r] : 0x40000000 + r;       // unique sentinel
-      const unsigned match = __match_any_sync(0xffffffffu, lab);
-      const unsigned lt = (1u << lane) - 1u;
-      trank[r] = __popc(match & lt);
-      if (r < tr && (match & lt) == 0) wcnt[warp * 64 + lab] = __popc(match);
+    // rows whose cluster changed (every row in a full recount)
+    if (threadIdx.x == 0) s_nchg = 0;
+    __syncthreads();
+    {   // one shared atomic per warp: ballot, then ranks within the warp
+      const bool mv = threadIdx.x < tr && tlab[threadIdx.x] != told[threadIdx.x];
+      const unsigned m = __ballot_sync(0xffffffffu, mv);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&s_nchg, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (mv) perm[base + __popc(m & ((1u << lane) - 1u))] = threadIdx.x;
     }
     __syncthreads();
-    if (threadIdx.x < k) {                // per label: warp bases, bucket size
-      const int l = threadIdx.x;
-      int run = 0;
+    if (dbg) p.tdbg[13] += s_nchg;
+    // a warp per changed row, lanes over columns: +fx to the new cluster,
+    // -fx to the old one (shared 64-bit atomics; integers: order free)
+    for (int c = warp; c < s_nchg; c += kDiscThreads / 32) {
+      const int r = perm[c], l = tlab[r], o = told[r];
+      const float* row = tl + r * SWQ;
+      unsigned* acc = reinterpret_cast<unsigned*>(gacc);
 #pragma unroll
-      for (int w = 0; w < kDiscThreads / 32; ++w) {
-        const int c = wcnt[w * 64 + l];
-        wcnt[w * 64 + l] = run;
-        run += c;
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (j < k) {
+          const long long fx = fx_round(row[j], sh);
+          if (fx != 0) {
+            sadd64(acc + 2 * (l * kq + j), fx);
+            if (o >= 0) sadd64(acc + 2 * (o * kq + j), -fx);
+          }
+        }
       }
-      bcnt[l] = run;
-    }
-    __syncthreads();
-    if (warp == 0) {
-      const int c0 = lane < k ? bcnt[lane] : 0, c1 = lane + 32 < k ? bcnt[lane + 32] : 0;
-      int x0 = c0, x1 = c1;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y0 = __shfl_up_sync(0xffffffffu, x0, o), y1 = __shfl_up_sync(0xffffffffu, x1, o);
-        if (lane >= o) { x0 += y0; x1 += y1; }
+      if (lane == 0) {
+        atomicAdd(&gcnt[l], 1);
+        if (o >= 0) atomicAdd(&gcnt[o], -1);
       }
-      const int tot0 = __shfl_sync(0xffffffffu, x0, 31);
-      if (lane < k) boff[lane] = x0 - c0;
-      if (lane + 32 < k) boff[lane + 32] = tot0 + x1 - c1;
-      if (lane == 0) boff[k] = tr;
-    }
-    __syncthreads();
-    if (threadIdx.x < tr) {
-      const int lab = tlab[threadIdx.x];
-      perm[boff[lab] + wcnt[warp * 64 + lab] + trank[threadIdx.x]] = threadIdx.x;
-    }
-    __syncthreads();
-    SUBSTAMP(11);
-    // a warp per bucket, lanes over columns: f64 sums in row order, one
-    // update of the CTA accumulator per (bucket, column)
-    for (int b = warp; b < k; b += kDiscThreads / 32) {
-      const int q0 = boff[b], q1 = boff[b + 1];
-      if (q0 == q1) continue;
-      double s0 = 0.0, s1 = 0.0;
-      const bool c0ok = lane < k, c1ok = lane + 32 < k;
-      for (int q = q0; q < q1; ++q) {
-        const float* row = tl + perm[q] * SWQ;
-        if (c0ok) s0 += (double)row[lane];
-        if (c1ok) s1 += (double)row[lane + 32];
-      }
-      if (c0ok) gsum[b * kq + lane] += s0;
-      if (c1ok) gsum[b * kq + lane + 32] += s1;
-      if (lane == 0) gcnt[b] += q1 - q0;
     }
     __syncthreads();
     SUBSTAMP(12);
   }
 #undef SUBSTAMP
-  // CTA sums -> 64-bit fixed point -> global totals (integer atomics: order free)
+  // CTA deltas -> global totals (integer atomics: order free)
   for (int e = threadIdx.x; e < kk; e += blockDim.x) {
     const int l = e / k, j = e - l * k;
-    const long long v = __double2ll_rn(gsum[l * kq + j] * p.fx_scale);
+    const long long v = gacc[l * kq + j];
     if (v != 0) atomicAdd(gdst + e, (unsigned long long)v);
   }
   for (int e = threadIdx.x; e < k; e += blockDim.x)
-    if (gcnt[e] != 0) atomicAdd(gdst + kk + e, (unsigned long long)gcnt[e]);
+    if (gcnt[e] != 0) atomicAdd(gdst + kk + e, (unsigned long long)(long long)gcnt[e]);
   __syncthreads();
 }
 
@@ -908,13 +912,55 @@ __device__ double polar_ns_small_cta(const double* A, double* X, int k, int* ite
   return tr;
 }
 
-__device__ double polar_ns(const double* A, double* X, double* Y, double* T, int k, int* flag,
-                           double* red, int* iters) {
+// C = op(A) B for k x k row-major blocks (op(A) = A^T when TA): 16 x 16
+// threads, each a TB x TB register block (TB = ceil(k / 16), compile time)
+template <int TB, bool TA>
+__device__ __forceinline__ void mm_blk(const double* A, const double* B, double (&acc)[TB][TB], int k) {
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+#pragma unroll
+  for (int u = 0; u < TB; ++u)
+#pragma unroll
+    for (int v = 0; v < TB; ++v) acc[u][v] = 0.0;
+  for (int l = 0; l < k; ++l) {
+    double xa[TB], xb[TB];
+#pragma unroll
+    for (int u = 0; u < TB; ++u) {
+      const int a = ty * TB + u, b = tx * TB + u;
+      xa[u] = a < k ? (TA ? A[l * k + a] : A[a * k + l]) : 0.0;
+      xb[u] = b < k ? B[l * k + b] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < TB; ++u)
+#pragma unroll
+      for (int v = 0; v < TB; ++v) acc[u][v] = fma(xa[u], xb[v], acc[u][v]);
+  }
+}
+template <int TB, typename F>
+__device__ __forceinline__ void blk_each(int k, F f) {
+  const int ty = threadIdx.x / 16, tx = threadIdx.x % 16;
+#pragma unroll
+  for (int u = 0; u < TB; ++u)
+#pragma unroll
+    for (int v = 0; v < TB; ++v) {
+      const int a = ty * TB + u, b = tx * TB + v;
+      if (a < k && b < k) f(u, v, a * k + b);
+    }
+}
+
+// k > 8: X -> polar factor by Newton-Schulz in f64.  `qs` quintic sweeps
+// X <- X (a I + b Y + c Y^2), Y = X^T X, first (small singular values grow
+// 3.44x per sweep for 3 products, against 1.5x per cubic step for 2; all
+// stay in (0, 1.13], inside the cubic basin), then cubic steps to the
+// fixed point.  The caller sizes qs from the previous round's count (the
+// rounds of one call have similar conditioning); the limit is the polar
+// factor either way.
+template <int TB>
+__device__ double polar_ns_tb(const double* A, double* X, double* Y, double* T, int k, int qs,
+                              int* flag, double* red, int* iters) {
   __shared__ double s_tr;
-  if (k <= 8) return polar_ns_small_cta(A, X, k, iters, red);
   const int kk = k * k, t = threadIdx.x;
   if (t < 32) {
-    const double sb = sigma_bound_warp(A, k, true);   // k = 47: 11.6 -> 7.1 sweeps per round
+    const double sb = sigma_bound_warp(A, k, true);
     if (t == 0) s_tr = sb;
   }
   __syncthreads();
@@ -922,74 +968,43 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
   __syncthreads();
   for (int e = t; e < kk; e += blockDim.x) X[(e % k) * k + e / k] = A[e] * inv;  // A^T
   __syncthreads();
-  // 16 x 16 threads, each a TB x TB register block of the k x k products
-  const int TB = (k + 15) / 16;            // <= 4 for k <= 64
-  const int ty = t / 16, tx = t % 16;
+  double acc[TB][TB];
   int it = 0;
-  for (; it < 100; ++it) {
-    double acc[4][4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int l = 0; l < k; ++l) {            // Y = X^T X: Y[a][b] = sum_l X[l][a] X[l][b]
-      double xa[4], xb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int a = ty * TB + u, b = tx * TB + u;
-        xa[u] = (u < TB && a < k) ? X[l * k + a] : 0.0;
-        xb[u] = (u < TB && b < k) ? X[l * k + b] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] += xa[u] * xb[v];
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int a = ty * TB + u, b = tx * TB + v;
-        if (u < TB && v < TB && a < k && b < k) Y[a * k + b] = acc[u][v];
-      }
+  for (int q = 0; q < qs; ++q, ++it) {
+    constexpr double qa = 3.4445, qb = -4.7750, qc = 2.0315;
+    mm_blk<TB, true>(X, X, acc, k);                      // Y = X^T X
+    blk_each<TB>(k, [&](int u, int v, int e) { Y[e] = acc[u][v]; });
+    __syncthreads();
+    mm_blk<TB, false>(Y, Y, acc, k);                     // T = a I + b Y + c Y^2
+    blk_each<TB>(k, [&](int u, int v, int e) {
+      T[e] = qb * Y[e] + qc * acc[u][v] + ((e / k == e % k) ? qa : 0.0);
+    });
+    __syncthreads();
+    mm_blk<TB, false>(X, T, acc, k);                     // X <- X T
+    __syncthreads();
+    blk_each<TB>(k, [&](int u, int v, int e) { X[e] = acc[u][v]; });
+    __syncthreads();
+  }
+  for (int c = 0; c < 100; ++c) {
+    mm_blk<TB, true>(X, X, acc, k);                      // Y = X^T X
+    blk_each<TB>(k, [&](int u, int v, int e) { Y[e] = acc[u][v]; });
     __syncthreads();
     if (t == 0) *flag = 0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int l = 0; l < k; ++l) {            // T = X Y: T[a][b] = sum_l X[a][l] Y[l][b]
-      double xa[4], yb[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int a = ty * TB + u, b = tx * TB + u;
-        xa[u] = (u < TB && a < k) ? X[a * k + l] : 0.0;
-        yb[u] = (u < TB && b < k) ? Y[l * k + b] : 0.0;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] += xa[u] * yb[v];
-    }
-    __syncthreads();                          // all reads of X done
+    mm_blk<TB, false>(X, Y, acc, k);                     // T = X Y
+    __syncthreads();                                     // all reads of X done
     bool moved = false;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int a = ty * TB + u, b = tx * TB + v;
-        if (u < TB && v < TB && a < k && b < k) {
-          const double xo = X[a * k + b];
-          const double xn = 1.5 * xo - 0.5 * acc[u][v];
-          moved |= fabs(xn - xo) > 1e-14 * k;
-          X[a * k + b] = xn;
-        }
-      }
+    blk_each<TB>(k, [&](int u, int v, int e) {
+      const double xo = X[e];
+      const double xn = 1.5 * xo - 0.5 * acc[u][v];
+      moved |= fabs(xn - xo) > 1e-14 * k;
+      X[e] = xn;
+    });
+    ++it;
     if (moved) *flag = 1;
     __syncthreads();
     const bool more = *flag != 0;
     __syncthreads();
-    if (!more) { ++it; break; }
+    if (!more) break;
   }
   double tr = 0.0;                                        // tr(X A)
   for (int e = t; e < kk; e += blockDim.x) {
@@ -1000,6 +1015,14 @@ __device__ double polar_ns(const double* A, double* X, double* Y, double* T, int
   if (t == 0) *iters = it;
   __syncthreads();
   return tr;
+}
+
+template <int KMAX>
+__device__ double polar_ns(const double* A, double* X, double* Y, double* T, int k, int qs,
+                           int* flag, double* red, int* iters) {
+  if (k <= 8) return polar_ns_small_cta(A, X, k, iters, red);
+  constexpr int TB = KMAX <= 16 ? 1 : KMAX <= 32 ? 2 : KMAX <= 48 ? 3 : 4;
+  return polar_ns_tb<TB>(A, X, Y, T, k, qs, flag, red, iters);
 }
 
 // Totals accumulated by the fixed-point atomics of phase A (buffer ri % 3);
@@ -1026,6 +1049,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (p.tdbg && blockIdx.x == 0 && threadIdx.x == 0) {               \
       const unsigned long long _n = gtimer();                          \
       if ((s) != 0) p.tdbg[(s)] += _n - t_prev;                        \
+      else if (t_prev) p.tdbg[15] += _n - t_prev;                      \
       t_prev = _n;                                                     \
     }                                                                  \
   } while (0)
@@ -1087,6 +1111,7 @@ discretize_kernel(DiscParams p) {
     __syncthreads();
   }
 
+  int qs_next = 0;             // quintic Newton-Schulz sweeps for the next polar factor
   for (int run = p.run_lo; run < p.run_hi; ++run) {
     // ---------------------------------------------------- initial rotation
     if (run == 0) {
@@ -1118,22 +1143,48 @@ discretize_kernel(DiscParams p) {
             s_pcol[m] = (l >= 0 && l < k) ? sRp[l * k + (j - 1)] : 0.0;
           }
           __syncthreads();
-          for (int64_t t0 = rows.r0; t0 < rows.r1; t0 += kDiscThreads) {
+          // double-buffered window tiles: the copy of tile ti + 1 overlaps
+          // the dot products of tile ti
+          const int ntl = (int)ceil_div(rows.r1 - rows.r0, (int64_t)kDiscThreads);
+          const size_t wbuf = (size_t)kDiscThreads * SW;
+          auto issue = [&](int ti) {
+            const int64_t s0 = rows.r0 + (int64_t)ti * kDiscThreads;
+            stage_window_issue(p, s0, (int)lmin(kDiscThreads, rows.r1 - s0),
+                               tile + (p.dbuf ? (ti & 1) * wbuf : 0), SW, vec);
+          };
+          if (ntl > 0 && p.dbuf) issue(0);
+          // 1/||q_i|| and the running sum of this thread's row, one tile ahead
+          double inv_next = 0.0, acc_next = 0.0;
+          if (rows.r0 + threadIdx.x < rows.r1) {
+            inv_next = p.qinv[rows.r0 + threadIdx.x];
+            acc_next = p.proto_acc[rows.r0 + threadIdx.x];
+          }
+          for (int ti = 0; ti < ntl; ++ti) {
+            const int64_t t0 = rows.r0 + (int64_t)ti * kDiscThreads;
             const int tr = (int)lmin(kDiscThreads, rows.r1 - t0);
-            stage_window(p, t0, tr, tile, SW, vec);
+            const double inv = inv_next, acc_prev = acc_next;
+            if (t0 + kDiscThreads + threadIdx.x < rows.r1) {
+              inv_next = p.qinv[t0 + kDiscThreads + threadIdx.x];
+              acc_next = p.proto_acc[t0 + kDiscThreads + threadIdx.x];
+            }
+            if (!p.dbuf) {
+              issue(ti);
+              asm volatile("cp.async.wait_group 0;" ::: "memory");
+            } else if (ti + 1 < ntl) {
+              issue(ti + 1);
+              asm volatile("cp.async.wait_group 1;" ::: "memory");
+            } else {
+              asm volatile("cp.async.wait_group 0;" ::: "memory");
+            }
+            __syncthreads();
             if (threadIdx.x < tr) {
               const int64_t i = t0 + threadIdx.x;
               float raw[KW];
-              load_window<KMAX>(tile + threadIdx.x * SW, off, k, raw);
-              double s2 = 0.0;
-#pragma unroll
-              for (int m = 0; m < KW; ++m) s2 += (double)raw[m] * (double)raw[m];
-              const double nrm = sqrt(s2);
-              const double inv = nrm > 0 ? 1.0 / nrm : 0.0;
+              load_window<KMAX>(tile + (p.dbuf ? (ti & 1) * wbuf : 0) + threadIdx.x * SW, off, k, raw);
               double d = 0.0;
 #pragma unroll
               for (int m = 0; m < KW; ++m) d += ((double)raw[m] * inv) * s_pcol[m];
-              const double a = p.proto_acc[i] + fabs(d);
+              const double a = acc_prev + fabs(d);
               p.proto_acc[i] = a;
               if (bi < 0 || a < best) { best = a; bi = i; }
             }
@@ -1185,7 +1236,9 @@ discretize_kernel(DiscParams p) {
       TSTAMP(0);
       if (KMAX > 8)
         phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, true,
-                                  p.gfx + (size_t)(ri % 3) * (kk + k));
+                                  p.gfx + (size_t)(ri % 3) * (kk + k),
+                                  (run == p.run_lo && it == 0) ? nullptr
+                                                               : p.gfx + (size_t)((ri + 2) % 3) * (kk + k));
       else
         phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, true,
                                (run == 0 && it == 0) ? &s_zero : nullptr,
@@ -1240,7 +1293,7 @@ discretize_kernel(DiscParams p) {
         }
         if (KMAX > 8)
           phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, false,
-                                    p.gfx + (size_t)(ri % 3) * (kk + k));
+                                    p.gfx + (size_t)(ri % 3) * (kk + k), nullptr);
         else
           phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, false, nullptr,
                                  p.gfx + (size_t)(ri % 3) * (kk + k));
@@ -1257,8 +1310,13 @@ discretize_kernel(DiscParams p) {
       __syncthreads();
       TSTAMP(3);
       int ns_it = 0;
-      const double ssum = polar_ns(M, X, Y, T, k, &s_flag, red, &s_flag);
+      const double ssum = polar_ns<KMAX>(M, X, Y, T, k, qs_next, &s_flag, red, &s_flag);
       ns_it = s_flag;
+      {   // quintic sweeps for the next round: each replaces ~3 cubic steps
+        const int cubic = ns_it - qs_next;
+        qs_next = cubic > 7 ? qs_next + (cubic - 5) / 3 : (cubic < 5 && qs_next > 0 ? qs_next - 1 : qs_next);
+        if (qs_next > 12) qs_next = 12;
+      }
       if (p.tdbg && cta0 && threadIdx.x == 0) p.tdbg[7] += ns_it;
       TSTAMP(4);
       const double obj = (double)p.n - 2.0 * ssum;
@@ -1351,7 +1409,7 @@ static size_t disc_smem(int k, int G, int off, int dbuf = 1) {
   const size_t fixed = align_dev(disc_rot_bytes(k, off)) + align_dev(kk * 8);
   const size_t a = k > 8 ? align_dev(disc_tc_acc_bytes(k, G)) + align_dev((size_t)G * k * 4) +
                                align_dev(disc_tc_tile_bytes(k, off, dbuf)) +
-                               (4 * kDiscThreads + 68 + 64) * 4 + 8 * 64 * 8 + 8 * 64 * 4
+                               (5 * kDiscThreads + 68 + 64) * 4 + 8 * 64 * 8 + 8 * 64 * 4
                          : align_dev((size_t)G * kk * 8) + align_dev(disc_tile_bytes(k, off)) +
                                (kDiscThreads + (size_t)G * k) * 4;
   const size_t b = 4 * kk * 8 + (size_t)k * 8;

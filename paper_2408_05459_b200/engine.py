@@ -455,6 +455,19 @@ class _WideDiscretizer:
 
 _WIDE = {}
 
+#: ANCKA_DISC_TIMING=1: the discretize kernel's per-phase timers (ns / clocks,
+#: slots as tools/disc_timing.py names them) summed over the calls of a run
+DISC_PROFILE = {} if os.environ.get("ANCKA_DISC_TIMING") else None
+
+
+def _disc_profile_add(info, k):
+    t = info[8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k:].cpu().numpy().view(np.uint64)
+    h = info[:8].cpu().numpy()
+    DISC_PROFILE["calls"] = DISC_PROFILE.get("calls", 0) + 1
+    DISC_PROFILE["rounds"] = DISC_PROFILE.get("rounds", 0) + int(h[6] + h[7])
+    for i, v in enumerate(t):
+        DISC_PROFILE[i] = DISC_PROFILE.get(i, 0) + int(v)
+
 
 def _discretize_device(q32: torch.Tensor, col0: int, k: int, max_iter: int, tol: float,
                        labels_out: torch.Tensor, info: torch.Tensor):
@@ -821,7 +834,9 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         loop = _Loop(op, c, k, params.tau, use_graphs, fused)
         mhc = _MhcRunner(op, k, _lib.F32)
         lab_t = torch.empty(n, dtype=torch.int32, device=dev())
-        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64, device=dev())
+        # (+16: per-phase timers when ANCKA_DISC_TIMING is set)
+        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k + 16, dtype=torch.float64,
+                           device=dev())
         error, stop_reason, converged, t = None, "max_iterations", False, 0
         host_info = torch.empty(8, dtype=torch.float64, pin_memory=True)
         host_rb = torch.empty(4, dtype=torch.float64, pin_memory=True)
@@ -840,6 +855,8 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
             qt = loop.q
             with timer.span("discretize_ms"):
                 _discretize_device(qt, 1, kd, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, lab_t, info)
+                if DISC_PROFILE is not None:
+                    _disc_profile_add(info, kd)
                 if kd < k:
                     _repair_missing_columns(qt, kd, k, lab_t, info)
             with timer.span("mhc_ms"):

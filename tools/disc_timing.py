@@ -41,11 +41,11 @@ for rep in range(3):
     b.record()
     b.synchronize()
     t = info[8 + 200 + 2 * k * k:].cpu().numpy().view(np.uint64)
-    names = ["-", "sync_after_A", "reduce", "-", "polar", "proto_iter", "phaseA", "ns_iters"]
+    names = ["to_round_start", "sync_after_A", "reduce", "reseed+scale", "polar", "proto_iter", "phaseA", "ns_iters"]
     inf = info[:8].cpu().numpy()
     print(f"total {a.elapsed_time(b)*1e3:.0f} us rounds={inf[6]:.0f}+{inf[7]:.0f}",
-          {names[i]: int(t[i]) // 1000 for i in (1, 2, 4, 5, 6)}, "us; NS iterations", int(t[7]))
+          {names[i]: int(t[i if i else 15]) // 1000 for i in (0, 1, 2, 3, 4, 5, 6)}, "us; NS iterations", int(t[7]))
     if len(t) > 8:
         sub = ["wait+stage", "score+argmax", "rescore", "sort", "accumulate"]
         print("   CTA0 clocks (M):", {sub[j]: round(int(t[8 + j]) / 1e6, 2) for j in range(5)},
-              "flagged rows (CTA0):", int(t[14]))
+              "flagged rows (CTA0):", int(t[14]), "changed rows (CTA0):", int(t[13]))
