@@ -34,6 +34,18 @@ namespace cg = cooperative_groups;
 namespace ancka {
 
 constexpr int kDiscThreads = 256;
+constexpr int kDiscWideMaxK = 192;
+// disc_wide_dev.cu: 64 < k <= 192
+size_t discretize_wide_workspace(int64_t n, int k);
+int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k, int max_iter,
+                    double tol, int32_t* labels_out, double* info, void* ws, size_t wsb,
+                    cudaStream_t st);
+// blocks wider than this take the wide path (ANCKA_DISC_WIDE_MIN, >= 8, lets
+// tests run it on narrower blocks)
+static int disc_wide_min() {
+  const char* e = getenv("ANCKA_DISC_WIDE_MIN");
+  return e ? std::max(8, atoi(e)) : 64;
+}
 
 struct DiscParams {
   const float* Q;
@@ -708,22 +720,40 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
 }
 
 // Exact (f64) second-best scores of every row of this CTA, before the rare
-// empty-cluster reseed picks the largest margin (engine.py:170-179).
+// empty-cluster reseed picks the largest margin (engine.py:170-179).  A
+// thread per row: q~_i in registers, R in shared memory (broadcast reads),
+// two score columns per pass; each score sums l = 0..k-1 in order, the same
+// f64 values as score_row_exact_warp.
 template <int KMAX>
-__device__ void exact_margins(const DiscParams& p, const double* sR64, double* wq) {
+__device__ void exact_margins(const DiscParams& p, const double* sR64) {
   const Rows R = my_rows(p.n);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int64_t i = R.r0 + warp; i < R.r1; i += kDiscThreads / 32) {
-    int lab;
-    float second;
-    score_row_exact_warp(p, sR64, i, wq + warp * 64, lab, second);
-    if (lane == 0) p.margin[i] = second;
+  const int k = p.k;
+  for (int64_t i = R.r0 + threadIdx.x; i < R.r1; i += blockDim.x) {
+    const float* src = p.Q + i * p.ldq + p.col0;
+    const double inv = p.qinv[i];
+    double q[KMAX];
+#pragma unroll
+    for (int l = 0; l < KMAX; ++l) q[l] = l < k ? (double)src[l] * inv : 0.0;
+    double best = -INFINITY, second = -INFINITY;
+    for (int j = 0; j < k; j += 2) {
+      const bool two = j + 1 < k;
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int l = 0; l < KMAX; ++l)
+        if (l < k) {
+          s0 = fma(q[l], sR64[l * k + j], s0);
+          if (two) s1 = fma(q[l], sR64[l * k + j + 1], s1);
+        }
+      if (s0 > best) { second = best; best = s0; } else if (s0 > second) second = s0;
+      if (two) {
+        if (s1 > best) { second = best; best = s1; } else if (s1 > second) second = s1;
+      }
+    }
+    p.margin[i] = (float)second;
   }
   __syncthreads();
 }
 
-// Every CTA: reduce (value, index, label) partials of buffer `buf`.
-// want_max: first max (larger value, then smaller index), else first min.
 __device__ void reduce_arg(const double* part, int nb, bool want_max, double& v_out,
                            long long& i_out, int& lab_out, double* sv, long long* si, int* sl) {
   double v = 0.0;
@@ -1093,6 +1123,8 @@ discretize_kernel(DiscParams p) {
   __shared__ double red[32];
   __shared__ int s_flag, s_zero;
   __shared__ double s_pcol[KMAX > 8 ? Win<KMAX>::KW : 1];
+  __shared__ long long s_mvi[64];    // reseed moves: row, old cluster, new cluster
+  __shared__ int s_mvo[64], s_mvc[64], s_nmv;
   const bool vec = (p.ldq % 4 == 0) && ((reinterpret_cast<uintptr_t>(p.Q) & 15) == 0);
 
   const bool cta0 = blockIdx.x == 0;
@@ -1261,8 +1293,10 @@ discretize_kernel(DiscParams p) {
       for (int c = 0; c < k; ++c) nempty += sizes[c] == 0;
       if (nempty > 0 && k >= 2) {
         if (KMAX > 8)
-          exact_margins<KMAX>(p, sR64, reinterpret_cast<double*>(tlab + 4 * kDiscThreads + 68 + 64));
+          exact_margins<KMAX>(p, sR64);
         // _reseed_empty_columns (engine.py:162-180): every CTA tracks sizes
+        if (threadIdx.x == 0) s_nmv = 0;
+        __syncthreads();
         for (int c = 0; c < k; ++c) {
           if (sizes[c] != 0) continue;
           double bestm = 0.0;
@@ -1288,13 +1322,42 @@ discretize_kernel(DiscParams p) {
             sizes[old] -= 1;
             sizes[c] += 1;
             if (idx >= rows.r0 && idx < rows.r1) p.labels[idx] = c;   // owner CTA
+            s_mvi[s_nmv] = idx;
+            s_mvo[s_nmv] = old;
+            s_mvc[s_nmv] = c;
+            ++s_nmv;
           }
           __syncthreads();
         }
-        if (KMAX > 8)
-          phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, false,
-                                    p.gfx + (size_t)(ri % 3) * (kk + k), nullptr);
-        else
+        if (KMAX > 8) {
+          // new totals = previous totals (carried slice by slice) + the moved
+          // rows' fixed-point deltas, applied by their owner CTAs: the exact
+          // integers a recount gives (phase_accumulate_tc's invariant)
+          unsigned long long* gdst = p.gfx + (size_t)(ri % 3) * (kk + k);
+          const unsigned long long* gprev = p.gfx + (size_t)((ri + 2) % 3) * (kk + k);
+          for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kk + k;
+               e += (int64_t)gridDim.x * blockDim.x) {
+            const unsigned long long v = __ldcg(gprev + e);
+            if (v) atomicAdd(gdst + e, v);
+          }
+          const int sh = ilogb(p.fx_scale), kq = disc_kq(k);
+          for (int m = 0; m < s_nmv; ++m) {
+            const long long idx = s_mvi[m];
+            if (idx < rows.r0 || idx >= rows.r1) continue;
+            const int old = s_mvo[m], c = s_mvc[m];
+            for (int j = threadIdx.x; j < k; j += blockDim.x) {
+              const long long fx = fx_round(p.qn[idx * kq + j], sh);
+              if (fx != 0) {
+                atomicAdd(gdst + c * k + j, (unsigned long long)fx);
+                atomicAdd(gdst + old * k + j, (unsigned long long)(-fx));
+              }
+            }
+            if (threadIdx.x == 0) {
+              atomicAdd(gdst + kk + c, 1ull);
+              atomicAdd(gdst + kk + old, ~0ull);
+            }
+          }
+        } else
           phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, false, nullptr,
                                  p.gfx + (size_t)(ri % 3) * (kk + k));
         grid.sync();
@@ -1433,6 +1496,7 @@ static int disc_grid_cap() { return 4 * kNumSMs; }
 
 extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t max_iter) {
   (void)max_iter;
+  if (k > disc_wide_min()) return discretize_wide_workspace(n, k);
   Carver cv(nullptr, 0);
   const int grid = disc_grid_cap();
   cv.take<int32_t>(n);              // labels_run0
@@ -1521,7 +1585,11 @@ static bool disc_split(int64_t n, int k) {
 extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64_t n, int32_t k,
                                 int32_t max_iter, double tol, int32_t* labels_out, double* info,
                                 void* workspace, size_t workspace_bytes, ancka_stream_t stream) {
-  ANCKA_REQUIRE(k >= 1 && k <= 64, ANCKA_ERR_UNSUPPORTED, "discretize: k=%d outside [1, 64]", k);
+  ANCKA_REQUIRE(k >= 1 && k <= kDiscWideMaxK, ANCKA_ERR_UNSUPPORTED, "discretize: k=%d outside [1, %d]",
+                k, kDiscWideMaxK);
+  if (k > disc_wide_min())   // wide blocks: device-driven rounds (disc_wide_dev.cu)
+    return discretize_wide(Q, ldq, col0, n, k, max_iter, tol, labels_out, info, workspace,
+                           workspace_bytes, as_stream(stream));
   ANCKA_REQUIRE(n >= 1 && max_iter >= 1, ANCKA_ERR_ARG, "discretize: empty input");
   Carver cv(workspace, workspace_bytes);
   DiscParams p{};

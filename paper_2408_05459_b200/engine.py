@@ -334,14 +334,15 @@ def orthogonal_step(op: WalkOperator, q_prev, rng: np.random.Generator):
 
 
 # --------------------------------------------------------- discretize -------
-#: blocks wider than this use the host-driven wide path (per-round n-sized
-#: work on the device, the k x k SVD on the host as np.linalg.svd); narrower
-#: ones the single cooperative kernel (discretize.cu), which is faster there
-WIDE_DISCRETIZE_K = 64
+#: blocks up to this width run on the device (discretize.cu for k <= 64,
+#: disc_wide_dev.cu's device-driven rounds above); wider ones the
+#: host-driven path (per-round n-sized work on the device, the k x k SVD on
+#: the host as np.linalg.svd)
+WIDE_DISCRETIZE_K = 192
 
 
 class _WideDiscretizer:
-    """_alternate_rounding / _prototype_rotation (engine.py:183-218) for k > 16.
+    """_alternate_rounding / _prototype_rotation (engine.py:183-218) for k > 192.
     Buffers are per (n, k) and reused across calls."""
 
     def __init__(self, n: int, k: int):

@@ -290,16 +290,23 @@ def test_real_valued_knn_certified(n, d, K, dup):
         assert fallback == 0
 
 
+@pytest.mark.parametrize("path", ["device", "host"])
 @pytest.mark.parametrize("n,k,noise", [(3000, 20, 0.25), (2500, 47, 0.2), (3000, 72, 0.1),
                                        (4000, 172, 0.05)])
-def test_wide_discretize_matches_oracle(n, k, noise, monkeypatch):
-    """Host-driven wide rounds (device scoring / fixed-point accumulation, host
-    SVD; the path for k > 64, forced here for every k) against the oracle
-    restatement of engine.py:221-263."""
+def test_wide_discretize_matches_oracle(n, k, noise, path, monkeypatch):
+    """Wide rounds against the oracle restatement of engine.py:221-263, forced
+    here for every k: "device" = disc_wide_dev.cu's device-driven rounds (the
+    path for 64 < k <= 192: tensor-core scoring with certified f64
+    rescoring, incremental fixed-point totals, device Newton-Schulz polar
+    factor, no host SVD); "host" = the host-driven rounds kept for k > 192
+    (device scoring / accumulation, host SVD)."""
     from sklearn.metrics import adjusted_rand_score as ari_
 
     from paper_2408_05459_b200 import engine
-    monkeypatch.setattr(engine, "WIDE_DISCRETIZE_K", 16)
+    if path == "host":
+        monkeypatch.setattr(engine, "WIDE_DISCRETIZE_K", 16)
+    else:
+        monkeypatch.setenv("ANCKA_DISC_WIDE_MIN", "8")
     rng = np.random.default_rng(k)
     lab = rng.integers(0, k, n)
     q = np.zeros((n, k))

@@ -208,15 +208,19 @@ def _starved_block(n, k, seed):
     return q.astype(np.float32).astype(np.float64)
 
 
-@pytest.mark.parametrize("k,wide", [(6, False), (20, False), (47, False), (20, True)])
+@pytest.mark.parametrize("k,wide", [(6, None), (20, None), (47, None), (20, "host"),
+                                    (20, "device"), (47, "device"), (80, "device")])
 def test_empty_column_reseed(k, wide, monkeypatch):
     """engine.py:162-180: the in-loop reseed moves the node with the largest
     second-best score (from clusters of size >= 2) into the empty column.
     Device labels and objective against the oracle; the reseeded cluster is
-    populated on both sides."""
+    populated on both sides.  wide: the host-driven wide rounds, or the
+    device-driven wide path (disc_wide_dev.cu) forced on narrower blocks."""
     from paper_2408_05459_b200 import engine
-    if wide:
+    if wide == "host":
         monkeypatch.setattr(engine, "WIDE_DISCRETIZE_K", 16)
+    elif wide == "device":
+        monkeypatch.setenv("ANCKA_DISC_WIDE_MIN", "8")
     q = _starved_block(1500, k, k)
     ref = oc.discretize(q)
     d = ancka.discretize(q)
