@@ -127,6 +127,10 @@ int ancka_knn_exact(const double* X, int64_t n, int64_t d, int64_t ldx, int32_t 
  * and the f64 scan recomputed.  Synchronises with the device. */
 int ancka_knn_fallback_rows(void* workspace, size_t workspace_bytes, int64_t n, int64_t d,
                             int32_t K, int64_t q_begin, int64_t q_end, int32_t* out_rows);
+/* Same count copied to device memory on `stream` (no synchronisation). */
+int ancka_knn_fallback_rows_async(void* workspace, size_t workspace_bytes, int64_t n, int64_t d,
+                                  int32_t K, int64_t q_begin, int64_t q_end, int32_t* out_rows_dev,
+                                  ancka_stream_t stream);
 
 /* Same, with X given as a CSR matrix (indptr n+1, sorted indices, f64 data):
  * the quantised tensor-core operand is built directly from the nonzeros (no

@@ -50,6 +50,8 @@ _SIGS = {
                                   c_void_p]),
     "ancka_knn_fallback_rows": (c_int32, [c_void_p, c_size_t, c_int64, c_int64, c_int32, c_int64,
                                           c_int64, c_void_p]),
+    "ancka_knn_fallback_rows_async": (c_int32, [c_void_p, c_size_t, c_int64, c_int64, c_int32,
+                                                c_int64, c_int64, c_void_p, c_void_p]),
     "ancka_knn_exact_csr": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,
                                       c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                       c_size_t, c_void_p]),

@@ -132,3 +132,11 @@ extern "C" int ancka_knn_fallback_rows(void* workspace, size_t workspace_bytes, 
   ANCKA_REQUIRE(out_rows != nullptr, ANCKA_ERR_ARG, "knn_fallback_rows: null output");
   return knn_real_flag_count(workspace, workspace_bytes, n, d, K, q_begin, q_end, out_rows);
 }
+
+extern "C" int ancka_knn_fallback_rows_async(void* workspace, size_t workspace_bytes, int64_t n,
+                                             int64_t d, int32_t K, int64_t q_begin, int64_t q_end,
+                                             int32_t* out_rows_dev, ancka_stream_t stream) {
+  ANCKA_REQUIRE(out_rows_dev != nullptr, ANCKA_ERR_ARG, "knn_fallback_rows_async: null output");
+  return knn_real_flag_count_async(workspace, workspace_bytes, n, d, K, q_begin, q_end, out_rows_dev,
+                                   as_stream(stream));
+}

@@ -21,6 +21,8 @@ int knn_real(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_t 
              KeyRange kr = {0, -1});
 int knn_real_flag_count(void* ws, size_t wsb, int64_t n, int64_t d, int K, int64_t q_begin,
                         int64_t q_end, int* out_host);
+int knn_real_flag_count_async(void* ws, size_t wsb, int64_t n, int64_t d, int K, int64_t q_begin,
+                              int64_t q_end, int* out_dev, cudaStream_t st);
 
 // tcgen05 integer-exact path (knn_tc.cu)
 size_t knn_tc_workspace(int64_t n, int64_t d, int K);

@@ -41,8 +41,14 @@ knn_simt_kernel(const double* __restrict__ xn, int64_t n, int64_t ldn, const dou
                 int K, int64_t q_begin, int64_t q_end, const int32_t* __restrict__ qlist,
                 const int* __restrict__ qcount, int32_t* __restrict__ ids,
                 double* __restrict__ scores, int64_t seg_len, double* __restrict__ part_v,
-                int32_t* __restrict__ part_i) {
+                int32_t* __restrict__ part_i, int64_t seg_cap) {
   extern __shared__ __align__(16) unsigned char smraw[];
+  // seg_cap > 0: the segmented launch, which runs only when *qcount <= seg_cap;
+  // seg_cap < 0: the single-segment launch, which runs only when *qcount > -seg_cap
+  if (seg_cap != 0 && qlist) {
+    const int64_t c = *qcount;
+    if (seg_cap > 0 ? c > seg_cap : c <= -seg_cap) return;
+  }
   double* As = reinterpret_cast<double*>(smraw);           // BM x BK
   double* Bs = As + BM * BK;                                // BN x BK
   double* S = Bs + BN * BK;                                 // BM x (BN+1)
@@ -144,31 +150,44 @@ int knn_simt(const double* xn, int64_t n, int64_t ldn, const double* norms, int 
   ANCKA_REQUIRE(smem <= 220 * 1024, ANCKA_ERR_UNSUPPORTED, "knn_simt: K=%d too large", K);
   ANCKA_CUDA(cudaFuncSetAttribute(knn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   knn_simt_kernel<<<(unsigned)ceil_div(q_end - q_begin, BM), 256, smem, st>>>(
-      xn, n, ldn, norms, K, q_begin, q_end, nullptr, nullptr, ids, scores, n, nullptr, nullptr);
+      xn, n, ldn, norms, K, q_begin, q_end, nullptr, nullptr, ids, scores, n, nullptr, nullptr, 0);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
 
-// merge the per-segment lists of each listed row: order (s desc, j asc)
-__global__ void knn_simt_merge_kernel(const double* __restrict__ part_v,
-                                      const int32_t* __restrict__ part_i, int64_t nrows, int nseg,
-                                      int K, const int32_t* __restrict__ qlist, int64_t q_begin,
-                                      int32_t* __restrict__ ids, double* __restrict__ scores) {
-  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrows;
+// Exact f64 rescan of the rows in qlist[0 .. *qcount) -- the count stays on
+// the device, so the host does not wait for the search: up to kSegCap rows
+// (the usual case: a handful) are spread over kSegs key segments so the
+// rescan uses the whole GPU, then merged; more rows take one launch that
+// strides over row chunks.  Each launch returns at once when the count
+// selects the other.
+constexpr int kSegs = 16;
+constexpr int64_t kSegCap = 4 * BM * kNumSMs / kSegs * 4;
+
+size_t knn_simt_list_workspace(int K) {
+  return (size_t)kSegCap * kSegs * K * (sizeof(double) + sizeof(int32_t)) + 1024;
+}
+
+__global__ void knn_simt_merge_gate(const double* part_v, const int32_t* part_i, const int* qcount,
+                                    int nseg, int K, const int32_t* qlist, int64_t q_begin,
+                                    int32_t* ids, double* scores) {
+  const int64_t c = *qcount;
+  if (c == 0 || c > kSegCap) return;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < c;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = (qlist[r] - q_begin) * K;
     const double* v = part_v + r * nseg * K;
     const int32_t* id = part_i + r * nseg * K;
-    int head[64];                                   // cursor per segment (nseg <= 64)
-    for (int s = 0; s < nseg; ++s) head[s] = 0;
+    int head[kSegs];
+    for (int s2 = 0; s2 < nseg; ++s2) head[s2] = 0;
     for (int t = 0; t < K; ++t) {
       int best = -1;
-      for (int s = 0; s < nseg; ++s) {
-        const int h = head[s];
-        if (h >= K || id[s * K + h] < 0) continue;
-        if (best < 0) { best = s; continue; }
-        const double a = v[s * K + h], b = v[best * K + head[best]];
-        if (a > b || (a == b && id[s * K + h] < id[best * K + head[best]])) best = s;
+      for (int s2 = 0; s2 < nseg; ++s2) {
+        const int h = head[s2];
+        if (h >= K || id[s2 * K + h] < 0) continue;
+        if (best < 0) { best = s2; continue; }
+        const double a = v[s2 * K + h], b = v[best * K + head[best]];
+        if (a > b || (a == b && id[s2 * K + h] < id[best * K + head[best]])) best = s2;
       }
       if (best < 0) { ids[o + t] = -1; scores[o + t] = 0.0; continue; }
       ids[o + t] = id[best * K + head[best]];
@@ -178,43 +197,30 @@ __global__ void knn_simt_merge_kernel(const double* __restrict__ part_v,
   }
 }
 
-size_t knn_simt_list_workspace(int K) {
-  return (size_t)BM * 2 * kNumSMs * K * (sizeof(double) + sizeof(int32_t)) + 1024;
-}
-
-// Exact f64 rescan of the rows in qlist[0 .. *qcount) (device count; read
-// back here, the KNN phase runs once per clustering).  Few rows are spread
-// over key segments so the rescan uses the whole GPU, then merged.
 int knn_simt_list(const double* xn, int64_t n, int64_t ldn, const double* norms, int K,
                   int64_t q_begin, const int32_t* qlist, const int* qcount, int32_t* ids,
                   double* scores, void* ws, size_t wsb, cudaStream_t st) {
   const size_t smem = knn_simt_smem(K);
   ANCKA_REQUIRE(smem <= 220 * 1024, ANCKA_ERR_UNSUPPORTED, "knn_simt: K=%d too large", K);
-  int cnt = 0;
-  ANCKA_CUDA(cudaMemcpyAsync(&cnt, qcount, sizeof(int), cudaMemcpyDeviceToHost, st));
-  ANCKA_CUDA(cudaStreamSynchronize(st));
-  if (cnt == 0) return ANCKA_OK;
   ANCKA_CUDA(cudaFuncSetAttribute(knn_simt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int64_t chunks = ceil_div((int64_t)cnt, BM);
-  int64_t nseg = std::min<int64_t>(std::min<int64_t>(2 * kNumSMs / chunks, 64), ceil_div(n, 4 * BN));
-  if (nseg <= 1) {
-    knn_simt_kernel<<<(unsigned)chunks, 256, smem, st>>>(xn, n, ldn, norms, K, q_begin, 0, qlist,
-                                                        qcount, ids, scores, n, nullptr, nullptr);
-    ANCKA_LAUNCHED();
-    return ANCKA_OK;
-  }
+  const int64_t nseg = std::max<int64_t>(1, std::min<int64_t>(kSegs, ceil_div(n, 4 * BN)));
   const int64_t seg_len = ceil_div(ceil_div(n, nseg), BN) * BN;
-  nseg = ceil_div(n, seg_len);
+  const int64_t nseg2 = ceil_div(n, seg_len);
   Carver cv(ws, wsb);
-  double* pv = cv.take<double>((size_t)chunks * BM * nseg * K);
-  int32_t* pi = cv.take<int32_t>((size_t)chunks * BM * nseg * K);
+  double* pv = cv.take<double>((size_t)kSegCap * nseg2 * K);
+  int32_t* pi = cv.take<int32_t>((size_t)kSegCap * nseg2 * K);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_simt_list: workspace too small");
-  dim3 grid((unsigned)chunks, (unsigned)nseg);
-  knn_simt_kernel<<<grid, 256, smem, st>>>(xn, n, ldn, norms, K, q_begin, 0, qlist, qcount, ids,
-                                           scores, seg_len, pv, pi);
+  // few rows: (row chunks x key segments), partial lists, merge
+  const unsigned gx = (unsigned)std::max<int64_t>(1, 2 * kNumSMs / nseg2);
+  knn_simt_kernel<<<dim3(gx, (unsigned)nseg2), 256, smem, st>>>(
+      xn, n, ldn, norms, K, q_begin, 0, qlist, qcount, ids, scores, seg_len, pv, pi, kSegCap);
   ANCKA_LAUNCHED();
-  knn_simt_merge_kernel<<<(unsigned)ceil_div(cnt, 128), 128, 0, st>>>(pv, pi, cnt, (int)nseg, K,
-                                                                      qlist, q_begin, ids, scores);
+  knn_simt_merge_gate<<<2 * kNumSMs, 128, 0, st>>>(pv, pi, qcount, (int)nseg2, K, qlist, q_begin,
+                                                   ids, scores);
+  ANCKA_LAUNCHED();
+  // many rows: one segment, CTAs stride over row chunks
+  knn_simt_kernel<<<2 * kNumSMs, 256, smem, st>>>(xn, n, ldn, norms, K, q_begin, 0, qlist, qcount,
+                                                  ids, scores, n, nullptr, nullptr, -kSegCap);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

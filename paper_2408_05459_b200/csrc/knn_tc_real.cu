@@ -1256,4 +1256,15 @@ int knn_real_flag_count(void* ws, size_t wsb, int64_t n, int64_t d, int K, int64
   return ANCKA_OK;
 }
 
+int knn_real_flag_count_async(void* ws, size_t wsb, int64_t n, int64_t d, int K, int64_t q_begin,
+                              int64_t q_end, int* out_dev, cudaStream_t st) {
+  const RealLayout R = real_layout(n, d, q_end - q_begin);
+  Carver cv(ws, wsb);
+  RealWs w;
+  carve_real(cv, R, n, K, w);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "knn_real: workspace too small");
+  ANCKA_CUDA(cudaMemcpyAsync(out_dev, w.nflag, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return ANCKA_OK;
+}
+
 }  // namespace ancka

@@ -233,18 +233,35 @@ def knn_search_exact_device(X, K: int, integer: int | None = None, rows=None):
     else:
         _lib.call("ancka_knn_exact", xd.data_ptr(), n, d, xd.stride(0), K, int(integer), q0, q1,
                   ids.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream())
-    if integer == 0:
-        out = np.zeros(1, dtype=np.int32)
-        _lib.call("ancka_knn_fallback_rows", ws.data_ptr(), ws.numel(), n, d, K, q0, q1,
-                  out.ctypes.data)
-        LAST_STATS["fallback_rows"] = int(out[0])
+    LAST_STATS.pop("fallback_rows", None)
+    if integer == 0:   # the count stays on the device until someone reads it
+        cnt = torch.zeros(1, dtype=torch.int32, device=dv)
+        _lib.call("ancka_knn_fallback_rows_async", ws.data_ptr(), ws.numel(), n, d, K, q0, q1,
+                  cnt.data_ptr(), _lib.stream())
+        LAST_STATS["fallback_rows"] = lambda: int(cnt.item())
     LAST_STATS["level"] = int(integer)
     return ids, scores
 
 
+class _LazyStats(dict):
+    """Values may be zero-argument callables, evaluated (and cached) on first
+    read: a device count read back only when asked for, so the search itself
+    never waits for the GPU."""
+
+    def __getitem__(self, key):
+        v = super().__getitem__(key)
+        if callable(v):
+            v = v()
+            super().__setitem__(key, v)
+        return v
+
+    def get(self, key, default=None):
+        return self[key] if key in self else default
+
+
 #: diagnostics of the last device search: path level and, for real-valued
 #: attributes, how many rows the tensor-core certificate sent to the f64 scan
-LAST_STATS: dict = {}
+LAST_STATS: dict = _LazyStats()
 
 
 def knn_search_exact(X, K: int, block_rows: int | None = None) -> NeighborLists:
