@@ -69,6 +69,8 @@ struct DiscParams {
   float* qn;            // k > 8: normalised block q~ (n x kq, f32, zero padded)
   double* qinv;         // k > 8: 1 / ||q_i|| (0 for all-zero rows)
   int dbuf;             // k > 8: double-buffered row tiles (when shared memory allows)
+  double* key;          // k > 8: per row, drift level below which its label is certified
+  int32_t* rid;         // k > 8: rows to score this round (per-CTA slices)
 };
 
 // Row i of Q[:, col0:col0+k], normalised in f64 (engine.py:226-232) and
@@ -424,7 +426,7 @@ constexpr float kCert = 2e-5f;
 // second-best value (all lanes return them).  qw: 64 doubles of scratch.
 __device__ __forceinline__ void score_row_exact_warp(const DiscParams& p, const double* sR64,
                                                      int64_t i, double* qw, int& lab,
-                                                     float& second_out) {
+                                                     float& second_out, double* margin_out = nullptr) {
   const int k = p.k, lane = threadIdx.x & 31;
   const float* src = p.Q + i * p.ldq + p.col0;
   const double inv = p.qinv[i];
@@ -455,6 +457,7 @@ __device__ __forceinline__ void score_row_exact_warp(const DiscParams& p, const 
   }
   lab = bi;
   second_out = (float)second;
+  if (margin_out) *margin_out = best - second;
   __syncwarp();
 }
 
@@ -493,7 +496,8 @@ __device__ __forceinline__ void sadd64(unsigned* cell, long long v) {
 template <int KMAX>
 __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const double* sR64,
                                     float* tile, int* tlab, long long* gacc, int* gcnt, bool score,
-                                    unsigned long long* gdst, const unsigned long long* gprev) {
+                                    unsigned long long* gdst, const unsigned long long* gprev,
+                                    double cdrift, bool keys_valid) {
   constexpr int NBM = disc_nbmax(KMAX);
   const int k = p.k, kk = k * k, kq = disc_kq(k), ks16 = kq / 16, nb8 = kq / 8;
   const int SWQ = kq + 4;
@@ -502,7 +506,8 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
   double* wq = reinterpret_cast<double*>(flagged + kDiscThreads);   // 8 warps x 64, 16-B aligned
   int* wcnt = flagged + kDiscThreads + 2 * 8 * 64;    // 8 warps x 64 labels (after wq)
   int* told = wcnt + 8 * 64;                          // kDiscThreads
-  __shared__ int s_nflag;
+  int* tids = told + kDiscThreads;                    // kDiscThreads: row of each tile slot
+  __shared__ int s_nflag, s_cnt;
   // Cluster sums in 64-bit fixed point, element by element (fx_round: the
   // same integer for the same q~ entry every round), so totals can be
   // carried: a round after the first adds only the rows whose label moved
@@ -530,10 +535,55 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const bool dbg = p.tdbg && blockIdx.x == 0 && threadIdx.x == 0;
+  const bool dbg0 = p.tdbg && blockIdx.x == 0 && threadIdx.x == 0;
   const Rows R = my_rows(p.n);
-  const int ntile = (int)ceil_div(R.r1 - R.r0, (int64_t)kDiscThreads);
+  // Rows to score.  A row scored when the cumulative rotation drift was C0
+  // with a certified margin m keeps its argmax while the drift since then
+  // stays below m / 2 (|q~ (R' - R)_j| <= max_j ||R'_j - R_j|| per score,
+  // unit rows): key = C0 + m / 2, and it is scored again only once the
+  // drift cdrift reaches its key.  Until the keys of this start exist, or
+  // when most rows are due, every row is scored.
+  int64_t nrows = R.r1 - R.r0;
+  bool list = false;
+  if (score && keys_valid) {
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    for (int64_t i0 = R.r0; i0 < R.r1; i0 += kDiscThreads) {
+      const int64_t i = i0 + threadIdx.x;
+      const bool due = i < R.r1 && p.key[i] <= cdrift;
+      const unsigned m = __ballot_sync(0xffffffffu, due);
+      int base = 0;
+      if (lane == 0 && m) base = atomicAdd(&s_cnt, __popc(m));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (due) p.rid[R.r0 + base + __popc(m & ((1u << lane) - 1u))] = (int32_t)i;
+    }
+    __syncthreads();
+    if (2 * (int64_t)s_cnt <= nrows) {
+      list = true;
+      nrows = s_cnt;
+    }
+    if (dbg0) p.tdbg[11] += (unsigned long long)(R.r1 - R.r0 - nrows);   // rows skipped
+  }
+  const int ntile = (int)ceil_div(nrows, (int64_t)kDiscThreads);
   const int c4 = kq / 4;
-  auto stage = [&](int ti) {   // 16-byte async copies of tile ti into buffer ti & 1
+  auto slot_id = [&](int ti) -> int64_t {    // row of this thread's slot in tile ti
+    const int64_t pos = (int64_t)ti * kDiscThreads + threadIdx.x;
+    if (pos >= nrows) return -1;
+    return list ? (int64_t)p.rid[R.r0 + pos] : R.r0 + pos;
+  };
+  auto stage = [&](int ti, int64_t my_id) {   // 16-byte async copies of tile ti into buffer ti & 1
+    if (list) {   // gathered rows: each thread copies its own slot's row
+      float* dst = tile + (ti & 1) * tile_floats + threadIdx.x * SWQ;
+      if (my_id >= 0)
+        for (int c = 0; c < c4; ++c)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                           (uint32_t)__cvta_generic_to_shared(dst + 4 * c)),
+                       "l"(p.qn + my_id * kq + 4 * c)
+                       : "memory");
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      return;
+    }
     const int64_t t0 = R.r0 + (int64_t)ti * kDiscThreads;
     const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
     float* dst = tile + (ti & 1) * tile_floats;
@@ -550,7 +600,6 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  const bool dbg = p.tdbg && blockIdx.x == 0 && threadIdx.x == 0;
   long long c_prev = dbg ? clock64() : 0;
 #define SUBSTAMP(slot)                                  \
   do {                                                  \
@@ -560,20 +609,22 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
       c_prev = _c;                                      \
     }                                                   \
   } while (0)
-  if (ntile > 0 && p.dbuf) stage(0);
-  // labels before this round, read one tile ahead (latency off the scoring path)
-  int old_next = (!full && threadIdx.x < R.r1 - R.r0) ? __ldcg(p.labels + R.r0 + threadIdx.x) : -1;
+  // slot rows and their labels before this round, read ahead (latency off
+  // the scoring path)
+  int64_t id_cur = slot_id(0), id_nxt = slot_id(1);
+  int old_cur = (!full && id_cur >= 0) ? __ldcg(p.labels + id_cur) : -1;
+  if (ntile > 0 && p.dbuf) stage(0, id_cur);
   for (int ti = 0; ti < ntile; ++ti) {
-    const int64_t t0 = R.r0 + (int64_t)ti * kDiscThreads;
-    const int tr = (int)lmin(kDiscThreads, R.r1 - t0);
-    told[threadIdx.x] = old_next;
-    old_next = (!full && t0 + kDiscThreads + threadIdx.x < R.r1)
-                   ? __ldcg(p.labels + t0 + kDiscThreads + threadIdx.x) : -1;
+    const int tr = (int)lmin(kDiscThreads, nrows - (int64_t)ti * kDiscThreads);
+    told[threadIdx.x] = old_cur;
+    tids[threadIdx.x] = (int)id_cur;
+    const int64_t id_nn = slot_id(ti + 2);
+    const int old_nxt = (!full && id_nxt >= 0) ? __ldcg(p.labels + id_nxt) : -1;
     if (!p.dbuf) {
-      stage(ti);
+      stage(ti, id_cur);
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     } else if (ti + 1 < ntile) {
-      stage(ti + 1);                       // overlaps this tile's work
+      stage(ti + 1, id_nxt);               // overlaps this tile's work
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -644,8 +695,10 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
             }
             const int row = warp * 32 + mb * 16 + g + h * 8;
             if (t == 0 && row < tr) {
+              const int64_t id = tids[row];
               if (!(best - second > kCert)) flagged[atomicAdd(&s_nflag, 1)] = row;
-              p.labels[t0 + row] = bi;
+              else p.key[id] = cdrift + 0.5 * ((double)best - (double)second - (double)kCert);
+              p.labels[id] = bi;
               tlab[row] = bi;
             }
           }
@@ -656,16 +709,19 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
       // exact f64 rescoring (a warp per row) of the rows the margin does not certify
       for (int f = warp; f < s_nflag; f += kDiscThreads / 32) {
         const int row = flagged[f];
+        const int64_t id = tids[row];
         int lab;
         float second;
-        score_row_exact_warp(p, sR64, t0 + row, wq + warp * 64, lab, second);
+        double marg;
+        score_row_exact_warp(p, sR64, id, wq + warp * 64, lab, second, &marg);
         if (lane == 0) {
-          p.labels[t0 + row] = lab;
+          p.labels[id] = lab;
+          p.key[id] = cdrift + 0.5 * marg;
           tlab[row] = lab;
         }
       }
     } else {
-      for (int r = threadIdx.x; r < tr; r += blockDim.x) tlab[r] = p.labels[t0 + r];
+      for (int r = threadIdx.x; r < tr; r += blockDim.x) tlab[r] = p.labels[tids[r]];
     }
     __syncthreads();
     SUBSTAMP(10);
@@ -706,6 +762,9 @@ __device__ void phase_accumulate_tc(const DiscParams& p, const uint4* sRf, const
     }
     __syncthreads();
     SUBSTAMP(12);
+    id_cur = id_nxt;
+    old_cur = old_nxt;
+    id_nxt = id_nn;
   }
 #undef SUBSTAMP
   // CTA deltas -> global totals (integer atomics: order free)
@@ -1262,6 +1321,7 @@ discretize_kernel(DiscParams p) {
 
     // ---------------------------------------------------------- rounds
     double obj_prev = 0.0;
+    double cdrift = 0.0;         // cumulative rotation drift of this start (row keys)
     bool conv = false;
     int rounds = 0;
     for (int it = 0; it < p.max_iter; ++it) {
@@ -1270,7 +1330,8 @@ discretize_kernel(DiscParams p) {
         phase_accumulate_tc<KMAX>(p, sRf, sR64, tile, tlab, gacc, gcnt, true,
                                   p.gfx + (size_t)(ri % 3) * (kk + k),
                                   (run == p.run_lo && it == 0) ? nullptr
-                                                               : p.gfx + (size_t)((ri + 2) % 3) * (kk + k));
+                                                               : p.gfx + (size_t)((ri + 2) % 3) * (kk + k),
+                                  cdrift, it > 0);
       else
         phase_accumulate<KMAX>(p, sR, tile, tlab, acc, cnt, true,
                                (run == 0 && it == 0) ? &s_zero : nullptr,
@@ -1321,7 +1382,10 @@ discretize_kernel(DiscParams p) {
           if (threadIdx.x == 0) {
             sizes[old] -= 1;
             sizes[c] += 1;
-            if (idx >= rows.r0 && idx < rows.r1) p.labels[idx] = c;   // owner CTA
+            if (idx >= rows.r0 && idx < rows.r1) {                  // owner CTA
+              p.labels[idx] = c;
+              if (KMAX > 8) p.key[idx] = -INFINITY;                  // score it next round
+            }
             s_mvi[s_nmv] = idx;
             s_mvo[s_nmv] = old;
             s_mvc[s_nmv] = c;
@@ -1394,8 +1458,29 @@ discretize_kernel(DiscParams p) {
         break;
       }
       // next rotation R = V U^T (engine.py:205)
-      if (KMAX > 8)
+      if (KMAX > 8) {
+        // drift of the rotation: max_j ||X_j - R_j|| bounds every row's score
+        // change (row keys, phase_accumulate_tc)
+        double cm = 0.0;
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+          double s2 = 0.0;
+          for (int l = 0; l < k; ++l) {
+            const double d = X[l * k + j] - sR64[l * k + j];
+            s2 += d * d;
+          }
+          cm = fmax(cm, sqrt(s2));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+        __syncthreads();
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cm;
+        __syncthreads();
+        double dmax = 0.0;
+        for (int w = 0; w < kDiscThreads / 32; ++w) dmax = fmax(dmax, red[w]);
+        cdrift += dmax * (1.0 + 1e-6) + 1e-14;    // rows of norm 1 + O(2^-24), f64 rounding
+        __syncthreads();
         store_rot_frag(smraw, k, [&](int l, int j) { return X[l * k + j]; });
+      }
       else
         for (int e = threadIdx.x; e < k * kp; e += blockDim.x)
           sR[e] = e % kp < k ? (float)X[(e / kp) * k + e % kp] : 0.f;
@@ -1472,7 +1557,7 @@ static size_t disc_smem(int k, int G, int off, int dbuf = 1) {
   const size_t fixed = align_dev(disc_rot_bytes(k, off)) + align_dev(kk * 8);
   const size_t a = k > 8 ? align_dev(disc_tc_acc_bytes(k, G)) + align_dev((size_t)G * k * 4) +
                                align_dev(disc_tc_tile_bytes(k, off, dbuf)) +
-                               (5 * kDiscThreads + 68 + 64) * 4 + 8 * 64 * 8 + 8 * 64 * 4
+                               (6 * kDiscThreads + 68 + 64) * 4 + 8 * 64 * 8 + 8 * 64 * 4
                          : align_dev((size_t)G * kk * 8) + align_dev(disc_tile_bytes(k, off)) +
                                (kDiscThreads + (size_t)G * k) * 4;
   const size_t b = 4 * kk * 8 + (size_t)k * 8;
@@ -1505,6 +1590,8 @@ extern "C" size_t ancka_discretize_workspace_size(int64_t n, int32_t k, int32_t 
   if (k > 8) {
     cv.take<float>((size_t)n * disc_kq(k));   // qn
     cv.take<double>(n);                       // qinv
+    cv.take<double>(n);                       // key
+    cv.take<int32_t>(n);                      // rid
   }
   for (int r = 0; r < 2; ++r) {     // per start (split launches run concurrently)
     cv.take<float>(n);              // margin
@@ -1602,6 +1689,8 @@ extern "C" int ancka_discretize(const float* Q, int64_t ldq, int64_t col0, int64
   if (k > 8) {
     p.qn = cv.take<float>((size_t)n * disc_kq(k));
     p.qinv = cv.take<double>(n);
+    p.key = cv.take<double>(n);
+    p.rid = cv.take<int32_t>(n);
   }
   DiscParams pr[2];
   for (int r = 0; r < 2; ++r) {

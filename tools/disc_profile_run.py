@@ -26,6 +26,6 @@ ns = {"round_gap": 15, "sync_after_A": 1, "reduce": 2, "reseed+scale": 3, "polar
       "proto_iter": 5, "phaseA": 6}
 print(f"calls {P['calls']} rounds {P['rounds']} NS iterations {P[7]}")
 print("ms:", {n: round(P[i] / 1e6, 1) for n, i in ns.items()})
-sub = ["wait+stage", "score+argmax", "rescore", "-", "accumulate"]
+sub = ["wait+stage", "score+argmax", "rescore", "skipped rows", "accumulate"]
 print("CTA0 Mclk:", {sub[j]: round(P[8 + j] / 1e6, 1) for j in range(5)},
       "flagged", P[14], "changed", P[13])

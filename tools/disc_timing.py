@@ -46,6 +46,6 @@ for rep in range(3):
     print(f"total {a.elapsed_time(b)*1e3:.0f} us rounds={inf[6]:.0f}+{inf[7]:.0f}",
           {names[i]: int(t[i if i else 15]) // 1000 for i in (0, 1, 2, 3, 4, 5, 6)}, "us; NS iterations", int(t[7]))
     if len(t) > 8:
-        sub = ["wait+stage", "score+argmax", "rescore", "sort", "accumulate"]
+        sub = ["wait+stage", "score+argmax", "rescore", "skipped rows (CTA0)", "accumulate"]
         print("   CTA0 clocks (M):", {sub[j]: round(int(t[8 + j]) / 1e6, 2) for j in range(5)},
               "flagged rows (CTA0):", int(t[14]), "changed rows (CTA0):", int(t[13]))
