@@ -49,8 +49,11 @@ struct Ctl {
   int flags[3];     // Newton-Schulz "moved" flags (rotating)
   int zero_rows;
   int ns_total;
+  int nlist;        // rows due for scoring this round (-1: all rows)
+  int pad_;
   double obj_prev;
   double obj_last[2];
+  double cdrift;    // cumulative rotation drift of the current start (row keys)
 };
 
 struct Params {
@@ -73,6 +76,8 @@ struct Params {
   double* part;                // per-CTA partials
   double* margin;              // n, exact second-best scores (reseed)
   double* proto_acc;           // n
+  double* key;                 // n: drift level below which the row's label is certified
+  int32_t* rid;                // n: rows due for scoring this round
   Ctl* ctl;
   double* info;
 };
@@ -147,7 +152,8 @@ __device__ __forceinline__ uint4 frag_entry(int e, int k, int nb8, Get get) {
 
 // f64 scores of row i against R64 (lanes over columns j = lane + 32 m, l
 // summed in ascending order), first-max argmax and the second-best score
-__device__ void exact_row(const Params& p, int64_t i, int& lab, double& second_out) {
+__device__ void exact_row(const Params& p, int64_t i, int& lab, double& second_out,
+                          double* margin_out = nullptr) {
   const int k = p.k, lane = threadIdx.x & 31;
   const float* src = p.Q + i * p.ldq + p.col0;
   const double inv = p.qinv[i];
@@ -194,6 +200,7 @@ __device__ void exact_row(const Params& p, int64_t i, int& lab, double& second_o
   }
   lab = bi;
   second_out = second;
+  if (margin_out) *margin_out = best - second;
 }
 
 // ----------------------------------------------------------- normalise ---
@@ -231,6 +238,30 @@ __global__ void dw_identity(Params p) {
 }
 
 // ------------------------------------------------------------- scoring ---
+// Rows due this round.  A row scored at cumulative rotation drift C0 with a
+// certified margin m keeps its argmax while the drift since then stays
+// below m / 2 (each score moves by at most max_j ||R'_j - R_j|| for a unit
+// row): key = C0 + m / 2.  The first round of a start scores every row, and
+// so does a round where most rows are due.
+__global__ void dw_list(Params p, int run) {
+  if (ld_vol(&p.ctl->done[run])) return;
+  if (ld_vol(&p.ctl->it) == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl->nlist = -1;
+    return;
+  }
+  const double c = *reinterpret_cast<volatile double*>(&p.ctl->cdrift);
+  const int lane = threadIdx.x & 31;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < p.n; i0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    const bool due = i < p.n && p.key[i] <= c;
+    const unsigned m = __ballot_sync(0xffffffffu, due);
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(&p.ctl->nlist, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (due) p.rid[base + __popc(m & ((1u << lane) - 1u))] = (int32_t)i;
+  }
+}
+
 template <int NBMAX>
 __global__ void __launch_bounds__(kT, 1) dw_score(Params p, int run, int first) {
   if (ld_vol(&p.ctl->done[run])) return;
@@ -239,9 +270,18 @@ __global__ void __launch_bounds__(kT, 1) dw_score(Params p, int run, int first) 
   for (int e = threadIdx.x; e < ks16 * nb8 * 32; e += kT) sRf[e] = p.Rfrag[e];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int64_t n = p.n, nmb = ceil_div(n, 16);
+  const int64_t n = p.n;
+  const int nl = ld_vol(&p.ctl->nlist);
+  const bool list = nl >= 0 && 2 * (int64_t)nl <= n;
+  const int64_t nrows = list ? nl : n;
+  const int64_t nmb = ceil_div(nrows, 16);
+  const double cdrift = *reinterpret_cast<volatile double*>(&p.ctl->cdrift);
   for (int64_t mb = (int64_t)blockIdx.x * (kT / 32) + warp; mb < nmb; mb += (int64_t)gridDim.x * (kT / 32)) {
-    const int64_t r0 = mb * 16 + g, r1 = r0 + 8;
+    // the warp's 16 rows: slots mb * 16 + g and + 8 (rows of the list, or
+    // consecutive rows); slots past the end read a valid row, write nothing
+    const int64_t s0 = mb * 16 + g, s1 = s0 + 8;
+    const int64_t r0 = s0 < nrows ? (list ? (int64_t)p.rid[s0] : s0) : n;
+    const int64_t r1 = s1 < nrows ? (list ? (int64_t)p.rid[s1] : s1) : n;
     const int64_t c0 = r0 < n ? r0 : n - 1, c1 = r1 < n ? r1 : n - 1;   // clamped reads
     int old0 = -1, old1 = -1;
     if (!first && t == 0) {
@@ -310,6 +350,8 @@ __global__ void __launch_bounds__(kT, 1) dw_score(Params p, int run, int first) 
       }
       lab[h] = bi;
       flag[h] = !(best - second > p.cert);
+      const int64_t rr = h == 0 ? r0 : r1;
+      if (t == 0 && !flag[h] && rr < n) p.key[rr] = cdrift + 0.5 * ((double)best - (double)second - (double)p.cert);
     }
     // rows the margin does not certify: exact f64 rescoring by the warp
     const unsigned fm = __ballot_sync(0xffffffffu, t == 0 && ((flag[0] && r0 < n) || (flag[1] && r1 < n)));
@@ -321,12 +363,15 @@ __global__ void __launch_bounds__(kT, 1) dw_score(Params p, int run, int first) 
       const int f1 = __shfl_sync(0xffffffffu, (int)flag[1], src);
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int64_t row = mb * 16 + (src >> 2) + 8 * h;
+        const int64_t row = __shfl_sync(0xffffffffu, h == 0 ? r0 : r1, src);
         if (!(h == 0 ? f0 : f1) || row >= n) continue;
         int el;
-        double sec;
-        exact_row(p, row, el, sec);
-        if (lane == src) lab[h] = el;
+        double sec, marg;
+        exact_row(p, row, el, sec, &marg);
+        if (lane == src) {
+          lab[h] = el;
+          p.key[row] = cdrift + 0.5 * marg;
+        }
       }
     }
     // labels, moved rows
@@ -428,6 +473,18 @@ __global__ void __launch_bounds__(kT) dw_delta(Params p, int run, int first) {
       atomicAdd(dst + (size_t)k * k + o, ~0ull);
     }
   }
+}
+
+__device__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double r = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) r = fmax(r, red[w]);
+  __syncthreads();
+  return r;
 }
 
 // --------------------------------------------------- block argmax helpers ---
@@ -536,6 +593,7 @@ __global__ void __launch_bounds__(kT, 1) dw_reseed(Params p, int run) {
         atomicAdd(tot + (size_t)k * k + c, 1ull);
         atomicAdd(tot + (size_t)k * k + old, ~0ull);
         p.labels[idx] = c;
+        p.key[idx] = -INFINITY;                       // scored again next round
         p.part[4 * gridDim.x] = (double)old;          // the other CTAs learn the donor
       }
     }
@@ -687,6 +745,28 @@ __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
   const double obj = (double)p.n - 2.0 * ssum;
   const bool conv = it >= 1 && fabs(obj - obj_prev) < p.tol;
   const bool done = conv || it + 1 == p.max_iter;
+  // rotation drift max_j ||X_j - R_j|| (row keys): per-CTA column partials
+  // of this tile, summed over row tiles in a fixed order
+  double dmax = 0.0;
+  if (!done) {
+    double* pd = ptr + G;                       // tpr x kq
+    const double dv = (a < k && b < k) ? xab - p.R64[(size_t)a * k + b] : 0.0;
+    sA[ty][tx] = dv * dv;
+    __syncthreads();
+    if (threadIdx.x < 16) {
+      double cs = 0.0;
+      for (int u = 0; u < 16; ++u) cs += sA[u][threadIdx.x];
+      pd[(size_t)by * kq + 16 * bx + threadIdx.x] = cs;
+    }
+    __syncthreads();
+    grid.sync();
+    for (int c2 = threadIdx.x; c2 < k; c2 += kT) {
+      double cs = 0.0;
+      for (int t2 = 0; t2 < tpr; ++t2) cs += __ldcg(pd + (size_t)t2 * kq + c2);
+      dmax = fmax(dmax, sqrt(cs));
+    }
+    dmax = block_max(dmax, red);
+  }
   if (!done) {   // next rotation R = V U^T (engine.py:205): this CTA's tile of X
     sA[ty][tx] = xab;
     __syncthreads();
@@ -704,6 +784,8 @@ __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
     Ctl* c = p.ctl;
     c->obj_prev = obj;
     c->obj_last[run] = obj;
+    if (!done) c->cdrift += dmax * (1.0 + 1e-6) + 1e-14;   // rows of norm 1 + O(2^-24), f64 rounding
+    c->nlist = 0;
     c->it = it + 1;
     c->gr = gr + 1;
     c->nchg = 0;
@@ -814,9 +896,11 @@ void carve_wide(Carver& cv, int64_t n, int k, dw::Params& p, int32_t** labels_ru
   p.R64 = cv.take<double>((size_t)k * k);
   p.Rfrag = cv.take<uint4>((size_t)(kq / 16) * (kq / 8) * 32);
   p.W = cv.take<double>((size_t)5 * kq * kq);
-  p.part = cv.take<double>((size_t)4 * 1024 + 16 + 2 * (size_t)kq * (kq / 16));
+  p.part = cv.take<double>((size_t)4 * 1024 + 16 + 3 * (size_t)kq * (kq / 16));
   p.margin = cv.take<double>(n);
   p.proto_acc = cv.take<double>(n);
+  p.key = cv.take<double>(n);
+  p.rid = cv.take<int32_t>(n);
   p.ctl = cv.take<dw::Ctl>(1);
 }
 
@@ -837,6 +921,8 @@ int coop(const void* fn, int grid, size_t smem, cudaStream_t st, void** args) {
 }
 
 int launch_round(dw::Params& p, int run, int first, cudaStream_t st, int coop_grid) {
+  dw::dw_list<<<2 * kNumSMs, dw::kT, 0, st>>>(p, run);
+  ANCKA_LAUNCHED();
   ANCKA_TRY(p.nb8 <= 16 ? launch_score<16>(p, run, first, st) : launch_score<24>(p, run, first, st));
   const int ne = p.k * p.k + p.k;
   dw::dw_carry<<<(int)std::min<int64_t>(ceil_div(ne, dw::kT), 2 * kNumSMs), dw::kT, 0, st>>>(p, run, first);
@@ -922,6 +1008,7 @@ int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k,
       // the prototype start continues from run 0's labels and totals
       ANCKA_CUDA(cudaMemcpyAsync(labels_out, labels_run0, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
       ANCKA_CUDA(cudaMemsetAsync(&p.ctl->it, 0, sizeof(int), st));
+      ANCKA_CUDA(cudaMemsetAsync(&p.ctl->cdrift, 0, sizeof(double), st));
       void* args[] = {&p};
       ANCKA_TRY(coop((const void*)dw::dw_proto, coop_grid, 0, st, args));
     }
