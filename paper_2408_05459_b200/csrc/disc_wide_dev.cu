@@ -489,12 +489,13 @@ __device__ double block_max(double v, double* red) {
 
 // --------------------------------------------------- block argmax helpers ---
 // (value, index) arg-best of a CTA, ties to the smaller index; want_max or min
+template <int NT = kT>
 __device__ void block_best(double v, long long id, bool want_max, double* sv, long long* si,
                            double& v_out, long long& i_out) {
   sv[threadIdx.x] = v;
   si[threadIdx.x] = id;
   __syncthreads();
-  for (int s = kT / 2; s > 0; s >>= 1) {
+  for (int s = NT / 2; s > 0; s >>= 1) {
     if (threadIdx.x < s) {
       const double v2 = sv[threadIdx.x + s], v1 = sv[threadIdx.x];
       const long long i2 = si[threadIdx.x + s], i1 = si[threadIdx.x];
@@ -508,17 +509,18 @@ __device__ void block_best(double v, long long id, bool want_max, double* sv, lo
   __syncthreads();
 }
 // global arg-best from per-CTA (value, index) partials, same order in every CTA
+template <int NT = kT>
 __device__ void grid_best(const double* part, int nb, bool want_max, double* sv, long long* si,
                           double& v_out, long long& i_out) {
   double v = 0.0;
   long long id = -1;
-  for (int b = threadIdx.x; b < nb; b += kT) {
+  for (int b = threadIdx.x; b < nb; b += NT) {
     const double v2 = __ldcg(part + 2 * b);
     const long long i2 = (long long)__ldcg(part + 2 * b + 1);
     const bool take = i2 >= 0 && (id < 0 || (want_max ? v2 > v : v2 < v) || (v2 == v && i2 < id));
     if (take) { v = v2; id = i2; }
   }
-  block_best(v, id, want_max, sv, si, v_out, i_out);
+  block_best<NT>(v, id, want_max, sv, si, v_out, i_out);
 }
 
 // --------------------------------------------------------------- reseed ---
@@ -808,56 +810,83 @@ __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
 // _prototype_rotation (engine.py:209-218): R[:, 0] = q~_0; pass j adds
 // |q~ . R[:, j-1]| to every row's running sum and R[:, j] = q~ of the first
 // row with the smallest sum.  q~ in f64 (Q / ||Q||).
-__global__ void __launch_bounds__(kT, 1) dw_proto(Params p) {
+constexpr int kTP = 512;          // prototype kernel: more rows in flight per SM
+__global__ void __launch_bounds__(kTP, 1) dw_proto(Params p) {
   cg::grid_group grid = cg::this_grid();
   const int k = p.k;
   __shared__ double r[kMaxK];
-  __shared__ double sv[kT];
-  __shared__ long long si[kT];
+  __shared__ double sv[kTP];
+  __shared__ long long si[kTP];
   const int64_t rpb = ceil_div(p.n, gridDim.x);
   const int64_t a0 = (int64_t)blockIdx.x * rpb, a1 = lmin(p.n, a0 + rpb);
   auto load_row = [&](int64_t i) {
     const float* src = p.Q + i * p.ldq + p.col0;
     const double inv = p.qinv[i];
-    for (int l = threadIdx.x; l < k; l += kT) r[l] = (double)src[l] * inv;
+    for (int l = threadIdx.x; l < k; l += kTP) r[l] = (double)src[l] * inv;
   };
   load_row(0);
-  for (int64_t i = a0 + threadIdx.x; i < a1; i += kT) p.proto_acc[i] = 0.0;
+  for (int64_t i = a0 + threadIdx.x; i < a1; i += kTP) p.proto_acc[i] = 0.0;
   __syncthreads();
   if (blockIdx.x == 0)
-    for (int l = threadIdx.x; l < k; l += kT) p.R64[(size_t)l * k] = r[l];
+    for (int l = threadIdx.x; l < k; l += kTP) p.R64[(size_t)l * k] = r[l];
   int buf = 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int j = 1; j < k; ++j) {
+    // a warp per 32 consecutive rows: each row's dot product with lanes over
+    // columns (coalesced reads, fixed shuffle-tree sum), lane r keeps row r's;
+    // the running sums and 1/||q|| of the 32 rows load coalesced up front
     double best = 0.0;
     long long bi = -1;
-    for (int64_t i = a0 + threadIdx.x; i < a1; i += kT) {
-      const float* src = p.Q + i * p.ldq + p.col0;
-      const double inv = p.qinv[i];
-      double d = 0.0;
-      for (int l = 0; l < k; ++l) d += ((double)src[l] * inv) * r[l];
-      const double acc = p.proto_acc[i] + fabs(d);
-      p.proto_acc[i] = acc;
-      if (bi < 0 || acc < best) { best = acc; bi = i; }
+    for (int64_t base = a0 + (int64_t)warp * 32; base < a1; base += (int64_t)(kTP / 32) * 32) {
+      const int64_t me = base + lane;
+      const bool ok = me < a1;
+      const double acc0 = ok ? p.proto_acc[me] : 0.0;
+      const double inv = ok ? p.qinv[me] : 0.0;
+      const int nr = (int)lmin(32, a1 - base);
+      double mine = 0.0;
+      for (int rr = 0; rr < nr; rr += 4) {      // four rows in flight
+        double d[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float* src = p.Q + (base + min(rr + u, nr - 1)) * p.ldq + p.col0;
+          d[u] = 0.0;
+#pragma unroll
+          for (int m = 0; m < kMaxK / 32; ++m) {
+            const int l = lane + 32 * m;
+            if (l < k) d[u] = fma((double)src[l], r[l], d[u]);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          d[u] = warp_sum(d[u]);
+          if (lane == rr + u) mine = d[u];
+        }
+      }
+      if (ok) {
+        const double av = acc0 + fabs(mine * inv);
+        p.proto_acc[me] = av;
+        if (bi < 0 || av < best) { best = av; bi = me; }
+      }
     }
     double v;
     long long idx;
-    block_best(best, bi, false, sv, si, v, idx);
+    block_best<kTP>(best, bi, false, sv, si, v, idx);
     double* part = p.part + (size_t)buf * gridDim.x * 2;
     if (threadIdx.x == 0) {
       part[2 * blockIdx.x] = v;
       part[2 * blockIdx.x + 1] = (double)idx;
     }
     grid.sync();
-    grid_best(part, gridDim.x, false, sv, si, v, idx);
+    grid_best<kTP>(part, gridDim.x, false, sv, si, v, idx);
     buf ^= 1;
     load_row(idx < 0 ? 0 : idx);
     __syncthreads();
     if (blockIdx.x == 0)
-      for (int l = threadIdx.x; l < k; l += kT) p.R64[(size_t)l * k + j] = r[l];
+      for (int l = threadIdx.x; l < k; l += kTP) p.R64[(size_t)l * k + j] = r[l];
   }
   grid.sync();
   const int ne = (p.kq / 16) * p.nb8 * 32;
-  for (int e = blockIdx.x * kT + threadIdx.x; e < ne; e += gridDim.x * kT)
+  for (int e = blockIdx.x * kTP + threadIdx.x; e < ne; e += gridDim.x * kTP)
     p.Rfrag[e] = frag_entry(e, k, p.nb8, [&](int l, int jj) { return __ldcg(p.R64 + (size_t)l * k + jj); });
 }
 
@@ -914,9 +943,9 @@ int launch_score(const dw::Params& p, int run, int first, cudaStream_t st) {
   return ANCKA_OK;
 }
 
-int coop(const void* fn, int grid, size_t smem, cudaStream_t st, void** args) {
+int coop(const void* fn, int grid, size_t smem, cudaStream_t st, void** args, int threads = dw::kT) {
   note_launch();
-  ANCKA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(dw::kT), args, smem, st));
+  ANCKA_CUDA(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, st));
   return ANCKA_OK;
 }
 
@@ -993,7 +1022,7 @@ int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k,
     int per_sm = 0;
     ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dw::dw_reseed, dw::kT, 0));
     int per_sm2 = 0;
-    ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, dw::dw_proto, dw::kT, 0));
+    ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm2, dw::dw_proto, dw::kTP, 0));
     coop_grid = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)std::min(per_sm, per_sm2) * kNumSMs,
                                                               (int64_t)kNumSMs, ceil_div(n, dw::kT)}));
   }
@@ -1010,7 +1039,7 @@ int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k,
       ANCKA_CUDA(cudaMemsetAsync(&p.ctl->it, 0, sizeof(int), st));
       ANCKA_CUDA(cudaMemsetAsync(&p.ctl->cdrift, 0, sizeof(double), st));
       void* args[] = {&p};
-      ANCKA_TRY(coop((const void*)dw::dw_proto, coop_grid, 0, st, args));
+      ANCKA_TRY(coop((const void*)dw::dw_proto, coop_grid, 0, st, args, dw::kTP));
     }
     for (int it0 = 0; it0 < max_iter; it0 += dw::kRoundsPerSync) {
       const int it1 = std::min(max_iter, it0 + dw::kRoundsPerSync);
