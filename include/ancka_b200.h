@@ -313,7 +313,7 @@ int ancka_qr_f64(double* Z, int64_t n, int64_t ld, int32_t c, double* rdiag,
  * and prototype start), up to max_iter rounds each, |d obj| < tol.
  * 1 <= k <= 192: k <= 64 one cooperative kernel; 64 < k <= 192 device-driven
  * rounds (the call synchronises the stream once every 8 rounds to read the
- * convergence flag; no host arithmetic). */
+ * convergence flag; no host arithmetic).
  * labels_out: int32[n]; info (device f64[8 + 2*max_iter + 2*k*k]):
  *   [0] final objective  [1] rounds  [2] converged  [3] winning run (0 id, 1 proto)
  *   [4] empty clusters left (repair impossible -> NetworkError)
