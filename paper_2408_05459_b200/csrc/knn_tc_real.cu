@@ -198,6 +198,8 @@ struct RealParams {
   uint32_t* row_bound;  // nq: shared pruning floor (order-mapped f32)
   int64_t q_begin, q_end;
   int debug;
+  unsigned long long* stats;   // debug 4: [chunks passing the max test, candidates buffered,
+                               //           top-K inserts, pool adds]
 };
 }  // namespace
 
@@ -319,12 +321,16 @@ __device__ __forceinline__ void real_epilogue(uint64_t* tfull, uint64_t* tempty,
 //   (lanes hit candidates at independent times); batched, the lanes insert
 //   together.  The threshold is refreshed at each drain, so between drains it
 //   is a (valid, lower) stale bound.
-template <class SL, bool PAIR = false>
+template <class SL, bool PAIR = false, int TN = tc::BN>
 __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t* tempty,
                                                       uint32_t tmem, float* stash_base,
                                                       const RealParams& p, int64_t q0, int seg,
                                                       int kt0, int ntiles) {
   using namespace tc;
+  // TN key columns per accumulator tile, NACC tiles in TMEM (512 columns);
+  // ntiles counts TN-column tiles from key tile kt0 (in BN units)
+  constexpr int NACC = TMEM_COLS / TN;
+  constexpr int ECOLS = TN / (EPI_WARPS / 4);     // columns per epilogue warp and tile
   constexpr int PB = 8, DRAIN = 4;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int ew = warp - 2;
@@ -373,11 +379,18 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   float* stash = stash_base + (threadIdx.x - 64) * 33;
   // drain(upto): insert the buffered candidates; upto bounds the loop (the
   // warp-wide maximum of pc when all lanes drain together, PB otherwise)
+  unsigned long long st_chunks = 0, st_cand = 0, st_top = 0, st_pool = 0;
   auto drain = [&](int upto) {
 #pragma unroll
     for (int t = 0; t < PB; ++t) {
       if (t >= upto) break;
-      if (t < pc && pf[t] >= C.thr) C.insert(pf[t], pj[t], band_i);
+      if (t < pc && pf[t] >= C.thr) {
+        if (p.debug == 4) {
+          if (pf[t] > C.f[KT - 1] || (pf[t] == C.f[KT - 1] && pj[t] < C.j[KT - 1])) ++st_top;
+          else ++st_pool;
+        }
+        C.insert(pf[t], pj[t], band_i);
+      }
     }
     pc = 0;
     const float b = C.kth() - band_i;
@@ -388,22 +401,22 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
   };
   uint32_t floor_next = live ? __ldcg(p.row_bound + (i - p.q_begin)) : 0u;
   for (int t = 0; t < ntiles; ++t) {
-    const int acc = t & 1;
-    const uint32_t acc_phase = (t >> 1) & 1;
+    const int acc = t % NACC;
+    const uint32_t acc_phase = (t / NACC) & 1;
     mbar_wait_backoff(&tfull[acc], acc_phase);
     if (live) {
       C.raise_floor(ord2f(floor_next));
       floor_next = __ldcg(p.row_bound + (i - p.q_begin));
     }
     tc_fence_after();
-    const int64_t j0 = (int64_t)(kt0 + t) * BN + half * EPI_COLS;
+    const int64_t j0 = (int64_t)kt0 * BN + (int64_t)t * TN + half * ECOLS;
 #pragma unroll 1
-    for (int ch = 0; ch < EPI_COLS / 32; ch += 2) {
+    for (int ch = 0; ch < ECOLS / 32; ch += 2) {
       uint32_t r[2][32];
-      tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + ch * 32, r[0]);
-      tmem_ld32(tmem + lane_off + acc * BN + half * EPI_COLS + (ch + 1) * 32, r[1]);
+      tmem_ld32(tmem + lane_off + acc * TN + half * ECOLS + ch * 32, r[0]);
+      tmem_ld32(tmem + lane_off + acc * TN + half * ECOLS + (ch + 1) * 32, r[1]);
       tmem_ld_wait();
-      if (ch + 2 == EPI_COLS / 32) {
+      if (ch + 2 == ECOLS / 32) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -423,7 +436,7 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
 #pragma unroll
           for (int u = 0; u < w; ++u) mx[u] = fmaxf(mx[u], mx[u + w]);
         if (mx[0] >= C.thr && p.debug != 3) {   // debug 3: the scan without admissions
-
+          if (p.debug == 4) ++st_chunks;
           const int64_t jb = j0 + (ch + h2) * 32;
           uint32_t mask = 0;
 #pragma unroll
@@ -447,6 +460,7 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
               pj[q] = q == pc ? (int32_t)(jb + u) : pj[q];
             }
             ++pc;
+            if (p.debug == 4) ++st_cand;
           }
         }
       }
@@ -454,6 +468,12 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
     }
   }
   drain(__reduce_max_sync(0xffffffffu, pc));
+  if (p.debug == 4 && p.stats && live) {
+    atomicAdd(p.stats + 0, st_chunks);
+    atomicAdd(p.stats + 1, st_cand);
+    atomicAdd(p.stats + 2, st_top);
+    atomicAdd(p.stats + 3, st_pool);
+  }
   if (live) {
 #pragma unroll
     for (int t = 0; t < KT; ++t)
@@ -633,10 +653,16 @@ __host__ __device__ constexpr size_t smem(int nks) {
 }
 }  // namespace res16
 
+template <int TN>
 __global__ void __launch_bounds__(tc::THREADS, 1)
 knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   RealParams p) {
   using namespace tc;
+  // TN = 256: two 256-column accumulators; TN = 128: four 128-column ones
+  // (the epilogue frees each after two chunk loads, and the MMA has three
+  // tiles of slack instead of one); keys stream as TN-row k-blocks
+  constexpr int NACC = TMEM_COLS / TN;
+  constexpr int TB_BYTES = TN * ROW_BYTES;
   extern __shared__ __align__(1024) unsigned char smraw[];
   const int nks = p.nkb_seg, S = res16::stages(nks);
   unsigned char* base = reinterpret_cast<unsigned char*>(
@@ -646,8 +672,8 @@ knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + S * res16::B_BYTES);
   uint64_t* empty = full + 6;
   uint64_t* tfull = empty + 6;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* afull = tempty + 2;
+  uint64_t* tempty = tfull + 4;
+  uint64_t* afull = tempty + 4;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(afull + 1);
   float* stash_base = reinterpret_cast<float*>(base + nks * res16::A_BYTES + S * res16::B_BYTES + 256);
 
@@ -656,12 +682,12 @@ knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
   const int seg = blockIdx.y;
   const int kt0 = p.kt_base + seg * p.tiles_per_seg;
   const int kt1 = min(p.key_tiles, kt0 + p.tiles_per_seg);
-  const int ntiles = kt1 - kt0;
+  const int ntiles = (kt1 - kt0) * (BN / TN);   // TN-column tiles
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s2 = 0; s2 < S; ++s2) { mbar_init(&full[s2], 1); mbar_init(&empty[s2], 1); }
-    for (int s2 = 0; s2 < 2; ++s2) { mbar_init(&tfull[s2], 1); mbar_init(&tempty[s2], EPI_WARPS); }
+    for (int s2 = 0; s2 < NACC; ++s2) { mbar_init(&tfull[s2], 1); mbar_init(&tempty[s2], EPI_WARPS); }
     mbar_init(afull, 1);
     fence_barrier_init();
   }
@@ -679,28 +705,28 @@ knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int krow = (kt0 + t) * BN;
+        const int krow = kt0 * BN + t * TN;
         for (int kb = 0; kb < nks; ++kb) {
           mbar_wait_backoff(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], res16::B_BYTES);
-          tma_load_2d(sB + stage * res16::B_BYTES, &tmB, &full[stage], kb * EL, krow);
+          mbar_arrive_expect_tx(&full[stage], TB_BYTES);
+          tma_load_2d(sB + stage * res16::B_BYTES, TN == BN ? &tmB : &tmA, &full[stage], kb * EL, krow);
           if (++stage == S) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(0u, BM, BN);     // kind::f16, F16 inputs
+      constexpr uint32_t idesc = make_idesc(0u, BM, TN);     // kind::f16, F16 inputs
       const bool skip = p.debug == 2;
       mbar_wait_sleep(afull, 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int t = 0; t < ntiles; ++t) {
-        const int acc = t & 1;
-        const uint32_t acc_phase = (t >> 1) & 1;
+        const int acc = t % NACC;
+        const uint32_t acc_phase = (t / NACC) & 1;
         mbar_wait_backoff(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t dtm = tmem + acc * BN;
+        const uint32_t dtm = tmem + acc * TN;
         for (int kb = 0; kb < nks; ++kb) {
           mbar_wait_backoff(&full[stage], phase);
           tc_fence_after();
@@ -719,7 +745,7 @@ knn_real16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant
       }
     }
   } else {
-    real_epilogue_batched<SlotsF16>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
+    real_epilogue_batched<SlotsF16, false, TN>(tfull, tempty, tmem, stash_base, p, q0, seg, kt0, ntiles);
   }
   tc_fence_before();
   __syncthreads();
@@ -1124,6 +1150,11 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
   p.q_end = q_end;
   p.debug = getenv("ANCKA_KNN_DEBUG") ? atoi(getenv("ANCKA_KNN_DEBUG")) : 0;
   p.spin = getenv("ANCKA_KNN_SPIN") ? atoi(getenv("ANCKA_KNN_SPIN")) : 0;
+  p.stats = nullptr;
+  if (p.debug == 4) {
+    ANCKA_CUDA(cudaMallocAsync(&p.stats, 4 * sizeof(unsigned long long), st));
+    ANCKA_CUDA(cudaMemsetAsync(p.stats, 0, 4 * sizeof(unsigned long long), st));
+  }
   ANCKA_CUDA(cudaMemsetAsync(w.rb, 0, sizeof(uint32_t) * nq, st));
   ANCKA_CUDA(cudaMemsetAsync(w.nflag, 0, sizeof(int), st));
   // Key segments as successive launches over all query tiles: the CTAs in
@@ -1137,19 +1168,24 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
   const int kt_first = (int)(R.kr.k0 / tc::BN);
   const int nlaunch = (int)ceil_div(R.g.key_tiles, seg_tiles);
   int lists = R.lists;
-  // CTA pairs (cta_group::2) unless ANCKA_KNN_PAIR=0
-  const bool pair = !getenv("ANCKA_KNN_PAIR") || atoi(getenv("ANCKA_KNN_PAIR")) != 0;
+  // CTA pairs (cta_group::2) only with ANCKA_KNN_PAIR=1 (measured equal)
+  const bool pair = getenv("ANCKA_KNN_PAIR") && atoi(getenv("ANCKA_KNN_PAIR")) != 0;
+  // 128-key accumulator tiles (four TMEM buffers: more slack between the MMA
+  // and the epilogue) only with ANCKA_KNN_N128=1: measured slower (Amazon2M
+  // 2.48 s against 1.85 s; 2.09 s with the admission work skipped)
+  const bool n128 = getenv("ANCKA_KNN_N128") && atoi(getenv("ANCKA_KNN_N128")) != 0;
   const size_t sm = pair ? pair16::smem(p.nkb_seg) : res16::smem(p.nkb_seg);
   const int qt = pair ? (int)((R.g.q_tiles + 1) & ~1) : R.g.q_tiles;
   if (pair)
     ANCKA_CUDA(cudaFuncSetAttribute(knn_real16_pair_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   else
-    ANCKA_CUDA(cudaFuncSetAttribute(knn_real16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)sm));
+    ANCKA_CUDA(cudaFuncSetAttribute(n128 ? knn_real16_kernel<128> : knn_real16_kernel<256>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
   auto launch = [&](dim3 grid) {
     if (pair) knn_real16_pair_kernel<<<grid, tc::THREADS, sm, st>>>(ma, p);
-    else knn_real16_kernel<<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+    else if (n128) knn_real16_kernel<128><<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
+    else knn_real16_kernel<256><<<grid, tc::THREADS, sm, st>>>(ma, mb, p);
   };
   if (nlaunch <= 1) {
     launch(dim3(qt, R.g.nseg));
@@ -1164,6 +1200,14 @@ int knn_real16(const double* X, int64_t n, int64_t d, int64_t ldx, int K, int64_
       launch(dim3(qt, 1));
       ANCKA_LAUNCHED();
     }
+  }
+  if (p.stats) {   // debug 4: admission counters
+    unsigned long long h[4];
+    ANCKA_CUDA(cudaMemcpyAsync(h, p.stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+    ANCKA_CUDA(cudaStreamSynchronize(st));
+    fprintf(stderr, "knn16 admissions: rows %lld chunks>=thr %llu candidates %llu top-K inserts %llu pool adds %llu\n",
+            (long long)nq, h[0], h[1], h[2], h[3]);
+    ANCKA_CUDA(cudaFreeAsync(p.stats, st));
   }
   const int mg = (int)std::min<int64_t>(ceil_div(nq * 32, 256), 16 * kNumSMs);
   knn_real_merge_kernel<SlotsF16><<<mg, 256, 0, st>>>(w.part, q_begin, nq, lists, K, 0.f,
