@@ -399,14 +399,27 @@ __device__ __forceinline__ void real_epilogue_batched(uint64_t* tfull, uint64_t*
       published = b;
     }
   };
-  uint32_t floor_next = live ? __ldcg(p.row_bound + (i - p.q_begin)) : 0u;
+  // The shared floor is fetched one tile ahead into this thread's spare
+  // stash slot by cp.async: a register copy of it was spilled (the load's
+  // latency then stalled every tile on the spill store)
+  uint32_t* floor_slot = reinterpret_cast<uint32_t*>(stash) + 32;
+  const uint32_t* floor_src = p.row_bound + (live ? i - p.q_begin : 0);
+  auto fetch_floor = [&]() {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n\tcp.async.commit_group;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(floor_slot)),
+                 "l"(floor_src)
+                 : "memory");
+  };
+  *floor_slot = 0u;
+  if (live) fetch_floor();
   for (int t = 0; t < ntiles; ++t) {
     const int acc = t % NACC;
     const uint32_t acc_phase = (t / NACC) & 1;
     mbar_wait_backoff(&tfull[acc], acc_phase);
     if (live) {
-      C.raise_floor(ord2f(floor_next));
-      floor_next = __ldcg(p.row_bound + (i - p.q_begin));
+      asm volatile("cp.async.wait_all;" ::: "memory");
+      C.raise_floor(ord2f(*reinterpret_cast<volatile uint32_t*>(floor_slot)));
+      fetch_floor();
     }
     tc_fence_after();
     const int64_t j0 = (int64_t)kt0 * BN + (int64_t)t * TN + half * ECOLS;
