@@ -16,6 +16,45 @@ def dev():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_PIN = {}          # device -> (two pinned staging buffers, their reuse events)
+_PIN_CHUNK = 64 << 20
+_POOL = None
+
+
+def to_device(a: np.ndarray) -> torch.Tensor:
+    """Host array -> new device tensor on the current stream, through two
+    pinned 64 MiB staging buffers: host threads fill one chunk while the
+    other one's copy runs (a pageable copy stages serially through one
+    driver buffer).  Small arrays take the plain copy."""
+    global _POOL
+    a = np.ascontiguousarray(a)
+    d = dev()
+    if a.nbytes < 4 * _PIN_CHUNK:
+        return torch.from_numpy(a).to(d)
+    from concurrent.futures import ThreadPoolExecutor
+    if _POOL is None:
+        _POOL = ThreadPoolExecutor(max_workers=4)
+    if d not in _PIN:
+        bufs = [torch.empty(_PIN_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        _PIN[d] = (bufs, [torch.cuda.Event(), torch.cuda.Event()])
+    bufs, evs = _PIN[d]
+    out = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, device=d)
+    src = a.reshape(-1).view(np.uint8)
+    dst = out.view(-1).view(torch.uint8)
+    stream = torch.cuda.current_stream()
+    quarter = _PIN_CHUNK // 4
+    for k, o in enumerate(range(0, src.size, _PIN_CHUNK)):
+        b = k & 1
+        evs[b].synchronize()                       # the buffer's previous copy is done
+        m = min(_PIN_CHUNK, src.size - o)
+        hb = bufs[b].numpy()
+        list(_POOL.map(lambda q: np.copyto(hb[q:min(q + quarter, m)], src[o + q:o + min(q + quarter, m)]),
+                       range(0, m, quarter)))
+        dst[o:o + m].copy_(bufs[b][:m], non_blocking=True)
+        evs[b].record(stream)
+    return out
+
+
 class DeviceCSR:
     """Row-sorted CSR on the device with f64 and f32 value copies."""
 

@@ -20,7 +20,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _lib
-from ._device import WORKSPACE, DeviceCSR, dev
+from ._device import WORKSPACE, DeviceCSR, dev, to_device
 from .network import KnnMode, NetworkError
 
 _PAD = -1
@@ -156,7 +156,7 @@ class DeviceAttributes:
                 self.dense = t.to_dense().contiguous()
                 self.indptr = self.indices = self.data = None
         else:
-            self.dense = torch.from_numpy(np.ascontiguousarray(X, dtype=np.float64)).to(d)
+            self.dense = to_device(np.asarray(X, dtype=np.float64))
             if level is None:
                 level = self._check(None, self.dense.data_ptr(), self.dense.stride(0),
                                     self.dense.shape[1])
