@@ -484,7 +484,7 @@ def run_single_gpu(name, args, with_e2e, with_cpu, steps, warmup, clocks=None):
                       "d2h_bytes_per_step": int(lab.size * 4 + 8 * 13 * (r2.iterations // 5 + 2)),
                       "runs_s": [round(x, 4) for x in e2e_t],
                       "note": "median of 3 wall-clock run_ancka(net, params) calls from host "
-                              "numpy/scipy inputs: validation, pageable H2D copies, labels D2H"}
+                              "numpy/scipy inputs: validation (overlapping the KNN), H2D copies (attributes through pinned staging buffers, structure pageable on a side stream), labels D2H"}
         del r2
     if with_cpu:
         est, wall, sample, per_kernel = cpu_estimate(name, inst, counts, 1.0 / 16, 100)
