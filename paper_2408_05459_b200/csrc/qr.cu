@@ -62,27 +62,46 @@ gram_blocked_kernel(const float* __restrict__ Z, int64_t n, int64_t ld, int c,
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_block;
   const int64_t r1 = lmin(n, r0 + rows_per_block);
   const int ld4 = (int)(ld / 4);
-  for (int64_t t0 = r0; t0 < r1; t0 += kGT) {
+  // double-buffered tiles: the copy of tile t + 1 runs under tile t's FMAs
+  auto stage = [&](int64_t t0, int b) {
     const int tr = (int)lmin(kGT, r1 - t0);
-    __syncthreads();
     const float4* src = reinterpret_cast<const float4*>(Z + t0 * ld);
-    float4* dst = reinterpret_cast<float4*>(gtile);
-    for (int e = threadIdx.x; e < tr * ld4; e += blockDim.x) dst[e] = __ldg(src + e);
-    __syncthreads();
-    if (!active) continue;
-#pragma unroll
-    for (int u = 0; u < 16; ++u) acc32[u] = 0.f;
-    for (int r = g; r < tr; r += groups) {
-      const float4 a = *reinterpret_cast<const float4*>(gtile + r * ld + 4 * bi);
-      const float4 b = *reinterpret_cast<const float4*>(gtile + r * ld + 4 * bj);
-      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) acc32[u * 4 + v] = fmaf(av[u], bv[v], acc32[u * 4 + v]);
+    float* dst = gtile + (size_t)b * kGT * ld;
+    for (int e = threadIdx.x; e < tr * ld4; e += blockDim.x)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(dst + 4 * e)),
+                   "l"(src + e)
+                   : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  if (r0 < r1) stage(r0, 0);
+  int buf = 0;
+  for (int64_t t0 = r0; t0 < r1; t0 += kGT, buf ^= 1) {
+    const int tr = (int)lmin(kGT, r1 - t0);
+    if (t0 + kGT < r1) {
+      stage(t0 + kGT, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
+    __syncthreads();
+    const float* tile = gtile + (size_t)buf * kGT * ld;
+    if (active) {
 #pragma unroll
-    for (int u = 0; u < 16; ++u) acc64[u] += (double)acc32[u];
+      for (int u = 0; u < 16; ++u) acc32[u] = 0.f;
+      for (int r = g; r < tr; r += groups) {
+        const float4 a = *reinterpret_cast<const float4*>(tile + r * ld + 4 * bi);
+        const float4 b = *reinterpret_cast<const float4*>(tile + r * ld + 4 * bj);
+        const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < 4; ++v) acc32[u * 4 + v] = fmaf(av[u], bv[v], acc32[u * 4 + v]);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) acc64[u] += (double)acc32[u];
+    }
+    __syncthreads();                          // buffer free for the copy after next
   }
   __syncthreads();
   double* red = reinterpret_cast<double*>(gtile);  // groups x nq x 16 doubles
@@ -168,6 +187,71 @@ apply_rinv_tiled_kernel(const float* __restrict__ Z, const float* __restrict__ Q
           if (j0 + v < c) dq += d * d;
         }
         *reinterpret_cast<float4*>(Q + row * ld + j0) = make_float4(o[u][0], o[u][1], o[u][2], o[u][3]);
+      }
+    }
+  }
+  dq = block_sum(dq, red);
+  if (threadIdx.x == 0) dq_partial[blockIdx.x] = dq;
+}
+
+// Q = Z R^-1 for c <= 64: a thread per row, the row and its c outputs in
+// registers, R^-1 in shared memory (every lane reads the same entry:
+// broadcast); Z, Q_prev and Q rows move as float4s.  The same f32 sums in
+// the same l order as apply_rinv_tiled_kernel (R^-1 is upper triangular, the
+// skipped terms are exact zeros).
+template <int CM>
+__global__ void __launch_bounds__(256)
+apply_rinv_rows_kernel(const float* __restrict__ Z, const float* __restrict__ Qprev,
+                       float* __restrict__ Q, int64_t n, int64_t ld, int c,
+                       const float* __restrict__ rinv, double* __restrict__ dq_partial) {
+  __shared__ __align__(16) float rs[CM * CM];     // R^-1 (row l, col j), zero outside c
+  __shared__ double red[32];
+  for (int e = threadIdx.x; e < CM * CM; e += blockDim.x) {
+    const int l = e / CM, j = e % CM;
+    rs[e] = (l < c && j < c) ? rinv[l * c + j] : 0.f;
+  }
+  __syncthreads();
+  const int ld4 = (int)(ld / 4);
+  double dq = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    float z[CM], o[CM];
+    const float4* zr = reinterpret_cast<const float4*>(Z + i * ld);
+#pragma unroll
+    for (int q = 0; q < CM / 4; ++q) {
+      const float4 v = q < ld4 ? __ldg(zr + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+      z[4 * q] = v.x; z[4 * q + 1] = v.y; z[4 * q + 2] = v.z; z[4 * q + 3] = v.w;
+    }
+#pragma unroll
+    for (int j = 0; j < CM; ++j) o[j] = 0.f;
+#pragma unroll
+    for (int l = 0; l < CM; ++l) {
+      if (l < c) {
+        const float zl = z[l];
+        const float4* rl = reinterpret_cast<const float4*>(rs + l * CM);
+#pragma unroll
+        for (int q = l / 4; q < CM / 4; ++q) {
+          const float4 w = rl[q];
+          o[4 * q] = fmaf(zl, w.x, o[4 * q]);
+          o[4 * q + 1] = fmaf(zl, w.y, o[4 * q + 1]);
+          o[4 * q + 2] = fmaf(zl, w.z, o[4 * q + 2]);
+          o[4 * q + 3] = fmaf(zl, w.w, o[4 * q + 3]);
+        }
+      }
+    }
+    const float4* pr = reinterpret_cast<const float4*>(Qprev + i * ld);
+    float4* qr = reinterpret_cast<float4*>(Q + i * ld);
+#pragma unroll
+    for (int q = 0; q < CM / 4; ++q) {
+      if (q < ld4) {
+        const float4 pv = __ldg(pr + q);
+        const float pvv[4] = {pv.x, pv.y, pv.z, pv.w};
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const double d = (double)o[4 * q + v] - (double)pvv[v];
+          if (4 * q + v < c) dq += d * d;
+        }
+        qr[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
       }
     }
   }
@@ -311,7 +395,7 @@ static int launch_gram(const float* Z, int64_t n, int64_t ld, int c, double* par
   const int ny = (nbp + kGramThreads - 1) / kGramThreads;
   const int nq = (nbp + ny - 1) / ny;
   const int groups = nq >= kGramThreads ? 1 : kGramThreads / nq;
-  const size_t smem = std::max<size_t>((size_t)kGT * ld * sizeof(float),
+  const size_t smem = std::max<size_t>((size_t)2 * kGT * ld * sizeof(float),
                                        (size_t)groups * nq * 16 * sizeof(double));
   if (smem > 48 * 1024)
     ANCKA_CUDA(cudaFuncSetAttribute(gram_blocked_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -323,6 +407,15 @@ static int launch_gram(const float* Z, int64_t n, int64_t ld, int c, double* par
 
 static int launch_apply(const float* Z, const float* Qprev, float* Qout, int64_t n, int64_t ld,
                         int c, const float* rinv, double* dq_partial, cudaStream_t st) {
+  if (c <= 64 && !getenv("ANCKA_QR_TILED_APPLY")) {
+    const int cm = c <= 16 ? 16 : c <= 32 ? 32 : c <= 48 ? 48 : 64;
+    if (cm == 16) apply_rinv_rows_kernel<16><<<kApplyBlocks, 256, 0, st>>>(Z, Qprev, Qout, n, ld, c, rinv, dq_partial);
+    else if (cm == 32) apply_rinv_rows_kernel<32><<<kApplyBlocks, 256, 0, st>>>(Z, Qprev, Qout, n, ld, c, rinv, dq_partial);
+    else if (cm == 48) apply_rinv_rows_kernel<48><<<kApplyBlocks, 256, 0, st>>>(Z, Qprev, Qout, n, ld, c, rinv, dq_partial);
+    else apply_rinv_rows_kernel<64><<<kApplyBlocks, 256, 0, st>>>(Z, Qprev, Qout, n, ld, c, rinv, dq_partial);
+    ANCKA_LAUNCHED();
+    return ANCKA_OK;
+  }
   const size_t smem = ((size_t)c * ld + (size_t)ld * kATS) * sizeof(float);
   ANCKA_REQUIRE(smem <= 227 * 1024 && ld / 4 <= 256, ANCKA_ERR_UNSUPPORTED, "apply: c=%d too large", c);
   if (smem > 48 * 1024)
