@@ -10,9 +10,11 @@ This module stores the same content as raw arrays in a directory:
     attributes.npy | attributes_{indptr,indices,data}.npy
     labels.npy                 (optional)
 
-`load_network` memory-maps the arrays (no parse step), so the only O(nnz)
-host work left is the canonicalisation `AttributedNetwork` performs, exactly
-as for any other input.  `save_network` mirrors the reference's
+`load_network` memory-maps the arrays (no parse step) and validates them in
+place: a canonical CSR (what `save_network` writes) is checked with one read
+of its arrays and never copied; anything else is canonicalised exactly as
+for any other input.  `cli.py` is the RunConfig / command-line driver on
+top (reference cli.py:86-128, io.py:426-517).  `save_network` mirrors the reference's
 `io.save_network(out_dir, net, labels)` (`io.py:384-418`).
 """
 from __future__ import annotations
@@ -91,12 +93,12 @@ def load_network(src_dir, mmap: bool = True):
     kind = NetworkKind(meta["kind"])
     if kind is NetworkKind.HYPERGRAPH:
         net = AttributedNetwork.hypergraph(_load_csr(src, "structure", meta["structure_shape"],
-                                                     mmap), x)
+                                                     mmap), x, copy=False)
     elif kind is NetworkKind.GRAPH:
         net = AttributedNetwork.graph(_load_csr(src, "structure", meta["structure_shape"], mmap),
-                                      x, directed=bool(meta["directed"]))
+                                      x, directed=bool(meta["directed"]), copy=False)
     else:
         layers = [_load_csr(src, f"layer{i}", (n, n), mmap) for i in range(int(meta["n_layers"]))]
-        net = AttributedNetwork.multiplex(layers, x)
+        net = AttributedNetwork.multiplex(layers, x, copy=False)
     labels = np.load(src / "labels.npy") if meta.get("labels") else None
     return net, labels

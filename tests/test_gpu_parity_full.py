@@ -264,3 +264,24 @@ def test_planted_partition_end_to_end():
             res = ancka.run_ancka(net, ancka.ClusterParams(k=k, knn_k=10, seed=seed))
             assert res.error is None
             assert ari(res.y.assignment, lab) == 1.0, (seed, net.kind)
+
+
+def test_cli_run_binary_matches_in_memory(tmp_path):
+    """f3: `python -m ... run` over a binary directory (mapped arrays,
+    validated in place) returns the in-memory run's labels and phi."""
+    import json
+
+    from paper_2408_05459_b200 import cli
+    assert cli.main(["gen", "--shape", "dblp", "--n", "3000", "--out", str(tmp_path / "d")]) == 0
+    out = tmp_path / "r.json"
+    rc = cli.main(["run", "--net-dir", str(tmp_path / "d"), "-k", "6", "--knn-k", "10",
+                   "--knn-mode", "exact", "-o", str(out)])
+    assert rc == cli.EXIT_OK
+    doc = json.loads(out.read_text())
+    inst = synth.make("dblp", seed=0, n=3000)
+    ref = ancka.run_ancka(_net(inst), ancka.ClusterParams(k=6, knn_k=10, seed=0,
+                                                          knn_mode=ancka.KnnMode.EXACT))
+    assert np.array_equal(np.asarray(doc["assignment"]), ref.y.assignment)
+    assert doc["mhc"] == ref.mhc and doc["iterations"] == ref.iterations
+    assert doc["stop_reason"] == ref.stop_reason and "load_ms" in doc
+    assert set(doc["metrics"]) == {"ari", "nmi"}
