@@ -374,6 +374,67 @@ int ancka_beta_vector(const double* degrees, const uint8_t* knn_zero_rows, int64
 int ancka_cluster_sizes(const int32_t* labels, int64_t n, int32_t k, int64_t* sizes_out,
                         ancka_stream_t stream);
 
+/* ---- approximate KNN: inverted-file index (knn.py:143-280, knn_search_approx;
+ * csrc/knn_ivf.cu).  xn is the n x dp f32 copy of the row-normalised
+ * attributes (dp = d rounded up to 4, zero padded), the matrix the reference
+ * searches (knn.py:172-174). */
+/* xn = f32(x * (1/||x||)) from dense f64 X (X != NULL) or CSR attributes. */
+int ancka_ivf_normalize(const double* X, int64_t ldx, const int64_t* indptr,
+                        const int32_t* indices, const double* data, int64_t n, int64_t d,
+                        float* xn, int64_t dp, ancka_stream_t stream);
+/* S = A[arows] B^T + bias (f32): stored to C (m x ldc) when C != NULL, and/or
+ * reduced to a first-max argmax per row into argmax_keys (zeroed u64, packed
+ * score | ~column; decode with ancka_ivf_argmax_finish).  knn.py:216-222
+ * (_batched_argmax_assign) and the probe scores of knn.py:246. */
+int ancka_ivf_gemm(const float* A, int64_t lda, const int32_t* arows, int64_t m, const float* B,
+                   int64_t ldb, int32_t nb, int64_t d, const float* bias, float* C, int64_t ldc,
+                   unsigned long long* argmax_keys, ancka_stream_t stream);
+/* labels[r] = argmax column; counts label changes into *changed (nullable);
+ * re-zeroes the keys. */
+int ancka_ivf_argmax_finish(unsigned long long* argmax_keys, int64_t m, int32_t* labels,
+                            int32_t* changed, ancka_stream_t stream);
+/* probes[r] = the nprobe largest of S[r, :nb] (knn.py:250, argpartition;
+ * ties to the smaller column). */
+int ancka_ivf_topsel(const float* S, int64_t lds, int64_t m, int32_t nb, int32_t nprobe,
+                     int32_t* probes, ancka_stream_t stream);
+/* Counting sort of count entries by key: ptr (nbuckets + 1) offsets, ent =
+ * entry indices grouped by key; tiles (nullable) = per-bucket offsets of
+ * ceil(size / tile) tiles.  Inverted lists (knn.py:200-203) and pair lists. */
+size_t ancka_ivf_bucket_workspace_size(int32_t nbuckets);
+int ancka_ivf_bucket(const int32_t* keys, int64_t count, int32_t nbuckets, int64_t* ptr,
+                     int64_t* tiles, int32_t tile, int32_t* ent, void* workspace,
+                     size_t workspace_bytes, ancka_stream_t stream);
+/* Per (query, probe slot) pair: top-K2 f32 scores of the probed list's keys
+ * (score desc, id asc; self excluded; scores <= -err dropped) into
+ * part_s/part_i ((m * nprobe) x K2).  _ivf_search_all, knn.py:236-262.
+ * qthr: m zeroed u32, the per-query threshold shared across pairs. */
+int ancka_ivf_search(const float* xn, int64_t dp, const int32_t* perm, const int64_t* list_ptr,
+                     const int64_t* pair_ptr, const int32_t* pair_ent, const int64_t* tile_ptr,
+                     int32_t* counter, int32_t nlist, int32_t nprobe, int64_t q0, int32_t K2,
+                     float err, float* part_s, int32_t* part_i, uint32_t* qthr,
+                     ancka_stream_t stream);
+/* Per query: merge the partial lists, re-rank in f64, top-K positive
+ * (knn.py:257-260 with _ordered_top_k, knn.py:83-98); uncertified rows are
+ * appended (global ids) to flagged / *nflag. */
+int ancka_ivf_merge(const float* xn, int64_t dp, int64_t q0, int64_t m, int32_t nprobe, int32_t K2,
+                    int32_t K, const float* part_s, const int32_t* part_i, float err, int32_t* ids,
+                    double* scores, int32_t* flagged, int32_t* nflag, ancka_stream_t stream);
+/* Exact top-K (f64 accumulation) for the listed rows against their probe
+ * lists (probes != NULL) or all keys (the recall audit, _exact_rows_for,
+ * knn.py:225-233).  compact: output row b instead of rows[b] - q0. */
+int ancka_ivf_rows_exact(const float* xn, int64_t dp, int64_t n, const int32_t* rows,
+                         int64_t nrows, const int32_t* probes, int32_t nprobe, int64_t q0,
+                         const int32_t* perm, const int64_t* list_ptr, int32_t K, int32_t* ids,
+                         double* scores, int32_t compact, ancka_stream_t stream);
+/* One Lloyd update of the IVF centroids (_train_ivf, knn.py:143-153): cluster
+ * sums in 64-bit fixed point (sums: nlist x d u64, counts: nlist, both
+ * zeroed and left zeroed), C = mean (empty clusters keep their centre), bias
+ * = -|C|^2/2 for the L2 assignment.  sums == NULL: bias only. */
+int ancka_ivf_kmeans_update(const float* S, int64_t lds, const int32_t* arows, int64_t m,
+                            const int32_t* labels, int32_t nlist, int64_t d,
+                            unsigned long long* sums, int32_t* counts, float* C, int64_t ldc,
+                            float* bias, ancka_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

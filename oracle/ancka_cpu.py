@@ -188,6 +188,142 @@ def knn_exact(X, K, block_rows=None):
     return ids, scores
 
 
+# ----------------------------------------------------------------------------
+# knn.py (approximate mode: inverted-file index, knn.py:143-280)
+# ----------------------------------------------------------------------------
+def ivf_defaults(n, nlist=None, nprobe=None):
+    """knn.py:181-187."""
+    if nlist is None:
+        nlist = int(min(4096, max(8, round(np.sqrt(n)))))
+    nlist = min(nlist, n)
+    if nprobe is None:
+        nprobe = max(4, nlist // 32)
+    return nlist, min(nprobe, nlist)
+
+
+def ivf_unit_f32(X):
+    """knn.py:172-175: the f32 dense copy of the normalised rows."""
+    xn, nrm = unit_rows(X)
+    if sp.issparse(xn):
+        xn = np.asarray(xn.todense())
+    return np.ascontiguousarray(xn, dtype=np.float32), nrm
+
+
+def ivf_train(xn, nlist, seed):
+    """_train_ivf (knn.py:143-153): sklearn KMeans on at most 50 nlist rows."""
+    from sklearn.cluster import KMeans
+    sample = xn
+    if xn.shape[0] > 50 * nlist:
+        rng = np.random.default_rng(seed)
+        sample = xn[rng.choice(xn.shape[0], size=50 * nlist, replace=False)]
+    km = KMeans(n_clusters=nlist, n_init=1, max_iter=25, random_state=seed)
+    km.fit(sample)
+    return km.cluster_centers_.astype(xn.dtype)
+
+
+def ivf_assign(xn, centroids):
+    """_batched_argmax_assign (knn.py:216-222)."""
+    n = xn.shape[0]
+    out = np.empty(n, dtype=np.int64)
+    step = max(1, int(2.5e7 // max(centroids.shape[0], 1)))
+    for lo in range(0, n, step):
+        out[lo: lo + step] = np.argmax(xn[lo: lo + step] @ centroids.T, axis=1)
+    return out
+
+
+def ivf_lists(labels, nlist):
+    """knn.py:198-203: member rows of each list, ascending."""
+    order = np.argsort(labels, kind="stable")
+    cuts = np.searchsorted(labels[order], np.arange(nlist + 1))
+    return [order[cuts[c]: cuts[c + 1]] for c in range(nlist)]
+
+
+def ivf_probes(xn, centroids, rows, nprobe):
+    """The probe sets of knn.py:246-250 (as sets; argpartition's order is not
+    part of the contract) plus the f32 centroid scores."""
+    cd = xn[rows] @ centroids.T
+    return np.argpartition(-cd, nprobe - 1, axis=1)[:, :nprobe], cd
+
+
+def ivf_search_all(xn, nrm, centroids, lists, K, nprobe):
+    """_ivf_search_all (knn.py:236-262): (ids (n,K) padded -1, scores)."""
+    n, nlist = xn.shape[0], centroids.shape[0]
+    ids = np.full((n, K), -1, dtype=np.int64)
+    scores = np.zeros((n, K), dtype=np.float64)
+    step = max(1, int(2.5e7 // max(nlist, 1)))
+    for lo in range(0, n, step):
+        hi = min(lo + step, n)
+        cd = xn[lo:hi] @ centroids.T
+        probes = None if nprobe >= nlist else np.argpartition(-cd, nprobe - 1, axis=1)[:, :nprobe]
+        for r in range(hi - lo):
+            q = lo + r
+            if nrm[q] == 0.0:
+                continue
+            cand = np.arange(n) if probes is None else np.sort(np.concatenate(
+                [lists[c] for c in probes[r]]))
+            sims = xn[cand] @ xn[q]
+            sims[cand == q] = -1.0
+            sel = _select_row(sims.astype(np.float64), K)
+            ids[q, : sel.size] = cand[sel]
+            scores[q, : sel.size] = np.minimum(sims[sel].astype(np.float64), 1.0)
+    return ids, scores
+
+
+def ivf_exact_rows(xn, nrm, rows, K):
+    """_exact_rows_for (knn.py:225-233): f32 similarities of the audit rows."""
+    out = {}
+    step = max(1, int(2.5e7 // max(xn.shape[0], 1)))
+    for lo in range(0, rows.size, step):
+        chunk = rows[lo: lo + step]
+        sims = xn[chunk] @ xn.T
+        sims[np.arange(chunk.size), chunk] = -1.0
+        for j, i in enumerate(chunk):
+            out[int(i)] = (np.empty(0, dtype=np.int64) if nrm[i] == 0.0
+                           else _select_row(sims[j].astype(np.float64), K).astype(np.int64))
+    return out
+
+
+def ivf_recall(ids, truth, rows):
+    """_audit_recall (knn.py:265-274)."""
+    hits = []
+    for i in rows:
+        t = truth[int(i)]
+        if t.size == 0:
+            continue
+        got = ids[int(i)]
+        hits.append(np.isin(t, got[got >= 0]).mean())
+    return float(np.mean(hits)) if hits else 1.0
+
+
+def knn_approx(X, K, recall_target=0.9, seed=0, nlist=None, nprobe=None, audit_size=1000,
+               centroids=None):
+    """knn_search_approx (knn.py:156-213).  Returns (ids, scores, info) with
+    info = {nlist, nprobe (final), recall, escalations, centroids}."""
+    xn, nrm = ivf_unit_f32(X)
+    n = xn.shape[0]
+    if K >= n:
+        raise OracleError(f"K={K} must be smaller than n={n}")
+    if centroids is not None:
+        nlist = centroids.shape[0]
+    nlist, nprobe = ivf_defaults(n, nlist, nprobe)
+    C = ivf_train(xn, nlist, seed) if centroids is None else np.asarray(centroids, np.float32)
+    lists = ivf_lists(ivf_assign(xn, C), nlist)
+    rng = np.random.default_rng(seed)
+    m = min(n, max(audit_size, 1000))
+    audit = np.sort(rng.choice(n, size=m, replace=False))
+    truth = ivf_exact_rows(xn, nrm, audit, K)
+    esc = 0
+    while True:
+        ids, scores = ivf_search_all(xn, nrm, C, lists, K, nprobe)
+        recall = ivf_recall(ids, truth, audit)
+        if recall >= recall_target or nprobe >= nlist:
+            break
+        nprobe = min(nlist, nprobe * 2)
+        esc += 1
+    return ids, scores, {"nlist": nlist, "nprobe": nprobe, "recall": recall, "escalations": esc,
+                         "centroids": C}
+
+
 def knn_adjacency(ids, scores):
     """build_knn_adjacency (knn.py:294-309): A_K = M + M^T, sorted CSR."""
     n = ids.shape[0]

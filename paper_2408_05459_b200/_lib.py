@@ -69,6 +69,28 @@ _SIGS = {
     "ancka_knn_exact_csr_keys": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64,
                                            c_int32, c_int32, c_int64, c_int64, c_int64, c_int64,
                                            c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_ivf_normalize": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64,
+                                      c_int64, c_void_p, c_int64, c_void_p]),
+    "ancka_ivf_gemm": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p, c_int64, c_int32,
+                                 c_int64, c_void_p, c_void_p, c_int64, c_void_p, c_void_p]),
+    "ancka_ivf_argmax_finish": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p]),
+    "ancka_ivf_topsel": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_int32, c_void_p,
+                                   c_void_p]),
+    "ancka_ivf_bucket_workspace_size": (c_size_t, [c_int32]),
+    "ancka_ivf_bucket": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p, c_int32,
+                                   c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_ivf_search": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                   c_void_p, c_void_p, c_int32, c_int32, c_int64, c_int32,
+                                   ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ancka_ivf_merge": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32,
+                                  c_void_p, c_void_p, ctypes.c_float, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p]),
+    "ancka_ivf_rows_exact": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                       c_int32, c_int64, c_void_p, c_void_p, c_int32, c_void_p,
+                                       c_void_p, c_int32, c_void_p]),
+    "ancka_ivf_kmeans_update": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p,
+                                          c_int32, c_int64, c_void_p, c_void_p, c_void_p,
+                                          c_int64, c_void_p, c_void_p]),
     "ancka_knn_merge_lists": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,
                                         c_void_p]),
     "ancka_knn_graph_coo_workspace_size": (c_size_t, [c_int64]),

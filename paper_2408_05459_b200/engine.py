@@ -31,8 +31,8 @@ import torch
 from . import _lib
 from ._device import WORKSPACE, dev, ld_for, padded
 from .knn import (KnnGraph, NeighborLists, attributes_to_device, build_knn_graph_device,
-                  cache_key, integer_exact, knn_search_exact_device, load_neighbor_cache,
-                  save_neighbor_cache)
+                  cache_key, integer_exact, knn_search_approx, knn_search_exact_device,
+                  load_neighbor_cache, resolve_knn_mode, save_neighbor_cache)
 from .network import (AttributedNetwork, BcmMatrix, ClusterParams, KnnMode, NetworkError,
                       default_knn_k, validate_network, NetworkKind)
 from .walk import StructureFactors, WalkOperator, build_walk_operator
@@ -650,10 +650,12 @@ def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):
     if prep.cache_path is not None and prep.cache_path.exists():
         neighbors, mode_used = load_neighbor_cache(prep.cache_path)
     if neighbors is None:
-        if params.knn_mode is KnnMode.APPROX:
-            warnings.warn("approximate KNN is not implemented on B200; running exact search")
-        ids, scores = knn_search_exact_device(prep.x_dev, K, integer=prep.x_level)
-        neighbors, mode_used = NeighborLists(ids_dev=ids, scores_dev=scores, K=K), KnnMode.EXACT
+        if resolve_knn_mode(params.knn_mode, n) is KnnMode.APPROX:      # knn.py:286-291
+            neighbors = knn_search_approx(prep.x_dev, K, seed=params.seed)
+            mode_used = KnnMode.APPROX
+        else:
+            ids, scores = knn_search_exact_device(prep.x_dev, K, integer=prep.x_level)
+            neighbors, mode_used = NeighborLists(ids_dev=ids, scores_dev=scores, K=K), KnnMode.EXACT
         if prep.cache_path is not None:
             prep.cache_path.parent.mkdir(parents=True, exist_ok=True)
             save_neighbor_cache(prep.cache_path, neighbors, mode_used)

@@ -6,8 +6,9 @@ candidates + exact f64 re-rank with an error certificate for real-valued
 attributes, uncertified rows recomputed by the f64 CUDA-core scan) and `build_knn_adjacency` / `knn_transition` run
 `ancka_knn_graph`.  Results stay in HBM; the numpy/scipy views the reference
 API exposes (`NeighborLists.ids`, `KnnGraph.adjacency`, ...) are materialised
-lazily on first access.  Approximate search is not offered: every mode runs
-the exact kernel.
+lazily on first access.  `knn_search_approx` is the reference's inverted-file
+search (knn.py:143-280) on the device (csrc/knn_ivf.cu); `search_knn` and the
+engine dispatch AUTO as the reference does (approximate at n >= 100k).
 """
 from __future__ import annotations
 
@@ -21,7 +22,7 @@ import torch
 
 from . import _lib
 from ._device import WORKSPACE, DeviceCSR, dev, to_device
-from .network import KnnMode, NetworkError
+from .network import APPROX_KNN_THRESHOLD, KnnMode, NetworkError
 
 _PAD = -1
 #: route attributes to the tcgen05 kernels (knn_tc.cu, knn_tc_real.cu); when
@@ -271,14 +272,275 @@ def knn_search_exact(X, K: int, block_rows: int | None = None) -> NeighborLists:
     return NeighborLists(ids_dev=ids, scores_dev=scores, K=K)
 
 
+# --------------------------------------------------------------------------
+# Approximate search: inverted-file index (knn.py:143-280; csrc/knn_ivf.cu)
+# --------------------------------------------------------------------------
+
+#: per-chunk device bytes for the probe scores and partial lists
+IVF_CHUNK_BYTES = 8 << 30
+#: extra slots per (query, list) partial list and in the merged list; the
+#: f64 re-rank certifies the top-K against the K2-th f32 score
+IVF_MARGIN = 8
+
+
+def ivf_defaults(n: int, nlist: int | None, nprobe: int | None):
+    """knn.py:181-187."""
+    if nlist is None:
+        nlist = int(min(4096, max(8, round(np.sqrt(n)))))
+    nlist = min(nlist, n)
+    if nprobe is None:
+        nprobe = max(4, nlist // 32)
+    return nlist, min(nprobe, nlist)
+
+
+def _ivf_xn(X):
+    """Row-normalised f32 attributes on the device (knn.py:172-174): n x dp."""
+    n, d = X.shape
+    dp = max(4, (d + 3) // 4 * 4)
+    xn = torch.empty((n, dp), dtype=torch.float32, device=dev())
+    if isinstance(X, torch.Tensor):
+        _lib.call("ancka_ivf_normalize", X.data_ptr(), X.stride(0), None, None, None, n, d,
+                  xn.data_ptr(), dp, _lib.stream())
+        return xn
+    xa = X if isinstance(X, DeviceAttributes) else DeviceAttributes(X, 0)
+    if xa.dense is not None:
+        _lib.call("ancka_ivf_normalize", xa.dense.data_ptr(), xa.dense.stride(0), None, None, None,
+                  n, d, xn.data_ptr(), dp, _lib.stream())
+    else:
+        _lib.call("ancka_ivf_normalize", None, 0, xa.indptr.data_ptr(), xa.indices.data_ptr(),
+                  xa.data.data_ptr(), n, d, xn.data_ptr(), dp, _lib.stream())
+    return xn
+
+
+def _bucket(keys, count: int, nbuckets: int, tile: int = 0):
+    dv = keys.device
+    ptr = torch.empty(nbuckets + 1, dtype=torch.int64, device=dv)
+    tiles = torch.empty(nbuckets + 1, dtype=torch.int64, device=dv) if tile else None
+    ent = torch.empty(max(count, 1), dtype=torch.int32, device=dv)
+    wsb = _lib.load().ancka_ivf_bucket_workspace_size(nbuckets)
+    ws = WORKSPACE.get("ivf_bucket", wsb)
+    _lib.call("ancka_ivf_bucket", keys.data_ptr(), count, nbuckets, ptr.data_ptr(),
+              tiles.data_ptr() if tile else None, tile, ent.data_ptr(), ws.data_ptr(), ws.numel(),
+              _lib.stream())
+    return ptr, tiles, ent
+
+
+def _argmax_rows(xn, rows, m, C, bias, labels, changed=None):
+    keys = torch.zeros(m, dtype=torch.int64, device=xn.device)
+    _lib.call("ancka_ivf_gemm", xn.data_ptr(), xn.stride(0),
+              rows.data_ptr() if rows is not None else None, m, C.data_ptr(), C.stride(0),
+              C.shape[0], xn.shape[1], bias.data_ptr() if bias is not None else None, None, 0,
+              keys.data_ptr(), _lib.stream())
+    _lib.call("ancka_ivf_argmax_finish", keys.data_ptr(), m, labels.data_ptr(),
+              changed.data_ptr() if changed is not None else None, _lib.stream())
+
+
+def train_ivf_device(xn, nlist: int, seed: int, max_iter: int = 25):
+    """Centroids for the index (knn.py:143-153) by Lloyd iterations on the
+    device, on the reference's training sample (the same `rng.choice` rows).
+    The reference runs sklearn's KMeans (k-means++ seeding); here the first
+    centres are `nlist` sample rows drawn from a second seeded generator, and
+    the iterations stop when no assignment changes or after `max_iter`
+    (sklearn's strict-convergence rule and cap).  Parity with the reference
+    is pinned by passing its centroids (`knn_search_approx(centroids=...)`)."""
+    n, dp = xn.shape
+    dv = xn.device
+    max_train = 50 * nlist
+    if n > max_train:
+        rng = np.random.default_rng(seed)
+        rows_h = rng.choice(n, size=max_train, replace=False)
+    else:
+        rows_h = np.arange(n)
+    ms = rows_h.size
+    rows = torch.from_numpy(rows_h.astype(np.int32)).to(dv)
+    init = np.random.default_rng([seed, 1]).choice(ms, size=nlist, replace=False)
+    C = xn[torch.from_numpy(rows_h[init].astype(np.int64)).to(dv)].contiguous()
+    bias = torch.empty(nlist, dtype=torch.float32, device=dv)
+    sums = torch.zeros((nlist, dp), dtype=torch.int64, device=dv)
+    counts = torch.zeros(nlist, dtype=torch.int32, device=dv)
+    _lib.call("ancka_ivf_kmeans_update", None, 0, None, 0, None, nlist, dp, None, None,
+              C.data_ptr(), C.stride(0), bias.data_ptr(), _lib.stream())
+    labels = torch.full((ms,), -1, dtype=torch.int32, device=dv)
+    changed = torch.zeros(1, dtype=torch.int32, device=dv)
+    iters = 0
+    for it in range(max_iter):
+        changed.zero_()
+        _argmax_rows(xn, rows, ms, C, bias, labels, changed)
+        iters = it + 1
+        if it > 0 and int(changed.item()) == 0:
+            break
+        _lib.call("ancka_ivf_kmeans_update", xn.data_ptr(), xn.stride(0), rows.data_ptr(), ms,
+                  labels.data_ptr(), nlist, dp, sums.data_ptr(), counts.data_ptr(), C.data_ptr(),
+                  C.stride(0), bias.data_ptr(), _lib.stream())
+    return C, iters
+
+
+class IvfIndex:
+    """Device inverted-file index: f32 normalised rows, centroids, and the
+    lists as (list_ptr, perm) -- rows of list c are perm[list_ptr[c]:
+    list_ptr[c+1]] (knn.py:198-203)."""
+
+    def __init__(self, xn, C, labels, list_ptr, perm, train_iters):
+        self.xn, self.C, self.labels = xn, C, labels
+        self.list_ptr, self.perm = list_ptr, perm
+        self.nlist = C.shape[0]
+        self.train_iters = train_iters
+
+
+def build_ivf_index(X, nlist: int, seed: int = 0, centroids=None) -> IvfIndex:
+    xn = X if (isinstance(X, torch.Tensor) and X.dtype == torch.float32) else _ivf_xn(X)
+    n, dp = xn.shape
+    iters = 0
+    if centroids is None:
+        C, iters = train_ivf_device(xn, nlist, seed)
+    else:
+        c = np.asarray(centroids, dtype=np.float32)
+        C = torch.zeros((c.shape[0], dp), dtype=torch.float32, device=xn.device)
+        C[:, :c.shape[1]] = torch.from_numpy(c).to(xn.device)
+    labels = torch.empty(n, dtype=torch.int32, device=xn.device)
+    _argmax_rows(xn, None, n, C, None, labels)                 # knn.py:197 (inner product)
+    list_ptr, _, perm = _bucket(labels, n, C.shape[0])
+    return IvfIndex(xn, C, labels, list_ptr, perm, iters)
+
+
+def _ivf_err(dp: int) -> float:
+    """Bound on |f32 dot - exact dot| for unit rows: (dp + 2) u (Cauchy-Schwarz)."""
+    return float((dp + 2) * 2.0 ** -24 * 1.001)
+
+
+def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | None = None):
+    """_ivf_search_all (knn.py:236-262) for every row: (ids int32, scores f64)."""
+    xn, nlist = index.xn, index.nlist
+    n, dp = xn.shape
+    dv = xn.device
+    K2 = min(K + IVF_MARGIN, 256)
+    err = _ivf_err(dp)
+    ids = torch.empty((n, K), dtype=torch.int32, device=dv)
+    scores = torch.empty((n, K), dtype=torch.float64, device=dv)
+    per_row = nlist * 4 + nprobe * 4 + nprobe * K2 * 8
+    chunk = int(max(1, min(n, IVF_CHUNK_BYTES // per_row)))
+    flagged = torch.empty(chunk, dtype=torch.int32, device=dv)
+    nflag = torch.zeros(1, dtype=torch.int32, device=dv)
+    counter = torch.zeros(1, dtype=torch.int32, device=dv)
+    S = torch.empty((chunk, nlist), dtype=torch.float32, device=dv)
+    probes = torch.empty((chunk, nprobe), dtype=torch.int32, device=dv)
+    part_s = torch.empty(chunk * nprobe * K2, dtype=torch.float32, device=dv)
+    part_i = torch.empty(chunk * nprobe * K2, dtype=torch.int32, device=dv)
+    qthr = torch.empty(chunk, dtype=torch.int32, device=dv)
+    st = _lib.stream()
+    total_flag = 0
+    for q0 in range(0, n, chunk):
+        m = min(chunk, n - q0)
+        _lib.call("ancka_ivf_gemm", xn[q0:].data_ptr(), dp, None, m, index.C.data_ptr(), dp, nlist,
+                  dp, None, S.data_ptr(), nlist, None, st)
+        _lib.call("ancka_ivf_topsel", S.data_ptr(), nlist, m, nlist, nprobe, probes.data_ptr(), st)
+        pair_ptr, tile_ptr, pair_ent = _bucket(probes, m * nprobe, nlist, tile=64)
+        qthr.zero_()
+        _lib.call("ancka_ivf_search", xn.data_ptr(), dp, index.perm.data_ptr(),
+                  index.list_ptr.data_ptr(), pair_ptr.data_ptr(), pair_ent.data_ptr(),
+                  tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe, q0, K2, err,
+                  part_s.data_ptr(), part_i.data_ptr(), qthr.data_ptr(), st)
+        nflag.zero_()
+        _lib.call("ancka_ivf_merge", xn.data_ptr(), dp, q0, m, nprobe, K2, K, part_s.data_ptr(),
+                  part_i.data_ptr(), err, ids[q0:].data_ptr(), scores[q0:].data_ptr(),
+                  flagged.data_ptr(), nflag.data_ptr(), st)
+        nf = int(nflag.item())
+        if nf:
+            _lib.call("ancka_ivf_rows_exact", xn.data_ptr(), dp, n, flagged.data_ptr(), nf,
+                      probes.data_ptr(), nprobe, q0, index.perm.data_ptr(),
+                      index.list_ptr.data_ptr(), K, ids[q0:].data_ptr(), scores[q0:].data_ptr(),
+                      0, st)
+        total_flag += nf
+    if stats is not None:
+        stats["uncertified_rows"] = stats.get("uncertified_rows", 0) + total_flag
+        stats["chunks"] = (n + chunk - 1) // chunk
+    return ids, scores
+
+
+def ivf_exact_rows_device(xn, rows: np.ndarray, K: int):
+    """Exact top-K of the listed rows against all keys (the audit truth,
+    _exact_rows_for, knn.py:225-233): (ids int32, scores f64), row b = rows[b]."""
+    n, dp = xn.shape
+    m = rows.size
+    r = torch.from_numpy(rows.astype(np.int32)).to(xn.device)
+    ids = torch.empty((max(m, 1), K), dtype=torch.int32, device=xn.device)
+    scores = torch.empty((max(m, 1), K), dtype=torch.float64, device=xn.device)
+    _lib.call("ancka_ivf_rows_exact", xn.data_ptr(), dp, n, r.data_ptr(), m, None, 0, 0, None, None,
+              K, ids.data_ptr(), scores.data_ptr(), 1, _lib.stream())
+    return ids[:m], scores[:m]
+
+
+def _audit_recall(ids_h: np.ndarray, truth_h: np.ndarray) -> float:
+    """knn.py:265-274 on the audit rows (host, m x K)."""
+    hits = []
+    for got, truth in zip(ids_h, truth_h):
+        t = truth[truth >= 0]
+        if t.size == 0:
+            continue
+        hits.append(np.isin(t, got[got >= 0]).mean())
+    return float(np.mean(hits)) if hits else 1.0
+
+
+def knn_search_approx(X, K: int, recall_target: float = 0.9, seed: int = 0,
+                      nlist: int | None = None, nprobe: int | None = None,
+                      audit_size: int = 1000, centroids=None) -> NeighborLists:
+    """Approximate top-K cosine neighbours through an inverted-file index
+    (knn.py:156-213): same defaults, the same audit sample and the same
+    probe escalation (x2 until the audited recall reaches `recall_target`
+    or every list is probed, warning as the reference does).  `centroids`
+    (nlist x d) replaces the device training, e.g. with the reference's
+    sklearn centroids for parity.  Diagnostics in LAST_STATS["approx"]."""
+    _lib.require_device()
+    n = X.shape[0]
+    if K >= n:
+        raise NetworkError(f"K={K} must be smaller than n={n}")
+    if centroids is not None:
+        nlist = np.asarray(centroids).shape[0]
+    nlist, nprobe = ivf_defaults(n, nlist, nprobe)
+    index = build_ivf_index(X, nlist, seed, centroids)
+    rng = np.random.default_rng(seed)                               # knn.py:205-208
+    m = min(n, max(audit_size, 1000))
+    audit_idx = np.sort(rng.choice(n, size=m, replace=False))
+    truth, _ = ivf_exact_rows_device(index.xn, audit_idx, K)
+    truth_h = truth.cpu().numpy()
+    audit_dev = torch.from_numpy(audit_idx.astype(np.int64)).to(index.xn.device)
+    stats = {"nlist": nlist, "train_iters": index.train_iters, "escalations": 0}
+    while True:
+        if nprobe >= nlist:     # probing every list is the exact search (knn.py:244-245)
+            ids, scores = knn_search_exact_device(X, K)
+        else:
+            ids, scores = ivf_search_all_device(index, K, nprobe, stats)
+        recall = _audit_recall(ids[audit_dev].cpu().numpy(), truth_h)
+        if recall >= recall_target or nprobe >= nlist:
+            if recall < recall_target:
+                warnings.warn(f"approximate KNN recall {recall:.3f} below target "
+                              f"{recall_target:.3f} even at exhaustive probing")
+            break
+        old = nprobe
+        nprobe = min(nlist, nprobe * 2)
+        stats["escalations"] += 1
+        warnings.warn(f"approximate KNN recall {recall:.3f} < {recall_target:.3f}; "
+                      f"escalating probes {old} -> {nprobe}")
+    stats.update(nprobe=nprobe, recall=recall)
+    LAST_STATS["approx"] = stats
+    return NeighborLists(ids_dev=ids, scores_dev=scores, K=K)
+
+
+def resolve_knn_mode(mode: KnnMode, n: int) -> KnnMode:
+    """AUTO: exact below APPROX_KNN_THRESHOLD nodes, approximate at or above
+    (knn.py:286-287, network.py:36)."""
+    if mode is KnnMode.AUTO:
+        return KnnMode.EXACT if n < APPROX_KNN_THRESHOLD else KnnMode.APPROX
+    return mode
+
+
 def search_knn(X, K: int, mode: KnnMode = KnnMode.AUTO, seed: int = 0,
                recall_target: float = 0.9):
-    """Mode dispatch (knn.py:283-291).  Exact search is fast enough on B200 at
-    every supported size, so AUTO and APPROX both run the exact kernel and
-    report `KnnMode.EXACT`."""
-    if mode is KnnMode.APPROX:
-        warnings.warn("approximate KNN is not implemented on B200; running exact search")
-    return knn_search_exact(X, K), KnnMode.EXACT
+    """Mode dispatch (knn.py:283-291)."""
+    mode = resolve_knn_mode(mode, X.shape[0])
+    if mode is KnnMode.EXACT:
+        return knn_search_exact(X, K), KnnMode.EXACT
+    return knn_search_approx(X, K, recall_target=recall_target, seed=seed), KnnMode.APPROX
 
 
 def build_knn_graph_device(ids, scores, n: int):

@@ -69,3 +69,10 @@ def golden_multiplex():
     z = np.load(GOLDEN / "multiplex.npz")
     meta = json.loads((GOLDEN / "multiplex.json").read_text())
     return z, meta
+
+
+@pytest.fixture(scope="session")
+def golden_approx():
+    z = np.load(GOLDEN / "approx.npz")
+    meta = json.loads((GOLDEN / "approx.json").read_text())
+    return z, meta

@@ -237,6 +237,37 @@ def aknn_cache():
     (HERE / "aknn.json").write_text(json.dumps(meta, indent=1))
 
 
+def approx_knn():
+    """Approximate KNN (knn.py:156-280): the reference's knn_search_approx
+    lists, its trained centroids (knn._train_ivf on its own f32 copy) and
+    the escalation count read from its warnings, on three seeded inputs --
+    continuous dense, binary sparse, and a forced escalation."""
+    cases = {
+        "dense": (synth.make("amazon2m", seed=0, n=3000).X, 10, 0.9, None, 0),
+        "binary": (synth.make("citeseer", seed=1, n=2500).X, 10, 0.9, None, 1),
+        "escalate": (np.abs(np.random.default_rng(3).normal(size=(2000, 16))), 8, 0.99, 1, 2),
+    }
+    out, meta = {}, {}
+    for name, (x, K, target, nprobe, seed) in cases.items():
+        _x(name + "_X", x, out)
+        with warnings.catch_warnings(record=True) as rec:
+            warnings.simplefilter("always")
+            nl = knn.knn_search_approx(x, K, recall_target=target, seed=seed, nprobe=nprobe)
+        esc = sum("escalating probes" in str(w.message) for w in rec)
+        xn, _ = knn._normalize_rows(x)
+        if sp.issparse(xn):
+            xn = np.asarray(xn.todense())
+        xn = np.ascontiguousarray(xn, dtype=np.float32)
+        n = xn.shape[0]
+        nlist = int(min(4096, max(8, round(np.sqrt(n)))))
+        out[name + "_centroids"] = knn._train_ivf(xn, nlist, seed)
+        out[name + "_ids"], out[name + "_scores"] = nl.ids, nl.scores
+        meta[name] = {"K": K, "recall_target": target, "nprobe": nprobe, "seed": seed,
+                      "nlist": nlist, "escalations": esc}
+    np.savez_compressed(HERE / "approx.npz", **out)
+    (HERE / "approx.json").write_text(json.dumps(meta, indent=1))
+
+
 if __name__ == "__main__":
     which = set(sys.argv[1:])
     if not which or "spec" in which:
@@ -249,5 +280,7 @@ if __name__ == "__main__":
         end_to_end_multiplex()
     if not which or "aknn" in which:
         aknn_cache()
+    if not which or "approx" in which:
+        approx_knn()
     for f in sorted(HERE.glob("*.npz")):
         print(f.name, f.stat().st_size)
