@@ -294,6 +294,21 @@ def discretize_dist(B, Q_loc, k: int, plan: Plan, max_iter: int = 100, tol: floa
     return B.disc_labels_host(res[3]), res[4]
 
 
+#: discretisation mode of the row-partitioned path: "auto" replicates the
+#: device discretisation on every rank (the gathered n x c f32 block, the
+#: single-GPU kernels, no host round trips) when that block is at most
+#: DISC_REPLICATED_BYTES, else runs `discretize_dist`; "replicated" /
+#: "partitioned" force one of them
+DISC_MODE = "auto"
+DISC_REPLICATED_BYTES = 16 << 30
+
+
+def _replicated_disc(B, n: int, c: int) -> bool:
+    if not hasattr(B, "disc_replicated") or DISC_MODE == "partitioned":
+        return False
+    return DISC_MODE == "replicated" or n * ((c + 3) // 4 * 4) * 4 <= DISC_REPLICATED_BYTES
+
+
 def _centers(deg: np.ndarray, k: int) -> np.ndarray:
     """Top-k degree nodes, ties to the smaller index, sorted (engine.py:97-110)."""
     n = deg.size
@@ -319,6 +334,7 @@ class DistResult:
     converged: bool
     error: str | None = None
     replays: int = 0
+    timings_ms: dict | None = None
 
 
 def _q0_chunk(B, labels: np.ndarray, sizes: np.ndarray, n: int, c: int, c0: int, cc: int):
@@ -361,9 +377,32 @@ def exact_step_dist(B, op: DistOperator, plan: Plan, Q_src, c: int, rng, labels0
     return Q, Z
 
 
+#: phase wall times in DistResult.timings_ms (synchronises at phase ends)
+DIST_TIMING = False
+
+
+class _Phases:
+    def __init__(self, B, on: bool):
+        import time
+        self.B, self.on, self.t = B, on, {}
+        self._clock = time.perf_counter
+        self._t0 = self._clock() if on else 0.0
+
+    def mark(self, key):
+        if not self.on:
+            return
+        sync = getattr(self.B, "synchronize", None)
+        if sync is not None:
+            sync()
+        now = self._clock()
+        self.t[key] = self.t.get(key, 0.0) + (now - self._t0) * 1e3
+        self._t0 = now
+
+
 def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop: bool = True) -> DistResult:
     """run_ancka (engine.py:343-437) row-partitioned over the backend's ranks."""
     rank, world = B.rank, B.world
+    ph = _Phases(B, DIST_TIMING)
     net, report = validate_network(net)
     if net.kind is NetworkKind.MULTIPLEX:
         raise NetworkError("the row-partitioned path covers graphs and hypergraphs")
@@ -374,9 +413,11 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     fac = ShardFactors(net, report.degrees)
     plan = make_plan(fac, K, rank, world)
     r0, r1 = plan.r0, plan.r1
+    ph.mark("host_prepare_ms")
 
     # ---- KNN: key ring, then A_K / P_K rows from an all-to-all of triples
     ids_loc, sc_loc = knn_ring(B, net.attributes, K, plan)
+    ph.mark("knn_ms")
     pk_rows, zero_loc = B.knn_graph_rows(ids_loc, sc_loc, plan, K)
 
     # beta_vector / self-loops (walk.py:47-57, 121-123) on the local rows
@@ -386,6 +427,7 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     beta[zero_loc] = 0.0
     selfloop = (deg[r0:r1] == 0) & (beta == 0.0)
     op = DistOperator(B, fac, plan, pk_rows, beta, selfloop, params.alpha, params.gamma)
+    ph.mark("graph_operator_ms")
 
     # ---- greedy init (engine.py:87-127): T_i transposed restart walks per
     # chunk of centres, running first-max argmax over the chunks
@@ -426,10 +468,12 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
         tr = B.sync_scalars([B.trace_labels(F_loc, labels[r0:r1], yhat)])[0]
         return 1.0 - tr / k
 
+    ph.mark("init_ms")
     rng = np.random.default_rng(params.seed)
     c = min(k + 1, n)
     sizes0 = np.bincount(lab0, minlength=k)
     best_phi = mhc(lab0, "f64")
+    ph.mark("mhc_ms")
     best = lab0.copy()
     hist = [(0, best_phi)]
 
@@ -440,6 +484,7 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
         q0_loc = B.fix_q0_rows(q0_loc, n)      # the 1/sqrt(n) column uses the global n
     dq = float(np.sqrt(B.sync_scalars([B.diff2(Q1, q0_loc, c)])[0]))
     Q_loc = B.to_f32(Q1, c)
+    ph.mark("step1_ms")
     stop, converged, t, err, replays = "max_iterations", False, 1, None, 0
     kd = c - 1
     try:
@@ -460,15 +505,23 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
                         dq2_g = B.sync_scalars([B.diff2(Q64, prev, c)])[0]
                         Q_loc = B.to_f32(Q64, c)
                     dq = float(np.sqrt(dq2_g))
+                ph.mark("ortho_ms")
                 if kd < 1:
                     raise NetworkError("discretize expects an n x k block with k >= 1")
-                lab_loc, empties = discretize_dist(B, Q_loc, kd, plan)
+                if _replicated_disc(B, n, c):
+                    labels, empties = B.disc_replicated(Q_loc, plan.row_counts(), 1, kd)
+                else:
+                    lab_loc, empties = discretize_dist(B, Q_loc, kd, plan)
+                    labels = None
                 if empties > 0:
                     raise NetworkError("cannot repair empty clusters: no movable nodes")
-                labels = B.all_gather_labels(lab_loc, plan.row_counts())
+                if labels is None:
+                    labels = B.all_gather_labels(lab_loc, plan.row_counts())
                 if kd < k:                                     # k == n (engine.py:392-394)
                     raise NetworkError("the row-partitioned path needs k < n")
+                ph.mark("discretize_ms")
                 phi = mhc(labels, "f32")
+                ph.mark("mhc_ms")
                 hist.append((t, phi))
                 if phi < best_phi:
                     best_phi, best = phi, labels.copy()
@@ -495,7 +548,9 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
                 break
     except NetworkError as exc:
         err, stop = str(exc), "error"
-    return DistResult(best, best_phi, t, stop, hist, converged, err, replays)
+    ph.mark("ortho_ms")
+    return DistResult(best, best_phi, t, stop, hist, converged, err, replays,
+                      {k_: round(v, 1) for k_, v in ph.t.items()} if ph.on else None)
 
 
 # ----------------------------------------------------------------------------
@@ -648,6 +703,9 @@ class CudaBackend:
         if self.world > 1:
             self.dist.all_reduce(t, group=self.group)
         return t.cpu().numpy()
+
+    def synchronize(self):
+        self.torch.cuda.synchronize()
 
     def all_reduce_dev(self, t):
         """In-place sum over ranks of a device tensor (no host round trip)."""
@@ -987,6 +1045,21 @@ class CudaBackend:
         lab = torch.as_tensor(labels_loc, device="cuda").long()
         vals = F[torch.arange(F.shape[0], device="cuda"), lab].double()
         return (vals * torch.as_tensor(yhat, device="cuda")[lab]).sum()
+
+    def disc_replicated(self, Q_loc, counts, col0, k):
+        """discretize (engine.py:183-263) on every rank from the gathered
+        block with the single-GPU device kernels: the same input on every
+        rank gives the same labels (deterministic kernels).  Returns (host
+        labels, empties left)."""
+        torch = self.torch
+        from .engine import DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, _discretize_device
+        q = self.all_gather_rows(Q_loc, counts).contiguous()
+        n = q.shape[0]
+        labels = torch.empty(n, dtype=torch.int32, device="cuda")
+        info = torch.zeros(8 + 2 * DISCRETIZE_MAX_ITER + 2 * k * k, dtype=torch.float64,
+                           device="cuda")
+        _discretize_device(q, col0, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, labels, info)
+        return labels.cpu().numpy().astype(np.int64), int(info[4].item())
 
     # --- row-partitioned discretisation primitives (discretize_dist)
     def disc_prepare(self, Q_loc, col0, k):

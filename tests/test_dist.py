@@ -387,11 +387,15 @@ def _golden_net(z, m, i):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["replicated", "partitioned"])
 @pytest.mark.parametrize("i", range(6))
-def test_cuda_backend_world1_matches_reference(golden_runs, i):
+def test_cuda_backend_world1_matches_reference(golden_runs, i, mode, monkeypatch):
+    """Both discretisation modes of the row-partitioned path: the replicated
+    device kernels and the partitioned rounds (dist.DISC_MODE)."""
     from sklearn.metrics import adjusted_rand_score
     z, meta = golden_runs
     net, params = _golden_net(z, meta[i], i)
+    monkeypatch.setattr(D, "DISC_MODE", mode)
     res = D.run_ancka_dist(net, params, D.CudaBackend(), early_stop=meta[i]["early_stop"])
     assert res.error is None, res.error
     a = adjusted_rand_score(z[f"r{i}_labels"], res.labels)
