@@ -295,7 +295,12 @@ def kernel_rooflines(prep, res, inst, hbm, bf16):
     knn_ms = time_events(lambda: knn_search_exact_device(prep.x_dev, K, integer=prep.x_level), 1)
     flops = 2.0 * n * n * d
     fp8 = prep.x_level == 2
-    peak = 4500.0 if fp8 else bf16
+    fp8_peak, fp8_src = 4500.0, "nominal dense fp8 4.5 PFLOP/s (B200_PROFILING.md)"
+    tp = ROOT / "profiles" / "r02" / "tc_peak.json"
+    if tp.exists():   # tools/tc_peak.py: tcgen05 kind::f8f6f4 M=128 N=256, operands in smem
+        fp8_peak = json.loads(tp.read_text())["fp8_e4m3"]["tflops"]
+        fp8_src = "measured tcgen05 kind::f8f6f4 microbenchmark (profiles/r02/tc_peak.json)"
+    peak = fp8_peak if fp8 else bf16
     out["knn"] = {"kernel": ("knn_tc_kernel (tcgen05 kind::f8f6f4, exact integer)" if fp8 else
                              "knn_real16_kernel (tcgen05 kind::f16, fp16 operands) + certified f64 re-rank"),
                   "bound": "tensor", "achieved": round(flops / (knn_ms * 1e-3) / 1e12, 1),
@@ -303,8 +308,7 @@ def kernel_rooflines(prep, res, inst, hbm, bf16):
                   "frac": round(flops / (knn_ms * 1e-3) / 1e12 / peak, 4),
                   "algorithmic": f"2*n^2*d = {flops:.4e} FLOP per search",
                   "duration_ms": round(knn_ms, 2),
-                  "peak_source": ("nominal dense fp8 4.5 PFLOP/s (B200_PROFILING.md; no measured fp8 peak)"
-                                  if fp8 else "measured bf16 burst (MEASURED_PEAKS.json)"),
+                  "peak_source": (fp8_src if fp8 else "measured bf16 burst (MEASURED_PEAKS.json)"),
                   "timed": "whole ancka_knn_exact call (all kernels of the search)"}
     if not fp8:
         # the bound that binds: every score leaves TMEM once through tcgen05.ld

@@ -435,6 +435,14 @@ int ancka_ivf_kmeans_update(const float* S, int64_t lds, const int32_t* arows, i
                             unsigned long long* sums, int32_t* counts, float* C, int64_t ldc,
                             float* bias, ancka_stream_t stream);
 
+/* Tensor-pipe peak microbenchmark (roofline denominators, no reference
+ * counterpart): back-to-back tcgen05.mma M=128 N=256 on every SM, fmt 0 =
+ * kind::f8f6f4 e4m3, 1 = kind::f16 bf16; returns the FLOP issued and the
+ * event-timed milliseconds (synchronises `stream`); cycles: 148 per-CTA
+ * clock64 spans (device memory). */
+int ancka_tc_peak(int32_t fmt, int32_t iters, double* flop_out, double* ms_out,
+                  long long* cycles, ancka_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif
