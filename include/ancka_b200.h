@@ -435,6 +435,38 @@ int ancka_ivf_kmeans_update(const float* S, int64_t lds, const int32_t* arows, i
                             unsigned long long* sums, int32_t* counts, float* C, int64_t ldc,
                             float* bias, ancka_stream_t stream);
 
+/* Row-partitioned discretisation (engine.py:162-263 over a rank's rows
+ * [row0, row0 + n_loc) of n_glob, 8 < k <= 192; dist.py drives it): the
+ * device-driven rounds of the wide path with the caller's collectives in
+ * between -- `tots` (k k + k u64 fixed-point cluster totals) is summed over
+ * the ranks after each ANCKA_DW_ROUND_LOCAL (and ANCKA_DW_SNAP), `rvec`
+ * (k f64) after each ANCKA_DW_PROTO_PICK, and `locbest` (3 f64: value,
+ * global row, label) is all-gathered after each ANCKA_DW_PROTO_PASS /
+ * ANCKA_DW_RESEED_CAND (the pass's into the buffer passed to PICK).  Labels (local rows) land in `labels`; `info` as ancka_discretize. */
+enum {
+  ANCKA_DW_START = 0,          /* a = run (0 identity, 1 prototype start) */
+  ANCKA_DW_ROUND_LOCAL = 1,    /* a = run, b = first round: score, totals, snap into tots */
+  ANCKA_DW_SNAP = 2,           /* the rank's current totals into tots */
+  ANCKA_DW_CHECK_EMPTY = 3,    /* a = run: an empty global cluster sets the pause flag */
+  ANCKA_DW_POLAR = 4,          /* a = run: rotation step from the global totals */
+  ANCKA_DW_CLEAR_PAUSE = 5,
+  ANCKA_DW_MARGINS = 6,        /* exact second-best scores of the local rows (reseed) */
+  ANCKA_DW_MOVE_ROW = 7,       /* a = target cluster, b = local row */
+  ANCKA_DW_PROTO_PASS = 8,     /* b = column j >= 1: running sums, local first minimum */
+  ANCKA_DW_PROTO_PICK = 9,     /* a = world, b = forced global row or -1, ptr = gathered pairs */
+  ANCKA_DW_PROTO_SETCOL = 10,  /* b = column j: R[:, j] = rvec */
+  ANCKA_DW_FLAGS = 11,         /* ptr = device int32[6]: done0, done1, pause, empties0, empties1, it */
+  ANCKA_DW_FINISH = 12,        /* winner's labels into `labels`; releases the host state */
+  ANCKA_DW_RESEED_CAND = 13    /* ptr = device int64[k] global sizes: locbest = (margin, row, label) */
+};
+size_t ancka_discw_dist_workspace_size(int64_t n_loc, int32_t k);
+int ancka_discw_dist_init(const float* Q, int64_t ldq, int64_t col0, int64_t n_loc, int64_t n_glob,
+                          int64_t row0, int32_t k, int32_t max_iter, double tol, uint64_t* tots,
+                          double* rvec, double* locbest, int32_t* labels, double* info, void* ws,
+                          size_t workspace_bytes, ancka_stream_t stream);
+int ancka_discw_dist_op(void* ws, int32_t op, int64_t a, int64_t b, const void* ptr,
+                        ancka_stream_t stream);
+
 /* Tensor-pipe peak microbenchmark (roofline denominators, no reference
  * counterpart): back-to-back tcgen05.mma M=128 N=256 on every SM, fmt 0 =
  * kind::f8f6f4 e4m3, 1 = kind::f16 bf16; returns the FLOP issued and the

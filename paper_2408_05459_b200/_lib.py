@@ -91,6 +91,11 @@ _SIGS = {
     "ancka_ivf_kmeans_update": (c_int32, [c_void_p, c_int64, c_void_p, c_int64, c_void_p,
                                           c_int32, c_int64, c_void_p, c_void_p, c_void_p,
                                           c_int64, c_void_p, c_void_p]),
+    "ancka_discw_dist_workspace_size": (c_size_t, [c_int64, c_int32]),
+    "ancka_discw_dist_init": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_int64,
+                                        c_int32, c_int32, c_double, c_void_p, c_void_p, c_void_p,
+                                        c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ancka_discw_dist_op": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
     "ancka_tc_peak": (c_int32, [c_int32, c_int32, ctypes.POINTER(c_double),
                                 ctypes.POINTER(c_double), c_void_p, c_void_p]),
     "ancka_knn_merge_lists": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,

@@ -54,6 +54,8 @@ struct Ctl {
   double obj_prev;
   double obj_last[2];
   double cdrift;    // cumulative rotation drift of the current start (row keys)
+  int pause;        // row-partitioned mode: an empty cluster awaits the host reseed
+  int pad2_;
 };
 
 struct Params {
@@ -80,9 +82,26 @@ struct Params {
   int32_t* rid;                // n: rows due for scoring this round
   Ctl* ctl;
   double* info;
+  // row-partitioned mode (dist.py): this rank holds global rows
+  // [row0, row0 + n) of n_glob; `tots` receives the rank's current totals
+  // and, after the caller's sum all-reduce, holds the global totals the
+  // polar factor reads.  Single GPU: tots == nullptr, n_glob == n.
+  int64_t n_glob, row0;
+  unsigned long long* tots;
+  double* rvec;                // k: a prototype row, summed over ranks by the caller
+  double* locbest;             // 2: this rank's (value, global row) of a prototype pass
 };
 
 __device__ __forceinline__ int ld_vol(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
+
+__device__ __forceinline__ bool stopped(const Params& p, int run) {
+  return ld_vol(&p.ctl->done[run]) || ld_vol(&p.ctl->pause);
+}
+// totals the rotation step reads: the global ones in the row-partitioned mode
+__device__ __forceinline__ const unsigned long long* tot_glob(const Params& p, int gr) {
+  return p.tots ? p.tots : p.tot + (size_t)(gr % 3) * (p.k * p.k + p.k);
+}
+
 
 __device__ __forceinline__ void mma_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
@@ -244,7 +263,7 @@ __global__ void dw_identity(Params p) {
 // row): key = C0 + m / 2.  The first round of a start scores every row, and
 // so does a round where most rows are due.
 __global__ void dw_list(Params p, int run) {
-  if (ld_vol(&p.ctl->done[run])) return;
+  if (stopped(p, run)) return;
   if (ld_vol(&p.ctl->it) == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl->nlist = -1;
     return;
@@ -264,7 +283,7 @@ __global__ void dw_list(Params p, int run) {
 
 template <int NBMAX>
 __global__ void __launch_bounds__(kT, 1) dw_score(Params p, int run, int first) {
-  if (ld_vol(&p.ctl->done[run])) return;
+  if (stopped(p, run)) return;
   extern __shared__ uint4 sRf[];
   const int k = p.k, kq = p.kq, ks16 = kq / 16, nb8 = p.nb8;
   for (int e = threadIdx.x; e < ks16 * nb8 * 32; e += kT) sRf[e] = p.Rfrag[e];
@@ -409,7 +428,7 @@ __device__ __forceinline__ bool full_recount(const Params& p, int first) {
 }
 
 __global__ void dw_carry(Params p, int run, int first) {
-  if (ld_vol(&p.ctl->done[run])) return;
+  if (stopped(p, run)) return;
   const int ne = p.k * p.k + p.k, gr = ld_vol(&p.ctl->gr);
   unsigned long long* dst = p.tot + (size_t)(gr % 3) * ne;
   const unsigned long long* prev = p.tot + (size_t)((gr + 2) % 3) * ne;
@@ -420,7 +439,7 @@ __global__ void dw_carry(Params p, int run, int first) {
 
 // grid (row blocks, ceil(k / 32)): warp per row, lane per column
 __global__ void __launch_bounds__(kT) dw_full(Params p, int run, int first) {
-  if (ld_vol(&p.ctl->done[run]) || !full_recount(p, first)) return;
+  if (stopped(p, run) || !full_recount(p, first)) return;
   extern __shared__ unsigned sacc[];          // k x 32 cells (lo, hi) + k counts
   const int k = p.k, kq = p.kq, ne = k * k + k;
   unsigned* cnt = sacc + (size_t)k * 64;
@@ -453,7 +472,7 @@ __global__ void __launch_bounds__(kT) dw_full(Params p, int run, int first) {
 
 // warp per moved row
 __global__ void __launch_bounds__(kT) dw_delta(Params p, int run, int first) {
-  if (ld_vol(&p.ctl->done[run]) || full_recount(p, first)) return;
+  if (stopped(p, run) || full_recount(p, first)) return;
   const int k = p.k, kq = p.kq, ne = k * k + k, nchg = ld_vol(&p.ctl->nchg);
   unsigned long long* dst = p.tot + (size_t)(ld_vol(&p.ctl->gr) % 3) * ne;
   const int lane = threadIdx.x & 31;
@@ -529,7 +548,7 @@ __device__ void grid_best(const double* part, int nb, bool want_max, double* sv,
 // (cluster size >= 2) with the largest margin moves there; its fixed-point
 // delta goes to the totals (owner CTA).
 __global__ void __launch_bounds__(kT, 1) dw_reseed(Params p, int run) {
-  if (ld_vol(&p.ctl->done[run])) return;
+  if (stopped(p, run)) return;
   const int k = p.k, kq = p.kq, ne = k * k + k;
   if (k < 2) return;
   cg::grid_group grid = cg::this_grid();
@@ -631,7 +650,7 @@ __device__ __forceinline__ double tile_mm(const double* A, const double* B, int 
 }
 
 __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
-  if (ld_vol(&p.ctl->done[run])) return;
+  if (stopped(p, run)) return;
   cg::grid_group grid = cg::this_grid();
   const int k = p.k, kq = p.kq, kk = k * k, ne = kk + k, tpr = kq / 16;
   const int by = blockIdx.x / tpr, bx = blockIdx.x % tpr, G = gridDim.x;
@@ -648,7 +667,7 @@ __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
   __shared__ long long ssz[kMaxK];
   const int it = ld_vol(&p.ctl->it), gr = ld_vol(&p.ctl->gr), qs = ld_vol(&p.ctl->qs);
   const double obj_prev = *reinterpret_cast<volatile double*>(&p.ctl->obj_prev);
-  const unsigned long long* tot = p.tot + (size_t)(gr % 3) * ne;
+  const unsigned long long* tot = tot_glob(p, gr);
   for (int c = threadIdx.x; c < k; c += kT) ssz[c] = (long long)__ldcg(tot + kk + c);
   __syncthreads();
   // M = Y~^T Q~: cluster sums / sizes (engine.py:196-200), kq x kq zero padded
@@ -744,7 +763,7 @@ __global__ void __launch_bounds__(kT, 1) dw_polar(Params p, int run) {
   grid.sync();
   double ssum = 0.0;
   for (int c2 = 0; c2 < G; ++c2) ssum += __ldcg(ptr + c2);
-  const double obj = (double)p.n - 2.0 * ssum;
+  const double obj = (double)p.n_glob - 2.0 * ssum;
   const bool conv = it >= 1 && fabs(obj - obj_prev) < p.tol;
   const bool done = conv || it + 1 == p.max_iter;
   // rotation drift max_j ||X_j - R_j|| (row keys): per-CTA column partials
@@ -910,6 +929,215 @@ __global__ void dw_finish(Params p, const int32_t* labels_run0, int32_t* labels_
       labels_out[i] = labels_run0[i];
 }
 
+// ------------------------------------------------- row-partitioned mode ---
+// (dist.py: the rank's rows are [row0, row0 + n) of n_glob; the caller sums
+// `tots` and the prototype buffers over ranks between these kernels)
+
+// this rank's current totals -> tots (the caller all-reduces them in place)
+__global__ void dw_snap(Params p) {
+  const int ne = p.k * p.k + p.k;
+  const unsigned long long* src = p.tot + (size_t)(ld_vol(&p.ctl->gr) % 3) * ne;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x)
+    p.tots[e] = src[e];
+}
+
+// an empty cluster in the global totals pauses the rounds for the host reseed
+__global__ void dw_check_empty(Params p, int run) {
+  if (stopped(p, run) || p.k < 2) return;
+  __shared__ int e;
+  if (threadIdx.x == 0) e = 0;
+  __syncthreads();
+  for (int c = threadIdx.x; c < p.k; c += blockDim.x)
+    if (p.tots[(size_t)p.k * p.k + c] == 0ull) atomicAdd(&e, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && e) p.ctl->pause = 1;
+}
+
+// exact second-best scores of the local rows (the reseed's margins)
+__global__ void dw_margins(Params p) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = warp; i < p.n; i += nw) {
+    int lab;
+    double sec;
+    exact_row(p, i, lab, sec);
+    if ((threadIdx.x & 31) == 0) p.margin[i] = sec;
+  }
+}
+
+// move local row i to cluster c: labels and the rank's current totals
+__global__ void dw_move_row(Params p, int64_t i, int c) {
+  const int k = p.k, ne = k * k + k;
+  unsigned long long* tot = p.tot + (size_t)(ld_vol(&p.ctl->gr) % 3) * ne;
+  const int old = p.labels[i];
+  __syncthreads();
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const long long fx = fx_round(p.qn[i * p.kq + j], p.fx_shift);
+    if (fx) {
+      atomicAdd(tot + (size_t)c * k + j, (unsigned long long)fx);
+      atomicAdd(tot + (size_t)old * k + j, (unsigned long long)(-fx));
+    }
+  }
+  if (threadIdx.x == 0) {
+    atomicAdd(tot + (size_t)k * k + c, 1ull);
+    atomicAdd(tot + (size_t)k * k + old, ~0ull);
+    p.labels[i] = c;
+    p.key[i] = -INFINITY;
+  }
+}
+
+// prototype start, pass j (j >= 1): acc_i += |q~_i . R[:, j-1]| over the
+// local rows with dw_proto's arithmetic, then per-CTA first minima
+__global__ void __launch_bounds__(kTP) dw_ppass(Params p, int j) {
+  const int k = p.k;
+  __shared__ double r[kMaxK];
+  __shared__ double sv[kTP];
+  __shared__ long long si[kTP];
+  for (int l = threadIdx.x; l < k; l += kTP) r[l] = p.R64[(size_t)l * k + j - 1];
+  __syncthreads();
+  const int64_t rpb = ceil_div(p.n, gridDim.x);
+  const int64_t a0 = (int64_t)blockIdx.x * rpb, a1 = lmin(p.n, a0 + rpb);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double best = 0.0;
+  long long bi = -1;
+  for (int64_t base = a0 + (int64_t)warp * 32; base < a1; base += (int64_t)(kTP / 32) * 32) {
+    const int64_t me = base + lane;
+    const bool ok = me < a1;
+    const double acc0 = ok ? p.proto_acc[me] : 0.0;
+    const double inv = ok ? p.qinv[me] : 0.0;
+    const int nr = (int)lmin(32, a1 - base);
+    double mine = 0.0;
+    for (int rr = 0; rr < nr; rr += 4) {
+      double d[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float* src = p.Q + (base + min(rr + u, nr - 1)) * p.ldq + p.col0;
+        d[u] = 0.0;
+#pragma unroll
+        for (int m = 0; m < kMaxK / 32; ++m) {
+          const int l = lane + 32 * m;
+          if (l < k) d[u] = fma((double)src[l], r[l], d[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        d[u] = warp_sum(d[u]);
+        if (lane == rr + u) mine = d[u];
+      }
+    }
+    if (ok) {
+      const double av = acc0 + fabs(mine * inv);
+      p.proto_acc[me] = av;
+      if (bi < 0 || av < best) { best = av; bi = me; }
+    }
+  }
+  double v;
+  long long idx;
+  block_best<kTP>(best, bi, false, sv, si, v, idx);
+  if (threadIdx.x == 0) {
+    p.part[2 * blockIdx.x] = v;
+    p.part[2 * blockIdx.x + 1] = (double)idx;
+  }
+}
+
+// the rank's first minimum -> locbest = (value, global row) (row -1: none)
+__global__ void __launch_bounds__(kTP) dw_pbest(Params p, int nb) {
+  __shared__ double sv[kTP];
+  __shared__ long long si[kTP];
+  double v;
+  long long idx;
+  grid_best<kTP>(p.part, nb, false, sv, si, v, idx);
+  if (threadIdx.x == 0) {
+    p.locbest[0] = idx < 0 ? INFINITY : v;
+    p.locbest[1] = idx < 0 ? -1.0 : (double)(p.row0 + idx);
+    p.locbest[2] = 0.0;
+  }
+}
+
+// reseed candidates (_reseed_empty_columns, engine.py:162-180): per CTA the
+// movable local row (cluster size >= 2 by the caller's global sizes) with
+// the largest exact second-best score, ties to the smaller row
+__global__ void __launch_bounds__(kT) dw_rcand(Params p, const long long* sizes) {
+  __shared__ double sv[kT];
+  __shared__ long long si[kT];
+  const int64_t rpb = ceil_div(p.n, gridDim.x);
+  const int64_t a0 = (int64_t)blockIdx.x * rpb, a1 = lmin(p.n, a0 + rpb);
+  double best = 0.0;
+  long long bi = -1;
+  for (int64_t i = a0 + threadIdx.x; i < a1; i += kT) {
+    if (sizes[p.labels[i]] >= 2) {
+      const double m = p.margin[i];
+      if (bi < 0 || m > best) { best = m; bi = i; }
+    }
+  }
+  double v;
+  long long idx;
+  block_best(best, bi, true, sv, si, v, idx);
+  if (threadIdx.x == 0) {
+    p.part[2 * blockIdx.x] = v;
+    p.part[2 * blockIdx.x + 1] = (double)idx;
+  }
+}
+
+__global__ void __launch_bounds__(kT) dw_rbest(Params p, int nb) {
+  __shared__ double sv[kT];
+  __shared__ long long si[kT];
+  double v;
+  long long idx;
+  grid_best(p.part, nb, true, sv, si, v, idx);
+  if (threadIdx.x == 0) {
+    p.locbest[0] = idx < 0 ? -INFINITY : v;
+    p.locbest[1] = idx < 0 ? -1.0 : (double)(p.row0 + idx);
+    p.locbest[2] = idx < 0 ? -1.0 : (double)p.labels[idx];
+  }
+}
+
+// global first minimum over the ranks' (value, row) pairs (or the forced
+// row); its owner writes q~ of that row (f64) into rvec, the others zeros
+__global__ void dw_ppick(Params p, const double* gath, int world, long long force) {
+  __shared__ long long g;
+  if (threadIdx.x == 0) {
+    long long gi = force;
+    if (gi < 0) {
+      double bv = 0.0;
+      for (int w = 0; w < world; ++w) {
+        const double v = gath[3 * w];
+        const long long i = (long long)gath[3 * w + 1];
+        if (i < 0) continue;
+        if (gi < 0 || v < bv || (v == bv && i < gi)) { bv = v; gi = i; }
+      }
+      if (gi < 0) gi = 0;
+    }
+    g = gi;
+  }
+  __syncthreads();
+  const long long li = g - p.row0;
+  const bool own = li >= 0 && li < p.n;
+  for (int l = threadIdx.x; l < p.k; l += blockDim.x)
+    p.rvec[l] = own ? (double)p.Q[li * p.ldq + p.col0 + l] * p.qinv[li] : 0.0;
+}
+
+__global__ void dw_psetcol(Params p, int j) {
+  for (int l = threadIdx.x; l < p.k; l += blockDim.x) p.R64[(size_t)l * p.k + j] = p.rvec[l];
+}
+
+__global__ void dw_pfrag(Params p) {
+  const int ne = (p.kq / 16) * p.nb8 * 32;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ne; e += gridDim.x * blockDim.x)
+    p.Rfrag[e] = frag_entry(e, p.k, p.nb8, [&](int l, int jj) { return p.R64[(size_t)l * p.k + jj]; });
+}
+
+// ctl -> flags[0..5] = done[0], done[1], pause, empties[0], empties[1], it
+__global__ void dw_flags(Params p, int32_t* out) {
+  if (threadIdx.x == 0) {
+    out[0] = p.ctl->done[0];
+    out[1] = p.ctl->done[1];
+    out[2] = p.ctl->pause;
+    out[3] = p.ctl->empties[0];
+    out[4] = p.ctl->empties[1];
+    out[5] = p.ctl->it;
+  }
+}
+
 }  // namespace dw
 
 // ------------------------------------------------------------------ host ---
@@ -997,6 +1225,7 @@ int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k,
   carve_wide(cv, n, k, p, &labels_run0);
   ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize: workspace too small");
   p.Q = Q; p.ldq = ldq; p.col0 = col0; p.n = n; p.k = k;
+  p.n_glob = n;
   p.kq = (k + 15) & ~15;
   p.nb8 = p.kq / 8;
   p.max_iter = max_iter;
@@ -1058,3 +1287,195 @@ int discretize_wide(const float* Q, int64_t ldq, int64_t col0, int64_t n, int k,
 }
 
 }  // namespace ancka
+
+// --------------------------------------- row-partitioned mode: C entries ---
+// One discretisation of a rank's rows, driven by the caller (dist.py) with
+// collectives between the phases; the Params of a workspace are kept on the
+// host, keyed by the workspace pointer, between ancka_discw_dist_init and
+// the ANCKA_DW_FINISH op.
+#include <mutex>
+#include <unordered_map>
+
+namespace {
+struct DistDisc {
+  ancka::dw::Params p;
+  int32_t* labels_out;   // the caller's buffer: labels of the prototype start, then the winner
+  int32_t* labels_run0;  // workspace: labels of the identity start
+  int run;
+};
+std::mutex g_dw_mu;
+std::unordered_map<const void*, DistDisc> g_dw;
+}  // namespace
+
+using namespace ancka;
+
+extern "C" size_t ancka_discw_dist_workspace_size(int64_t n_loc, int32_t k) {
+  return discretize_wide_workspace(n_loc < 1 ? 1 : n_loc, k);
+}
+
+extern "C" int ancka_discw_dist_init(const float* Q, int64_t ldq, int64_t col0, int64_t n_loc,
+                                     int64_t n_glob, int64_t row0, int32_t k, int32_t max_iter,
+                                     double tol, uint64_t* tots, double* rvec, double* locbest,
+                                     int32_t* labels, double* info, void* ws, size_t wsb,
+                                     ancka_stream_t stream) {
+  ANCKA_REQUIRE(k > 8 && k <= dw::kMaxK, ANCKA_ERR_UNSUPPORTED,
+                "discretize (row-partitioned): 8 < k <= %d (got %d)", dw::kMaxK, k);
+  ANCKA_REQUIRE(n_loc >= 1 && n_glob >= n_loc && n_glob < (1ll << 31), ANCKA_ERR_ARG,
+                "discretize (row-partitioned): n_loc=%lld n_glob=%lld", (long long)n_loc,
+                (long long)n_glob);
+  cudaStream_t st = as_stream(stream);
+  Carver cv(ws, wsb);
+  dw::Params p{};
+  int32_t* labels_run0 = nullptr;
+  carve_wide(cv, n_loc, k, p, &labels_run0);
+  ANCKA_REQUIRE(cv.ok(), ANCKA_ERR_ARG, "discretize (row-partitioned): workspace too small");
+  p.Q = Q; p.ldq = ldq; p.col0 = col0; p.n = n_loc; p.k = k;
+  p.n_glob = n_glob;
+  p.row0 = row0;
+  p.kq = (k + 15) & ~15;
+  p.nb8 = p.kq / 8;
+  p.max_iter = max_iter;
+  p.tol = tol;
+  p.cert = (float)(2.0 * (3.0 * p.kq * 0x1p-24 + 3.0 * 0x1p-22 + 0x1p-24));
+  {
+    int bits = 1;                       // sums over all n_glob rows fit 63 bits
+    while ((1ll << bits) <= n_glob) ++bits;
+    p.fx_shift = 61 - bits;
+    p.fx_scale = std::ldexp(1.0, p.fx_shift);
+  }
+  p.info = info;
+  p.tots = reinterpret_cast<unsigned long long*>(tots);
+  p.rvec = rvec;
+  p.locbest = locbest;
+  p.labels = labels_run0;
+  ANCKA_CUDA(cudaMemsetAsync(info, 0, sizeof(double) * (8 + 2 * (size_t)max_iter + 2 * (size_t)k * k), st));
+  ANCKA_CUDA(cudaMemsetAsync(p.ctl, 0, sizeof(dw::Ctl), st));
+  ANCKA_CUDA(cudaMemsetAsync(p.tot, 0, sizeof(unsigned long long) * 3 * ((size_t)k * k + k), st));
+  ANCKA_CUDA(cudaMemsetAsync(p.W, 0, sizeof(double) * 5 * (size_t)p.kq * p.kq, st));
+  dw::dw_normalize<<<(int)std::min<int64_t>(ceil_div(n_loc * 32, dw::kT), 8 * kNumSMs), dw::kT, 0, st>>>(p);
+  ANCKA_LAUNCHED();
+  std::lock_guard<std::mutex> lk(g_dw_mu);
+  g_dw[ws] = DistDisc{p, labels, labels_run0, 0};
+  return ANCKA_OK;
+}
+
+extern "C" int ancka_discw_dist_op(void* ws, int32_t op, int64_t a, int64_t b, const void* ptr,
+                                   ancka_stream_t stream) {
+  DistDisc d;
+  {
+    std::lock_guard<std::mutex> lk(g_dw_mu);
+    auto it = g_dw.find(ws);
+    ANCKA_REQUIRE(it != g_dw.end(), ANCKA_ERR_ARG, "discretize (row-partitioned): unknown workspace");
+    if (op == ANCKA_DW_START) it->second.run = (int)a;
+    d = it->second;
+  }
+  dw::Params p = d.p;
+  int32_t* labels_out = d.labels_out;
+  int32_t* labels_run0 = d.labels_run0;
+  cudaStream_t st = as_stream(stream);
+  const int run = (int)a;
+  p.labels = d.run == 1 ? labels_out : labels_run0;
+  switch (op) {
+    case ANCKA_DW_START:             // a = run: 0 identity, 1 prototype setup
+      if (run == 0) {
+        dw::dw_identity<<<8, dw::kT, 0, st>>>(p);
+        ANCKA_LAUNCHED();
+      } else {
+        ANCKA_CUDA(cudaMemcpyAsync(labels_out, labels_run0, sizeof(int32_t) * p.n, cudaMemcpyDeviceToDevice, st));
+        ANCKA_CUDA(cudaMemsetAsync(&p.ctl->it, 0, sizeof(int), st));
+        ANCKA_CUDA(cudaMemsetAsync(&p.ctl->cdrift, 0, sizeof(double), st));
+        ANCKA_CUDA(cudaMemsetAsync(p.proto_acc, 0, sizeof(double) * p.n, st));
+      }
+      return ANCKA_OK;
+    case ANCKA_DW_ROUND_LOCAL: {     // a = run, b = first round of the call
+      dw::dw_list<<<2 * kNumSMs, dw::kT, 0, st>>>(p, run);
+      ANCKA_LAUNCHED();
+      ANCKA_TRY(p.nb8 <= 16 ? launch_score<16>(p, run, (int)b, st) : launch_score<24>(p, run, (int)b, st));
+      const int ne = p.k * p.k + p.k;
+      dw::dw_carry<<<(int)std::min<int64_t>(ceil_div(ne, dw::kT), 2 * kNumSMs), dw::kT, 0, st>>>(p, run, (int)b);
+      ANCKA_LAUNCHED();
+      {
+        const size_t smem = sizeof(unsigned) * ((size_t)p.k * 64 + p.k);
+        ANCKA_CUDA(cudaFuncSetAttribute(dw::dw_full, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const int gx = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(p.n, 4096), kNumSMs));
+        dw::dw_full<<<dim3(gx, (p.k + 31) / 32), dw::kT, smem, st>>>(p, run, (int)b);
+        ANCKA_LAUNCHED();
+      }
+      dw::dw_delta<<<2 * kNumSMs, dw::kT, 0, st>>>(p, run, (int)b);
+      ANCKA_LAUNCHED();
+      dw::dw_snap<<<(int)std::min<int64_t>(ceil_div(ne, dw::kT), 2 * kNumSMs), dw::kT, 0, st>>>(p);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    }
+    case ANCKA_DW_SNAP: {
+      const int ne = p.k * p.k + p.k;
+      dw::dw_snap<<<(int)std::min<int64_t>(ceil_div(ne, dw::kT), 2 * kNumSMs), dw::kT, 0, st>>>(p);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    }
+    case ANCKA_DW_CHECK_EMPTY:
+      dw::dw_check_empty<<<1, dw::kT, 0, st>>>(p, run);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    case ANCKA_DW_POLAR: {
+      void* args[] = {&p, const_cast<int*>(&run)};
+      ANCKA_TRY(coop((const void*)dw::dw_polar, (p.kq / 16) * (p.kq / 16), 0, st, args));
+      return ANCKA_OK;
+    }
+    case ANCKA_DW_CLEAR_PAUSE:
+      ANCKA_CUDA(cudaMemsetAsync(&p.ctl->pause, 0, sizeof(int), st));
+      return ANCKA_OK;
+    case ANCKA_DW_MARGINS:
+      dw::dw_margins<<<(int)std::min<int64_t>(ceil_div(p.n * 32, dw::kT), 8 * kNumSMs), dw::kT, 0, st>>>(p);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    case ANCKA_DW_MOVE_ROW:          // a = target cluster, b = local row
+      dw::dw_move_row<<<1, dw::kT, 0, st>>>(p, b, (int)a);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    case ANCKA_DW_RESEED_CAND: {     // ptr = device int64[k] global cluster sizes
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(p.n, dw::kT)));
+      dw::dw_rcand<<<nb, dw::kT, 0, st>>>(p, static_cast<const long long*>(ptr));
+      ANCKA_LAUNCHED();
+      dw::dw_rbest<<<1, dw::kT, 0, st>>>(p, nb);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    }
+    case ANCKA_DW_PROTO_PASS: {      // a = run (1), b = column j >= 1
+      const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(kNumSMs, ceil_div(p.n, dw::kTP)));
+      dw::dw_ppass<<<nb, dw::kTP, 0, st>>>(p, (int)b);
+      ANCKA_LAUNCHED();
+      dw::dw_pbest<<<1, dw::kTP, 0, st>>>(p, nb);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    }
+    case ANCKA_DW_PROTO_PICK:        // b = forced global row (>= 0) or -1; ptr = gathered pairs, a = world
+      dw::dw_ppick<<<1, 256, 0, st>>>(p, static_cast<const double*>(ptr), run, (long long)b);
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    case ANCKA_DW_PROTO_SETCOL:      // b = column
+      dw::dw_psetcol<<<1, 256, 0, st>>>(p, (int)b);
+      ANCKA_LAUNCHED();
+      if (b == p.k - 1 || p.k == 1) {
+        dw::dw_pfrag<<<8, dw::kT, 0, st>>>(p);
+        ANCKA_LAUNCHED();
+      }
+      return ANCKA_OK;
+    case ANCKA_DW_FLAGS:             // ptr = int32[6] device
+      dw::dw_flags<<<1, 32, 0, st>>>(p, static_cast<int32_t*>(const_cast<void*>(ptr)));
+      ANCKA_LAUNCHED();
+      return ANCKA_OK;
+    case ANCKA_DW_FINISH: {          // labels_out <- winner; forget the workspace
+      dw::dw_finish<<<(int)std::min<int64_t>(ceil_div(p.n, dw::kT), 2 * kNumSMs), dw::kT, 0, st>>>(
+          p, labels_run0, labels_out);
+      ANCKA_LAUNCHED();
+      std::lock_guard<std::mutex> lk(g_dw_mu);
+      g_dw.erase(ws);
+      return ANCKA_OK;
+    }
+    default:
+      break;
+  }
+  set_error("discretize (row-partitioned): unknown op %d", op);
+  return ANCKA_ERR_ARG;
+}

@@ -294,19 +294,32 @@ def discretize_dist(B, Q_loc, k: int, plan: Plan, max_iter: int = 100, tol: floa
     return B.disc_labels_host(res[3]), res[4]
 
 
+# ANCKA_DW_* ops of ancka_discw_dist_op (include/ancka_b200.h)
+(DW_START, DW_ROUND_LOCAL, DW_SNAP, DW_CHECK_EMPTY, DW_POLAR, DW_CLEAR_PAUSE, DW_MARGINS,
+ DW_MOVE_ROW, DW_PROTO_PASS, DW_PROTO_PICK, DW_PROTO_SETCOL, DW_FLAGS, DW_FINISH,
+ DW_RESEED_CAND) = range(14)
+
 #: discretisation mode of the row-partitioned path: "auto" replicates the
 #: device discretisation on every rank (the gathered n x c f32 block, the
 #: single-GPU kernels, no host round trips) when that block is at most
-#: DISC_REPLICATED_BYTES, else runs `discretize_dist`; "replicated" /
-#: "partitioned" force one of them
+#: DISC_REPLICATED_BYTES, else runs the device row-partitioned rounds
+#: (`CudaBackend.disc_partitioned`, 8 < k <= 192) or the host rounds
+#: (`discretize_dist`); "replicated" / "partitioned" / "host" force one
 DISC_MODE = "auto"
 DISC_REPLICATED_BYTES = 16 << 30
 
 
 def _replicated_disc(B, n: int, c: int) -> bool:
-    if not hasattr(B, "disc_replicated") or DISC_MODE == "partitioned":
+    if not hasattr(B, "disc_replicated") or DISC_MODE in ("partitioned", "host"):
         return False
     return DISC_MODE == "replicated" or n * ((c + 3) // 4 * 4) * 4 <= DISC_REPLICATED_BYTES
+
+
+def _device_partitioned_disc(B, k: int, plan) -> bool:
+    """The device row-partitioned rounds cover 8 < k <= 192 with every rank
+    holding rows; otherwise (and with DISC_MODE "host") the host rounds."""
+    return (hasattr(B, "disc_partitioned") and DISC_MODE != "host" and 8 < k <= 192
+            and int(np.min(plan.row_counts())) >= 1)
 
 
 def _centers(deg: np.ndarray, k: int) -> np.ndarray:
@@ -510,6 +523,9 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
                     raise NetworkError("discretize expects an n x k block with k >= 1")
                 if _replicated_disc(B, n, c):
                     labels, empties = B.disc_replicated(Q_loc, plan.row_counts(), 1, kd)
+                elif _device_partitioned_disc(B, kd, plan):
+                    lab_loc, empties = B.disc_partitioned(Q_loc, plan, 1, kd)
+                    labels = None
                 else:
                     lab_loc, empties = discretize_dist(B, Q_loc, kd, plan)
                     labels = None
@@ -1060,6 +1076,106 @@ class CudaBackend:
                            device="cuda")
         _discretize_device(q, col0, k, DISCRETIZE_MAX_ITER, DISCRETIZE_TOL, labels, info)
         return labels.cpu().numpy().astype(np.int64), int(info[4].item())
+
+    def disc_partitioned(self, Q_loc, plan, col0, k):
+        """discretize (engine.py:162-263) over this rank's rows on the device
+        (`disc_wide_dev.cu`, ANCKA_DW_* ops): the wide path's rounds with the
+        cluster totals summed over the ranks by an integer all-reduce, the
+        rotation replicated, the prototype passes as (value, row) all-gathers
+        plus one summed row, and the empty-cluster reseed as a host loop of
+        global (margin, row) choices -- no host SVD, one read-back per 8
+        rounds.  8 < k <= 192.  Returns (local labels as numpy, empties)."""
+        torch, _lib = self.torch, self._lib
+        from .engine import DISCRETIZE_MAX_ITER as MI, DISCRETIZE_TOL as TOL
+        n_loc, world = int(Q_loc.shape[0]), self.world
+        dv = "cuda"
+        tots = torch.zeros(k * k + k, dtype=torch.int64, device=dv)
+        rvec = torch.zeros(k, dtype=torch.float64, device=dv)
+        loc = torch.zeros(3, dtype=torch.float64, device=dv)
+        gath = torch.zeros(3 * world, dtype=torch.float64, device=dv)
+        labels = torch.empty(n_loc, dtype=torch.int32, device=dv)
+        info = torch.zeros(8 + 2 * MI + 2 * k * k, dtype=torch.float64, device=dv)
+        flags = torch.zeros(6, dtype=torch.int32, device=dv)
+        sizes_dev = torch.zeros(k, dtype=torch.int64, device=dv)
+        ws = torch.empty(int(_lib.load().ancka_discw_dist_workspace_size(n_loc, k)),
+                         dtype=torch.uint8, device=dv)
+        st = _lib.stream()
+        _lib.call("ancka_discw_dist_init", Q_loc.data_ptr(), Q_loc.stride(0), col0, n_loc, plan.n,
+                  plan.r0, k, MI, float(TOL), tots.data_ptr(), rvec.data_ptr(), loc.data_ptr(),
+                  labels.data_ptr(), info.data_ptr(), ws.data_ptr(), ws.numel(), st)
+
+        def op(code, a=0, b=0, ptr=None):
+            _lib.call("ancka_discw_dist_op", ws.data_ptr(), code, a, b, ptr, st)
+
+        def summed(t):
+            if world > 1:
+                self.dist.all_reduce(t, group=self.group)
+
+        def gathered():
+            if world == 1:
+                gath.copy_(loc)
+            else:
+                self.dist.all_gather_into_tensor(gath, loc, group=self.group) if self._nccl else \
+                    gath.copy_(torch.cat(self._gather_list(loc)))
+
+        def reseed():
+            sizes = tots[k * k:].cpu().numpy().astype(np.int64)
+            op(DW_MARGINS)
+            for c in np.flatnonzero(sizes == 0):
+                sizes_dev.copy_(torch.from_numpy(sizes))
+                op(DW_RESEED_CAND, 0, 0, sizes_dev.data_ptr())
+                gathered()
+                g = gath.view(world, 3).cpu().numpy()
+                ok = g[:, 1] >= 0
+                if not ok.any():
+                    break                               # no movable node left
+                cand = g[ok]
+                w = np.lexsort((cand[:, 1], -cand[:, 0]))[0]    # margin desc, row asc
+                row, old = int(cand[w, 1]), int(cand[w, 2])
+                if plan.r0 <= row < plan.r1:
+                    op(DW_MOVE_ROW, int(c), row - plan.r0)
+                sizes[old] -= 1
+                sizes[c] += 1
+            op(DW_SNAP)
+            summed(tots)
+
+        for run in (0, 1):
+            op(DW_START, run)
+            if run == 1:                                    # _prototype_rotation
+                op(DW_PROTO_PICK, world, 0, gath.data_ptr())
+                summed(rvec)
+                op(DW_PROTO_SETCOL, 1, 0)
+                for j in range(1, k):
+                    op(DW_PROTO_PASS, 1, j)
+                    gathered()
+                    op(DW_PROTO_PICK, world, -1, gath.data_ptr())
+                    summed(rvec)
+                    op(DW_PROTO_SETCOL, 1, j)
+            first = run == 0
+            while True:
+                for _ in range(8):
+                    op(DW_ROUND_LOCAL, run, int(first))
+                    first = False
+                    summed(tots)
+                    op(DW_CHECK_EMPTY, run)
+                    op(DW_POLAR, run)
+                op(DW_FLAGS, 0, 0, flags.data_ptr())
+                f = flags.cpu().numpy()
+                if f[2]:                                    # an empty cluster: reseed, then rotate
+                    reseed()
+                    op(DW_CLEAR_PAUSE)
+                    op(DW_POLAR, run)
+                    continue
+                if f[run]:
+                    break
+        op(DW_FINISH)
+        inf = info[:8].cpu().numpy()
+        return labels.cpu().numpy().astype(np.int64), int(inf[4])
+
+    def _gather_list(self, t):
+        out = [self.torch.empty_like(t) for _ in range(self.world)]
+        self.dist.all_gather(out, t, group=self.group)
+        return out
 
     # --- row-partitioned discretisation primitives (discretize_dist)
     def disc_prepare(self, Q_loc, col0, k):

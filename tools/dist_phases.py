@@ -26,6 +26,7 @@ net = (ancka.AttributedNetwork.hypergraph if inst.kind == "hypergraph"
        else ancka.AttributedNetwork.graph)(inst.structure, inst.X)
 params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
 D.DIST_TIMING = True
+D.DISC_MODE = os.environ.get("DISC_MODE", "auto")
 B = D.CudaBackend()
 for rep in range(2):
     res = D.run_ancka_dist(net, params, B)
