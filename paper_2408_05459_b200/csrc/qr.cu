@@ -543,14 +543,24 @@ cgs2_fused_kernel(double* __restrict__ Z, int64_t n, int64_t ld, int c,
       // j products of a 32-row batch are summed across the warp per column
       for (int l = threadIdx.x; l < kCgsWarps * kMaxC; l += blockDim.x) (&wpart[0][0])[l] = 0.0;
       __syncthreads();
-      for (int64_t i0 = r0 + (int64_t)w * 32; i0 < r1; i0 += 32 * kCgsWarps) {
-        const int64_t i = i0 + lane;
-        const bool ok = i < r1;
-        const double zj = ok ? Z[i * ld + j] : 0.0;
-        for (int l = 0; l < j; ++l) {
-          double v = ok ? Z[i * ld + l] * zj : 0.0;
-          v = warp_sum(v);
-          if (lane == 0) wpart[w][l] += v;
+      // per-thread partial dots in registers over 16-column blocks, one warp
+      // reduction per block (fixed order: rows by thread, lanes by tree)
+      for (int lb = 0; lb < j; lb += 16) {
+        double acc[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc[u] = 0.0;
+        for (int64_t i = r0 + (int64_t)w * 32 + lane; i < r1; i += 32 * kCgsWarps) {
+          const double* row = Z + i * ld;
+          const double zj = row[j];
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (lb + u < j) acc[u] = fma(row[lb + u], zj, acc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          if (lb + u >= j) break;
+          const double v = warp_sum(acc[u]);
+          if (lane == 0) wpart[w][lb + u] = v;
         }
       }
       reduce_cols(j, part);
