@@ -336,6 +336,7 @@ __device__ __forceinline__ bool before(float s, int id, float s2, int id2) {
 // 32-dim chunk; key chunks [KC][QS]; per-tile candidate buffers (scores that
 // beat the query's current K2-th entry) and the per-query top-K2 lists.
 constexpr int QS = TQ + 4;  // row stride: float4-aligned, 4-way store conflicts at worst
+constexpr int SKC = 16;     // dims per staged key chunk (3 CTAs per SM at d = 100)
 constexpr int kResD = 256;
 
 struct SearchSmem {
@@ -344,12 +345,12 @@ struct SearchSmem {
 
 __host__ __device__ inline SearchSmem search_layout(int64_t dp, int K2) {
   SearchSmem L;
-  const int64_t dq = dp <= kResD ? dp : 2 * KC;
+  const int64_t dq = dp <= kResD ? dp : 2 * SKC;
   size_t o = 0;
   L.qs = o; o += align_dev(sizeof(float) * (size_t)dq * QS);
-  L.ks = o; o += align_dev(sizeof(float) * (size_t)2 * KC * QS);
+  L.ks = o; o += align_dev(sizeof(float) * (size_t)2 * SKC * QS);
   L.cbs = o; o += align_dev(sizeof(float) * (size_t)TQ * TK);
-  L.cbi = o; o += align_dev(sizeof(int32_t) * (size_t)TQ * TK);
+  L.cbi = o; o += align_dev(sizeof(uint8_t) * (size_t)TQ * TK);
   L.ts = o; o += align_dev(sizeof(float) * (size_t)TQ * K2);
   L.ti = o; o += align_dev(sizeof(int32_t) * (size_t)TQ * K2);
   L.ints = o; o += align_dev(sizeof(int32_t) * (6 * TQ + TK));
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
   float* qs = reinterpret_cast<float*>(smem_raw + L.qs);
   float* ks = reinterpret_cast<float*>(smem_raw + L.ks);
   float* cbs = reinterpret_cast<float*>(smem_raw + L.cbs);
-  int32_t* cbi = reinterpret_cast<int32_t*>(smem_raw + L.cbi);
+  uint8_t* cbi = smem_raw + L.cbi;             // key slot within the tile
   float* ts = reinterpret_cast<float*>(smem_raw + L.ts);
   int32_t* ti = reinterpret_cast<int32_t*>(smem_raw + L.ti);
   int32_t* qrow = reinterpret_cast<int32_t*>(smem_raw + L.ints);
@@ -420,14 +421,14 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
       __syncthreads();
       // key chunks (and query chunks when not resident) are fetched into
       // registers one chunk ahead and stored to the other shared buffer
-      constexpr int NF = TK * (KC / 4) / kT;  // float4 per thread per chunk
+      constexpr int NF = TK * (SKC / 4) / kT;  // float4 per thread per chunk
       float4 pk[NF], pq[NF];
       auto fetch = [&](int64_t d0) {
-        const int kc = (int)lmin(KC, dp - d0);
+        const int kc = (int)lmin(SKC, dp - d0);
 #pragma unroll
         for (int u = 0; u < NF; ++u) {
           const int f = tid + u * kT;
-          const int r = f / (KC / 4), c4 = (f % (KC / 4)) * 4;
+          const int r = f / (SKC / 4), c4 = (f % (SKC / 4)) * 4;
           pk[u] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (kid[r] >= 0 && c4 < kc)
             pk[u] = *reinterpret_cast<const float4*>(p.xn + (int64_t)kid[r] * dp + d0 + c4);
@@ -439,12 +440,12 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
         }
       };
       auto stash = [&](int buf) {
-        float* kb_ = ks + buf * KC * QS;
-        float* qb_ = qs + buf * KC * QS;
+        float* kb_ = ks + buf * SKC * QS;
+        float* qb_ = qs + buf * SKC * QS;
 #pragma unroll
         for (int u = 0; u < NF; ++u) {
           const int f = tid + u * kT;
-          const int r = f / (KC / 4), c4 = (f % (KC / 4)) * 4;
+          const int r = f / (SKC / 4), c4 = (f % (SKC / 4)) * 4;
           kb_[(c4 + 0) * QS + r] = pk[u].x;
           kb_[(c4 + 1) * QS + r] = pk[u].y;
           kb_[(c4 + 2) * QS + r] = pk[u].z;
@@ -461,12 +462,12 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
       stash(0);
       __syncthreads();
       int buf = 0;
-      for (int64_t d0 = 0; d0 < dp; d0 += KC) {
-        const int kc = (int)lmin(KC, dp - d0);
-        const bool more = d0 + KC < dp;
-        if (more) fetch(d0 + KC);
-        const float* qb = RES ? qs + d0 * QS : qs + buf * KC * QS;
-        const float* kb_ = ks + buf * KC * QS;
+      for (int64_t d0 = 0; d0 < dp; d0 += SKC) {
+        const int kc = (int)lmin(SKC, dp - d0);
+        const bool more = d0 + SKC < dp;
+        if (more) fetch(d0 + SKC);
+        const float* qb = RES ? qs + d0 * QS : qs + buf * SKC * QS;
+        const float* kb_ = ks + buf * SKC * QS;
 #pragma unroll 4
         for (int kk = 0; kk < kc; ++kk) {
           const float4 a = *reinterpret_cast<const float4*>(qb + kk * QS + ty * 4);
@@ -498,7 +499,7 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
           if (sv > g_ && (full ? before(sv, id, ts_, ti_) : sv > ts_)) {
             const int slot = atomicAdd(&ccnt[q], 1);
             cbs[q * TK + slot] = sv;
-            cbi[q * TK + slot] = id;
+            cbi[q * TK + slot] = (uint8_t)(tx * 4 + j);
           }
         }
       }
@@ -514,7 +515,7 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
           int ei = lane < cnt ? ti[q * p.K2 + lane] : 0x7fffffff;
           for (int u = 0; u < nb; ++u) {
             const float sv = cbs[q * TK + u];
-            const int id = cbi[q * TK + u];
+            const int id = kid[cbi[q * TK + u]];
             const float ls_ = __shfl_sync(0xffffffffu, es, p.K2 - 1);
             const int li_ = __shfl_sync(0xffffffffu, ei, p.K2 - 1);
             if (cnt == p.K2 && !before(sv, id, ls_, li_)) continue;
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
         const int nb = ccnt[q];
         for (int u = 0; u < nb; ++u) {
           const float sv = cbs[q * TK + u];
-          const int id = cbi[q * TK + u];
+          const int id = kid[cbi[q * TK + u]];
           if (cnt == p.K2 && !before(sv, id, ls[cnt - 1], li[cnt - 1])) continue;
           int pos = cnt < p.K2 ? cnt++ : p.K2 - 1;
           while (pos > 0 && before(sv, id, ls[pos - 1], li[pos - 1])) {
