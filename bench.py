@@ -350,6 +350,17 @@ def kernel_rooflines(prep, res, inst, hbm, bf16):
                    "gather_note": "SURVEY.md §8(d) gather model: every gathered row from HBM; "
                                   "above the HBM peak = the gathers hit L2 (rows grouped by cluster)",
                    "duration_ms": round(apply_ms, 3), "peak_source": "measured HBM copy"}
+    tp = ROOT / "profiles" / "r02" / "tc_peak.json"
+    if tp.exists() and "l2_read_gather192" in json.loads(tp.read_text()):
+        l2 = json.loads(tp.read_text())["l2_read_gather192"]["tb_per_s"] * 1e3
+        g = b_op / (apply_ms * 1e-3) / 1e9
+        out["spmm"]["l2_gather"] = {
+            "bound": "l2", "achieved": round(g, 1), "peak": round(l2, 1), "unit": "GB/s",
+            "frac": round(g / l2, 4),
+            "peak_source": "measured L2 read of hashed 192-byte rows, ld.global.cg "
+                           "(tools/tc_peak.py, profiles/r02/tc_peak.json)",
+            "note": "gather-model bytes (every gathered row counted; L1 hits included) over the "
+                    "measured L2 gather bandwidth: the apply's actual bound"}
     stats = torch.tensor([0.0, 1.0, 0.0, 0.0] + [0.0] * 12, dtype=torch.float64, device="cuda")
     ws = WORKSPACE.get("orth", _lib.load().ancka_orth_workspace_size(s32, c))
     G = torch.empty(c * (c + 1) // 2, dtype=torch.float64, device="cuda")

@@ -474,6 +474,12 @@ int ancka_discw_dist_op(void* ws, int32_t op, int64_t a, int64_t b, const void* 
  * clock64 spans (device memory). */
 int ancka_tc_peak(int32_t fmt, int32_t iters, double* flop_out, double* ms_out,
                   long long* cycles, ancka_stream_t stream);
+/* L2 read-bandwidth microbenchmark (the SpMM gather's denominator): `iters`
+ * sweeps over a rows x row_floats f32 table that fits L2, rows read in order
+ * (gather = 0) or hashed (gather = 1, the SpMM's row gathers). */
+int ancka_l2_read(const float* table, int64_t rows, int32_t row_floats, int32_t iters,
+                  int32_t gather, float* sink, double* bytes_out, double* ms_out,
+                  ancka_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -96,6 +96,8 @@ _SIGS = {
                                         c_int32, c_int32, c_double, c_void_p, c_void_p, c_void_p,
                                         c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
     "ancka_discw_dist_op": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p]),
+    "ancka_l2_read": (c_int32, [c_void_p, c_int64, c_int32, c_int32, c_int32, c_void_p,
+                                ctypes.POINTER(c_double), ctypes.POINTER(c_double), c_void_p]),
     "ancka_tc_peak": (c_int32, [c_int32, c_int32, ctypes.POINTER(c_double),
                                 ctypes.POINTER(c_double), c_void_p, c_void_p]),
     "ancka_knn_merge_lists": (c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_int64, c_int32,

@@ -88,3 +88,72 @@ extern "C" int ancka_tc_peak(int32_t fmt, int32_t iters, double* flop_out, doubl
   *ms_out = ms;
   return ANCKA_OK;
 }
+
+// L2 read-bandwidth microbenchmark (the SpMM gather's roofline): every
+// thread walks rows of a table that fits L2, reading one float4 per row
+// chunk -- sequential (row = thread index stride) or gathered (row =
+// hash of the index, rows of `row_floats` floats as the SpMM's Q rows).
+namespace ancka {
+namespace {
+__global__ void __launch_bounds__(256) l2_read_kernel(const float4* __restrict__ tab, int64_t rows,
+                                                      int row_f4, int iters, int gather,
+                                                      float* __restrict__ sink) {
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t nthreads = gridDim.x * blockDim.x;
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t total = (uint32_t)(rows * row_f4);
+  const uint32_t mask = (uint32_t)rows - 1u;     // rows: a power of two
+  for (int it = 0; it < iters; ++it) {
+    uint32_t e = tid;
+    for (; e + 3 * nthreads < total; e += 4 * nthreads) {   // four loads in flight
+      float4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t ee = e + u * nthreads;
+        uint32_t r = ee / (uint32_t)row_f4;
+        const uint32_t c = ee - r * (uint32_t)row_f4;
+        if (gather) r = ((r + (uint32_t)it) * 2654435761u) & mask;
+        v[u] = __ldcg(tab + (size_t)r * row_f4 + c);           // L2, not L1
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; acc.z += v[u].z; acc.w += v[u].w; }
+    }
+    for (; e < total; e += nthreads) {
+      uint32_t r = e / (uint32_t)row_f4;
+      const uint32_t c = e - r * (uint32_t)row_f4;
+      if (gather) r = ((r + (uint32_t)it) * 2654435761u) & mask;
+      const float4 v = __ldcg(tab + (size_t)r * row_f4 + c);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+  }
+  if (acc.x + acc.y + acc.z + acc.w == 1.2345f) sink[0] = acc.x;   // keep the loads
+}
+}  // namespace
+}  // namespace ancka
+
+/* L2 read bandwidth: bytes read and event-timed ms for `iters` sweeps over a
+ * rows x row_floats f32 table (device memory, fits L2), sequential or
+ * gathered rows. */
+extern "C" int ancka_l2_read(const float* table, int64_t rows, int32_t row_floats, int32_t iters,
+                             int32_t gather, float* sink, double* bytes_out, double* ms_out,
+                             ancka_stream_t stream) {
+  ANCKA_REQUIRE(row_floats % 4 == 0 && rows > 0 && (rows & (rows - 1)) == 0, ANCKA_ERR_ARG,
+                "l2_read: row_floats a multiple of 4, rows a power of two");
+  cudaStream_t st = as_stream(stream);
+  cudaEvent_t a, b;
+  ANCKA_CUDA(cudaEventCreate(&a));
+  ANCKA_CUDA(cudaEventCreate(&b));
+  ANCKA_CUDA(cudaEventRecord(a, st));
+  l2_read_kernel<<<kNumSMs * 8, 256, 0, st>>>(reinterpret_cast<const float4*>(table), rows,
+                                             row_floats / 4, iters, gather, sink);
+  ANCKA_LAUNCHED();
+  ANCKA_CUDA(cudaEventRecord(b, st));
+  ANCKA_CUDA(cudaEventSynchronize(b));
+  float ms = 0.f;
+  ANCKA_CUDA(cudaEventElapsedTime(&ms, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *bytes_out = 4.0 * (double)rows * row_floats * iters;
+  *ms_out = ms;
+  return ANCKA_OK;
+}

@@ -30,5 +30,18 @@ for fmt, name in ((0, "fp8_e4m3"), (1, "bf16")):
     out[name] = {"tflops": round(best, 1), "sm_cycles_median": int(sorted(c)[74]),
                  "per_sm_flop_per_clk": round(2 * 128 * 256 * (32 if fmt == 0 else 16) * 4 *
                                               20000 / float(sorted(c)[74]), 1)}
+# L2 read bandwidth (ld.global.cg, L1 bypassed): 12.6 MB of 192-byte rows (an
+# Amazon2M cluster's rows of Q at c = 48), sequential and hashed-row gathers
+rows, rf = 65536, 48
+tab = torch.randn(rows * rf, device="cuda")
+sink = torch.zeros(1, device="cuda")
+for gather, name in ((0, "l2_read_seq"), (1, "l2_read_gather192")):
+    best = 0.0
+    for _ in range(3):
+        b, ms = ctypes.c_double(), ctypes.c_double()
+        _lib.call("ancka_l2_read", tab.data_ptr(), rows, rf, 200, gather, sink.data_ptr(),
+                  ctypes.byref(b), ctypes.byref(ms), _lib.stream())
+        best = max(best, b.value / (ms.value * 1e-3) / 1e12)
+    out[name] = {"tb_per_s": round(best, 2), "table_mb": round(rows * rf * 4 / 1e6, 1)}
 print(json.dumps(out))
 (ROOT / "profiles" / "r02" / "tc_peak.json").write_text(json.dumps(out, indent=1) + "\n")
