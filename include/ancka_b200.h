@@ -418,7 +418,21 @@ int ancka_ivf_search(const float* xn, int64_t dp, const int32_t* perm, const int
  * appended (global ids) to flagged / *nflag. */
 int ancka_ivf_merge(const float* xn, int64_t dp, int64_t q0, int64_t m, int32_t nprobe, int32_t K2,
                     int32_t K, const float* part_s, const int32_t* part_i, float err, int32_t* ids,
-                    double* scores, int32_t* flagged, int32_t* nflag, ancka_stream_t stream);
+                    double* scores, int32_t* flagged, int32_t* nflag, const float* lres,
+                    const uint32_t* lmax_bits, ancka_stream_t stream);
+/* The scan on the tensor cores: h = fp16(xn) (n x dh, dh = ceil16(d) <= 256,
+ * entries below 2^-14 flushed) with per-row residual norms lres = ||xn - h||
+ * and their maximum (u32 bits of a non-negative float); ancka_ivf_search_tc
+ * scores each (list, pair tile) with mma.sync m16n8k16 (f32 accumulation),
+ * floors and certificate at e_q = l_q + l_max + l_q l_max + acc_err (pass
+ * lres / lmax_bits to ancka_ivf_merge; NULL there for the f32 scan). */
+int ancka_ivf_half_prep(const float* xn, int64_t n, int64_t dp, void* h, int64_t dh, float* lres,
+                        uint32_t* lmax_bits, ancka_stream_t stream);
+int ancka_ivf_search_tc(const void* h, int64_t dh, const float* lres, const uint32_t* lmax_bits,
+                        const int32_t* perm, const int64_t* list_ptr, const int64_t* pair_ptr,
+                        const int32_t* pair_ent, const int64_t* tile_ptr, int32_t* counter,
+                        int32_t nlist, int32_t nprobe, int64_t q0, int32_t K2, float acc_err,
+                        float* part_s, int32_t* part_i, uint32_t* qthr, ancka_stream_t stream);
 /* Exact top-K (f64 accumulation) for the listed rows against their probe
  * lists (probes != NULL) or all keys (the recall audit, _exact_rows_for,
  * knn.py:225-233).  compact: output row b instead of rows[b] - q0. */

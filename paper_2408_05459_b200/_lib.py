@@ -84,7 +84,13 @@ _SIGS = {
                                    ctypes.c_float, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ancka_ivf_merge": (c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32,
                                   c_void_p, c_void_p, ctypes.c_float, c_void_p, c_void_p,
-                                  c_void_p, c_void_p, c_void_p]),
+                                  c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ancka_ivf_half_prep": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
+                                      c_void_p, c_void_p]),
+    "ancka_ivf_search_tc": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
+                                      c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
+                                      c_int64, c_int32, ctypes.c_float, c_void_p, c_void_p,
+                                      c_void_p, c_void_p]),
     "ancka_ivf_rows_exact": (c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_int64, c_void_p,
                                        c_int32, c_int64, c_void_p, c_void_p, c_int32, c_void_p,
                                        c_void_p, c_int32, c_void_p]),

@@ -37,6 +37,7 @@
 // Every selection is a total order (score desc, id asc), so the results do
 // not depend on the order of entries inside a list or on CTA scheduling.
 #include <cfloat>
+#include <cuda_fp16.h>
 
 #include "common.cuh"
 
@@ -576,6 +577,247 @@ __global__ void __launch_bounds__(kT) ivf_search(SearchP p) {
   }
 }
 
+// ------------------------------------------------ tensor-core scan (fp16) ---
+// The same (list, 64-pair) tiles scored on the tensor cores: h = fp16(xn)
+// (entries below 2^-14 flushed), one mma.sync.m16n8k16 product per 16 dims
+// with f32 accumulation.  |h_q.h_j - xn_q.xn_j| <= l_q + l_j + l_q l_j + acc
+// with l the per-row residual ||xn - h|| (ivf_half_prep), so a row's
+// floor and the merge's certificate use e_q = l_q + l_max + l_q l_max + e.
+__global__ void ivf_half_prep(const float* __restrict__ xn, int64_t n, int64_t dp, __half* __restrict__ h,
+                              int64_t dh, float* __restrict__ lres, unsigned* __restrict__ lmax_bits) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n;
+       r += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    double s2 = 0.0;
+    for (int64_t c = lane; c < dh; c += 32) {
+      const float v = c < dp ? xn[r * dp + c] : 0.f;
+      __half hv = __float2half_rn(v);
+      if (fabsf(v) < 0x1p-14f) hv = __float2half_rn(0.f);
+      h[r * dh + c] = hv;
+      const double d = (double)v - (double)__half2float(hv);
+      s2 = fma(d, d, s2);
+    }
+    s2 = warp_sum(s2);
+    if (lane == 0) {
+      const float l = (float)(sqrt(s2) * (1.0 + 1e-6)) + 1e-30f;   // rounded up
+      lres[r] = l;
+      atomicMax(lmax_bits, __float_as_uint(l));                    // l >= 0: bit order = value order
+    }
+  }
+}
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+struct SearchTcP {
+  SearchP s;
+  const __half* h;   // n x dh
+  int64_t dh;
+  const float* lres;
+  const unsigned* lmax_bits;
+  float acc_err;
+};
+
+constexpr int kMaxDh = 256;
+
+__host__ __device__ inline size_t search_tc_smem(int64_t dh, int K2) {
+  const size_t hs = (size_t)(dh + 8);                      // halves per staged row
+  return align_dev(2 * hs * TQ) + 2 * align_dev(2 * hs * TK) + align_dev(4 * (size_t)TQ * TK) +
+         align_dev((size_t)TQ * TK) + align_dev(4 * (size_t)TQ * K2) + align_dev(4 * (size_t)TQ * K2) +
+         align_dev(4 * (7 * (size_t)TQ + TK));
+}
+
+__global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
+  const SearchP& p = P.s;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int hs = (int)P.dh + 8;
+  unsigned char* o = smem_raw;
+  __half* qh = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TQ);
+  __half* kh[2];
+  kh[0] = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TK);
+  kh[1] = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TK);
+  float* cbs = reinterpret_cast<float*>(o); o += align_dev(4 * (size_t)TQ * TK);
+  uint8_t* cbi = o; o += align_dev((size_t)TQ * TK);
+  float* ts = reinterpret_cast<float*>(o); o += align_dev(4 * (size_t)TQ * p.K2);
+  int32_t* ti = reinterpret_cast<int32_t*>(o); o += align_dev(4 * (size_t)TQ * p.K2);
+  int32_t* qrow = reinterpret_cast<int32_t*>(o);
+  int32_t* qent = qrow + TQ;
+  int32_t* tn = qent + TQ;
+  int32_t* ccnt = tn + TQ;
+  float* thr = reinterpret_cast<float*>(ccnt + TQ);
+  float* gt = thr + TQ;
+  float* eq = gt + TQ;
+  int32_t* kid = reinterpret_cast<int32_t*>(eq + TQ);
+  __shared__ int s_work;
+  __shared__ int32_t kidn[TK];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wr = (warp & 3) * 16, wc = (warp >> 2) * 32;   // warp tile: 16 queries x 32 keys
+  const int64_t total = p.tile_ptr[p.nlist];
+  const int nch = (int)(P.dh / 8);                          // 16-byte chunks per row
+  const float lmax = __uint_as_float(*P.lmax_bits);
+  auto stage_keys = [&](const int32_t* ids, int b) {
+    for (int e = tid; e < TK * nch; e += kT) {
+      const int r = e / nch, ch = e - r * nch;
+      const int32_t id = ids[r];
+      __half* dst = kh[b] + (size_t)r * hs + ch * 8;
+      if (id >= 0) {
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                     "l"(P.h + (int64_t)id * P.dh + ch * 8)
+                     : "memory");
+      } else {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  for (;;) {
+    if (tid == 0) s_work = atomicAdd(p.counter, 1);
+    __syncthreads();
+    const int64_t w = s_work;
+    if (w >= total) break;
+    int lo = 0, hi = p.nlist;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (p.tile_ptr[mid] <= w) lo = mid; else hi = mid;
+    }
+    const int c = lo;
+    const int64_t pb = p.pair_ptr[c] + (w - p.tile_ptr[c]) * TQ;
+    const int nq = (int)lmin(TQ, p.pair_ptr[c + 1] - pb);
+    const int64_t kb = p.list_ptr[c], ke = p.list_ptr[c + 1];
+    if (tid < TQ) {
+      const int32_t e = tid < nq ? p.pair_ent[pb + tid] : -1;
+      qent[tid] = e;
+      const int32_t qr = e >= 0 ? (int32_t)(p.q0 + e / p.nprobe) : -1;
+      qrow[tid] = qr;
+      tn[tid] = 0;
+      ccnt[tid] = 0;
+      const float lq = qr >= 0 ? P.lres[qr] : 0.f;
+      const float e_q = lq + lmax + lq * lmax + P.acc_err;
+      eq[tid] = e_q;
+      thr[tid] = -e_q;
+      gt[tid] = e >= 0 ? fmaxf(-e_q, key_ord(p.qthr[e / p.nprobe])) : -e_q;
+    }
+    if (tid < TK) kid[tid] = kb + tid < ke ? p.perm[kb + tid] : -1;
+    __syncthreads();
+    for (int e = tid; e < TQ * nch; e += kT) {             // the tile's queries (fp16)
+      const int r = e / nch, ch = e - r * nch;
+      const int32_t qr = qrow[r];
+      *reinterpret_cast<uint4*>(qh + (size_t)r * hs + ch * 8) =
+          qr >= 0 ? *reinterpret_cast<const uint4*>(P.h + (int64_t)qr * P.dh + ch * 8) : make_uint4(0u, 0u, 0u, 0u);
+    }
+    stage_keys(kid, 0);
+    int buf = 0;
+    for (int64_t k0 = kb; k0 < ke; k0 += TK, buf ^= 1) {
+      const int nk = (int)lmin(TK, ke - k0);
+      const bool more = k0 + TK < ke;
+      if (more) {
+        if (tid < TK) kidn[tid] = k0 + TK + tid < ke ? p.perm[k0 + TK + tid] : -1;
+        __syncthreads();
+        stage_keys(kidn, buf ^ 1);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      }
+      __syncthreads();
+      float acc[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[nt][u] = 0.f;
+      const __half* kb_ = kh[buf];
+      for (int k = 0; k < (int)P.dh; k += 16) {
+        uint32_t a[4];
+        const __half* qa = qh + (size_t)(wr + g) * hs + k + 2 * t4;
+        a[0] = *reinterpret_cast<const uint32_t*>(qa);
+        a[1] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs);
+        a[2] = *reinterpret_cast<const uint32_t*>(qa + 8);
+        a[3] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs + 8);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          const __half* kbp = kb_ + (size_t)(wc + nt * 8 + g) * hs + k + 2 * t4;
+          mma16816(acc[nt], a, *reinterpret_cast<const uint32_t*>(kbp),
+                   *reinterpret_cast<const uint32_t*>(kbp + 8));
+        }
+      }
+      // filter: lane holds rows wr+g, wr+g+8 and keys wc + 8 nt + 2 t4 + {0,1}
+#pragma unroll
+      for (int hrow = 0; hrow < 2; ++hrow) {
+        const int q = wr + g + 8 * hrow;
+        if (q >= nq) continue;
+        const bool full = tn[q] == p.K2;
+        const float ts_ = thr[q], g_ = gt[q];
+        const int ti_ = full ? ti[q * p.K2 + p.K2 - 1] : 0;
+        const int me = qrow[q];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int slot = wc + nt * 8 + 2 * t4 + u;
+            const int id = kid[slot];
+            const float sv = acc[nt][2 * hrow + u];
+            if (slot >= nk || id < 0 || id == me) continue;
+            if (sv > g_ && (full ? before(sv, id, ts_, ti_) : sv > ts_)) {
+              const int pos = atomicAdd(&ccnt[q], 1);
+              cbs[q * TK + pos] = sv;
+              cbi[q * TK + pos] = (uint8_t)slot;
+            }
+          }
+      }
+      __syncthreads();
+      // warp-cooperative insertion (K2 <= 32: lane t holds entry t)
+      for (int q = warp; q < nq; q += kT / 32) {
+        const int nb = ccnt[q];
+        if (nb == 0) continue;
+        int cnt = tn[q];
+        float es = lane < cnt ? ts[q * p.K2 + lane] : -FLT_MAX;
+        int ei = lane < cnt ? ti[q * p.K2 + lane] : 0x7fffffff;
+        for (int u = 0; u < nb; ++u) {
+          const float sv = cbs[q * TK + u];
+          const int id = kid[cbi[q * TK + u]];
+          const float ls_ = __shfl_sync(0xffffffffu, es, p.K2 - 1);
+          const int li_ = __shfl_sync(0xffffffffu, ei, p.K2 - 1);
+          if (cnt == p.K2 && !before(sv, id, ls_, li_)) continue;
+          const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && before(es, ei, sv, id)));
+          const float us = __shfl_up_sync(0xffffffffu, es, 1);
+          const int ui = __shfl_up_sync(0xffffffffu, ei, 1);
+          if (lane > pos) { es = us; ei = ui; }
+          if (lane == pos) { es = sv; ei = id; }
+          cnt = min(cnt + 1, p.K2);
+        }
+        if (lane < cnt) {
+          ts[q * p.K2 + lane] = es;
+          ti[q * p.K2 + lane] = ei;
+        }
+        const float last = __shfl_sync(0xffffffffu, es, p.K2 - 1);
+        if (lane == 0) {
+          tn[q] = cnt;
+          ccnt[q] = 0;
+          thr[q] = cnt == p.K2 ? last : -eq[q];
+        }
+      }
+      __syncthreads();
+      if (more && tid < TK) kid[tid] = kidn[tid];
+    }
+    if (tid < nq) {
+      const int r = tid;
+      const int64_t base = (int64_t)qent[r] * p.K2;
+      const int cnt = tn[r];
+      for (int t = 0; t < p.K2; ++t) {
+        p.part_s[base + t] = t < cnt ? ts[r * p.K2 + t] : -FLT_MAX;
+        p.part_i[base + t] = t < cnt ? ti[r * p.K2 + t] : -1;
+      }
+      if (cnt == p.K2) atomicMax(p.qthr + qent[r] / p.nprobe, ord_key(ts[r * p.K2 + p.K2 - 1]));
+    }
+    __syncthreads();
+  }
+}
+
 // ----------------------------------------------------------------- merge ---
 struct MergeP {
   const float* xn;
@@ -589,6 +831,8 @@ struct MergeP {
   double* scores;
   int32_t* flagged;  // global row ids of uncertified rows
   int32_t* nflag;
+  const float* lres;  // fp16 scan: per-row residual norms (e_q = l_q + l_max + l_q l_max + e)
+  const unsigned* lmax_bits;
 };
 
 constexpr int kMergeWarps = 8;
@@ -663,7 +907,10 @@ __global__ void __launch_bounds__(32 * kMergeWarps) ivf_merge(MergeP p) {
       // certificate: everything not kept scored (f32) <= the K2-th kept
       // f32 score, so its exact value is <= that + e
       const float last = cnt == p.K2 ? ws[p.K2 - 1] : -FLT_MAX;
-      const double bound = (double)last + (double)p.e;
+      const double lmax = p.lres ? (double)__uint_as_float(*p.lmax_bits) : 0.0;
+      const double eq = p.lres ? (double)p.lres[gq] + lmax + (double)p.lres[gq] * lmax + p.e
+                               : (double)p.e;
+      const double bound = (double)last + eq;
       int npos = 0, nabove = 0;
       for (int t = 0; t < cnt; ++t) {
         if (wd[t] > 0.0) ++npos;
@@ -962,15 +1209,57 @@ extern "C" int ancka_ivf_search(const float* xn, int64_t dp, const int32_t* perm
   return ANCKA_OK;
 }
 
+extern "C" int ancka_ivf_half_prep(const float* xn, int64_t n, int64_t dp, void* h, int64_t dh,
+                                   float* lres, uint32_t* lmax_bits, ancka_stream_t stream) {
+  ANCKA_REQUIRE(dh % 16 == 0 && dh >= dp, ANCKA_ERR_ARG, "ivf_half_prep: dh=%lld", (long long)dh);
+  cudaStream_t st = as_stream(stream);
+  ANCKA_CUDA(cudaMemsetAsync(lmax_bits, 0, sizeof(uint32_t), st));
+  if (n == 0) return ANCKA_OK;
+  ivf_half_prep<<<grid_for(n * 32, kT), kT, 0, st>>>(xn, n, dp, static_cast<__half*>(h), dh, lres,
+                                                    reinterpret_cast<unsigned*>(lmax_bits));
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+extern "C" int ancka_ivf_search_tc(const void* h, int64_t dh, const float* lres,
+                                   const uint32_t* lmax_bits, const int32_t* perm,
+                                   const int64_t* list_ptr, const int64_t* pair_ptr,
+                                   const int32_t* pair_ent, const int64_t* tile_ptr, int32_t* counter,
+                                   int32_t nlist, int32_t nprobe, int64_t q0, int32_t K2, float acc_err,
+                                   float* part_s, int32_t* part_i, uint32_t* qthr,
+                                   ancka_stream_t stream) {
+  ANCKA_REQUIRE(K2 >= 1 && K2 <= 32 && dh % 16 == 0 && dh <= kMaxDh, ANCKA_ERR_ARG,
+                "ivf_search_tc: K2=%d dh=%lld", K2, (long long)dh);
+  cudaStream_t st = as_stream(stream);
+  const size_t smem = search_tc_smem(dh, K2);
+  ANCKA_CUDA(cudaFuncSetAttribute(ivf_search_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  ANCKA_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), st));
+  int per_sm = 0;
+  ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ivf_search_tc, kT, smem));
+  SearchTcP P{};
+  P.s = SearchP{nullptr, 0, perm, list_ptr, pair_ptr, pair_ent, tile_ptr, counter, nlist, nprobe, q0, K2,
+                0.f, part_s, part_i, qthr};
+  P.h = static_cast<const __half*>(h);
+  P.dh = dh;
+  P.lres = lres;
+  P.lmax_bits = reinterpret_cast<const unsigned*>(lmax_bits);
+  P.acc_err = acc_err;
+  ivf_search_tc<<<kNumSMs * std::max(1, per_sm), kT, smem, st>>>(P);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
 extern "C" int ancka_ivf_merge(const float* xn, int64_t dp, int64_t q0, int64_t m, int32_t nprobe,
                                int32_t K2, int32_t K, const float* part_s, const int32_t* part_i,
                                float err, int32_t* ids, double* scores, int32_t* flagged,
-                               int32_t* nflag, ancka_stream_t stream) {
+                               int32_t* nflag, const float* lres, const uint32_t* lmax_bits,
+                               ancka_stream_t stream) {
   ANCKA_REQUIRE(K >= 1 && K2 >= K && K2 <= 256, ANCKA_ERR_ARG, "ivf_merge: K=%d K2=%d", K, K2);
   if (m == 0) return ANCKA_OK;
   const size_t smem = align_dev((size_t)kMergeWarps * K2 * 8) + (size_t)kMergeWarps * K2 * 8;
   ANCKA_CUDA(cudaFuncSetAttribute(ivf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  MergeP p{xn, dp, q0, m, nprobe, K2, K, part_s, part_i, err, ids, scores, flagged, nflag};
+  MergeP p{xn, dp, q0, m, nprobe, K2, K, part_s, part_i, err, ids, scores, flagged, nflag, lres,
+           reinterpret_cast<const unsigned*>(lmax_bits)};
   ivf_merge<<<grid_for(m * 32, 32 * kMergeWarps, kNumSMs * 32), 32 * kMergeWarps, smem,
               as_stream(stream)>>>(p);
   ANCKA_LAUNCHED();

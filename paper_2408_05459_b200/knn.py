@@ -281,6 +281,9 @@ IVF_CHUNK_BYTES = 8 << 30
 #: extra slots per (query, list) partial list and in the merged list; the
 #: f64 re-rank certifies the top-K against the K2-th f32 score
 IVF_MARGIN = 8
+#: score the scan on the tensor cores (fp16 single product, certified; 32
+#: list slots) when d <= 256; False: the f32 SIMT scan
+IVF_TENSOR_CORES = True
 
 
 def ivf_defaults(n: int, nlist: int | None, nprobe: int | None):
@@ -378,13 +381,27 @@ def train_ivf_device(xn, nlist: int, seed: int, max_iter: int = 25):
 class IvfIndex:
     """Device inverted-file index: f32 normalised rows, centroids, and the
     lists as (list_ptr, perm) -- rows of list c are perm[list_ptr[c]:
-    list_ptr[c+1]] (knn.py:198-203)."""
+    list_ptr[c+1]] (knn.py:198-203).  `half()` adds the fp16 copy and the
+    per-row residual norms the tensor-core scan certifies with."""
 
     def __init__(self, xn, C, labels, list_ptr, perm, train_iters):
         self.xn, self.C, self.labels = xn, C, labels
         self.list_ptr, self.perm = list_ptr, perm
         self.nlist = C.shape[0]
         self.train_iters = train_iters
+        self._half = None
+
+    def half(self):
+        if self._half is None:
+            n, dp = self.xn.shape
+            dh = (dp + 15) // 16 * 16
+            h = torch.empty((n, dh), dtype=torch.float16, device=self.xn.device)
+            lres = torch.empty(n, dtype=torch.float32, device=self.xn.device)
+            lmax = torch.zeros(1, dtype=torch.int32, device=self.xn.device)
+            _lib.call("ancka_ivf_half_prep", self.xn.data_ptr(), n, dp, h.data_ptr(), dh,
+                      lres.data_ptr(), lmax.data_ptr(), _lib.stream())
+            self._half = (h, dh, lres, lmax)
+        return self._half
 
 
 def build_ivf_index(X, nlist: int, seed: int = 0, centroids=None) -> IvfIndex:
@@ -413,8 +430,12 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
     xn, nlist = index.xn, index.nlist
     n, dp = xn.shape
     dv = xn.device
-    K2 = min(K + IVF_MARGIN, 256)
+    tc = IVF_TENSOR_CORES and (dp + 15) // 16 * 16 <= 256 and K + IVF_MARGIN <= 32
+    K2 = 32 if tc else min(K + IVF_MARGIN, 256)
     err = _ivf_err(dp)
+    if tc:
+        h, dh, lres, lmax = index.half()
+        err = float((dh + 2) * 2.0 ** -22)
     ids = torch.empty((n, K), dtype=torch.int32, device=dv)
     scores = torch.empty((n, K), dtype=torch.float64, device=dv)
     per_row = nlist * 4 + nprobe * 4 + nprobe * K2 * 8
@@ -436,14 +457,21 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
         _lib.call("ancka_ivf_topsel", S.data_ptr(), nlist, m, nlist, nprobe, probes.data_ptr(), st)
         pair_ptr, tile_ptr, pair_ent = _bucket(probes, m * nprobe, nlist, tile=64)
         qthr.zero_()
-        _lib.call("ancka_ivf_search", xn.data_ptr(), dp, index.perm.data_ptr(),
-                  index.list_ptr.data_ptr(), pair_ptr.data_ptr(), pair_ent.data_ptr(),
-                  tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe, q0, K2, err,
-                  part_s.data_ptr(), part_i.data_ptr(), qthr.data_ptr(), st)
+        if tc:
+            _lib.call("ancka_ivf_search_tc", h.data_ptr(), dh, lres.data_ptr(), lmax.data_ptr(),
+                      index.perm.data_ptr(), index.list_ptr.data_ptr(), pair_ptr.data_ptr(),
+                      pair_ent.data_ptr(), tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe,
+                      q0, K2, err, part_s.data_ptr(), part_i.data_ptr(), qthr.data_ptr(), st)
+        else:
+            _lib.call("ancka_ivf_search", xn.data_ptr(), dp, index.perm.data_ptr(),
+                      index.list_ptr.data_ptr(), pair_ptr.data_ptr(), pair_ent.data_ptr(),
+                      tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe, q0, K2, err,
+                      part_s.data_ptr(), part_i.data_ptr(), qthr.data_ptr(), st)
         nflag.zero_()
         _lib.call("ancka_ivf_merge", xn.data_ptr(), dp, q0, m, nprobe, K2, K, part_s.data_ptr(),
                   part_i.data_ptr(), err, ids[q0:].data_ptr(), scores[q0:].data_ptr(),
-                  flagged.data_ptr(), nflag.data_ptr(), st)
+                  flagged.data_ptr(), nflag.data_ptr(), lres.data_ptr() if tc else None,
+                  lmax.data_ptr() if tc else None, st)
         nf = int(nflag.item())
         if nf:
             _lib.call("ancka_ivf_rows_exact", xn.data_ptr(), dp, n, flagged.data_ptr(), nf,
@@ -454,6 +482,7 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
     if stats is not None:
         stats["uncertified_rows"] = stats.get("uncertified_rows", 0) + total_flag
         stats["chunks"] = (n + chunk - 1) // chunk
+        stats["scan"] = "tensor-core fp16" if tc else "f32 SIMT"
     return ids, scores
 
 

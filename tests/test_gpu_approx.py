@@ -56,8 +56,11 @@ def _compare_lists(x, C, K, nprobe, ids_gpu, ids_ref, sc_gpu, sc_ref):
     return bad.size
 
 
+@pytest.mark.parametrize("scan", ["tensor", "simt"])
 @pytest.mark.parametrize("case", ["dense", "binary", "escalate"])
-def test_approx_with_reference_centroids(golden_approx, case):
+def test_approx_with_reference_centroids(golden_approx, case, scan, monkeypatch):
+    """scan: the fp16 tensor-core scan (certified, d <= 256) or the f32 SIMT one."""
+    monkeypatch.setattr(aknn, "IVF_TENSOR_CORES", scan == "tensor")
     z, meta = golden_approx
     m = meta[case]
     x = load_x(z, case + "_X")
@@ -72,7 +75,7 @@ def test_approx_with_reference_centroids(golden_approx, case):
         assert nbad <= 0.01 * x.shape[0]     # those by f32 rounding noise
 
 
-@pytest.mark.parametrize("shape,n", [("amazon2m", 20000), ("dblp", 12000)])
+@pytest.mark.parametrize("shape,n", [("amazon2m", 20000), ("dblp", 12000), ("papers100m", 20000)])
 def test_approx_device_training(shape, n):
     inst = synth.make(shape, seed=4, n=n)
     K = 10
