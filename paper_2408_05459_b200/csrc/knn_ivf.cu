@@ -950,6 +950,9 @@ struct RowsP {
   double* scores;
   int compact;  // output row b (audit) instead of rows[b] - q0
   int R;        // query rows per CTA (1 with probes)
+  int nsplit;   // all-keys mode: key segments (blockIdx.y); > 1 writes exact partial lists
+  double* seg_sc;   // nrows x nsplit x K partial scores (f64), ids below
+  int32_t* seg_id;
 };
 
 __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
@@ -979,6 +982,11 @@ __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
   const int nseg = p.probes ? p.nprobe : 1;
   for (int sg = 0; sg < nseg; ++sg) {
     int64_t cb = 0, ce = p.n;
+    if (!p.probes && p.nsplit > 1) {          // this CTA's key segment
+      const int64_t len = ceil_div(p.n, p.nsplit);
+      cb = lmin(p.n, (int64_t)blockIdx.y * len);
+      ce = lmin(p.n, cb + len);
+    }
     if (p.probes) {
       const int c = p.probes[(int64_t)(qid[0] - p.q0) * p.nprobe + sg];
       cb = p.list_ptr[c];
@@ -1047,12 +1055,48 @@ __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
   }
   if (tid < nr) {
     const int r = tid;
+    if (!p.probes && p.nsplit > 1) {          // exact partial list of this key segment
+      const int64_t base = ((b0 + r) * p.nsplit + blockIdx.y) * p.K;
+      for (int t = 0; t < p.K; ++t) {
+        const bool v = t < lcnt[r];
+        p.seg_id[base + t] = v ? li[(size_t)r * p.K + t] : -1;
+        p.seg_sc[base + t] = v ? ls[(size_t)r * p.K + t] : -INFINITY;
+      }
+      return;
+    }
     const int64_t orow = p.compact ? b0 + r : (int64_t)qid[r] - p.q0;
     for (int t = 0; t < p.K; ++t) {
       const bool v = t < lcnt[r];
       p.ids[orow * p.K + t] = v ? li[(size_t)r * p.K + t] : -1;
       p.scores[orow * p.K + t] = v ? (double)fminf((float)ls[(size_t)r * p.K + t], 1.0f) : 0.0;
     }
+  }
+}
+
+// merge of the key-segment partial lists (exact f64 scores): top-K by
+// (score desc, id asc), one thread per row (compact output)
+__global__ void ivf_rows_seg_merge(const double* __restrict__ seg_sc, const int32_t* __restrict__ seg_id,
+                                   int64_t nrows, int nsplit, int K, int32_t* __restrict__ ids,
+                                   double* __restrict__ scores) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  int head[64];
+  for (int s = 0; s < nsplit; ++s) head[s] = 0;
+  for (int t = 0; t < K; ++t) {
+    int bs = -1;
+    double bv = 0.0;
+    int bi = 0x7fffffff;
+    for (int s = 0; s < nsplit; ++s) {
+      if (head[s] >= K) continue;
+      const int64_t e = (r * nsplit + s) * K + head[s];
+      const int id = seg_id[e];
+      if (id < 0) continue;
+      const double v = seg_sc[e];
+      if (bs < 0 || v > bv || (v == bv && id < bi)) { bs = s; bv = v; bi = id; }
+    }
+    ids[r * K + t] = bs < 0 ? -1 : bi;
+    scores[r * K + t] = bs < 0 ? 0.0 : (double)fminf((float)bv, 1.0f);
+    if (bs >= 0) ++head[bs];
   }
 }
 
@@ -1280,9 +1324,23 @@ extern "C" int ancka_ivf_rows_exact(const float* xn, int64_t dp, int64_t n, cons
                 (long long)dp, K);
   ANCKA_CUDA(cudaFuncSetAttribute(ivf_rows_exact, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
-  RowsP p{xn, dp, n, rows, nrows, probes, nprobe, q0, perm, list_ptr, K, ids, scores, compact, R};
-  ivf_rows_exact<<<(unsigned)ceil_div(nrows, R), kT, smem, as_stream(stream)>>>(p);
+  RowsP p{xn, dp, n, rows, nrows, probes, nprobe, q0, perm, list_ptr, K, ids, scores, compact, R,
+          1, nullptr, nullptr};
+  const int64_t gx = ceil_div(nrows, R);
+  if (!probes && compact && gx < 4 * kNumSMs) {     // few rows: split the keys as well
+    p.nsplit = (int)std::min<int64_t>(64, ceil_div(4 * kNumSMs, gx));
+    ANCKA_CUDA(cudaMallocAsync(&p.seg_sc, sizeof(double) * nrows * p.nsplit * K, as_stream(stream)));
+    ANCKA_CUDA(cudaMallocAsync(&p.seg_id, sizeof(int32_t) * nrows * p.nsplit * K, as_stream(stream)));
+  }
+  ivf_rows_exact<<<dim3((unsigned)gx, (unsigned)p.nsplit), kT, smem, as_stream(stream)>>>(p);
   ANCKA_LAUNCHED();
+  if (p.nsplit > 1) {
+    ivf_rows_seg_merge<<<(unsigned)ceil_div(nrows, 128), 128, 0, as_stream(stream)>>>(
+        p.seg_sc, p.seg_id, nrows, p.nsplit, K, ids, scores);
+    ANCKA_LAUNCHED();
+    ANCKA_CUDA(cudaFreeAsync(p.seg_sc, as_stream(stream)));
+    ANCKA_CUDA(cudaFreeAsync(p.seg_id, as_stream(stream)));
+  }
   return ANCKA_OK;
 }
 
