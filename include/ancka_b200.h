@@ -237,7 +237,7 @@ int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_csr* S, cons
                 int64_t lds, const ancka_csr* K, const void* k_src, int64_t ldk, const void* beta,
                 const uint8_t* selfloop, const void* self_src, int64_t ld_self, int64_t row_offset,
                 const int32_t* tag, const void* tagval, double scale, void* out, int64_t ldo,
-                ancka_stream_t stream);
+                const int32_t* order, ancka_stream_t stream);
 
 /* Split Cholesky-QR for row-partitioned blocks: G = Z^T Z of the local rows
  * (packed upper, f64, c(c+1)/2), all-reduced by the caller, then factor +

@@ -58,7 +58,7 @@ _SIGS = {
     "ancka_spmm2": (c_int32, [c_int32, c_int64, c_int32, POINTER(CSR), c_void_p, c_int64,
                               POINTER(CSR), c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
                               c_int64, c_int64, c_void_p, c_void_p, c_double, c_void_p, c_int64,
-                              c_void_p]),
+                              c_void_p, c_void_p]),
     "ancka_gram_f32": (c_int32, [c_void_p, c_int64, c_int64, c_int32, c_void_p, c_void_p,
                                  c_size_t, c_void_p]),
     "ancka_cholqr_apply_f32": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_int64, c_int32,

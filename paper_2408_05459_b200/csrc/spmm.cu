@@ -390,7 +390,7 @@ extern "C" int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_c
                            int64_t ldk, const void* beta, const uint8_t* selfloop,
                            const void* self_src, int64_t ld_self, int64_t row_offset,
                            const int32_t* tag, const void* tagval, double scale, void* out,
-                           int64_t ldo, ancka_stream_t stream) {
+                           int64_t ldo, const int32_t* order, ancka_stream_t stream) {
   using namespace ancka;
   auto st = as_stream(stream);
   auto fill = [&](auto* tp) -> int {
@@ -419,6 +419,7 @@ extern "C" int ancka_spmm2(int32_t dtype, int64_t rows, int32_t c, const ancka_c
     a.scale = (T)scale;
     a.out = static_cast<T*>(out);
     a.ldo = ldo;
+    if constexpr (sizeof(T) == 4) a.order = order;   // row processing order (sums unchanged)
     return launch_spmm<T>(a, st);
   };
   if (dtype == ANCKA_F64) return fill((double*)nullptr);

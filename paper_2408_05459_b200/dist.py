@@ -176,6 +176,11 @@ class DistOperator:
         self.K = p_k_rows
         self.beta = B.vec(beta_loc)
         self.selfloop = B.mask(selfloop_loc)
+        self.order = None     # f32 row order (locality), refreshed at every sample
+
+    def set_order(self, labels_loc, k):
+        if hasattr(self.B, "locality_order"):
+            self.order = self.B.locality_order(labels_loc, k)
 
     # -- joint apply (walk.py:177-190) on the local rows; Q_full gathered
     def apply(self, Q_full, c, dtype, tag=None, tagval=None, scale=1.0):
@@ -185,6 +190,9 @@ class DistOperator:
             src = B.all_gather_rows(T_loc, pl.edge_counts())
         else:
             src = Q_full
+        if self.order is not None and dtype == "f32":
+            return B.spmm(self.S, src, self.K, Q_full, self.beta, self.selfloop, Q_full, pl.r0,
+                          tag, tagval, scale, c, dtype, order=self.order)
         return B.spmm(self.S, src, self.K, Q_full, self.beta, self.selfloop, Q_full, pl.r0,
                       tag, tagval, scale, c, dtype)
 
@@ -351,6 +359,12 @@ class DistResult:
 
 
 def _q0_chunk(B, labels: np.ndarray, sizes: np.ndarray, n: int, c: int, c0: int, cc: int):
+    if hasattr(B, "q0_chunk"):                 # built on the device from the labels
+        return B.q0_chunk(labels, sizes, n, c, c0, cc)
+    return _q0_chunk_host(B, labels, sizes, n, c, c0, cc)
+
+
+def _q0_chunk_host(B, labels: np.ndarray, sizes: np.ndarray, n: int, c: int, c0: int, cc: int):
     """Columns [c0, c0 + cc) of Q^(0) = [1/sqrt(n) | Yhat0] (engine.py:368-371)
     for all n rows, built from the replicated labels (no gather)."""
     q = np.zeros((n, cc))
@@ -490,11 +504,15 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     best = lab0.copy()
     hist = [(0, best_phi)]
 
+    op.set_order(lab0[r0:r1], k)
     # ---- t = 1: exact f64 step from the replicated labels (no gather of Q0)
     Q1, _ = exact_step_dist(B, op, plan, None, c, rng, labels0=lab0, sizes0=sizes0)
-    q0_loc = _q0_chunk(B, lab0[r0:r1], sizes0, r1 - r0, c, 0, c)
-    if r1 > r0:
-        q0_loc = B.fix_q0_rows(q0_loc, n)      # the 1/sqrt(n) column uses the global n
+    if hasattr(B, "q0_chunk"):                 # local rows, 1/sqrt(n) with the global n
+        q0_loc = B.q0_chunk(lab0[r0:r1], sizes0, n, c, 0, c)
+    else:
+        q0_loc = _q0_chunk_host(B, lab0[r0:r1], sizes0, r1 - r0, c, 0, c)
+        if r1 > r0:
+            q0_loc = B.fix_q0_rows(q0_loc, n)  # the 1/sqrt(n) column uses the global n
     dq = float(np.sqrt(B.sync_scalars([B.diff2(Q1, q0_loc, c)])[0]))
     Q_loc = B.to_f32(Q1, c)
     ph.mark("step1_ms")
@@ -538,6 +556,7 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
                 ph.mark("discretize_ms")
                 phi = mhc(labels, "f32")
                 ph.mark("mhc_ms")
+                op.set_order(labels[r0:r1], k)
                 hist.append((t, phi))
                 if phi < best_phi:
                     best_phi, best = phi, labels.copy()
@@ -675,6 +694,27 @@ class CudaBackend:
         return Z
 
     def fix_q0_rows(self, q, n):
+        return q
+
+    def q0_chunk(self, labels, sizes, n, c, c0, cc):
+        """_q0_chunk on the device: columns [c0, c0 + cc) of [1/sqrt(n) | Yhat0]
+        (n = the global node count of the first column) for the given rows'
+        labels, without a host-built dense block or its upload."""
+        torch = self.torch
+        rows = int(labels.shape[0])
+        from ._device import ld_for
+        q = torch.zeros((rows, ld_for(cc, torch.float64)), dtype=torch.float64, device="cuda")
+        if rows == 0:
+            return q
+        if c0 == 0:
+            q[:, 0] = 1.0 / np.sqrt(n)
+        lab = torch.as_tensor(np.asarray(labels, dtype=np.int64), device="cuda")
+        inv = torch.as_tensor(1.0 / np.sqrt(np.maximum(np.asarray(sizes, dtype=np.float64), 1.0)),
+                              device="cuda")
+        col = lab + 1 - c0
+        ok = (col >= 0) & (col < cc) & (lab + 1 < c)
+        idx = torch.nonzero(ok, as_tuple=True)[0]
+        q[idx, col[idx]] = inv[lab[idx]]
         return q
 
     def copy(self, a):
@@ -974,7 +1014,7 @@ class CudaBackend:
         return P, zero[:nloc].cpu().numpy().astype(bool)
 
     def spmm(self, S, s_src, Kc, k_src, beta, selfloop, self_src, row_offset, tag, tagval, scale,
-             c, dtype):
+             c, dtype, order=None):
         torch, _lib = self.torch, self._lib
         f64 = dtype == "f64"
         dt = torch.float64 if f64 else torch.float32
@@ -1001,8 +1041,25 @@ class CudaBackend:
                   self_src.stride(0) if self_src is not None else 0, row_offset,
                   tag.data_ptr() if tag is not None else None,
                   tagval_t.data_ptr() if tagval_t is not None else None, float(scale),
-                  out.data_ptr(), out.stride(0), _lib.stream())
+                  out.data_ptr(), out.stride(0),
+                  order.data_ptr() if (order is not None and not f64) else None, _lib.stream())
         return out
+
+    def locality_order(self, labels_loc, k):
+        """Local rows grouped by cluster label (ancka_locality_order): the
+        processing order of the f32 row pass, so the rows in flight gather
+        mostly their own cluster's rows of Q from L2 (sums unchanged)."""
+        torch, _lib = self.torch, self._lib
+        n = int(labels_loc.shape[0])
+        if n == 0:
+            return None
+        lab = torch.as_tensor(np.asarray(labels_loc, dtype=np.int32), device="cuda")
+        order = torch.empty(n, dtype=torch.int32, device="cuda")
+        ws = torch.empty(int(_lib.load().ancka_locality_order_workspace_size(n)), dtype=torch.uint8,
+                         device="cuda")
+        _lib.call("ancka_locality_order", lab.data_ptr(), n, k, order.data_ptr(), ws.data_ptr(),
+                  ws.numel(), _lib.stream())
+        return order
 
     def gram(self, Z, c):
         """Local Gram Z^T Z (packed upper, f64) on the device (ancka_gram_f32)."""
