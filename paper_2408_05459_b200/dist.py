@@ -124,7 +124,7 @@ class ShardFactors:
             # reference row sums of H^T (node degrees) and of H (edge sizes)
             self.dv = np.asarray(self.h.sum(axis=0)).ravel()
             self.de = np.asarray(self.h.sum(axis=1)).ravel()
-            self.row_nnz = np.diff(self.h.tocsc().indptr).astype(np.float64)
+            self.row_nnz = np.bincount(self.h.indices, minlength=self.n).astype(np.float64)
         else:
             a = symmetrize_union(net.adjacency) if net.directed else net.adjacency
             self.a = _binary(a)
@@ -137,6 +137,18 @@ class ShardFactors:
 
     def edge_cost(self) -> np.ndarray:
         return np.diff(self.h.indptr).astype(np.float64) + 1
+
+
+def _raw_row_cost(net: AttributedNetwork, K: int) -> np.ndarray:
+    """Row costs from the unvalidated input's pattern (degrees + 2K + 1)."""
+    if net.kind is NetworkKind.HYPERGRAPH:
+        deg = np.bincount(net.incidence.indices, minlength=net.n)
+    else:
+        a = net.adjacency
+        deg = np.diff(a.indptr)
+        if net.directed:
+            deg = deg + np.bincount(a.indices, minlength=net.n)
+    return deg.astype(np.float64) + 2 * K + 1
 
 
 def make_plan(fac: ShardFactors, K: int, rank: int, world: int) -> Plan:
@@ -430,20 +442,25 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     """run_ancka (engine.py:343-437) row-partitioned over the backend's ranks."""
     rank, world = B.rank, B.world
     ph = _Phases(B, DIST_TIMING)
-    net, report = validate_network(net)
     if net.kind is NetworkKind.MULTIPLEX:
         raise NetworkError("the row-partitioned path covers graphs and hypergraphs")
     params.validate_for(net.n)
     n, k = net.n, params.k
     K = params.knn_k if params.knn_k is not None else default_knn_k(net.kind, n)
     K = min(K, n - 1)
-    fac = ShardFactors(net, report.degrees)
-    plan = make_plan(fac, K, rank, world)
+    # rows are balanced on the input's pattern (any split is correct), so the
+    # KNN ring starts before the host validation, which then overlaps it
+    # (the attributes the ring reads are not changed by validation)
+    rows = partition_rows(_raw_row_cost(net, K), world)
+    plan = Plan(rank, world, n, 0, rows, np.zeros(world + 1, dtype=np.int64))
     r0, r1 = plan.r0, plan.r1
-    ph.mark("host_prepare_ms")
 
     # ---- KNN: key ring, then A_K / P_K rows from an all-to-all of triples
     ids_loc, sc_loc = knn_ring(B, net.attributes, K, plan)
+    net, report = validate_network(net)
+    fac = ShardFactors(net, report.degrees)
+    if fac.kind is NetworkKind.HYPERGRAPH:
+        plan = Plan(rank, world, n, fac.m, rows, partition_rows(fac.edge_cost(), world))
     ph.mark("knn_ms")
     pk_rows, zero_loc = B.knn_graph_rows(ids_loc, sc_loc, plan, K)
 
