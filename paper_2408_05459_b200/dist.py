@@ -638,28 +638,51 @@ class CudaBackend:
     def mask(self, a):
         return self._t(np.asarray(a, dtype=np.uint8), self.torch.uint8)
 
+    def _pattern(self, m):
+        """Device CSR of a row slice, uploaded once per slice object: its
+        row-normalised and column-scaled value arrays are both formed on the
+        device from the same rowptr / colidx / values."""
+        from ._device import DeviceCSR
+        cache = self.__dict__.setdefault("_patterns", {})
+        hit = cache.get(id(m))
+        if hit is not None and hit[0] is m:
+            return hit[1]
+        mm = sp.csr_matrix(m)
+        if not mm.has_sorted_indices:
+            mm = mm.copy()
+            mm.sort_indices()
+        torch = self.torch
+        rp = torch.from_numpy(np.ascontiguousarray(mm.indptr, dtype=np.int64)).to("cuda")
+        ci = torch.from_numpy(np.ascontiguousarray(mm.indices, dtype=np.int32)).to("cuda")
+        v = torch.from_numpy(np.ascontiguousarray(mm.data, dtype=np.float64)).to("cuda")
+        d = DeviceCSR(mm.shape[0], mm.shape[1], rp, ci, v, None)
+        if len(cache) > 8:
+            cache.clear()
+        cache[id(m)] = (m, d)
+        return d
+
     def csr_rownorm(self, m):
         """Row-normalised device CSR of a (binary) row slice, numpy's row-sum
         order (ancka_csr_row_normalize)."""
         from ._device import DeviceCSR
-        d = DeviceCSR.from_scipy(sp.csr_matrix(m, dtype=np.float64))
-        out = self.torch.empty_like(d.val64)
-        if d.nnz:
-            self._lib.call("ancka_csr_row_normalize", d.struct(self._lib.F64), out.data_ptr(),
+        base = self._pattern(m)
+        out = self.torch.empty_like(base.val64)
+        if base.nnz:
+            self._lib.call("ancka_csr_row_normalize", base.struct(self._lib.F64), out.data_ptr(),
                            None, self._lib.stream())
-        d.val64, d.val32 = out, out.to(self.torch.float32)
-        return d
+        return DeviceCSR(base.rows, base.cols, base.rowptr, base.colidx, out,
+                         out.to(self.torch.float32))
 
     def csr_colscale(self, m, col_scale):
         from ._device import DeviceCSR
-        d = DeviceCSR.from_scipy(sp.csr_matrix(m, dtype=np.float64))
-        out = self.torch.empty_like(d.val64)
+        base = self._pattern(m)
+        out = self.torch.empty_like(base.val64)
         cs = self.vec(col_scale)
-        if d.nnz:
-            self._lib.call("ancka_csr_col_scale", d.struct(self._lib.F64), cs.data_ptr(),
+        if base.nnz:
+            self._lib.call("ancka_csr_col_scale", base.struct(self._lib.F64), cs.data_ptr(),
                            out.data_ptr(), self._lib.stream())
-        d.val64, d.val32 = out, out.to(self.torch.float32)
-        return d
+        return DeviceCSR(base.rows, base.cols, base.rowptr, base.colidx, out,
+                         out.to(self.torch.float32))
 
     def _ld(self, c, dtype):
         from ._device import ld_for
