@@ -57,6 +57,14 @@ from .network import (AttributedNetwork, ClusterParams, NetworkError, NetworkKin
 #: centre columns per chunk of the init walk / step-1 apply (bounds the f64
 #: n x chunk block each rank holds: Papers100M 111M x 32 x 8 B = 28 GB)
 INIT_CHUNK = 32
+#: f64 bytes of one gathered n x chunk block allowed before chunking at INIT_CHUNK
+INIT_CHUNK_BYTES = 4 << 30
+
+
+def _f64_chunk(n: int, cols: int) -> int:
+    """Columns per f64 walk / step-1 chunk: all of them when the gathered
+    n x cols f64 block fits INIT_CHUNK_BYTES, else INIT_CHUNK."""
+    return cols if n * cols * 8 <= INIT_CHUNK_BYTES else INIT_CHUNK
 
 
 # ----------------------------------------------------------------------------
@@ -398,8 +406,9 @@ def exact_step_dist(B, op: DistOperator, plan: Plan, Q_src, c: int, rng, labels0
     Returns (Q_loc f64, Z_loc f64)."""
     n = plan.n
     parts = []
-    for c0 in range(0, c, INIT_CHUNK):
-        cc = min(INIT_CHUNK, c - c0)
+    ch = _f64_chunk(n, c)
+    for c0 in range(0, c, ch):
+        cc = min(ch, c - c0)
         if Q_src is None:
             full = _q0_chunk(B, labels0, sizes0, n, c, c0, cc)
         else:
@@ -479,8 +488,9 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
     center_of = np.full(n, -1, dtype=np.int64)
     center_of[centers] = np.arange(k)
     best_v, best_i = None, None
-    for c0 in range(0, k, INIT_CHUNK):
-        cc = min(INIT_CHUNK, k - c0)
+    ch = _f64_chunk(n, k)
+    for c0 in range(0, k, ch):
+        cc = min(ch, k - c0)
         loc = center_of[r0:r1] - c0
         loc = np.where((center_of[r0:r1] >= 0) & (loc >= 0) & (loc < cc), loc, -1)
         tag_loc = B.ivec(loc)
