@@ -519,7 +519,7 @@ def run_ancka_dist(net: AttributedNetwork, params: ClusterParams, B, early_stop:
         for _ in range(params.gamma):
             F_full = B.all_gather_rows(F_loc, plan.row_counts())
             F_loc = op.apply(F_full, k, dtype, tag, tv, 1.0 - params.alpha)
-        tr = B.sync_scalars([B.trace_labels(F_loc, labels[r0:r1], yhat)])[0]
+        tr = B.sync_scalars([B.trace_labels(F_loc, tag, yhat)])[0]
         return 1.0 - tr / k
 
     ph.mark("init_ms")
@@ -1164,6 +1164,7 @@ class CudaBackend:
         return torch.where(take, v, best_v), torch.where(take, i, best_i)
 
     def trace_labels(self, F, labels_loc, yhat):
+        """sum_i yhat[l_i] F[i, l_i] (labels: the device tag vector or host)."""
         torch = self.torch
         lab = torch.as_tensor(labels_loc, device="cuda").long()
         vals = F[torch.arange(F.shape[0], device="cuda"), lab].double()
