@@ -276,8 +276,9 @@ def knn_search_exact(X, K: int, block_rows: int | None = None) -> NeighborLists:
 # Approximate search: inverted-file index (knn.py:143-280; csrc/knn_ivf.cu)
 # --------------------------------------------------------------------------
 
-#: per-chunk device bytes for the probe scores and partial lists
-IVF_CHUNK_BYTES = 8 << 30
+#: per-chunk device bytes for the probe scores and partial lists (at most;
+#: also at most a quarter of the free device memory)
+IVF_CHUNK_BYTES = 32 << 30
 #: extra slots per (query, list) partial list and in the merged list; the
 #: f64 re-rank certifies the top-K against the K2-th f32 score
 IVF_MARGIN = 8
@@ -439,7 +440,8 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
     ids = torch.empty((n, K), dtype=torch.int32, device=dv)
     scores = torch.empty((n, K), dtype=torch.float64, device=dv)
     per_row = nlist * 4 + nprobe * 4 + nprobe * K2 * 8
-    chunk = int(max(1, min(n, IVF_CHUNK_BYTES // per_row)))
+    budget = min(IVF_CHUNK_BYTES, torch.cuda.mem_get_info(dv)[0] // 4)
+    chunk = int(max(1, min(n, budget // per_row)))
     flagged = torch.empty(chunk, dtype=torch.int32, device=dv)
     nflag = torch.zeros(1, dtype=torch.int32, device=dv)
     counter = torch.zeros(1, dtype=torch.int32, device=dv)
