@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(kT) ivf_topsel(const float* __restrict__ S, in
 __global__ void ivf_bucket_count(const int32_t* __restrict__ keys, int64_t cnt, int32_t* __restrict__ c) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&c[keys[i]], 1);
+    if (keys[i] >= 0) atomicAdd(&c[keys[i]], 1);   // negative keys: entry not bucketed
 }
 
 // exclusive scan of nbk counts (one CTA), ptr[nbk] = total; also the tile
@@ -301,7 +301,7 @@ __global__ void ivf_bucket_fill(const int32_t* __restrict__ keys, int64_t cnt,
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t k = keys[i];
-    ent[ptr[k] + atomicAdd(&cursor[k], 1)] = (int32_t)i;
+    if (k >= 0) ent[ptr[k] + atomicAdd(&cursor[k], 1)] = (int32_t)i;
   }
 }
 
@@ -627,10 +627,12 @@ constexpr int kMaxDh = 256;
 
 __host__ __device__ inline size_t search_tc_smem(int64_t dh, int K2) {
   const size_t hs = (size_t)(dh + 8);                      // halves per staged row
-  return align_dev(2 * hs * TQ) + 2 * align_dev(2 * hs * TK) + align_dev(4 * (size_t)TQ * TK) +
+  return align_dev(2 * hs * TQ) + 3 * align_dev(2 * hs * TK) + align_dev(4 * (size_t)TQ * TK) +
          align_dev((size_t)TQ * TK) + align_dev(4 * (size_t)TQ * K2) + align_dev(4 * (size_t)TQ * K2) +
          align_dev(4 * (7 * (size_t)TQ + TK));
 }
+
+constexpr int kTcStages = 3;      // key tiles in flight
 
 __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   const SearchP& p = P.s;
@@ -638,9 +640,11 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   const int hs = (int)P.dh + 8;
   unsigned char* o = smem_raw;
   __half* qh = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TQ);
-  __half* kh[2];
-  kh[0] = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TK);
-  kh[1] = reinterpret_cast<__half*>(o); o += align_dev(2 * (size_t)hs * TK);
+  __half* kh[kTcStages];
+  for (int st = 0; st < kTcStages; ++st) {
+    kh[st] = reinterpret_cast<__half*>(o);
+    o += align_dev(2 * (size_t)hs * TK);
+  }
   float* cbs = reinterpret_cast<float*>(o); o += align_dev(4 * (size_t)TQ * TK);
   uint8_t* cbi = o; o += align_dev((size_t)TQ * TK);
   float* ts = reinterpret_cast<float*>(o); o += align_dev(4 * (size_t)TQ * p.K2);
@@ -652,19 +656,21 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   float* thr = reinterpret_cast<float*>(ccnt + TQ);
   float* gt = thr + TQ;
   float* eq = gt + TQ;
-  int32_t* kid = reinterpret_cast<int32_t*>(eq + TQ);
   __shared__ int s_work;
-  __shared__ int32_t kidn[TK];
+  __shared__ int32_t kids[kTcStages][TK];                 // key ids of each staged tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wr = (warp & 3) * 16, wc = (warp >> 2) * 32;   // warp tile: 16 queries x 32 keys
   const int64_t total = p.tile_ptr[p.nlist];
   const int nch = (int)(P.dh / 8);                          // 16-byte chunks per row
   const float lmax = __uint_as_float(*P.lmax_bits);
-  auto stage_keys = [&](const int32_t* ids, int b) {
+  // stage key tile [k0, k0 + TK) of the list (ids read from perm by the
+  // issuing threads; thread r < TK records id r for the filter)
+  auto stage_keys = [&](int64_t k0, int64_t ke, int b) {
+    if (tid < TK) kids[b][tid] = k0 + tid < ke ? p.perm[k0 + tid] : -1;
     for (int e = tid; e < TK * nch; e += kT) {
       const int r = e / nch, ch = e - r * nch;
-      const int32_t id = ids[r];
+      const int32_t id = k0 + r < ke ? p.perm[k0 + r] : -1;
       __half* dst = kh[b] + (size_t)r * hs + ch * 8;
       if (id >= 0) {
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
@@ -690,6 +696,12 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
     const int64_t pb = p.pair_ptr[c] + (w - p.tile_ptr[c]) * TQ;
     const int nq = (int)lmin(TQ, p.pair_ptr[c + 1] - pb);
     const int64_t kb = p.list_ptr[c], ke = p.list_ptr[c + 1];
+    const int ntile = (int)ceil_div(ke - kb, TK);
+    // the first stages' keys start loading before the query tile is set up
+    for (int st = 0; st < kTcStages - 1; ++st) {
+      if (st < ntile) stage_keys(kb + (int64_t)st * TK, ke, st);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+    }
     if (tid < TQ) {
       const int32_t e = tid < nq ? p.pair_ent[pb + tid] : -1;
       qent[tid] = e;
@@ -703,7 +715,6 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
       thr[tid] = -e_q;
       gt[tid] = e >= 0 ? fmaxf(-e_q, key_ord(p.qthr[e / p.nprobe])) : -e_q;
     }
-    if (tid < TK) kid[tid] = kb + tid < ke ? p.perm[kb + tid] : -1;
     __syncthreads();
     for (int e = tid; e < TQ * nch; e += kT) {             // the tile's queries (fp16)
       const int r = e / nch, ch = e - r * nch;
@@ -711,26 +722,21 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
       *reinterpret_cast<uint4*>(qh + (size_t)r * hs + ch * 8) =
           qr >= 0 ? *reinterpret_cast<const uint4*>(P.h + (int64_t)qr * P.dh + ch * 8) : make_uint4(0u, 0u, 0u, 0u);
     }
-    stage_keys(kid, 0);
-    int buf = 0;
-    for (int64_t k0 = kb; k0 < ke; k0 += TK, buf ^= 1) {
+    for (int t = 0; t < ntile; ++t) {
+      const int b = t % kTcStages;
+      const int64_t k0 = kb + (int64_t)t * TK;
       const int nk = (int)lmin(TK, ke - k0);
-      const bool more = k0 + TK < ke;
-      if (more) {
-        if (tid < TK) kidn[tid] = k0 + TK + tid < ke ? p.perm[k0 + TK + tid] : -1;
-        __syncthreads();
-        stage_keys(kidn, buf ^ 1);
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      } else {
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-      }
+      if (t + kTcStages - 1 < ntile) stage_keys(kb + (int64_t)(t + kTcStages - 1) * TK, ke, (t + kTcStages - 1) % kTcStages);
+      else asm volatile("cp.async.commit_group;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kTcStages - 1) : "memory");
       __syncthreads();
+      const int32_t* kid = kids[b];
       float acc[4][4];
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[nt][u] = 0.f;
-      const __half* kb_ = kh[buf];
+      const __half* kb_ = kh[b];
       for (int k = 0; k < (int)P.dh; k += 16) {
         uint32_t a[4];
         const __half* qa = qh + (size_t)(wr + g) * hs + k + 2 * t4;
@@ -754,19 +760,20 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
         const float ts_ = thr[q], g_ = gt[q];
         const int ti_ = full ? ti[q * p.K2 + p.K2 - 1] : 0;
         const int me = qrow[q];
+        const float lo2 = fmaxf(g_, ts_);
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
+            const float sv = acc[nt][2 * hrow + u];
+            if (!(sv > g_) || sv < lo2 || (!full && !(sv > ts_))) continue;
             const int slot = wc + nt * 8 + 2 * t4 + u;
             const int id = kid[slot];
-            const float sv = acc[nt][2 * hrow + u];
             if (slot >= nk || id < 0 || id == me) continue;
-            if (sv > g_ && (full ? before(sv, id, ts_, ti_) : sv > ts_)) {
-              const int pos = atomicAdd(&ccnt[q], 1);
-              cbs[q * TK + pos] = sv;
-              cbi[q * TK + pos] = (uint8_t)slot;
-            }
+            if (full && !before(sv, id, ts_, ti_)) continue;
+            const int pos = atomicAdd(&ccnt[q], 1);
+            cbs[q * TK + pos] = sv;
+            cbi[q * TK + pos] = (uint8_t)slot;
           }
       }
       __syncthreads();
@@ -802,8 +809,8 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
         }
       }
       __syncthreads();
-      if (more && tid < TK) kid[tid] = kidn[tid];
     }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid < nq) {
       const int r = tid;
       const int64_t base = (int64_t)qent[r] * p.K2;
@@ -1261,6 +1268,89 @@ extern "C" int ancka_ivf_half_prep(const float* xn, int64_t n, int64_t dp, void*
   if (n == 0) return ANCKA_OK;
   ivf_half_prep<<<grid_for(n * 32, kT), kT, 0, st>>>(xn, n, dp, static_cast<__half*>(h), dh, lres,
                                                     reinterpret_cast<unsigned*>(lmax_bits));
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+// Seed of the per-query threshold (fp16 scan): the K2-th best approximate
+// score of the query against up to 64 keys of its own list, less a margin
+// for the scan's different f32 summation order -- a lower bound on the K2-th
+// approximate score of its merged list (those keys are among its
+// candidates), so every pair filters from its first key tile on.
+__global__ void ivf_seed_kernel(const __half* __restrict__ h, int64_t dh, const int32_t* __restrict__ labels,
+                                const int32_t* __restrict__ perm, const int64_t* __restrict__ list_ptr,
+                                int64_t q0, int64_t m, int K2, float margin, uint32_t* __restrict__ qthr) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < m;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t gq = q0 + q;
+    const int c = labels[gq];
+    const int64_t kb = list_ptr[c], ke = lmin(list_ptr[c + 1], kb + 64);
+    float best[2] = {-FLT_MAX, -FLT_MAX};    // lane's two keys (64 keys over 32 lanes)
+    const __half* xq = h + gq * dh;
+    for (int u = 0; u < 2; ++u) {
+      const int64_t j = kb + lane + 32 * u;
+      if (j >= ke) continue;
+      const int32_t id = perm[j];
+      if (id == gq) continue;
+      const __half* xk = h + (int64_t)id * dh;
+      float a = 0.f;
+      for (int64_t cc = 0; cc < dh; ++cc) a = fmaf(__half2float(xq[cc]), __half2float(xk[cc]), a);
+      best[u] = a;
+    }
+    // K2-th largest of the (up to) 64 values: count-based selection
+    float kth = -FLT_MAX;
+    int have = 0;
+    for (int u = 0; u < 2; ++u) have += __popc(__ballot_sync(0xffffffffu, best[u] > -FLT_MAX));
+    if (have >= K2) {
+      for (int src = 0; src < 64; ++src) {
+        const float v = __shfl_sync(0xffffffffu, best[src >> 5], src & 31);
+        int above = 0;
+        for (int u = 0; u < 2; ++u) above += __popc(__ballot_sync(0xffffffffu, best[u] > v));
+        if (v > -FLT_MAX && above < K2) {
+          int ge = 0;
+          for (int u = 0; u < 2; ++u) ge += __popc(__ballot_sync(0xffffffffu, best[u] >= v));
+          if (ge >= K2 && v > kth) kth = v;
+        }
+      }
+    }
+    if (lane == 0 && kth > -FLT_MAX) atomicMax(qthr + q, ord_key(kth - margin));
+  }
+}
+
+// Probe split for the two-phase scan: own[] keeps, per query, the probe slot
+// of its own list (the list it is assigned to, always among its probes) and
+// -1 elsewhere; rest[] the other slots.  Scanning the own pairs first sets
+// each query's shared threshold from a whole list before the other pairs.
+__global__ void ivf_split_probes_kernel(const int32_t* __restrict__ probes, const int32_t* __restrict__ labels,
+                                        int64_t q0, int64_t m, int nprobe, int32_t* __restrict__ own,
+                                        int32_t* __restrict__ rest) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < m * nprobe;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = e / nprobe;
+    const int32_t c = probes[e];
+    const bool mine = c == labels[q0 + q];
+    own[e] = mine ? c : -1;
+    rest[e] = mine ? -1 : c;
+  }
+}
+
+extern "C" int ancka_ivf_split_probes(const int32_t* probes, const int32_t* labels, int64_t q0,
+                                      int64_t m, int32_t nprobe, int32_t* own, int32_t* rest,
+                                      ancka_stream_t stream) {
+  if (m == 0) return ANCKA_OK;
+  ivf_split_probes_kernel<<<grid_for(m * nprobe, kT), kT, 0, as_stream(stream)>>>(probes, labels, q0, m,
+                                                                                 nprobe, own, rest);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+extern "C" int ancka_ivf_seed(const void* h, int64_t dh, const int32_t* labels, const int32_t* perm,
+                              const int64_t* list_ptr, int64_t q0, int64_t m, int32_t K2,
+                              float margin, uint32_t* qthr, ancka_stream_t stream) {
+  if (m == 0) return ANCKA_OK;
+  ivf_seed_kernel<<<grid_for(m * 32, kT), kT, 0, as_stream(stream)>>>(
+      static_cast<const __half*>(h), dh, labels, perm, list_ptr, q0, m, K2, margin, qthr);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

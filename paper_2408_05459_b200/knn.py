@@ -450,6 +450,8 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
     part_s = torch.empty(chunk * nprobe * K2, dtype=torch.float32, device=dv)
     part_i = torch.empty(chunk * nprobe * K2, dtype=torch.int32, device=dv)
     qthr = torch.empty(chunk, dtype=torch.int32, device=dv)
+    own = torch.empty((chunk, nprobe), dtype=torch.int32, device=dv) if tc else None
+    rest = torch.empty((chunk, nprobe), dtype=torch.int32, device=dv) if tc else None
     st = _lib.stream()
     total_flag = 0
     for q0 in range(0, n, chunk):
@@ -457,14 +459,21 @@ def ivf_search_all_device(index: IvfIndex, K: int, nprobe: int, stats: dict | No
         _lib.call("ancka_ivf_gemm", xn[q0:].data_ptr(), dp, None, m, index.C.data_ptr(), dp, nlist,
                   dp, None, S.data_ptr(), nlist, None, st)
         _lib.call("ancka_ivf_topsel", S.data_ptr(), nlist, m, nlist, nprobe, probes.data_ptr(), st)
-        pair_ptr, tile_ptr, pair_ent = _bucket(probes, m * nprobe, nlist, tile=64)
         qthr.zero_()
         if tc:
-            _lib.call("ancka_ivf_search_tc", h.data_ptr(), dh, lres.data_ptr(), lmax.data_ptr(),
-                      index.perm.data_ptr(), index.list_ptr.data_ptr(), pair_ptr.data_ptr(),
-                      pair_ent.data_ptr(), tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe,
-                      q0, K2, err, part_s.data_ptr(), part_i.data_ptr(), qthr.data_ptr(), st)
+            # two phases: every query's own list first (a whole-list threshold
+            # for each query), then its other probes with that threshold
+            _lib.call("ancka_ivf_split_probes", probes.data_ptr(), index.labels.data_ptr(), q0, m,
+                      nprobe, own.data_ptr(), rest.data_ptr(), st)
+            for keys in (own, rest):
+                pair_ptr, tile_ptr, pair_ent = _bucket(keys, m * nprobe, nlist, tile=64)
+                _lib.call("ancka_ivf_search_tc", h.data_ptr(), dh, lres.data_ptr(),
+                          lmax.data_ptr(), index.perm.data_ptr(), index.list_ptr.data_ptr(),
+                          pair_ptr.data_ptr(), pair_ent.data_ptr(), tile_ptr.data_ptr(),
+                          counter.data_ptr(), nlist, nprobe, q0, K2, err, part_s.data_ptr(),
+                          part_i.data_ptr(), qthr.data_ptr(), st)
         else:
+            pair_ptr, tile_ptr, pair_ent = _bucket(probes, m * nprobe, nlist, tile=64)
             _lib.call("ancka_ivf_search", xn.data_ptr(), dp, index.perm.data_ptr(),
                       index.list_ptr.data_ptr(), pair_ptr.data_ptr(), pair_ent.data_ptr(),
                       tile_ptr.data_ptr(), counter.data_ptr(), nlist, nprobe, q0, K2, err,

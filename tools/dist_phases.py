@@ -28,7 +28,7 @@ params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.
 D.DIST_TIMING = True
 D.DISC_MODE = os.environ.get("DISC_MODE", "auto")
 B = D.CudaBackend()
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "2"))):
     res = D.run_ancka_dist(net, params, B)
     print(json.dumps({"rep": rep, "iterations": res.iterations, "stop": res.stop_reason,
                       "timings_ms": res.timings_ms, "total_ms": round(sum(res.timings_ms.values()), 1)}))
