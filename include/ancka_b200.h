@@ -433,12 +433,6 @@ int ancka_ivf_half_prep(const float* xn, int64_t n, int64_t dp, void* h, int64_t
  * negative keys. */
 int ancka_ivf_split_probes(const int32_t* probes, const int32_t* labels, int64_t q0, int64_t m,
                            int32_t nprobe, int32_t* own, int32_t* rest, ancka_stream_t stream);
-/* Seed of the per-query thresholds (fp16 scan): qthr[q] >= the K2-th best
- * approximate score of query q0 + q against up to 64 keys of its own list,
- * less `margin` (the scan's summation-order difference). */
-int ancka_ivf_seed(const void* h, int64_t dh, const int32_t* labels, const int32_t* perm,
-                   const int64_t* list_ptr, int64_t q0, int64_t m, int32_t K2, float margin,
-                   uint32_t* qthr, ancka_stream_t stream);
 int ancka_ivf_search_tc(const void* h, int64_t dh, const float* lres, const uint32_t* lmax_bits,
                         const int32_t* perm, const int64_t* list_ptr, const int64_t* pair_ptr,
                         const int32_t* pair_ent, const int64_t* tile_ptr, int32_t* counter,

@@ -89,8 +89,6 @@ _SIGS = {
                                       c_void_p, c_void_p]),
     "ancka_ivf_split_probes": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int32, c_void_p,
                                          c_void_p, c_void_p]),
-    "ancka_ivf_seed": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_int64, c_int64,
-                                 c_int32, ctypes.c_float, c_void_p, c_void_p]),
     "ancka_ivf_search_tc": (c_int32, [c_void_p, c_int64, c_void_p, c_void_p, c_void_p, c_void_p,
                                       c_void_p, c_void_p, c_void_p, c_void_p, c_int32, c_int32,
                                       c_int64, c_int32, ctypes.c_float, c_void_p, c_void_p,

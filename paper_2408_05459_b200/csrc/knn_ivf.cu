@@ -1272,52 +1272,6 @@ extern "C" int ancka_ivf_half_prep(const float* xn, int64_t n, int64_t dp, void*
   return ANCKA_OK;
 }
 
-// Seed of the per-query threshold (fp16 scan): the K2-th best approximate
-// score of the query against up to 64 keys of its own list, less a margin
-// for the scan's different f32 summation order -- a lower bound on the K2-th
-// approximate score of its merged list (those keys are among its
-// candidates), so every pair filters from its first key tile on.
-__global__ void ivf_seed_kernel(const __half* __restrict__ h, int64_t dh, const int32_t* __restrict__ labels,
-                                const int32_t* __restrict__ perm, const int64_t* __restrict__ list_ptr,
-                                int64_t q0, int64_t m, int K2, float margin, uint32_t* __restrict__ qthr) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < m;
-       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int64_t gq = q0 + q;
-    const int c = labels[gq];
-    const int64_t kb = list_ptr[c], ke = lmin(list_ptr[c + 1], kb + 64);
-    float best[2] = {-FLT_MAX, -FLT_MAX};    // lane's two keys (64 keys over 32 lanes)
-    const __half* xq = h + gq * dh;
-    for (int u = 0; u < 2; ++u) {
-      const int64_t j = kb + lane + 32 * u;
-      if (j >= ke) continue;
-      const int32_t id = perm[j];
-      if (id == gq) continue;
-      const __half* xk = h + (int64_t)id * dh;
-      float a = 0.f;
-      for (int64_t cc = 0; cc < dh; ++cc) a = fmaf(__half2float(xq[cc]), __half2float(xk[cc]), a);
-      best[u] = a;
-    }
-    // K2-th largest of the (up to) 64 values: count-based selection
-    float kth = -FLT_MAX;
-    int have = 0;
-    for (int u = 0; u < 2; ++u) have += __popc(__ballot_sync(0xffffffffu, best[u] > -FLT_MAX));
-    if (have >= K2) {
-      for (int src = 0; src < 64; ++src) {
-        const float v = __shfl_sync(0xffffffffu, best[src >> 5], src & 31);
-        int above = 0;
-        for (int u = 0; u < 2; ++u) above += __popc(__ballot_sync(0xffffffffu, best[u] > v));
-        if (v > -FLT_MAX && above < K2) {
-          int ge = 0;
-          for (int u = 0; u < 2; ++u) ge += __popc(__ballot_sync(0xffffffffu, best[u] >= v));
-          if (ge >= K2 && v > kth) kth = v;
-        }
-      }
-    }
-    if (lane == 0 && kth > -FLT_MAX) atomicMax(qthr + q, ord_key(kth - margin));
-  }
-}
-
 // Probe split for the two-phase scan: own[] keeps, per query, the probe slot
 // of its own list (the list it is assigned to, always among its probes) and
 // -1 elsewhere; rest[] the other slots.  Scanning the own pairs first sets
@@ -1341,16 +1295,6 @@ extern "C" int ancka_ivf_split_probes(const int32_t* probes, const int32_t* labe
   if (m == 0) return ANCKA_OK;
   ivf_split_probes_kernel<<<grid_for(m * nprobe, kT), kT, 0, as_stream(stream)>>>(probes, labels, q0, m,
                                                                                  nprobe, own, rest);
-  ANCKA_LAUNCHED();
-  return ANCKA_OK;
-}
-
-extern "C" int ancka_ivf_seed(const void* h, int64_t dh, const int32_t* labels, const int32_t* perm,
-                              const int64_t* list_ptr, int64_t q0, int64_t m, int32_t K2,
-                              float margin, uint32_t* qthr, ancka_stream_t stream) {
-  if (m == 0) return ANCKA_OK;
-  ivf_seed_kernel<<<grid_for(m * 32, kT), kT, 0, as_stream(stream)>>>(
-      static_cast<const __half*>(h), dh, labels, perm, list_ptr, q0, m, K2, margin, qthr);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
