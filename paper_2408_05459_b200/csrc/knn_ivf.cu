@@ -634,6 +634,18 @@ __host__ __device__ inline size_t search_tc_smem(int64_t dh, int K2) {
 
 constexpr int kTcStages = 3;      // key tiles in flight
 
+// B fragments of two 8-key column tiles (keys n0..n0+15 of a row-major
+// key tile, k-step k) with one ldmatrix.x4: {b0, b1} of tile n0, then n0 + 8
+__device__ __forceinline__ void ldsm_b2(const __half* kt, int hs, int n0, int k, int lane, uint32_t (&b)[4]) {
+  const __half* ptr = kt + (size_t)(n0 + ((lane >> 4) << 3) + (lane & 7)) * hs + k + ((lane >> 3) & 1) * 8;
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3])
+               : "r"((uint32_t)__cvta_generic_to_shared(ptr)));
+}
+
+// KS > 0: dh == 16 KS at most, the warp's query fragments stay in registers
+// for all key tiles of a pair tile; KS == 0: re-read from shared per k-step
+template <int KS>
 __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   const SearchP& p = P.s;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -664,6 +676,7 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   const int64_t total = p.tile_ptr[p.nlist];
   const int nch = (int)(P.dh / 8);                          // 16-byte chunks per row
   const float lmax = __uint_as_float(*P.lmax_bits);
+  uint32_t areg[KS > 0 ? KS : 1][4];
   // stage key tile [k0, k0 + TK) of the list (ids read from perm by the
   // issuing threads; thread r < TK records id r for the filter)
   auto stage_keys = [&](int64_t k0, int64_t ke, int b) {
@@ -737,18 +750,45 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
 #pragma unroll
         for (int u = 0; u < 4; ++u) acc[nt][u] = 0.f;
       const __half* kb_ = kh[b];
-      for (int k = 0; k < (int)P.dh; k += 16) {
-        uint32_t a[4];
-        const __half* qa = qh + (size_t)(wr + g) * hs + k + 2 * t4;
-        a[0] = *reinterpret_cast<const uint32_t*>(qa);
-        a[1] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs);
-        a[2] = *reinterpret_cast<const uint32_t*>(qa + 8);
-        a[3] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs + 8);
+      if constexpr (KS > 0) {
+        if (t == 0) {                                          // qh complete (barrier above)
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) {
-          const __half* kbp = kb_ + (size_t)(wc + nt * 8 + g) * hs + k + 2 * t4;
-          mma16816(acc[nt], a, *reinterpret_cast<const uint32_t*>(kbp),
-                   *reinterpret_cast<const uint32_t*>(kbp + 8));
+          for (int s = 0; s < KS; ++s) {
+            if (16 * s >= (int)P.dh) break;
+            const __half* qa = qh + (size_t)(wr + g) * hs + 16 * s + 2 * t4;
+            areg[s][0] = *reinterpret_cast<const uint32_t*>(qa);
+            areg[s][1] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs);
+            areg[s][2] = *reinterpret_cast<const uint32_t*>(qa + 8);
+            areg[s][3] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs + 8);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < KS; ++s) {
+          if (16 * s < (int)P.dh) {
+            uint32_t bf[4];
+            ldsm_b2(kb_, hs, wc, 16 * s, lane, bf);
+            mma16816(acc[0], areg[s], bf[0], bf[1]);
+            mma16816(acc[1], areg[s], bf[2], bf[3]);
+            ldsm_b2(kb_, hs, wc + 16, 16 * s, lane, bf);
+            mma16816(acc[2], areg[s], bf[0], bf[1]);
+            mma16816(acc[3], areg[s], bf[2], bf[3]);
+          }
+        }
+      } else {
+        for (int k = 0; k < (int)P.dh; k += 16) {
+          uint32_t a[4];
+          const __half* qa = qh + (size_t)(wr + g) * hs + k + 2 * t4;
+          a[0] = *reinterpret_cast<const uint32_t*>(qa);
+          a[1] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs);
+          a[2] = *reinterpret_cast<const uint32_t*>(qa + 8);
+          a[3] = *reinterpret_cast<const uint32_t*>(qa + 8 * hs + 8);
+          uint32_t bf[4];
+          ldsm_b2(kb_, hs, wc, k, lane, bf);
+          mma16816(acc[0], a, bf[0], bf[1]);
+          mma16816(acc[1], a, bf[2], bf[3]);
+          ldsm_b2(kb_, hs, wc + 16, k, lane, bf);
+          mma16816(acc[2], a, bf[0], bf[1]);
+          mma16816(acc[3], a, bf[2], bf[3]);
         }
       }
       // filter: lane holds rows wr+g, wr+g+8 and keys wc + 8 nt + 2 t4 + {0,1}
@@ -1310,10 +1350,11 @@ extern "C" int ancka_ivf_search_tc(const void* h, int64_t dh, const float* lres,
                 "ivf_search_tc: K2=%d dh=%lld", K2, (long long)dh);
   cudaStream_t st = as_stream(stream);
   const size_t smem = search_tc_smem(dh, K2);
-  ANCKA_CUDA(cudaFuncSetAttribute(ivf_search_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  auto kern = dh <= 128 ? ivf_search_tc<8> : ivf_search_tc<0>;
+  ANCKA_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ANCKA_CUDA(cudaMemsetAsync(counter, 0, sizeof(int32_t), st));
   int per_sm = 0;
-  ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ivf_search_tc, kT, smem));
+  ANCKA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kT, smem));
   SearchTcP P{};
   P.s = SearchP{nullptr, 0, perm, list_ptr, pair_ptr, pair_ent, tile_ptr, counter, nlist, nprobe, q0, K2,
                 0.f, part_s, part_i, qthr};
@@ -1322,7 +1363,7 @@ extern "C" int ancka_ivf_search_tc(const void* h, int64_t dh, const float* lres,
   P.lres = lres;
   P.lmax_bits = reinterpret_cast<const unsigned*>(lmax_bits);
   P.acc_err = acc_err;
-  ivf_search_tc<<<kNumSMs * std::max(1, per_sm), kT, smem, st>>>(P);
+  kern<<<kNumSMs * std::max(1, per_sm), kT, smem, st>>>(P);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }
