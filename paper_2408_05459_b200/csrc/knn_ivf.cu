@@ -668,8 +668,9 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   float* thr = reinterpret_cast<float*>(ccnt + TQ);
   float* gt = thr + TQ;
   float* eq = gt + TQ;
-  __shared__ int s_work;
+  __shared__ int s_work, s_nql;
   __shared__ int32_t kids[kTcStages][TK];                 // key ids of each staged tile
+  __shared__ int32_t qlist[TQ];                           // queries with candidates in the tile
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int wr = (warp & 3) * 16, wc = (warp >> 2) * 32;   // warp tile: 16 queries x 32 keys
@@ -680,21 +681,24 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
   // stage key tile [k0, k0 + TK) of the list (ids read from perm by the
   // issuing threads; thread r < TK records id r for the filter)
   auto stage_keys = [&](int64_t k0, int64_t ke, int b) {
-    if (tid < TK) kids[b][tid] = k0 + tid < ke ? p.perm[k0 + tid] : -1;
-    for (int e = tid; e < TK * nch; e += kT) {
-      const int r = e / nch, ch = e - r * nch;
-      const int32_t id = k0 + r < ke ? p.perm[k0 + r] : -1;
-      __half* dst = kh[b] + (size_t)r * hs + ch * 8;
+    static_assert(kT == 4 * TK, "four threads per staged key row");
+    const int r = tid >> 2;
+    const int32_t id = k0 + r < ke ? p.perm[k0 + r] : -1;
+    if ((tid & 3) == 0) kids[b][r] = id;
+    __half* dst = kh[b] + (size_t)r * hs;
+    const __half* src = P.h + (int64_t)(id >= 0 ? id : 0) * P.dh;
+    for (int ch = tid & 3; ch < nch; ch += 4) {
       if (id >= 0) {
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-                     "l"(P.h + (int64_t)id * P.dh + ch * 8)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst + ch * 8)),
+                     "l"(src + ch * 8)
                      : "memory");
       } else {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(dst + ch * 8) = make_uint4(0u, 0u, 0u, 0u);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
+  if (tid == 0) s_nql = 0;
   for (;;) {
     if (tid == 0) s_work = atomicAdd(p.counter, 1);
     __syncthreads();
@@ -812,13 +816,19 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
             if (slot >= nk || id < 0 || id == me) continue;
             if (full && !before(sv, id, ts_, ti_)) continue;
             const int pos = atomicAdd(&ccnt[q], 1);
+            if (pos == 0) qlist[atomicAdd(&s_nql, 1)] = q;
             cbs[q * TK + pos] = sv;
             cbi[q * TK + pos] = (uint8_t)slot;
           }
       }
       __syncthreads();
+      // no candidates in the tile: nothing to insert, and nothing read after
+      // this barrier needs protecting before the next tile's top barrier
+      const int nql = s_nql;
+      if (nql == 0) continue;
       // warp-cooperative insertion (K2 <= 32: lane t holds entry t)
-      for (int q = warp; q < nq; q += kT / 32) {
+      for (int iq = warp; iq < nql; iq += kT / 32) {
+        const int q = qlist[iq];
         const int nb = ccnt[q];
         if (nb == 0) continue;
         int cnt = tn[q];
@@ -849,6 +859,7 @@ __global__ void __launch_bounds__(kT) ivf_search_tc(SearchTcP P) {
         }
       }
       __syncthreads();
+      if (tid == 0) s_nql = 0;
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     if (tid < nq) {
