@@ -902,60 +902,80 @@ __global__ void knn_real_merge_kernel(const int2* __restrict__ partial, int64_t 
       for (int t = lane; t < K; t += 32) { oid[t] = -1; osc[t] = 0.0; }
       continue;
     }
-    constexpr int L = SL::L, E = SL::E;
+    constexpr int L = SL::L, E = SL::E, KSLOT = L - E - 1;
+    static_assert(L <= 32, "one list entry per lane");
     const float eps = row_eps ? row_eps[i] : eps_g;
     const float band = 2.f * eps;
     const int live_n = K + E;
-    CandList<L, E> M;
-    M.clear(K, -eps);
+    // the merged list M (CandList order: a desc, j asc; L - E - K leading
+    // +inf sentinels put the K-th real entry at KSLOT) spread over the
+    // warp, lane t holding entry t: an insert is one ballot and one shift
+    const bool slot = lane < L;
+    float mf = slot && lane < L - E - K ? kInf : -kInf;
+    int32_t mj = -1;
+    const float floor_ = -eps;
+    float thr = floor_;
     float over = -kInf;                          // best candidate any list dropped
     for (int s = 0; s < lists; ++s) {
       const int2* src = partial + ((size_t)li * lists + s) * live_n;
       over = fmaxf(over, __int_as_float(src[live_n - 1].x));
-      for (int t = 0; t < live_n; ++t) {
-        const int2 e = src[t];
-        if (e.y < 0) break;
-        const float f = __int_as_float(e.x);
-        if (f >= M.thr) M.insert(f, e.y, band);
+      for (int t0 = 0; t0 < live_n; t0 += 32) {
+        const int t = t0 + lane;
+        const int2 e = t < live_n ? src[t] : make_int2(0, -1);
+        const unsigned stop = __ballot_sync(0xffffffffu, e.y < 0);   // lists end at the first j < 0
+        const int lim = stop ? __ffs(stop) - 1 : 32;
+        // the threshold only rises: entries below it now are refused later
+        unsigned m = __ballot_sync(0xffffffffu, lane < lim && __int_as_float(e.x) >= thr);
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const float ff = __int_as_float(__shfl_sync(0xffffffffu, e.x, b));
+          const int32_t jj = __shfl_sync(0xffffffffu, e.y, b);
+          if (!(ff >= thr)) continue;                                // warp-uniform
+          const int pos = __popc(__ballot_sync(0xffffffffu, slot && (mf > ff || (mf == ff && mj < jj))));
+          const float uf = __shfl_up_sync(0xffffffffu, mf, 1);
+          const int32_t uj = __shfl_up_sync(0xffffffffu, mj, 1);
+          if (slot && lane > pos) { mf = uf; mj = uj; }
+          if (slot && lane == pos) { mf = ff; mj = jj; }
+          const float last = __shfl_sync(0xffffffffu, mf, L - 1);
+          const float kth = __shfl_sync(0xffffffffu, mf, KSLOT);
+          thr = fmaxf(fmaxf(last, kth - band), floor_);
+        }
+        if (stop) break;
       }
     }
-    const float theta = fmaxf(M.kth() - band, -eps);
-    over = fmaxf(over, M.f[L - 1]);
+    const float theta = fmaxf(__shfl_sync(0xffffffffu, mf, KSLOT) - band, -eps);
+    over = fmaxf(over, __shfl_sync(0xffffffffu, mf, L - 1));
     if (!(over < theta)) {                       // not certified: exact rescan later
       if (lane == 0) flagged[atomicAdd(nflag, 1)] = (int32_t)i;
       continue;
     }
     const double* xi = xn + i * ldn;
-    double sv[L];
-#pragma unroll
-    for (int t = 0; t < L; ++t) {
-      sv[t] = -1.0;
-      if (M.j[t] >= 0 && M.f[t] >= theta) {      // warp-uniform branch
-        const double* xj = xn + (int64_t)M.j[t] * ldn;
-        double acc = 0.0;
-        for (int64_t c = lane; c < d; c += 32) acc = fma(xi[c], xj[c], acc);
-        sv[t] = warp_sum(acc);
-      }
+    double sv = -1.0;                            // lane t: f64 score of entry t
+    for (unsigned m = __ballot_sync(0xffffffffu, slot && mj >= 0 && mf >= theta); m; m &= m - 1) {
+      const int b = __ffs(m) - 1;
+      const double* xj = xn + (int64_t)__shfl_sync(0xffffffffu, mj, b) * ldn;
+      double acc = 0.0;
+      for (int64_t c = lane; c < d; c += 32) acc = fma(xi[c], xj[c], acc);
+      acc = warp_sum(acc);
+      if (lane == b) sv = acc;
     }
-    // top K of (s desc, j asc) among s > 0, by repeated selection
-    uint32_t used = 0;
-    for (int r = 0; r < K; ++r) {
-      int best = -1;
-      double bs = 0.0;
-      int32_t bj = 0;
-#pragma unroll
-      for (int t = 0; t < L; ++t) {
-        const bool ok = !((used >> t) & 1u) && sv[t] > 0.0 &&
-                        (best < 0 || sv[t] > bs || (sv[t] == bs && M.j[t] < bj));
-        best = ok ? t : best;
-        bs = ok ? sv[t] : bs;
-        bj = ok ? M.j[t] : bj;
-      }
-      if (best >= 0) used |= 1u << best;
-      if (lane == 0) {
-        oid[r] = best >= 0 ? bj : -1;
-        osc[r] = best >= 0 ? fmin(bs, 1.0) : 0.0;
-      }
+    // top K of (s desc, j asc) among s > 0: each entry's rank among them
+    const bool live = sv > 0.0;
+    int rank = 0;
+    for (int u = 0; u < L; ++u) {
+      const double su = __shfl_sync(0xffffffffu, sv, u);
+      const int32_t ju = __shfl_sync(0xffffffffu, mj, u);
+      rank += (su > 0.0 && (su > sv || (su == sv && ju < mj))) ? 1 : 0;
+    }
+    const int cnt = __popc(__ballot_sync(0xffffffffu, live));
+    if (live && rank < K) {
+      oid[rank] = mj;
+      osc[rank] = fmin(sv, 1.0);
+    }
+    for (int r = cnt + lane; r < K; r += 32) {
+      oid[r] = -1;
+      osc[r] = 0.0;
     }
   }
 }
