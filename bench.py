@@ -274,7 +274,10 @@ def _sm_clock_hz():
         import pynvml
         pynvml.nvmlInit()
         h = pynvml.nvmlDeviceGetHandleByIndex(0)
-        return 1e6 * pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+        # the maximum SM clock (the timed runs sit at it, `clocks.sm_mhz`): the
+        # current clock read after the run can be an idle step and would
+        # understate the ceiling
+        return 1e6 * pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
     except Exception:
         return 1.965e9
 
