@@ -986,6 +986,88 @@ __global__ void __launch_bounds__(32 * kMergeWarps) ivf_merge(MergeP p) {
   }
 }
 
+// ivf_merge for K2 <= 32: the kept list spread over the warp (lane t holds
+// entry t), inserts by one ballot + shift, the f64 re-rank order by ranks
+// from shuffles -- the same lists, certificate and outputs as ivf_merge
+// without its lane-0 serial inserts and sort
+__global__ void __launch_bounds__(32 * kMergeWarps) ivf_merge_warp(MergeP p) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; q < p.m;
+       q += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t nc = (int64_t)p.nprobe * p.K2;
+    const float* cs = p.part_s + q * nc;
+    const int32_t* ci = p.part_i + q * nc;
+    float ls = -FLT_MAX;         // lane t < cnt: entry t of the kept list (f32 score, id)
+    int li = -1;
+    int cnt = 0;
+    for (int64_t b = 0; b < nc; b += 32) {
+      const int64_t j = b + lane;
+      const int id = j < nc ? ci[j] : -1;
+      const float s = j < nc ? cs[j] : -FLT_MAX;
+      const bool full = cnt == p.K2;
+      const float ts_ = __shfl_sync(0xffffffffu, ls, p.K2 - 1);
+      const int ti_ = __shfl_sync(0xffffffffu, li, p.K2 - 1);
+      unsigned pass = __ballot_sync(0xffffffffu, id >= 0 && (!full || before(s, id, ts_, ti_)));
+      while (pass) {
+        const int src = __ffs(pass) - 1;
+        pass &= pass - 1;
+        const float s2 = __shfl_sync(0xffffffffu, s, src);
+        const int id2 = __shfl_sync(0xffffffffu, id, src);
+        if (cnt == p.K2) {
+          const float lsl = __shfl_sync(0xffffffffu, ls, p.K2 - 1);
+          const int lil = __shfl_sync(0xffffffffu, li, p.K2 - 1);
+          if (!before(s2, id2, lsl, lil)) continue;                 // warp-uniform
+        }
+        const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && before(ls, li, s2, id2)));
+        const float us = __shfl_up_sync(0xffffffffu, ls, 1);
+        const int ui = __shfl_up_sync(0xffffffffu, li, 1);
+        if (lane > pos && lane < p.K2) { ls = us; li = ui; }
+        if (lane == pos) { ls = s2; li = id2; }
+        cnt = min(cnt + 1, p.K2);
+      }
+    }
+    // exact re-rank: f64 sums of the (exact) f32 x f32 products
+    const int64_t gq = p.q0 + q;
+    const float* xq = p.xn + gq * p.dp;
+    double wd = 0.0;
+    for (int t = 0; t < cnt; ++t) {
+      const float* xk = p.xn + (int64_t)__shfl_sync(0xffffffffu, li, t) * p.dp;
+      double a = 0.0;
+      for (int64_t c = lane; c < p.dp; c += 32) a = fma((double)xq[c], (double)xk[c], a);
+      a = warp_sum(a);
+      if (lane == t) wd = a;
+    }
+    // certificate: everything not kept scored (f32) <= the K2-th kept
+    // f32 score, so its exact value is <= that + e
+    const float last = cnt == p.K2 ? __shfl_sync(0xffffffffu, ls, p.K2 - 1) : -FLT_MAX;
+    const double lmax = p.lres ? (double)__uint_as_float(*p.lmax_bits) : 0.0;
+    const double eq = p.lres ? (double)p.lres[gq] + lmax + (double)p.lres[gq] * lmax + p.e
+                             : (double)p.e;
+    const double bound = (double)last + eq;
+    const bool mine = lane < cnt;
+    const int npos = __popc(__ballot_sync(0xffffffffu, mine && wd > 0.0));
+    const int nabove = __popc(__ballot_sync(0xffffffffu, mine && wd > bound && wd > 0.0));
+    const bool ok = cnt < p.K2 || bound <= 0.0 || nabove >= p.K;
+    if (lane == 0 && !ok) p.flagged[atomicAdd(p.nflag, 1)] = (int32_t)gq;
+    // rank in (f64 desc, id asc) among the kept entries
+    int rank = 0;
+    for (int u = 0; u < cnt; ++u) {
+      const double du = __shfl_sync(0xffffffffu, wd, u);
+      const int iu = __shfl_sync(0xffffffffu, li, u);
+      rank += (du > wd || (du == wd && iu < li)) ? 1 : 0;
+    }
+    const int take = min(npos, p.K);
+    if (mine && rank < take) {
+      p.ids[q * p.K + rank] = li;
+      p.scores[q * p.K + rank] = (double)fminf((float)wd, 1.0f);
+    }
+    for (int t = take + lane; t < p.K; t += 32) {
+      p.ids[q * p.K + t] = -1;
+      p.scores[q * p.K + t] = 0.0;
+    }
+  }
+}
+
 // ------------------------------------------------------------ rows exact ---
 // R query rows per CTA share one candidate stream (all keys, probes ==
 // nullptr) or R = 1 with the row's own probe lists.  Every candidate scored
@@ -1386,10 +1468,16 @@ extern "C" int ancka_ivf_merge(const float* xn, int64_t dp, int64_t q0, int64_t 
                                ancka_stream_t stream) {
   ANCKA_REQUIRE(K >= 1 && K2 >= K && K2 <= 256, ANCKA_ERR_ARG, "ivf_merge: K=%d K2=%d", K, K2);
   if (m == 0) return ANCKA_OK;
-  const size_t smem = align_dev((size_t)kMergeWarps * K2 * 8) + (size_t)kMergeWarps * K2 * 8;
-  ANCKA_CUDA(cudaFuncSetAttribute(ivf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   MergeP p{xn, dp, q0, m, nprobe, K2, K, part_s, part_i, err, ids, scores, flagged, nflag, lres,
            reinterpret_cast<const unsigned*>(lmax_bits)};
+  if (K2 <= 32) {
+    ivf_merge_warp<<<grid_for(m * 32, 32 * kMergeWarps, kNumSMs * 32), 32 * kMergeWarps, 0,
+                     as_stream(stream)>>>(p);
+    ANCKA_LAUNCHED();
+    return ANCKA_OK;
+  }
+  const size_t smem = align_dev((size_t)kMergeWarps * K2 * 8) + (size_t)kMergeWarps * K2 * 8;
+  ANCKA_CUDA(cudaFuncSetAttribute(ivf_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   ivf_merge<<<grid_for(m * 32, 32 * kMergeWarps, kNumSMs * 32), 32 * kMergeWarps, smem,
               as_stream(stream)>>>(p);
   ANCKA_LAUNCHED();
