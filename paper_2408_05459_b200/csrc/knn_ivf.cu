@@ -1073,7 +1073,7 @@ __global__ void __launch_bounds__(32 * kMergeWarps) ivf_merge_warp(MergeP p) {
 // nullptr) or R = 1 with the row's own probe lists.  Every candidate scored
 // with f64 accumulation; per row a top-K list (score desc, id asc) of the
 // positive scores, self excluded.
-constexpr int kRowsR = 8;
+constexpr int kRowsR = 16;
 
 struct RowsP {
   const float* xn;
@@ -1100,9 +1100,10 @@ __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
   const int R = p.R;
   double* ls = reinterpret_cast<double*>(smem_raw);                            // R x K
   int32_t* li = reinterpret_cast<int32_t*>(ls + (size_t)R * p.K);              // R x K
-  float* xq = reinterpret_cast<float*>(smem_raw + align_dev((size_t)R * p.K * 12));  // R x dp
+  // query rows held as f64 (exact widening, done once instead of per key)
+  double* xq = reinterpret_cast<double*>(smem_raw + align_dev((size_t)R * p.K * 12));  // R x dp
   double* bs = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(xq) +
-                                         align_dev((size_t)R * p.dp * 4));     // R x kT
+                                         align_dev((size_t)R * p.dp * 8));     // R x kT
   int32_t* bi = reinterpret_cast<int32_t*>(bs + (size_t)R * kT);
   __shared__ int bcnt[kRowsR], lcnt[kRowsR], qid[kRowsR];
   const int tid = threadIdx.x;
@@ -1116,7 +1117,7 @@ __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
   __syncthreads();
   for (int64_t i = tid; i < (int64_t)R * p.dp; i += kT) {
     const int r = (int)(i / p.dp);
-    xq[i] = qid[r] >= 0 ? p.xn[(int64_t)qid[r] * p.dp + (i % p.dp)] : 0.0f;
+    xq[i] = qid[r] >= 0 ? (double)p.xn[(int64_t)qid[r] * p.dp + (i % p.dp)] : 0.0;
   }
   // candidate ranges: all keys, or the row's probe lists (through perm)
   const int nseg = p.probes ? p.nprobe : 1;
@@ -1144,14 +1145,16 @@ __global__ void __launch_bounds__(kT) ivf_rows_exact(RowsP p) {
         for (int r = 0; r < kRowsR; ++r) a[r] = 0.0;
         for (int64_t c = 0; c < p.dp; c += 4) {
           const float4 v = *reinterpret_cast<const float4*>(xk + c);
+          const double v0 = v.x, v1 = v.y, v2 = v.z, v3 = v.w;
 #pragma unroll
           for (int r = 0; r < kRowsR; ++r) {
             if (r < R) {
-              const float4 x = *reinterpret_cast<const float4*>(xq + (size_t)r * p.dp + c);
-              a[r] = fma((double)x.x, (double)v.x, a[r]);
-              a[r] = fma((double)x.y, (double)v.y, a[r]);
-              a[r] = fma((double)x.z, (double)v.z, a[r]);
-              a[r] = fma((double)x.w, (double)v.w, a[r]);
+              const double2 x01 = *reinterpret_cast<const double2*>(xq + (size_t)r * p.dp + c);
+              const double2 x23 = *reinterpret_cast<const double2*>(xq + (size_t)r * p.dp + c + 2);
+              a[r] = fma(x01.x, v0, a[r]);
+              a[r] = fma(x01.y, v1, a[r]);
+              a[r] = fma(x23.x, v2, a[r]);
+              a[r] = fma(x23.y, v3, a[r]);
             }
           }
         }
@@ -1241,7 +1244,7 @@ __global__ void ivf_rows_seg_merge(const double* __restrict__ seg_sc, const int3
 }
 
 size_t rows_smem(int R, int64_t dp, int K) {
-  return align_dev((size_t)R * K * 12) + align_dev((size_t)R * dp * 4) + (size_t)R * kT * 12;
+  return align_dev((size_t)R * K * 12) + align_dev((size_t)R * dp * 8) + (size_t)R * kT * 12;
 }
 
 // ---------------------------------------------------------------- k-means ---
