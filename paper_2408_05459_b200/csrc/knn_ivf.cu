@@ -11,7 +11,7 @@
 //
 //   ivf_normalize  xn = f32(x * (1/||x||)) with numpy's norm (knn.py:54-65;
 //                  the approximate path searches the f32 copy, knn.py:174)
-//   ivf_gemm       S = A B^T + bias (f32 SIMT tiles, 64 x 64, 4 x 4 per
+//   ivf_gemm       S = A B^T + bias (f32 SIMT tiles, 128 x 128, 8 x 8 per
 //                  thread): stored (probe scores) or reduced to a first-max
 //                  argmax per row through a packed 64-bit atomicMax
 //                  (list assignment, k-means assignment)
@@ -114,51 +114,75 @@ struct GemmP {
   unsigned long long* amax;
 };
 
+// 128 x 128 output tile per CTA, 8 x 8 per thread (rows ty + 16 i, columns
+// tx + 16 j: conflict-free broadcast reads of the k-major staged operands),
+// A and B staged 32 k at a time by float4 row reads; every output is the
+// same k-ordered fmaf chain (zero-padded past d) as a plain dot product
+constexpr int GT = 128, GLD = GT + 1;
 __global__ void __launch_bounds__(kT) ivf_gemm(GemmP p) {
-  __shared__ float as[KC][TQ + 1];
-  __shared__ float bs[KC][TK + 1];
+  __shared__ float as[KC][GLD];
+  __shared__ float bs[KC][GLD];
   const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  const int64_t r0 = (int64_t)blockIdx.x * TQ;
-  const int c0 = blockIdx.y * TK;
-  float acc[4][4];
+  const int64_t r0 = (int64_t)blockIdx.x * GT;
+  const int c0 = blockIdx.y * GT;
+  float acc[8][8];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+  const bool vec = (p.lda % 4) == 0 && (p.ldb % 4) == 0;
   for (int64_t d0 = 0; d0 < p.d; d0 += KC) {
-    for (int idx = tid; idx < TQ * KC; idx += kT) {
-      const int r = idx / KC, kk = idx % KC;
+    // thread: row r = idx / 8, k quad q = idx % 8 of this 32-k block
+    for (int idx = tid; idx < GT * (KC / 4); idx += kT) {
+      const int r = idx >> 3, q = idx & 7;
+      const int64_t k = d0 + 4 * q;
+      float4 va = make_float4(0.f, 0.f, 0.f, 0.f), vb = va;
       const int64_t gr = r0 + r;
-      float v = 0.0f;
-      if (gr < p.m && d0 + kk < p.d) {
-        const int64_t ar = p.arows ? p.arows[gr] : gr;
-        v = p.A[ar * p.lda + d0 + kk];
+      if (gr < p.m) {
+        const float* src = p.A + (p.arows ? (int64_t)p.arows[gr] : gr) * p.lda + k;
+        if (vec && k + 4 <= p.d) va = *reinterpret_cast<const float4*>(src);
+        else {
+          if (k < p.d) va.x = src[0];
+          if (k + 1 < p.d) va.y = src[1];
+          if (k + 2 < p.d) va.z = src[2];
+          if (k + 3 < p.d) va.w = src[3];
+        }
       }
-      as[kk][r] = v;
       const int gc = c0 + r;
-      bs[kk][r] = (gc < p.nb && d0 + kk < p.d) ? p.B[(int64_t)gc * p.ldb + d0 + kk] : 0.0f;
+      if (gc < p.nb) {
+        const float* src = p.B + (int64_t)gc * p.ldb + k;
+        if (vec && k + 4 <= p.d) vb = *reinterpret_cast<const float4*>(src);
+        else {
+          if (k < p.d) vb.x = src[0];
+          if (k + 1 < p.d) vb.y = src[1];
+          if (k + 2 < p.d) vb.z = src[2];
+          if (k + 3 < p.d) vb.w = src[3];
+        }
+      }
+      as[4 * q][r] = va.x; as[4 * q + 1][r] = va.y; as[4 * q + 2][r] = va.z; as[4 * q + 3][r] = va.w;
+      bs[4 * q][r] = vb.x; bs[4 * q + 1][r] = vb.y; bs[4 * q + 2][r] = vb.z; bs[4 * q + 3][r] = vb.w;
     }
     __syncthreads();
-#pragma unroll 8
+#pragma unroll 4
     for (int kk = 0; kk < KC; ++kk) {
-      float a[4], b[4];
+      float a[8], b[8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = as[kk][ty + 16 * i];
+      for (int i = 0; i < 8; ++i) a[i] = as[kk][ty + 16 * i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = bs[kk][tx + 16 * j];
+      for (int j = 0; j < 8; ++j) b[j] = bs[kk][tx + 16 * j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 8; ++i) {
     const int64_t gr = r0 + ty + 16 * i;
     unsigned long long best = 0ull;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 8; ++j) {
       const int gc = c0 + tx + 16 * j;
       if (gc >= p.nb) continue;
       const float s = p.bias ? acc[i][j] + p.bias[gc] : acc[i][j];
@@ -1322,9 +1346,9 @@ extern "C" int ancka_ivf_gemm(const float* A, int64_t lda, const int32_t* arows,
   ANCKA_REQUIRE(m >= 0 && nb > 0 && d > 0 && (C || argmax_keys), ANCKA_ERR_ARG,
                 "ivf_gemm: bad arguments");
   if (m == 0) return ANCKA_OK;
-  ANCKA_REQUIRE(ceil_div(nb, TK) < 65536, ANCKA_ERR_ARG, "ivf_gemm: nb=%d too large", nb);
+  ANCKA_REQUIRE(ceil_div(nb, GT) < 65536, ANCKA_ERR_ARG, "ivf_gemm: nb=%d too large", nb);
   GemmP p{A, lda, arows, m, B, ldb, nb, d, bias, C, ldc, argmax_keys};
-  dim3 grid((unsigned)ceil_div(m, TQ), (unsigned)ceil_div(nb, TK));
+  dim3 grid((unsigned)ceil_div(m, GT), (unsigned)ceil_div(nb, GT));
   ivf_gemm<<<grid, kT, 0, as_stream(stream)>>>(p);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
