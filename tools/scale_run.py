@@ -1,4 +1,8 @@
-"""One clustering of a full-size shape on 1 GPU with a phase breakdown."""
+"""One clustering of a full-size shape on 1 GPU with a phase breakdown.
+
+    python tools/scale_run.py SHAPE [scale] [reps]   (KNN_MODE=exact|auto|approx, default exact)
+"""
+import os
 import sys
 import time
 import warnings
@@ -20,7 +24,9 @@ print(f"generated {shape} n={inst.structure.shape[1]} nnz={inst.structure.nnz} "
       f"X nnz={getattr(inst.X, 'nnz', inst.X.size)} in {time.perf_counter() - t0:.1f}s", flush=True)
 net = (ancka.AttributedNetwork.hypergraph(inst.structure, inst.X) if inst.kind == "hypergraph"
        else ancka.AttributedNetwork.graph(inst.structure, inst.X))
-params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=ancka.KnnMode.EXACT)
+mode = {"exact": ancka.KnnMode.EXACT, "auto": ancka.KnnMode.AUTO,
+        "approx": ancka.KnnMode.APPROX}[os.environ.get("KNN_MODE", "exact")]
+params = ancka.ClusterParams(k=inst.k, knn_k=10, seed=0, knn_mode=mode)
 t0 = time.perf_counter()
 prep = ancka.prepare_network(net, params)
 torch.cuda.synchronize()
