@@ -8,6 +8,11 @@ import time
 import warnings
 from pathlib import Path
 
+# large shapes (Papers100M/8 peaks at ~182 GB) need the allocator to grow
+# segments instead of carving fixed ones: fragmentation otherwise fails an
+# 18 GB block with 21 GB reserved but unallocated
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 warnings.simplefilter("ignore")
 import torch  # noqa: E402
