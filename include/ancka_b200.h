@@ -332,6 +332,12 @@ size_t ancka_mhc_workspace_size(const ancka_operator* op, int32_t k);
 int ancka_mhc(const ancka_operator* op, const int32_t* labels, int32_t k, double alpha,
               int32_t gamma, double* phi_out, int64_t* sizes_out,
               void* workspace, size_t workspace_bytes, ancka_stream_t stream);
+/* same_out (device int32) = 1 iff labels a and b (int32[n] in [0, k), every
+ * cluster nonempty) are the same partition up to relabelling -- the MHC of
+ * b then repeats the MHC of a exactly (calc_mhc depends on the partition
+ * only).  minmax_ws: device int32[2k] scratch. */
+int ancka_same_partition(const int32_t* a, const int32_t* b, int64_t n, int32_t k,
+                         int32_t* minmax_ws, int32_t* same_out, ancka_stream_t stream);
 
 /* Diagnostics of the fused MHC kernel (k <= 8, set ANCKA_MHC_TIMING=1 before
  * the first call): copies the phase timers (host u64[64 + 9 * 1024]: per

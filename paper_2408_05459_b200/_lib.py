@@ -159,6 +159,8 @@ _SIGS = {
     "ancka_mhc": (c_int32, [_OP, c_void_p, c_int32, c_double, c_int32, c_void_p, c_void_p,
                             c_void_p, c_size_t, c_void_p]),
     "ancka_mhc_timing": (None, [c_void_p, c_int32]),
+    "ancka_same_partition": (c_int32, [c_void_p, c_void_p, c_int64, c_int32, c_void_p, c_void_p,
+                                       c_void_p]),
     "ancka_cluster_sizes": (c_int32, [c_void_p, c_int64, c_int32, c_void_p, c_void_p]),
     "ancka_row_split_workspace_size": (c_size_t, [c_int64]),
     "ancka_beta_vector": (c_int32, [c_void_p, c_void_p, c_int64, c_double, c_void_p, c_void_p,

@@ -1,5 +1,7 @@
 // Multi-hop conductance (engine.py:291-299) and greedy BCM initialisation
 // (engine.py:87-127) on top of the fused SpMM epilogues.
+#include <climits>
+
 #include "common.cuh"
 #include "spmm.cuh"
 
@@ -298,6 +300,80 @@ extern "C" int ancka_init_bcm(const ancka_operator* op64, const int64_t* centers
     std::swap(cur, nxt);
   }
   argmax_rows_kernel<<<std::max(g, 1), 256, 0, st>>>(cur, n, ld, k, labels_out);
+  ANCKA_LAUNCHED();
+  return ANCKA_OK;
+}
+
+// ------------------------------------------------------- same partition ---
+// a and b (labels in [0, k)) describe the same partition up to relabelling
+// iff every cluster of a maps to one cluster of b (min == max of b over its
+// rows) and the map is injective; phi is a function of the partition (the
+// walk's columns and the trace's per-row terms do not depend on the ids), so
+// the MHC of a relabelled partition repeats the previous value bit for bit.
+namespace {
+constexpr int kSameSmemK = 4096;
+
+__global__ void same_init_kernel(int32_t* __restrict__ mn, int32_t* __restrict__ mx, int k) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < k; c += gridDim.x * blockDim.x) {
+    mn[c] = INT_MAX;
+    mx[c] = INT_MIN;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+same_minmax_kernel(const int32_t* __restrict__ a, const int32_t* __restrict__ b, int64_t n, int k,
+                   int32_t* __restrict__ mn, int32_t* __restrict__ mx) {
+  __shared__ int32_t smn[kSameSmemK], smx[kSameSmemK];
+  const bool loc = k <= kSameSmemK;
+  if (loc)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) { smn[c] = INT_MAX; smx[c] = INT_MIN; }
+  __syncthreads();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t x = a[i], y = b[i];
+    if (x < 0 || x >= k) { atomicMin(mn, INT_MIN); continue; }   // out of range: never "same"
+    if (loc) { atomicMin(&smn[x], y); atomicMax(&smx[x], y); }
+    else { atomicMin(&mn[x], y); atomicMax(&mx[x], y); }
+  }
+  __syncthreads();
+  if (loc)
+    for (int c = threadIdx.x; c < k; c += blockDim.x)
+      if (smx[c] != INT_MIN) { atomicMin(&mn[c], smn[c]); atomicMax(&mx[c], smx[c]); }
+}
+
+__global__ void __launch_bounds__(256)
+same_finish_kernel(const int32_t* __restrict__ mn, const int32_t* __restrict__ mx, int k,
+                   int32_t* __restrict__ same) {
+  __shared__ unsigned bits[kSameSmemK / 32];
+  __shared__ int ok;
+  if (threadIdx.x == 0) ok = k <= kSameSmemK;
+  for (int w = threadIdx.x; w < kSameSmemK / 32; w += blockDim.x) bits[w] = 0u;
+  __syncthreads();
+  if (ok)
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+      const int32_t lo = mn[c], hi = mx[c];
+      if (lo != hi || lo < 0 || lo >= k) { ok = 0; continue; }   // split, empty or out of range
+      if (atomicOr(&bits[lo >> 5], 1u << (lo & 31)) & (1u << (lo & 31))) ok = 0;   // not injective
+    }
+  __syncthreads();
+  if (threadIdx.x == 0) *same = ok;
+}
+}  // namespace
+
+extern "C" int ancka_same_partition(const int32_t* a, const int32_t* b, int64_t n, int32_t k,
+                                    int32_t* minmax_ws, int32_t* same_out, ancka_stream_t stream) {
+  ANCKA_REQUIRE(k >= 1 && n >= 0, ANCKA_ERR_ARG, "same_partition: n=%lld k=%d", (long long)n, k);
+  auto st = as_stream(stream);
+  int32_t* mn = minmax_ws;
+  int32_t* mx = minmax_ws + k;
+  same_init_kernel<<<(int)std::min<int64_t>(ceil_div(k, 256), 64), 256, 0, st>>>(mn, mx, k);
+  ANCKA_LAUNCHED();
+  if (n > 0) {
+    same_minmax_kernel<<<(int)std::min<int64_t>(ceil_div(n, 256), 2 * kNumSMs), 256, 0, st>>>(
+        a, b, n, k, mn, mx);
+    ANCKA_LAUNCHED();
+  }
+  same_finish_kernel<<<1, 256, 0, st>>>(mn, mx, k, same_out);
   ANCKA_LAUNCHED();
   return ANCKA_OK;
 }

@@ -39,6 +39,9 @@ from .walk import StructureFactors, WalkOperator, build_walk_operator
 
 DISCRETIZE_MAX_ITER = 100
 DISCRETIZE_TOL = 1e-10
+#: reuse the previous tau sample's MHC when the new labels are the same
+#: partition relabelled (ancka_same_partition); ANCKA_MHC_REUSE=0 disables
+MHC_REUSE = os.environ.get("ANCKA_MHC_REUSE", "1") != "0"
 _TIMING_KEYS = ("knn_ms", "init_ms", "ortho_ms", "discretize_ms", "mhc_ms")
 
 
@@ -849,6 +852,18 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
         host_rb = torch.empty(4, dtype=torch.float64, pin_memory=True)
         host_rb0 = torch.empty(1, dtype=torch.float64, pin_memory=True)
         rb_ready = torch.cuda.Event()
+        # MHC reuse: a sample whose labels are the previous evaluated sample's
+        # partition relabelled repeats its phi exactly (calc_mhc depends on
+        # the partition only) -- the check is one small kernel and a flag read
+        mhc_reuse = MHC_REUSE
+        lab_mhc = torch.empty(n, dtype=torch.int32, device=dev()) if mhc_reuse else None
+        same_ws = torch.empty(2 * k, dtype=torch.int32, device=dev()) if mhc_reuse else None
+        same_dev = torch.zeros(1, dtype=torch.int32, device=dev())
+        host_same = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        same_ready = torch.cuda.Event()
+        phi_last = torch.zeros(1, dtype=torch.float64, device=dev())
+        have_mhc = False
+        mhc_reused = 0
 
         # discretize(state.q[:, 1:]) sees c - 1 columns: fewer than k only in
         # the degenerate k == n case (engine.py:370-371, 392-394)
@@ -866,8 +881,25 @@ def run_prepared(prep: PreparedNetwork, params: ClusterParams, early_stop: bool 
                     _disc_profile_add(info, kd)
                 if kd < k:
                     _repair_missing_columns(qt, kd, k, lab_t, info)
+            nonlocal have_mhc, mhc_reused
             with timer.span("mhc_ms"):
-                mhc(lab_t, loop.stats[3:4])
+                same = False
+                if mhc_reuse and have_mhc:
+                    _lib.call("ancka_same_partition", lab_mhc.data_ptr(), lab_t.data_ptr(), n, k,
+                              same_ws.data_ptr(), same_dev.data_ptr(), _lib.stream())
+                    host_same.copy_(same_dev, non_blocking=True)
+                    same_ready.record()
+                    same_ready.synchronize()
+                    same = bool(host_same[0])
+                if same:
+                    loop.stats[3:4].copy_(phi_last)
+                    mhc_reused += 1
+                else:
+                    mhc(lab_t, loop.stats[3:4])
+                    if mhc_reuse:
+                        phi_last.copy_(loop.stats[3:4])
+                        lab_mhc.copy_(lab_t)
+                        have_mhc = True
             op.set_locality(lab_t, k)     # regroup the apply's rows by the current clusters
             if dq_first is not None:
                 loop.stats[0] = dq_first * dq_first
