@@ -656,10 +656,6 @@ def build_pipeline_device(prep: PreparedNetwork, params: ClusterParams):
         if resolve_knn_mode(params.knn_mode, n) is KnnMode.APPROX:      # knn.py:286-291
             neighbors = knn_search_approx(prep.x_dev, K, seed=params.seed)
             mode_used = KnnMode.APPROX
-            # the search's chunk buffers (up to 32 GB) are free now: hand
-            # their segments back before the graph and loop blocks are carved
-            # out of them (Papers100M/8 otherwise fragments past 180 GB)
-            torch.cuda.empty_cache()
         else:
             ids, scores = knn_search_exact_device(prep.x_dev, K, integer=prep.x_level)
             neighbors, mode_used = NeighborLists(ids_dev=ids, scores_dev=scores, K=K), KnnMode.EXACT

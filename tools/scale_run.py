@@ -11,7 +11,8 @@ from pathlib import Path
 # large shapes (Papers100M/8 peaks at ~182 GB) need the allocator to grow
 # segments instead of carving fixed ones: fragmentation otherwise fails an
 # 18 GB block with 21 GB reserved but unallocated
-os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
+if len(sys.argv) > 1 and sys.argv[1] == "papers100m":
+    os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 warnings.simplefilter("ignore")
