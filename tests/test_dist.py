@@ -586,3 +586,21 @@ def test_device_partitioned_discretize_world2(k, starved):
     lab1, _ = _disc_partitioned(q, 1, 0)
     assert out[0][1] == 0 and out[1][1] == 0
     assert np.array_equal(lab2, lab1)
+
+
+def test_same_partition_host():
+    """The replicated-label check behind the row-partitioned path's MHC
+    reuse: relabelled -> same; one moved row or two merged clusters -> not."""
+    from paper_2408_05459_b200.dist import same_partition
+    rng = np.random.default_rng(0)
+    k, n = 23, 5000
+    a = rng.permutation(np.arange(n) % k)
+    perm = rng.permutation(k)
+    b = perm[a]
+    assert same_partition(a, b, k)
+    c = b.copy()
+    c[0] = (c[0] + 1) % k
+    assert not same_partition(a, c, k)
+    d = b.copy()
+    d[d == perm[1]] = perm[0]
+    assert not same_partition(a, d, k)
